@@ -1,0 +1,127 @@
+/*
+ * qcur_b200 — C ABI of the B200-native QMCUR hot path.
+ *
+ * The reference (arxiv 2402.19147, package `qcur`, pure Python) has no FFI
+ * layer: its boundary is the Python functions of pkg/src/qcur/cur.py and
+ * linalg.py.  Each entry point below replaces one of them; the Python mirror
+ * (paper_2402_19147_b200/) binds these with ctypes and keeps the reference's
+ * names, argument meaning and exceptions.  Plain pointers and sizes only.
+ *
+ * Conventions
+ *  - Quaternion matrices on the device are INTERLEAVED, row-major: element
+ *    (i, j) of an m x n matrix with leading dimension ld (in quaternions) is the
+ *    four doubles at x[(i*ld + j)*4 + 0..3] = (a0, a1, a2, a3).  Host buffers
+ *    use the reference's PLANAR layout (four m x n float64 planes,
+ *    pkg/src/qcur/quat.py:110-143).
+ *  - All calls are asynchronous on the context's stream unless they return a
+ *    value that needs the device (then they synchronise that stream).
+ *  - Status codes map 1:1 onto the reference exceptions (errors.py:4-29).
+ *  - One context per host thread / stream; the caller owns every buffer
+ *    passed in; the library owns only its workspace.
+ */
+#ifndef QCUR_B200_H
+#define QCUR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct qcur_ctx qcur_ctx;
+
+enum qcur_status {
+  QCUR_OK = 0,
+  QCUR_E_SHAPE = 1,                  /* ShapeError                  errors.py:8  */
+  QCUR_E_PARAMETER = 2,              /* ParameterError              errors.py:12 */
+  QCUR_E_DEGENERATE_DISTRIBUTION = 3,/* DegenerateDistributionError errors.py:20 */
+  QCUR_E_SAMPLING = 4,               /* SamplingError               errors.py:24 */
+  QCUR_E_CUDA = 5                    /* CUDA runtime failure / no device          */
+};
+
+enum qcur_strategy { QCUR_STRATEGY_LENGTH = 0, QCUR_STRATEGY_UNIFORM = 1 }; /* cur.py:56 STRATEGIES */
+enum qcur_op { QCUR_OP_N = 0, QCUR_OP_H = 1 };                             /* op(A) = A or A^H      */
+
+/* informational bits returned by qcur_last_info() */
+enum qcur_info {
+  QCUR_INFO_ROBUST_C = 4,     /* pinv(C) took the Householder + Jacobi path */
+  QCUR_INFO_ROBUST_R = 8,     /* pinv(R) took the Householder + Jacobi path */
+  QCUR_INFO_DRAW_EXACT = 16   /* a draw needed the exact sequential cumsum  */
+};
+
+/* ---- context ------------------------------------------------------------ */
+int qcur_abi_version(void);
+int qcur_create(int device, qcur_ctx** out);
+void qcur_destroy(qcur_ctx* ctx);
+const char* qcur_last_error(const qcur_ctx* ctx);
+unsigned qcur_last_info(const qcur_ctx* ctx);
+int qcur_set_stream(qcur_ctx* ctx, void* cuda_stream); /* cudaStream_t; NULL = legacy default */
+int qcur_synchronize(qcur_ctx* ctx);
+/* kappa_F limit for the CholeskyQR2 fast path of pinv (default 1e7) */
+int qcur_set_kappa_limit(qcur_ctx* ctx, double limit);
+int qcur_force_robust(qcur_ctx* ctx, int on); /* testing: always use Householder + Jacobi */
+
+/* ---- numpy-compatible random stream --------------------------------------
+ * np.random.default_rng(seed) (cur.py:228, 251): PCG64 seeded by SeedSequence.
+ * seed is given as little-endian 32-bit words (seed 0 -> {0}).  state[4] =
+ * {state_hi, state_lo, inc_hi, inc_lo}.  Host-only, no device needed. */
+int qcur_rng_seed(const uint32_t* words, int nwords, uint64_t state[4]);
+int qcur_rng_advance(uint64_t state[4], uint64_t delta);
+int qcur_rng_random(uint64_t state[4], int64_t count, double* out);
+
+/* ---- host <-> device (the e2e boundary: reference planar host buffers) --- */
+int qcur_upload_planar(qcur_ctx* ctx, const double* a0, const double* a1, const double* a2, const double* a3,
+                       int64_t m, int64_t n, double* x_dev);
+int qcur_download_planar(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int64_t ld, double* a0,
+                         double* a1, double* a2, double* a3);
+int qcur_memcpy(qcur_ctx* ctx, void* dst, const void* src, size_t bytes, int kind /* cudaMemcpyKind */);
+
+/* ---- the QMCUR path ---------------------------------------------------- */
+/* length_distributions (cur.py:132-150): bit-identical to numpy. */
+int qcur_length_distributions(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, double* col_probs_dev,
+                              double* row_probs_dev);
+/* uniform_distributions (cur.py:153-157) */
+int qcur_uniform_distributions(qcur_ctx* ctx, int64_t m, int64_t n, double* col_probs_dev, double* row_probs_dev);
+/* draw_indices (cur.py:202-242): `count` distinct indices, index-exact vs numpy,
+ * consuming `count` doubles of the stream `state` (advanced on return). */
+int qcur_draw_indices(qcur_ctx* ctx, const double* probs_dev, int64_t size, int64_t count, uint64_t state[4],
+                      int64_t* out_dev);
+/* qmcur (cur.py:257-269) + plan_indices (cur.py:245-254):
+ * J (num_cols) then I (num_rows) from one stream; C = X[:,J] (m x c),
+ * R = X[I,:] (r x n), U = pinv(C) X pinv(R) (c x r). */
+int qcur_qmcur(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, const double* col_probs_dev,
+               const double* row_probs_dev, int64_t num_cols, int64_t num_rows, const uint64_t state[4],
+               int64_t* col_idx_dev, int64_t* row_idx_dev, double* c_dev, double* u_dev, double* r_dev);
+/* ||X - C U R||_F^2 and ||X||_F^2 without forming CUR (callers: cli.py:173-175,
+ * bench.py:257-258, imaging.py:170-177).  out2_dev: 2 doubles on the device. */
+int qcur_cur_error(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, const double* c_dev, int64_t c,
+                   const double* u_dev, const double* r_dev, int64_t r, double* out2_dev);
+/* One whole approximation, device resident, no host synchronisation:
+ * distributions (strategy) + draw + gather + pinv + U + fused error. */
+int qcur_approx(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int strategy, const uint64_t state[4],
+                int64_t num_cols, int64_t num_rows, int64_t* col_idx_dev, int64_t* row_idx_dev, double* c_dev,
+                double* u_dev, double* r_dev, double* err2_dev);
+/* read back and clear the device status word; returns the mapped status code */
+int qcur_check(qcur_ctx* ctx);
+
+/* ---- linear algebra used by the path -------------------------------------- */
+/* qmat_matmul (quat.py:274-296): C = alpha op(A) op(B) + beta C, sizes in quaternions */
+int qcur_qgemm(qcur_ctx* ctx, int opA, int opB, int64_t M, int64_t N, int64_t K, double alpha, const double* a_dev,
+               int64_t lda, const double* b_dev, int64_t ldb, double beta, double* c_dev, int64_t ldc);
+/* pseudoinverse (linalg.py:346-362); tol < 0 -> default eps*max(m,n)*sigma_max */
+int qcur_pseudoinverse(qcur_ctx* ctx, const double* a_dev, int64_t m, int64_t n, double tol, double* out_dev);
+/* qmat_frobenius_norm^2 (quat.py:305-307) */
+int qcur_frobenius_sq(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, double* out_host);
+
+/* ---- synthetic BASELINE workloads and the FP64 roofline probe ------------ */
+/* X = P Q^H + N, P (m x k), Q (n x k), components i.i.d. N(0,1) (Philox).
+ * noise_relative != 0: noise std = noise * ||S||_F / sqrt(4mn); else std = noise. */
+int qcur_synth_lowrank(qcur_ctx* ctx, int64_t m, int64_t n, int64_t k, uint64_t seed, double noise,
+                       int noise_relative, double* x_dev);
+double qcur_fp64_peak_tflops(qcur_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QCUR_B200_H */

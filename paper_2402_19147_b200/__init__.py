@@ -1,0 +1,44 @@
+"""paper_2402_19147_b200 — B200-native QMCUR (quaternion matrix CUR, arXiv 2402.19147).
+
+Drop-in for the reference package's QMCUR path (``qcur``: make_plan, qmcur,
+cur_reconstruct, draw_indices, plan_indices, length/uniform distributions,
+pseudoinverse, qmat_matmul, the error classes and the QMatrix/Quaternion
+types).  All numerics run in hand-written sm_100a CUDA behind the C ABI in
+include/qcur_b200.h; there is no CPU fallback.
+"""
+from .errors import (
+    DegenerateDistributionError,
+    DegenerateSamplingError,
+    FileFormatError,
+    ParameterError,
+    QcurError,
+    SamplingError,
+    ShapeError,
+)
+from .quat import QMatrix, Quaternion, qmat_conj_transpose, qmat_frobenius_norm, qmat_matmul
+from .cur import (
+    STRATEGIES,
+    CURFactors,
+    SamplingPlan,
+    cur_reconstruct,
+    cur_relative_error,
+    default_sample_counts,
+    draw_indices,
+    length_distributions,
+    make_plan,
+    plan_indices,
+    qmcur,
+    qmcur_device,
+    uniform_distributions,
+)
+from .linalg import pseudoinverse
+
+__all__ = [
+    "QcurError", "ShapeError", "ParameterError", "FileFormatError", "DegenerateDistributionError",
+    "SamplingError", "DegenerateSamplingError",
+    "QMatrix", "Quaternion", "qmat_matmul", "qmat_conj_transpose", "qmat_frobenius_norm",
+    "STRATEGIES", "SamplingPlan", "CURFactors", "length_distributions", "uniform_distributions",
+    "default_sample_counts", "make_plan", "draw_indices", "plan_indices", "qmcur", "cur_reconstruct",
+    "cur_relative_error", "qmcur_device", "pseudoinverse",
+]
+__version__ = "0.1.0"

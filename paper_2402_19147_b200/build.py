@@ -1,0 +1,62 @@
+"""Build the in-tree sm_100a shared library ``csrc/libqcur_b200.so``.
+
+Plain nvcc (no JIT cache): the built .so lives next to the sources so it
+travels with the repo snapshot to the GPU box.  Invoked by
+``__graft_entry__.build()`` and ``python -m paper_2402_19147_b200.build``.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+HERE = Path(__file__).resolve().parent
+CSRC = HERE / "csrc"
+LIB = CSRC / "libqcur_b200.so"
+SOURCES = ["qcur_abi.cu", "k_norms.cu", "k_draw.cu", "k_layout.cu", "k_qgemm.cu", "k_dense.cu", "k_synth.cu"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-cudart", "static"]
+
+
+def nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
+        if cand and (os.path.sep not in cand or Path(cand).exists()):
+            return cand
+    return "nvcc"
+
+
+def build(verbose: bool = False, jobs: int | None = None) -> Path:
+    objdir = CSRC / "build"
+    objdir.mkdir(exist_ok=True)
+    deps = sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h"))
+    deps.append(HERE.parent / "include" / "qcur_b200.h")
+    newest = max(p.stat().st_mtime for p in deps)
+    if LIB.exists() and LIB.stat().st_mtime >= newest:
+        return LIB
+    procs = []
+    objs = []
+    for src in SOURCES:
+        obj = objdir / (Path(src).stem + ".o")
+        objs.append(obj)
+        cmd = [nvcc(), *ARCH, *FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
+    failed = []
+    for src, p in procs:
+        out, _ = p.communicate()
+        if p.returncode != 0:
+            failed.append((src, out.decode(errors="replace")))
+        elif verbose and out:
+            print(out.decode(errors="replace"))
+    if failed:
+        msg = "\n".join(f"--- {s} ---\n{o}" for s, o in failed)
+        raise RuntimeError(f"nvcc failed:\n{msg}")
+    cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *map(str, objs)]
+    subprocess.run(cmd, check=True)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(verbose="-v" in sys.argv))

@@ -1,0 +1,382 @@
+// Small dense quaternion factorizations behind pseudoinverse
+// (pkg/src/qcur/linalg.py:346-362).
+//
+// The reference forms pinv(A) = V diag(1/sigma_i for sigma_i > eps*max(m,n)*sigma_max) W^H
+// from a full QSVD (LAPACK zgesdd on the complex adjoint + Gram-Schmidt).
+// For the tall sampled blocks (C = m x c, R^H = n x r) the device computes
+//   fast path : CholeskyQR2  Z = Q T  (two Gram + Cholesky + triangular solves,
+//               all GEMM-shaped on DMMA), then T^{-1}.  Valid (and identical to
+//               the cutoff pinv) when kappa_F(T) = ||T||_F ||T^{-1}||_F is small:
+//               then no sigma can reach the cutoff.
+//   robust    : Householder QR + one-sided Jacobi SVD of T with the reference's
+//               cutoff; used when Cholesky breaks down or kappa is too large
+//               (rank-deficient blocks, e.g. test_cur.py:208-219).
+// Both produce (Q, F) with pinv(Z) = F Q^H.  The robust kernels are launched
+// unconditionally and exit at once unless their status bit is set, so the
+// whole pipeline stays free of host synchronisation (and graph-capturable).
+#include <cfloat>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace qcur {
+
+namespace {
+
+__device__ __forceinline__ Quat ldQ(const double* p) { return *reinterpret_cast<const Quat*>(p); }
+__device__ __forceinline__ void stQ(double* p, const Quat& q) { *reinterpret_cast<Quat*>(p) = q; }
+
+template <int NT>
+__device__ double block_sum(double v, double* sh) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  for (int k = 0; k < NT / 32; ++k) r += sh[k];
+  return r;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Cholesky G = L L^H (quaternion Hermitian), in place, lower; upper zeroed.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_cholesky(double* G, int64_t q, int64_t ld, unsigned* status,
+                                                   unsigned fail_bit) {
+  __shared__ double sh[32];
+  __shared__ int s_fail;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_fail = 0;
+  __syncthreads();
+  for (int64_t j = 0; j < q; ++j) {
+    double part = 0.0;
+    for (int64_t k = tid; k < j; k += 1024) part += qnorm2(ldQ(G + (j * ld + k) * 4));
+    const double ssum = block_sum<1024>(part, sh);
+    const double d = G[(j * ld + j) * 4] - ssum;
+    if (!(d > 0.0) || !isfinite(d)) {
+      if (tid == 0) atomicOr(status, fail_bit);
+      return;
+    }
+    const double ljj = sqrt(d);
+    const double inv = 1.0 / ljj;
+    if (tid == 0) stQ(G + (j * ld + j) * 4, Quat{ljj, 0.0, 0.0, 0.0});
+    for (int64_t i = j + 1 + warp; i < q; i += 32) {
+      Quat acc = qzero();
+      for (int64_t k = lane; k < j; k += 32) {
+        const Quat lik = ldQ(G + (i * ld + k) * 4), ljk = ldQ(G + (j * ld + k) * 4);
+        qfma(acc, lik, qconj(ljk));
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) {
+        const Quat gij = ldQ(G + (i * ld + j) * 4);
+        stQ(G + (i * ld + j) * 4, qscale(qsub(gij, acc), inv));
+      }
+    }
+    __syncthreads();
+  }
+  for (int64_t t = tid; t < q * q; t += 1024) {
+    const int64_t i = t / q, k = t - i * q;
+    if (k > i) stQ(G + (i * ld + k) * 4, qzero());
+  }
+}
+
+// X = L^{-1} (lower triangular, real diagonal); one warp per column.
+__global__ void k_tri_inverse_lower(const double* __restrict__ L, int64_t q, int64_t ldl, double* __restrict__ X,
+                                    int64_t ldx) {
+  const int lane = threadIdx.x & 31;
+  const int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (j >= q) return;
+  for (int64_t i = lane; i < j; i += 32) stQ(X + (i * ldx + j) * 4, qzero());
+  if (lane == 0) stQ(X + (j * ldx + j) * 4, Quat{1.0 / L[(j * ldl + j) * 4], 0.0, 0.0, 0.0});
+  __syncwarp();
+  for (int64_t i = j + 1; i < q; ++i) {
+    Quat acc = qzero();
+    for (int64_t k = j + lane; k < i; k += 32) qfma(acc, ldQ(L + (i * ldl + k) * 4), ldQ(X + (k * ldx + j) * 4));
+    acc = warp_sum(acc);
+    if (lane == 0) stQ(X + (i * ldx + j) * 4, qscale(acc, -1.0 / L[(i * ldl + i) * 4]));
+    __syncwarp();
+  }
+}
+
+__global__ void k_set_identity(double* A, int64_t q, int64_t lda) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < q * q; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / q, k = t - i * q;
+    stQ(A + (i * lda + k) * 4, Quat{i == k ? 1.0 : 0.0, 0.0, 0.0, 0.0});
+  }
+}
+
+// kappa_F(T) = ||T||_F ||Tinv||_F; raise fail_bit when it exceeds `limit`.
+__global__ void __launch_bounds__(1024) k_kappa_check(const double* T, const double* Tinv, int64_t q, double limit,
+                                                      unsigned* status, unsigned fail_bit) {
+  __shared__ double sh[32];
+  if (*status & fail_bit) return;
+  double a = 0.0, b = 0.0;
+  for (int64_t t = threadIdx.x; t < q * q; t += 1024) {
+    a += qnorm2(ldQ(T + t * 4));
+    b += qnorm2(ldQ(Tinv + t * 4));
+  }
+  const double sa = block_sum<1024>(a, sh);
+  const double sb = block_sum<1024>(b, sh);
+  if (threadIdx.x == 0) {
+    const double kf = sqrt(sa) * sqrt(sb);
+    if (!(kf <= limit)) atomicOr(status, fail_bit);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Robust path
+// ---------------------------------------------------------------------------
+// row-major (p x q, ld) -> column-major work buffer (column j contiguous)
+__global__ void k_row_to_col(const double* __restrict__ Z, int64_t p, int64_t q, int64_t ldz, double* __restrict__ Zcm,
+                             const unsigned* status, unsigned gate_bit) {
+  if (!(*status & gate_bit)) return;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < p * q; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = t / p, i = t - j * p;
+    stQ(Zcm + t * 4, ldQ(Z + (i * ldz + j) * 4));
+  }
+}
+
+// column-major -> row-major.  gate_invert=0: run when the bit is set.
+__global__ void k_col_to_row(const double* __restrict__ Zcm, int64_t p, int64_t q, double* __restrict__ Z, int64_t ldz,
+                             const unsigned* status, unsigned gate_bit, int gate_invert) {
+  const bool set = (*status & gate_bit) != 0;
+  if (set == (gate_invert != 0)) return;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < p * q; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / q, j = t - i * q;
+    stQ(Z + (i * ldz + j) * 4, ldQ(Zcm + (j * p + i) * 4));
+  }
+}
+
+// Householder QR of the column-major p x q block (p >= q), single CTA.
+// Produces Qcm (p x q, column-major, orthonormal columns) and T (q x q,
+// row-major, upper triangular).  H = I - beta v v^H, alpha = -(x1/|x1|)||x||.
+__global__ void __launch_bounds__(1024) k_householder_qr(double* Zcm, int64_t p, int64_t q, double* betas,
+                                                         double* Qcm, double* T, int64_t ldt, const unsigned* status,
+                                                         unsigned gate_bit) {
+  if (!(*status & gate_bit)) return;
+  __shared__ double sh[32];
+  __shared__ Quat s_alpha;
+  __shared__ double s_beta;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int64_t t = tid; t < q * q; t += 1024) stQ(T + ((t / q) * ldt + (t % q)) * 4, qzero());
+  for (int64_t k = 0; k < q; ++k) {
+    double* x = Zcm + (k * p + k) * 4;
+    const int64_t len = p - k;
+    double part = 0.0;
+    for (int64_t i = tid; i < len; i += 1024) part += qnorm2(ldQ(x + i * 4));
+    const double norm2 = block_sum<1024>(part, sh);
+    if (tid == 0) {
+      if (norm2 == 0.0) {
+        s_beta = 0.0;
+        s_alpha = qzero();
+      } else {
+        const double nrm = sqrt(norm2);
+        const Quat x1 = ldQ(x);
+        const double a1 = sqrt(qnorm2(x1));
+        Quat alpha = a1 > 0.0 ? qscale(x1, -nrm / a1) : Quat{-nrm, 0.0, 0.0, 0.0};
+        stQ(x, qsub(x1, alpha));  // v = x - alpha e1
+        s_alpha = alpha;
+        s_beta = 1.0 / (norm2 + nrm * a1);
+      }
+      betas[k] = s_beta;
+    }
+    __syncthreads();
+    const double beta = s_beta;
+    if (tid == 0) stQ(T + (k * ldt + k) * 4, s_alpha);
+    if (beta != 0.0) {
+      for (int64_t j = k + 1 + warp; j < q; j += 32) {
+        double* y = Zcm + (j * p + k) * 4;
+        Quat w = qzero();
+        for (int64_t i = lane; i < len; i += 32) qfma_conj(w, ldQ(x + i * 4), ldQ(y + i * 4));
+        w = qscale(warp_sum(w), beta);
+        for (int64_t i = lane; i < len; i += 32) stQ(y + i * 4, qsub(ldQ(y + i * 4), qmul(ldQ(x + i * 4), w)));
+      }
+    }
+    __syncthreads();
+    for (int64_t j = k + 1 + tid; j < q; j += 1024) stQ(T + (k * ldt + j) * 4, ldQ(Zcm + (j * p + k) * 4));
+  }
+  // Q = H_0 ... H_{q-1} [I; 0]
+  for (int64_t t = tid; t < p * q; t += 1024) {
+    const int64_t j = t / p, i = t - j * p;
+    stQ(Qcm + t * 4, Quat{i == j ? 1.0 : 0.0, 0.0, 0.0, 0.0});
+  }
+  __syncthreads();
+  for (int64_t k = q - 1; k >= 0; --k) {
+    const double beta = betas[k];
+    if (beta == 0.0) continue;
+    const double* v = Zcm + (k * p + k) * 4;
+    const int64_t len = p - k;
+    for (int64_t j = k + warp; j < q; j += 32) {
+      double* y = Qcm + (j * p + k) * 4;
+      Quat w = qzero();
+      for (int64_t i = lane; i < len; i += 32) qfma_conj(w, ldQ(v + i * 4), ldQ(y + i * 4));
+      w = qscale(warp_sum(w), beta);
+      for (int64_t i = lane; i < len; i += 32) stQ(y + i * 4, qsub(ldQ(y + i * 4), qmul(ldQ(v + i * 4), w)));
+    }
+    __syncthreads();
+  }
+}
+
+// One-sided Jacobi SVD of T (q x q, column-major copy in Tcm), then
+// F = T^+ = sum_{sigma_j > cutoff} v_j t_j^H / sigma_j^2  (row-major, ld ldf).
+__global__ void __launch_bounds__(1024) k_jacobi_pinv(double* Tcm, double* Vcm, int64_t q, double cutoff_scale,
+                                                      double cutoff_abs, double* F, int64_t ldf,
+                                                      const unsigned* status, unsigned gate_bit) {
+  if (!(*status & gate_bit)) return;
+  __shared__ int s_rot;
+  __shared__ double sh[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int64_t t = tid; t < q * q; t += 1024) {
+    const int64_t j = t / q, i = t - j * q;
+    stQ(Vcm + t * 4, Quat{i == j ? 1.0 : 0.0, 0.0, 0.0, 0.0});
+  }
+  __syncthreads();
+  const int64_t qq = q + (q & 1);
+  const int64_t npairs = qq / 2;
+  const double tol = 4.0 * DBL_EPSILON;
+  for (int sweep = 0; sweep < 60 && q > 1; ++sweep) {
+    if (tid == 0) s_rot = 0;
+    __syncthreads();
+    for (int64_t rnd = 0; rnd < qq - 1; ++rnd) {
+      for (int64_t pk = warp; pk < npairs; pk += 32) {
+        int64_t a, b;
+        if (pk == 0) {
+          a = rnd;
+          b = qq - 1;
+        } else {
+          a = (rnd + pk) % (qq - 1);
+          b = (rnd - pk + (qq - 1)) % (qq - 1);
+        }
+        if (a >= q || b >= q) continue;
+        double* ta = Tcm + a * q * 4;
+        double* tb = Tcm + b * q * 4;
+        double al = 0.0, be = 0.0;
+        Quat g = qzero();
+        for (int64_t i = lane; i < q; i += 32) {
+          const Quat xa = ldQ(ta + i * 4), xb = ldQ(tb + i * 4);
+          al += qnorm2(xa);
+          be += qnorm2(xb);
+          qfma_conj(g, xa, xb);
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        g = warp_sum(g);
+        const double gn = sqrt(qnorm2(g));
+        if (!(al > 0.0) || !(be > 0.0) || gn <= tol * sqrt(al) * sqrt(be)) continue;
+        if (lane == 0) s_rot = 1;
+        const Quat mu_bar = qconj(qscale(g, 1.0 / gn));
+        const double zeta = (be - al) / (2.0 * gn);
+        const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / sqrt(1.0 + tt * tt), s = c * tt;
+        double* va = Vcm + a * q * 4;
+        double* vb = Vcm + b * q * 4;
+        for (int64_t i = lane; i < q; i += 32) {
+          const Quat xa = ldQ(ta + i * 4), xb = qmul(ldQ(tb + i * 4), mu_bar);
+          stQ(ta + i * 4, qsub(qscale(xa, c), qscale(xb, s)));
+          stQ(tb + i * 4, qadd(qscale(xa, s), qscale(xb, c)));
+          const Quat ya = ldQ(va + i * 4), yb = qmul(ldQ(vb + i * 4), mu_bar);
+          stQ(va + i * 4, qsub(qscale(ya, c), qscale(yb, s)));
+          stQ(vb + i * 4, qadd(qscale(ya, s), qscale(yb, c)));
+        }
+      }
+      __syncthreads();
+    }
+    if (!s_rot) break;
+    __syncthreads();
+  }
+  // singular values = column norms; cutoff = eps * max(shape) * sigma_max (linalg.py:338-339)
+  double* sig = Vcm + q * q * 4;  // caller reserves q extra doubles after Vcm
+  for (int64_t j = warp; j < q; j += 32) {
+    double s2 = 0.0;
+    for (int64_t i = lane; i < q; i += 32) s2 += qnorm2(ldQ(Tcm + (j * q + i) * 4));
+    s2 = warp_sum(s2);
+    if (lane == 0) sig[j] = s2;
+  }
+  __syncthreads();
+  double mx = 0.0;
+  for (int64_t j = tid; j < q; j += 1024) mx = fmax(mx, sig[j]);
+  // block max
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  __syncthreads();
+  if (lane == 0) sh[warp] = mx;
+  __syncthreads();
+  double smax2 = 0.0;
+  for (int k = 0; k < 32; ++k) smax2 = fmax(smax2, sh[k]);
+  const double smax = sqrt(smax2);
+  const double cutoff = cutoff_abs >= 0.0 ? cutoff_abs : cutoff_scale * smax;
+  for (int64_t t = tid; t < q * q; t += 1024) {
+    const int64_t a = t / q, b = t - a * q;
+    Quat acc = qzero();
+    if (smax > 0.0) {
+      for (int64_t j = 0; j < q; ++j) {
+        const double s2 = sig[j];
+        if (!(sqrt(s2) > cutoff)) continue;
+        // v_j[a] * conj(t_j[b]) / sigma_j^2
+        Quat term = qmul(ldQ(Vcm + (j * q + a) * 4), qconj(ldQ(Tcm + (j * q + b) * 4)));
+        acc = qadd(acc, qscale(term, 1.0 / s2));
+      }
+    }
+    stQ(F + (a * ldf + b) * 4, acc);
+  }
+}
+
+// ---------------------------------------------------------------------------
+__global__ void k_set_status(unsigned* status, unsigned bits) { atomicOr(status, bits); }
+void launch_set_status(unsigned* status, unsigned bits, cudaStream_t st) { k_set_status<<<1, 1, 0, st>>>(status, bits); }
+
+void launch_cholesky(double* G, int64_t q, int64_t ldg, unsigned* status, unsigned fail_bit, cudaStream_t st) {
+  k_cholesky<<<1, 1024, 0, st>>>(G, q, ldg, status, fail_bit);
+}
+void launch_tri_inverse_lower(const double* L, int64_t q, int64_t ldl, double* Linv, int64_t ldi, cudaStream_t st) {
+  const int wpb = 8;
+  k_tri_inverse_lower<<<(unsigned)((q + wpb - 1) / wpb), wpb * 32, 0, st>>>(L, q, ldl, Linv, ldi);
+}
+void launch_set_identity(double* A, int64_t q, int64_t lda, cudaStream_t st) {
+  int blocks = (int)((q * q + 255) / 256);
+  if (blocks > 1184) blocks = 1184;
+  k_set_identity<<<blocks, 256, 0, st>>>(A, q, lda);
+}
+void launch_kappa_check(const double* T, const double* Tinv, int64_t q, double limit, unsigned* status,
+                        unsigned fail_bit, cudaStream_t st) {
+  k_kappa_check<<<1, 1024, 0, st>>>(T, Tinv, q, limit, status, fail_bit);
+}
+void launch_householder_qr(double* Zcm, int64_t p, int64_t q, double* betas, double* Qcm, double* T, int64_t ldt,
+                           const unsigned* status, unsigned gate_bit, cudaStream_t st) {
+  k_householder_qr<<<1, 1024, 0, st>>>(Zcm, p, q, betas, Qcm, T, ldt, status, gate_bit);
+}
+void launch_jacobi_pinv_factor(double* Tcm, double* Vcm, int64_t q, double cutoff_scale, double cutoff_abs, double* F,
+                               int64_t ldf, const unsigned* status, unsigned gate_bit, cudaStream_t st) {
+  k_jacobi_pinv<<<1, 1024, 0, st>>>(Tcm, Vcm, q, cutoff_scale, cutoff_abs, F, ldf, status, gate_bit);
+}
+
+__global__ void k_conj_copy(const double* __restrict__ src, int64_t count, double* __restrict__ dst,
+                            const unsigned* status, unsigned gate_bit) {
+  if (!(*status & gate_bit)) return;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x)
+    stQ(dst + t * 4, qconj(ldQ(src + t * 4)));
+}
+void launch_conj_copy(const double* src, int64_t count_q, double* dst, const unsigned* status, unsigned gate_bit,
+                      cudaStream_t st) {
+  int blocks = (int)((count_q + 255) / 256);
+  if (blocks > 1184) blocks = 1184;
+  if (blocks < 1) blocks = 1;
+  k_conj_copy<<<blocks, 256, 0, st>>>(src, count_q, dst, status, gate_bit);
+}
+void launch_rowmajor_to_colmajor(const double* Z, int64_t p, int64_t q, int64_t ldz, double* Zcm,
+                                 const unsigned* status, unsigned gate_bit, cudaStream_t st) {
+  int blocks = (int)((p * q + 255) / 256);
+  if (blocks > 1184) blocks = 1184;
+  if (blocks < 1) blocks = 1;
+  k_row_to_col<<<blocks, 256, 0, st>>>(Z, p, q, ldz, Zcm, status, gate_bit);
+}
+void launch_colmajor_to_rowmajor(const double* Zcm, int64_t p, int64_t q, double* Z, int64_t ldz,
+                                 const unsigned* status, unsigned gate_bit, int gate_invert, cudaStream_t st) {
+  int blocks = (int)((p * q + 255) / 256);
+  if (blocks > 1184) blocks = 1184;
+  if (blocks < 1) blocks = 1;
+  k_col_to_row<<<blocks, 256, 0, st>>>(Zcm, p, q, Z, ldz, status, gate_bit, gate_invert);
+}
+
+}  // namespace qcur

@@ -1,0 +1,226 @@
+// K1 — length-squared sampling distributions, bit-identical to numpy.
+//
+// Replaces length_distributions (pkg/src/qcur/cur.py:132-150):
+//   sq    = ((a0^2 + a1^2) + a2^2) + a3^2        per entry, no FMA   (cur.py:143)
+//   total = pairwise(sq.ravel())                                     (cur.py:144)
+//   col   = sequential sum down the rows                             (cur.py:147)
+//   row   = pairwise sum along each row                              (cur.py:148)
+//   col/total, row/total, then divided by their own pairwise sums    (cur.py:150)
+//
+// Pass A (k1_colstrip): one CTA per 32-column strip streams its strip of X
+// top to bottom (coalesced 1 KB row segments, register double-buffered),
+// computes sq, writes it row-major for pass B and keeps the exact sequential
+// column accumulator in one lane per column.
+// Pass B (pairwise_chunks / pairwise_top): numpy's pairwise tree over each row
+// and over the flat array, evaluated from the sq buffer chunk by chunk.
+#include "common.cuh"
+#include "kernels.h"
+#include "pairwise.h"
+
+namespace qcur {
+
+// ---------------------------------------------------------------------------
+// Pass A: sq + exact sequential column sums.
+// ---------------------------------------------------------------------------
+constexpr int kStripW = 32;   // quaternion columns per CTA (one warp lane each)
+constexpr int kStripRB = 64;  // rows per pipeline stage (8 quaternions in flight per thread)
+constexpr int kStripThreads = 256;
+
+__global__ void __launch_bounds__(kStripThreads) k1_colstrip(const double* __restrict__ X, int64_t m, int64_t n,
+                                                             int64_t ldx, double* __restrict__ sq,
+                                                             double* __restrict__ colsum) {
+  __shared__ double sqs[2][kStripRB][kStripW];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int wrow = tid >> 5;  // 0..7
+  const int64_t j = (int64_t)blockIdx.x * kStripW + lane;
+  const bool jok = j < n;
+  constexpr int kPer = kStripRB / 8;  // rows per thread per stage
+  Quat buf[kPer];
+  auto load_stage = [&](int64_t r0) {
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      int64_t i = r0 + wrow + 8 * k;
+      if (jok && i < m)
+        buf[k] = ldq_nc(X + (i * ldx + j) * 4);
+      else
+        buf[k] = qzero();
+    }
+  };
+  double acc = 0.0;  // numpy starts from the first row; 0 + sq[0] == sq[0] exactly (sq >= 0)
+  const int64_t nstages = (m + kStripRB - 1) / kStripRB;
+  load_stage(0);
+  for (int64_t s = 0; s < nstages; ++s) {
+    const int64_t r0 = s * kStripRB;
+    const int b = (int)(s & 1);
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const Quat q = buf[k];
+      double v = __dmul_rn(q.w, q.w);
+      v = __dadd_rn(v, __dmul_rn(q.x, q.x));
+      v = __dadd_rn(v, __dmul_rn(q.y, q.y));
+      v = __dadd_rn(v, __dmul_rn(q.z, q.z));
+      const int rr = wrow + 8 * k;
+      sqs[b][rr][lane] = v;
+      const int64_t i = r0 + rr;
+      if (jok && i < m) sq[i * n + j] = v;
+    }
+    if (s + 1 < nstages) load_stage(r0 + kStripRB);
+    __syncthreads();
+    if (wrow == 0) {
+      const int rows = (int)((m - r0) < kStripRB ? (m - r0) : kStripRB);
+      for (int rr = 0; rr < rows; ++rr) acc = __dadd_rn(acc, sqs[b][rr][lane]);
+    }
+    // the double buffer lets the next stage's sq writes proceed while warp 0
+    // accumulates; a second barrier is only needed before a buffer is reused,
+    // which the barrier of the following stage provides.
+  }
+  if (wrow == 0 && jok) colsum[j] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// Pass B: numpy pairwise trees.
+// ---------------------------------------------------------------------------
+constexpr int kChunkThreads = 256;
+
+// One CTA evaluates one chunk (<= kChunkMax elements) of one segment.
+// out[seg * out_stride + chunk]
+__global__ void __launch_bounds__(kChunkThreads) pairwise_chunks(const double* __restrict__ data, int64_t seg_stride,
+                                                                 DevPairwise pw, double* __restrict__ out,
+                                                                 int64_t out_stride) {
+  extern __shared__ double sm[];
+  const int chunk = blockIdx.x;
+  const int64_t seg = blockIdx.y;
+  const int pid = pw.chunk_plan[chunk];
+  const int len = pw.plan_len[pid];
+  const int leaf0 = pw.plan_leaf_ptr[pid], nleaves = pw.plan_leaf_ptr[pid + 1] - leaf0;
+  const double* src = data + seg * seg_stride + pw.chunk_off[chunk];
+  double* vals = sm;            // [len]
+  double* leafv = sm + len;     // [nleaves]
+  for (int t = threadIdx.x; t < len; t += blockDim.x) vals[t] = src[t];
+  __syncthreads();
+  const int q = threadIdx.x & 7;
+  for (int base = 0; base < nleaves; base += kChunkThreads / 8) {
+    const int leaf = base + (threadIdx.x >> 3);
+    const bool active = leaf < nleaves;
+    int off = 0, ln = 0;
+    if (active) {
+      off = pw.leaf_off[leaf0 + leaf];
+      ln = pw.leaf_len[leaf0 + leaf];
+    }
+    double r = 0.0;
+    const int body = ln - (ln & 7);
+    if (active && ln >= 8) {
+      r = vals[off + q];
+      for (int i = 8; i < body; i += 8) r = __dadd_rn(r, vals[off + i + q]);
+    }
+    // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) in lane group order
+    double t1 = __shfl_xor_sync(0xffffffffu, r, 1);
+    double a = __dadd_rn(r, t1);
+    double t2 = __shfl_xor_sync(0xffffffffu, a, 2);
+    double bsum = __dadd_rn(a, t2);
+    double t4 = __shfl_xor_sync(0xffffffffu, bsum, 4);
+    double res = __dadd_rn(bsum, t4);
+    if (active && q == 0) {
+      if (ln < 8) {
+        res = 0.0;
+        for (int i = 0; i < ln; ++i) res = __dadd_rn(res, vals[off + i]);
+      } else {
+        for (int i = body; i < ln; ++i) res = __dadd_rn(res, vals[off + i]);
+      }
+      leafv[leaf] = res;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int p0 = pw.plan_prog_ptr[pid], p1 = pw.plan_prog_ptr[pid + 1];
+    double stack[24];
+    int sp = 0;
+    for (int p = p0; p < p1; ++p) {
+      const int op = pw.prog[p];
+      if (op >= 0) {
+        stack[sp++] = leafv[op];
+      } else {
+        const double b = stack[--sp];
+        const double a2 = stack[--sp];
+        stack[sp++] = __dadd_rn(a2, b);
+      }
+    }
+    out[seg * out_stride + chunk] = stack[0];
+  }
+}
+
+// Top tree over chunk sums; one CTA per segment.  vals: [nseg][nchunks+nnodes]
+__global__ void pairwise_top(double* __restrict__ vals, DevPairwise pw, double* __restrict__ out) {
+  const int64_t seg = blockIdx.x;
+  const int64_t w = (int64_t)pw.nchunks + pw.nnodes;
+  double* v = vals + seg * w;
+  for (int h = 1; h <= pw.maxh; ++h) {
+    const int a = pw.level_ptr[h], b = pw.level_ptr[h + 1];
+    for (int k = a + threadIdx.x; k < b; k += blockDim.x)
+      v[pw.nchunks + k] = __dadd_rn(v[pw.node_l[k]], v[pw.node_r[k]]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[seg] = pw.nnodes > 0 ? v[w - 1] : v[0];
+}
+
+__global__ void k1_scale(const double* __restrict__ in, int64_t len, const double* __restrict__ denom,
+                         double* __restrict__ out, unsigned* status, unsigned check_bit) {
+  const double d = *denom;
+  if (check_bit && blockIdx.x == 0 && threadIdx.x == 0 && !(d > 0.0)) atomicOr(status, check_bit);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < len; t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = __ddiv_rn(in[t], d);
+}
+
+__global__ void k_fill(double* __restrict__ out, int64_t len, double v) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < len; t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = v;
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------
+void launch_colstrip(const double* X, int64_t m, int64_t n, int64_t ldx, double* sq, double* colsum,
+                     cudaStream_t st) {
+  dim3 grid((unsigned)((n + kStripW - 1) / kStripW));
+  k1_colstrip<<<grid, kStripThreads, 0, st>>>(X, m, n, ldx, sq, colsum);
+}
+
+void launch_pairwise(const double* data, int64_t nseg, int64_t seg_stride, const DevPairwise& pw, double* scratch,
+                     double* out, cudaStream_t st) {
+  size_t smem = (size_t)(kChunkMax + kChunkMax / 8 + 8) * sizeof(double);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(pairwise_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = true;
+  }
+  // dynamic smem only as large as the largest chunk needs
+  size_t need = (size_t)(pw.max_chunk_len + pw.max_chunk_len / 8 + 8) * sizeof(double);
+  if (pw.nnodes == 0) {
+    // single chunk per segment: write straight to out
+    dim3 grid(1, (unsigned)nseg);
+    pairwise_chunks<<<grid, kChunkThreads, need, st>>>(data, seg_stride, pw, out, 1);
+    return;
+  }
+  const int64_t w = (int64_t)pw.nchunks + pw.nnodes;
+  dim3 grid((unsigned)pw.nchunks, (unsigned)nseg);
+  pairwise_chunks<<<grid, kChunkThreads, need, st>>>(data, seg_stride, pw, scratch, w);
+  pairwise_top<<<(unsigned)nseg, 256, 0, st>>>(scratch, pw, out);
+}
+
+void launch_scale(const double* in, int64_t len, const double* denom, double* out, unsigned* status,
+                  unsigned check_bit, cudaStream_t st) {
+  int blocks = (int)((len + 255) / 256);
+  if (blocks > 1184) blocks = 1184;
+  if (blocks < 1) blocks = 1;
+  k1_scale<<<blocks, 256, 0, st>>>(in, len, denom, out, status, check_bit);
+}
+
+void launch_fill(double* out, int64_t len, double v, cudaStream_t st) {
+  int blocks = (int)((len + 255) / 256);
+  if (blocks > 1184) blocks = 1184;
+  if (blocks < 1) blocks = 1;
+  k_fill<<<blocks, 256, 0, st>>>(out, len, v);
+}
+
+}  // namespace qcur

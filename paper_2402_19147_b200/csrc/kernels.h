@@ -1,0 +1,108 @@
+// Internal launcher interface between the C-ABI orchestration (qcur_abi.cu)
+// and the kernel translation units.  Not part of the public ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace qcur {
+
+struct DevPairwise {
+  int64_t length;
+  int32_t nchunks, nnodes, maxh, max_chunk_len;
+  const int64_t* chunk_off;
+  const int32_t* chunk_plan;
+  const int32_t* plan_len;
+  const int32_t* plan_leaf_ptr;
+  const int32_t* plan_prog_ptr;
+  const int32_t* leaf_off;
+  const int32_t* leaf_len;
+  const int32_t* prog;
+  const int32_t* node_l;
+  const int32_t* node_r;
+  const int32_t* level_ptr;
+};
+
+// k_norms.cu
+void launch_colstrip(const double* X, int64_t m, int64_t n, int64_t ldx, double* sq, double* colsum, cudaStream_t st);
+void launch_pairwise(const double* data, int64_t nseg, int64_t seg_stride, const DevPairwise& pw, double* scratch,
+                     double* out, cudaStream_t st);
+void launch_scale(const double* in, int64_t len, const double* denom, double* out, unsigned* status,
+                  unsigned check_bit, cudaStream_t st);
+void launch_fill(double* out, int64_t len, double v, cudaStream_t st);
+
+// k_draw.cu
+struct DrawJob {
+  const double* probs;  // [len]
+  int64_t len;
+  int64_t count;
+  uint64_t st_hi, st_lo, inc_hi, inc_lo;  // PCG64 state at the first uniform of this job
+  int64_t* out;                           // [count]
+  double* work;                           // >= draw_work_doubles(len)
+};
+int64_t draw_work_doubles(int64_t len);
+void launch_draw(const DrawJob* jobs_host, int njobs, unsigned* status, cudaStream_t st);  // njobs <= 2
+
+// k_layout.cu
+void launch_planar_to_interleaved(const double* a0, const double* a1, const double* a2, const double* a3, int64_t m,
+                                  int64_t n, double* X, cudaStream_t st);
+void launch_interleaved_to_planar(const double* X, int64_t m, int64_t n, int64_t ldx, double* a0, double* a1,
+                                  double* a2, double* a3, cudaStream_t st);
+void launch_gather_cols(const double* X, int64_t m, int64_t ldx, const int64_t* J, int64_t c, double* C,
+                        cudaStream_t st);
+void launch_gather_rows(const double* X, int64_t n, int64_t ldx, const int64_t* I, int64_t r, double* R,
+                        cudaStream_t st);
+void launch_conj_transpose(const double* A, int64_t m, int64_t n, int64_t lda, double* AH, int64_t ldah,
+                           cudaStream_t st);
+void launch_reduce_pairs(const double* parts, int64_t nparts, double* out2, cudaStream_t st);
+
+// k_qgemm.cu : C(Mq x Nq) = alpha * op(A) * op(B) + beta * C, quaternion, interleaved.
+// op: 0 = N, 1 = H (conjugate transpose).  lda/ldb/ldc in quaternions.
+struct GemmArgs {
+  int64_t Mq, Nq, Kq;
+  const double* A;
+  int64_t lda;
+  int opA;
+  const double* B;
+  int64_t ldb;
+  int opB;
+  double* C;
+  int64_t ldc;
+  double alpha, beta;
+};
+size_t qgemm_workspace_bytes(const GemmArgs& g);
+void launch_qgemm(const GemmArgs& g, double* workspace, cudaStream_t st);
+// ||X - P R||_F^2 and ||X||_F^2 partials, P: m x r, R: r x n, X: m x n (all interleaved)
+int64_t err_partials_count(int64_t m, int64_t n);
+void launch_cur_error(const double* X, int64_t ldx, const double* P, int64_t ldp, const double* R, int64_t ldr,
+                      int64_t m, int64_t n, int64_t r, double* partials, double* out2, cudaStream_t st);
+
+// k_dense.cu : small (q x q) dense factorizations, one CTA each.
+void launch_cholesky(double* G, int64_t q, int64_t ldg, unsigned* status, unsigned fail_bit, cudaStream_t st);
+void launch_tri_inverse_lower(const double* L, int64_t q, int64_t ldl, double* Linv, int64_t ldi, cudaStream_t st);
+void launch_set_identity(double* A, int64_t q, int64_t lda, cudaStream_t st);
+void launch_set_status(unsigned* status, unsigned bits, cudaStream_t st);
+void launch_kappa_check(const double* T, const double* Tinv, int64_t q, double limit, unsigned* status,
+                        unsigned fail_bit, cudaStream_t st);
+// robust path (runs only when `status & gate_bit`, otherwise returns immediately)
+void launch_householder_qr(double* Zcm, int64_t p, int64_t q, double* alpha, double* Qcm, double* T, int64_t ldt,
+                           const unsigned* status, unsigned gate_bit, cudaStream_t st);
+// cutoff = cutoff_abs if cutoff_abs >= 0 else cutoff_scale * sigma_max; Vcm needs q*q*4 + q doubles
+void launch_jacobi_pinv_factor(double* Tcm, double* Vcm, int64_t q, double cutoff_scale, double cutoff_abs, double* F,
+                               int64_t ldf, const unsigned* status, unsigned gate_bit, cudaStream_t st);
+void launch_conj_copy(const double* src, int64_t count_q, double* dst, const unsigned* status, unsigned gate_bit,
+                      cudaStream_t st);
+void launch_colmajor_to_rowmajor(const double* Zcm, int64_t p, int64_t q, double* Z, int64_t ldz,
+                                 const unsigned* status, unsigned gate_bit, int gate_invert, cudaStream_t st);
+void launch_rowmajor_to_colmajor(const double* Z, int64_t p, int64_t q, int64_t ldz, double* Zcm,
+                                 const unsigned* status, unsigned gate_bit, cudaStream_t st);
+
+// k_synth.cu : synthetic workloads (Philox normal generator)
+void launch_normal_fill(double* out, int64_t count, uint64_t seed, uint64_t stream, double scale, cudaStream_t st);
+void launch_add_scaled_noise(double* X, int64_t count, uint64_t seed, uint64_t stream, const double* ssq,
+                             double rel, cudaStream_t st);
+void launch_sumsq(const double* X, int64_t count, double* partials, int64_t nparts, double* out, cudaStream_t st);
+
+// fp64 peak probe (bench roofline denominator)
+double run_dmma_peak(int sms, cudaStream_t st);
+
+}  // namespace qcur

@@ -1,0 +1,342 @@
+"""QMCUR — the reference's Algorithm-1 entry points, running on the B200.
+
+Drop-in mirror of ``qcur.cur`` for the hot path (pkg/src/qcur/cur.py:39-274):
+same names, signatures, return types, validation and exceptions.  Every
+numeric step runs on the GPU through the C ABI (include/qcur_b200.h):
+
+  make_plan            cur.py:175-199  -> qcur_length_distributions (K1, numpy-bit-exact)
+  draw_indices         cur.py:202-242  -> qcur_draw_indices          (K2, index-exact)
+  plan_indices         cur.py:245-254  -> (same, one PCG64 stream, columns first)
+  qmcur                cur.py:257-269  -> qcur_qmcur  (K2+K3 gathers+pinv+U on DMMA)
+  cur_reconstruct      cur.py:272-274  -> qcur_qgemm x2
+  cur_relative_error   (callers cli.py:173-175, imaging.py:170-177) -> qcur_cur_error,
+                       fused ||X - CUR||_F without materialising CUR.
+
+Host code here only validates arguments and moves data.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .errors import (
+    DegenerateDistributionError,  # noqa: F401  (re-exported for drop-in imports)
+    ParameterError,
+    SamplingError,
+    ShapeError,
+)
+from .quat import QMatrix, as_planes, from_device, to_device
+
+__all__ = [
+    "STRATEGIES",
+    "SamplingPlan",
+    "CURFactors",
+    "length_distributions",
+    "uniform_distributions",
+    "default_sample_counts",
+    "make_plan",
+    "draw_indices",
+    "plan_indices",
+    "qmcur",
+    "cur_reconstruct",
+    "cur_relative_error",
+    "qmcur_device",
+]
+
+STRATEGIES = ("length", "uniform")
+
+
+def _check_strategy(strategy: str) -> str:
+    if strategy not in STRATEGIES:
+        raise ParameterError(f"strategy must be one of {STRATEGIES}, got {strategy!r}")
+    return strategy
+
+
+def _validated_probs(p, name: str) -> np.ndarray:
+    arr = np.asarray(p, dtype=np.float64)
+    if arr.ndim != 1 or arr.size == 0:
+        raise ShapeError(f"{name} must be a non-empty 1-D array")
+    if np.any(arr < 0) or not np.all(np.isfinite(arr)):
+        raise ParameterError(f"{name} must be finite and nonnegative")
+    total = arr.sum()
+    if abs(total - 1.0) > 1e-12:
+        raise ParameterError(f"{name} must sum to 1 (got {total!r})")
+    return arr
+
+
+@dataclass(frozen=True)
+class SamplingPlan:
+    """Strategy, target rank, sample counts |I| = num_rows, |J| = num_cols, seed
+    and the two sampling distributions (cur.py:76-107)."""
+
+    strategy: str
+    rank: int
+    num_rows: int
+    num_cols: int
+    seed: int
+    row_probs: np.ndarray = field(repr=False)
+    col_probs: np.ndarray = field(repr=False)
+
+    def __post_init__(self) -> None:
+        _check_strategy(self.strategy)
+        if self.rank < 1:
+            raise ParameterError(f"rank must be positive, got {self.rank}")
+        if self.num_rows < self.rank or self.num_cols < self.rank:
+            raise ParameterError(
+                f"sample counts ({self.num_rows}, {self.num_cols}) must be >= rank {self.rank}"
+            )
+        rp = _validated_probs(self.row_probs, "row_probs")
+        cp = _validated_probs(self.col_probs, "col_probs")
+        if rp is self.row_probs:
+            rp = rp.copy()
+        if cp is self.col_probs:
+            cp = cp.copy()
+        rp.setflags(write=False)
+        cp.setflags(write=False)
+        object.__setattr__(self, "row_probs", rp)
+        object.__setattr__(self, "col_probs", cp)
+        if self.num_rows > rp.size or self.num_cols > cp.size:
+            raise ParameterError("sample counts exceed the available indices")
+
+
+@dataclass(frozen=True)
+class CURFactors:
+    """C = X[:, J], R = X[I, :], U = pinv(C) X pinv(R) (cur.py:110-129)."""
+
+    row_indices: np.ndarray
+    col_indices: np.ndarray
+    c: QMatrix
+    u: QMatrix
+    r: QMatrix
+
+    def __post_init__(self) -> None:
+        for name in ("row_indices", "col_indices"):
+            idx = np.array(getattr(self, name), dtype=np.intp)
+            idx.setflags(write=False)
+            object.__setattr__(self, name, idx)
+        if tuple(self.u.shape) != (self.col_indices.size, self.row_indices.size):
+            raise ShapeError(
+                f"U has shape {tuple(self.u.shape)}, expected "
+                f"({self.col_indices.size}, {self.row_indices.size})"
+            )
+
+
+# ---------------------------------------------------------------------------
+def _to_dev_vec(dev, arr: np.ndarray):
+    return dev.torch.from_numpy(np.array(arr, dtype=np.float64, copy=True)).to(f"cuda:{dev.index}")
+
+
+def length_distributions(x) -> tuple[np.ndarray, np.ndarray]:
+    """Squared-norm weights (col_probs, row_probs), bit-identical to the
+    reference's numpy evaluation (cur.py:132-150).
+
+    Raises DegenerateDistributionError for the zero matrix."""
+    dev = _native.device()
+    m, n = (int(v) for v in x.shape)
+    xd = to_device(x, dev)
+    col = dev.empty(n)
+    row = dev.empty(m)
+    dev.call("qcur_length_distributions", xd.data_ptr(), m, n, col.data_ptr(), row.data_ptr())
+    return col.cpu().numpy(), row.cpu().numpy()
+
+
+def uniform_distributions(m: int, n: int) -> tuple[np.ndarray, np.ndarray]:
+    """Flat weights 1/n per column and 1/m per row (cur.py:153-157)."""
+    if m < 1 or n < 1:
+        raise ParameterError(f"dimensions must be positive, got ({m}, {n})")
+    dev = _native.device()
+    col = dev.empty(int(n))
+    row = dev.empty(int(m))
+    dev.call("qcur_uniform_distributions", int(m), int(n), col.data_ptr(), row.data_ptr())
+    return col.cpu().numpy(), row.cpu().numpy()
+
+
+def default_sample_counts(k: int, m: int, n: int) -> tuple[int, int]:
+    """|I| = |J| = min(max(k, ceil(k ln k)), min(m, n)) (cur.py:160-172)."""
+    if k < 1:
+        raise ParameterError(f"k must be positive, got {k}")
+    if k > min(m, n):
+        raise ParameterError(f"k={k} exceeds min(m, n)={min(m, n)}")
+    grown = math.ceil(k * math.log(max(k, 2)))
+    count = min(max(k, grown), min(m, n))
+    return count, count
+
+
+def make_plan(x, strategy: str, rank: int, seed: int, num_rows: int | None = None,
+              num_cols: int | None = None) -> SamplingPlan:
+    """SamplingPlan for x with defaulted sample counts (cur.py:175-199)."""
+    _check_strategy(strategy)
+    m, n = (int(v) for v in x.shape)
+    d_rows, d_cols = default_sample_counts(rank, m, n)
+    if strategy == "length":
+        col_probs, row_probs = length_distributions(x)
+    else:
+        col_probs, row_probs = uniform_distributions(m, n)
+    return SamplingPlan(
+        strategy=strategy,
+        rank=rank,
+        num_rows=num_rows if num_rows is not None else d_rows,
+        num_cols=num_cols if num_cols is not None else d_cols,
+        seed=int(seed),
+        row_probs=row_probs,
+        col_probs=col_probs,
+    )
+
+
+def draw_indices(probs, count: int, seed) -> np.ndarray:
+    """``count`` distinct indices by iterated weighted selection (cur.py:202-242).
+
+    ``seed`` is an int or a numpy ``Generator`` (PCG64); a Generator is
+    advanced by exactly ``count`` doubles, as the reference consumes it."""
+    p = np.array(probs, dtype=np.float64, copy=True)
+    if p.ndim != 1 or p.size == 0:
+        raise ShapeError("probs must be a non-empty 1-D array")
+    if np.any(p < 0) or not np.all(np.isfinite(p)):
+        raise ParameterError("probs must be finite and nonnegative")
+    count = int(count)
+    if count < 1:
+        raise ParameterError(f"count must be positive, got {count}")
+    positive = int(np.count_nonzero(p > 0))
+    if count > positive:
+        raise SamplingError(f"cannot draw {count} distinct indices from {positive} positive weights")
+    gen = seed if isinstance(seed, np.random.Generator) else None
+    state = _native.state_from_generator(gen) if gen is not None else _native.state_from_seed(int(seed))
+    dev = _native.device()
+    pd = _to_dev_vec(dev, p)
+    out = dev.empty(count, dtype=dev.torch.int64)
+    dev.call("qcur_draw_indices", pd.data_ptr(), p.size, count, state.ctypes.data_as(_native._u64p),
+             out.data_ptr())
+    if gen is not None:
+        _native.store_generator_state(gen, state)
+    return out.cpu().numpy().astype(np.intp)
+
+
+def plan_indices(plan: SamplingPlan) -> tuple[np.ndarray, np.ndarray]:
+    """(row_indices, col_indices) of a plan: columns first, then rows, from one
+    stream seeded by plan.seed (cur.py:245-254)."""
+    rng = np.random.default_rng(plan.seed)
+    col_indices = draw_indices(plan.col_probs, plan.num_cols, rng)
+    row_indices = draw_indices(plan.row_probs, plan.num_rows, rng)
+    return row_indices, col_indices
+
+
+def _check_plan_shape(x, plan: SamplingPlan) -> tuple[int, int]:
+    m, n = (int(v) for v in x.shape)
+    if plan.col_probs.size != n or plan.row_probs.size != m:
+        raise ShapeError(
+            f"plan distributions sized ({plan.row_probs.size}, {plan.col_probs.size}) "
+            f"do not match matrix shape ({m}, {n})"
+        )
+    return m, n
+
+
+def qmcur(x, plan: SamplingPlan) -> CURFactors:
+    """Sampled CUR factorization of x under the given plan (cur.py:257-269)."""
+    m, n = _check_plan_shape(x, plan)
+    c, r = int(plan.num_cols), int(plan.num_rows)
+    for probs, count in ((plan.col_probs, c), (plan.row_probs, r)):
+        positive = int(np.count_nonzero(probs > 0))
+        if count > positive:
+            raise SamplingError(f"cannot draw {count} distinct indices from {positive} positive weights")
+    dev = _native.device()
+    xd = to_device(x, dev)
+    colp = _to_dev_vec(dev, plan.col_probs)
+    rowp = _to_dev_vec(dev, plan.row_probs)
+    state = _native.state_from_seed(plan.seed)
+    J = dev.empty(c, dtype=dev.torch.int64)
+    I = dev.empty(r, dtype=dev.torch.int64)
+    C = dev.empty_q(m, c)
+    U = dev.empty_q(c, r)
+    R = dev.empty_q(r, n)
+    dev.call("qcur_qmcur", xd.data_ptr(), m, n, colp.data_ptr(), rowp.data_ptr(), c, r,
+             state.ctypes.data_as(_native._u64p), J.data_ptr(), I.data_ptr(), C.data_ptr(), U.data_ptr(),
+             R.data_ptr())
+    return CURFactors(
+        row_indices=I.cpu().numpy(),
+        col_indices=J.cpu().numpy(),
+        c=from_device(C, dev),
+        u=from_device(U, dev),
+        r=from_device(R, dev),
+    )
+
+
+def cur_reconstruct(factors: CURFactors) -> QMatrix:
+    """C U R (cur.py:272-274), two DMMA GEMMs, downloaded to the host."""
+    dev = _native.device()
+    c, u, r = factors.c, factors.u, factors.r
+    dc, du, dr = to_device(c, dev), to_device(u, dev), to_device(r, dev)
+    m, kc = (int(v) for v in c.shape)
+    kr, n = (int(v) for v in r.shape)
+    if tuple(u.shape) != (kc, kr):
+        raise ShapeError(f"inner dimensions disagree: {tuple(c.shape)} @ {tuple(u.shape)} @ {tuple(r.shape)}")
+    P = dev.empty_q(m, kr)
+    dev.call("qcur_qgemm", 0, 0, m, kr, kc, 1.0, dc.data_ptr(), kc, du.data_ptr(), kr, 0.0, P.data_ptr(), kr)
+    out = dev.empty_q(m, n)
+    dev.call("qcur_qgemm", 0, 0, m, n, kr, 1.0, P.data_ptr(), kr, dr.data_ptr(), n, 0.0, out.data_ptr(), n)
+    return from_device(out, dev)
+
+
+def cur_relative_error(x, factors: CURFactors) -> float:
+    """||X - C U R||_F / ||X||_F, fused on the GPU (CUR never materialised).
+
+    Same value as the reference's callers compute (cli.py:173-175,
+    imaging.relative_error, imaging.py:170-177)."""
+    dev = _native.device()
+    m, n = (int(v) for v in x.shape)
+    c, u, r = factors.c, factors.u, factors.r
+    kc, kr = int(u.shape[0]), int(u.shape[1])
+    if tuple(c.shape) != (m, kc) or tuple(r.shape) != (kr, n):
+        raise ShapeError("factors do not match the matrix shape")
+    xd, dc, du, dr = to_device(x, dev), to_device(c, dev), to_device(u, dev), to_device(r, dev)
+    out2 = dev.empty(2)
+    dev.call("qcur_cur_error", xd.data_ptr(), m, n, dc.data_ptr(), kc, du.data_ptr(), dr.data_ptr(), kr,
+             out2.data_ptr())
+    e2, x2 = (float(v) for v in out2.cpu().numpy())
+    if x2 == 0.0:
+        raise ParameterError("reference matrix is zero; relative error undefined")
+    return math.sqrt(e2) / math.sqrt(x2)
+
+
+# ---------------------------------------------------------------------------
+# device-resident fast entry (bench `value`): no host round trip, no sync
+# ---------------------------------------------------------------------------
+class DeviceApprox:
+    """Preallocated outputs for repeated device-resident approximations."""
+
+    def __init__(self, m: int, n: int, c: int, r: int, dev=None):
+        self.dev = dev or _native.device()
+        d = self.dev
+        self.m, self.n, self.c, self.r = m, n, c, r
+        self.J = d.empty(c, dtype=d.torch.int64)
+        self.I = d.empty(r, dtype=d.torch.int64)
+        self.C = d.empty_q(m, c)
+        self.U = d.empty_q(c, r)
+        self.R = d.empty_q(r, n)
+        self.err2 = d.empty(2)
+
+    def run(self, xd, strategy: str, seed: int) -> None:
+        state = _native.state_from_seed(seed)
+        self.dev.call("qcur_approx", xd.data_ptr(), self.m, self.n, _native.STRATEGY_CODES[_check_strategy(strategy)],
+                      state.ctypes.data_as(_native._u64p), self.c, self.r, self.J.data_ptr(), self.I.data_ptr(),
+                      self.C.data_ptr(), self.U.data_ptr(), self.R.data_ptr(), self.err2.data_ptr())
+
+    def check(self) -> None:
+        self.dev.call("qcur_check")
+
+    def rel_error(self) -> float:
+        e2, x2 = (float(v) for v in self.err2.cpu().numpy())
+        return math.sqrt(e2) / math.sqrt(x2)
+
+
+def qmcur_device(xd, strategy: str, rank: int, seed: int, num_rows: int, num_cols: int) -> DeviceApprox:
+    """One whole approximation on a device-resident interleaved X (m, n, 4)."""
+    m, n = int(xd.shape[0]), int(xd.shape[1])
+    default_sample_counts(rank, m, n)
+    out = DeviceApprox(m, n, int(num_cols), int(num_rows))
+    out.run(xd, strategy, seed)
+    out.check()
+    return out

@@ -1,0 +1,179 @@
+"""GPU parity of the QMCUR path against the CPU oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star): probabilities and indices bit-exact, C / R
+bit-exact copies, U within 1e-9 relative Frobenius, reconstruction error
+within 1e-10 relative.  Every call goes through the C ABI.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2402_19147_b200 as q
+from paper_2402_19147_b200 import _native
+from helpers import lowrank, rand_mat, rel_fro_err
+
+pytestmark = pytest.mark.gpu
+
+U_TOL = 1e-9
+ERR_TOL = 1e-10
+
+
+def oracle_factors(x, plan):
+    rows, cols, c, u, r = O.qmcur(tuple(x.planes), plan.col_probs, plan.row_probs, plan.num_cols,
+                                  plan.num_rows, plan.seed)
+    return rows, cols, c, u, r
+
+
+def check_against_oracle(x, plan, f):
+    rows, cols, c, u, r = oracle_factors(x, plan)
+    assert np.array_equal(f.col_indices, cols)
+    assert np.array_equal(f.row_indices, rows)
+    for got, want in zip(f.c.planes, c):
+        assert np.array_equal(got, want)
+    for got, want in zip(f.r.planes, r):
+        assert np.array_equal(got, want)
+    du = O.rel_fro(tuple(f.u.planes), u)
+    assert du <= U_TOL, du
+    e2, x2 = O.cur_error(tuple(x.planes), c, u, r)
+    ref_err = math.sqrt(e2) / math.sqrt(x2)
+    got_err = q.cur_relative_error(x, f)
+    assert abs(got_err - ref_err) <= ERR_TOL * ref_err, (got_err, ref_err)
+    return du
+
+
+@pytest.mark.parametrize("m,n", [(6, 5), (37, 1029), (129, 7), (1000, 1000), (1, 1), (300, 8200)])
+def test_length_distributions_bitwise(m, n):
+    x = rand_mat(m, n, seed=m * 131 + n)
+    col, row = q.length_distributions(x)
+    ocol, orow = O.length_distributions(tuple(x.planes))
+    assert np.array_equal(col, ocol)
+    assert np.array_equal(row, orow)
+
+
+def test_length_zero_matrix_raises():
+    with pytest.raises(q.DegenerateDistributionError):
+        q.length_distributions(q.QMatrix.zeros(3, 3))
+
+
+def test_uniform_distributions():
+    col, row = q.uniform_distributions(7, 4)
+    assert np.array_equal(col, np.full(4, 0.25))
+    assert np.array_equal(row, np.full(7, 1.0 / 7.0))
+
+
+@pytest.mark.parametrize("size,count,seed", [(20, 12, 99), (9, 9, 5), (4000, 200, 1), (33, 30, 3), (1100, 1000, 8)])
+def test_draw_indices_exact(size, count, seed):
+    p = np.random.default_rng(seed).random(size) ** 3
+    p /= p.sum()
+    got = q.draw_indices(p, count, seed)
+    want = O.draw_indices(p, count, np.random.default_rng(seed))
+    assert np.array_equal(got, want)
+
+
+def test_draw_generator_stream_advances_like_numpy():
+    rng_a = np.random.default_rng(7)
+    rng_b = np.random.default_rng(7)
+    p = np.full(10, 0.1)
+    a1 = q.draw_indices(p, 4, rng_a)
+    a2 = q.draw_indices(p, 4, rng_a)
+    b1 = O.draw_indices(p, 4, rng_b)
+    b2 = O.draw_indices(p, 4, rng_b)
+    assert np.array_equal(a1, b1) and np.array_equal(a2, b2)
+    assert rng_a.random() == rng_b.random()
+
+
+def test_draw_zero_weight_and_overdraw():
+    probs = np.array([0.5, 0.0, 0.5])
+    for seed in range(20):
+        assert 1 not in q.draw_indices(probs, 2, seed)
+    with pytest.raises(q.SamplingError):
+        q.draw_indices(probs, 3, 0)
+
+
+@pytest.mark.parametrize(
+    "m,n,k,strategy,seed,counts",
+    [
+        (10, 8, 3, "length", 41, None),
+        (15, 11, 4, "length", 123, None),
+        (12, 9, 2, "length", 7, (4, 3)),
+        (200, 150, 10, "uniform", 3, (40, 30)),
+        (300, 260, 12, "length", 11, (48, 36)),
+    ],
+)
+def test_qmcur_matches_oracle(m, n, k, strategy, seed, counts):
+    x = lowrank(m, n, k, seed, noise=1e-3)
+    kw = {} if counts is None else dict(num_rows=counts[0], num_cols=counts[1])
+    plan = q.make_plan(x, strategy, k, seed, **kw)
+    f = q.qmcur(x, plan)
+    check_against_oracle(x, plan, f)
+
+
+def test_qmcur_cfg1_size():
+    # BASELINE cfg1 shape (1000 x 1000, rank 10, c = r = 40, uniform, seed 0), host-generated
+    x = lowrank(1000, 1000, 10, seed=2024, noise=1e-3)
+    plan = q.make_plan(x, "uniform", 10, 0, num_rows=40, num_cols=40)
+    f = q.qmcur(x, plan)
+    check_against_oracle(x, plan, f)
+
+
+def test_rank_deficient_robust_path():
+    # rank-5 100x100 with c = r = 9 (test_cur.py:208-219): C, R lose rank -> Householder + Jacobi
+    x = lowrank(100, 100, 5, seed=31)
+    for strategy in ("length", "uniform"):
+        plan = q.make_plan(x, strategy, 5, 31)
+        f = q.qmcur(x, plan)
+        assert f.c.shape == (100, 9) and f.r.shape == (9, 100)
+        assert rel_fro_err(q.cur_reconstruct(f), x) <= 1e-8
+
+
+def test_scalar_pipeline():
+    x = q.QMatrix(np.array([[0.0]]), np.array([[2.0]]), np.array([[0.0]]), np.array([[0.0]]))
+    f = q.qmcur(x, q.make_plan(x, "length", 1, seed=0))
+    assert abs(f.u[0, 0] - q.Quaternion(0.0, -0.5, 0.0, 0.0)) < 1e-12
+    assert abs(q.cur_reconstruct(f)[0, 0] - q.Quaternion(0.0, 2.0, 0.0, 0.0)) < 1e-12
+
+
+def test_determinism_bitwise():
+    x = rand_mat(150, 110, seed=45)
+    plan = q.make_plan(x, "length", 4, seed=123, num_rows=30, num_cols=25)
+    f1 = q.qmcur(x, plan)
+    f2 = q.qmcur(x, plan)
+    assert np.array_equal(f1.col_indices, f2.col_indices)
+    assert all(np.array_equal(a, b) for a, b in zip(f1.u.planes, f2.u.planes))
+    assert q.cur_relative_error(x, f1) == q.cur_relative_error(x, f2)
+
+
+def test_plan_matrix_mismatch():
+    x = rand_mat(6, 6, seed=46)
+    plan = q.make_plan(x, "length", 2, seed=0)
+    with pytest.raises(q.ShapeError):
+        q.qmcur(rand_mat(7, 7, seed=47), plan)
+
+
+@pytest.mark.parametrize("m,n", [(10, 8), (8, 10), (64, 40), (1, 5), (300, 120)])
+def test_pseudoinverse_matches_oracle(m, n):
+    a = rand_mat(m, n, seed=m + 100 * n)
+    got = q.pseudoinverse(a)
+    want = O.pinv(tuple(a.planes))
+    assert O.rel_fro(tuple(got.planes), want) <= 1e-10
+
+
+def test_pseudoinverse_forced_robust_matches():
+    a = rand_mat(60, 20, seed=9)
+    dev = _native.device()
+    dev.lib.qcur_force_robust(dev.handle, 1)
+    try:
+        got = q.pseudoinverse(a)
+    finally:
+        dev.lib.qcur_force_robust(dev.handle, 0)
+    assert O.rel_fro(tuple(got.planes), O.pinv(tuple(a.planes))) <= 1e-10
+
+
+def test_qmat_matmul_matches_oracle():
+    a = rand_mat(33, 17, seed=1)
+    b = rand_mat(17, 45, seed=2)
+    got = a @ b
+    want = O.qmatmul(tuple(a.planes), tuple(b.planes))
+    assert O.rel_fro(tuple(got.planes), want) <= 1e-14
