@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""QMCUR benchmark (BASELINE.json metric: QMCUR approx/sec at m=n=4000).
+
+One *step* = one complete approximation of the BASELINE cfg2 workload on a
+device-resident matrix: length-squared distributions (numpy-bit-exact), the
+index draw, C/R gathers, pinv(C), pinv(R), U = pinv(C) X pinv(R) and the fused
+relative error ||X - CUR||_F / ||X||_F.  The input (512 MB) is larger than L2,
+so no flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+
+N > 1 is launched by torchrun, one rank per GPU: cfg1-cfg3 do not shard one
+matrix profitably, so ranks run independent replicas (weak
+scaling, no data-path collective); timing is the max over ranks.
+
+Rank 0 prints ONE JSON line.  Extra keys: roofline (dominant kernel, live CUDA
+events), phases (per-phase ms), step_roofline, cpu_baseline (the oracle port
+timed on this host), e2e (public API with pinned host buffers, H2D/D2H inside
+the timed region), clocks (NVML sampled during the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "QMCUR approx/sec at m=n=4000; achieved HBM GB/s and FP64 TFLOP/s vs B200 peak"
+
+CONFIGS = {
+    # BASELINE.json configs[0]: 1000x1000, rank 10, N(0, 1e-6) noise (std 1e-3), uniform, c=r=40, seed 0
+    "cfg1": dict(m=1000, n=1000, rank=10, noise=1e-3, relative=False, strategy="uniform", c=40, r=40,
+                 plan_seed=0, gen_seed=20240229, batch=1),
+    # configs[1]: 4000x4000, rank 50, noise 1e-3 relative to ||S||_F, length, c=r=200, seed 1  (the headline)
+    "cfg2": dict(m=4000, n=4000, rank=50, noise=1e-3, relative=True, strategy="length", c=200, r=200,
+                 plan_seed=1, gen_seed=20240229, batch=1),
+    # configs[3]: batch of 64 1024x1024, rank 20, 1e-4 relative noise, uniform, c=r=80, per-matrix seed b
+    "cfg4": dict(m=1024, n=1024, rank=20, noise=1e-4, relative=True, strategy="uniform", c=80, r=80,
+                 plan_seed=0, gen_seed=20240301, batch=64),
+}
+
+
+def workload_name(cfg_name: str, cfg: dict) -> str:
+    b = f"{cfg['batch']} x " if cfg["batch"] > 1 else ""
+    return (f"{cfg_name}: {b}{cfg['m']}x{cfg['n']} fp64 quaternion, rank {cfg['rank']} Gaussian factors + "
+            f"{'relative ' if cfg['relative'] else ''}noise {cfg['noise']:g}, {cfg['strategy']} sampling, "
+            f"c=r={cfg['c']}, plan seed {cfg['plan_seed']}")
+
+
+def alg_counts(cfg: dict) -> dict:
+    """Algorithmic work per approximation."""
+    m, n, c, r = cfg["m"], cfg["n"], cfg["c"], cfg["r"]
+    length = 1 if cfg["strategy"] == "length" else 0
+    return dict(
+        flop=32.0 * (c * m * n + c * n * r + m * c * r + m * r * n),
+        bytes=32.0 * m * n * (2 + length) + 64.0 * (m * c + r * n),
+        gemm_xq_flop=32.0 * m * n * r,
+        error_flop=32.0 * m * r * n,
+        length_bytes=32.0 * m * n,
+        gather_bytes=64.0 * (m * c + r * n),
+    )
+
+
+def load_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
+# ---------------------------------------------------------------------------
+# clocks (NVML) sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        0x4: "sw_power_cap",
+        0x8: "hw_slowdown",
+        0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown",
+    }
+
+    def __init__(self, index: int):
+        self.ok = False
+        self.samples = []
+        self.reasons = set()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for b, name in self.REASONS.items():
+                    if bits & b:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+def cpu_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+
+        n = [i.get("num_threads", 0) for i in threadpool_info() if i.get("internal_api") in ("openblas", "mkl")]
+        if n:
+            return int(max(n))
+    except Exception:
+        pass
+    return len(os.sched_getaffinity(0))
+
+
+def host_lowrank(cfg: dict, seed: int):
+    """Same shapes / distributions as the device generator, numpy on the host
+    (reference arm: no code of ours on its path)."""
+    import oracle as O
+
+    m, n, k = cfg["m"], cfg["n"], cfg["rank"]
+    g = np.random.default_rng(seed)
+    p = O.random_planes(g, m, k)
+    q = O.random_planes(g, n, k)
+    s = O.qmatmul(p, O.conj_t(q))
+    if cfg["relative"]:
+        sigma = cfg["noise"] * math.sqrt(O.frob2(s) / (4.0 * m * n))
+    else:
+        sigma = cfg["noise"]
+    return tuple(x + sigma * g.standard_normal(x.shape) for x in s)
+
+
+def run_reference(args, cfg_name: str, cfg: dict) -> None:
+    """--impl reference: the reference's CPU algorithm (oracle port) on this host."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+
+    planes = host_lowrank(cfg, cfg["gen_seed"])
+    cores = cpu_threads()
+    budget_s = float(os.environ.get("QCUR_REF_BUDGET_S", "150"))
+
+    def step(b: int):
+        O.approx(planes, cfg["strategy"], cfg["rank"], cfg["plan_seed"] + b, cfg["c"], cfg["r"])
+
+    for _ in range(min(args.warmup, 1)):
+        step(0)
+    times = []
+    t_all = time.perf_counter()
+    for s in range(args.steps):
+        t0 = time.perf_counter()
+        for b in range(cfg["batch"]):
+            step(b)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_all > budget_s:
+            break
+    elapsed = sum(times)
+    value = len(times) * cfg["batch"] / elapsed
+    ms = 1e3 * elapsed / len(times)
+    sample = (f"{len(times)} of {args.steps} requested steps timed (budget {budget_s:.0f}s), each step = "
+              f"{cfg['batch']} full approximation(s) of {cfg_name} (make_plan + qmcur + relative error)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "approx/s", "n_gpus": args.gpus,
+        "steps": len(times), "warmup": min(args.warmup, 1), "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (numpy host generator)",
+        "config": {"workload": workload_name(cfg_name, cfg)},
+        "cpu_baseline": {"value": value, "unit": "approx/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "approx/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, args.config, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+
+    from paper_2402_19147_b200 import _native
+    from paper_2402_19147_b200.cur import DeviceApprox, cur_relative_error, make_plan, qmcur
+    from paper_2402_19147_b200.quat import QMatrix, drop_device_copy
+
+    dev = _native.device(local)
+    m, n, c, r, batch = cfg["m"], cfg["n"], cfg["c"], cfg["r"], cfg["batch"]
+    # --- inputs on the device (Philox + DMMA GEMM, deterministic) ---
+    xs = []
+    for b in range(batch):
+        x = dev.empty_q(m, n)
+        dev.call("qcur_synth_lowrank", m, n, cfg["rank"], cfg["gen_seed"] + 1000 * b + 7919 * rank, cfg["noise"],
+                 1 if cfg["relative"] else 0, x.data_ptr())
+        xs.append(x)
+    outs = DeviceApprox(m, n, c, r, dev)
+
+    def step():
+        for b in range(batch):
+            outs.run(xs[b], cfg["strategy"], cfg["plan_seed"] + b)
+
+    stream = torch.cuda.current_stream()
+    for _ in range(max(args.warmup, 3)):
+        step()
+    outs.check()
+    torch.cuda.synchronize()
+
+    # --- timed region: device-resident value ---
+    sampler = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = dev.launches()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with sampler:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = dev.launches() - l0
+    if world > 1:
+        dist.barrier()
+    outs.check()
+    ms_total = e0.elapsed_time(e1)
+    t = torch.tensor([ms_total], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    value = world * args.steps * batch / (ms_total / 1e3)
+    rel_err = outs.rel_error()
+
+    # --- phase breakdown (events between phases, same stream), separate pass ---
+    dev.profile(True)
+    nprof = min(args.steps, 10)
+    for _ in range(nprof):
+        step()
+    phases = dev.profile_read()
+    dev.profile(False)
+    per_approx = {k: v[0] / max(v[1], 1) for k, v in phases.items()}
+    counts = alg_counts(cfg)
+    peak_tf = dev.lib.qcur_fp64_peak_tflops(dev.handle)
+    peaks = load_peaks()
+    hbm_peak = peaks.get("hbm_gbs")
+    dom = max(("gemm_xq", "error"), key=lambda k: per_approx.get(k, 0.0))
+    dom_ms = per_approx.get(dom, float("nan"))
+    dom_flop = counts["gemm_xq_flop"] if dom == "gemm_xq" else counts["error_flop"]
+    achieved = dom_flop / (dom_ms * 1e-3) / 1e12
+    roofline = {
+        "kernel": "qgemm_kernel<EPI_ERR> (fused C U R + error)" if dom == "error" else "qgemm_kernel (Y = X Q_R)",
+        "bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+        "frac": achieved / peak_tf if peak_tf else None, "traffic": None,
+        "peak_source": "FP64 DMMA (mma.sync m8n8k4 f64) peak measured live on this GPU by qcur_fp64_peak_tflops; "
+                       "MEASURED_PEAKS.json has no FP64 figure",
+        "algorithmic_flop_per_launch": dom_flop, "avg_launch_ms": dom_ms,
+    }
+    t_roof = max(counts["flop"] / (peak_tf * 1e12), counts["bytes"] / ((hbm_peak or 6544.3) * 1e9))
+    step_roof = {"flop": counts["flop"], "bytes": counts["bytes"], "t_roofline_ms": t_roof * 1e3,
+                 "frac": (t_roof * 1e3) / (ms_step / batch)}
+    extra_phase = {}
+    if "length" in per_approx:
+        extra_phase["length_GBps"] = counts["length_bytes"] / (per_approx["length"] * 1e-3) / 1e9
+        extra_phase["length_frac_hbm"] = extra_phase["length_GBps"] / (hbm_peak or 6544.3)
+    if "gather" in per_approx:
+        extra_phase["gather_GBps"] = counts["gather_bytes"] / (per_approx["gather"] * 1e-3) / 1e9
+    extra_phase["gemm_xq_TFps"] = counts["gemm_xq_flop"] / (per_approx.get("gemm_xq", float("nan")) * 1e-3) / 1e12
+    extra_phase["error_TFps"] = counts["error_flop"] / (per_approx.get("error", float("nan")) * 1e-3) / 1e12
+
+    # --- e2e through the public API with pinned host buffers ---
+    e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
+    pinned = [torch.empty((m, n), dtype=torch.float64, pin_memory=True) for _ in range(4)]
+    host_planes = [p.numpy() for p in pinned]
+    dev.download_planes(xs[0], m, n, pinned_out=host_planes)
+    xh = QMatrix._wrap(*host_planes)
+
+    def e2e_step():
+        drop_device_copy(xh)
+        plan = make_plan(xh, cfg["strategy"], cfg["rank"], cfg["plan_seed"], num_rows=r, num_cols=c)
+        f = qmcur(xh, plan)
+        return cur_relative_error(xh, f)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_err = e2e_step()
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    tt = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    e2e_s = float(tt.item())
+    e2e = {
+        "value": world * e2e_steps / e2e_s,
+        "unit": "approx/s",
+        "h2d_bytes_per_step": 32 * m * n + 8 * (m + n),
+        "d2h_bytes_per_step": 8 * (m + n) + 32 * (m * c + c * r + r * n) + 8 * (c + r) + 16,
+        "api": "make_plan + qmcur + cur_relative_error on a QMatrix with pinned host planes (device cache dropped "
+               "every step)",
+        "steps": e2e_steps,
+        "rel_err": e2e_err,
+    }
+
+    # --- CPU baseline: the oracle port on this host (rank 0, N = 1) ---
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+
+        planes = tuple(np.array(p) for p in host_planes)
+        t0 = time.perf_counter()
+        res = O.approx(planes, cfg["strategy"], cfg["rank"], cfg["plan_seed"], c, r)
+        cpu_s = time.perf_counter() - t0
+        cpu = {"value": 1.0 / cpu_s, "unit": "approx/s", "cores": cpu_threads(), "kind": "port",
+               "sample": f"1 full approximation of {args.config} (make_plan + qmcur + relative error) "
+                         f"by oracle/oracle.py on the same input",
+               "rel_err": res["rel_err"], "agrees_with_gpu_rel": abs(res["rel_err"] - rel_err) / res["rel_err"]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "approx/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: on-device Philox Gaussian quaternion factors, S = P Q^H on DMMA, Gaussian noise",
+            "config": {"workload": workload_name(args.config, cfg), "m": m, "n": n, "c": c, "r": r,
+                       "strategy": cfg["strategy"], "batch": batch,
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (512 MB per matrix); no flush" if m * n * 32 > 126e6
+                       else "input fits in L2; repeated on the same resident matrix"},
+            "gpu_launches": launches, "rel_err": rel_err,
+            "roofline": roofline, "step_roofline": step_roof,
+            "phases_ms_per_approx": per_approx, "phase_rates": extra_phase,
+            "clocks": sampler.summary(), "e2e": e2e, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

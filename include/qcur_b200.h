@@ -121,6 +121,16 @@ int qcur_synth_lowrank(qcur_ctx* ctx, int64_t m, int64_t n, int64_t k, uint64_t 
                        int noise_relative, double* x_dev);
 double qcur_fp64_peak_tflops(qcur_ctx* ctx);
 
+/* ---- measurement hooks (bench.py) ------------------------------------------
+ * qcur_profile(ctx, 1) records CUDA events on the context stream at the end of
+ * every pipeline phase (length, draw, gather, factor_c, factor_r, gemm_xq,
+ * core_u, cu, error); qcur_profile_read synchronises and writes
+ * "phase:total_ms:count;..." into buf.  qcur_launch_count is the number of
+ * kernels this library has launched in the process. */
+int qcur_profile(qcur_ctx* ctx, int on);
+int qcur_profile_read(qcur_ctx* ctx, char* buf, size_t len);
+unsigned long long qcur_launch_count(void);
+
 #ifdef __cplusplus
 }
 #endif

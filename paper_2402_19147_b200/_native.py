@@ -43,6 +43,7 @@ EXPORTS = (
     "qcur_length_distributions", "qcur_uniform_distributions", "qcur_draw_indices", "qcur_qmcur",
     "qcur_cur_error", "qcur_approx", "qcur_check", "qcur_qgemm", "qcur_pseudoinverse",
     "qcur_frobenius_sq", "qcur_synth_lowrank", "qcur_fp64_peak_tflops",
+    "qcur_profile", "qcur_profile_read", "qcur_launch_count",
 )
 
 _c_dp = ctypes.c_void_p
@@ -100,6 +101,9 @@ def load_library() -> ctypes.CDLL:
             "qcur_synth_lowrank": (ctypes.c_int, [_c_dp, _i64, _i64, _i64, ctypes.c_uint64, ctypes.c_double,
                                                   ctypes.c_int, _c_dp]),
             "qcur_fp64_peak_tflops": (ctypes.c_double, [_c_dp]),
+            "qcur_profile": (ctypes.c_int, [_c_dp, ctypes.c_int]),
+            "qcur_profile_read": (ctypes.c_int, [_c_dp, ctypes.c_char_p, ctypes.c_size_t]),
+            "qcur_launch_count": (ctypes.c_ulonglong, []),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -206,6 +210,23 @@ class Device:
 
     def info(self) -> int:
         return int(self.lib.qcur_last_info(self.handle))
+
+    def profile(self, on: bool) -> None:
+        self.call("qcur_profile", 1 if on else 0)
+
+    def profile_read(self) -> dict[str, tuple[float, int]]:
+        """{phase: (total_ms, count)} accumulated since profile(True)."""
+        buf = ctypes.create_string_buffer(8192)
+        self.call("qcur_profile_read", buf, len(buf))
+        out = {}
+        for item in buf.value.decode().split(";"):
+            if item:
+                name, ms, cnt = item.split(":")
+                out[name] = (float(ms), int(cnt))
+        return out
+
+    def launches(self) -> int:
+        return int(self.lib.qcur_launch_count())
 
     def empty_q(self, m: int, n: int):
         """Uninitialised interleaved quaternion matrix (m, n, 4) float64 on the device."""

@@ -94,3 +94,8 @@ enum StatusBits : unsigned {
 };
 
 }  // namespace qcur
+
+namespace qcur {
+// number of kernels this library has launched (bench.py reports it as gpu_launches)
+extern unsigned long long g_launches;
+}  // namespace qcur

@@ -102,26 +102,32 @@ __global__ void k_reduce_pairs(const double* __restrict__ parts, int64_t nparts,
 
 void launch_planar_to_interleaved(const double* a0, const double* a1, const double* a2, const double* a3, int64_t m,
                                   int64_t n, double* X, cudaStream_t st) {
+  ++::qcur::g_launches;
   k0_planar_to_interleaved<<<grid_for(m * n, 256), 256, 0, st>>>(a0, a1, a2, a3, m * n, X);
 }
 void launch_interleaved_to_planar(const double* X, int64_t m, int64_t n, int64_t ldx, double* a0, double* a1,
                                   double* a2, double* a3, cudaStream_t st) {
+  ++::qcur::g_launches;
   k0_interleaved_to_planar<<<grid_for(m * n, 256), 256, 0, st>>>(X, m, n, ldx, a0, a1, a2, a3);
 }
 void launch_gather_cols(const double* X, int64_t m, int64_t ldx, const int64_t* J, int64_t c, double* C,
                         cudaStream_t st) {
+  ++::qcur::g_launches;
   k3_gather_cols<<<grid_for(m * c, 256), 256, 0, st>>>(X, m, ldx, J, c, C);
 }
 void launch_gather_rows(const double* X, int64_t n, int64_t ldx, const int64_t* I, int64_t r, double* R,
                         cudaStream_t st) {
+  ++::qcur::g_launches;
   k3_gather_rows<<<grid_for(r * n, 256), 256, 0, st>>>(X, n, ldx, I, r, R);
 }
 void launch_conj_transpose(const double* A, int64_t m, int64_t n, int64_t lda, double* AH, int64_t ldah,
                            cudaStream_t st) {
   dim3 grid((unsigned)((n + 31) / 32), (unsigned)((m + 31) / 32));
+  ++::qcur::g_launches;
   k_conj_transpose<<<grid, dim3(32, 8), 0, st>>>(A, m, n, lda, AH, ldah);
 }
 void launch_reduce_pairs(const double* parts, int64_t nparts, double* out2, cudaStream_t st) {
+  ++::qcur::g_launches;
   k_reduce_pairs<<<1, 1024, 0, st>>>(parts, nparts, out2);
 }
 

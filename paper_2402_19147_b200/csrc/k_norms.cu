@@ -183,6 +183,7 @@ __global__ void k_fill(double* __restrict__ out, int64_t len, double v) {
 void launch_colstrip(const double* X, int64_t m, int64_t n, int64_t ldx, double* sq, double* colsum,
                      cudaStream_t st) {
   dim3 grid((unsigned)((n + kStripW - 1) / kStripW));
+  ++::qcur::g_launches;
   k1_colstrip<<<grid, kStripThreads, 0, st>>>(X, m, n, ldx, sq, colsum);
 }
 
@@ -199,12 +200,15 @@ void launch_pairwise(const double* data, int64_t nseg, int64_t seg_stride, const
   if (pw.nnodes == 0) {
     // single chunk per segment: write straight to out
     dim3 grid(1, (unsigned)nseg);
+    ++::qcur::g_launches;
     pairwise_chunks<<<grid, kChunkThreads, need, st>>>(data, seg_stride, pw, out, 1);
     return;
   }
   const int64_t w = (int64_t)pw.nchunks + pw.nnodes;
   dim3 grid((unsigned)pw.nchunks, (unsigned)nseg);
+  ++::qcur::g_launches;
   pairwise_chunks<<<grid, kChunkThreads, need, st>>>(data, seg_stride, pw, scratch, w);
+  ++::qcur::g_launches;
   pairwise_top<<<(unsigned)nseg, 256, 0, st>>>(scratch, pw, out);
 }
 
@@ -213,6 +217,7 @@ void launch_scale(const double* in, int64_t len, const double* denom, double* ou
   int blocks = (int)((len + 255) / 256);
   if (blocks > 1184) blocks = 1184;
   if (blocks < 1) blocks = 1;
+  ++::qcur::g_launches;
   k1_scale<<<blocks, 256, 0, st>>>(in, len, denom, out, status, check_bit);
 }
 
@@ -220,6 +225,7 @@ void launch_fill(double* out, int64_t len, double v, cudaStream_t st) {
   int blocks = (int)((len + 255) / 256);
   if (blocks > 1184) blocks = 1184;
   if (blocks < 1) blocks = 1;
+  ++::qcur::g_launches;
   k_fill<<<blocks, 256, 0, st>>>(out, len, v);
 }
 

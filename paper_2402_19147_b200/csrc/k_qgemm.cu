@@ -287,6 +287,7 @@ void launch_cfg(const KParams& kp, dim3 grid, cudaStream_t st) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM);
     set = true;
   }
+  ++::qcur::g_launches;
   kern<<<grid, CF::THREADS, CF::SMEM, st>>>(kp);
 }
 
@@ -339,6 +340,7 @@ void launch_qgemm(const GemmArgs& g, double* workspace, cudaStream_t st) {
     const int64_t total = g.Mq * 4 * g.Nq;
     int blocks = (int)((total + 255) / 256);
     if (blocks > 148 * 8) blocks = 148 * 8;
+    ++::qcur::g_launches;
     splitk_reduce<<<blocks, 256, 0, st>>>(workspace, spz, g.Mq, 4 * g.Nq, g.C, g.ldc, g.alpha, g.beta);
   }
 }

@@ -86,13 +86,16 @@ __global__ void k_sumsq_parts(const double* __restrict__ X, int64_t count, doubl
 }
 
 void launch_normal_fill(double* out, int64_t count, uint64_t seed, uint64_t stream, double scale, cudaStream_t st) {
+  ++::qcur::g_launches;
   k_normal_fill<<<148 * 8, 256, 0, st>>>(out, count, seed, stream, scale);
 }
 void launch_add_scaled_noise(double* X, int64_t count, uint64_t seed, uint64_t stream, const double* ssq, double rel,
                              cudaStream_t st) {
+  ++::qcur::g_launches;
   k_add_noise<<<148 * 8, 256, 0, st>>>(X, count, seed, stream, ssq, rel);
 }
 void launch_sumsq(const double* X, int64_t count, double* partials, int64_t nparts, double* out, cudaStream_t st) {
+  ++::qcur::g_launches;
   k_sumsq_parts<<<(unsigned)nparts, 256, 0, st>>>(X, count, partials);
   launch_reduce_pairs(partials, nparts, out, st);
 }
@@ -128,10 +131,12 @@ double run_dmma_peak(int sms, cudaStream_t st) {
   cudaEventCreate(&e1);
   const int threads = 256, blocks = sms * 2;
   int iters = 200;
+  ++::qcur::g_launches;
   k_dmma_probe<<<blocks, threads, 0, st>>>(out, 20);
   float ms = 0.f;
   for (int rep = 0; rep < 3; ++rep) {
     cudaEventRecord(e0, st);
+    ++::qcur::g_launches;
     k_dmma_probe<<<blocks, threads, 0, st>>>(out, iters);
     cudaEventRecord(e1, st);
     cudaEventSynchronize(e1);

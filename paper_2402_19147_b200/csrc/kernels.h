@@ -81,8 +81,23 @@ void launch_cholesky(double* G, int64_t q, int64_t ldg, unsigned* status, unsign
 void launch_tri_inverse_lower(const double* L, int64_t q, int64_t ldl, double* Linv, int64_t ldi, cudaStream_t st);
 void launch_set_identity(double* A, int64_t q, int64_t lda, cudaStream_t st);
 void launch_set_status(unsigned* status, unsigned bits, cudaStream_t st);
-void launch_kappa_check(const double* T, const double* Tinv, int64_t q, double limit, unsigned* status,
+void launch_kappa_check(const double* G1, const double* Tinv, int64_t q, double limit, unsigned* status,
                         unsigned fail_bit, cudaStream_t st);
+
+// k_chol_cluster.cu : Cholesky + inverse of up to two q x q Grams on 16-CTA clusters
+struct CholJob {
+  const double* G;  // q x q Hermitian (lower read)
+  double* L;        // out: Cholesky factor (upper zeroed)
+  double* X;        // out: L^{-1} (upper zeroed)
+  unsigned fail_bit;
+};
+int chol_cluster_qmax();
+// second CholeskyQR pass by series (k_dense.cu): M = lh(G2 - I - P) (P may be null; then also
+// checks max|G2 - I| <= thresh), L2inv = I - M1 + P2
+void launch_series_lh(const double* G2, const double* P, int64_t q, double* M, unsigned* status, unsigned fail_bit,
+                      double thresh, cudaStream_t st);
+void launch_series_final(const double* M1, const double* P2, int64_t q, double* L2inv, cudaStream_t st);
+void launch_chol_inv_cluster(const CholJob* jobs, int njobs, int64_t q, unsigned* status, cudaStream_t st);
 // robust path (runs only when `status & gate_bit`, otherwise returns immediately)
 void launch_householder_qr(double* Zcm, int64_t p, int64_t q, double* alpha, double* Qcm, double* T, int64_t ldt,
                            const unsigned* status, unsigned gate_bit, cudaStream_t st);

@@ -16,9 +16,30 @@
 
 using namespace qcur;
 
+unsigned long long qcur::g_launches = 0;
+
 namespace {
 
 constexpr double kEps = 2.220446049250313e-16;
+
+// Optional phase timing: CUDA events recorded on the launching stream between
+// pipeline phases; harvested (after a sync) by qcur_profile_read.
+struct Profiler {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  std::vector<std::pair<std::string, cudaEvent_t>> marks;  // phase name ends at this event
+  cudaEvent_t start = nullptr;
+  std::map<std::string, std::pair<double, long>> acc;       // name -> (total ms, count)
+  cudaEvent_t next() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+};
 
 struct DevProgram {
   DevPairwise d{};
@@ -52,6 +73,40 @@ struct qcur_ctx {
   Arena arena;
   std::map<int64_t, DevProgram> programs;
   std::string err;
+  Profiler prof;
+
+  // mark the end of a named phase (no-op unless profiling)
+  void mark(const char* name) {
+    if (!prof.on) return;
+    if (!prof.start) {
+      prof.start = prof.next();
+      cudaEventRecord(prof.start, stream);
+    }
+    cudaEvent_t e = prof.next();
+    cudaEventRecord(e, stream);
+    prof.marks.emplace_back(name, e);
+  }
+  void mark_begin() {
+    if (!prof.on) return;
+    if (!prof.start) {
+      prof.start = prof.next();
+      cudaEventRecord(prof.start, stream);
+    }
+  }
+  void harvest() {
+    cudaEvent_t prev = prof.start;
+    for (auto& mk : prof.marks) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, prev, mk.second);
+      auto& a = prof.acc[mk.first];
+      a.first += ms;
+      a.second += 1;
+      prev = mk.second;
+    }
+    prof.marks.clear();
+    prof.start = nullptr;
+    prof.used = 0;
+  }
 
   int fail(int code, const char* fmt, ...) {
     char buf[512];
@@ -195,6 +250,7 @@ int length_distributions_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t
   launch_scale(col, n, scal + 1, col, ctx->status_dev, 0, st);
   launch_scale(row, m, scal + 2, row, ctx->status_dev, 0, st);
   CK_LAUNCH(ctx, "length scale");
+  ctx->mark("length");
   return QCUR_OK;
 }
 
@@ -211,7 +267,7 @@ struct FactorOut {
 size_t factor_ws_bytes(int64_t p, int64_t q) {
   size_t b = 0;
   b += qbytes(p, q) * 3;        // Q1, Zcm, Qcm
-  b += qbytes(q, q) * 10;       // G1, L1inv, G2, L2inv, T, Tcm, Vcm, ...
+  b += qbytes(q, q) * 12;       // G1, L1, L1inv, G2, L2, L2inv, T, Tcm, Vcm, ...
   b += (size_t)(q + 8) * 8 * 4;  // betas, sigma
   GemmArgs g{};
   g.Mq = p;
@@ -251,67 +307,157 @@ GemmArgs gargs(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, in
   return g;
 }
 
-int factor_tall(qcur_ctx* ctx, const double* src, int zh, int64_t p, int64_t q, unsigned fail_bit, double cutoff_abs,
-                FactorOut out) {
+struct FactorSpec {
+  const double* src;  // Z = src (zh = 0, p x q) or Z = src^H (zh = 1, src is q x p)
+  int zh;
+  int64_t p, q;
+  unsigned fail_bit;
+  double cutoff_abs;  // >= 0: explicit pinv tolerance (forces the robust path)
+  FactorOut out;
+};
+
+// Factor up to two tall blocks together (C and R^H of one QMCUR step) so the
+// latency-bound small kernels (cluster Cholesky) serve both in one launch.
+int factor_multi(qcur_ctx* ctx, const FactorSpec* specs, int ns) {
   cudaStream_t st = ctx->stream;
   unsigned* status = ctx->status_dev;
-  double* G1 = ctx->take<double>((size_t)(q * q * 4));
-  double* L1i = ctx->take<double>((size_t)(q * q * 4));
-  double* Q1 = ctx->take<double>((size_t)(p * q * 4));
-  double* G2 = ctx->take<double>((size_t)(q * q * 4));
-  double* L2i = ctx->take<double>((size_t)(q * q * 4));
-  double* T = ctx->take<double>((size_t)(q * q * 4));
-  double* betas = ctx->take<double>((size_t)q + 8);
-  double* Zcm = ctx->take<double>((size_t)(p * q * 4));
-  double* Qcm = ctx->take<double>((size_t)(p * q * 4));
-  double* Tcm = ctx->take<double>((size_t)(q * q * 4));
-  double* Vcm = ctx->take<double>((size_t)(q * q * 4 + q + 8));
-  GemmArgs probe = gargs(p, q, q, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0);
-  GemmArgs probe2 = gargs(q, q, p, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0);
-  size_t wsb = qgemm_workspace_bytes(probe);
-  size_t wsb2 = qgemm_workspace_bytes(probe2);
-  double* gws = ctx->take<double>((wsb > wsb2 ? wsb : wsb2) / 8 + 16);
-  if (!G1 || !L1i || !Q1 || !G2 || !L2i || !T || !betas || !Zcm || !Qcm || !Tcm || !Vcm || !gws)
-    return ctx->fail(QCUR_E_CUDA, "workspace exhausted (factor)");
+  struct Bufs {
+    double *G1, *L1, *L1i, *Q1, *G2, *L2, *L2i, *T, *betas, *Zcm, *Qcm, *Tcm, *Vcm, *gws;
+  } B[2];
+  for (int k = 0; k < ns; ++k) {
+    const int64_t p = specs[k].p, q = specs[k].q;
+    Bufs& b = B[k];
+    b.G1 = ctx->take<double>((size_t)(q * q * 4));
+    b.L1 = ctx->take<double>((size_t)(q * q * 4));
+    b.L1i = ctx->take<double>((size_t)(q * q * 4));
+    b.Q1 = ctx->take<double>((size_t)(p * q * 4));
+    b.G2 = ctx->take<double>((size_t)(q * q * 4));
+    b.L2 = ctx->take<double>((size_t)(q * q * 4));
+    b.L2i = ctx->take<double>((size_t)(q * q * 4));
+    b.T = ctx->take<double>((size_t)(q * q * 4));
+    b.betas = ctx->take<double>((size_t)q + 8);
+    b.Zcm = ctx->take<double>((size_t)(p * q * 4));
+    b.Qcm = ctx->take<double>((size_t)(p * q * 4));
+    b.Tcm = ctx->take<double>((size_t)(q * q * 4));
+    b.Vcm = ctx->take<double>((size_t)(q * q * 4 + q + 8));
+    GemmArgs probe = gargs(p, q, q, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0);
+    GemmArgs probe2 = gargs(q, q, p, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0);
+    size_t w1 = qgemm_workspace_bytes(probe), w2 = qgemm_workspace_bytes(probe2);
+    b.gws = ctx->take<double>((w1 > w2 ? w1 : w2) / 8 + 16);
+    if (!b.G1 || !b.L1 || !b.L1i || !b.Q1 || !b.G2 || !b.L2 || !b.L2i || !b.T || !b.betas || !b.Zcm || !b.Qcm ||
+        !b.Tcm || !b.Vcm || !b.gws)
+      return ctx->fail(QCUR_E_CUDA, "workspace exhausted (factor)");
+  }
   int rc;
-  const bool robust_only = ctx->force_robust || cutoff_abs >= 0.0;
-  if (robust_only) {
-    launch_set_status(status, fail_bit, st);
+  bool fast[2] = {false, false};
+  for (int k = 0; k < ns; ++k) fast[k] = !(ctx->force_robust || specs[k].cutoff_abs >= 0.0);
+  // Cholesky + inverse of each Gram: one cluster launch when both fit, else per problem
+  auto chol_inv = [&](bool second) -> int {  // (second pass uses the series below)
+    CholJob jobs[2];
+    int nj = 0;
+    int64_t qj = -1;
+    bool together = true;
+    for (int k = 0; k < ns; ++k) {
+      if (!fast[k]) continue;
+      Bufs& b = B[k];
+      jobs[nj++] = CholJob{second ? b.G2 : b.G1, second ? b.L2 : b.L1, second ? b.L2i : b.L1i, specs[k].fail_bit};
+      if (qj >= 0 && qj != specs[k].q) together = false;
+      qj = specs[k].q;
+    }
+    if (nj == 0) return QCUR_OK;
+    if (together && qj <= chol_cluster_qmax()) {
+      launch_chol_inv_cluster(jobs, nj, qj, status, st);
+    } else {
+      for (int k = 0; k < ns; ++k) {
+        if (!fast[k]) continue;
+        Bufs& b = B[k];
+        const int64_t q = specs[k].q;
+        double* G = second ? b.G2 : b.G1;
+        double* L = second ? b.L2 : b.L1;
+        double* Li = second ? b.L2i : b.L1i;
+        if (q <= chol_cluster_qmax()) {
+          CholJob j1{G, L, Li, specs[k].fail_bit};
+          launch_chol_inv_cluster(&j1, 1, q, status, st);
+        } else {
+          cudaMemcpyAsync(L, G, (size_t)qbytes(q, q), cudaMemcpyDeviceToDevice, st);
+          launch_cholesky(L, q, q, status, specs[k].fail_bit, st);
+          launch_tri_inverse_lower(L, q, q, Li, q, st);
+        }
+      }
+    }
+    CK_LAUNCH(ctx, "cholesky");
+    return QCUR_OK;
+  };
+  for (int k = 0; k < ns; ++k) {
+    if (fast[k]) continue;
+    launch_set_status(status, specs[k].fail_bit, st);
     CK_LAUNCH(ctx, "force robust");
-  } else {
-    // G1 = Z^H Z
-    if (!zh) rc = gemm(ctx, gargs(q, q, p, src, q, 1, src, q, 0, G1, q), gws);
-    else rc = gemm(ctx, gargs(q, q, p, src, p, 0, src, p, 1, G1, q), gws);
+  }
+  // G1 = Z^H Z
+  for (int k = 0; k < ns; ++k) {
+    if (!fast[k]) continue;
+    const FactorSpec& f = specs[k];
+    const int64_t p = f.p, q = f.q;
+    if (!f.zh) rc = gemm(ctx, gargs(q, q, p, f.src, q, 1, f.src, q, 0, B[k].G1, q), B[k].gws);
+    else rc = gemm(ctx, gargs(q, q, p, f.src, p, 0, f.src, p, 1, B[k].G1, q), B[k].gws);
     if (rc) return rc;
-    launch_cholesky(G1, q, q, status, fail_bit, st);
-    launch_tri_inverse_lower(G1, q, q, L1i, q, st);
-    CK_LAUNCH(ctx, "chol1");
-    // Q1 = Z L1^{-H}
-    if (!zh) rc = gemm(ctx, gargs(p, q, q, src, q, 0, L1i, q, 1, Q1, q), gws);
-    else rc = gemm(ctx, gargs(p, q, q, src, p, 1, L1i, q, 1, Q1, q), gws);
+  }
+  if ((rc = chol_inv(false))) return rc;
+  // Q1 = Z L1^{-H};  G2 = Q1^H Q1
+  for (int k = 0; k < ns; ++k) {
+    if (!fast[k]) continue;
+    const FactorSpec& f = specs[k];
+    const int64_t p = f.p, q = f.q;
+    if (!f.zh) rc = gemm(ctx, gargs(p, q, q, f.src, q, 0, B[k].L1i, q, 1, B[k].Q1, q), B[k].gws);
+    else rc = gemm(ctx, gargs(p, q, q, f.src, p, 1, B[k].L1i, q, 1, B[k].Q1, q), B[k].gws);
     if (rc) return rc;
-    // G2 = Q1^H Q1
-    if ((rc = gemm(ctx, gargs(q, q, p, Q1, q, 1, Q1, q, 0, G2, q), gws))) return rc;
-    launch_cholesky(G2, q, q, status, fail_bit, st);
-    launch_tri_inverse_lower(G2, q, q, L2i, q, st);
-    CK_LAUNCH(ctx, "chol2");
-    // Q = Q1 L2^{-H};  F = T^{-1} = L1^{-H} L2^{-H};  T = L2^H L1^H
-    if ((rc = gemm(ctx, gargs(p, q, q, Q1, q, 0, L2i, q, 1, out.Q, q), gws))) return rc;
-    if ((rc = gemm(ctx, gargs(q, q, q, L1i, q, 1, L2i, q, 1, out.F, q), gws))) return rc;
-    if ((rc = gemm(ctx, gargs(q, q, q, G2, q, 1, G1, q, 1, T, q), gws))) return rc;
-    launch_kappa_check(T, out.F, q, ctx->kappa_limit, status, fail_bit, st);
+    if ((rc = gemm(ctx, gargs(q, q, p, B[k].Q1, q, 1, B[k].Q1, q, 0, B[k].G2, q), B[k].gws))) return rc;
+  }
+  // second pass: G2 = I + E with E ~ kappa^2 u; L2^{-1} by a second-order series
+  // (no sequential Cholesky; blocks with max|E| > 1e-5 take the robust path)
+  for (int k = 0; k < ns; ++k) {
+    if (!fast[k]) continue;
+    const int64_t q = specs[k].q;
+    Bufs& b = B[k];
+    double *M0 = b.L2, *P = b.T, *M1 = b.Tcm, *P2 = b.Vcm;
+    launch_series_lh(b.G2, nullptr, q, M0, status, specs[k].fail_bit, 1e-5, st);
+    if ((rc = gemm(ctx, gargs(q, q, q, M0, q, 0, M0, q, 1, P, q), b.gws))) return rc;
+    launch_series_lh(b.G2, P, q, M1, status, specs[k].fail_bit, 1e-5, st);
+    if ((rc = gemm(ctx, gargs(q, q, q, M1, q, 0, M1, q, 0, P2, q), b.gws))) return rc;
+    launch_series_final(M1, P2, q, b.L2i, st);
+    CK_LAUNCH(ctx, "series");
+  }
+  // Q = Q1 L2^{-H};  F = T^{-1} = L1^{-H} L2^{-H};  kappa_F(T) = ||C||_F ||F||_F = sqrt(tr G1) ||F||_F
+  for (int k = 0; k < ns; ++k) {
+    if (!fast[k]) continue;
+    const FactorSpec& f = specs[k];
+    const int64_t p = f.p, q = f.q;
+    if ((rc = gemm(ctx, gargs(p, q, q, B[k].Q1, q, 0, B[k].L2i, q, 1, f.out.Q, q), B[k].gws))) return rc;
+    if ((rc = gemm(ctx, gargs(q, q, q, B[k].L1i, q, 1, B[k].L2i, q, 1, f.out.F, q), B[k].gws))) return rc;
+    launch_kappa_check(B[k].G1, f.out.F, q, ctx->kappa_limit, status, f.fail_bit, st);
     CK_LAUNCH(ctx, "kappa");
   }
-  // robust path, gated on fail_bit
-  if (!zh) launch_rowmajor_to_colmajor(src, p, q, q, Zcm, status, fail_bit, st);
-  else launch_conj_copy(src, p * q, Zcm, status, fail_bit, st);
-  launch_householder_qr(Zcm, p, q, betas, Qcm, T, q, status, fail_bit, st);
-  launch_colmajor_to_rowmajor(Qcm, p, q, out.Q, q, status, fail_bit, 0, st);
-  launch_rowmajor_to_colmajor(T, q, q, q, Tcm, status, fail_bit, st);
-  launch_jacobi_pinv_factor(Tcm, Vcm, q, kEps * (double)(p > q ? p : q), cutoff_abs, out.F, q, status, fail_bit,
-                            st);
-  CK_LAUNCH(ctx, "robust factor");
+  // robust path, gated on each fail_bit (no-op launches when the fast path held)
+  for (int k = 0; k < ns; ++k) {
+    const FactorSpec& f = specs[k];
+    const int64_t p = f.p, q = f.q;
+    Bufs& b = B[k];
+    if (!f.zh) launch_rowmajor_to_colmajor(f.src, p, q, q, b.Zcm, status, f.fail_bit, st);
+    else launch_conj_copy(f.src, p * q, b.Zcm, status, f.fail_bit, st);
+    launch_householder_qr(b.Zcm, p, q, b.betas, b.Qcm, b.T, q, status, f.fail_bit, st);
+    launch_colmajor_to_rowmajor(b.Qcm, p, q, f.out.Q, q, status, f.fail_bit, 0, st);
+    launch_rowmajor_to_colmajor(b.T, q, q, q, b.Tcm, status, f.fail_bit, st);
+    launch_jacobi_pinv_factor(b.Tcm, b.Vcm, q, kEps * (double)(p > q ? p : q), f.cutoff_abs, f.out.F, q, status,
+                              f.fail_bit, st);
+    CK_LAUNCH(ctx, "robust factor");
+  }
   return QCUR_OK;
+}
+
+int factor_tall(qcur_ctx* ctx, const double* src, int zh, int64_t p, int64_t q, unsigned fail_bit, double cutoff_abs,
+                FactorOut out) {
+  FactorSpec f{src, zh, p, q, fail_bit, cutoff_abs, out};
+  return factor_multi(ctx, &f, 1);
 }
 
 // explicit pinv (any shape) into out (n x m), arena reserved by caller
@@ -375,11 +521,13 @@ int qmcur_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, const doubl
                     ctx->take<double>((size_t)draw_work_doubles(m))};
   if (!jobs[0].work || !jobs[1].work) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (draw)");
   launch_draw(jobs, 2, ctx->status_dev, st);
+  ctx->mark("draw");
   CK_LAUNCH(ctx, "draw");
   // 2. gathers (quat.py:215-225)
   launch_gather_cols(X, m, n, J, c, C, st);
   launch_gather_rows(X, n, n, I, r, R, st);
   CK_LAUNCH(ctx, "gather");
+  ctx->mark("gather");
   int rc;
   if (m >= c && n >= r) {
     double* QC = ctx->take<double>((size_t)(m * c * 4));
@@ -391,20 +539,24 @@ int qmcur_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, const doubl
     double* W = ctx->take<double>((size_t)(c * r * 4));
     if (!QC || !FC || !QR || !FR || !Y || !M || !W) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (qmcur)");
     // 3. pinv(C) = F_C Q_C^H ; pinv(R) = Q_R F_R^H  (R^H = Q_R T_R)
-    if ((rc = factor_tall(ctx, C, 0, m, c, ST_CHOL_FAIL_C, -1.0, FactorOut{QC, FC}))) return rc;
-    if ((rc = factor_tall(ctx, R, 1, n, r, ST_CHOL_FAIL_R, -1.0, FactorOut{QR, FR}))) return rc;
+    FactorSpec specs[2] = {FactorSpec{C, 0, m, c, ST_CHOL_FAIL_C, -1.0, FactorOut{QC, FC}},
+                           FactorSpec{R, 1, n, r, ST_CHOL_FAIL_R, -1.0, FactorOut{QR, FR}}};
+    if ((rc = factor_multi(ctx, specs, 2))) return rc;
     GemmArgs g1 = gargs(m, r, n, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0);
     GemmArgs g2a = gargs(c, r, m, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0);
     size_t a = qgemm_workspace_bytes(g1), d = qgemm_workspace_bytes(g2a);
     double* gws = ctx->take<double>((a > d ? a : d) / 8 + 16);
     if (!gws) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (qmcur gemm)");
+    ctx->mark("factor");
     // 4. Y = X Q_R (m x r) — the big contraction (cur.py:268)
     if ((rc = gemm(ctx, gargs(m, r, n, X, n, 0, QR, r, 0, Y, r), gws))) return rc;
+    ctx->mark("gemm_xq");
     // 5. M = Q_C^H Y (c x r)
     if ((rc = gemm(ctx, gargs(c, r, m, QC, c, 1, Y, r, 0, M, r), gws))) return rc;
     // 6. U = F_C M F_R^H
     if ((rc = gemm(ctx, gargs(c, r, c, FC, c, 0, M, r, 0, W, r), gws))) return rc;
     if ((rc = gemm(ctx, gargs(c, r, r, W, r, 0, FR, r, 1, U, r), gws))) return rc;
+    ctx->mark("core_u");
   } else {
     // non-standard shapes (c > m or r > n): explicit pseudoinverses
     double* PC = ctx->take<double>((size_t)(c * m * 4));
@@ -420,6 +572,7 @@ int qmcur_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, const doubl
     if (!gws) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (qmcur general gemm)");
     if ((rc = gemm(ctx, gargs(m, r, n, X, n, 0, PR, r, 0, Y, r), gws))) return rc;
     if ((rc = gemm(ctx, gargs(c, r, m, PC, m, 0, Y, r, 0, U, r), gws))) return rc;
+    ctx->mark("core_u");
   }
   return QCUR_OK;
 }
@@ -440,7 +593,9 @@ int error_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, const doubl
   int rc;
   // P = C U (m x r) (cur.py:274 left product), then the fused ||X - P R|| pass
   if ((rc = gemm(ctx, g, gws))) return rc;
+  ctx->mark("cu");
   launch_cur_error(X, n, P, r, R, n, m, n, r, parts, out2, ctx->stream);
+  ctx->mark("error");
   CK_LAUNCH(ctx, "cur_error");
   return QCUR_OK;
 }
@@ -673,17 +828,47 @@ int qcur_approx(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int st
   if (rc) return rc;
   double* colp = ctx->take<double>((size_t)n);
   double* rowp = ctx->take<double>((size_t)m);
+  ctx->mark_begin();
   if (strategy == QCUR_STRATEGY_LENGTH) {
     if ((rc = length_distributions_impl(ctx, x_dev, m, n, colp, rowp))) return rc;
   } else {
     launch_fill(colp, n, 1.0 / (double)n, ctx->stream);
     launch_fill(rowp, m, 1.0 / (double)m, ctx->stream);
+    ctx->mark("dists");
   }
   if ((rc = qmcur_impl(ctx, x_dev, m, n, colp, rowp, c, r, state, J, I, C, U, R))) return rc;
   return error_impl(ctx, x_dev, m, n, C, c, U, R, r, err2);
 }
 
 int qcur_check(qcur_ctx* ctx) { return sync_status(ctx); }
+
+int qcur_profile(qcur_ctx* ctx, int on) {
+  if (!ctx) return QCUR_E_PARAMETER;
+  cudaStreamSynchronize(ctx->stream);
+  ctx->prof.marks.clear();
+  ctx->prof.start = nullptr;
+  ctx->prof.used = 0;
+  ctx->prof.acc.clear();
+  ctx->prof.on = on != 0;
+  return QCUR_OK;
+}
+
+int qcur_profile_read(qcur_ctx* ctx, char* buf, size_t len) {
+  if (!ctx || !buf || len == 0) return QCUR_E_PARAMETER;
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) return ctx->cuda_fail(e, "profile sync");
+  ctx->harvest();
+  std::string out;
+  char tmp[160];
+  for (auto& kv : ctx->prof.acc) {
+    snprintf(tmp, sizeof tmp, "%s:%.6f:%ld;", kv.first.c_str(), kv.second.first, kv.second.second);
+    out += tmp;
+  }
+  snprintf(buf, len, "%s", out.c_str());
+  return QCUR_OK;
+}
+
+unsigned long long qcur_launch_count(void) { return qcur::g_launches; }
 
 int qcur_qgemm(qcur_ctx* ctx, int opA, int opB, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
                int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
