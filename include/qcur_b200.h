@@ -130,6 +130,9 @@ double qcur_fp64_peak_tflops(qcur_ctx* ctx);
 int qcur_profile(qcur_ctx* ctx, int on);
 int qcur_profile_read(qcur_ctx* ctx, char* buf, size_t len);
 unsigned long long qcur_launch_count(void);
+/* Host evaluation of the numpy pairwise-summation program the K1 kernels run
+ * (cur.py:144, 148, 150 orders); test hook, no device needed. */
+int qcur_pairwise_host(const double* data, int64_t n, double* out);
 
 #ifdef __cplusplus
 }

@@ -43,7 +43,7 @@ EXPORTS = (
     "qcur_length_distributions", "qcur_uniform_distributions", "qcur_draw_indices", "qcur_qmcur",
     "qcur_cur_error", "qcur_approx", "qcur_check", "qcur_qgemm", "qcur_pseudoinverse",
     "qcur_frobenius_sq", "qcur_synth_lowrank", "qcur_fp64_peak_tflops",
-    "qcur_profile", "qcur_profile_read", "qcur_launch_count",
+    "qcur_profile", "qcur_profile_read", "qcur_launch_count", "qcur_pairwise_host",
 )
 
 _c_dp = ctypes.c_void_p
@@ -104,6 +104,7 @@ def load_library() -> ctypes.CDLL:
             "qcur_profile": (ctypes.c_int, [_c_dp, ctypes.c_int]),
             "qcur_profile_read": (ctypes.c_int, [_c_dp, ctypes.c_char_p, ctypes.c_size_t]),
             "qcur_launch_count": (ctypes.c_ulonglong, []),
+            "qcur_pairwise_host": (ctypes.c_int, [_c_dp, _i64, ctypes.POINTER(ctypes.c_double)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)

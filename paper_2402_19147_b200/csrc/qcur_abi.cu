@@ -870,6 +870,54 @@ int qcur_profile_read(qcur_ctx* ctx, char* buf, size_t len) {
 
 unsigned long long qcur_launch_count(void) { return qcur::g_launches; }
 
+// Host evaluation of the compiled pairwise program (the exact tree the K1
+// kernels execute), so the plan compiler is testable without a GPU.
+int qcur_pairwise_host(const double* data, int64_t n, double* out) {
+  if (!data || !out || n < 0) return QCUR_E_PARAMETER;
+  PairwiseProgram pp = compile_pairwise(n);
+  std::vector<double> vals(pp.chunk_off.size() + pp.node_l.size());
+  for (size_t ch = 0; ch < pp.chunk_off.size(); ++ch) {
+    const ChunkPlan& cp = pp.plans[pp.chunk_plan[ch]];
+    const double* src = data + pp.chunk_off[ch];
+    std::vector<double> leaf(cp.leaf_off.size());
+    for (size_t l = 0; l < cp.leaf_off.size(); ++l) {
+      const double* a = src + cp.leaf_off[l];
+      const int len = cp.leaf_len[l];
+      double res;
+      if (len < 8) {
+        res = 0.0;
+        for (int i = 0; i < len; ++i) res += a[i];
+      } else {
+        double r[8];
+        for (int k = 0; k < 8; ++k) r[k] = a[k];
+        int i = 8;
+        for (; i < len - (len % 8); i += 8)
+          for (int k = 0; k < 8; ++k) r[k] += a[i + k];
+        res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < len; ++i) res += a[i];
+      }
+      leaf[l] = res;
+    }
+    std::vector<double> stack;
+    for (int32_t op : cp.prog) {
+      if (op >= 0) {
+        stack.push_back(leaf[op]);
+      } else {
+        double b = stack.back();
+        stack.pop_back();
+        double a = stack.back();
+        stack.pop_back();
+        stack.push_back(a + b);
+      }
+    }
+    vals[ch] = stack.empty() ? 0.0 : stack[0];
+  }
+  const size_t nch = pp.chunk_off.size();
+  for (size_t k = 0; k < pp.node_l.size(); ++k) vals[nch + k] = vals[pp.node_l[k]] + vals[pp.node_r[k]];
+  *out = pp.node_l.empty() ? (nch ? vals[0] : 0.0) : vals.back();
+  return QCUR_OK;
+}
+
 int qcur_qgemm(qcur_ctx* ctx, int opA, int opB, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
                int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
   if (M < 0 || N < 0 || K < 0) return ctx->fail(QCUR_E_SHAPE, "negative gemm size");

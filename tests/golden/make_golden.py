@@ -1,0 +1,69 @@
+"""Generate tests/golden/golden.npz from the REFERENCE package (qcur).
+
+Run in the build container only (the reference is not on the GPU box):
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+It imports /root/reference/pkg/src read-only, runs the reference's own
+make_plan / qmcur / cur_reconstruct / draw_indices / length_distributions /
+pseudoinverse on the inputs defined in cases.py, and stores the outputs.
+"""
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+
+sys.dont_write_bytecode = True
+os.environ.setdefault("QCUR_THREADS", "1")
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import numpy as np  # noqa: E402
+
+import cases  # noqa: E402
+import qcur  # noqa: E402  (the reference)
+
+
+def planes_hash(planes) -> str:
+    h = hashlib.sha256()
+    for p in planes:
+        h.update(np.ascontiguousarray(p, dtype="<f8").tobytes())
+    return h.hexdigest()
+
+
+def main() -> None:
+    out = {}
+    for name, case in cases.QMCUR_CASES.items():
+        m, n, k, noise, gseed, strategy, pseed, nr, nc = case
+        x = qcur.QMatrix(*cases.qmcur_input(case))
+        plan = qcur.make_plan(x, strategy, k, pseed, num_rows=nr, num_cols=nc)
+        f = qcur.qmcur(x, plan)
+        diff = x - qcur.cur_reconstruct(f)
+        rel = qcur.qmat_frobenius_norm(diff) / qcur.qmat_frobenius_norm(x)
+        out[f"{name}/col_probs"] = plan.col_probs
+        out[f"{name}/row_probs"] = plan.row_probs
+        out[f"{name}/cols"] = f.col_indices.astype(np.int64)
+        out[f"{name}/rows"] = f.row_indices.astype(np.int64)
+        out[f"{name}/u"] = f.u.to_array()
+        out[f"{name}/rel_err"] = np.array([rel])
+        out[f"{name}/c_sha"] = np.array([planes_hash(f.c.planes)])
+        out[f"{name}/r_sha"] = np.array([planes_hash(f.r.planes)])
+        print(name, "rel_err %.6e" % rel)
+    for name, case in cases.DIST_CASES.items():
+        col, row = qcur.length_distributions(qcur.QMatrix(*cases.dist_input(case)))
+        out[f"{name}/col"] = col
+        out[f"{name}/row"] = row
+    for name, case in cases.DRAW_CASES.items():
+        p, count, seed = cases.draw_input(case)
+        out[f"{name}/idx"] = qcur.draw_indices(p, count, seed).astype(np.int64)
+    for name, case in cases.PINV_CASES.items():
+        out[f"{name}/pinv"] = qcur.pseudoinverse(qcur.QMatrix(*cases.pinv_input(case))).to_array()
+    for s in cases.RNG_SEEDS:
+        out[f"rng/{s}"] = np.random.default_rng(s).random(8)
+    out["meta/numpy"] = np.array([np.__version__])
+    np.savez_compressed(os.path.join(HERE, "golden.npz"), **out)
+    print("wrote", os.path.join(HERE, "golden.npz"))
+
+
+if __name__ == "__main__":
+    main()

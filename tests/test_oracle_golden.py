@@ -1,0 +1,56 @@
+"""Pin the CPU oracle against golden outputs of the reference package
+(tests/golden/golden.npz, made by tests/golden/make_golden.py from qcur)."""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from golden import cases
+
+G = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden.npz"))
+
+
+@pytest.mark.parametrize("name", sorted(cases.QMCUR_CASES))
+def test_oracle_qmcur_matches_reference(name):
+    m, n, k, noise, gseed, strategy, pseed, nr, nc = cases.QMCUR_CASES[name]
+    planes = cases.qmcur_input(cases.QMCUR_CASES[name])
+    d_r, d_c = O.default_sample_counts(k, m, n)
+    nr = d_r if nr is None else nr
+    nc = d_c if nc is None else nc
+    res = O.approx(planes, strategy, k, pseed, nc, nr)
+    assert np.array_equal(res["col_probs"], G[f"{name}/col_probs"])
+    assert np.array_equal(res["row_probs"], G[f"{name}/row_probs"])
+    assert np.array_equal(res["cols"], G[f"{name}/cols"])
+    assert np.array_equal(res["rows"], G[f"{name}/rows"])
+    u_ref = tuple(G[f"{name}/u"])
+    assert O.rel_fro(res["u"], u_ref) <= 1e-9
+    ref = float(G[f"{name}/rel_err"][0])
+    assert abs(res["rel_err"] - ref) <= max(1e-10 * ref, 1e-14)
+
+
+@pytest.mark.parametrize("name", sorted(cases.DIST_CASES))
+def test_oracle_distributions_bitwise(name):
+    col, row = O.length_distributions(cases.dist_input(cases.DIST_CASES[name]))
+    assert np.array_equal(col, G[f"{name}/col"]) and np.array_equal(row, G[f"{name}/row"])
+
+
+@pytest.mark.parametrize("name", sorted(cases.DRAW_CASES))
+def test_oracle_draws_exact(name):
+    p, count, seed = cases.draw_input(cases.DRAW_CASES[name])
+    assert np.array_equal(O.draw_indices(p, count, np.random.default_rng(seed)), G[f"{name}/idx"])
+
+
+@pytest.mark.parametrize("name", sorted(cases.PINV_CASES))
+def test_oracle_pinv(name):
+    got = O.pinv(cases.pinv_input(cases.PINV_CASES[name]))
+    assert O.rel_fro(got, tuple(G[f"{name}/pinv"])) <= 1e-10
+
+
+def test_oracle_error_definition():
+    # relative error = ||X - CUR||_F / ||X||_F with planes summed in order
+    planes = cases.qmcur_input(cases.QMCUR_CASES["small_10x8"])
+    e2, x2 = O.cur_error(planes, planes, tuple(np.zeros((8, 8)) + (1.0 if s == 0 else 0.0) * np.eye(8) for s in range(4)),
+                         tuple(np.eye(8) * (1.0 if s == 0 else 0.0) for s in range(4)))
+    assert e2 == pytest.approx(0.0, abs=1e-24) and math.sqrt(x2) > 0
