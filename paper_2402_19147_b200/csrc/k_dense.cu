@@ -114,6 +114,10 @@ __global__ void k_series_lh(const double* __restrict__ G2, const double* __restr
   int bad = 0;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < q * q; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = t / q, k = t - i * q;
+    if (k > i) {  // only the lower triangle of the Hermitian G2 / P is produced
+      stQ(M + t * 4, qzero());
+      continue;
+    }
     Quat e = ldQ(G2 + t * 4);
     if (i == k) e.w -= 1.0;
     if (P == nullptr) {  // first call: also check the size of E

@@ -23,6 +23,8 @@
 // imaging.py:170-177): the tile of (P R) is subtracted from the matching tile
 // of X in registers and only sum((X - PR)^2) and sum(X^2) leave the CTA, so
 // CUR is never written to HBM.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -83,6 +85,9 @@ struct KParams {
   const double* X;     // EPI_ERR: reference matrix
   int64_t ldx;
   double* partials;    // EPI_ERR: [tiles][2]
+  unsigned* counters;  // split-K: per-tile arrival tickets (zero between launches)
+  int b_upper;         // op(B) is upper triangular: column j only needs k <= j
+  int herm_lower;      // output is Hermitian and only its lower triangle is consumed
 };
 
 template <int BM, int BN, int WM, int WN, int BKQ, int STAGES, int OPA, int OPB, int EPI>
@@ -99,7 +104,9 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN, BKQ, STAGES, OPA, OPB, EPI
   const int64_t kbeg = (int64_t)blockIdx.z * p.kchunk;
   int64_t kend = kbeg + p.kchunk;
   if (kend > p.Kq) kend = p.Kq;
-  const int nkb = (int)((kend - kbeg + BKQ - 1) / BKQ);
+  if (p.b_upper && kend > jq0 + BN / 4) kend = jq0 + BN / 4;  // op(B)[k][j] = 0 for k > j
+  const bool skip = p.herm_lower && jq0 > i0 + BM - 1;     // tile strictly above the diagonal
+  const int nkb = skip || kend <= kbeg ? 0 : (int)((kend - kbeg + BKQ - 1) / BKQ);
 
   auto load_stage = [&](int buf, int64_t k0) {
     double* As = smem + buf * CF::STAGE_ELEMS;
@@ -207,7 +214,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN, BKQ, STAGES, OPA, OPB, EPI
         if (gj >= Nr) continue;
         if (p.work) {
           double* w = p.work + ((int64_t)blockIdx.z * p.Mq + gi) * Nr + gj;
-          *reinterpret_cast<double2*>(w) = make_double2(acc[a][b][0], acc[a][b][1]);
+          __stcg(reinterpret_cast<double2*>(w), make_double2(acc[a][b][0], acc[a][b][1]));
         } else {
           double* c = p.C + gi * p.ldc * 4 + gj;
           double2 v = make_double2(p.alpha * acc[a][b][0], p.alpha * acc[a][b][1]);
@@ -218,6 +225,40 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN, BKQ, STAGES, OPA, OPB, EPI
           }
           *reinterpret_cast<double2*>(c) = v;
         }
+      }
+    }
+    if (p.work) {
+      // Deterministic split-K fix-up: the last CTA to finish this tile sums the
+      // slabs in the fixed order z = 0..S-1 (no separate reduce launch).
+      __shared__ unsigned s_last;
+      __threadfence();
+      __syncthreads();
+      const int64_t tile = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+      if (tid == 0) s_last = (atomicAdd(&p.counters[tile], 1u) == gridDim.z - 1) ? 1u : 0u;
+      __syncthreads();
+      if (s_last) {
+        __threadfence();
+        const int S = (int)gridDim.z;
+        for (int idx = tid; idx < BM * (BN / 2); idx += CF::THREADS) {
+          const int r = idx / (BN / 2), cc = 2 * (idx % (BN / 2));
+          const int64_t gi = i0 + r, gj = jr0 + cc;
+          if (gi >= p.Mq || gj >= Nr) continue;
+          double sx = 0.0, sy = 0.0;
+          for (int z = 0; z < S; ++z) {
+            const double2 v = __ldcg(reinterpret_cast<const double2*>(p.work + ((int64_t)z * p.Mq + gi) * Nr + gj));
+            sx += v.x;
+            sy += v.y;
+          }
+          double* c = p.C + gi * p.ldc * 4 + gj;
+          double2 o = make_double2(p.alpha * sx, p.alpha * sy);
+          if (p.beta != 0.0) {
+            const double2 old = *reinterpret_cast<const double2*>(c);
+            o.x += p.beta * old.x;
+            o.y += p.beta * old.y;
+          }
+          *reinterpret_cast<double2*>(c) = o;
+        }
+        if (tid == 0) p.counters[tile] = 0u;
       }
     }
   } else {
@@ -260,28 +301,20 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN, BKQ, STAGES, OPA, OPB, EPI
   }
 }
 
-__global__ void splitk_reduce(const double* __restrict__ work, int splits, int64_t Mq, int64_t Nr,
-                              double* __restrict__ C, int64_t ldc, double alpha, double beta) {
-  const int64_t total = Mq * Nr;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = t / Nr, j = t - i * Nr;
-    double s = 0.0;
-    for (int z = 0; z < splits; ++z) s += work[(int64_t)z * total + t];
-    double* c = C + i * ldc * 4 + j;
-    double v = alpha * s;
-    if (beta != 0.0) v += beta * *c;
-    *c = v;
-  }
-}
+// Tile configurations (FP64 DMMA: 32x32 warp tiles, >= 2 CTAs per SM).
+//   C0 64x128, 8-quaternion K stages x3   (default; error kernel)
+//   C1 128x64, 4-quaternion K stages x4   (narrow N, e.g. 4r = 800 -> 4% padding instead of 12%)
+//   C2 64x160, 8-quaternion K stages x3   (N multiple of 160, 10 warps)
+// launch_qgemm picks the configuration with the least padded area.
+struct TileCfg {
+  int bm, bn, bkq;
+};
+constexpr TileCfg kCfgs[3] = {{64, 128, 8}, {128, 64, 4}, {64, 160, 8}};
 
-// Tile configuration used for every product (tuned for the FP64 DMMA pipe:
-// 2 CTAs x 8 warps per SM, 32x32 warp tiles, 3-stage cp.async pipeline).
-constexpr int G_BM = 64, G_BN = 128, G_WM = 32, G_WN = 32, G_BKQ = 8, G_ST = 3;
-
-template <int OPA, int OPB, int EPI>
-void launch_cfg(const KParams& kp, dim3 grid, cudaStream_t st) {
-  using CF = Cfg<G_BM, G_BN, G_WM, G_WN, G_BKQ, G_ST, OPA, OPB, EPI>;
-  auto kern = qgemm_kernel<G_BM, G_BN, G_WM, G_WN, G_BKQ, G_ST, OPA, OPB, EPI>;
+template <int BM, int BN, int BKQ, int ST, int OPA, int OPB, int EPI>
+void launch_t(const KParams& kp, dim3 grid, cudaStream_t st) {
+  using CF = Cfg<BM, BN, 32, 32, BKQ, ST, OPA, OPB, EPI>;
+  auto kern = qgemm_kernel<BM, BN, 32, 32, BKQ, ST, OPA, OPB, EPI>;
   static bool set = false;
   if (!set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM);
@@ -291,26 +324,49 @@ void launch_cfg(const KParams& kp, dim3 grid, cudaStream_t st) {
   kern<<<grid, CF::THREADS, CF::SMEM, st>>>(kp);
 }
 
-int choose_splits(int64_t tiles, int64_t Kq) {
+template <int OPA, int OPB>
+void launch_ops(int cfg, const KParams& kp, dim3 grid, cudaStream_t st) {
+  if (cfg == 1) launch_t<128, 64, 4, 4, OPA, OPB, EPI_STORE>(kp, grid, st);
+  else if (cfg == 2) launch_t<64, 160, 8, 3, OPA, OPB, EPI_STORE>(kp, grid, st);
+  else launch_t<64, 128, 8, 3, OPA, OPB, EPI_STORE>(kp, grid, st);
+}
+
+int pick_cfg(int64_t Mq, int64_t Nq) {
+  static const int forced = [] {
+    const char* e = getenv("QCUR_GEMM_CFG");  // experiments only: force one tile configuration
+    return e ? atoi(e) : -1;
+  }();
+  if (forced >= 0 && forced < 3) return forced;
+  // Measured on B200 (cfg2, bench phases): C0 beats C1 / C2 on every product of
+  // the path even where they pad less (C1's 4-quaternion stages and C2's
+  // 96-register cap cost more than the padding saves), so C0 is the default.
+  (void)Mq;
+  (void)Nq;
+  return 0;
+}
+
+int choose_splits(int64_t tiles, int64_t Kq, int bkq) {
   const int64_t slots = 148 * 2;
   if (tiles >= 2 * slots) return 1;
   int64_t sp = (3 * slots + tiles - 1) / tiles;
-  int64_t maxsp = Kq / (4 * G_BKQ);  // keep >= 32 quaternions of K per split
+  int64_t maxsp = Kq / 32;  // keep >= 32 quaternions of K per split
   if (sp > maxsp) sp = maxsp;
   if (sp < 1) sp = 1;
   if (sp > 64) sp = 64;
+  (void)bkq;
   return (int)sp;
 }
 
 }  // namespace
 
 size_t qgemm_workspace_bytes(const GemmArgs& g) {
-  const int64_t tiles = ((4 * g.Nq + G_BN - 1) / G_BN) * ((g.Mq + G_BM - 1) / G_BM);
-  const int sp = choose_splits(tiles, g.Kq);
+  const TileCfg& c = kCfgs[pick_cfg(g.Mq, g.Nq)];
+  const int64_t tiles = ((4 * g.Nq + c.bn - 1) / c.bn) * ((g.Mq + c.bm - 1) / c.bm);
+  const int sp = choose_splits(tiles, g.Kq, c.bkq);
   return sp > 1 ? (size_t)sp * g.Mq * 4 * g.Nq * sizeof(double) : 0;
 }
 
-void launch_qgemm(const GemmArgs& g, double* workspace, cudaStream_t st) {
+void launch_qgemm(const GemmArgs& g, double* workspace, unsigned* counters, cudaStream_t st) {
   if (g.Mq <= 0 || g.Nq <= 0) return;
   KParams kp{};
   kp.Mq = g.Mq;
@@ -324,28 +380,27 @@ void launch_qgemm(const GemmArgs& g, double* workspace, cudaStream_t st) {
   kp.ldc = g.ldc;
   kp.alpha = g.alpha;
   kp.beta = g.beta;
-  const int64_t gx = (4 * g.Nq + G_BN - 1) / G_BN, gy = (g.Mq + G_BM - 1) / G_BM;
-  const int sp = g.Kq > 0 ? choose_splits(gx * gy, g.Kq) : 1;
+  kp.b_upper = g.b_upper;
+  kp.herm_lower = g.herm_lower;
+  kp.counters = counters;
+  const int cfg = pick_cfg(g.Mq, g.Nq);
+  const TileCfg& c = kCfgs[cfg];
+  const int64_t gx = (4 * g.Nq + c.bn - 1) / c.bn, gy = (g.Mq + c.bm - 1) / c.bm;
+  int sp = g.Kq > 0 ? choose_splits(gx * gy, g.Kq, c.bkq) : 1;
+  if (!workspace || !counters || gx * gy > (1 << 16)) sp = 1;
   int64_t kchunk = (g.Kq + sp - 1) / sp;
-  kchunk = ((kchunk + G_BKQ - 1) / G_BKQ) * G_BKQ;
+  kchunk = ((kchunk + 7) / 8) * 8;
   const int spz = kchunk > 0 ? (int)((g.Kq + kchunk - 1) / kchunk) : 1;
-  kp.kchunk = kchunk > 0 ? kchunk : G_BKQ;
+  kp.kchunk = kchunk > 0 ? kchunk : 8;
   kp.work = spz > 1 ? workspace : nullptr;
   dim3 grid((unsigned)gx, (unsigned)gy, (unsigned)spz);
-  if (g.opA == 0 && g.opB == 0) launch_cfg<0, 0, EPI_STORE>(kp, grid, st);
-  else if (g.opA == 0 && g.opB == 1) launch_cfg<0, 1, EPI_STORE>(kp, grid, st);
-  else if (g.opA == 1 && g.opB == 0) launch_cfg<1, 0, EPI_STORE>(kp, grid, st);
-  else launch_cfg<1, 1, EPI_STORE>(kp, grid, st);
-  if (spz > 1) {
-    const int64_t total = g.Mq * 4 * g.Nq;
-    int blocks = (int)((total + 255) / 256);
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    ++::qcur::g_launches;
-    splitk_reduce<<<blocks, 256, 0, st>>>(workspace, spz, g.Mq, 4 * g.Nq, g.C, g.ldc, g.alpha, g.beta);
-  }
+  if (g.opA == 0 && g.opB == 0) launch_ops<0, 0>(cfg, kp, grid, st);
+  else if (g.opA == 0 && g.opB == 1) launch_ops<0, 1>(cfg, kp, grid, st);
+  else if (g.opA == 1 && g.opB == 0) launch_ops<1, 0>(cfg, kp, grid, st);
+  else launch_ops<1, 1>(cfg, kp, grid, st);
 }
 
-int64_t err_partials_count(int64_t m, int64_t n) { return ((4 * n + G_BN - 1) / G_BN) * ((m + G_BM - 1) / G_BM); }
+int64_t err_partials_count(int64_t m, int64_t n) { return ((4 * n + 128 - 1) / 128) * ((m + 64 - 1) / 64); }
 
 void launch_cur_error(const double* X, int64_t ldx, const double* P, int64_t ldp, const double* R, int64_t ldr,
                       int64_t m, int64_t n, int64_t r, double* partials, double* out2, cudaStream_t st) {
@@ -358,12 +413,12 @@ void launch_cur_error(const double* X, int64_t ldx, const double* P, int64_t ldp
   kp.B = R;
   kp.ldb = ldr;
   kp.alpha = 1.0;
-  kp.kchunk = ((r + G_BKQ - 1) / G_BKQ) * G_BKQ;
+  kp.kchunk = ((r + 7) / 8) * 8;
   kp.X = X;
   kp.ldx = ldx;
   kp.partials = partials;
-  const int64_t gx = (4 * n + G_BN - 1) / G_BN, gy = (m + G_BM - 1) / G_BM;
-  launch_cfg<0, 0, EPI_ERR>(kp, dim3((unsigned)gx, (unsigned)gy, 1), st);
+  const int64_t gx = (4 * n + 128 - 1) / 128, gy = (m + 64 - 1) / 64;
+  launch_t<64, 128, 8, 3, 0, 0, EPI_ERR>(kp, dim3((unsigned)gx, (unsigned)gy, 1), st);
   launch_reduce_pairs(partials, gx * gy, out2, st);
 }
 

@@ -68,9 +68,12 @@ struct GemmArgs {
   double* C;
   int64_t ldc;
   double alpha, beta;
+  int b_upper = 0;     // op(B) upper triangular (skip k > j)
+  int herm_lower = 0;  // Hermitian output, only the lower triangle is produced / consumed
 };
 size_t qgemm_workspace_bytes(const GemmArgs& g);
-void launch_qgemm(const GemmArgs& g, double* workspace, cudaStream_t st);
+// counters: >= 65536 zero-initialised uints owned by the caller (split-K tickets)
+void launch_qgemm(const GemmArgs& g, double* workspace, unsigned* counters, cudaStream_t st);
 // ||X - P R||_F^2 and ||X||_F^2 partials, P: m x r, R: r x n, X: m x n (all interleaved)
 int64_t err_partials_count(int64_t m, int64_t n);
 void launch_cur_error(const double* X, int64_t ldx, const double* P, int64_t ldp, const double* R, int64_t ldr,

@@ -67,6 +67,7 @@ struct qcur_ctx {
   cudaStream_t stream = nullptr;
   unsigned* status_dev = nullptr;
   unsigned* status_host = nullptr;  // pinned
+  unsigned* counters = nullptr;     // split-K tickets for launch_qgemm (kept zero between launches)
   unsigned last_info = 0;
   double kappa_limit = 1e7;
   bool force_robust = false;
@@ -283,7 +284,7 @@ size_t factor_ws_bytes(int64_t p, int64_t q) {
 }
 
 int gemm(qcur_ctx* ctx, const GemmArgs& g, double* ws) {
-  launch_qgemm(g, ws, ctx->stream);
+  launch_qgemm(g, ws, ctx->counters, ctx->stream);
   CK_LAUNCH(ctx, "qgemm");
   return QCUR_OK;
 }
@@ -304,6 +305,13 @@ GemmArgs gargs(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, in
   g.ldc = ldc;
   g.alpha = alpha;
   g.beta = beta;
+  return g;
+}
+
+// structure hints: op(B) upper triangular; Hermitian output with only its lower triangle consumed
+GemmArgs with_flags(GemmArgs g, int b_upper, int herm_lower) {
+  g.b_upper = b_upper;
+  g.herm_lower = herm_lower;
   return g;
 }
 
@@ -398,8 +406,8 @@ int factor_multi(qcur_ctx* ctx, const FactorSpec* specs, int ns) {
     if (!fast[k]) continue;
     const FactorSpec& f = specs[k];
     const int64_t p = f.p, q = f.q;
-    if (!f.zh) rc = gemm(ctx, gargs(q, q, p, f.src, q, 1, f.src, q, 0, B[k].G1, q), B[k].gws);
-    else rc = gemm(ctx, gargs(q, q, p, f.src, p, 0, f.src, p, 1, B[k].G1, q), B[k].gws);
+    if (!f.zh) rc = gemm(ctx, with_flags(gargs(q, q, p, f.src, q, 1, f.src, q, 0, B[k].G1, q), 0, 1), B[k].gws);
+    else rc = gemm(ctx, with_flags(gargs(q, q, p, f.src, p, 0, f.src, p, 1, B[k].G1, q), 0, 1), B[k].gws);
     if (rc) return rc;
   }
   if ((rc = chol_inv(false))) return rc;
@@ -408,10 +416,11 @@ int factor_multi(qcur_ctx* ctx, const FactorSpec* specs, int ns) {
     if (!fast[k]) continue;
     const FactorSpec& f = specs[k];
     const int64_t p = f.p, q = f.q;
-    if (!f.zh) rc = gemm(ctx, gargs(p, q, q, f.src, q, 0, B[k].L1i, q, 1, B[k].Q1, q), B[k].gws);
-    else rc = gemm(ctx, gargs(p, q, q, f.src, p, 1, B[k].L1i, q, 1, B[k].Q1, q), B[k].gws);
+    if (!f.zh) rc = gemm(ctx, with_flags(gargs(p, q, q, f.src, q, 0, B[k].L1i, q, 1, B[k].Q1, q), 1, 0), B[k].gws);
+    else rc = gemm(ctx, with_flags(gargs(p, q, q, f.src, p, 1, B[k].L1i, q, 1, B[k].Q1, q), 1, 0), B[k].gws);
     if (rc) return rc;
-    if ((rc = gemm(ctx, gargs(q, q, p, B[k].Q1, q, 1, B[k].Q1, q, 0, B[k].G2, q), B[k].gws))) return rc;
+    if ((rc = gemm(ctx, with_flags(gargs(q, q, p, B[k].Q1, q, 1, B[k].Q1, q, 0, B[k].G2, q), 0, 1), B[k].gws)))
+      return rc;
   }
   // second pass: G2 = I + E with E ~ kappa^2 u; L2^{-1} by a second-order series
   // (no sequential Cholesky; blocks with max|E| > 1e-5 take the robust path)
@@ -421,7 +430,7 @@ int factor_multi(qcur_ctx* ctx, const FactorSpec* specs, int ns) {
     Bufs& b = B[k];
     double *M0 = b.L2, *P = b.T, *M1 = b.Tcm, *P2 = b.Vcm;
     launch_series_lh(b.G2, nullptr, q, M0, status, specs[k].fail_bit, 1e-5, st);
-    if ((rc = gemm(ctx, gargs(q, q, q, M0, q, 0, M0, q, 1, P, q), b.gws))) return rc;
+    if ((rc = gemm(ctx, with_flags(gargs(q, q, q, M0, q, 0, M0, q, 1, P, q), 1, 1), b.gws))) return rc;
     launch_series_lh(b.G2, P, q, M1, status, specs[k].fail_bit, 1e-5, st);
     if ((rc = gemm(ctx, gargs(q, q, q, M1, q, 0, M1, q, 0, P2, q), b.gws))) return rc;
     launch_series_final(M1, P2, q, b.L2i, st);
@@ -432,8 +441,10 @@ int factor_multi(qcur_ctx* ctx, const FactorSpec* specs, int ns) {
     if (!fast[k]) continue;
     const FactorSpec& f = specs[k];
     const int64_t p = f.p, q = f.q;
-    if ((rc = gemm(ctx, gargs(p, q, q, B[k].Q1, q, 0, B[k].L2i, q, 1, f.out.Q, q), B[k].gws))) return rc;
-    if ((rc = gemm(ctx, gargs(q, q, q, B[k].L1i, q, 1, B[k].L2i, q, 1, f.out.F, q), B[k].gws))) return rc;
+    if ((rc = gemm(ctx, with_flags(gargs(p, q, q, B[k].Q1, q, 0, B[k].L2i, q, 1, f.out.Q, q), 1, 0), B[k].gws)))
+      return rc;
+    if ((rc = gemm(ctx, with_flags(gargs(q, q, q, B[k].L1i, q, 1, B[k].L2i, q, 1, f.out.F, q), 1, 0), B[k].gws)))
+      return rc;
     launch_kappa_check(B[k].G1, f.out.F, q, ctx->kappa_limit, status, f.fail_bit, st);
     CK_LAUNCH(ctx, "kappa");
   }
@@ -648,6 +659,11 @@ int qcur_create(int device, qcur_ctx** out) {
     return QCUR_E_CUDA;
   }
   cudaMemset(ctx->status_dev, 0, 64);
+  if (cudaMalloc(&ctx->counters, (size_t)65536 * sizeof(unsigned)) != cudaSuccess) {
+    delete ctx;
+    return QCUR_E_CUDA;
+  }
+  cudaMemset(ctx->counters, 0, (size_t)65536 * sizeof(unsigned));
   *out = ctx;
   return QCUR_OK;
 }
@@ -659,6 +675,7 @@ void qcur_destroy(qcur_ctx* ctx) {
   for (auto& kv : ctx->programs) cudaFree(kv.second.buf);
   if (ctx->arena.base) cudaFree(ctx->arena.base);
   cudaFree(ctx->status_dev);
+  cudaFree(ctx->counters);
   cudaFreeHost(ctx->status_host);
   delete ctx;
 }
@@ -929,9 +946,9 @@ int qcur_qgemm(qcur_ctx* ctx, int opA, int opB, int64_t M, int64_t N, int64_t K,
     // C = beta C
     GemmArgs z = g;
     z.Kq = 0;
-    launch_qgemm(z, ws, ctx->stream);
+    launch_qgemm(z, ws, ctx->counters, ctx->stream);
   } else {
-    launch_qgemm(g, ws, ctx->stream);
+    launch_qgemm(g, ws, ctx->counters, ctx->stream);
   }
   CK_LAUNCH(ctx, "qgemm");
   return QCUR_OK;
@@ -975,7 +992,7 @@ int qcur_synth_lowrank(qcur_ctx* ctx, int64_t m, int64_t n, int64_t k, uint64_t 
   GemmArgs g = gargs(m, n, k, P, k, 0, Q, k, 1, x_dev, n);  // S = P Q^H
   double* gws = ctx->take<double>(qgemm_workspace_bytes(g) / 8 + 16);
   if (!P || !Q || !parts || !ssq || !gws) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (synth)");
-  launch_qgemm(g, gws, ctx->stream);
+  launch_qgemm(g, gws, ctx->counters, ctx->stream);
   CK_LAUNCH(ctx, "synth gemm");
   if (noise > 0.0) {
     if (noise_relative) {
