@@ -22,6 +22,7 @@
 namespace qcur {
 
 constexpr int kMaxLevels = 8;
+constexpr int64_t kDrawSmemMaxLen = 24576;  // p (+ its tree) fits the 224 KB dynamic shared memory cap
 
 struct Levels {
   double* lev[kMaxLevels];
@@ -74,7 +75,18 @@ __global__ void __launch_bounds__(1024) k2_draw(DrawJobs jobs, unsigned* status)
   const DrawJob job = jobs.j[blockIdx.x];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int64_t len = job.len;
+  // The weights and the sum tree live in shared memory (a draw is a chain of
+  // dependent probes: ~30-cycle smem latency instead of ~600-cycle L2); for
+  // very long axes only the tree does and p stays in the global work buffer.
+  extern __shared__ double sm_draw[];
   Levels L = make_levels(job.work, len);
+  {
+    const bool p_in_smem = len <= kDrawSmemMaxLen;
+    double* base = p_in_smem ? sm_draw : sm_draw - len;  // tree always follows p's slot in smem
+    Levels S = make_levels(base, len);
+    if (!p_in_smem) S.lev[0] = job.work;
+    L = S;
+  }
   // copy p and count positives
   __shared__ int s_pos[32];
   int pos = 0;
@@ -192,9 +204,23 @@ __global__ void __launch_bounds__(1024) k2_draw(DrawJobs jobs, unsigned* status)
 
 void launch_draw(const DrawJob* jobs, int njobs, unsigned* status, cudaStream_t st) {
   DrawJobs j{};
-  for (int k = 0; k < njobs && k < 2; ++k) j.j[k] = jobs[k];
+  size_t smem = 0;
+  for (int k = 0; k < njobs && k < 2; ++k) {
+    j.j[k] = jobs[k];
+    const int64_t len = jobs[k].len;
+    const int64_t tree = draw_work_doubles(len) - len;  // levels >= 1 (+ slack)
+    const int64_t need = (len <= kDrawSmemMaxLen ? len : 0) + tree;
+    if ((size_t)need * sizeof(double) > smem) smem = (size_t)need * sizeof(double);
+  }
+  static bool attr = false;
+  if (!attr) {
+    // 227 KB minus the kernel's static shared memory (a failing attribute call
+    // would otherwise surface as the launch's error)
+    cudaFuncSetAttribute(k2_draw, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);
+    attr = true;
+  }
   ++::qcur::g_launches;
-  k2_draw<<<njobs, 1024, 0, st>>>(j, status);
+  k2_draw<<<njobs, 1024, smem, st>>>(j, status);
 }
 
 }  // namespace qcur

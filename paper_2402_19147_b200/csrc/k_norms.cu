@@ -132,22 +132,17 @@ __global__ void __launch_bounds__(kChunkThreads) pairwise_chunks(const double* _
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    const int p0 = pw.plan_prog_ptr[pid], p1 = pw.plan_prog_ptr[pid + 1];
-    double stack[24];
-    int sp = 0;
-    for (int p = p0; p < p1; ++p) {
-      const int op = pw.prog[p];
-      if (op >= 0) {
-        stack[sp++] = leafv[op];
-      } else {
-        const double b = stack[--sp];
-        const double a2 = stack[--sp];
-        stack[sp++] = __dadd_rn(a2, b);
-      }
-    }
-    out[seg * out_stride + chunk] = stack[0];
+  // combine the chunk's tree one level at a time (all threads), numpy's order
+  const int n0 = pw.plan_node_ptr[pid], l0 = pw.plan_lvl_ptr[pid], nl = pw.plan_lvl_ptr[pid + 1] - l0;
+  int prev = 0;
+  for (int h = 0; h < nl; ++h) {
+    const int end = pw.clvl[l0 + h];
+    for (int k = prev + threadIdx.x; k < end; k += blockDim.x)
+      leafv[nleaves + k] = __dadd_rn(leafv[pw.cnode_l[n0 + k]], leafv[pw.cnode_r[n0 + k]]);
+    prev = end;
+    __syncthreads();
   }
+  if (threadIdx.x == 0) out[seg * out_stride + chunk] = nl > 0 ? leafv[nleaves + prev - 1] : leafv[0];
 }
 
 // Top tree over chunk sums; one CTA per segment.  vals: [nseg][nchunks+nnodes]

@@ -20,6 +20,12 @@ struct DevPairwise {
   const int32_t* node_l;
   const int32_t* node_r;
   const int32_t* level_ptr;
+  // chunk trees level by level (ChunkPlan::node_l/node_r/lvl, concatenated over plans)
+  const int32_t* plan_node_ptr;
+  const int32_t* plan_lvl_ptr;
+  const int32_t* cnode_l;
+  const int32_t* cnode_r;
+  const int32_t* clvl;
 };
 
 // k_norms.cu

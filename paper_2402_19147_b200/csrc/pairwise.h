@@ -25,7 +25,50 @@ struct ChunkPlan {
   int32_t len = 0;
   std::vector<int32_t> leaf_off, leaf_len;
   std::vector<int32_t> prog;  // >= 0: push leaf value; -1: pop b, pop a, push a + b
+  // the same tree level by level: value slots [0, nleaves) are leaves, slot
+  // nleaves + k is node k; nodes of height h are [lvl[h-1], lvl[h]) (h >= 1)
+  std::vector<int32_t> node_l, node_r, lvl;
 };
+
+// Re-express a postfix program as (left, right) node pairs grouped by height,
+// so a CTA can combine one whole level in parallel.
+inline void levelize(ChunkPlan& p) {
+  const int32_t nleaves = (int32_t)p.leaf_off.size();
+  std::vector<int32_t> tl, tr, th;
+  std::vector<std::pair<int32_t, int32_t>> st;  // (slot: leaf >= 0, node -(k+1)), height
+  for (int32_t op : p.prog) {
+    if (op >= 0) {
+      st.push_back({op, 0});
+    } else {
+      auto b = st.back();
+      st.pop_back();
+      auto a = st.back();
+      st.pop_back();
+      const int32_t h = (a.second > b.second ? a.second : b.second) + 1;
+      tl.push_back(a.first);
+      tr.push_back(b.first);
+      th.push_back(h);
+      st.push_back({-(int32_t)tl.size(), h});
+    }
+  }
+  int32_t maxh = 0;
+  for (int32_t h : th) maxh = h > maxh ? h : maxh;
+  std::vector<int32_t> order, newpos(tl.size());
+  p.lvl.clear();
+  for (int32_t h = 1; h <= maxh; ++h) {
+    for (size_t k = 0; k < tl.size(); ++k)
+      if (th[k] == h) order.push_back((int32_t)k);
+    p.lvl.push_back((int32_t)order.size());
+  }
+  for (size_t q = 0; q < order.size(); ++q) newpos[order[q]] = (int32_t)q;
+  auto remap = [&](int32_t s) { return s >= 0 ? s : nleaves + newpos[-s - 1]; };
+  p.node_l.resize(order.size());
+  p.node_r.resize(order.size());
+  for (size_t q = 0; q < order.size(); ++q) {
+    p.node_l[q] = remap(tl[order[q]]);
+    p.node_r[q] = remap(tr[order[q]]);
+  }
+}
 
 struct PairwiseProgram {
   int64_t length = 0;
@@ -65,6 +108,7 @@ struct TopBuilder {
         ChunkPlan cp;
         cp.len = (int32_t)n;
         chunk_tree(0, n, cp);
+        levelize(cp);
         pid = (int32_t)pp->plans.size();
         pp->plans.push_back(std::move(cp));
         plan_of_len[n] = pid;

@@ -148,6 +148,7 @@ const DevProgram* qcur_ctx::program(int64_t length) {
   if (it != programs.end()) return &it->second;
   PairwiseProgram pp = compile_pairwise(length);
   std::vector<int32_t> plan_len, leaf_ptr{0}, prog_ptr{0}, leaf_off, leaf_len, prog;
+  std::vector<int32_t> node_ptr{0}, lvl_ptr{0}, cnode_l, cnode_r, clvl;
   int32_t maxc = 0;
   for (const ChunkPlan& cp : pp.plans) {
     plan_len.push_back(cp.len);
@@ -157,10 +158,16 @@ const DevProgram* qcur_ctx::program(int64_t length) {
     prog.insert(prog.end(), cp.prog.begin(), cp.prog.end());
     leaf_ptr.push_back((int32_t)leaf_off.size());
     prog_ptr.push_back((int32_t)prog.size());
+    cnode_l.insert(cnode_l.end(), cp.node_l.begin(), cp.node_l.end());
+    cnode_r.insert(cnode_r.end(), cp.node_r.begin(), cp.node_r.end());
+    clvl.insert(clvl.end(), cp.lvl.begin(), cp.lvl.end());
+    node_ptr.push_back((int32_t)cnode_l.size());
+    lvl_ptr.push_back((int32_t)clvl.size());
   }
   // pack: int64 chunk_off first, then the int32 arrays
-  std::vector<const std::vector<int32_t>*> arrs = {&pp.chunk_plan, &plan_len, &leaf_ptr, &prog_ptr, &leaf_off,
-                                                   &leaf_len,      &prog,     &pp.node_l, &pp.node_r, &pp.level_ptr};
+  std::vector<const std::vector<int32_t>*> arrs = {
+      &pp.chunk_plan, &plan_len, &leaf_ptr, &prog_ptr, &leaf_off, &leaf_len, &prog,    &pp.node_l,
+      &pp.node_r,     &pp.level_ptr, &node_ptr, &lvl_ptr, &cnode_l,  &cnode_r,  &clvl};
   size_t bytes = pp.chunk_off.size() * 8;
   std::vector<size_t> offs;
   for (auto* a : arrs) {
@@ -183,9 +190,10 @@ const DevProgram* qcur_ctx::program(int64_t length) {
   if (dp.d.nnodes == 0) dp.d.maxh = 0;
   dp.d.max_chunk_len = maxc;
   dp.d.chunk_off = (const int64_t*)b;
-  const int32_t** dst[] = {&dp.d.chunk_plan, &dp.d.plan_len, &dp.d.plan_leaf_ptr, &dp.d.plan_prog_ptr,
-                           &dp.d.leaf_off,   &dp.d.leaf_len, &dp.d.prog,          &dp.d.node_l,
-                           &dp.d.node_r,     &dp.d.level_ptr};
+  const int32_t** dst[] = {&dp.d.chunk_plan,    &dp.d.plan_len,     &dp.d.plan_leaf_ptr, &dp.d.plan_prog_ptr,
+                           &dp.d.leaf_off,      &dp.d.leaf_len,     &dp.d.prog,          &dp.d.node_l,
+                           &dp.d.node_r,        &dp.d.level_ptr,    &dp.d.plan_node_ptr, &dp.d.plan_lvl_ptr,
+                           &dp.d.cnode_l,       &dp.d.cnode_r,      &dp.d.clvl};
   for (size_t k = 0; k < arrs.size(); ++k) *dst[k] = (const int32_t*)(b + offs[k]);
   dp.scratch_len = (int64_t)dp.d.nchunks + dp.d.nnodes;
   return &(programs[length] = dp);
@@ -915,19 +923,11 @@ int qcur_pairwise_host(const double* data, int64_t n, double* out) {
       }
       leaf[l] = res;
     }
-    std::vector<double> stack;
-    for (int32_t op : cp.prog) {
-      if (op >= 0) {
-        stack.push_back(leaf[op]);
-      } else {
-        double b = stack.back();
-        stack.pop_back();
-        double a = stack.back();
-        stack.pop_back();
-        stack.push_back(a + b);
-      }
-    }
-    vals[ch] = stack.empty() ? 0.0 : stack[0];
+    // the level-by-level node form the device kernel executes
+    const size_t nl = leaf.size();
+    leaf.resize(nl + cp.node_l.size());
+    for (size_t k = 0; k < cp.node_l.size(); ++k) leaf[nl + k] = leaf[cp.node_l[k]] + leaf[cp.node_r[k]];
+    vals[ch] = cp.node_l.empty() ? (nl ? leaf[0] : 0.0) : leaf.back();
   }
   const size_t nch = pp.chunk_off.size();
   for (size_t k = 0; k < pp.node_l.size(); ++k) vals[nch + k] = vals[pp.node_l[k]] + vals[pp.node_r[k]];
