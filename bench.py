@@ -43,6 +43,10 @@ CONFIGS = {
     # configs[1]: 4000x4000, rank 50, noise 1e-3 relative to ||S||_F, length, c=r=200, seed 1  (the headline)
     "cfg2": dict(m=4000, n=4000, rank=50, noise=1e-3, relative=True, strategy="length", c=200, r=200,
                  plan_seed=1, gen_seed=20240229, batch=1),
+    # configs[2]: 2048x2048 image-like pure quaternion (30 separable cosine products per colour plane,
+    # quantised to 1/255, + N(0, 0.02^2)), length sampling, c=r in {64, 128, 256} (--c), PSNR reported
+    "cfg3": dict(m=2048, n=2048, rank=64, noise=0.02, relative=False, strategy="length", c=128, r=128,
+                 plan_seed=3, gen_seed=20240303, batch=1, image=True),
     # configs[3]: batch of 64 1024x1024, rank 20, 1e-4 relative noise, uniform, c=r=80, per-matrix seed b
     "cfg4": dict(m=1024, n=1024, rank=20, noise=1e-4, relative=True, strategy="uniform", c=80, r=80,
                  plan_seed=0, gen_seed=20240301, batch=64),
@@ -51,6 +55,10 @@ CONFIGS = {
 
 def workload_name(cfg_name: str, cfg: dict) -> str:
     b = f"{cfg['batch']} x " if cfg["batch"] > 1 else ""
+    if cfg.get("image"):
+        return (f"{cfg_name}: {cfg['m']}x{cfg['n']} image-like pure quaternion (30 separable cosine products per "
+                f"plane, quantised 1/255, + N(0, {cfg['noise']:g}^2)), {cfg['strategy']} sampling, c=r={cfg['c']}, "
+                f"plan seed {cfg['plan_seed']}")
     return (f"{cfg_name}: {b}{cfg['m']}x{cfg['n']} fp64 quaternion, rank {cfg['rank']} Gaussian factors + "
             f"{'relative ' if cfg['relative'] else ''}noise {cfg['noise']:g}, {cfg['strategy']} sampling, "
             f"c=r={cfg['c']}, plan seed {cfg['plan_seed']}")
@@ -159,6 +167,20 @@ def host_lowrank(cfg: dict, seed: int):
 
     m, n, k = cfg["m"], cfg["n"], cfg["rank"]
     g = np.random.default_rng(seed)
+    if cfg.get("image"):  # same recipe as qcur_synth_image (numpy RNG instead of Philox)
+        y, x = np.arange(m)[:, None] / m, np.arange(n)[None, :] / n
+        planes = [np.zeros((m, n))]
+        for _ in range(3):
+            v = np.zeros((m, n))
+            for _ in range(30):
+                f = sum(g.standard_normal() / (t + 1) * np.cos(2 * np.pi * (8 * g.random() * y) + 2 * np.pi * g.random())
+                        for t in range(3))
+                h = sum(g.standard_normal() / (t + 1) * np.cos(2 * np.pi * (8 * g.random() * x) + 2 * np.pi * g.random())
+                        for t in range(3))
+                v += f * h
+            v = (v - v.min()) / (v.max() - v.min())
+            planes.append(np.rint(255 * v) / 255 + cfg["noise"] * g.standard_normal((m, n)))
+        return tuple(planes)
     p = O.random_planes(g, m, k)
     q = O.random_planes(g, n, k)
     s = O.qmatmul(p, O.conj_t(q))
@@ -220,8 +242,11 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--c", type=int, default=None, help="override c = r (cfg3: 64, 128 or 256)")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.c:
+        cfg["c"] = cfg["r"] = args.c
     if args.impl == "reference":
         run_reference(args, args.config, cfg)
         return
@@ -246,14 +271,18 @@ def main() -> None:
     xs = []
     for b in range(batch):
         x = dev.empty_q(m, n)
-        dev.call("qcur_synth_lowrank", m, n, cfg["rank"], cfg["gen_seed"] + 1000 * b + 7919 * rank, cfg["noise"],
-                 1 if cfg["relative"] else 0, x.data_ptr())
+        if cfg.get("image"):
+            dev.call("qcur_synth_image", m, n, 30, cfg["gen_seed"] + 7919 * rank, cfg["noise"], x.data_ptr())
+        else:
+            dev.call("qcur_synth_lowrank", m, n, cfg["rank"], cfg["gen_seed"] + 1000 * b + 7919 * rank,
+                     cfg["noise"], 1 if cfg["relative"] else 0, x.data_ptr())
         xs.append(x)
     outs = DeviceApprox(m, n, c, r, dev)
+    psnr_scale = 255.0 if cfg.get("image") else 0.0
 
     def step():
         for b in range(batch):
-            outs.run(xs[b], cfg["strategy"], cfg["plan_seed"] + b)
+            outs.run(xs[b], cfg["strategy"], cfg["plan_seed"] + b, psnr_scale)
 
     stream = torch.cuda.current_stream()
     for _ in range(max(args.warmup, 3)):
@@ -388,6 +417,7 @@ def main() -> None:
                        "l2": "inputs larger than L2 (512 MB per matrix); no flush" if m * n * 32 > 126e6
                        else "input fits in L2; repeated on the same resident matrix"},
             "gpu_launches": launches, "rel_err": rel_err,
+            "psnr": (dict(zip(("u8_db", "float_peak1_db"), outs.psnr())) if psnr_scale else None),
             "roofline": roofline, "step_roofline": step_roof,
             "phases_ms_per_approx": per_approx, "phase_rates": extra_phase,
             "clocks": sampler.summary(), "e2e": e2e, "cpu_baseline": cpu,

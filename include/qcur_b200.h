@@ -93,15 +93,18 @@ int qcur_draw_indices(qcur_ctx* ctx, const double* probs_dev, int64_t size, int6
 int qcur_qmcur(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, const double* col_probs_dev,
                const double* row_probs_dev, int64_t num_cols, int64_t num_rows, const uint64_t state[4],
                int64_t* col_idx_dev, int64_t* row_idx_dev, double* c_dev, double* u_dev, double* r_dev);
-/* ||X - C U R||_F^2 and ||X||_F^2 without forming CUR (callers: cli.py:173-175,
- * bench.py:257-258, imaging.py:170-177).  out2_dev: 2 doubles on the device. */
+/* Error statistics of X - C U R without forming CUR (callers: cli.py:173-175,
+ * bench.py:257-258, imaging.py:170-177).  out4_dev (4 doubles, device):
+ *   [0] ||X - CUR||_F^2   [1] ||X||_F^2   [2] imaginary-part ||X - CUR||^2 (float PSNR)
+ *   [3] sum of squared differences of the u8 images qmat_to_image(s X) and
+ *       qmat_to_image(s CUR) (imaging.py:90-124; exact integers) when psnr_scale s > 0 */
 int qcur_cur_error(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, const double* c_dev, int64_t c,
-                   const double* u_dev, const double* r_dev, int64_t r, double* out2_dev);
+                   const double* u_dev, const double* r_dev, int64_t r, double psnr_scale, double* out4_dev);
 /* One whole approximation, device resident, no host synchronisation:
  * distributions (strategy) + draw + gather + pinv + U + fused error. */
 int qcur_approx(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int strategy, const uint64_t state[4],
                 int64_t num_cols, int64_t num_rows, int64_t* col_idx_dev, int64_t* row_idx_dev, double* c_dev,
-                double* u_dev, double* r_dev, double* err2_dev);
+                double* u_dev, double* r_dev, double psnr_scale, double* err4_dev);
 /* read back and clear the device status word; returns the mapped status code */
 int qcur_check(qcur_ctx* ctx);
 
@@ -120,6 +123,11 @@ int qcur_frobenius_sq(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, 
 int qcur_synth_lowrank(qcur_ctx* ctx, int64_t m, int64_t n, int64_t k, uint64_t seed, double noise,
                        int noise_relative, double* x_dev);
 double qcur_fp64_peak_tflops(qcur_ctx* ctx);
+/* cfg3 image-like pure quaternion matrix: each imaginary plane = sum of `nterms`
+ * separable products of random cosine series (frequencies U[0,8]), min-max to
+ * [0,1], quantised to 1/255, plus N(0, noise_std^2); real part 0. */
+int qcur_synth_image(qcur_ctx* ctx, int64_t m, int64_t n, int nterms, uint64_t seed, double noise_std,
+                     double* x_dev);
 
 /* ---- measurement hooks (bench.py) ------------------------------------------
  * qcur_profile(ctx, 1) records CUDA events on the context stream at the end of

@@ -178,6 +178,22 @@ def approx(planes, strategy: str, rank: int, seed: int, num_cols: int, num_rows:
                 rel_err=math.sqrt(e2) / math.sqrt(x2))
 
 
+def image_u8(planes, scale: float = 255.0):
+    """qmat_to_image(scale * X) (imaging.py:90-100): the three imaginary planes,
+    clipped to [0, 255] and rounded half to even."""
+    return [np.rint(np.clip(scale * p, 0.0, 255.0)).astype(np.uint8) for p in planes[1:]]
+
+
+def psnr_u8(ref_planes, test_planes, scale: float = 255.0) -> float:
+    """imaging.psnr (imaging.py:111-124) of the two decoded images."""
+    total = 0.0
+    for a, b in zip(image_u8(ref_planes, scale), image_u8(test_planes, scale)):
+        d = a.astype(np.float64) - b.astype(np.float64)
+        total += float(np.sum(d * d))
+    mse = total / (3 * ref_planes[0].shape[0] * ref_planes[0].shape[1])
+    return float("inf") if mse == 0.0 else 10.0 * math.log10(255.0 ** 2 / mse)
+
+
 def rel_fro(a, b) -> float:
     """||a - b||_F / ||b||_F for plane tuples."""
     return math.sqrt(frob2(tuple(x - y for x, y in zip(a, b)))) / math.sqrt(frob2(b))

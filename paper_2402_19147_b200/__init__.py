@@ -20,6 +20,7 @@ from .cur import (
     STRATEGIES,
     CURFactors,
     SamplingPlan,
+    cur_psnr,
     cur_reconstruct,
     cur_relative_error,
     default_sample_counts,
@@ -39,6 +40,6 @@ __all__ = [
     "QMatrix", "Quaternion", "qmat_matmul", "qmat_conj_transpose", "qmat_frobenius_norm",
     "STRATEGIES", "SamplingPlan", "CURFactors", "length_distributions", "uniform_distributions",
     "default_sample_counts", "make_plan", "draw_indices", "plan_indices", "qmcur", "cur_reconstruct",
-    "cur_relative_error", "qmcur_device", "pseudoinverse",
+    "cur_relative_error", "cur_psnr", "qmcur_device", "pseudoinverse",
 ]
 __version__ = "0.1.0"

@@ -43,7 +43,7 @@ EXPORTS = (
     "qcur_length_distributions", "qcur_uniform_distributions", "qcur_draw_indices", "qcur_qmcur",
     "qcur_cur_error", "qcur_approx", "qcur_check", "qcur_qgemm", "qcur_pseudoinverse",
     "qcur_frobenius_sq", "qcur_synth_lowrank", "qcur_fp64_peak_tflops",
-    "qcur_profile", "qcur_profile_read", "qcur_launch_count", "qcur_pairwise_host",
+    "qcur_profile", "qcur_profile_read", "qcur_launch_count", "qcur_pairwise_host", "qcur_synth_image",
 )
 
 _c_dp = ctypes.c_void_p
@@ -90,9 +90,10 @@ def load_library() -> ctypes.CDLL:
             "qcur_draw_indices": (ctypes.c_int, [_c_dp, _c_dp, _i64, _i64, _u64p, _c_dp]),
             "qcur_qmcur": (ctypes.c_int, [_c_dp, _c_dp, _i64, _i64, _c_dp, _c_dp, _i64, _i64, _u64p,
                                           _c_dp, _c_dp, _c_dp, _c_dp, _c_dp]),
-            "qcur_cur_error": (ctypes.c_int, [_c_dp, _c_dp, _i64, _i64, _c_dp, _i64, _c_dp, _c_dp, _i64, _c_dp]),
+            "qcur_cur_error": (ctypes.c_int, [_c_dp, _c_dp, _i64, _i64, _c_dp, _i64, _c_dp, _c_dp, _i64, ctypes.c_double,
+                                              _c_dp]),
             "qcur_approx": (ctypes.c_int, [_c_dp, _c_dp, _i64, _i64, ctypes.c_int, _u64p, _i64, _i64,
-                                           _c_dp, _c_dp, _c_dp, _c_dp, _c_dp, _c_dp]),
+                                           _c_dp, _c_dp, _c_dp, _c_dp, _c_dp, ctypes.c_double, _c_dp]),
             "qcur_check": (ctypes.c_int, [_c_dp]),
             "qcur_qgemm": (ctypes.c_int, [_c_dp, ctypes.c_int, ctypes.c_int, _i64, _i64, _i64, ctypes.c_double,
                                           _c_dp, _i64, _c_dp, _i64, ctypes.c_double, _c_dp, _i64]),
@@ -105,6 +106,8 @@ def load_library() -> ctypes.CDLL:
             "qcur_profile_read": (ctypes.c_int, [_c_dp, ctypes.c_char_p, ctypes.c_size_t]),
             "qcur_launch_count": (ctypes.c_ulonglong, []),
             "qcur_pairwise_host": (ctypes.c_int, [_c_dp, _i64, ctypes.POINTER(ctypes.c_double)]),
+            "qcur_synth_image": (ctypes.c_int, [_c_dp, _i64, _i64, ctypes.c_int, ctypes.c_uint64, ctypes.c_double,
+                                                _c_dp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)

@@ -31,7 +31,7 @@ namespace qcur {
 namespace {
 constexpr int kCl = 16;  // CTAs per cluster (non-portable size, supported on B200)
 constexpr int kThreads = 512;
-constexpr int kClusterQMax = 216;  // rows + inverse columns + 3 column buffers within 227 KB of smem
+constexpr int kClusterQMax = 304;  // compact triangles + 3 column buffers within 227 KB of smem
 
 __device__ __forceinline__ Quat ldQ(const double* p) { return *reinterpret_cast<const Quat*>(p); }
 __device__ __forceinline__ void stQ(double* p, const Quat& q) { *reinterpret_cast<Quat*>(p) = q; }
@@ -89,18 +89,25 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1) k_cho
   constexpr int kWarps = kThreads / 32;
   const int nown = (q - c + kCl - 1) / kCl;  // own rows i = c + 16 s  and own columns k = c + 16 u
   const int nmax = (q + kCl - 1) / kCl;      // identical layout in every CTA: DSMEM offsets must agree
+  // Fixed-offset region first (identical in every CTA: DSMEM targets), then the
+  // CTA's own triangles stored compactly: Gram row i = c + 16 s keeps k <= i
+  // (rowbase(s) + k), inverse column k = c + 16 u keeps i >= k (colbase(u) + i - k).
   extern __shared__ __align__(32) double sm[];
-  double* rows = sm;                             // [nmax][q] quaternions: Gram rows (lower part)
-  double* wcol = rows + (size_t)nmax * q * 4;    // [nmax][q] quaternions: inverse columns W_{:,k}
-  double* colbuf = wcol + (size_t)nmax * q * 4;  // [3][q] quaternions: columns of L in flight
+  double* colbuf = sm;                           // [3][q] quaternions: columns of L in flight
   double* diag = colbuf + 3 * (size_t)q * 4;     // [q] replicated running diagonal
   uint64_t* mbar = reinterpret_cast<uint64_t*>(diag + q + (q & 1));  // [3] one per column buffer
+  double* rows = reinterpret_cast<double*>(mbar + 4);
+  auto rowbase = [&](int s) -> size_t { return (size_t)s * (c + 1) + (size_t)8 * s * (s - 1); };
+  auto colbase = [&](int u) -> size_t { return (size_t)u * (q - c) - (size_t)8 * u * (u - 1); };
+  double* wcol = rows + rowbase(nown) * 4;
+  (void)nmax;
 
-  for (int t = tid; t < nown * q; t += kThreads) {
-    const int s = t / q, k = t - s * q;
-    const int i = c + kCl * s;  // own row i (Gram) and own column i (inverse), k runs along it
-    stQ(rows + (size_t)t * 4, k <= i ? ldQ(pr.G + ((size_t)i * q + k) * 4) : qzero());
-    stQ(wcol + (size_t)t * 4, Quat{k == i ? 1.0 : 0.0, 0.0, 0.0, 0.0});  // W = I
+  for (int s = 0; s < nown; ++s) {
+    const int i = c + kCl * s;
+    double* row = rows + rowbase(s) * 4;
+    for (int k = tid; k <= i; k += kThreads) stQ(row + (size_t)k * 4, ldQ(pr.G + ((size_t)i * q + k) * 4));
+    double* col = wcol + colbase(s) * 4;  // own column k = i
+    for (int r = i + tid; r < q; r += kThreads) stQ(col + (size_t)(r - i) * 4, Quat{r == i ? 1.0 : 0.0, 0.0, 0.0, 0.0});
   }
   for (int i = tid; i < q; i += kThreads) diag[i] = pr.G[((size_t)i * q + i) * 4];
   if (tid == 0) {
@@ -122,7 +129,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1) k_cho
       const int s = t / kCl, dst = t - s * kCl;
       const int i = c + kCl * s;
       if (i <= j) continue;
-      st_async_quat(mapa(cb_u + 32u * (unsigned)i, dst), qscale(ldQ(rows + ((size_t)s * q + j) * 4), inv),
+      st_async_quat(mapa(cb_u + 32u * (unsigned)i, dst), qscale(ldQ(rows + (rowbase(s) + j) * 4), inv),
                     mapa(mb_u, dst));
     }
     if (tid < kCl) mbar_arrive_remote(mapa(mb_u, tid));
@@ -142,7 +149,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1) k_cho
       for (int s = tid; s < nown; s += kThreads) {
         const int i = c + kCl * s;
         if (i <= j + 1) continue;
-        double* e = rows + ((size_t)s * q + j + 1) * 4;
+        double* e = rows + (rowbase(s) + j + 1) * 4;
         stQ(e, qsub(ldQ(e), qmul(ldQ(cb + (size_t)i * 4), qconj(lj1))));
       }
       if (tid == 0) diag[j + 1] = diag[j + 1] - qnorm2(lj1);
@@ -154,7 +161,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1) k_cho
       const int i = c + kCl * s;
       if (i <= j + 1) continue;
       const Quat lij = ldQ(cb + (size_t)i * 4);
-      double* row = rows + (size_t)s * q * 4;
+      double* row = rows + rowbase(s) * 4;
       int k = j + 2 + lane;
       for (; k + 32 <= i; k += 64) {  // two independent updates in flight
         const Quat a0 = ldQ(row + (size_t)k * 4), b0 = ldQ(cb + (size_t)k * 4);
@@ -168,7 +175,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1) k_cho
     for (int u = warp; u < nown; u += kWarps) {
       const int k = c + kCl * u;
       if (k > j) continue;
-      double* w = wcol + (size_t)u * q * 4;
+      double* w = wcol + colbase(u) * 4 - (size_t)k * 4;  // w + i*4 addresses W_ik (i >= k)
       const Quat xjk = qscale(ldQ(w + (size_t)j * 4), inv);
       if (lane == 0) stQ(w + (size_t)j * 4, xjk);
       int i = j + 1 + lane;
@@ -189,23 +196,35 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1) k_cho
     return;
   }
   // X_ik for own columns k (i >= k), zero above the diagonal
-  for (int t = tid; t < nown * q; t += kThreads) {
-    const int u = t / q, i = t - u * q;
+  for (int u = 0; u < nown; ++u) {
     const int k = c + kCl * u;
-    stQ(pr.X + ((size_t)i * q + k) * 4, i >= k ? ldQ(wcol + (size_t)t * 4) : qzero());
+    const double* w = wcol + colbase(u) * 4;
+    for (int i = tid; i < q; i += kThreads) stQ(pr.X + ((size_t)i * q + k) * 4, i >= k ? ldQ(w + (size_t)(i - k) * 4) : qzero());
   }
   cluster_barrier();
 }
 
 int chol_cluster_qmax() { return kClusterQMax; }
 
+// dynamic shared memory of the CTA with the largest triangles (rank 0)
+static size_t chol_cluster_smem(int64_t q) {
+  size_t best = 0;
+  for (int c = 0; c < kCl; ++c) {
+    const int64_t nown = (q - c + kCl - 1) / kCl;
+    const int64_t rows = nown * (c + 1) + 8 * nown * (nown - 1);
+    const int64_t cols = nown * (q - c) - 8 * nown * (nown - 1);
+    const size_t b = (size_t)(3 * q * 4 + q + (q & 1) + 4 + 4 * (rows + cols)) * sizeof(double);
+    best = b > best ? b : best;
+  }
+  return best;
+}
+
 void launch_chol_inv_cluster(const CholJob* jobs, int njobs, int64_t q, unsigned* status, cudaStream_t st) {
   CholProblems P{};
   for (int k = 0; k < njobs && k < 2; ++k) P.p[k] = jobs[k];
   P.q = q;
   P.status = status;
-  const int nmax = (int)((q + kCl - 1) / kCl);
-  const size_t smem = ((size_t)2 * nmax * q * 4 + 3 * (size_t)q * 4 + q + 16) * sizeof(double);
+  const size_t smem = chol_cluster_smem(q);
   static bool set = false;
   if (!set) {
     cudaFuncSetAttribute(k_chol_inv_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

@@ -100,6 +100,28 @@ __global__ void k_reduce_pairs(const double* __restrict__ parts, int64_t nparts,
   }
 }
 
+// Deterministic fixed-order column sums of a [nrows][width] table (width <= 8).
+__global__ void k_reduce_rows(const double* __restrict__ parts, int64_t nrows, int width, double* __restrict__ out) {
+  __shared__ double sh[8][256];
+  for (int c = 0; c < width; ++c) {
+    double a = 0.0;
+    for (int64_t t = threadIdx.x; t < nrows; t += blockDim.x) a += parts[t * width + c];
+    sh[c][threadIdx.x] = a;
+  }
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s)
+      for (int c = 0; c < width; ++c) sh[c][threadIdx.x] += sh[c][threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x < width) out[threadIdx.x] = sh[threadIdx.x][0];
+}
+
+void launch_reduce_rows(const double* parts, int64_t nrows, int width, double* out, cudaStream_t st) {
+  ++::qcur::g_launches;
+  k_reduce_rows<<<1, 256, 0, st>>>(parts, nrows, width, out);
+}
+
 void launch_planar_to_interleaved(const double* a0, const double* a1, const double* a2, const double* a3, int64_t m,
                                   int64_t n, double* X, cudaStream_t st) {
   ++::qcur::g_launches;

@@ -84,7 +84,8 @@ struct KParams {
   int64_t kchunk;      // quaternions of K per split
   const double* X;     // EPI_ERR: reference matrix
   int64_t ldx;
-  double* partials;    // EPI_ERR: [tiles][2]
+  double* partials;    // EPI_ERR: [tiles][4]
+  double psnr_scale;   // EPI_ERR: > 0 -> also the u8 image statistic at this scale (255)
   unsigned* counters;  // split-K: per-tile arrival tickets (zero between launches)
   int b_upper;         // op(B) is upper triangular: column j only needs k <= j
   int herm_lower;      // output is Hermitian and only its lower triangle is consumed
@@ -262,9 +263,14 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN, BKQ, STAGES, OPA, OPB, EPI
       }
     }
   } else {
-    __shared__ double red[2][CF::THREADS / 32];
+    // per tile: [0] sum (X - PR)^2, [1] sum X^2, [2] sum over the imaginary
+    // components of (X - PR)^2 (float PSNR), [3] sum of squared differences of
+    // the u8 images rint(clip(s X, 0, 255)) vs rint(clip(s PR, 0, 255)) over the
+    // imaginary components (imaging.py:90-124 semantics; integers, exact in fp64)
+    __shared__ double red[4][CF::THREADS / 32];
     const int64_t Nr = 4 * p.Nq;
-    double e = 0.0, xs = 0.0;
+    const double s = p.psnr_scale;
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
     for (int a = 0; a < CF::FM; ++a) {
       const int64_t gi = i0 + wm0 + 8 * a + arow;
@@ -273,30 +279,38 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN, BKQ, STAGES, OPA, OPB, EPI
         const int64_t gj = jr0 + wn0 + 8 * b + 2 * t;
         if (gi < p.Mq && gj < Nr) {
           const double2 x = __ldg(reinterpret_cast<const double2*>(p.X + gi * p.ldx * 4 + gj));
-          const double d0 = x.x - p.alpha * acc[a][b][0], d1 = x.y - p.alpha * acc[a][b][1];
-          e += d0 * d0;
-          e += d1 * d1;
-          xs += x.x * x.x;
-          xs += x.y * x.y;
+          const double r0 = p.alpha * acc[a][b][0], r1 = p.alpha * acc[a][b][1];
+          const double d0 = x.x - r0, d1 = x.y - r1;
+          v[0] += d0 * d0;
+          v[0] += d1 * d1;
+          v[1] += x.x * x.x;
+          v[1] += x.y * x.y;
+          const bool first_real = (gj & 3) == 0;  // (gj, gj+1) = components (0,1) or (2,3)
+          if (!first_real) v[2] += d0 * d0;
+          v[2] += d1 * d1;
+          if (s > 0.0) {
+            auto u8 = [&](double z) { return rint(fmin(fmax(s * z, 0.0), 255.0)); };
+            const double q1 = u8(x.y) - u8(r1);
+            v[3] += q1 * q1;
+            if (!first_real) {
+              const double q0 = u8(x.x) - u8(r0);
+              v[3] += q0 * q0;
+            }
+          }
         }
       }
     }
-    e = warp_sum(e);
-    xs = warp_sum(xs);
-    if (lane == 0) {
-      red[0][warp] = e;
-      red[1][warp] = xs;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[k] = warp_sum(v[k]);
+      if (lane == 0) red[k][warp] = v[k];
     }
     __syncthreads();
-    if (tid == 0) {
-      double se = 0.0, sx = 0.0;
-      for (int w = 0; w < CF::THREADS / 32; ++w) {
-        se += red[0][w];
-        sx += red[1][w];
-      }
+    if (tid < 4) {
+      double acc4 = 0.0;
+      for (int w = 0; w < CF::THREADS / 32; ++w) acc4 += red[tid][w];
       const int64_t tile = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
-      p.partials[2 * tile] = se;
-      p.partials[2 * tile + 1] = sx;
+      p.partials[4 * tile + tid] = acc4;
     }
   }
 }
@@ -403,7 +417,8 @@ void launch_qgemm(const GemmArgs& g, double* workspace, unsigned* counters, cuda
 int64_t err_partials_count(int64_t m, int64_t n) { return ((4 * n + 128 - 1) / 128) * ((m + 64 - 1) / 64); }
 
 void launch_cur_error(const double* X, int64_t ldx, const double* P, int64_t ldp, const double* R, int64_t ldr,
-                      int64_t m, int64_t n, int64_t r, double* partials, double* out2, cudaStream_t st) {
+                      int64_t m, int64_t n, int64_t r, double psnr_scale, double* partials, double* out4,
+                      cudaStream_t st) {
   KParams kp{};
   kp.Mq = m;
   kp.Nq = n;
@@ -417,9 +432,10 @@ void launch_cur_error(const double* X, int64_t ldx, const double* P, int64_t ldp
   kp.X = X;
   kp.ldx = ldx;
   kp.partials = partials;
+  kp.psnr_scale = psnr_scale;
   const int64_t gx = (4 * n + 128 - 1) / 128, gy = (m + 64 - 1) / 64;
   launch_t<64, 128, 8, 3, 0, 0, EPI_ERR>(kp, dim3((unsigned)gx, (unsigned)gy, 1), st);
-  launch_reduce_pairs(partials, gx * gy, out2, st);
+  launch_reduce_rows(partials, gx * gy, 4, out4, st);
 }
 
 }  // namespace qcur

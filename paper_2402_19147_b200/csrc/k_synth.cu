@@ -101,6 +101,125 @@ void launch_sumsq(const double* X, int64_t count, double* partials, int64_t npar
 }
 
 // ---------------------------------------------------------------------------
+// cfg3: synthetic colour-image-like pure quaternion matrix (BASELINE.json
+// configs[2]).  Plane p in {i, j, k} = sum_{l < L} f_{p,l}(y) g_{p,l}(x) with
+// random cosine series f(y) = sum_{t<3} a_t cos(2 pi w_t y / H + phi_t),
+// a_t ~ N(0,1)/(t+1), w_t ~ U[0, 8], phi_t ~ U[0, 2 pi) (same for g over x),
+// min-max mapped to [0, 1], quantised to multiples of 1/255, plus N(0, noise^2).
+// The real part is zero.  All randomness is Philox (seed, stream, counter).
+// ---------------------------------------------------------------------------
+constexpr int kImgTerms = 3;
+
+__device__ inline void uniform_pair(uint64_t seed, uint64_t stream, uint64_t idx, double& u0, double& u1) {
+  uint32_t c[4] = {(uint32_t)idx, (uint32_t)(idx >> 32), (uint32_t)stream, (uint32_t)(stream >> 32)};
+  philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+  u0 = (double)((((uint64_t)c[0] << 21) ^ c[1]) & ((1ull << 53) - 1)) * (1.0 / 9007199254740992.0);
+  u1 = (double)((((uint64_t)c[2] << 21) ^ c[3]) & ((1ull << 53) - 1)) * (1.0 / 9007199254740992.0);
+}
+
+// F[(p * L + l) * 2 + side][pos]: side 0 = f over rows (len m), side 1 = g over columns (len n)
+__global__ void k_img_series(double* __restrict__ F, int64_t m, int64_t n, int L, uint64_t seed) {
+  const int64_t maxlen = m > n ? m : n;
+  const int64_t total = 3LL * L * 2 * maxlen;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t fn = t / maxlen, pos = t - fn * maxlen;
+    const int side = (int)(fn & 1);
+    const int64_t len = side ? n : m;
+    if (pos >= len) continue;
+    double v = 0.0;
+    for (int k = 0; k < kImgTerms; ++k) {
+      double z0, z1, u0, u1;
+      normal_pair(seed, 100, (uint64_t)(fn * kImgTerms + k), z0, z1);
+      uniform_pair(seed, 101, (uint64_t)(fn * kImgTerms + k), u0, u1);
+      const double amp = z0 / (double)(k + 1), w = 8.0 * u0, phi = 2.0 * u1;  // phase in units of pi
+      v += amp * cospi(2.0 * w * (double)pos / (double)len + phi);
+    }
+    F[fn * maxlen + pos] = v;
+  }
+}
+
+// X(i, j) = (0, V_1, V_2, V_3), V_p = sum_l f_{p,l}(i) g_{p,l}(j)
+__global__ void k_img_compose(const double* __restrict__ F, int64_t m, int64_t n, int L, double* __restrict__ X) {
+  const int64_t maxlen = m > n ? m : n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m * n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / n, j = t - i * n;
+    double v[3];
+    for (int p = 0; p < 3; ++p) {
+      double s = 0.0;
+      for (int l = 0; l < L; ++l) {
+        const int64_t fn = (int64_t)(p * L + l) * 2;
+        s += F[fn * maxlen + i] * F[(fn + 1) * maxlen + j];
+      }
+      v[p] = s;
+    }
+    stq(X + t * 4, Quat{0.0, v[0], v[1], v[2]});
+  }
+}
+
+// per-block min / max of the three imaginary planes -> part[block][6]
+__global__ void k_img_minmax(const double* __restrict__ X, int64_t count, double* __restrict__ part) {
+  __shared__ double sh[6][256];
+  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x)
+    for (int p = 0; p < 3; ++p) {
+      const double v = X[t * 4 + 1 + p];
+      mn[p] = fmin(mn[p], v);
+      mx[p] = fmax(mx[p], v);
+    }
+  for (int p = 0; p < 3; ++p) {
+    sh[p][threadIdx.x] = mn[p];
+    sh[3 + p][threadIdx.x] = mx[p];
+  }
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s)
+      for (int p = 0; p < 3; ++p) {
+        sh[p][threadIdx.x] = fmin(sh[p][threadIdx.x], sh[p][threadIdx.x + s]);
+        sh[3 + p][threadIdx.x] = fmax(sh[3 + p][threadIdx.x], sh[3 + p][threadIdx.x + s]);
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x < 6) part[blockIdx.x * 6 + threadIdx.x] = sh[threadIdx.x][0];
+}
+
+// v <- rint(255 (v - min) / (max - min)) / 255 + noise N(0, sigma^2)
+__global__ void k_img_finish(double* __restrict__ X, int64_t count, const double* __restrict__ part, int nparts,
+                             uint64_t seed, double sigma) {
+  double mn[3], mx[3];
+  for (int p = 0; p < 3; ++p) {
+    mn[p] = INFINITY;
+    mx[p] = -INFINITY;
+    for (int b = 0; b < nparts; ++b) {
+      mn[p] = fmin(mn[p], part[b * 6 + p]);
+      mx[p] = fmax(mx[p], part[b * 6 + 3 + p]);
+    }
+  }
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x) {
+    double z[4];
+    normal_pair(seed, 102, (uint64_t)(2 * t), z[0], z[1]);
+    normal_pair(seed, 102, (uint64_t)(2 * t + 1), z[2], z[3]);
+    for (int p = 0; p < 3; ++p) {
+      const double span = mx[p] > mn[p] ? mx[p] - mn[p] : 1.0;
+      const double v = (X[t * 4 + 1 + p] - mn[p]) / span;
+      X[t * 4 + 1 + p] = rint(255.0 * v) / 255.0 + sigma * z[p];
+    }
+  }
+}
+
+void launch_synth_image(int64_t m, int64_t n, int L, uint64_t seed, double sigma, double* F, double* part,
+                        double* X, cudaStream_t st) {
+  const int nparts = 296;
+  ++::qcur::g_launches;
+  k_img_series<<<148 * 8, 256, 0, st>>>(F, m, n, L, seed);
+  ++::qcur::g_launches;
+  k_img_compose<<<148 * 8, 256, 0, st>>>(F, m, n, L, X);
+  ++::qcur::g_launches;
+  k_img_minmax<<<nparts, 256, 0, st>>>(X, m * n, part);
+  ++::qcur::g_launches;
+  k_img_finish<<<148 * 8, 256, 0, st>>>(X, m * n, part, nparts, seed, sigma);
+}
+
+// ---------------------------------------------------------------------------
 // FP64 DMMA peak probe (same instruction mix as the GEMM inner loop)
 // ---------------------------------------------------------------------------
 __global__ void k_dmma_probe(double* out, int iters) {

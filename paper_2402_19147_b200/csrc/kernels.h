@@ -60,6 +60,7 @@ void launch_gather_rows(const double* X, int64_t n, int64_t ldx, const int64_t* 
 void launch_conj_transpose(const double* A, int64_t m, int64_t n, int64_t lda, double* AH, int64_t ldah,
                            cudaStream_t st);
 void launch_reduce_pairs(const double* parts, int64_t nparts, double* out2, cudaStream_t st);
+void launch_reduce_rows(const double* parts, int64_t nrows, int width, double* out, cudaStream_t st);  // width <= 8
 
 // k_qgemm.cu : C(Mq x Nq) = alpha * op(A) * op(B) + beta * C, quaternion, interleaved.
 // op: 0 = N, 1 = H (conjugate transpose).  lda/ldb/ldc in quaternions.
@@ -80,10 +81,12 @@ struct GemmArgs {
 size_t qgemm_workspace_bytes(const GemmArgs& g);
 // counters: >= 65536 zero-initialised uints owned by the caller (split-K tickets)
 void launch_qgemm(const GemmArgs& g, double* workspace, unsigned* counters, cudaStream_t st);
-// ||X - P R||_F^2 and ||X||_F^2 partials, P: m x r, R: r x n, X: m x n (all interleaved)
-int64_t err_partials_count(int64_t m, int64_t n);
+// Fused error of X - P R (P: m x r, R: r x n, X: m x n, all interleaved).  out4 =
+// {||X-PR||^2, ||X||^2, imaginary part of ||X-PR||^2, u8-image squared-diff sum at psnr_scale}
+int64_t err_partials_count(int64_t m, int64_t n);  // tiles; the partial buffer needs 4 doubles per tile
 void launch_cur_error(const double* X, int64_t ldx, const double* P, int64_t ldp, const double* R, int64_t ldr,
-                      int64_t m, int64_t n, int64_t r, double* partials, double* out2, cudaStream_t st);
+                      int64_t m, int64_t n, int64_t r, double psnr_scale, double* partials, double* out4,
+                      cudaStream_t st);
 
 // k_dense.cu : small (q x q) dense factorizations, one CTA each.
 void launch_cholesky(double* G, int64_t q, int64_t ldg, unsigned* status, unsigned fail_bit, cudaStream_t st);
@@ -125,6 +128,9 @@ void launch_normal_fill(double* out, int64_t count, uint64_t seed, uint64_t stre
 void launch_add_scaled_noise(double* X, int64_t count, uint64_t seed, uint64_t stream, const double* ssq,
                              double rel, cudaStream_t st);
 void launch_sumsq(const double* X, int64_t count, double* partials, int64_t nparts, double* out, cudaStream_t st);
+// cfg3 image-like input; F: 6 L max(m,n) doubles, part: 296*6 doubles scratch
+void launch_synth_image(int64_t m, int64_t n, int L, uint64_t seed, double sigma, double* F, double* part,
+                        double* X, cudaStream_t st);
 
 // fp64 peak probe (bench roofline denominator)
 double run_dmma_peak(int sms, cudaStream_t st);

@@ -599,13 +599,13 @@ int qmcur_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, const doubl
 size_t error_ws_bytes(int64_t m, int64_t n, int64_t c, int64_t r) {
   (void)c;
   GemmArgs g = gargs(m, r, c, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0);
-  return qbytes(m, r) + (size_t)err_partials_count(m, n) * 16 + qgemm_workspace_bytes(g) + 4096;
+  return qbytes(m, r) + (size_t)err_partials_count(m, n) * 32 + qgemm_workspace_bytes(g) + 4096;
 }
 
 int error_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, const double* C, int64_t c, const double* U,
-               const double* R, int64_t r, double* out2) {
+               const double* R, int64_t r, double psnr_scale, double* out4) {
   double* P = ctx->take<double>((size_t)(m * r * 4));
-  double* parts = ctx->take<double>((size_t)err_partials_count(m, n) * 2);
+  double* parts = ctx->take<double>((size_t)err_partials_count(m, n) * 4);
   GemmArgs g = gargs(m, r, c, C, c, 0, U, r, 0, P, r);
   double* gws = ctx->take<double>(qgemm_workspace_bytes(g) / 8 + 16);
   if (!P || !parts || !gws) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (error)");
@@ -613,7 +613,7 @@ int error_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, const doubl
   // P = C U (m x r) (cur.py:274 left product), then the fused ||X - P R|| pass
   if ((rc = gemm(ctx, g, gws))) return rc;
   ctx->mark("cu");
-  launch_cur_error(X, n, P, r, R, n, m, n, r, parts, out2, ctx->stream);
+  launch_cur_error(X, n, P, r, R, n, m, n, r, psnr_scale, parts, out4, ctx->stream);
   ctx->mark("error");
   CK_LAUNCH(ctx, "cur_error");
   return QCUR_OK;
@@ -836,14 +836,15 @@ int qcur_qmcur(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, const d
 }
 
 int qcur_cur_error(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, const double* C, int64_t c,
-                   const double* U, const double* R, int64_t r, double* out2) {
+                   const double* U, const double* R, int64_t r, double psnr_scale, double* out4) {
   int rc = ctx->reserve(error_ws_bytes(m, n, c, r));
   if (rc) return rc;
-  return error_impl(ctx, x_dev, m, n, C, c, U, R, r, out2);
+  return error_impl(ctx, x_dev, m, n, C, c, U, R, r, psnr_scale, out4);
 }
 
 int qcur_approx(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int strategy, const uint64_t state[4],
-                int64_t c, int64_t r, int64_t* J, int64_t* I, double* C, double* U, double* R, double* err2) {
+                int64_t c, int64_t r, int64_t* J, int64_t* I, double* C, double* U, double* R, double psnr_scale,
+                double* err4) {
   if (m < 1 || n < 1 || c < 1 || r < 1 || c > n || r > m) return ctx->fail(QCUR_E_SHAPE, "qcur_approx: bad sizes");
   if (strategy != QCUR_STRATEGY_LENGTH && strategy != QCUR_STRATEGY_UNIFORM)
     return ctx->fail(QCUR_E_PARAMETER, "unknown strategy %d", strategy);
@@ -862,7 +863,7 @@ int qcur_approx(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int st
     ctx->mark("dists");
   }
   if ((rc = qmcur_impl(ctx, x_dev, m, n, colp, rowp, c, r, state, J, I, C, U, R))) return rc;
-  return error_impl(ctx, x_dev, m, n, C, c, U, R, r, err2);
+  return error_impl(ctx, x_dev, m, n, C, c, U, R, r, psnr_scale, err4);
 }
 
 int qcur_check(qcur_ctx* ctx) { return sync_status(ctx); }
@@ -1007,5 +1008,18 @@ int qcur_synth_lowrank(qcur_ctx* ctx, int64_t m, int64_t n, int64_t k, uint64_t 
 }
 
 double qcur_fp64_peak_tflops(qcur_ctx* ctx) { return run_dmma_peak(ctx->sms, ctx->stream); }
+
+int qcur_synth_image(qcur_ctx* ctx, int64_t m, int64_t n, int nterms, uint64_t seed, double noise_std,
+                     double* x_dev) {
+  if (m < 1 || n < 1 || nterms < 1) return ctx->fail(QCUR_E_PARAMETER, "synth_image: bad sizes");
+  const int64_t maxlen = m > n ? m : n;
+  int rc = ctx->reserve((size_t)(6 * nterms * maxlen + 296 * 6) * 8 + 4096);
+  if (rc) return rc;
+  double* F = ctx->take<double>((size_t)(6 * nterms * maxlen));
+  double* part = ctx->take<double>(296 * 6);
+  launch_synth_image(m, n, nterms, seed, noise_std, F, part, x_dev, ctx->stream);
+  CK_LAUNCH(ctx, "synth_image");
+  return QCUR_OK;
+}
 
 }  // extern "C"

@@ -44,6 +44,7 @@ __all__ = [
     "qmcur",
     "cur_reconstruct",
     "cur_relative_error",
+    "cur_psnr",
     "qmcur_device",
 ]
 
@@ -291,14 +292,48 @@ def cur_relative_error(x, factors: CURFactors) -> float:
     kc, kr = int(u.shape[0]), int(u.shape[1])
     if tuple(c.shape) != (m, kc) or tuple(r.shape) != (kr, n):
         raise ShapeError("factors do not match the matrix shape")
-    xd, dc, du, dr = to_device(x, dev), to_device(c, dev), to_device(u, dev), to_device(r, dev)
-    out2 = dev.empty(2)
-    dev.call("qcur_cur_error", xd.data_ptr(), m, n, dc.data_ptr(), kc, du.data_ptr(), dr.data_ptr(), kr,
-             out2.data_ptr())
-    e2, x2 = (float(v) for v in out2.cpu().numpy())
+    e2, x2, _, _ = _error_stats(x, factors, 0.0)
     if x2 == 0.0:
         raise ParameterError("reference matrix is zero; relative error undefined")
     return math.sqrt(e2) / math.sqrt(x2)
+
+
+def _error_stats(x, factors: CURFactors, psnr_scale: float) -> tuple[float, float, float, float]:
+    dev = _native.device()
+    m, n = (int(v) for v in x.shape)
+    c, u, r = factors.c, factors.u, factors.r
+    kc, kr = int(u.shape[0]), int(u.shape[1])
+    if tuple(c.shape) != (m, kc) or tuple(r.shape) != (kr, n):
+        raise ShapeError("factors do not match the matrix shape")
+    xd, dc, du, dr = to_device(x, dev), to_device(c, dev), to_device(u, dev), to_device(r, dev)
+    out4 = dev.empty(4)
+    dev.call("qcur_cur_error", xd.data_ptr(), m, n, dc.data_ptr(), kc, du.data_ptr(), dr.data_ptr(), kr,
+             float(psnr_scale), out4.data_ptr())
+    return tuple(float(v) for v in out4.cpu().numpy())
+
+
+def psnr_from_stats(u8_sq: float, imag_sq: float, m: int, n: int) -> tuple[float, float]:
+    """(u8 PSNR, float PSNR with peak 1) from the fused statistics.
+
+    u8: imaging.psnr (imaging.py:111-124) of qmat_to_image(s X) vs
+    qmat_to_image(s CUR): MSE pooled over the 3 channels, peak 255, +inf when
+    identical.  float: the same over the imaginary planes without quantisation."""
+    denom = 3.0 * m * n
+    mse = u8_sq / denom
+    p8 = float("inf") if mse == 0.0 else 10.0 * math.log10(255.0 ** 2 / mse)
+    msef = imag_sq / denom
+    pf = float("inf") if msef == 0.0 else 10.0 * math.log10(1.0 / msef)
+    return p8, pf
+
+
+def cur_psnr(x, factors: CURFactors, scale: float = 255.0) -> tuple[float, float]:
+    """PSNR of the CUR reconstruction of an image-like pure quaternion matrix,
+    fused on the GPU: (psnr(qmat_to_image(scale X), qmat_to_image(scale CUR)),
+    float PSNR at peak 1).  Mirrors imaging.psnr / qmat_to_image
+    (imaging.py:90-124) without materialising CUR or the images."""
+    _, _, imag_sq, u8_sq = _error_stats(x, factors, scale)
+    m, n = (int(v) for v in x.shape)
+    return psnr_from_stats(u8_sq, imag_sq, m, n)
 
 
 # ---------------------------------------------------------------------------
@@ -316,20 +351,28 @@ class DeviceApprox:
         self.C = d.empty_q(m, c)
         self.U = d.empty_q(c, r)
         self.R = d.empty_q(r, n)
-        self.err2 = d.empty(2)
+        self.err4 = d.empty(4)
 
-    def run(self, xd, strategy: str, seed: int) -> None:
+    def run(self, xd, strategy: str, seed: int, psnr_scale: float = 0.0) -> None:
         state = _native.state_from_seed(seed)
         self.dev.call("qcur_approx", xd.data_ptr(), self.m, self.n, _native.STRATEGY_CODES[_check_strategy(strategy)],
                       state.ctypes.data_as(_native._u64p), self.c, self.r, self.J.data_ptr(), self.I.data_ptr(),
-                      self.C.data_ptr(), self.U.data_ptr(), self.R.data_ptr(), self.err2.data_ptr())
+                      self.C.data_ptr(), self.U.data_ptr(), self.R.data_ptr(), float(psnr_scale),
+                      self.err4.data_ptr())
 
     def check(self) -> None:
         self.dev.call("qcur_check")
 
+    def stats(self) -> tuple[float, float, float, float]:
+        return tuple(float(v) for v in self.err4.cpu().numpy())
+
     def rel_error(self) -> float:
-        e2, x2 = (float(v) for v in self.err2.cpu().numpy())
+        e2, x2, _, _ = self.stats()
         return math.sqrt(e2) / math.sqrt(x2)
+
+    def psnr(self) -> tuple[float, float]:
+        _, _, imag_sq, u8_sq = self.stats()
+        return psnr_from_stats(u8_sq, imag_sq, self.m, self.n)
 
 
 def qmcur_device(xd, strategy: str, rank: int, seed: int, num_rows: int, num_cols: int) -> DeviceApprox:

@@ -177,3 +177,39 @@ def test_qmat_matmul_matches_oracle():
     got = a @ b
     want = O.qmatmul(tuple(a.planes), tuple(b.planes))
     assert O.rel_fro(tuple(got.planes), want) <= 1e-14
+
+
+def test_fused_psnr_matches_reference_semantics():
+    # image-like pure quaternion input in [0, 1] (quantised to 1/255 plus noise), as cfg3
+    g = np.random.default_rng(77)
+    m, n = 96, 80
+    y, x_ = np.arange(m)[:, None] / m, np.arange(n)[None, :] / n
+    planes = [np.zeros((m, n))]
+    for p in range(3):
+        v = sum(np.cos(2 * np.pi * (g.random() * 8 * y + g.random())) * np.cos(2 * np.pi * (g.random() * 8 * x_))
+                for _ in range(5))
+        v = (v - v.min()) / (v.max() - v.min())
+        planes.append(np.rint(255 * v) / 255 + 0.02 * g.standard_normal((m, n)))
+    x = q.QMatrix(*planes)
+    plan = q.make_plan(x, "length", 8, seed=3, num_rows=24, num_cols=24)
+    f = q.qmcur(x, plan)
+    p8, pf = q.cur_psnr(x, f)
+    rows, cols, c, u, r = oracle_factors(x, plan)
+    recon = O.qmatmul(O.qmatmul(c, u), r)
+    want8 = O.psnr_u8(tuple(planes), recon)
+    assert abs(p8 - want8) <= 1e-6 * want8, (p8, want8)
+    diff = sum(float(np.sum((a - b) ** 2)) for a, b in zip(planes[1:], recon[1:]))
+    wantf = 10 * math.log10(1.0 / (diff / (3 * m * n)))
+    assert abs(pf - wantf) <= 1e-9 * abs(wantf)
+
+
+def test_synth_image_is_image_like_and_deterministic():
+    dev = _native.device()
+    a = dev.empty_q(64, 48)
+    b = dev.empty_q(64, 48)
+    dev.call("qcur_synth_image", 64, 48, 30, 5, 0.02, a.data_ptr())
+    dev.call("qcur_synth_image", 64, 48, 30, 5, 0.02, b.data_ptr())
+    A = a.cpu().numpy()
+    assert np.array_equal(A, b.cpu().numpy())
+    assert np.all(A[..., 0] == 0.0)
+    assert -0.2 < A[..., 1:].min() < 0.1 and 0.9 < A[..., 1:].max() < 1.2

@@ -11,7 +11,7 @@ struct Q { double w, x, y, z; };
 static Q mul(Q a, Q b) { return {a.w*b.w-a.x*b.x-a.y*b.y-a.z*b.z, a.w*b.x+a.x*b.w+a.y*b.z-a.z*b.y, a.w*b.y-a.x*b.z+a.y*b.w+a.z*b.x, a.w*b.z+a.x*b.y-a.y*b.x+a.z*b.w}; }
 static Q cj(Q a) { return {a.w, -a.x, -a.y, -a.z}; }
 int main() {
-  for (int q : {4, 17, 40, 200, 216}) {
+  for (int q : {4, 17, 40, 200, 256, 300}) {
     int p = q + 30;
     std::vector<Q> Z(p * q), G(q * q);
     srand(q);
