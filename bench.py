@@ -47,6 +47,10 @@ CONFIGS = {
     # quantised to 1/255, + N(0, 0.02^2)), length sampling, c=r in {64, 128, 256} (--c), PSNR reported
     "cfg3": dict(m=2048, n=2048, rank=64, noise=0.02, relative=False, strategy="length", c=128, r=128,
                  plan_seed=3, gen_seed=20240303, batch=1, image=True),
+    # configs[4]: 32768x32768 (34.4 GB, generated on device), rank 200, 1e-3 relative noise, length,
+    # c=r=1000; the CPU oracle is not run (host RAM / hours)
+    "cfg5": dict(m=32768, n=32768, rank=200, noise=1e-3, relative=True, strategy="length", c=1000, r=1000,
+                 plan_seed=5, gen_seed=20240305, batch=1, no_cpu=True),
     # configs[3]: batch of 64 1024x1024, rank 20, 1e-4 relative noise, uniform, c=r=80, per-matrix seed b
     "cfg4": dict(m=1024, n=1024, rank=20, noise=1e-4, relative=True, strategy="uniform", c=80, r=80,
                  plan_seed=0, gen_seed=20240301, batch=64),
@@ -268,21 +272,27 @@ def main() -> None:
     dev = _native.device(local)
     m, n, c, r, batch = cfg["m"], cfg["n"], cfg["c"], cfg["r"], cfg["batch"]
     # --- inputs on the device (Philox + DMMA GEMM, deterministic) ---
+    # batch configs (cfg4) split the matrices across ranks (no collective, strong
+    # scaling); single-matrix configs run one replica per rank (weak scaling)
+    from paper_2402_19147_b200.sharding import shard_range
+
+    mine = list(shard_range(batch, world, rank)) if batch > 1 else [0]
     xs = []
-    for b in range(batch):
+    for b in mine:
         x = dev.empty_q(m, n)
         if cfg.get("image"):
             dev.call("qcur_synth_image", m, n, 30, cfg["gen_seed"] + 7919 * rank, cfg["noise"], x.data_ptr())
         else:
-            dev.call("qcur_synth_lowrank", m, n, cfg["rank"], cfg["gen_seed"] + 1000 * b + 7919 * rank,
-                     cfg["noise"], 1 if cfg["relative"] else 0, x.data_ptr())
+            seed_b = cfg["gen_seed"] + 1000 * b + (7919 * rank if batch == 1 else 0)
+            dev.call("qcur_synth_lowrank", m, n, cfg["rank"], seed_b, cfg["noise"], 1 if cfg["relative"] else 0,
+                     x.data_ptr())
         xs.append(x)
     outs = DeviceApprox(m, n, c, r, dev)
     psnr_scale = 255.0 if cfg.get("image") else 0.0
 
     def step():
-        for b in range(batch):
-            outs.run(xs[b], cfg["strategy"], cfg["plan_seed"] + b, psnr_scale)
+        for x, b in zip(xs, mine):
+            outs.run(x, cfg["strategy"], cfg["plan_seed"] + b, psnr_scale)
 
     stream = torch.cuda.current_stream()
     for _ in range(max(args.warmup, 3)):
@@ -314,7 +324,8 @@ def main() -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total = float(t.item())
     ms_step = ms_total / args.steps
-    value = world * args.steps * batch / (ms_total / 1e3)
+    # units completed by all ranks together / slowest rank's time
+    value = (args.steps * batch if batch > 1 else world * args.steps) / (ms_total / 1e3)
     rel_err = outs.rel_error()
 
     # --- phase breakdown (events between phases, same stream), separate pass ---
@@ -392,7 +403,10 @@ def main() -> None:
 
     # --- CPU baseline: the oracle port on this host (rank 0, N = 1) ---
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if cfg.get("no_cpu") and not args.no_cpu_baseline:
+        cpu = {"value": None, "unit": "approx/s", "cores": cpu_threads(), "kind": "port",
+               "sample": "not run: the oracle needs ~100 GB of host temporaries and hours for one 32768^2 approximation"}
+    elif rank == 0 and world == 1 and not args.no_cpu_baseline:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import oracle as O
 
@@ -408,13 +422,17 @@ def main() -> None:
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "approx/s", "n_gpus": world, "steps": args.steps,
-            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if batch > 1 else "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: on-device Philox Gaussian quaternion factors, S = P Q^H on DMMA, Gaussian noise",
             "config": {"workload": workload_name(args.config, cfg), "m": m, "n": n, "c": c, "r": r,
                        "strategy": cfg["strategy"], "batch": batch,
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                       "l2": "inputs larger than L2 (512 MB per matrix); no flush" if m * n * 32 > 126e6
+                       "parallelism": ("single GPU" if world == 1 else
+                                       (f"batch split by matrix over {world} GPUs" if batch > 1
+                                        else f"replicas x{world}")),
+                       "l2": f"inputs larger than L2 ({m * n * 32 / 1e6:.0f} MB per matrix); no flush"
+                       if m * n * 32 > 126e6
                        else "input fits in L2; repeated on the same resident matrix"},
             "gpu_launches": launches, "rel_err": rel_err,
             "psnr": (dict(zip(("u8_db", "float_peak1_db"), outs.psnr())) if psnr_scale else None),

@@ -288,6 +288,8 @@ size_t factor_ws_bytes(int64_t p, int64_t q) {
   g.Kq = p;
   size_t w2 = qgemm_workspace_bytes(g);
   b += (w1 > w2 ? w1 : w2) + 4096;
+  if (q > 304)  // blocked Cholesky scratch (chol_inv_blocked): A, L, blocks, T and its GEMM slabs
+    b += 2 * qbytes(q, q) + 2 * qbytes(256, 256) + qbytes(256, q) + (size_t)16 * q * q * 8 + 8192;
   return b + 16 * 256;
 }
 
@@ -321,6 +323,70 @@ GemmArgs with_flags(GemmArgs g, int b_upper, int herm_lower) {
   g.b_upper = b_upper;
   g.herm_lower = herm_lower;
   return g;
+}
+
+// Blocked Cholesky + inverse for Grams larger than one cluster holds (q > 304,
+// e.g. cfg5's c = r = 1000).  Diagonal blocks of kBlk run on the 16-CTA cluster
+// kernel; panels L_ik = A_ik X_kk^H and trailing updates A -= L_p L_p^H run on
+// the DMMA GEMM; X = L^{-1} follows by block forward substitution
+// X_i,0:i = -X_ii (L_i,0:i X_0:i,0:i).  G is read only; X (q x q) receives L^{-1}.
+constexpr int64_t kBlk = 256;
+
+size_t chol_blocked_ws_bytes(int64_t q) {
+  GemmArgs g = gargs(q, q, kBlk, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0);
+  GemmArgs g2 = gargs(kBlk, q, q, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0);
+  size_t w1 = qgemm_workspace_bytes(g), w2 = qgemm_workspace_bytes(g2);
+  return 2 * qbytes(q, q) + 2 * qbytes(kBlk, kBlk) + qbytes(kBlk, q) + (w1 > w2 ? w1 : w2) + 8 * 256;
+}
+
+int chol_inv_blocked(qcur_ctx* ctx, const double* G, int64_t q, double* X, unsigned fail_bit) {
+  cudaStream_t st = ctx->stream;
+  double* A = ctx->take<double>((size_t)(q * q * 4));
+  double* L = ctx->take<double>((size_t)(q * q * 4));
+  double* D = ctx->take<double>((size_t)(kBlk * kBlk * 4));
+  double* Xb = ctx->take<double>((size_t)(kBlk * kBlk * 4));
+  double* T = ctx->take<double>((size_t)(kBlk * q * 4));
+  GemmArgs g = gargs(q, q, kBlk, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0);
+  GemmArgs g2 = gargs(kBlk, q, q, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0);
+  size_t w1 = qgemm_workspace_bytes(g), w2 = qgemm_workspace_bytes(g2);
+  double* gws = ctx->take<double>((w1 > w2 ? w1 : w2) / 8 + 16);
+  if (!A || !L || !D || !Xb || !T || !gws) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (blocked cholesky)");
+  const size_t row = (size_t)q * 32, qb = 32;
+  cudaMemcpyAsync(A, G, (size_t)qbytes(q, q), cudaMemcpyDeviceToDevice, st);
+  cudaMemsetAsync(X, 0, (size_t)qbytes(q, q), st);
+  cudaMemsetAsync(L, 0, (size_t)qbytes(q, q), st);
+  int rc;
+  const int64_t nb = (q + kBlk - 1) / kBlk;
+  for (int64_t k = 0; k < nb; ++k) {
+    const int64_t kb = k * kBlk, bs = (q - kb) < kBlk ? (q - kb) : kBlk, rem = q - kb - bs;
+    cudaMemcpy2DAsync(D, bs * qb, A + (kb * q + kb) * 4, row, bs * qb, bs, cudaMemcpyDeviceToDevice, st);
+    CholJob job{D, nullptr, Xb, fail_bit};
+    launch_chol_inv_cluster(&job, 1, bs, ctx->status_dev, st);
+    cudaMemcpy2DAsync(X + (kb * q + kb) * 4, row, Xb, bs * qb, bs * qb, bs, cudaMemcpyDeviceToDevice, st);
+    CK_LAUNCH(ctx, "blocked cholesky diag");
+    if (rem == 0) break;
+    double* Lp = L + ((kb + bs) * q + kb) * 4;
+    // panel L_ik = A_ik X_kk^H  (op(B) upper triangular)
+    if ((rc = gemm(ctx, with_flags(gargs(rem, bs, bs, A + ((kb + bs) * q + kb) * 4, q, 0, Xb, bs, 1, Lp, q), 1, 0),
+                   gws)))
+      return rc;
+    // trailing A_jj -= L_p L_p^H (lower triangle only)
+    if ((rc = gemm(ctx,
+                   with_flags(gargs(rem, rem, bs, Lp, q, 0, Lp, q, 1, A + ((kb + bs) * q + kb + bs) * 4, q, -1.0, 1.0),
+                              0, 1),
+                   gws)))
+      return rc;
+  }
+  for (int64_t i = 1; i < nb; ++i) {
+    const int64_t ib = i * kBlk, bs = (q - ib) < kBlk ? (q - ib) : kBlk;
+    // T = L_i,0:i X_0:i,0:i   (bs x ib)
+    if ((rc = gemm(ctx, gargs(bs, ib, ib, L + ib * q * 4, q, 0, X, q, 0, T, ib), gws))) return rc;
+    // X_i,0:i = -X_ii T
+    if ((rc = gemm(ctx, gargs(bs, ib, bs, X + (ib * q + ib) * 4, q, 0, T, ib, 0, X + ib * q * 4, q, -1.0, 0.0), gws)))
+      return rc;
+  }
+  (void)row;
+  return QCUR_OK;
 }
 
 struct FactorSpec {
@@ -395,9 +461,9 @@ int factor_multi(qcur_ctx* ctx, const FactorSpec* specs, int ns) {
           CholJob j1{G, L, Li, specs[k].fail_bit};
           launch_chol_inv_cluster(&j1, 1, q, status, st);
         } else {
-          cudaMemcpyAsync(L, G, (size_t)qbytes(q, q), cudaMemcpyDeviceToDevice, st);
-          launch_cholesky(L, q, q, status, specs[k].fail_bit, st);
-          launch_tri_inverse_lower(L, q, q, Li, q, st);
+          (void)L;
+          const int rcb = chol_inv_blocked(ctx, G, q, Li, specs[k].fail_bit);
+          if (rcb) return rcb;
         }
       }
     }

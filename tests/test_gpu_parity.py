@@ -213,3 +213,28 @@ def test_synth_image_is_image_like_and_deterministic():
     assert np.array_equal(A, b.cpu().numpy())
     assert np.all(A[..., 0] == 0.0)
     assert -0.2 < A[..., 1:].min() < 0.1 and 0.9 < A[..., 1:].max() < 1.2
+
+
+@pytest.mark.slow
+def test_pseudoinverse_blocked_cholesky_q400():
+    # q = 400 > one cluster: blocked Cholesky (cluster diagonal blocks + DMMA panels)
+    a = rand_mat(700, 400, seed=5)
+    got = q.pseudoinverse(a)
+    assert O.rel_fro(tuple(got.planes), O.pinv(tuple(a.planes))) <= 1e-10
+
+
+@pytest.mark.slow
+def test_qmcur_large_counts_blocked_path():
+    x = lowrank(1300, 1100, 60, seed=8, noise=1e-3)
+    plan = q.make_plan(x, "length", 60, 8, num_rows=330, num_cols=320)
+    f = q.qmcur(x, plan)
+    check_against_oracle(x, plan, f)
+
+
+def test_draw_long_axis_global_memory_path():
+    # axes longer than 24576 keep p in global memory (cfg5: n = 32768)
+    p = np.random.default_rng(4).random(30000) ** 2
+    p /= p.sum()
+    got = q.draw_indices(p, 60, 17)
+    want = O.draw_indices(p, 60, np.random.default_rng(17))
+    assert np.array_equal(got, want)
