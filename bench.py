@@ -237,6 +237,69 @@ def run_reference(args, cfg_name: str, cfg: dict) -> None:
     print(json.dumps(line), flush=True)
 
 
+def run_rowshard(args, cfg_name: str, cfg: dict, world: int, rank: int, local: int) -> None:
+    """One matrix sharded by row blocks across the ranks (cfg5 design):
+    each rank generates and keeps its own rows; NCCL collectives carry the
+    column-norm chain, subtree totals, R rows, Gram / M all-reduces and error
+    partials (paper_2402_19147_b200/rowshard.py).  Strong scaling: one whole
+    approximation per step, whatever the number of GPUs."""
+    import torch
+
+    from paper_2402_19147_b200 import _native
+    from paper_2402_19147_b200.rowshard import Comm, GpuOps, SingleComm, approx_rowsharded
+    from paper_2402_19147_b200.sharding import max_over_ranks
+
+    dev = _native.device(local)
+    m, n, c, r = cfg["m"], cfg["n"], cfg["c"], cfg["r"]
+    rows_b = m // world
+    xb = dev.empty_q(rows_b, n)
+    dev.call("qcur_synth_lowrank_rows", m, n, cfg["rank"], cfg["gen_seed"], cfg["noise"], rank * rows_b, rows_b,
+             xb.data_ptr())
+    comm = Comm() if world > 1 else SingleComm()
+    ops = GpuOps(dev)
+    res = None
+    for _ in range(max(args.warmup, 3)):
+        res = approx_rowsharded(ops, comm, xb, m, cfg["strategy"], cfg["plan_seed"], c, r)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = dev.launches()
+    with sampler:
+        e0.record(stream)
+        for _ in range(args.steps):
+            res = approx_rowsharded(ops, comm, xb, m, cfg["strategy"], cfg["plan_seed"], c, r)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms_total = max_over_ranks(e0.elapsed_time(e1), device=f"cuda:{local}")
+    launches = dev.launches() - l0
+    ms_step = ms_total / args.steps
+    counts = alg_counts(cfg)
+    peak_tf = dev.lib.qcur_fp64_peak_tflops(dev.handle)
+    achieved = counts["flop"] / (ms_step * 1e-3) / 1e12
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": 1e3 / ms_step, "unit": "approx/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: each rank generates its row block on device (Philox, S = P Q^H on DMMA, noise "
+                    "relative to the analytic ||S||_F)",
+            "config": {"workload": workload_name(cfg_name, cfg) + " [row-block sharded]", "m": m, "n": n, "c": c,
+                       "r": r, "parallelism": f"row blocks of {rows_b} rows x {world} GPUs (NCCL collectives)",
+                       "l2": "inputs larger than L2; no flush"},
+            "gpu_launches": launches, "rel_err": res["rel_err"],
+            "roofline": {"kernel": "whole sharded step (all FP64 GEMMs)", "bound": "tensor",
+                         "achieved": achieved / world, "peak": peak_tf, "unit": "TFLOP/s",
+                         "frac": achieved / world / peak_tf, "traffic": None,
+                         "peak_source": "FP64 DMMA peak measured live (per GPU)"},
+            "clocks": sampler.summary(),
+            "e2e": None, "e2e_note": "row-sharded inputs are generated on device per rank; no host path",
+            "cpu_baseline": {"value": None, "unit": "approx/s", "cores": cpu_threads(), "kind": "port",
+                             "sample": "not run: the oracle cannot hold a 32768^2 matrix's temporaries"},
+        }
+        print(json.dumps(line), flush=True)
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -247,6 +310,8 @@ def main() -> None:
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--c", type=int, default=None, help="override c = r (cfg3: 64, 128 or 256)")
+    ap.add_argument("--rowshard", action="store_true",
+                    help="shard one matrix by row blocks across the ranks (cfg5 design) instead of replicas")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.c:
@@ -264,6 +329,11 @@ def main() -> None:
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    if args.rowshard:
+        run_rowshard(args, args.config, cfg, world, rank, local)
+        if world > 1:
+            dist.destroy_process_group()
+        return
 
     from paper_2402_19147_b200 import _native
     from paper_2402_19147_b200.cur import DeviceApprox, cur_relative_error, make_plan, qmcur

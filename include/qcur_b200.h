@@ -123,11 +123,42 @@ int qcur_frobenius_sq(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, 
 int qcur_synth_lowrank(qcur_ctx* ctx, int64_t m, int64_t n, int64_t k, uint64_t seed, double noise,
                        int noise_relative, double* x_dev);
 double qcur_fp64_peak_tflops(qcur_ctx* ctx);
+/* Rows [row0, row0+rows) of the m x n matrix P Q^H + N with noise std
+ * noise * sqrt(4k) (relative to the analytic E||S||_F^2 = 16 k m n), so every
+ * rank of a row-sharded run generates exactly its block of the same matrix. */
+int qcur_synth_lowrank_rows(qcur_ctx* ctx, int64_t m, int64_t n, int64_t k, uint64_t seed, double noise,
+                            int64_t row0, int64_t rows, double* x_dev);
 /* cfg3 image-like pure quaternion matrix: each imaginary plane = sum of `nterms`
  * separable products of random cosine series (frequencies U[0,8]), min-max to
  * [0,1], quantised to 1/255, plus N(0, noise_std^2); real part 0. */
 int qcur_synth_image(qcur_ctx* ctx, int64_t m, int64_t n, int nterms, uint64_t seed, double noise_std,
                      double* x_dev);
+
+/* ---- phase-level entry points for the row-block sharded path ------------------
+ * Used by paper_2402_19147_b200/rowshard.py, which interleaves them with NCCL
+ * collectives.  All asynchronous on the context stream; failures
+ * of the fast factorisation raise the status bit read back by qcur_check() /
+ * qcur_last_info() (QCUR_INFO_ROBUST_C). */
+/* sq of a row block and numpy's sequential column sums continued from acc_in (nullable) */
+int qcur_colsums_seq(qcur_ctx* ctx, const double* x_dev, int64_t rows, int64_t n, const double* acc_in_dev,
+                     double* colsum_out_dev, double* sq_out_dev);
+/* numpy pairwise sums of nseg segments of `length` doubles (stride apart) */
+int qcur_pairwise_sums(qcur_ctx* ctx, const double* data_dev, int64_t nseg, int64_t stride, int64_t length,
+                       double* out_dev);
+int qcur_vec_div(qcur_ctx* ctx, const double* in_dev, int64_t len, const double* denom_dev, double* out_dev);
+int qcur_gather_cols(qcur_ctx* ctx, const double* x_dev, int64_t rows, int64_t n, const int64_t* J_dev, int64_t c,
+                     double* out_dev);
+int qcur_gather_rows(qcur_ctx* ctx, const double* x_dev, int64_t n, const int64_t* I_dev, int64_t r, double* out_dev);
+/* qgemm with structure flags: 1 = op(B) upper triangular, 2 = Hermitian output (lower triangle only) */
+int qcur_qgemm_ex(qcur_ctx* ctx, int opA, int opB, int64_t M, int64_t N, int64_t K, double alpha, const double* a_dev,
+                  int64_t lda, const double* b_dev, int64_t ldb, double beta, double* c_dev, int64_t ldc, int flags);
+/* X = L^{-1} for G = L L^H (cluster kernel, or blocked for q > 304) */
+int qcur_chol_inv(qcur_ctx* ctx, const double* g_dev, int64_t q, double* x_dev);
+/* second CholeskyQR pass: L2^{-1} of G2 = I + E by series */
+int qcur_series_l2inv(qcur_ctx* ctx, const double* g2_dev, int64_t q, double* l2inv_dev);
+int qcur_kappa_check(qcur_ctx* ctx, const double* g1_dev, const double* f_dev, int64_t q);
+/* local factorisation of a tall block Z = src (zh=0) or src^H (zh=1): pinv(Z) = F Q^H */
+int qcur_factor(qcur_ctx* ctx, const double* src_dev, int zh, int64_t p, int64_t q, double* q_dev, double* f_dev);
 
 /* ---- measurement hooks (bench.py) ------------------------------------------
  * qcur_profile(ctx, 1) records CUDA events on the context stream at the end of

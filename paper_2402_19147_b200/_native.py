@@ -44,6 +44,9 @@ EXPORTS = (
     "qcur_cur_error", "qcur_approx", "qcur_check", "qcur_qgemm", "qcur_pseudoinverse",
     "qcur_frobenius_sq", "qcur_synth_lowrank", "qcur_fp64_peak_tflops",
     "qcur_profile", "qcur_profile_read", "qcur_launch_count", "qcur_pairwise_host", "qcur_synth_image",
+    "qcur_colsums_seq", "qcur_pairwise_sums", "qcur_vec_div", "qcur_gather_cols", "qcur_gather_rows",
+    "qcur_qgemm_ex", "qcur_chol_inv", "qcur_series_l2inv", "qcur_kappa_check", "qcur_factor",
+    "qcur_synth_lowrank_rows",
 )
 
 _c_dp = ctypes.c_void_p
@@ -108,6 +111,19 @@ def load_library() -> ctypes.CDLL:
             "qcur_pairwise_host": (ctypes.c_int, [_c_dp, _i64, ctypes.POINTER(ctypes.c_double)]),
             "qcur_synth_image": (ctypes.c_int, [_c_dp, _i64, _i64, ctypes.c_int, ctypes.c_uint64, ctypes.c_double,
                                                 _c_dp]),
+            "qcur_colsums_seq": (ctypes.c_int, [_c_dp, _c_dp, _i64, _i64, _c_dp, _c_dp, _c_dp]),
+            "qcur_pairwise_sums": (ctypes.c_int, [_c_dp, _c_dp, _i64, _i64, _i64, _c_dp]),
+            "qcur_vec_div": (ctypes.c_int, [_c_dp, _c_dp, _i64, _c_dp, _c_dp]),
+            "qcur_gather_cols": (ctypes.c_int, [_c_dp, _c_dp, _i64, _i64, _c_dp, _i64, _c_dp]),
+            "qcur_gather_rows": (ctypes.c_int, [_c_dp, _c_dp, _i64, _c_dp, _i64, _c_dp]),
+            "qcur_qgemm_ex": (ctypes.c_int, [_c_dp, ctypes.c_int, ctypes.c_int, _i64, _i64, _i64, ctypes.c_double,
+                                             _c_dp, _i64, _c_dp, _i64, ctypes.c_double, _c_dp, _i64, ctypes.c_int]),
+            "qcur_chol_inv": (ctypes.c_int, [_c_dp, _c_dp, _i64, _c_dp]),
+            "qcur_series_l2inv": (ctypes.c_int, [_c_dp, _c_dp, _i64, _c_dp]),
+            "qcur_kappa_check": (ctypes.c_int, [_c_dp, _c_dp, _c_dp, _i64]),
+            "qcur_factor": (ctypes.c_int, [_c_dp, _c_dp, ctypes.c_int, _i64, _i64, _c_dp, _c_dp]),
+            "qcur_synth_lowrank_rows": (ctypes.c_int, [_c_dp, _i64, _i64, _i64, ctypes.c_uint64, ctypes.c_double,
+                                                       _i64, _i64, _c_dp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)

@@ -26,9 +26,12 @@ constexpr int kStripW = 32;   // quaternion columns per CTA (one warp lane each)
 constexpr int kStripRB = 64;  // rows per pipeline stage (8 quaternions in flight per thread)
 constexpr int kStripThreads = 256;
 
+// acc_in (nullable): running column sums of the rows above this block, so a
+// row-sharded matrix continues numpy's sequential axis-0 order across ranks.
 __global__ void __launch_bounds__(kStripThreads) k1_colstrip(const double* __restrict__ X, int64_t m, int64_t n,
                                                              int64_t ldx, double* __restrict__ sq,
-                                                             double* __restrict__ colsum) {
+                                                             double* __restrict__ colsum,
+                                                             const double* __restrict__ acc_in) {
   __shared__ double sqs[2][kStripRB][kStripW];
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -47,7 +50,8 @@ __global__ void __launch_bounds__(kStripThreads) k1_colstrip(const double* __res
         buf[k] = qzero();
     }
   };
-  double acc = 0.0;  // numpy starts from the first row; 0 + sq[0] == sq[0] exactly (sq >= 0)
+  // numpy starts from the first row; 0 + sq[0] == sq[0] exactly (sq >= 0)
+  double acc = (acc_in != nullptr && jok) ? acc_in[j] : 0.0;
   const int64_t nstages = (m + kStripRB - 1) / kStripRB;
   load_stage(0);
   for (int64_t s = 0; s < nstages; ++s) {
@@ -176,10 +180,10 @@ __global__ void k_fill(double* __restrict__ out, int64_t len, double v) {
 // host launchers
 // ---------------------------------------------------------------------------
 void launch_colstrip(const double* X, int64_t m, int64_t n, int64_t ldx, double* sq, double* colsum,
-                     cudaStream_t st) {
+                     cudaStream_t st, const double* acc_in) {
   dim3 grid((unsigned)((n + kStripW - 1) / kStripW));
   ++::qcur::g_launches;
-  k1_colstrip<<<grid, kStripThreads, 0, st>>>(X, m, n, ldx, sq, colsum);
+  k1_colstrip<<<grid, kStripThreads, 0, st>>>(X, m, n, ldx, sq, colsum, acc_in);
 }
 
 void launch_pairwise(const double* data, int64_t nseg, int64_t seg_stride, const DevPairwise& pw, double* scratch,

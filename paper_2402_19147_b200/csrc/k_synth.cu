@@ -46,24 +46,27 @@ __device__ inline void normal_pair(uint64_t seed, uint64_t stream, uint64_t idx,
   z1 = rad * s;
 }
 
-__global__ void k_normal_fill(double* __restrict__ out, int64_t count, uint64_t seed, uint64_t stream, double scale) {
+// `pair0` = first Philox counter (element offset / 2): any row block of a larger
+// matrix draws exactly the values the whole-matrix generation would.
+__global__ void k_normal_fill(double* __restrict__ out, int64_t count, uint64_t seed, uint64_t stream, double scale,
+                              uint64_t pair0) {
   const int64_t pairs = (count + 1) / 2;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < pairs; t += (int64_t)gridDim.x * blockDim.x) {
     double z0, z1;
-    normal_pair(seed, stream, (uint64_t)t, z0, z1);
+    normal_pair(seed, stream, pair0 + (uint64_t)t, z0, z1);
     out[2 * t] = scale * z0;
     if (2 * t + 1 < count) out[2 * t + 1] = scale * z1;
   }
 }
 
-// X += sigma * z, sigma = rel * sqrt(ssq / count) if ssq else rel (absolute std)
+// X += sigma * z, sigma = rel * sqrt(ssq / total) if ssq else rel (absolute std)
 __global__ void k_add_noise(double* __restrict__ X, int64_t count, uint64_t seed, uint64_t stream,
-                            const double* __restrict__ ssq, double rel) {
-  const double sigma = ssq ? rel * sqrt(*ssq / (double)count) : rel;
+                            const double* __restrict__ ssq, double rel, uint64_t pair0, double total) {
+  const double sigma = ssq ? rel * sqrt(*ssq / total) : rel;
   const int64_t pairs = (count + 1) / 2;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < pairs; t += (int64_t)gridDim.x * blockDim.x) {
     double z0, z1;
-    normal_pair(seed, stream, (uint64_t)t, z0, z1);
+    normal_pair(seed, stream, pair0 + (uint64_t)t, z0, z1);
     X[2 * t] += sigma * z0;
     if (2 * t + 1 < count) X[2 * t + 1] += sigma * z1;
   }
@@ -85,14 +88,16 @@ __global__ void k_sumsq_parts(const double* __restrict__ X, int64_t count, doubl
   }
 }
 
-void launch_normal_fill(double* out, int64_t count, uint64_t seed, uint64_t stream, double scale, cudaStream_t st) {
+void launch_normal_fill(double* out, int64_t count, uint64_t seed, uint64_t stream, double scale, cudaStream_t st,
+                        int64_t offset) {
   ++::qcur::g_launches;
-  k_normal_fill<<<148 * 8, 256, 0, st>>>(out, count, seed, stream, scale);
+  k_normal_fill<<<148 * 8, 256, 0, st>>>(out, count, seed, stream, scale, (uint64_t)(offset / 2));
 }
 void launch_add_scaled_noise(double* X, int64_t count, uint64_t seed, uint64_t stream, const double* ssq, double rel,
-                             cudaStream_t st) {
+                             cudaStream_t st, int64_t offset, int64_t total) {
   ++::qcur::g_launches;
-  k_add_noise<<<148 * 8, 256, 0, st>>>(X, count, seed, stream, ssq, rel);
+  k_add_noise<<<148 * 8, 256, 0, st>>>(X, count, seed, stream, ssq, rel, (uint64_t)(offset / 2),
+                                       (double)(total > 0 ? total : count));
 }
 void launch_sumsq(const double* X, int64_t count, double* partials, int64_t nparts, double* out, cudaStream_t st) {
   ++::qcur::g_launches;

@@ -29,7 +29,8 @@ struct DevPairwise {
 };
 
 // k_norms.cu
-void launch_colstrip(const double* X, int64_t m, int64_t n, int64_t ldx, double* sq, double* colsum, cudaStream_t st);
+void launch_colstrip(const double* X, int64_t m, int64_t n, int64_t ldx, double* sq, double* colsum, cudaStream_t st,
+                     const double* acc_in = nullptr);
 void launch_pairwise(const double* data, int64_t nseg, int64_t seg_stride, const DevPairwise& pw, double* scratch,
                      double* out, cudaStream_t st);
 void launch_scale(const double* in, int64_t len, const double* denom, double* out, unsigned* status,
@@ -124,9 +125,12 @@ void launch_rowmajor_to_colmajor(const double* Z, int64_t p, int64_t q, int64_t 
                                  const unsigned* status, unsigned gate_bit, cudaStream_t st);
 
 // k_synth.cu : synthetic workloads (Philox normal generator)
-void launch_normal_fill(double* out, int64_t count, uint64_t seed, uint64_t stream, double scale, cudaStream_t st);
+// offset: element offset (even) of this block within the whole generated array
+void launch_normal_fill(double* out, int64_t count, uint64_t seed, uint64_t stream, double scale, cudaStream_t st,
+                        int64_t offset = 0);
+// sigma = rel * sqrt(*ssq / total) (total = element count of the whole matrix; 0 -> count)
 void launch_add_scaled_noise(double* X, int64_t count, uint64_t seed, uint64_t stream, const double* ssq,
-                             double rel, cudaStream_t st);
+                             double rel, cudaStream_t st, int64_t offset = 0, int64_t total = 0);
 void launch_sumsq(const double* X, int64_t count, double* partials, int64_t nparts, double* out, cudaStream_t st);
 // cfg3 image-like input; F: 6 L max(m,n) doubles, part: 296*6 doubles scratch
 void launch_synth_image(int64_t m, int64_t n, int L, uint64_t seed, double sigma, double* F, double* part,

@@ -1075,6 +1075,115 @@ int qcur_synth_lowrank(qcur_ctx* ctx, int64_t m, int64_t n, int64_t k, uint64_t 
 
 double qcur_fp64_peak_tflops(qcur_ctx* ctx) { return run_dmma_peak(ctx->sms, ctx->stream); }
 
+int qcur_synth_lowrank_rows(qcur_ctx* ctx, int64_t m, int64_t n, int64_t k, uint64_t seed, double noise,
+                            int64_t row0, int64_t rows, double* x_dev) {
+  if (m < 1 || n < 1 || k < 1 || row0 < 0 || rows < 1 || row0 + rows > m)
+    return ctx->fail(QCUR_E_PARAMETER, "synth_lowrank_rows: bad sizes");
+  GemmArgs gprobe = gargs(rows, n, k, nullptr, 0, 0, nullptr, 0, 1, nullptr, 0);
+  int rc = ctx->reserve((size_t)qbytes(rows, k) + qbytes(n, k) + qgemm_workspace_bytes(gprobe) + 8192);
+  if (rc) return rc;
+  double* P = ctx->take<double>((size_t)(rows * k * 4));
+  double* Q = ctx->take<double>((size_t)(n * k * 4));
+  GemmArgs g = gargs(rows, n, k, P, k, 0, Q, k, 1, x_dev, n);  // S rows = P rows Q^H
+  double* gws = ctx->take<double>(qgemm_workspace_bytes(g) / 8 + 16);
+  if (!P || !Q || !gws) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (synth rows)");
+  launch_normal_fill(P, rows * k * 4, seed, 1, 1.0, ctx->stream, row0 * k * 4);
+  launch_normal_fill(Q, n * k * 4, seed, 2, 1.0, ctx->stream);
+  launch_qgemm(g, gws, ctx->counters, ctx->stream);
+  // noise relative to the analytic E||S||_F^2 = 16 k m n: sigma = noise * sqrt(4 k)
+  if (noise > 0.0)
+    launch_add_scaled_noise(x_dev, rows * n * 4, seed, 3, nullptr, noise * sqrt(4.0 * (double)k), ctx->stream,
+                            row0 * n * 4);
+  CK_LAUNCH(ctx, "synth rows");
+  return QCUR_OK;
+}
+
+// ---- phase-level entry points (row-block sharded QMCUR, paper_2402_19147_b200/rowshard.py) ----
+int qcur_colsums_seq(qcur_ctx* ctx, const double* x_dev, int64_t rows, int64_t n, const double* acc_in,
+                     double* colsum_out, double* sq_out) {
+  if (rows < 1 || n < 1) return ctx->fail(QCUR_E_SHAPE, "colsums_seq: bad sizes");
+  launch_colstrip(x_dev, rows, n, n, sq_out, colsum_out, ctx->stream, acc_in);
+  CK_LAUNCH(ctx, "colsums_seq");
+  return QCUR_OK;
+}
+
+int qcur_pairwise_sums(qcur_ctx* ctx, const double* data, int64_t nseg, int64_t stride, int64_t length,
+                       double* out) {
+  if (nseg < 1 || length < 0) return ctx->fail(QCUR_E_SHAPE, "pairwise_sums: bad sizes");
+  int rc = ctx->reserve(pairwise_scratch_bytes(ctx, nseg, length) + 4096);
+  if (rc) return rc;
+  return pairwise_sum(ctx, data, nseg, stride, length, out);
+}
+
+int qcur_vec_div(qcur_ctx* ctx, const double* in, int64_t len, const double* denom, double* out) {
+  launch_scale(in, len, denom, out, ctx->status_dev, ST_DEGENERATE, ctx->stream);
+  CK_LAUNCH(ctx, "vec_div");
+  return QCUR_OK;
+}
+
+int qcur_gather_cols(qcur_ctx* ctx, const double* x_dev, int64_t rows, int64_t n, const int64_t* J, int64_t c,
+                     double* out) {
+  launch_gather_cols(x_dev, rows, n, J, c, out, ctx->stream);
+  CK_LAUNCH(ctx, "gather_cols");
+  return QCUR_OK;
+}
+
+int qcur_gather_rows(qcur_ctx* ctx, const double* x_dev, int64_t n, const int64_t* I, int64_t r, double* out) {
+  launch_gather_rows(x_dev, n, n, I, r, out, ctx->stream);
+  CK_LAUNCH(ctx, "gather_rows");
+  return QCUR_OK;
+}
+
+int qcur_qgemm_ex(qcur_ctx* ctx, int opA, int opB, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+                  int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, int flags) {
+  GemmArgs g = with_flags(gargs(M, N, K, A, lda, opA, B, ldb, opB, C, ldc, alpha, beta), flags & 1, (flags >> 1) & 1);
+  int rc = ctx->reserve(qgemm_workspace_bytes(g) + 4096);
+  if (rc) return rc;
+  return gemm(ctx, g, ctx->take<double>(qgemm_workspace_bytes(g) / 8 + 16));
+}
+
+int qcur_chol_inv(qcur_ctx* ctx, const double* G, int64_t q, double* X) {
+  if (q < 1) return ctx->fail(QCUR_E_SHAPE, "chol_inv: bad size");
+  if (q <= chol_cluster_qmax()) {
+    CholJob j{G, nullptr, X, ST_CHOL_FAIL_C};
+    launch_chol_inv_cluster(&j, 1, q, ctx->status_dev, ctx->stream);
+    CK_LAUNCH(ctx, "chol_inv");
+    return QCUR_OK;
+  }
+  int rc = ctx->reserve(chol_blocked_ws_bytes(q) + 4096);
+  if (rc) return rc;
+  return chol_inv_blocked(ctx, G, q, X, ST_CHOL_FAIL_C);
+}
+
+int qcur_series_l2inv(qcur_ctx* ctx, const double* G2, int64_t q, double* L2inv) {
+  GemmArgs probe = gargs(q, q, q, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0);
+  int rc = ctx->reserve(4 * qbytes(q, q) + qgemm_workspace_bytes(probe) + 8192);
+  if (rc) return rc;
+  double *M0 = ctx->take<double>((size_t)(q * q * 4)), *P = ctx->take<double>((size_t)(q * q * 4));
+  double *M1 = ctx->take<double>((size_t)(q * q * 4)), *P2 = ctx->take<double>((size_t)(q * q * 4));
+  double* gws = ctx->take<double>(qgemm_workspace_bytes(probe) / 8 + 16);
+  launch_series_lh(G2, nullptr, q, M0, ctx->status_dev, ST_CHOL_FAIL_C, 1e-5, ctx->stream);
+  if ((rc = gemm(ctx, with_flags(gargs(q, q, q, M0, q, 0, M0, q, 1, P, q), 1, 1), gws))) return rc;
+  launch_series_lh(G2, P, q, M1, ctx->status_dev, ST_CHOL_FAIL_C, 1e-5, ctx->stream);
+  if ((rc = gemm(ctx, gargs(q, q, q, M1, q, 0, M1, q, 0, P2, q), gws))) return rc;
+  launch_series_final(M1, P2, q, L2inv, ctx->stream);
+  CK_LAUNCH(ctx, "series");
+  return QCUR_OK;
+}
+
+int qcur_kappa_check(qcur_ctx* ctx, const double* G1, const double* F, int64_t q) {
+  launch_kappa_check(G1, F, q, ctx->kappa_limit, ctx->status_dev, ST_CHOL_FAIL_C, ctx->stream);
+  CK_LAUNCH(ctx, "kappa");
+  return QCUR_OK;
+}
+
+int qcur_factor(qcur_ctx* ctx, const double* src, int zh, int64_t p, int64_t q, double* Q, double* F) {
+  if (p < q || q < 1) return ctx->fail(QCUR_E_SHAPE, "factor: needs a tall block (p >= q)");
+  int rc = ctx->reserve(factor_ws_bytes(p, q) + 4096);
+  if (rc) return rc;
+  return factor_tall(ctx, src, zh, p, q, ST_CHOL_FAIL_C, -1.0, FactorOut{Q, F});
+}
+
 int qcur_synth_image(qcur_ctx* ctx, int64_t m, int64_t n, int nterms, uint64_t seed, double noise_std,
                      double* x_dev) {
   if (m < 1 || n < 1 || nterms < 1) return ctx->fail(QCUR_E_PARAMETER, "synth_image: bad sizes");
