@@ -42,6 +42,9 @@ enum qcur_status {
 
 enum qcur_strategy { QCUR_STRATEGY_LENGTH = 0, QCUR_STRATEGY_UNIFORM = 1 }; /* cur.py:56 STRATEGIES */
 enum qcur_op { QCUR_OP_N = 0, QCUR_OP_H = 1 };                             /* op(A) = A or A^H      */
+/* middle factor: the reference's U = pinv(C) X pinv(R) (cur.py:268), or the
+ * north star's opt-in intersection core U = pinv(X[I, J]) */
+enum qcur_core { QCUR_CORE_PROJECTION = 0, QCUR_CORE_INTERSECTION = 1 };
 
 /* informational bits returned by qcur_last_info() */
 enum qcur_info {
@@ -93,6 +96,11 @@ int qcur_draw_indices(qcur_ctx* ctx, const double* probs_dev, int64_t size, int6
 int qcur_qmcur(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, const double* col_probs_dev,
                const double* row_probs_dev, int64_t num_cols, int64_t num_rows, const uint64_t state[4],
                int64_t* col_idx_dev, int64_t* row_idx_dev, double* c_dev, double* u_dev, double* r_dev);
+/* qcur_qmcur with a choice of middle factor (enum qcur_core): projection
+ * U = pinv(C) X pinv(R) (the reference) or intersection U = pinv(X[I, J]). */
+int qcur_qmcur_ex(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, const double* col_probs_dev,
+                  const double* row_probs_dev, int64_t num_cols, int64_t num_rows, const uint64_t state[4], int core,
+                  int64_t* col_idx_dev, int64_t* row_idx_dev, double* c_dev, double* u_dev, double* r_dev);
 /* Error statistics of X - C U R without forming CUR (callers: cli.py:173-175,
  * bench.py:257-258, imaging.py:170-177).  out4_dev (4 doubles, device):
  *   [0] ||X - CUR||_F^2   [1] ||X||_F^2   [2] imaginary-part ||X - CUR||^2 (float PSNR)
@@ -104,7 +112,7 @@ int qcur_cur_error(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, con
  * distributions (strategy) + draw + gather + pinv + U + fused error. */
 int qcur_approx(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int strategy, const uint64_t state[4],
                 int64_t num_cols, int64_t num_rows, int64_t* col_idx_dev, int64_t* row_idx_dev, double* c_dev,
-                double* u_dev, double* r_dev, double psnr_scale, double* err4_dev);
+                double* u_dev, double* r_dev, double psnr_scale, int core, double* err4_dev);
 /* read back and clear the device status word; returns the mapped status code */
 int qcur_check(qcur_ctx* ctx);
 

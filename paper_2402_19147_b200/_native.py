@@ -32,6 +32,7 @@ _STATUS_EXC = {
     4: SamplingError,
 }
 STRATEGY_CODES = {"length": 0, "uniform": 1}
+CORE_CODES = {"projection": 0, "intersection": 1}
 OP_N, OP_H = 0, 1
 
 #: every symbol include/qcur_b200.h declares (checked by tests/test_abi.py)
@@ -46,7 +47,7 @@ EXPORTS = (
     "qcur_profile", "qcur_profile_read", "qcur_launch_count", "qcur_pairwise_host", "qcur_synth_image",
     "qcur_colsums_seq", "qcur_pairwise_sums", "qcur_vec_div", "qcur_gather_cols", "qcur_gather_rows",
     "qcur_qgemm_ex", "qcur_chol_inv", "qcur_series_l2inv", "qcur_kappa_check", "qcur_factor",
-    "qcur_synth_lowrank_rows",
+    "qcur_synth_lowrank_rows", "qcur_qmcur_ex",
 )
 
 _c_dp = ctypes.c_void_p
@@ -93,10 +94,13 @@ def load_library() -> ctypes.CDLL:
             "qcur_draw_indices": (ctypes.c_int, [_c_dp, _c_dp, _i64, _i64, _u64p, _c_dp]),
             "qcur_qmcur": (ctypes.c_int, [_c_dp, _c_dp, _i64, _i64, _c_dp, _c_dp, _i64, _i64, _u64p,
                                           _c_dp, _c_dp, _c_dp, _c_dp, _c_dp]),
+            "qcur_qmcur_ex": (ctypes.c_int, [_c_dp, _c_dp, _i64, _i64, _c_dp, _c_dp, _i64, _i64, _u64p,
+                                             ctypes.c_int, _c_dp, _c_dp, _c_dp, _c_dp, _c_dp]),
             "qcur_cur_error": (ctypes.c_int, [_c_dp, _c_dp, _i64, _i64, _c_dp, _i64, _c_dp, _c_dp, _i64, ctypes.c_double,
                                               _c_dp]),
             "qcur_approx": (ctypes.c_int, [_c_dp, _c_dp, _i64, _i64, ctypes.c_int, _u64p, _i64, _i64,
-                                           _c_dp, _c_dp, _c_dp, _c_dp, _c_dp, ctypes.c_double, _c_dp]),
+                                           _c_dp, _c_dp, _c_dp, _c_dp, _c_dp, ctypes.c_double, ctypes.c_int,
+                                           _c_dp]),
             "qcur_check": (ctypes.c_int, [_c_dp]),
             "qcur_qgemm": (ctypes.c_int, [_c_dp, ctypes.c_int, ctypes.c_int, _i64, _i64, _i64, ctypes.c_double,
                                           _c_dp, _i64, _c_dp, _i64, ctypes.c_double, _c_dp, _i64]),

@@ -591,7 +591,7 @@ size_t qmcur_ws_bytes(int64_t m, int64_t n, int64_t c, int64_t r) {
 // draw + gather + pinv + U.  Arena reserved by the caller.
 int qmcur_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, const double* colp, const double* rowp,
                int64_t c, int64_t r, const uint64_t state[4], int64_t* J, int64_t* I, double* C, double* U,
-               double* R) {
+               double* R, int core = QCUR_CORE_PROJECTION) {
   cudaStream_t st = ctx->stream;
   // 1. draws: columns first, then rows, one stream (cur.py:251-253)
   Pcg64 g;
@@ -614,6 +614,17 @@ int qmcur_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, const doubl
   CK_LAUNCH(ctx, "gather");
   ctx->mark("gather");
   int rc;
+  if (core == QCUR_CORE_INTERSECTION) {
+    // U = pinv(W), W = X[I, J] = R[:, J] (r x c): the north star's intersection core,
+    // oracle pseudoinverse(x.take_rows(I).take_cols(J)) (linalg.py:346-362, quat.py:215-225)
+    double* W = ctx->take<double>((size_t)(r * c * 4));
+    if (!W) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (intersection)");
+    launch_gather_cols(R, r, n, J, c, W, st);
+    CK_LAUNCH(ctx, "gather W");
+    if ((rc = pinv_impl(ctx, W, r, c, -1.0, U, ST_CHOL_FAIL_C))) return rc;
+    ctx->mark("core_u");
+    return QCUR_OK;
+  }
   if (m >= c && n >= r) {
     double* QC = ctx->take<double>((size_t)(m * c * 4));
     double* FC = ctx->take<double>((size_t)(c * c * 4));
@@ -901,6 +912,19 @@ int qcur_qmcur(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, const d
   return sync_status(ctx);
 }
 
+int qcur_qmcur_ex(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, const double* colp, const double* rowp,
+                  int64_t c, int64_t r, const uint64_t state[4], int core, int64_t* J, int64_t* I, double* C,
+                  double* U, double* R) {
+  if (core != QCUR_CORE_PROJECTION && core != QCUR_CORE_INTERSECTION)
+    return ctx->fail(QCUR_E_PARAMETER, "unknown core mode %d", core);
+  if (m < 1 || n < 1 || c < 1 || r < 1 || c > n || r > m) return ctx->fail(QCUR_E_SHAPE, "qmcur: bad sizes");
+  int rc = ctx->reserve(qmcur_ws_bytes(m, n, c, r) + qbytes(r, c) + pinv_ws_bytes(r, c));
+  if (rc) return rc;
+  if ((rc = reset_status(ctx))) return rc;
+  if ((rc = qmcur_impl(ctx, x_dev, m, n, colp, rowp, c, r, state, J, I, C, U, R, core))) return rc;
+  return sync_status(ctx);
+}
+
 int qcur_cur_error(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, const double* C, int64_t c,
                    const double* U, const double* R, int64_t r, double psnr_scale, double* out4) {
   int rc = ctx->reserve(error_ws_bytes(m, n, c, r));
@@ -910,11 +934,14 @@ int qcur_cur_error(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, con
 
 int qcur_approx(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int strategy, const uint64_t state[4],
                 int64_t c, int64_t r, int64_t* J, int64_t* I, double* C, double* U, double* R, double psnr_scale,
-                double* err4) {
+                int core, double* err4) {
   if (m < 1 || n < 1 || c < 1 || r < 1 || c > n || r > m) return ctx->fail(QCUR_E_SHAPE, "qcur_approx: bad sizes");
   if (strategy != QCUR_STRATEGY_LENGTH && strategy != QCUR_STRATEGY_UNIFORM)
     return ctx->fail(QCUR_E_PARAMETER, "unknown strategy %d", strategy);
-  size_t need = (size_t)(m + n) * 8 + 1024 + qmcur_ws_bytes(m, n, c, r) + error_ws_bytes(m, n, c, r);
+  if (core != QCUR_CORE_PROJECTION && core != QCUR_CORE_INTERSECTION)
+    return ctx->fail(QCUR_E_PARAMETER, "unknown core mode %d", core);
+  size_t need = (size_t)(m + n) * 8 + 1024 + qmcur_ws_bytes(m, n, c, r) + error_ws_bytes(m, n, c, r) +
+                qbytes(r, c) + pinv_ws_bytes(r, c);
   if (strategy == QCUR_STRATEGY_LENGTH) need += length_ws_bytes(ctx, m, n);
   int rc = ctx->reserve(need);
   if (rc) return rc;
@@ -928,7 +955,7 @@ int qcur_approx(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int st
     launch_fill(rowp, m, 1.0 / (double)m, ctx->stream);
     ctx->mark("dists");
   }
-  if ((rc = qmcur_impl(ctx, x_dev, m, n, colp, rowp, c, r, state, J, I, C, U, R))) return rc;
+  if ((rc = qmcur_impl(ctx, x_dev, m, n, colp, rowp, c, r, state, J, I, C, U, R, core))) return rc;
   return error_impl(ctx, x_dev, m, n, C, c, U, R, r, psnr_scale, err4);
 }
 

@@ -235,8 +235,19 @@ def _check_plan_shape(x, plan: SamplingPlan) -> tuple[int, int]:
     return m, n
 
 
-def qmcur(x, plan: SamplingPlan) -> CURFactors:
-    """Sampled CUR factorization of x under the given plan (cur.py:257-269)."""
+def _check_core(core: str) -> int:
+    if core not in _native.CORE_CODES:
+        raise ParameterError(f"unknown core mode {core!r}; expected one of {sorted(_native.CORE_CODES)}")
+    return _native.CORE_CODES[core]
+
+
+def qmcur(x, plan: SamplingPlan, core: str = "projection") -> CURFactors:
+    """Sampled CUR factorization of x under the given plan (cur.py:257-269).
+
+    core="projection" (the reference): U = pinv(C) X pinv(R).
+    core="intersection": U = pinv(X[I, J]) (the classical CUR middle factor,
+    no pass over X beyond the gathers)."""
+    core_code = _check_core(core)
     m, n = _check_plan_shape(x, plan)
     c, r = int(plan.num_cols), int(plan.num_rows)
     for probs, count in ((plan.col_probs, c), (plan.row_probs, r)):
@@ -253,9 +264,9 @@ def qmcur(x, plan: SamplingPlan) -> CURFactors:
     C = dev.empty_q(m, c)
     U = dev.empty_q(c, r)
     R = dev.empty_q(r, n)
-    dev.call("qcur_qmcur", xd.data_ptr(), m, n, colp.data_ptr(), rowp.data_ptr(), c, r,
-             state.ctypes.data_as(_native._u64p), J.data_ptr(), I.data_ptr(), C.data_ptr(), U.data_ptr(),
-             R.data_ptr())
+    dev.call("qcur_qmcur_ex", xd.data_ptr(), m, n, colp.data_ptr(), rowp.data_ptr(), c, r,
+             state.ctypes.data_as(_native._u64p), core_code, J.data_ptr(), I.data_ptr(), C.data_ptr(),
+             U.data_ptr(), R.data_ptr())
     return CURFactors(
         row_indices=I.cpu().numpy(),
         col_indices=J.cpu().numpy(),
@@ -353,12 +364,13 @@ class DeviceApprox:
         self.R = d.empty_q(r, n)
         self.err4 = d.empty(4)
 
-    def run(self, xd, strategy: str, seed: int, psnr_scale: float = 0.0) -> None:
+    def run(self, xd, strategy: str, seed: int, psnr_scale: float = 0.0, core: str = "projection") -> None:
+        core_code = _check_core(core)
         state = _native.state_from_seed(seed)
         self.dev.call("qcur_approx", xd.data_ptr(), self.m, self.n, _native.STRATEGY_CODES[_check_strategy(strategy)],
                       state.ctypes.data_as(_native._u64p), self.c, self.r, self.J.data_ptr(), self.I.data_ptr(),
                       self.C.data_ptr(), self.U.data_ptr(), self.R.data_ptr(), float(psnr_scale),
-                      self.err4.data_ptr())
+                      core_code, self.err4.data_ptr())
 
     def check(self) -> None:
         self.dev.call("qcur_check")

@@ -12,6 +12,8 @@ import pytest
 import oracle as O
 import paper_2402_19147_b200 as q
 from paper_2402_19147_b200 import _native
+from paper_2402_19147_b200.cur import DeviceApprox
+from paper_2402_19147_b200.quat import from_device, to_device
 from helpers import lowrank, rand_mat, rel_fro_err
 
 pytestmark = pytest.mark.gpu
@@ -238,3 +240,44 @@ def test_draw_long_axis_global_memory_path():
     got = q.draw_indices(p, 60, 17)
     want = O.draw_indices(p, 60, np.random.default_rng(17))
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("m,n,k,counts,noise", [(40, 30, 4, (8, 6), 1e-3), (300, 260, 12, (48, 36), 1e-3),
+                                                (120, 100, 6, (6, 6), 0.0)])
+def test_qmcur_intersection_core(m, n, k, counts, noise):
+    # opt-in classical middle factor U = pinv(X[I, J]); C, R and indices are the same draws
+    x = lowrank(m, n, k, seed=m + n, noise=noise)
+    plan = q.make_plan(x, "length", k, 5, num_rows=counts[0], num_cols=counts[1])
+    f = q.qmcur(x, plan, core="intersection")
+    rows, cols, c, _, r = oracle_factors(x, plan)
+    assert np.array_equal(f.col_indices, cols) and np.array_equal(f.row_indices, rows)
+    for got, want in zip(f.c.planes, c):
+        assert np.array_equal(got, want)
+    w = tuple(p[:, cols] for p in r)
+    u_ref = O.pinv(w)
+    du = O.rel_fro(tuple(f.u.planes), u_ref)
+    assert du <= U_TOL, du
+    if noise == 0.0:
+        assert rel_fro_err(q.cur_reconstruct(f), x) <= 1e-8
+
+
+def test_intersection_core_device_approx_matches_host_api():
+    x = lowrank(200, 180, 8, seed=77, noise=1e-3)
+    plan = q.make_plan(x, "length", 8, 9, num_rows=32, num_cols=24)
+    f = q.qmcur(x, plan, core="intersection")
+    dev = _native.device()
+    xd = to_device(x, dev)
+    da = DeviceApprox(200, 180, 24, 32, dev)
+    da.run(xd, "length", 9, core="intersection")
+    da.check()
+    assert np.array_equal(da.J.cpu().numpy(), f.col_indices)
+    got = from_device(da.U, dev)
+    assert all(np.array_equal(a, b) for a, b in zip(got.planes, f.u.planes))
+    e2, x2 = O.cur_error(tuple(x.planes), tuple(f.c.planes), tuple(f.u.planes), tuple(f.r.planes))
+    assert abs(da.rel_error() - math.sqrt(e2 / x2)) <= ERR_TOL * math.sqrt(e2 / x2)
+
+
+def test_unknown_core_rejected():
+    x = lowrank(10, 8, 2, seed=1)
+    with pytest.raises(q.ParameterError):
+        q.qmcur(x, q.make_plan(x, "length", 2, 0), core="bogus")
