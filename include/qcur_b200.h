@@ -101,6 +101,16 @@ int qcur_qmcur(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, const d
 int qcur_qmcur_ex(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, const double* col_probs_dev,
                   const double* row_probs_dev, int64_t num_cols, int64_t num_rows, const uint64_t state[4], int core,
                   int64_t* col_idx_dev, int64_t* row_idx_dev, double* c_dev, double* u_dev, double* r_dev);
+/* qcur_qmcur_ex that also delivers the factors to host memory in the reference's
+ * planar layout (four float64 planes per matrix, quat.py:110-143): C, R and the
+ * indices stream out on a copy stream while the factorizations and the X Q_R
+ * contraction run; U follows.  Host buffers should be pinned for the overlap.
+ * The device outputs are written as in qcur_qmcur_ex.  Returns after the copies. */
+int qcur_qmcur_host(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, const double* col_probs_dev,
+                    const double* row_probs_dev, int64_t num_cols, int64_t num_rows, const uint64_t state[4],
+                    int core, int64_t* col_idx_dev, int64_t* row_idx_dev, double* c_dev, double* u_dev,
+                    double* r_dev, int64_t* col_idx_host, int64_t* row_idx_host, double* const c_host[4],
+                    double* const u_host[4], double* const r_host[4]);
 /* Error statistics of X - C U R without forming CUR (callers: cli.py:173-175,
  * bench.py:257-258, imaging.py:170-177).  out4_dev (4 doubles, device):
  *   [0] ||X - CUR||_F^2   [1] ||X||_F^2   [2] imaginary-part ||X - CUR||^2 (float PSNR)

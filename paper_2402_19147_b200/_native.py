@@ -47,12 +47,13 @@ EXPORTS = (
     "qcur_profile", "qcur_profile_read", "qcur_launch_count", "qcur_pairwise_host", "qcur_synth_image",
     "qcur_colsums_seq", "qcur_pairwise_sums", "qcur_vec_div", "qcur_gather_cols", "qcur_gather_rows",
     "qcur_qgemm_ex", "qcur_chol_inv", "qcur_series_l2inv", "qcur_kappa_check", "qcur_factor",
-    "qcur_synth_lowrank_rows", "qcur_qmcur_ex",
+    "qcur_synth_lowrank_rows", "qcur_qmcur_ex", "qcur_qmcur_host",
 )
 
 _c_dp = ctypes.c_void_p
 _i64 = ctypes.c_int64
 _u64p = ctypes.POINTER(ctypes.c_uint64)
+_c_dp4 = ctypes.c_void_p * 4
 _lib = None
 _lib_lock = threading.Lock()
 
@@ -96,6 +97,9 @@ def load_library() -> ctypes.CDLL:
                                           _c_dp, _c_dp, _c_dp, _c_dp, _c_dp]),
             "qcur_qmcur_ex": (ctypes.c_int, [_c_dp, _c_dp, _i64, _i64, _c_dp, _c_dp, _i64, _i64, _u64p,
                                              ctypes.c_int, _c_dp, _c_dp, _c_dp, _c_dp, _c_dp]),
+            "qcur_qmcur_host": (ctypes.c_int, [_c_dp, _c_dp, _i64, _i64, _c_dp, _c_dp, _i64, _i64, _u64p,
+                                               ctypes.c_int, _c_dp, _c_dp, _c_dp, _c_dp, _c_dp, _c_dp, _c_dp,
+                                               _c_dp4, _c_dp4, _c_dp4]),
             "qcur_cur_error": (ctypes.c_int, [_c_dp, _c_dp, _i64, _i64, _c_dp, _i64, _c_dp, _c_dp, _i64, ctypes.c_double,
                                               _c_dp]),
             "qcur_approx": (ctypes.c_int, [_c_dp, _c_dp, _i64, _i64, ctypes.c_int, _u64p, _i64, _i64,
@@ -260,6 +264,16 @@ class Device:
         dtype = dtype or self.torch.float64
         return self.torch.empty(shape, dtype=dtype, device=f"cuda:{self.index}")
 
+    def pinned_planes(self, m: int, n: int) -> list:
+        """Four (m, n) float64 host planes in one page-locked block (torch's caching
+        host allocator, so repeated calls reuse the block).  D2H into pinned memory
+        runs at full PCIe rate and never page-faults."""
+        block = self.torch.empty((4, int(m), int(n)), dtype=self.torch.float64, pin_memory=True)
+        return [block[k].numpy() for k in range(4)]
+
+    def pinned_vec(self, count: int, dtype=None):
+        return self.torch.empty(int(count), dtype=dtype or self.torch.int64, pin_memory=True).numpy()
+
     def upload_planes(self, planes) -> "object":
         a0, a1, a2, a3 = (np.ascontiguousarray(p, dtype=np.float64) for p in planes)
         m, n = a0.shape
@@ -271,7 +285,7 @@ class Device:
     def download_planes(self, x, m: int | None = None, n: int | None = None, pinned_out=None):
         m = int(x.shape[0]) if m is None else m
         n = int(x.shape[1]) if n is None else n
-        planes = pinned_out if pinned_out is not None else [np.empty((m, n), dtype=np.float64) for _ in range(4)]
+        planes = pinned_out if pinned_out is not None else self.pinned_planes(m, n)
         self.call("qcur_download_planar", x.data_ptr(), m, n, n, *(p.ctypes.data for p in planes))
         return planes
 

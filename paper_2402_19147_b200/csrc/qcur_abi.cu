@@ -65,6 +65,8 @@ struct qcur_ctx {
   int device = 0;
   int sms = 148;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // D2H of finished factors, overlapped with the rest of the pipeline
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   unsigned* status_dev = nullptr;
   unsigned* status_host = nullptr;  // pinned
   unsigned* counters = nullptr;     // split-K tickets for launch_qgemm (kept zero between launches)
@@ -588,10 +590,57 @@ size_t qmcur_ws_bytes(int64_t m, int64_t n, int64_t c, int64_t r) {
   return b + 64 * 256;
 }
 
-// draw + gather + pinv + U.  Arena reserved by the caller.
+int qmcur_core(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, int64_t c, int64_t r, const int64_t* J,
+               const double* C, double* U, const double* R, int core);
+
+// Host destinations for qcur_qmcur_host (planar, the reference's QMatrix layout).
+struct HostOut {
+  int64_t* J;
+  int64_t* I;
+  double* C[4];
+  double* U[4];
+  double* R[4];
+};
+
+size_t host_out_ws_bytes(int64_t m, int64_t n, int64_t c, int64_t r) {
+  return qbytes(m, c) + qbytes(r, n) + qbytes(c, r) + 1024;
+}
+
+// Fork the copy stream off the main stream at this point and queue there the
+// planar conversion + D2H of a finished p x q interleaved factor (and optional
+// index vectors).  The main stream carries on with the pipeline.
+int copy_out(qcur_ctx* ctx, const double* A, int64_t p, int64_t q, double* const dst[4], const int64_t* idx_a,
+             int64_t na, int64_t* host_a, const int64_t* idx_b, int64_t nb, int64_t* host_b) {
+  cudaStream_t cs = ctx->copy_stream;
+  cudaError_t e = cudaEventRecord(ctx->ev_fork, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ctx->ev_fork, 0);
+  if (e != cudaSuccess) return ctx->cuda_fail(e, "copy fork");
+  const size_t pb = (size_t)(p * q) * sizeof(double);
+  double* planes[4];
+  for (int k = 0; k < 4; ++k) planes[k] = ctx->take<double>((size_t)(p * q));
+  if (!planes[3]) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (host copy)");
+  launch_interleaved_to_planar(A, p, q, q, planes[0], planes[1], planes[2], planes[3], cs);
+  CK_LAUNCH(ctx, "copy-out planar");
+  for (int k = 0; k < 4 && e == cudaSuccess; ++k) e = cudaMemcpyAsync(dst[k], planes[k], pb, cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess && host_a) e = cudaMemcpyAsync(host_a, idx_a, (size_t)na * 8, cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess && host_b) e = cudaMemcpyAsync(host_b, idx_b, (size_t)nb * 8, cudaMemcpyDeviceToHost, cs);
+  if (e != cudaSuccess) return ctx->cuda_fail(e, "copy-out D2H");
+  return QCUR_OK;
+}
+
+// Join: the main stream waits for every queued copy-out.
+int copy_join(qcur_ctx* ctx) {
+  cudaError_t e = cudaEventRecord(ctx->ev_join, ctx->copy_stream);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0);
+  return e == cudaSuccess ? QCUR_OK : ctx->cuda_fail(e, "copy join");
+}
+
+// draw + gather + pinv + U.  Arena reserved by the caller.  With `ho`, C, R
+// and the indices stream to the host while the factorizations and the X Q_R
+// contraction run; U follows at the end.
 int qmcur_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, const double* colp, const double* rowp,
                int64_t c, int64_t r, const uint64_t state[4], int64_t* J, int64_t* I, double* C, double* U,
-               double* R, int core = QCUR_CORE_PROJECTION) {
+               double* R, int core = QCUR_CORE_PROJECTION, const HostOut* ho = nullptr) {
   cudaStream_t st = ctx->stream;
   // 1. draws: columns first, then rows, one stream (cur.py:251-253)
   Pcg64 g;
@@ -613,6 +662,23 @@ int qmcur_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, const doubl
   launch_gather_rows(X, n, n, I, r, R, st);
   CK_LAUNCH(ctx, "gather");
   ctx->mark("gather");
+  int rc;
+  if (ho) {
+    if ((rc = copy_out(ctx, C, m, c, ho->C, J, c, ho->J, I, r, ho->I))) return rc;
+    if ((rc = copy_out(ctx, R, r, n, ho->R, nullptr, 0, nullptr, nullptr, 0, nullptr))) return rc;
+  }
+  if ((rc = qmcur_core(ctx, X, m, n, c, r, J, C, U, R, core))) return rc;
+  if (ho) {
+    if ((rc = copy_out(ctx, U, c, r, ho->U, nullptr, 0, nullptr, nullptr, 0, nullptr))) return rc;
+    if ((rc = copy_join(ctx))) return rc;
+  }
+  return QCUR_OK;
+}
+
+// U from the gathered C, R (projection: pinv(C) X pinv(R); intersection: pinv(R[:, J]))
+int qmcur_core(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, int64_t c, int64_t r, const int64_t* J,
+               const double* C, double* U, const double* R, int core) {
+  cudaStream_t st = ctx->stream;
   int rc;
   if (core == QCUR_CORE_INTERSECTION) {
     // U = pinv(W), W = X[I, J] = R[:, J] (r x c): the north star's intersection core,
@@ -749,6 +815,12 @@ int qcur_create(int device, qcur_ctx** out) {
     return QCUR_E_CUDA;
   }
   cudaMemset(ctx->counters, 0, (size_t)65536 * sizeof(unsigned));
+  if (cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+    delete ctx;
+    return QCUR_E_CUDA;
+  }
   *out = ctx;
   return QCUR_OK;
 }
@@ -762,6 +834,10 @@ void qcur_destroy(qcur_ctx* ctx) {
   cudaFree(ctx->status_dev);
   cudaFree(ctx->counters);
   cudaFreeHost(ctx->status_host);
+  cudaStreamSynchronize(ctx->copy_stream);
+  cudaStreamDestroy(ctx->copy_stream);
+  cudaEventDestroy(ctx->ev_fork);
+  cudaEventDestroy(ctx->ev_join);
   delete ctx;
 }
 
@@ -922,6 +998,31 @@ int qcur_qmcur_ex(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, cons
   if (rc) return rc;
   if ((rc = reset_status(ctx))) return rc;
   if ((rc = qmcur_impl(ctx, x_dev, m, n, colp, rowp, c, r, state, J, I, C, U, R, core))) return rc;
+  return sync_status(ctx);
+}
+
+int qcur_qmcur_host(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, const double* colp,
+                    const double* rowp, int64_t c, int64_t r, const uint64_t state[4], int core, int64_t* J,
+                    int64_t* I, double* C, double* U, double* R, int64_t* J_host, int64_t* I_host,
+                    double* const C_host[4], double* const U_host[4], double* const R_host[4]) {
+  if (core != QCUR_CORE_PROJECTION && core != QCUR_CORE_INTERSECTION)
+    return ctx->fail(QCUR_E_PARAMETER, "unknown core mode %d", core);
+  if (m < 1 || n < 1 || c < 1 || r < 1 || c > n || r > m) return ctx->fail(QCUR_E_SHAPE, "qmcur: bad sizes");
+  if (!J_host || !I_host || !C_host || !U_host || !R_host) return ctx->fail(QCUR_E_PARAMETER, "null host output");
+  HostOut ho{J_host, I_host, {}, {}, {}};
+  for (int k = 0; k < 4; ++k) {
+    ho.C[k] = C_host[k];
+    ho.U[k] = U_host[k];
+    ho.R[k] = R_host[k];
+    if (!ho.C[k] || !ho.U[k] || !ho.R[k]) return ctx->fail(QCUR_E_PARAMETER, "null host plane");
+  }
+  int rc = ctx->reserve(qmcur_ws_bytes(m, n, c, r) + qbytes(r, c) + pinv_ws_bytes(r, c) + host_out_ws_bytes(m, n, c, r));
+  if (rc) return rc;
+  if ((rc = reset_status(ctx))) return rc;
+  if ((rc = qmcur_impl(ctx, x_dev, m, n, colp, rowp, c, r, state, J, I, C, U, R, core, &ho))) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    return rc;
+  }
   return sync_status(ctx);
 }
 

@@ -264,16 +264,26 @@ def qmcur(x, plan: SamplingPlan, core: str = "projection") -> CURFactors:
     C = dev.empty_q(m, c)
     U = dev.empty_q(c, r)
     R = dev.empty_q(r, n)
-    dev.call("qcur_qmcur_ex", xd.data_ptr(), m, n, colp.data_ptr(), rowp.data_ptr(), c, r,
+    # host factors land in pinned planes; C, R and the indices download while U is computed
+    hj, hi = dev.pinned_vec(c), dev.pinned_vec(r)
+    hc, hu, hr = dev.pinned_planes(m, c), dev.pinned_planes(c, r), dev.pinned_planes(r, n)
+    ptrs = [_native._c_dp4(*(p.ctypes.data for p in planes)) for planes in (hc, hu, hr)]
+    dev.call("qcur_qmcur_host", xd.data_ptr(), m, n, colp.data_ptr(), rowp.data_ptr(), c, r,
              state.ctypes.data_as(_native._u64p), core_code, J.data_ptr(), I.data_ptr(), C.data_ptr(),
-             U.data_ptr(), R.data_ptr())
+             U.data_ptr(), R.data_ptr(), hj.ctypes.data, hi.ctypes.data, *ptrs)
     return CURFactors(
-        row_indices=I.cpu().numpy(),
-        col_indices=J.cpu().numpy(),
-        c=from_device(C, dev),
-        u=from_device(U, dev),
-        r=from_device(R, dev),
+        row_indices=hi,
+        col_indices=hj,
+        c=_wrap_resident(hc, C, dev),
+        u=_wrap_resident(hu, U, dev),
+        r=_wrap_resident(hr, R, dev),
     )
+
+
+def _wrap_resident(planes, t, dev) -> QMatrix:
+    out = QMatrix._wrap(*planes)
+    out._dev = (dev, t)
+    return out
 
 
 def cur_reconstruct(factors: CURFactors) -> QMatrix:
