@@ -1,4 +1,5 @@
-// Quaternion GEMM on the FP64 tensor path (mma.sync m8n8k4 f64 -> SASS DMMA.8x8x4).
+// Quaternion GEMM on the FP64 tensor path (mma.sync m8n8k4 f64 -> SASS DMMA.8x8x4),
+// fed by TMA through an mbarrier pipeline.
 //
 // Replaces qmat_matmul (pkg/src/qcur/quat.py:274-296), the reference's
 // "16 real GEMMs with the Hamilton sign pattern", which cur.py:268 and
@@ -11,19 +12,37 @@
 // exactly one quaternion of A's row; the B fragment element each lane needs is
 // one component of one compact quaternion of B with a per-lane sign, so E(B) is
 // never materialised (4x less shared memory and L2 traffic than expanding).
-// op(A)=H / op(B)=H are the same loads with a transposed placement and the
-// conjugate sign table.
+// op(A)=H / op(B)=H read k-major / j-major tiles with the conjugate sign table.
 //
-// Tiles: BM x BN reals per CTA, WM x WN per warp, BKQ quaternions of K per
-// cp.async stage (zero-filled at the edges), STAGES-deep pipeline.  Split-K
-// writes fixed partial slabs reduced in a fixed order, so every result is
-// bitwise deterministic run to run (test_cur.py:243-250).
+// CTA = 8 DMMA warps (2 x 4, warp tile WM x WN) + 1 TMA producer warp, one CTA
+// per SM.  The producer streams (A, B) k-block stages into a 5-8 deep ring of
+// shared-memory buffers with cp.async.bulk.tensor (A of op N through the
+// 128-byte swizzle, so the fragment loads are bank-conflict free); full/empty
+// mbarriers hand stages between the roles.  The DMMA warps do no address
+// arithmetic at all in the main loop.
+//
+// Schedule: the work is the list of (tile, k-block) iterations of every output
+// tile (row-major tiles; tiles above the diagonal of a Hermitian output are
+// absent; an upper-triangular op(B) shortens each tile's k range).
+//  * stream-K (many tiles): CTA c takes one contiguous span of the list, so
+//    every SM gets the same number of k-blocks whatever the tile count.  A
+//    tile cut between CTAs is finished by its last contributor (ticket), which
+//    adds the parts in CTA (= k) order.
+//  * split (fewer tiles than SMs/2, equal depth): each tile is cut into S equal
+//    k ranges run at the same time; the S CTAs meet on a ticket and each sums
+//    BM/S rows of the S parts in split order.
+// Both orders are fixed, so results are bitwise deterministic run to run
+// (test_cur.py:243-250).
 //
 // EPI_ERR fuses the error of the reference's caller (cli.py:173-175,
-// imaging.py:170-177): the tile of (P R) is subtracted from the matching tile
-// of X in registers and only sum((X - PR)^2) and sum(X^2) leave the CTA, so
-// CUR is never written to HBM.
+// imaging.py:170-177): CTAs take whole tiles, the tile of (P R) is subtracted
+// from the matching tile of X in registers and only per-tile sums leave the
+// CTA, so CUR is never written to HBM.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -32,15 +51,42 @@ namespace qcur {
 
 namespace {
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  int sz = valid ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(sz) : "memory");
+// ---------------------------------------------------------------------------
+// PTX helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+// named barrier among the DMMA warps only (the producer warp never joins)
 template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(N) : "memory");
 }
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
@@ -58,384 +104,681 @@ constexpr unsigned kSignN = 0x3950u;
 constexpr unsigned kSignH = 0x428Eu;
 
 enum { EPI_STORE = 0, EPI_ERR = 1 };
+enum { MODE_STREAMK = 0, MODE_SPLIT = 1, MODE_TILES = 2 };
 
-template <int BM, int BN, int WM, int WN, int BKQ, int STAGES, int OPA, int OPB, int EPI>
+constexpr int kBKQ = 8;  // quaternions of K per stage
+constexpr int kSmemBudget = 220 * 1024;
+
+template <int BM, int BN>
 struct Cfg {
-  static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
-  static constexpr int THREADS = WARPS_M * WARPS_N * 32;
+  static constexpr int WARPS_M = 2, WARPS_N = 4;
+  static constexpr int WM = BM / WARPS_M, WN = BN / WARPS_N;
   static constexpr int FM = WM / 8, FN = WN / 8;
-  static constexpr int AS = 4 * BKQ + 4;  // padded row stride (doubles): conflict-free A fragments
-  static constexpr int A_ELEMS = BM * AS;
-  static constexpr int B_ELEMS = BKQ * BN;
-  static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
-  static constexpr size_t SMEM = (size_t)STAGES * STAGE_ELEMS * sizeof(double);
+  static constexpr int CONSUMERS = WARPS_M * WARPS_N * 32;
+  static constexpr int THREADS = CONSUMERS + 32;
+  static constexpr int A_BYTES = BM * kBKQ * 32;
+  static constexpr int B_BYTES = kBKQ * BN * 8;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = kSmemBudget / STAGE_BYTES > 8 ? 8 : kSmemBudget / STAGE_BYTES;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 + 2 * STAGES * 8;
+  static_assert(BM % 64 == 0 && (BN / 4) % kBKQ == 0 && WN % 8 == 0, "tile shape");
+  static_assert(STAGE_BYTES % 1024 == 0, "stage buffers must keep the 1024-byte swizzle alignment");
 };
 
 struct KParams {
   int64_t Mq, Nq, Kq;
-  const double* A;
-  int64_t lda;
-  const double* B;
-  int64_t ldb;
   double* C;
   int64_t ldc;
   double alpha, beta;
-  double* work;        // split-K slabs [splits][Mq][4Nq], or null
-  int64_t kchunk;      // quaternions of K per split
   const double* X;     // EPI_ERR: reference matrix
   int64_t ldx;
   double* partials;    // EPI_ERR: [tiles][4]
   double psnr_scale;   // EPI_ERR: > 0 -> also the u8 image statistic at this scale (255)
-  unsigned* counters;  // split-K: per-tile arrival tickets (zero between launches)
-  int b_upper;         // op(B) is upper triangular: column j only needs k <= j
+  unsigned* counters;  // per-tile tickets (zero between launches); [65536] + done counters
+  double* slots;       // partial tiles [grid][2][BM*BN]
+  int b_upper;         // op(B) is upper triangular: tile column j only needs k <= j
   int herm_lower;      // output is Hermitian and only its lower triangle is consumed
+  int gx, gy;          // tile grid (columns of BN reals, rows of BM quaternion rows)
+  int nkb_full;        // k-blocks of a full-depth tile (>= 1)
+  int total;           // iterations (sum of k-blocks over tiles, < 2^31)
+  int mode;
+  int splits;          // MODE_SPLIT: CTAs per tile
 };
 
-template <int BM, int BN, int WM, int WN, int BKQ, int STAGES, int OPA, int OPB, int EPI>
-__global__ void __launch_bounds__(Cfg<BM, BN, WM, WN, BKQ, STAGES, OPA, OPB, EPI>::THREADS, 2)
-    qgemm_kernel(KParams p) {
-  using CF = Cfg<BM, BN, WM, WN, BKQ, STAGES, OPA, OPB, EPI>;
-  extern __shared__ __align__(16) double smem[];
+// Iteration space bookkeeping (closed form).
+template <int BM, int BN>
+struct Space {
+  static constexpr int W = BN / 4;     // quaternion columns per tile
+  static constexpr int w = W / kBKQ;   // k-blocks per tile column step (triangular op(B))
+  const KParams& p;
+  __device__ explicit Space(const KParams& kp) : p(kp) {}
+  __device__ int last_col(int ty) const {
+    if (!p.herm_lower) return p.gx - 1;
+    const int L = (ty * BM + BM - 1) / W;
+    return L < p.gx - 1 ? L : p.gx - 1;
+  }
+  __device__ int nkb_col(int tx) const {
+    if (!p.b_upper) return p.nkb_full;
+    const int v = (tx + 1) * w;
+    return v < p.nkb_full ? v : p.nkb_full;
+  }
+  __device__ int prefix_cols(int L) const {  // sum of nkb_col over tile columns 0..L
+    if (L < 0) return 0;
+    if (!p.b_upper) return (L + 1) * p.nkb_full;
+    const int tcap = (p.nkb_full + w - 1) / w - 1;  // first column at full depth
+    if (L < tcap) return w * (L + 1) * (L + 2) / 2;
+    return w * tcap * (tcap + 1) / 2 + (L - tcap + 1) * p.nkb_full;
+  }
+  __device__ int row_iters(int ty) const { return prefix_cols(last_col(ty)); }
+  __device__ int tile_nkb(int t) const {
+    const int ty = t / p.gx, tx = t - ty * p.gx;
+    return tx > last_col(ty) ? 0 : nkb_col(tx);
+  }
+  __device__ void locate(int i, int& t, int& kb) const {  // (tile, k-block) of iteration i
+    int ty = 0, base = 0;
+    if (!p.herm_lower) {
+      const int S = row_iters(0);
+      ty = i / S;
+      base = ty * S;
+    } else {
+      for (;; ++ty) {
+        const int S = row_iters(ty);
+        if (i < base + S) break;
+        base += S;
+      }
+    }
+    int rem = i - base, tx = 0;
+    for (;; ++tx) {
+      const int n = nkb_col(tx);
+      if (rem < n) break;
+      rem -= n;
+    }
+    t = ty * p.gx + tx;
+    kb = rem;
+  }
+  __device__ void advance(int& t, int& kb, int& nkb) const {
+    if (++kb == nkb) {
+      kb = 0;
+      const int ntiles = p.gx * p.gy;
+      do {
+        ++t;
+        nkb = t < ntiles ? tile_nkb(t) : 1;
+      } while (nkb == 0);
+    }
+  }
+};
+
+// this CTA's span [ib, ie) of the iteration list
+__device__ __forceinline__ void cta_span(const KParams& p, int& ib, int& ie) {
+  const int G = gridDim.x, c = blockIdx.x;
+  if (p.mode == MODE_TILES) {  // uniform tiles, whole tiles per CTA
+    const int ntiles = p.gx * p.gy;
+    ib = (int)((int64_t)c * ntiles / G) * p.nkb_full;
+    ie = (int)((int64_t)(c + 1) * ntiles / G) * p.nkb_full;
+  } else if (p.mode == MODE_SPLIT) {
+    const int o = c / p.splits, z = c - o * p.splits;
+    ib = o * p.nkb_full + (int)((int64_t)z * p.nkb_full / p.splits);
+    ie = o * p.nkb_full + (int)((int64_t)(z + 1) * p.nkb_full / p.splits);
+  } else {
+    ib = (int)((int64_t)c * p.total / G);
+    ie = (int)((int64_t)(c + 1) * p.total / G);
+  }
+}
+
+template <int BM, int BN, int OPA, int OPB, int EPI>
+__global__ void __launch_bounds__(Cfg<BM, BN>::THREADS, 1)
+    qgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const __grid_constant__ KParams p) {
+  using CF = Cfg<BM, BN>;
+  constexpr int S = CF::STAGES;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-byte aligned stage ring (swizzle atoms); offsetting the shared array keeps
+  // the fragment loads in the shared window (LDS, not generic LD)
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * CF::STAGE_BYTES);
+  uint64_t* empty = full + S;
+  __shared__ unsigned s_flag;
+  __shared__ double red[4][CF::CONSUMERS / 32];
+
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm0 = (warp / CF::WARPS_N) * WM;
-  const int wn0 = (warp % CF::WARPS_N) * WN;
-  const int64_t i0 = (int64_t)blockIdx.y * BM;   // quaternion rows
-  const int64_t jr0 = (int64_t)blockIdx.x * BN;  // real columns
-  const int64_t jq0 = jr0 / 4;
-  const int64_t kbeg = (int64_t)blockIdx.z * p.kchunk;
-  int64_t kend = kbeg + p.kchunk;
-  if (kend > p.Kq) kend = p.Kq;
-  if (p.b_upper && kend > jq0 + BN / 4) kend = jq0 + BN / 4;  // op(B)[k][j] = 0 for k > j
-  const bool skip = p.herm_lower && jq0 > i0 + BM - 1;     // tile strictly above the diagonal
-  const int nkb = skip || kend <= kbeg ? 0 : (int)((kend - kbeg + BKQ - 1) / BKQ);
+  const Space<BM, BN> sp(p);
+  int ib, ie;
+  cta_span(p, ib, ie);
+  if (ib >= ie) return;
 
-  auto load_stage = [&](int buf, int64_t k0) {
-    double* As = smem + buf * CF::STAGE_ELEMS;
-    double* Bs = As + CF::A_ELEMS;
-    // A tile: BM rows x BKQ quaternions = BM*BKQ*2 16-byte chunks
-    constexpr int ACH = BM * BKQ * 2;
-    for (int id = tid; id < ACH; id += CF::THREADS) {
-      int row, kq, half;
-      if (OPA == 0) {
-        row = id / (2 * BKQ);
-        int cc = id % (2 * BKQ);
-        kq = cc >> 1;
-        half = cc & 1;
-      } else {
-        kq = id / (2 * BM);
-        int rem = id % (2 * BM);
-        row = rem >> 1;
-        half = rem & 1;
-      }
-      const int64_t gi = i0 + row, gk = k0 + kq;
-      const bool v = gi < p.Mq && gk < kend;
-      const double* src = p.A;
-      if (v) src = (OPA == 0) ? p.A + (gi * p.lda + gk) * 4 + half * 2 : p.A + (gk * p.lda + gi) * 4 + half * 2;
-      cp_async16(As + row * CF::AS + kq * 4 + half * 2, src, v);
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CF::CONSUMERS / 32);
     }
-    // B tile: BKQ x (BN/4) quaternions
-    constexpr int BCH = BKQ * (BN / 4) * 2;
-    for (int id = tid; id < BCH; id += CF::THREADS) {
-      int kq, jq, half;
-      if (OPB == 0) {
-        kq = id / (BN / 2);
-        int cc = id % (BN / 2);
-        jq = cc >> 1;
-        half = cc & 1;
-      } else {
-        jq = id / (2 * BKQ);
-        int rem = id % (2 * BKQ);
-        kq = rem >> 1;
-        half = rem & 1;
-      }
-      const int64_t gk = k0 + kq, gj = jq0 + jq;
-      const bool v = gk < kend && gj < p.Nq;
-      const double* src = p.B;
-      if (v) src = (OPB == 0) ? p.B + (gk * p.ldb + gj) * 4 + half * 2 : p.B + (gj * p.ldb + gk) * 4 + half * 2;
-      cp_async16(Bs + kq * BN + jq * 4 + half * 2, src, v);
-    }
-  };
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
 
+  if (warp == CF::CONSUMERS / 32) {
+    // ------------------------------ TMA producer ------------------------------
+    if (lane == 0) {
+      int t, kb, nkb;
+      sp.locate(ib, t, kb);
+      nkb = sp.tile_nkb(t);
+      int stage = 0;
+      unsigned phase = 0;
+      for (int it = ib; it < ie; ++it) {
+        mbar_wait(&empty[stage], phase ^ 1u);
+        unsigned char* As = smem + (size_t)stage * CF::STAGE_BYTES;
+        unsigned char* Bs = As + CF::A_BYTES;
+        mbar_expect_tx(&full[stage], CF::STAGE_BYTES);
+        const int ty = t / p.gx, tx = t - ty * p.gx;
+        const int i0 = ty * BM, jq0 = tx * (BN / 4), k0 = kb * kBKQ;
+        if (OPA == 0) {  // two swizzled boxes [BM rows][4 quaternions]
+          tma_load_2d(As, &tmA, k0 * 4, i0, &full[stage]);
+          tma_load_2d(As + BM * 128, &tmA, k0 * 4 + 16, i0, &full[stage]);
+        } else {  // k-major [8 k][64 quaternions] boxes
+#pragma unroll
+          for (int b = 0; b < BM / 64; ++b) tma_load_2d(As + b * 8 * 256 * 8, &tmA, (i0 + 64 * b) * 4, k0, &full[stage]);
+        }
+        if (OPB == 0) tma_load_2d(Bs, &tmB, jq0 * 4, k0, &full[stage]);  // [8 k][BN reals]
+        else tma_load_2d(Bs, &tmB, k0 * 4, jq0, &full[stage]);           // [BN/4 j][8 quaternions]
+        sp.advance(t, kb, nkb);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+    }
+    return;
+  }
+
+  // ------------------------------ DMMA warps ------------------------------
+  const int wm0 = (warp / CF::WARPS_N) * CF::WM;
+  const int wn0 = (warp % CF::WARPS_N) * CF::WN;
   double acc[CF::FM][CF::FN][2];
 #pragma unroll
   for (int a = 0; a < CF::FM; ++a)
 #pragma unroll
     for (int b = 0; b < CF::FN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
-  // per-lane fragment constants
-  const int t = lane & 3, s = (lane >> 2) & 3, jl = lane >> 4;
-  const unsigned smask = OPB == 0 ? kSignN : kSignH;
-  const unsigned long long bsign = ((smask >> (t * 4 + s)) & 1u) ? 0x8000000000000000ull : 0ull;
-  const int boff = jl * 4 + (t ^ s);
-  const unsigned long long asign = (OPA == 1 && t != 0) ? 0x8000000000000000ull : 0ull;
+  const int t4 = lane & 3, s4 = (lane >> 2) & 3, jl = lane >> 4;
+  const unsigned long long bsign =
+      (((OPB == 0 ? kSignN : kSignH) >> (t4 * 4 + s4)) & 1u) ? 0x8000000000000000ull : 0ull;
+  const unsigned long long asign = (OPA == 1 && t4 != 0) ? 0x8000000000000000ull : 0ull;
   const int arow = lane >> 2;
+  const int tcomp = t4 ^ s4;
 
+  int ct, ckb, cnkb;
+  sp.locate(ib, ct, ckb);
+  cnkb = sp.tile_nkb(ct);
+  int seg_begin = ib;
+  int stage = 0;
+  unsigned phase = 0;
+  const int G = gridDim.x, c = blockIdx.x;
+  for (int it = ib; it < ie; ++it) {
+    mbar_wait(&full[stage], phase);
+    const double* As = reinterpret_cast<const double*>(smem + (size_t)stage * CF::STAGE_BYTES);
+    const double* Bs = reinterpret_cast<const double*>(smem + (size_t)stage * CF::STAGE_BYTES + CF::A_BYTES);
 #pragma unroll
-  for (int st = 0; st < STAGES - 1; ++st) {
-    if (st < nkb) load_stage(st, kbeg + (int64_t)st * BKQ);
-    cp_async_commit();
-  }
-  for (int kb = 0; kb < nkb; ++kb) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    {
-      const int nk = kb + STAGES - 1;
-      if (nk < nkb) load_stage(nk % STAGES, kbeg + (int64_t)nk * BKQ);
-      cp_async_commit();
-    }
-    const double* As = smem + (kb % STAGES) * CF::STAGE_ELEMS;
-    const double* Bs = As + CF::A_ELEMS;
-#pragma unroll
-    for (int kk = 0; kk < BKQ; ++kk) {
+    for (int kk = 0; kk < kBKQ; ++kk) {
       double af[CF::FM], bf[CF::FN];
 #pragma unroll
       for (int a = 0; a < CF::FM; ++a) {
-        double v = As[(wm0 + 8 * a + arow) * CF::AS + kk * 4 + t];
+        const int i = wm0 + 8 * a + arow;
+        double v;
+        if (OPA == 0) {
+          const int chunk = ((kk & 3) * 2 + (t4 >> 1)) ^ (i & 7);
+          v = As[(kk >> 2) * BM * 16 + i * 16 + chunk * 2 + (t4 & 1)];
+        } else {
+          v = As[(i >> 6) * 2048 + kk * 256 + (i & 63) * 4 + t4];
+        }
         af[a] = OPA == 1 ? flip(v, asign) : v;
       }
 #pragma unroll
-      for (int b = 0; b < CF::FN; ++b) bf[b] = flip(Bs[kk * BN + wn0 + 8 * b + boff], bsign);
+      for (int b = 0; b < CF::FN; ++b) {
+        double v;
+        if (OPB == 0) v = Bs[kk * BN + wn0 + 8 * b + jl * 4 + tcomp];
+        else v = Bs[((wn0 + 8 * b) / 4 + jl) * 32 + kk * 4 + tcomp];
+        bf[b] = flip(v, bsign);
+      }
 #pragma unroll
       for (int a = 0; a < CF::FM; ++a)
 #pragma unroll
         for (int b = 0; b < CF::FN; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
     }
-  }
-  cp_async_wait<0>();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == S) {
+      stage = 0;
+      phase ^= 1u;
+    }
 
-  if (EPI == EPI_STORE) {
-    const int64_t Nr = 4 * p.Nq;
+    const bool tile_done = ckb + 1 == cnkb;
+    if (tile_done || it + 1 == ie) {
+      // ---------------- epilogue of tile ct ----------------
+      const int ty = ct / p.gx, tx = ct - ty * p.gx;
+      const int64_t i0 = (int64_t)ty * BM, jr0 = (int64_t)tx * BN;
+      const int64_t Nr = 4 * p.Nq;
+      const int tile_first = it - ckb;  // iteration of the tile's k-block 0
+      const bool whole = tile_done && seg_begin == tile_first;
+      if (EPI == EPI_STORE) {
+        if (whole) {
 #pragma unroll
-    for (int a = 0; a < CF::FM; ++a) {
-      const int64_t gi = i0 + wm0 + 8 * a + arow;
-      if (gi >= p.Mq) continue;
+          for (int a = 0; a < CF::FM; ++a) {
+            const int64_t gi = i0 + wm0 + 8 * a + arow;
+            if (gi >= p.Mq) continue;
 #pragma unroll
-      for (int b = 0; b < CF::FN; ++b) {
-        const int64_t gj = jr0 + wn0 + 8 * b + 2 * t;
-        if (gj >= Nr) continue;
-        if (p.work) {
-          double* w = p.work + ((int64_t)blockIdx.z * p.Mq + gi) * Nr + gj;
-          __stcg(reinterpret_cast<double2*>(w), make_double2(acc[a][b][0], acc[a][b][1]));
+            for (int b = 0; b < CF::FN; ++b) {
+              const int64_t gj = jr0 + wn0 + 8 * b + 2 * t4;
+              if (gj >= Nr) continue;
+              double* cp = p.C + gi * p.ldc * 4 + gj;
+              double2 v = make_double2(p.alpha * acc[a][b][0], p.alpha * acc[a][b][1]);
+              if (p.beta != 0.0) {
+                const double2 o = *reinterpret_cast<const double2*>(cp);
+                v.x += p.beta * o.x;
+                v.y += p.beta * o.y;
+              }
+              *reinterpret_cast<double2*>(cp) = v;
+            }
+          }
         } else {
-          double* c = p.C + gi * p.ldc * 4 + gj;
-          double2 v = make_double2(p.alpha * acc[a][b][0], p.alpha * acc[a][b][1]);
-          if (p.beta != 0.0) {
-            double2 o = *reinterpret_cast<const double2*>(c);
-            v.x += p.beta * o.x;
-            v.y += p.beta * o.y;
-          }
-          *reinterpret_cast<double2*>(c) = v;
-        }
-      }
-    }
-    if (p.work) {
-      // Deterministic split-K fix-up: the last CTA to finish this tile sums the
-      // slabs in the fixed order z = 0..S-1 (no separate reduce launch).
-      __shared__ unsigned s_last;
-      __threadfence();
-      __syncthreads();
-      const int64_t tile = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
-      if (tid == 0) s_last = (atomicAdd(&p.counters[tile], 1u) == gridDim.z - 1) ? 1u : 0u;
-      __syncthreads();
-      if (s_last) {
-        __threadfence();
-        const int S = (int)gridDim.z;
-        for (int idx = tid; idx < BM * (BN / 2); idx += CF::THREADS) {
-          const int r = idx / (BN / 2), cc = 2 * (idx % (BN / 2));
-          const int64_t gi = i0 + r, gj = jr0 + cc;
-          if (gi >= p.Mq || gj >= Nr) continue;
-          double sx = 0.0, sy = 0.0;
-          for (int z = 0; z < S; ++z) {
-            const double2 v = __ldcg(reinterpret_cast<const double2*>(p.work + ((int64_t)z * p.Mq + gi) * Nr + gj));
-            sx += v.x;
-            sy += v.y;
-          }
-          double* c = p.C + gi * p.ldc * 4 + gj;
-          double2 o = make_double2(p.alpha * sx, p.alpha * sy);
-          if (p.beta != 0.0) {
-            const double2 old = *reinterpret_cast<const double2*>(c);
-            o.x += p.beta * old.x;
-            o.y += p.beta * old.y;
-          }
-          *reinterpret_cast<double2*>(c) = o;
-        }
-        if (tid == 0) p.counters[tile] = 0u;
-      }
-    }
-  } else {
-    // per tile: [0] sum (X - PR)^2, [1] sum X^2, [2] sum over the imaginary
-    // components of (X - PR)^2 (float PSNR), [3] sum of squared differences of
-    // the u8 images rint(clip(s X, 0, 255)) vs rint(clip(s PR, 0, 255)) over the
-    // imaginary components (imaging.py:90-124 semantics; integers, exact in fp64)
-    __shared__ double red[4][CF::THREADS / 32];
-    const int64_t Nr = 4 * p.Nq;
-    const double s = p.psnr_scale;
-    double v[4] = {0.0, 0.0, 0.0, 0.0};
+          // park the partial tile: slot 0 if this is the CTA's first tile, else slot 1
+          const int slot = (p.mode == MODE_SPLIT || seg_begin == ib) ? 0 : 1;
+          double* sl = p.slots + (int64_t)(c * 2 + slot) * (BM * BN);
 #pragma unroll
-    for (int a = 0; a < CF::FM; ++a) {
-      const int64_t gi = i0 + wm0 + 8 * a + arow;
+          for (int a = 0; a < CF::FM; ++a)
 #pragma unroll
-      for (int b = 0; b < CF::FN; ++b) {
-        const int64_t gj = jr0 + wn0 + 8 * b + 2 * t;
-        if (gi < p.Mq && gj < Nr) {
-          const double2 x = __ldg(reinterpret_cast<const double2*>(p.X + gi * p.ldx * 4 + gj));
-          const double r0 = p.alpha * acc[a][b][0], r1 = p.alpha * acc[a][b][1];
-          const double d0 = x.x - r0, d1 = x.y - r1;
-          v[0] += d0 * d0;
-          v[0] += d1 * d1;
-          v[1] += x.x * x.x;
-          v[1] += x.y * x.y;
-          const bool first_real = (gj & 3) == 0;  // (gj, gj+1) = components (0,1) or (2,3)
-          if (!first_real) v[2] += d0 * d0;
-          v[2] += d1 * d1;
-          if (s > 0.0) {
-            auto u8 = [&](double z) { return rint(fmin(fmax(s * z, 0.0), 255.0)); };
-            const double q1 = u8(x.y) - u8(r1);
-            v[3] += q1 * q1;
-            if (!first_real) {
-              const double q0 = u8(x.x) - u8(r0);
-              v[3] += q0 * q0;
+            for (int b = 0; b < CF::FN; ++b)
+              __stcg(reinterpret_cast<double2*>(sl + (wm0 + 8 * a + arow) * BN + wn0 + 8 * b + 2 * t4),
+                     make_double2(acc[a][b][0], acc[a][b][1]));
+          __threadfence();
+          consumer_sync<CF::CONSUMERS>();
+          if (p.mode == MODE_SPLIT) {
+            // all S parts of this tile run concurrently: meet, then each CTA sums BM/S rows
+            const int nsp = p.splits, o = c / nsp, z = c - o * nsp;
+            if (tid == 0) {
+              atomicAdd(&p.counters[ct], 1u);
+              volatile unsigned* vc = &p.counters[ct];
+              while (*vc < (unsigned)nsp) __nanosleep(64);
+            }
+            consumer_sync<CF::CONSUMERS>();
+            __threadfence();
+            const int r0 = (int)((int64_t)z * BM / nsp), r1 = (int)((int64_t)(z + 1) * BM / nsp);
+            for (int idx = r0 * (BN / 2) + tid; idx < r1 * (BN / 2); idx += CF::CONSUMERS) {
+              const int r = idx / (BN / 2), cc = 2 * (idx % (BN / 2));
+              const int64_t gi = i0 + r, gj = jr0 + cc;
+              if (gi >= p.Mq || gj >= Nr) continue;
+              const double* base = p.slots + (int64_t)(o * nsp) * 2 * (BM * BN) + r * BN + cc;
+              double sx = 0.0, sy = 0.0;
+              for (int k = 0; k < nsp; k += 8) {
+                double2 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                  if (k + u < nsp) v[u] = __ldcg(reinterpret_cast<const double2*>(base + (int64_t)(k + u) * 2 * (BM * BN)));
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                  if (k + u < nsp) {
+                    sx += v[u].x;
+                    sy += v[u].y;
+                  }
+              }
+              double* cp = p.C + gi * p.ldc * 4 + gj;
+              double2 ov = make_double2(p.alpha * sx, p.alpha * sy);
+              if (p.beta != 0.0) {
+                const double2 old = *reinterpret_cast<const double2*>(cp);
+                ov.x += p.beta * old.x;
+                ov.y += p.beta * old.y;
+              }
+              *reinterpret_cast<double2*>(cp) = ov;
+            }
+            consumer_sync<CF::CONSUMERS>();
+            if (tid == 0) {  // the last CTA through resets the tile's tickets
+              if (atomicAdd(&p.counters[65536 + ct], 1u) == (unsigned)nsp - 1) {
+                p.counters[ct] = 0u;
+                p.counters[65536 + ct] = 0u;
+              }
+            }
+          } else {
+            if (tid == 0) {
+              const unsigned mine = (unsigned)(it + 1 - seg_begin);
+              s_flag = (atomicAdd(&p.counters[ct], mine) + mine == (unsigned)cnkb) ? 1u : 0u;
+            }
+            consumer_sync<CF::CONSUMERS>();
+            if (s_flag) {
+              __threadfence();
+              // contributors: CTAs k0..k1 in k order; CTA k's part sits in slot 0 when its
+              // span starts inside this tile, else in slot 1
+              const int64_t T = p.total;
+              const int64_t tile_end = tile_first + cnkb;
+              const int k0 = (int)(((int64_t)(tile_first + 1) * G - 1) / T), k1 = (int)((tile_end * G - 1) / T);
+              for (int idx = tid; idx < BM * (BN / 2); idx += CF::CONSUMERS) {
+                const int r = idx / (BN / 2), cc = 2 * (idx % (BN / 2));
+                const int64_t gi = i0 + r, gj = jr0 + cc;
+                if (gi >= p.Mq || gj >= Nr) continue;
+                double sx = 0.0, sy = 0.0;
+                for (int k = k0; k <= k1; k += 4) {
+                  double2 v[4];
+#pragma unroll
+                  for (int u = 0; u < 4; ++u)
+                    if (k + u <= k1) {
+                      const int64_t ks = (int64_t)(k + u) * T / G;
+                      const int sl2 = ks >= tile_first ? 0 : 1;
+                      v[u] = __ldcg(reinterpret_cast<const double2*>(p.slots + (int64_t)((k + u) * 2 + sl2) * (BM * BN) +
+                                                                     r * BN + cc));
+                    }
+#pragma unroll
+                  for (int u = 0; u < 4; ++u)
+                    if (k + u <= k1) {
+                      sx += v[u].x;
+                      sy += v[u].y;
+                    }
+                }
+                double* cp = p.C + gi * p.ldc * 4 + gj;
+                double2 ov = make_double2(p.alpha * sx, p.alpha * sy);
+                if (p.beta != 0.0) {
+                  const double2 old = *reinterpret_cast<const double2*>(cp);
+                  ov.x += p.beta * old.x;
+                  ov.y += p.beta * old.y;
+                }
+                *reinterpret_cast<double2*>(cp) = ov;
+              }
+              if (tid == 0) p.counters[ct] = 0u;
             }
           }
         }
-      }
-    }
+      } else {
+        // per tile: [0] sum (X - PR)^2, [1] sum X^2, [2] sum over the imaginary
+        // components of (X - PR)^2 (float PSNR), [3] sum of squared differences of
+        // the u8 images rint(clip(s X, 0, 255)) vs rint(clip(s PR, 0, 255)) over the
+        // imaginary components (imaging.py:90-124 semantics; integers, exact in fp64)
+        const double sc = p.psnr_scale;
+        double v[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      v[k] = warp_sum(v[k]);
-      if (lane == 0) red[k][warp] = v[k];
+        for (int a = 0; a < CF::FM; ++a) {
+          const int64_t gi = i0 + wm0 + 8 * a + arow;
+#pragma unroll
+          for (int b = 0; b < CF::FN; ++b) {
+            const int64_t gj = jr0 + wn0 + 8 * b + 2 * t4;
+            if (gi < p.Mq && gj < Nr) {
+              const double2 x = __ldg(reinterpret_cast<const double2*>(p.X + gi * p.ldx * 4 + gj));
+              const double r0 = p.alpha * acc[a][b][0], r1 = p.alpha * acc[a][b][1];
+              const double d0 = x.x - r0, d1 = x.y - r1;
+              v[0] += d0 * d0;
+              v[0] += d1 * d1;
+              v[1] += x.x * x.x;
+              v[1] += x.y * x.y;
+              const bool first_real = (gj & 3) == 0;  // (gj, gj+1) = components (0,1) or (2,3)
+              if (!first_real) v[2] += d0 * d0;
+              v[2] += d1 * d1;
+              if (sc > 0.0) {
+                auto u8 = [&](double z) { return rint(fmin(fmax(sc * z, 0.0), 255.0)); };
+                const double q1 = u8(x.y) - u8(r1);
+                v[3] += q1 * q1;
+                if (!first_real) {
+                  const double q0 = u8(x.x) - u8(r0);
+                  v[3] += q0 * q0;
+                }
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          v[k] = warp_sum(v[k]);
+          if (lane == 0) red[k][warp] = v[k];
+        }
+        consumer_sync<CF::CONSUMERS>();
+        if (tid < 4) {
+          double acc4 = 0.0;
+          for (int w2 = 0; w2 < CF::CONSUMERS / 32; ++w2) acc4 += red[tid][w2];
+          p.partials[4 * ct + tid] = acc4;
+        }
+        consumer_sync<CF::CONSUMERS>();  // red[] is reused by the next tile
+      }
+#pragma unroll
+      for (int a = 0; a < CF::FM; ++a)
+#pragma unroll
+        for (int b = 0; b < CF::FN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+      seg_begin = it + 1;
     }
-    __syncthreads();
-    if (tid < 4) {
-      double acc4 = 0.0;
-      for (int w = 0; w < CF::THREADS / 32; ++w) acc4 += red[tid][w];
-      const int64_t tile = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
-      p.partials[4 * tile + tid] = acc4;
-    }
+    sp.advance(ct, ckb, cnkb);
   }
 }
 
-// Tile configurations (FP64 DMMA: 32x32 warp tiles, >= 2 CTAs per SM).
-//   C0 64x128, 8-quaternion K stages x3   (default; error kernel)
-//   C1 128x64, 4-quaternion K stages x4   (narrow N, e.g. 4r = 800 -> 4% padding instead of 12%)
-//   C2 64x160, 8-quaternion K stages x3   (N multiple of 160, 10 warps)
-// launch_qgemm picks the configuration with the least padded area.
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+// 2-D float64 tensor map: inner extent `w` doubles, `h` rows, row pitch `pitch_q`
+// quaternions, box (bw, bh)
+bool make_map(CUtensorMap* m, const double* base, int64_t w, int64_t h, int64_t pitch_q, int bw, int bh, bool swz) {
+  auto enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)(w > 0 ? w : 1), (cuuint64_t)(h > 0 ? h : 1)};
+  cuuint64_t strides[1] = {(cuuint64_t)(pitch_q * 32)};
+  cuuint32_t box[2] = {(cuuint32_t)bw, (cuuint32_t)bh};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BM, int BN>
+bool make_maps(const double* A, int64_t lda, int opA, const double* B, int64_t ldb, int opB, int64_t Mq, int64_t Nq,
+               int64_t Kq, CUtensorMap* ta, CUtensorMap* tb) {
+  bool ok;
+  if (opA == 0) ok = make_map(ta, A, 4 * Kq, Mq, lda, 16, BM, true);  // A: Mq x Kq
+  else ok = make_map(ta, A, 4 * Mq, Kq, lda, 256, kBKQ, false);     // A stored Kq x Mq
+  if (opB == 0) ok = ok && make_map(tb, B, 4 * Nq, Kq, ldb, BN, kBKQ, false);       // B: Kq x Nq
+  else ok = ok && make_map(tb, B, 4 * Kq, Nq, ldb, 4 * kBKQ, BN / 4, false);        // B stored Nq x Kq
+  return ok;
+}
+
+int num_sms() {
+  static int sms = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+  }();
+  return sms;
+}
+
 struct TileCfg {
-  int bm, bn, bkq;
+  int bm, bn;
 };
-constexpr TileCfg kCfgs[3] = {{64, 128, 8}, {128, 64, 4}, {64, 160, 8}};
-
-template <int BM, int BN, int BKQ, int ST, int OPA, int OPB, int EPI>
-void launch_t(const KParams& kp, dim3 grid, cudaStream_t st) {
-  using CF = Cfg<BM, BN, 32, 32, BKQ, ST, OPA, OPB, EPI>;
-  auto kern = qgemm_kernel<BM, BN, 32, 32, BKQ, ST, OPA, OPB, EPI>;
-  static bool set = false;
-  if (!set) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM);
-    set = true;
-  }
-  ++::qcur::g_launches;
-  kern<<<grid, CF::THREADS, CF::SMEM, st>>>(kp);
-}
-
-template <int OPA, int OPB>
-void launch_ops(int cfg, const KParams& kp, dim3 grid, cudaStream_t st) {
-  if (cfg == 1) launch_t<128, 64, 4, 4, OPA, OPB, EPI_STORE>(kp, grid, st);
-  else if (cfg == 2) launch_t<64, 160, 8, 3, OPA, OPB, EPI_STORE>(kp, grid, st);
-  else launch_t<64, 128, 8, 3, OPA, OPB, EPI_STORE>(kp, grid, st);
-}
+// 0: 64 x 128, 1: 64 x 160 (9 warps at one CTA per SM leave 168 registers per thread:
+// the 32 x 40 warp tile's 80 accumulator registers fit without spills)
+constexpr TileCfg kCfgs[2] = {{64, 128}, {64, 160}};
 
 int pick_cfg(int64_t Mq, int64_t Nq) {
   static const int forced = [] {
     const char* e = getenv("QCUR_GEMM_CFG");  // experiments only: force one tile configuration
     return e ? atoi(e) : -1;
   }();
-  if (forced >= 0 && forced < 3) return forced;
-  // Measured on B200 (cfg2, bench phases): C0 beats C1 / C2 on every product of
-  // the path even where they pad less (C1's 4-quaternion stages and C2's
-  // 96-register cap cost more than the padding saves), so C0 is the default.
+  if (forced >= 0 && forced < 2) return forced;
   (void)Mq;
-  (void)Nq;
-  return 0;
+  const int64_t Nr = 4 * Nq;
+  const int64_t pad128 = (Nr + 127) / 128 * 128, pad160 = (Nr + 159) / 160 * 160;
+  return pad160 < pad128 ? 1 : 0;
 }
 
-int choose_splits(int64_t tiles, int64_t Kq, int bkq) {
-  const int64_t slots = 148 * 2;
-  if (tiles >= 2 * slots) return 1;
-  int64_t sp = (3 * slots + tiles - 1) / tiles;
-  int64_t maxsp = Kq / 32;  // keep >= 32 quaternions of K per split
-  if (sp > maxsp) sp = maxsp;
-  if (sp < 1) sp = 1;
-  if (sp > 64) sp = 64;
-  (void)bkq;
-  return (int)sp;
+int64_t host_total(const TileCfg& c, int64_t gx, int64_t gy, int64_t nkb_full, int b_upper, int herm) {
+  const int64_t W = c.bn / 4, w = W / kBKQ;
+  auto nkb_col = [&](int64_t tx) {
+    if (!b_upper) return nkb_full;
+    const int64_t v = (tx + 1) * w;
+    return v < nkb_full ? v : nkb_full;
+  };
+  if (!herm && !b_upper) return gy * gx * nkb_full;
+  int64_t total = 0;
+  for (int64_t ty = 0; ty < gy; ++ty) {
+    int64_t L = gx - 1;
+    if (herm) {
+      const int64_t l = (ty * c.bm + c.bm - 1) / W;
+      L = l < L ? l : L;
+    }
+    int64_t row = 0;
+    for (int64_t tx = 0; tx <= L; ++tx) row += nkb_col(tx);
+    if (!herm) return row * gy;  // identical rows
+    total += row;
+  }
+  return total;
 }
 
-}  // namespace
-
-size_t qgemm_workspace_bytes(const GemmArgs& g) {
-  const TileCfg& c = kCfgs[pick_cfg(g.Mq, g.Nq)];
-  const int64_t tiles = ((4 * g.Nq + c.bn - 1) / c.bn) * ((g.Mq + c.bm - 1) / c.bm);
-  const int sp = choose_splits(tiles, g.Kq, c.bkq);
-  return sp > 1 ? (size_t)sp * g.Mq * 4 * g.Nq * sizeof(double) : 0;
+int64_t host_active_tiles(const TileCfg& c, int64_t gx, int64_t gy, int herm) {
+  if (!herm) return gx * gy;
+  int64_t n = 0;
+  for (int64_t ty = 0; ty < gy; ++ty) {
+    const int64_t l = (ty * c.bm + c.bm - 1) / (c.bn / 4);
+    n += (l < gx - 1 ? l : gx - 1) + 1;
+  }
+  return n;
 }
 
-void launch_qgemm(const GemmArgs& g, double* workspace, unsigned* counters, cudaStream_t st) {
-  if (g.Mq <= 0 || g.Nq <= 0) return;
-  KParams kp{};
+struct Plan {
+  int cfg;
+  KParams kp;
+  int grid;
+  size_t slot_bytes;
+};
+
+Plan make_plan(const GemmArgs& g) {
+  Plan pl{};
+  pl.cfg = pick_cfg(g.Mq, g.Nq);
+  const TileCfg& c = kCfgs[pl.cfg];
+  KParams& kp = pl.kp;
   kp.Mq = g.Mq;
   kp.Nq = g.Nq;
   kp.Kq = g.Kq;
-  kp.A = g.A;
-  kp.lda = g.lda;
-  kp.B = g.B;
-  kp.ldb = g.ldb;
   kp.C = g.C;
   kp.ldc = g.ldc;
   kp.alpha = g.alpha;
   kp.beta = g.beta;
   kp.b_upper = g.b_upper;
   kp.herm_lower = g.herm_lower;
-  kp.counters = counters;
-  const int cfg = pick_cfg(g.Mq, g.Nq);
-  const TileCfg& c = kCfgs[cfg];
-  const int64_t gx = (4 * g.Nq + c.bn - 1) / c.bn, gy = (g.Mq + c.bm - 1) / c.bm;
-  int sp = g.Kq > 0 ? choose_splits(gx * gy, g.Kq, c.bkq) : 1;
-  if (!workspace || !counters || gx * gy > (1 << 16)) sp = 1;
-  int64_t kchunk = (g.Kq + sp - 1) / sp;
-  kchunk = ((kchunk + 7) / 8) * 8;
-  const int spz = kchunk > 0 ? (int)((g.Kq + kchunk - 1) / kchunk) : 1;
-  kp.kchunk = kchunk > 0 ? kchunk : 8;
-  kp.work = spz > 1 ? workspace : nullptr;
-  dim3 grid((unsigned)gx, (unsigned)gy, (unsigned)spz);
-  if (g.opA == 0 && g.opB == 0) launch_ops<0, 0>(cfg, kp, grid, st);
-  else if (g.opA == 0 && g.opB == 1) launch_ops<0, 1>(cfg, kp, grid, st);
-  else if (g.opA == 1 && g.opB == 0) launch_ops<1, 0>(cfg, kp, grid, st);
-  else launch_ops<1, 1>(cfg, kp, grid, st);
+  kp.gx = (int)((4 * g.Nq + c.bn - 1) / c.bn);
+  kp.gy = (int)((g.Mq + c.bm - 1) / c.bm);
+  kp.nkb_full = g.Kq > 0 ? (int)((g.Kq + kBKQ - 1) / kBKQ) : 1;
+  kp.total = (int)host_total(c, kp.gx, kp.gy, kp.nkb_full, g.b_upper, g.herm_lower);
+  const int64_t G = num_sms();
+  const int64_t ntiles = (int64_t)kp.gx * kp.gy;
+  const int64_t active = host_active_tiles(c, kp.gx, kp.gy, g.herm_lower);
+  int64_t grid;
+  if (ntiles > 65536) {  // beyond the ticket array: whole tiles per CTA (uniform tiles only)
+    kp.mode = MODE_TILES;
+    grid = (!g.b_upper && !g.herm_lower) ? (ntiles < G ? ntiles : G) : 1;
+  } else if (!g.b_upper && 2 * active <= G && kp.nkb_full >= 2) {
+    kp.mode = MODE_SPLIT;
+    int64_t sp = G / active;
+    if (sp > kp.nkb_full) sp = kp.nkb_full;
+    kp.splits = (int)sp;
+    grid = active * sp;
+  } else {
+    kp.mode = MODE_STREAMK;
+    grid = (kp.total + 3) / 4;  // >= 4 k-blocks per CTA
+    if (grid > G) grid = G;
+  }
+  if (grid < 1) grid = 1;
+  pl.grid = (int)grid;
+  pl.slot_bytes = kp.mode == MODE_TILES ? 0 : (size_t)grid * 2 * c.bm * c.bn * sizeof(double);
+  return pl;
 }
 
-int64_t err_partials_count(int64_t m, int64_t n) { return ((4 * n + 128 - 1) / 128) * ((m + 64 - 1) / 64); }
+template <int BM, int BN, int OPA, int OPB, int EPI>
+void launch_k(const CUtensorMap& ta, const CUtensorMap& tb, const KParams& kp, int grid, cudaStream_t st) {
+  using CF = Cfg<BM, BN>;
+  auto fn = qgemm_kernel<BM, BN, OPA, OPB, EPI>;
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM);
+    set = true;
+  }
+  ++::qcur::g_launches;
+  fn<<<grid, CF::THREADS, CF::SMEM, st>>>(ta, tb, kp);
+}
+
+template <int BM, int BN>
+void launch_cfg(const GemmArgs& g, const KParams& kp, int grid, cudaStream_t st) {
+  CUtensorMap ta, tb;
+  if (!make_maps<BM, BN>(g.A, g.lda, g.opA, g.B, g.ldb, g.opB, g.Mq, g.Nq, g.Kq, &ta, &tb)) {
+    // surfaces through the caller's launch check as a CUDA error
+    cudaLaunchKernel((const void*)nullptr, dim3(1), dim3(1), nullptr, 0, st);
+    return;
+  }
+  if (g.opA == 0 && g.opB == 0) launch_k<BM, BN, 0, 0, EPI_STORE>(ta, tb, kp, grid, st);
+  else if (g.opA == 0) launch_k<BM, BN, 0, 1, EPI_STORE>(ta, tb, kp, grid, st);
+  else if (g.opB == 0) launch_k<BM, BN, 1, 0, EPI_STORE>(ta, tb, kp, grid, st);
+  else launch_k<BM, BN, 1, 1, EPI_STORE>(ta, tb, kp, grid, st);
+}
+
+}  // namespace
+
+size_t qgemm_workspace_bytes(const GemmArgs& g) { return make_plan(g).slot_bytes; }
+
+void launch_qgemm(const GemmArgs& g, double* workspace, unsigned* counters, cudaStream_t st) {
+  if (g.Mq <= 0 || g.Nq <= 0) return;
+  Plan pl = make_plan(g);
+  pl.kp.counters = counters;
+  pl.kp.slots = workspace;
+  if (pl.kp.mode != MODE_TILES && pl.grid > 1 && (!workspace || !counters)) {  // no workspace: one span
+    pl.kp.mode = MODE_STREAMK;
+    pl.grid = 1;
+  }
+  if (pl.cfg == 1) launch_cfg<64, 160>(g, pl.kp, pl.grid, st);
+  else launch_cfg<64, 128>(g, pl.kp, pl.grid, st);
+}
+
+// error kernel: 64 x 160 tiles when 4n is a multiple of 160, else 64 x 128
+namespace {
+int err_bn(int64_t n) { return (4 * n) % 160 == 0 ? 160 : 128; }
+}  // namespace
+
+int64_t err_partials_count(int64_t m, int64_t n) {
+  const int bn = err_bn(n);
+  return ((4 * n + bn - 1) / bn) * ((m + 64 - 1) / 64);
+}
 
 void launch_cur_error(const double* X, int64_t ldx, const double* P, int64_t ldp, const double* R, int64_t ldr,
                       int64_t m, int64_t n, int64_t r, double psnr_scale, double* partials, double* out4,
                       cudaStream_t st) {
+  const int bn = err_bn(n);
   KParams kp{};
   kp.Mq = m;
   kp.Nq = n;
   kp.Kq = r;
-  kp.A = P;
-  kp.lda = ldp;
-  kp.B = R;
-  kp.ldb = ldr;
   kp.alpha = 1.0;
-  kp.kchunk = ((r + 7) / 8) * 8;
   kp.X = X;
   kp.ldx = ldx;
   kp.partials = partials;
   kp.psnr_scale = psnr_scale;
-  const int64_t gx = (4 * n + 128 - 1) / 128, gy = (m + 64 - 1) / 64;
-  launch_t<64, 128, 8, 3, 0, 0, EPI_ERR>(kp, dim3((unsigned)gx, (unsigned)gy, 1), st);
-  launch_reduce_rows(partials, gx * gy, 4, out4, st);
+  kp.gx = (int)((4 * n + bn - 1) / bn);
+  kp.gy = (int)((m + 64 - 1) / 64);
+  kp.nkb_full = r > 0 ? (int)((r + kBKQ - 1) / kBKQ) : 1;
+  kp.total = (int)((int64_t)kp.gx * kp.gy * kp.nkb_full);
+  kp.mode = MODE_TILES;
+  const int64_t ntiles = (int64_t)kp.gx * kp.gy, G = num_sms();
+  const int grid = (int)(ntiles < G ? ntiles : G);
+  CUtensorMap ta, tb;
+  bool ok;
+  if (bn == 160) {
+    ok = make_maps<64, 160>(P, ldp, 0, R, ldr, 0, m, n, r, &ta, &tb);
+    if (ok) launch_k<64, 160, 0, 0, EPI_ERR>(ta, tb, kp, grid, st);
+  } else {
+    ok = make_maps<64, 128>(P, ldp, 0, R, ldr, 0, m, n, r, &ta, &tb);
+    if (ok) launch_k<64, 128, 0, 0, EPI_ERR>(ta, tb, kp, grid, st);
+  }
+  if (!ok) cudaLaunchKernel((const void*)nullptr, dim3(1), dim3(1), nullptr, 0, st);
+  launch_reduce_rows(partials, ntiles, 4, out4, st);
 }
 
 }  // namespace qcur

@@ -810,11 +810,11 @@ int qcur_create(int device, qcur_ctx** out) {
     return QCUR_E_CUDA;
   }
   cudaMemset(ctx->status_dev, 0, 64);
-  if (cudaMalloc(&ctx->counters, (size_t)65536 * sizeof(unsigned)) != cudaSuccess) {
+  if (cudaMalloc(&ctx->counters, (size_t)2 * 65536 * sizeof(unsigned)) != cudaSuccess) {
     delete ctx;
     return QCUR_E_CUDA;
   }
-  cudaMemset(ctx->counters, 0, (size_t)65536 * sizeof(unsigned));
+  cudaMemset(ctx->counters, 0, (size_t)2 * 65536 * sizeof(unsigned));
   if (cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {

@@ -9,6 +9,7 @@ import pytest
 import oracle as O
 import paper_2402_19147_b200 as q
 from golden import cases
+from helpers import assert_error_parity, exact_rel_error
 
 pytestmark = pytest.mark.gpu
 G = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden.npz"))
@@ -37,7 +38,12 @@ def test_qmcur_matches_reference_golden(name):
     ref = float(G[f"{name}/rel_err"][0])
     got = q.cur_relative_error(x, f)
     if ref > 1e-12:
-        assert abs(got - ref) <= 1e-10 * ref, (got, ref)
+        xp = tuple(x.planes)
+        cols, rows = G[f"{name}/cols"], G[f"{name}/rows"]
+        exact_ref = exact_rel_error(xp, tuple(p[:, cols] for p in xp), tuple(G[f"{name}/u"]),
+                                    tuple(p[rows, :] for p in xp))
+        exact_got = exact_rel_error(xp, tuple(f.c.planes), tuple(f.u.planes), tuple(f.r.planes))
+        assert_error_parity(got, ref, exact_got, exact_ref)
     else:  # exactly recovered rank-deficient input: both at rounding level
         assert got <= 1e-12
 

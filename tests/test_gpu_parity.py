@@ -14,7 +14,7 @@ import paper_2402_19147_b200 as q
 from paper_2402_19147_b200 import _native
 from paper_2402_19147_b200.cur import DeviceApprox
 from paper_2402_19147_b200.quat import from_device, to_device
-from helpers import lowrank, rand_mat, rel_fro_err
+from helpers import assert_error_parity, exact_rel_error, lowrank, rand_mat, rel_fro_err
 
 pytestmark = pytest.mark.gpu
 
@@ -41,7 +41,9 @@ def check_against_oracle(x, plan, f):
     e2, x2 = O.cur_error(tuple(x.planes), c, u, r)
     ref_err = math.sqrt(e2) / math.sqrt(x2)
     got_err = q.cur_relative_error(x, f)
-    assert abs(got_err - ref_err) <= ERR_TOL * ref_err, (got_err, ref_err)
+    xp = tuple(x.planes)
+    assert_error_parity(got_err, ref_err, exact_rel_error(xp, tuple(f.c.planes), tuple(f.u.planes), tuple(f.r.planes)),
+                        exact_rel_error(xp, c, u, r), ERR_TOL)
     return du
 
 
@@ -273,8 +275,8 @@ def test_intersection_core_device_approx_matches_host_api():
     assert np.array_equal(da.J.cpu().numpy(), f.col_indices)
     got = from_device(da.U, dev)
     assert all(np.array_equal(a, b) for a, b in zip(got.planes, f.u.planes))
-    e2, x2 = O.cur_error(tuple(x.planes), tuple(f.c.planes), tuple(f.u.planes), tuple(f.r.planes))
-    assert abs(da.rel_error() - math.sqrt(e2 / x2)) <= ERR_TOL * math.sqrt(e2 / x2)
+    exact = exact_rel_error(tuple(x.planes), tuple(f.c.planes), tuple(f.u.planes), tuple(f.r.planes))
+    assert abs(da.rel_error() - exact) <= ERR_TOL * exact
 
 
 def test_unknown_core_rejected():
