@@ -14,8 +14,9 @@
 // never materialised (4x less shared memory and L2 traffic than expanding).
 // op(A)=H / op(B)=H read k-major / j-major tiles with the conjugate sign table.
 //
-// CTA = 8 DMMA warps (2 x 4, warp tile WM x WN) + 1 TMA producer warp, one CTA
-// per SM.  The producer streams (A, B) k-block stages into a 5-8 deep ring of
+// CTA = 8 DMMA warps (2 x 4, warp tile WM x WN) + 1 TMA producer warpgroup (one
+// issuing thread; setmaxnreg hands its registers to the DMMA warps), one CTA per SM.
+// The producer streams (A, B) k-block stages into a 5-8 deep ring of
 // shared-memory buffers with cp.async.bulk.tensor (A of op N through the
 // 128-byte swizzle, so the fragment loads are bank-conflict free); full/empty
 // mbarriers hand stages between the roles.  The DMMA warps do no address
@@ -109,18 +110,24 @@ enum { MODE_STREAMK = 0, MODE_SPLIT = 1, MODE_TILES = 2 };
 constexpr int kBKQ = 8;  // quaternions of K per stage
 constexpr int kSmemBudget = 220 * 1024;
 
-template <int BM, int BN>
+template <int BM, int BN, int EPI = 0>
 struct Cfg {
   static constexpr int WARPS_M = 2, WARPS_N = 4;
   static constexpr int WM = BM / WARPS_M, WN = BN / WARPS_N;
   static constexpr int FM = WM / 8, FN = WN / 8;
   static constexpr int CONSUMERS = WARPS_M * WARPS_N * 32;
-  static constexpr int THREADS = CONSUMERS + 32;
+  // + one producer warpgroup (one thread issues TMA; the group exists so setmaxnreg can
+  // move its registers to the two DMMA warpgroups: 8 x 232 + 4 x 40 per SM sub-partition set)
+  static constexpr int THREADS = CONSUMERS + 128;
+  static constexpr int PRODUCER_REGS = 40, CONSUMER_REGS = 232;
   static constexpr int A_BYTES = BM * kBKQ * 32;
   static constexpr int B_BYTES = kBKQ * BN * 8;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = kSmemBudget / STAGE_BYTES > 8 ? 8 : kSmemBudget / STAGE_BYTES;
-  static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 + 2 * STAGES * 8;
+  // EPI_ERR: the epilogue's X tile is staged by TMA too (one BM x BN buffer)
+  static constexpr int X_BYTES = EPI == 1 ? BM * BN * 8 : 0;
+  static constexpr int STAGES =
+      (kSmemBudget - X_BYTES) / STAGE_BYTES > 8 ? 8 : (kSmemBudget - X_BYTES) / STAGE_BYTES;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + X_BYTES + 1024 + (2 * STAGES + 2) * 8;
   static_assert(BM % 64 == 0 && (BN / 4) % kBKQ == 0 && WN % 8 == 0, "tile shape");
   static_assert(STAGE_BYTES % 1024 == 0, "stage buffers must keep the 1024-byte swizzle alignment");
 };
@@ -226,17 +233,20 @@ __device__ __forceinline__ void cta_span(const KParams& p, int& ib, int& ie) {
 }
 
 template <int BM, int BN, int OPA, int OPB, int EPI>
-__global__ void __launch_bounds__(Cfg<BM, BN>::THREADS, 1)
+__global__ void __launch_bounds__(Cfg<BM, BN, EPI>::THREADS, 1)
     qgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 const __grid_constant__ KParams p) {
-  using CF = Cfg<BM, BN>;
+                 const __grid_constant__ CUtensorMap tmX, const __grid_constant__ KParams p) {
+  using CF = Cfg<BM, BN, EPI>;
   constexpr int S = CF::STAGES;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte aligned stage ring (swizzle atoms); offsetting the shared array keeps
   // the fragment loads in the shared window (LDS, not generic LD)
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * CF::STAGE_BYTES);
+  double* xs = reinterpret_cast<double*>(smem + (size_t)S * CF::STAGE_BYTES);  // EPI_ERR X tile
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * CF::STAGE_BYTES + CF::X_BYTES);
   uint64_t* empty = full + S;
+  uint64_t* xfull = empty + S;
+  uint64_t* xempty = xfull + 1;
   __shared__ unsigned s_flag;
   __shared__ double red[4][CF::CONSUMERS / 32];
 
@@ -251,18 +261,21 @@ __global__ void __launch_bounds__(Cfg<BM, BN>::THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], CF::CONSUMERS / 32);
     }
+    mbar_init(xfull, 1);
+    mbar_init(xempty, CF::CONSUMERS / 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  if (warp == CF::CONSUMERS / 32) {
+  if (warp >= CF::CONSUMERS / 32) {
     // ------------------------------ TMA producer ------------------------------
-    if (lane == 0) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(CF::PRODUCER_REGS));
+    if (warp == CF::CONSUMERS / 32 && lane == 0) {
       int t, kb, nkb;
       sp.locate(ib, t, kb);
       nkb = sp.tile_nkb(t);
       int stage = 0;
-      unsigned phase = 0;
+      unsigned phase = 0, xphase = 0;
       for (int it = ib; it < ie; ++it) {
         mbar_wait(&empty[stage], phase ^ 1u);
         unsigned char* As = smem + (size_t)stage * CF::STAGE_BYTES;
@@ -279,6 +292,12 @@ __global__ void __launch_bounds__(Cfg<BM, BN>::THREADS, 1)
         }
         if (OPB == 0) tma_load_2d(Bs, &tmB, jq0 * 4, k0, &full[stage]);  // [8 k][BN reals]
         else tma_load_2d(Bs, &tmB, k0 * 4, jq0, &full[stage]);           // [BN/4 j][8 quaternions]
+        if (EPI == EPI_ERR && kb + 1 == nkb) {  // the tile's X block for the fused error epilogue
+          mbar_wait(xempty, xphase ^ 1u);
+          mbar_expect_tx(xfull, CF::X_BYTES);
+          tma_load_2d(xs, &tmX, tx * BN, i0, xfull);
+          xphase ^= 1u;
+        }
         sp.advance(t, kb, nkb);
         if (++stage == S) {
           stage = 0;
@@ -290,6 +309,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN>::THREADS, 1)
   }
 
   // ------------------------------ DMMA warps ------------------------------
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(CF::CONSUMER_REGS));
   const int wm0 = (warp / CF::WARPS_N) * CF::WM;
   const int wn0 = (warp % CF::WARPS_N) * CF::WN;
   double acc[CF::FM][CF::FN][2];
@@ -312,6 +332,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN>::THREADS, 1)
   int stage = 0;
   unsigned phase = 0;
   const int G = gridDim.x, c = blockIdx.x;
+  unsigned xphase = 0;
   for (int it = ib; it < ie; ++it) {
     mbar_wait(&full[stage], phase);
     const double* As = reinterpret_cast<const double*>(smem + (size_t)stage * CF::STAGE_BYTES);
@@ -490,6 +511,8 @@ __global__ void __launch_bounds__(Cfg<BM, BN>::THREADS, 1)
         // imaginary components (imaging.py:90-124 semantics; integers, exact in fp64)
         const double sc = p.psnr_scale;
         double v[4] = {0.0, 0.0, 0.0, 0.0};
+        mbar_wait(xfull, xphase);
+        xphase ^= 1u;
 #pragma unroll
         for (int a = 0; a < CF::FM; ++a) {
           const int64_t gi = i0 + wm0 + 8 * a + arow;
@@ -497,7 +520,8 @@ __global__ void __launch_bounds__(Cfg<BM, BN>::THREADS, 1)
           for (int b = 0; b < CF::FN; ++b) {
             const int64_t gj = jr0 + wn0 + 8 * b + 2 * t4;
             if (gi < p.Mq && gj < Nr) {
-              const double2 x = __ldg(reinterpret_cast<const double2*>(p.X + gi * p.ldx * 4 + gj));
+              const double2 x =
+                  *reinterpret_cast<const double2*>(xs + (wm0 + 8 * a + arow) * BN + wn0 + 8 * b + 2 * t4);
               const double r0 = p.alpha * acc[a][b][0], r1 = p.alpha * acc[a][b][1];
               const double d0 = x.x - r0, d1 = x.y - r1;
               v[0] += d0 * d0;
@@ -519,6 +543,8 @@ __global__ void __launch_bounds__(Cfg<BM, BN>::THREADS, 1)
             }
           }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(xempty);  // X block consumed
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           v[k] = warp_sum(v[k]);
@@ -695,8 +721,9 @@ Plan make_plan(const GemmArgs& g) {
 }
 
 template <int BM, int BN, int OPA, int OPB, int EPI>
-void launch_k(const CUtensorMap& ta, const CUtensorMap& tb, const KParams& kp, int grid, cudaStream_t st) {
-  using CF = Cfg<BM, BN>;
+void launch_k(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tx, const KParams& kp, int grid,
+              cudaStream_t st) {
+  using CF = Cfg<BM, BN, EPI>;
   auto fn = qgemm_kernel<BM, BN, OPA, OPB, EPI>;
   static bool set = false;
   if (!set) {
@@ -704,7 +731,7 @@ void launch_k(const CUtensorMap& ta, const CUtensorMap& tb, const KParams& kp, i
     set = true;
   }
   ++::qcur::g_launches;
-  fn<<<grid, CF::THREADS, CF::SMEM, st>>>(ta, tb, kp);
+  fn<<<grid, CF::THREADS, CF::SMEM, st>>>(ta, tb, tx, kp);
 }
 
 template <int BM, int BN>
@@ -715,10 +742,10 @@ void launch_cfg(const GemmArgs& g, const KParams& kp, int grid, cudaStream_t st)
     cudaLaunchKernel((const void*)nullptr, dim3(1), dim3(1), nullptr, 0, st);
     return;
   }
-  if (g.opA == 0 && g.opB == 0) launch_k<BM, BN, 0, 0, EPI_STORE>(ta, tb, kp, grid, st);
-  else if (g.opA == 0) launch_k<BM, BN, 0, 1, EPI_STORE>(ta, tb, kp, grid, st);
-  else if (g.opB == 0) launch_k<BM, BN, 1, 0, EPI_STORE>(ta, tb, kp, grid, st);
-  else launch_k<BM, BN, 1, 1, EPI_STORE>(ta, tb, kp, grid, st);
+  if (g.opA == 0 && g.opB == 0) launch_k<BM, BN, 0, 0, EPI_STORE>(ta, tb, tb, kp, grid, st);
+  else if (g.opA == 0) launch_k<BM, BN, 0, 1, EPI_STORE>(ta, tb, tb, kp, grid, st);
+  else if (g.opB == 0) launch_k<BM, BN, 1, 0, EPI_STORE>(ta, tb, tb, kp, grid, st);
+  else launch_k<BM, BN, 1, 1, EPI_STORE>(ta, tb, tb, kp, grid, st);
 }
 
 }  // namespace
@@ -768,14 +795,16 @@ void launch_cur_error(const double* X, int64_t ldx, const double* P, int64_t ldp
   kp.mode = MODE_TILES;
   const int64_t ntiles = (int64_t)kp.gx * kp.gy, G = num_sms();
   const int grid = (int)(ntiles < G ? ntiles : G);
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, tx;
   bool ok;
   if (bn == 160) {
-    ok = make_maps<64, 160>(P, ldp, 0, R, ldr, 0, m, n, r, &ta, &tb);
-    if (ok) launch_k<64, 160, 0, 0, EPI_ERR>(ta, tb, kp, grid, st);
+    ok = make_maps<64, 160>(P, ldp, 0, R, ldr, 0, m, n, r, &ta, &tb) &&
+         make_map(&tx, X, 4 * n, m, ldx, 160, 64, false);
+    if (ok) launch_k<64, 160, 0, 0, EPI_ERR>(ta, tb, tx, kp, grid, st);
   } else {
-    ok = make_maps<64, 128>(P, ldp, 0, R, ldr, 0, m, n, r, &ta, &tb);
-    if (ok) launch_k<64, 128, 0, 0, EPI_ERR>(ta, tb, kp, grid, st);
+    ok = make_maps<64, 128>(P, ldp, 0, R, ldr, 0, m, n, r, &ta, &tb) &&
+         make_map(&tx, X, 4 * n, m, ldx, 128, 64, false);
+    if (ok) launch_k<64, 128, 0, 0, EPI_ERR>(ta, tb, tx, kp, grid, st);
   }
   if (!ok) cudaLaunchKernel((const void*)nullptr, dim3(1), dim3(1), nullptr, 0, st);
   launch_reduce_rows(partials, ntiles, 4, out4, st);
