@@ -703,8 +703,12 @@ Plan make_plan(const GemmArgs& g) {
   if (ntiles > 65536) {  // beyond the ticket array: whole tiles per CTA (uniform tiles only)
     kp.mode = MODE_TILES;
     grid = (!g.b_upper && !g.herm_lower) ? (ntiles < G ? ntiles : G) : 1;
-  } else if (!g.b_upper && 2 * active <= G && kp.nkb_full >= 2) {
+  } else if (2 * active <= G && kp.nkb_full >= 2) {
+    // few tiles: cut each into equal k ranges.  A triangular op(B) runs at full depth
+    // here (its zero triangle is stored as zeros, so the extra products add exact zeros)
     kp.mode = MODE_SPLIT;
+    kp.b_upper = 0;
+    kp.total = (int)host_total(c, kp.gx, kp.gy, kp.nkb_full, 0, g.herm_lower);
     int64_t sp = G / active;
     if (sp > kp.nkb_full) sp = kp.nkb_full;
     kp.splits = (int)sp;

@@ -277,7 +277,7 @@ struct FactorOut {
 
 size_t factor_ws_bytes(int64_t p, int64_t q) {
   size_t b = 0;
-  b += qbytes(p, q) * 3;        // Q1, Zcm, Qcm
+  b += qbytes(p, q) * 2;        // Zcm, Qcm
   b += qbytes(q, q) * 12;       // G1, L1, L1inv, G2, L2, L2inv, T, Tcm, Vcm, ...
   b += (size_t)(q + 8) * 8 * 4;  // betas, sigma
   GemmArgs g{};
@@ -406,7 +406,7 @@ int factor_multi(qcur_ctx* ctx, const FactorSpec* specs, int ns) {
   cudaStream_t st = ctx->stream;
   unsigned* status = ctx->status_dev;
   struct Bufs {
-    double *G1, *L1, *L1i, *Q1, *G2, *L2, *L2i, *T, *betas, *Zcm, *Qcm, *Tcm, *Vcm, *gws;
+    double *G1, *L1, *L1i, *G2, *L2, *L2i, *T, *betas, *Zcm, *Qcm, *Tcm, *Vcm, *gws;
   } B[2];
   for (int k = 0; k < ns; ++k) {
     const int64_t p = specs[k].p, q = specs[k].q;
@@ -414,7 +414,6 @@ int factor_multi(qcur_ctx* ctx, const FactorSpec* specs, int ns) {
     b.G1 = ctx->take<double>((size_t)(q * q * 4));
     b.L1 = ctx->take<double>((size_t)(q * q * 4));
     b.L1i = ctx->take<double>((size_t)(q * q * 4));
-    b.Q1 = ctx->take<double>((size_t)(p * q * 4));
     b.G2 = ctx->take<double>((size_t)(q * q * 4));
     b.L2 = ctx->take<double>((size_t)(q * q * 4));
     b.L2i = ctx->take<double>((size_t)(q * q * 4));
@@ -428,7 +427,7 @@ int factor_multi(qcur_ctx* ctx, const FactorSpec* specs, int ns) {
     GemmArgs probe2 = gargs(q, q, p, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0);
     size_t w1 = qgemm_workspace_bytes(probe), w2 = qgemm_workspace_bytes(probe2);
     b.gws = ctx->take<double>((w1 > w2 ? w1 : w2) / 8 + 16);
-    if (!b.G1 || !b.L1 || !b.L1i || !b.Q1 || !b.G2 || !b.L2 || !b.L2i || !b.T || !b.betas || !b.Zcm || !b.Qcm ||
+    if (!b.G1 || !b.L1 || !b.L1i || !b.G2 || !b.L2 || !b.L2i || !b.T || !b.betas || !b.Zcm || !b.Qcm ||
         !b.Tcm || !b.Vcm || !b.gws)
       return ctx->fail(QCUR_E_CUDA, "workspace exhausted (factor)");
   }
@@ -487,15 +486,15 @@ int factor_multi(qcur_ctx* ctx, const FactorSpec* specs, int ns) {
     if (rc) return rc;
   }
   if ((rc = chol_inv(false))) return rc;
-  // Q1 = Z L1^{-H};  G2 = Q1^H Q1
+  // Q1 = Z L1^{-H} (written straight into the output Q);  G2 = Q1^H Q1
   for (int k = 0; k < ns; ++k) {
     if (!fast[k]) continue;
     const FactorSpec& f = specs[k];
     const int64_t p = f.p, q = f.q;
-    if (!f.zh) rc = gemm(ctx, with_flags(gargs(p, q, q, f.src, q, 0, B[k].L1i, q, 1, B[k].Q1, q), 1, 0), B[k].gws);
-    else rc = gemm(ctx, with_flags(gargs(p, q, q, f.src, p, 1, B[k].L1i, q, 1, B[k].Q1, q), 1, 0), B[k].gws);
+    if (!f.zh) rc = gemm(ctx, with_flags(gargs(p, q, q, f.src, q, 0, B[k].L1i, q, 1, f.out.Q, q), 1, 0), B[k].gws);
+    else rc = gemm(ctx, with_flags(gargs(p, q, q, f.src, p, 1, B[k].L1i, q, 1, f.out.Q, q), 1, 0), B[k].gws);
     if (rc) return rc;
-    if ((rc = gemm(ctx, with_flags(gargs(q, q, p, B[k].Q1, q, 1, B[k].Q1, q, 0, B[k].G2, q), 0, 1), B[k].gws)))
+    if ((rc = gemm(ctx, with_flags(gargs(q, q, p, f.out.Q, q, 1, f.out.Q, q, 0, B[k].G2, q), 0, 1), B[k].gws)))
       return rc;
   }
   // second pass: G2 = I + E with E ~ kappa^2 u; L2^{-1} by a second-order series
@@ -512,17 +511,21 @@ int factor_multi(qcur_ctx* ctx, const FactorSpec* specs, int ns) {
     launch_series_final(M1, P2, q, b.L2i, st);
     CK_LAUNCH(ctx, "series");
   }
-  // Q = Q1 L2^{-H};  F = T^{-1} = L1^{-H} L2^{-H};  kappa_F(T) = ||C||_F ||F||_F = sqrt(tr G1) ||F||_F
+  // Z = Q T with Q = Q1 L2^{-H}, T = L2^H L1^H.  The tall product Q1 L2^{-H} is never
+  // formed: pinv(Z) = T^{-1} Q^H = (T^{-1} L2^{-1}) Q1^H, so the factor pair is
+  // (Q1, F = T^{-1} L2^{-1}) and every consumer (X Q_R, Q_C^H Y, F Q^H) applies the
+  // well-conditioned L2^{-1} (kappa ~ 1 + kappa(Z)^2 u) on the small side instead.
+  // kappa_F(T) = ||Z||_F ||T^{-1}||_F = sqrt(tr G1) ||T^{-1}||_F guards the fast path.
   for (int k = 0; k < ns; ++k) {
     if (!fast[k]) continue;
     const FactorSpec& f = specs[k];
-    const int64_t p = f.p, q = f.q;
-    if ((rc = gemm(ctx, with_flags(gargs(p, q, q, B[k].Q1, q, 0, B[k].L2i, q, 1, f.out.Q, q), 1, 0), B[k].gws)))
+    const int64_t q = f.q;
+    double* Tinv = B[k].T;
+    if ((rc = gemm(ctx, with_flags(gargs(q, q, q, B[k].L1i, q, 1, B[k].L2i, q, 1, Tinv, q), 1, 0), B[k].gws)))
       return rc;
-    if ((rc = gemm(ctx, with_flags(gargs(q, q, q, B[k].L1i, q, 1, B[k].L2i, q, 1, f.out.F, q), 1, 0), B[k].gws)))
-      return rc;
-    launch_kappa_check(B[k].G1, f.out.F, q, ctx->kappa_limit, status, f.fail_bit, st);
+    launch_kappa_check(B[k].G1, Tinv, q, ctx->kappa_limit, status, f.fail_bit, st);
     CK_LAUNCH(ctx, "kappa");
+    if ((rc = gemm(ctx, gargs(q, q, q, Tinv, q, 0, B[k].L2i, q, 0, f.out.F, q), B[k].gws))) return rc;
   }
   // robust path, gated on each fail_bit (no-op launches when the fast path held)
   for (int k = 0; k < ns; ++k) {

@@ -320,9 +320,12 @@ def approx_rowsharded(ops, comm, xb, m: int, strategy: str, seed: int, c: int, r
     Q1 = ops.gemm(Cb, X1, opB=1, flags=1)
     G2 = comm.all_reduce_sum(ops.gemm(Q1, Q1, opA=1, flags=2))
     L2i = ops.series(G2)
-    QC = ops.gemm(Q1, L2i, opB=1, flags=1)
-    FC = ops.gemm(X1, L2i, opA=1, opB=1, flags=1)
-    ops.kappa(G1, FC)
+    # (Q1, T^-1 L2^-1) as in the monolithic factor (qcur_abi.cu factor_multi): the tall
+    # product Q1 L2^-H is never formed
+    QC = Q1
+    Tinv = ops.gemm(X1, L2i, opA=1, opB=1, flags=1)
+    ops.kappa(G1, Tinv)
+    FC = ops.gemm(Tinv, L2i)
     failed = ops.fast_failed()
     if comm.all_max(1 if failed else 0):  # robust path: factor the gathered C locally
         Cfull = comm.all_gather_cat(Cb)
