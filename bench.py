@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import argparse
 import json
+from pathlib import Path
 import math
 import os
 import statistics
@@ -80,6 +81,20 @@ def alg_counts(cfg: dict) -> dict:
         length_bytes=32.0 * m * n,
         gather_bytes=64.0 * (m * c + r * n),
     )
+
+
+def ncu_traffic(cfg_name: str, kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel, from the
+    committed `ncu --set full` capture summary (profiles/*_ncu_traffic_<cfg>.json, written by
+    tools/ncu_traffic.py); (None, None) when no capture of this config exists."""
+    files = sorted(Path(__file__).resolve().parent.glob(f"profiles/*_ncu_traffic_{cfg_name}.json"))
+    if not files:
+        return None, None
+    try:
+        d = json.loads(files[-1].read_text())
+        return float(d[kernel]["traffic_bytes"]), f"{files[-1].name}: {d[kernel]['kernel']}"
+    except (KeyError, TypeError, ValueError):
+        return None, None
 
 
 def load_peaks() -> dict:
@@ -414,10 +429,11 @@ def main() -> None:
     dom_ms = per_approx.get(dom, float("nan"))
     dom_flop = counts["gemm_xq_flop"] if dom == "gemm_xq" else counts["error_flop"]
     achieved = dom_flop / (dom_ms * 1e-3) / 1e12
+    traffic, traffic_src = ncu_traffic(args.config, "gemm_xq" if dom == "gemm_xq" else "error")
     roofline = {
         "kernel": "qgemm_kernel<EPI_ERR> (fused C U R + error)" if dom == "error" else "qgemm_kernel (Y = X Q_R)",
         "bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-        "frac": achieved / peak_tf if peak_tf else None, "traffic": None,
+        "frac": achieved / peak_tf if peak_tf else None, "traffic": traffic, "traffic_source": traffic_src,
         "peak_source": "FP64 DMMA (mma.sync m8n8k4 f64) peak measured live on this GPU by qcur_fp64_peak_tflops; "
                        "MEASURED_PEAKS.json has no FP64 figure",
         "algorithmic_flop_per_launch": dom_flop, "avg_launch_ms": dom_ms,
