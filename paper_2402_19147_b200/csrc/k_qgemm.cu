@@ -150,6 +150,7 @@ struct KParams {
   int total;           // iterations (sum of k-blocks over tiles, < 2^31)
   int mode;
   int splits;          // MODE_SPLIT: CTAs per tile
+  int waves;           // MODE_STREAMK: rounds of whole tiles before the stream-K tail
 };
 
 // Iteration space bookkeeping (closed form).
@@ -215,21 +216,38 @@ struct Space {
   }
 };
 
-// this CTA's span [ib, ie) of the iteration list
-__device__ __forceinline__ void cta_span(const KParams& p, int& ib, int& ie) {
+// Span s of this CTA: [sb, se) in the iteration list; false past the last span.
+//  * whole tiles: one contiguous run of tiles (the error kernel);
+//  * split: one equal k range of one tile;
+//  * stream-K: `waves` rounds of whole tiles (tile w*G + c: CTAs in lock step work on
+//    neighbouring tiles, so each A row block is fetched from HBM once and the other
+//    column tiles hit L2), then one contiguous span of the remaining tiles' iterations.
+__device__ __forceinline__ bool cta_span(const KParams& p, int s, int& sb, int& se) {
   const int G = gridDim.x, c = blockIdx.x;
-  if (p.mode == MODE_TILES) {  // uniform tiles, whole tiles per CTA
-    const int ntiles = p.gx * p.gy;
-    ib = (int)((int64_t)c * ntiles / G) * p.nkb_full;
-    ie = (int)((int64_t)(c + 1) * ntiles / G) * p.nkb_full;
-  } else if (p.mode == MODE_SPLIT) {
-    const int o = c / p.splits, z = c - o * p.splits;
-    ib = o * p.nkb_full + (int)((int64_t)z * p.nkb_full / p.splits);
-    ie = o * p.nkb_full + (int)((int64_t)(z + 1) * p.nkb_full / p.splits);
-  } else {
-    ib = (int)((int64_t)c * p.total / G);
-    ie = (int)((int64_t)(c + 1) * p.total / G);
+  if (s < p.waves) {
+    const int t = c + s * G;
+    sb = t * p.nkb_full;
+    se = sb + p.nkb_full;
+    return true;
   }
+  if (s > p.waves) return false;
+  if (p.mode == MODE_TILES) {
+    const int ntiles = p.gx * p.gy;
+    sb = (int)((int64_t)c * ntiles / G) * p.nkb_full;
+    se = (int)((int64_t)(c + 1) * ntiles / G) * p.nkb_full;
+    return true;
+  }
+  if (p.mode == MODE_SPLIT) {
+    const int o = c / p.splits, z = c - o * p.splits;
+    sb = o * p.nkb_full + (int)((int64_t)z * p.nkb_full / p.splits);
+    se = o * p.nkb_full + (int)((int64_t)(z + 1) * p.nkb_full / p.splits);
+    return true;
+  }
+  const int base = p.waves * G * p.nkb_full;
+  const int64_t tail = (int64_t)p.total - base;
+  sb = base + (int)((int64_t)c * tail / G);
+  se = base + (int)((int64_t)(c + 1) * tail / G);
+  return true;
 }
 
 template <int BM, int BN, int OPA, int OPB, int EPI>
@@ -252,9 +270,10 @@ __global__ void __launch_bounds__(Cfg<BM, BN, EPI>::THREADS, 1)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const Space<BM, BN> sp(p);
-  int ib, ie;
-  cta_span(p, ib, ie);
-  if (ib >= ie) return;
+  {
+    int sb, se;
+    if (!cta_span(p, 0, sb, se) || sb >= se) return;
+  }
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
@@ -271,12 +290,14 @@ __global__ void __launch_bounds__(Cfg<BM, BN, EPI>::THREADS, 1)
     // ------------------------------ TMA producer ------------------------------
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(CF::PRODUCER_REGS));
     if (warp == CF::CONSUMERS / 32 && lane == 0) {
-      int t, kb, nkb;
-      sp.locate(ib, t, kb);
-      nkb = sp.tile_nkb(t);
       int stage = 0;
       unsigned phase = 0, xphase = 0;
-      for (int it = ib; it < ie; ++it) {
+      int sb, se;
+      for (int sidx = 0; cta_span(p, sidx, sb, se); ++sidx) {
+      int t, kb, nkb;
+      sp.locate(sb, t, kb);
+      nkb = sp.tile_nkb(t);
+      for (int it = sb; it < se; ++it) {
         mbar_wait(&empty[stage], phase ^ 1u);
         unsigned char* As = smem + (size_t)stage * CF::STAGE_BYTES;
         unsigned char* Bs = As + CF::A_BYTES;
@@ -304,6 +325,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, EPI>::THREADS, 1)
           phase ^= 1u;
         }
       }
+      }
     }
     return;
   }
@@ -325,14 +347,16 @@ __global__ void __launch_bounds__(Cfg<BM, BN, EPI>::THREADS, 1)
   const int arow = lane >> 2;
   const int tcomp = t4 ^ s4;
 
-  int ct, ckb, cnkb;
-  sp.locate(ib, ct, ckb);
-  cnkb = sp.tile_nkb(ct);
-  int seg_begin = ib;
   int stage = 0;
   unsigned phase = 0;
   const int G = gridDim.x, c = blockIdx.x;
   unsigned xphase = 0;
+  int ib, ie;
+  for (int sidx = 0; cta_span(p, sidx, ib, ie); ++sidx) {
+  int ct, ckb, cnkb;
+  sp.locate(ib, ct, ckb);
+  cnkb = sp.tile_nkb(ct);
+  int seg_begin = ib;
   for (int it = ib; it < ie; ++it) {
     mbar_wait(&full[stage], phase);
     const double* As = reinterpret_cast<const double*>(smem + (size_t)stage * CF::STAGE_BYTES);
@@ -464,11 +488,13 @@ __global__ void __launch_bounds__(Cfg<BM, BN, EPI>::THREADS, 1)
             consumer_sync<CF::CONSUMERS>();
             if (s_flag) {
               __threadfence();
-              // contributors: CTAs k0..k1 in k order; CTA k's part sits in slot 0 when its
-              // span starts inside this tile, else in slot 1
-              const int64_t T = p.total;
-              const int64_t tile_end = tile_first + cnkb;
-              const int k0 = (int)(((int64_t)(tile_first + 1) * G - 1) / T), k1 = (int)((tile_end * G - 1) / T);
+              // contributors (stream-K tail, iterations counted from its base): CTAs k0..k1 in
+              // k order; CTA k's part sits in slot 0 when its span starts inside this tile,
+              // else in slot 1
+              const int base = p.waves * G * p.nkb_full;
+              const int64_t T = (int64_t)p.total - base;
+              const int64_t tf = tile_first - base, tile_end = tf + cnkb;
+              const int k0 = (int)(((tf + 1) * G - 1) / T), k1 = (int)((tile_end * G - 1) / T);
               for (int idx = tid; idx < BM * (BN / 2); idx += CF::CONSUMERS) {
                 const int r = idx / (BN / 2), cc = 2 * (idx % (BN / 2));
                 const int64_t gi = i0 + r, gj = jr0 + cc;
@@ -480,7 +506,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, EPI>::THREADS, 1)
                   for (int u = 0; u < 4; ++u)
                     if (k + u <= k1) {
                       const int64_t ks = (int64_t)(k + u) * T / G;
-                      const int sl2 = ks >= tile_first ? 0 : 1;
+                      const int sl2 = ks >= tf ? 0 : 1;
                       v[u] = __ldcg(reinterpret_cast<const double2*>(p.slots + (int64_t)((k + u) * 2 + sl2) * (BM * BN) +
                                                                      r * BN + cc));
                     }
@@ -565,6 +591,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, EPI>::THREADS, 1)
       seg_begin = it + 1;
     }
     sp.advance(ct, ckb, cnkb);
+  }
   }
 }
 
@@ -717,6 +744,9 @@ Plan make_plan(const GemmArgs& g) {
     kp.mode = MODE_STREAMK;
     grid = (kp.total + 3) / 4;  // >= 4 k-blocks per CTA
     if (grid > G) grid = G;
+    // deep uniform GEMMs (X Q_R): whole-tile rounds first so the X row blocks are read
+    // from HBM about once; stream-K only over the remainder
+    if (!g.b_upper && !g.herm_lower && grid == G && kp.nkb_full >= 64) kp.waves = (int)(ntiles / G);
   }
   if (grid < 1) grid = 1;
   pl.grid = (int)grid;
