@@ -49,7 +49,8 @@ __host__ __device__ inline Levels make_levels(double* work, int64_t len) {
   return L;
 }
 
-int64_t draw_work_doubles(int64_t len) {
+// work buffer: p (len) | tree levels | 64 slack | uniforms (count <= len)
+__host__ __device__ inline int64_t draw_uniform_offset(int64_t len) {
   int64_t total = len, s = len;
   while (s > 32) {
     s = (s + 31) / 32;
@@ -57,6 +58,8 @@ int64_t draw_work_doubles(int64_t len) {
   }
   return total + 64;
 }
+
+int64_t draw_work_doubles(int64_t len) { return draw_uniform_offset(len) + len; }
 
 // recompute node `node` of level h (h >= 1) from its 32 children; called by a full warp
 __device__ __forceinline__ void refresh_node(const Levels& L, int h, int64_t node, int lane) {
@@ -104,6 +107,17 @@ __global__ void __launch_bounds__(1024) k2_draw(DrawJobs jobs, unsigned* status)
     for (int64_t node = warp; node < L.sz[h]; node += nw) refresh_node(L, h, node, lane);
     __syncthreads();
   }
+  // the draw's uniforms: uniform t is the stream advanced by t (numpy draws one
+  // double per draw, columns first), computed in parallel instead of in the chain
+  double* uni = job.work + draw_uniform_offset(len);
+  for (int64_t t = tid; t < job.count; t += blockDim.x) {
+    Pcg64 g;
+    g.state = u128{job.st_hi, job.st_lo};
+    g.inc = u128{job.inc_hi, job.inc_lo};
+    g.advance((uint64_t)t);
+    uni[t] = g.next_double();
+  }
+  __syncthreads();
   if (warp != 0) return;
   int positive = 0;
   for (int w = 0; w < nw; ++w) positive += s_pos[w];
@@ -113,34 +127,30 @@ __global__ void __launch_bounds__(1024) k2_draw(DrawJobs jobs, unsigned* status)
     for (int64_t t = lane; t < job.count; t += 32) job.out[t] = 0;
     return;
   }
-  Pcg64 rng;
-  rng.state = u128{job.st_hi, job.st_lo};
-  rng.inc = u128{job.inc_hi, job.inc_lo};
   const double u53 = 1.0 / 9007199254740992.0;
-  for (int64_t t = 0; t < job.count; ++t) {
-    const double u = rng.next_double();  // identical on every lane
-    // total from the top level
-    double tv = lane < L.sz[L.top] ? L.lev[L.top][lane] : 0.0;
-    const double total = warp_sum(tv);
-    if (!(total > 0.0)) {
-      if (lane == 0) atomicOr(status, (unsigned)ST_SAMPLING);
-      for (int64_t q = t + lane; q < job.count; q += 32) job.out[q] = 0;
-      return;
-    }
-    const double target = u * total;
-    // descend
-    double base = 0.0, lower = 0.0, upper = 0.0;
-    int64_t g = 0;
+  const int count = (int)job.count;
+  double u_next = uni[0];
+  for (int t = 0; t < count; ++t) {
+    const double u = u_next;  // identical on every lane
+    if (t + 1 < count) u_next = uni[t + 1];
+    // descend; the top level's inclusive scan also yields the total
+    double base = 0.0, lower = 0.0, upper = 0.0, total = 0.0, target = 0.0;
+    int g = 0;
     bool ok = true;
     for (int h = L.top; h >= 0; --h) {
-      const int64_t c = g * 32 + lane;
-      const bool valid = c < L.sz[h];
+      const int c = g * 32 + lane;
+      const bool valid = c < (int)L.sz[h];
       double s = valid ? L.lev[h][c] : 0.0;
       // inclusive Hillis-Steele scan (fixed order)
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         double y = __shfl_up_sync(0xffffffffu, s, o);
         if (lane >= o) s += y;
+      }
+      if (h == L.top) {
+        total = __shfl_sync(0xffffffffu, s, 31);
+        if (!(total > 0.0)) break;
+        target = u * total;
       }
       const double posv = base + s;
       const unsigned hit = __ballot_sync(0xffffffffu, valid && posv > target);
@@ -158,6 +168,11 @@ __global__ void __launch_bounds__(1024) k2_draw(DrawJobs jobs, unsigned* status)
       }
       base = nb;
       g = g * 32 + k;
+    }
+    if (!(total > 0.0)) {
+      if (lane == 0) atomicOr(status, (unsigned)ST_SAMPLING);
+      for (int q = t + lane; q < count; q += 32) job.out[q] = 0;
+      return;
     }
     int64_t idx = g;
     if (ok) {
@@ -194,7 +209,7 @@ __global__ void __launch_bounds__(1024) k2_draw(DrawJobs jobs, unsigned* status)
       L.lev[0][idx] = 0.0;
     }
     __syncwarp();
-    int64_t node = idx;
+    int node = (int)idx;
     for (int h = 1; h <= L.top; ++h) {
       node >>= 5;
       refresh_node(L, h, node, lane);
@@ -208,7 +223,7 @@ void launch_draw(const DrawJob* jobs, int njobs, unsigned* status, cudaStream_t 
   for (int k = 0; k < njobs && k < 2; ++k) {
     j.j[k] = jobs[k];
     const int64_t len = jobs[k].len;
-    const int64_t tree = draw_work_doubles(len) - len;  // levels >= 1 (+ slack)
+    const int64_t tree = draw_uniform_offset(len) - len;  // levels >= 1 (+ slack)
     const int64_t need = (len <= kDrawSmemMaxLen ? len : 0) + tree;
     if ((size_t)need * sizeof(double) > smem) smem = (size_t)need * sizeof(double);
   }
