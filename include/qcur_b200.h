@@ -111,6 +111,25 @@ int qcur_qmcur_host(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, co
                     int core, int64_t* col_idx_dev, int64_t* row_idx_dev, double* c_dev, double* u_dev,
                     double* r_dev, int64_t* col_idx_host, int64_t* row_idx_host, double* const c_host[4],
                     double* const u_host[4], double* const r_host[4]);
+/* C = X[:, J], R = X[I, :], U = pinv(C) X pinv(R) for given index sets: the factors of
+ * stabilized_reconstruct (cur.py:277-286).  J, I: device int64. */
+int qcur_cur_given(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, const int64_t* col_idx_dev,
+                   int64_t num_cols, const int64_t* row_idx_dev, int64_t num_rows, double* c_dev, double* u_dev,
+                   double* r_dev);
+/* ---- low-rank completion (Algorithm 2; completion.py) ---- */
+/* out = mask ? y : x elementwise (project_observed, completion.py:101-111); mask: m x n bytes,
+ * nonzero = observed. */
+int qcur_project_observed(qcur_ctx* ctx, const double* x_dev, const double* y_dev, const unsigned char* mask_dev,
+                          int64_t m, int64_t n, double* out_dev);
+/* One completion sweep on the device iterate cur (completion.py:204-219): sample count rows and
+ * columns (make_plan with `strategy` and the PCG64 `state`, or the given fixed index sets for
+ * index_policy "fixed" = stabilized_reconstruct), reconstruct C U R, restore the observed entries
+ * into out_dev and return stats4_dev = {||out - cur||_F^2, ||cur||_F^2, 0, 0}.  J_out / I_out
+ * (nullable, device) receive the index sets.  Synchronizes; maps degenerate draws to status codes. */
+int qcur_complete_sweep(qcur_ctx* ctx, const double* cur_dev, const double* y_dev, const unsigned char* mask_dev,
+                        int64_t m, int64_t n, int strategy, const uint64_t state[4], int64_t count,
+                        const int64_t* fixed_J, const int64_t* fixed_I, int64_t* J_out, int64_t* I_out,
+                        double* out_dev, double* stats4_dev);
 /* Error statistics of X - C U R without forming CUR (callers: cli.py:173-175,
  * bench.py:257-258, imaging.py:170-177).  out4_dev (4 doubles, device):
  *   [0] ||X - CUR||_F^2   [1] ||X||_F^2   [2] imaginary-part ||X - CUR||^2 (float PSNR)

@@ -224,3 +224,79 @@ def lowrank_planes(rng: np.random.Generator, m: int, n: int, k: int):
         for s in range(4):
             out[s] = out[s] + prod[s]
     return tuple(out)
+
+
+# ---------------------------------------------------------------------------
+# low-rank completion, Algorithm 2 (completion.py) — the first "next" row of SURVEY §8(f)
+# ---------------------------------------------------------------------------
+def derive_seed(seed: int, *parts) -> int:
+    """bench.py:72-80."""
+    import hashlib
+
+    text = "\x1f".join(str(p) for p in parts)
+    digest = hashlib.blake2b(text.encode("utf-8"), digest_size=8).digest()
+    return (int(seed) ^ int.from_bytes(digest, "little")) & ((1 << 64) - 1)
+
+
+def random_mask(m: int, n: int, missing_ratio: float, seed: int) -> np.ndarray:
+    """completion.py:82-98 (boolean observed map)."""
+    total = m * n
+    count = round(missing_ratio * total)
+    observed = np.ones(total, dtype=bool)
+    if count:
+        observed[np.random.default_rng(seed).permutation(total)[:count]] = False
+    return observed.reshape(m, n)
+
+
+def project_observed(x, observed, y):
+    """completion.py:101-111."""
+    return tuple(np.where(observed, yp, xp) for xp, yp in zip(x, y))
+
+
+def stabilized_reconstruct(planes, rows, cols):
+    """cur.py:277-286: C pinv(C) X pinv(R) R for given index sets."""
+    c = tuple(np.ascontiguousarray(p[:, cols]) for p in planes)
+    r = tuple(np.ascontiguousarray(p[rows, :]) for p in planes)
+    u = qmatmul(qmatmul(pinv(c), planes), pinv(r))
+    return qmatmul(qmatmul(c, u), r)
+
+
+def complete(y, observed, rank: int, strategy: str = "length", max_iters: int = 200, rel_tol: float = 1e-4,
+             index_policy: str = "resample_each_iter", seed: int = 0):
+    """completion.py:157-246: alternating CUR approximation + observed-entry re-projection.
+    Returns (x_star planes, history list, converged)."""
+    m, n = y[0].shape
+    current = project_observed(tuple(np.zeros((m, n)) for _ in range(4)), observed, y)
+    count = min(rank + 5, m, n)
+
+    def dists(planes):
+        return length_distributions(planes) if strategy == "length" else uniform_distributions(m, n)
+
+    fixed = None
+    if index_policy == "fixed":
+        colp, rowp = dists(current)
+        fixed = plan_indices(colp, rowp, count, count, derive_seed(seed, "draw"))
+    history = []
+    converged = False
+    for t in range(max_iters):
+        if fixed is not None:
+            approx_p = stabilized_reconstruct(current, fixed[0], fixed[1])
+        else:
+            colp, rowp = dists(current)
+            rows, cols, c, u, r = qmcur(current, colp, rowp, count, count, derive_seed(seed, "sweep", t))
+            approx_p = qmatmul(qmatmul(c, u), r)
+        updated = project_observed(approx_p, observed, y)
+        step = math.sqrt(frob2(tuple(a - b for a, b in zip(updated, current))))
+        scale = math.sqrt(frob2(current))
+        if scale > 0.0:
+            rel = step / scale
+        elif step <= 1e-15:
+            rel = 0.0
+        else:
+            rel = float("inf")
+        history.append(float(rel))
+        current = updated
+        if rel <= rel_tol:
+            converged = True
+            break
+    return current, history, converged

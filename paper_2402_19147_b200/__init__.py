@@ -3,7 +3,8 @@
 Drop-in for the reference package's QMCUR path (``qcur``: make_plan, qmcur,
 cur_reconstruct, draw_indices, plan_indices, length/uniform distributions,
 pseudoinverse, qmat_matmul, the error classes and the QMatrix/Quaternion
-types).  All numerics run in hand-written sm_100a CUDA behind the C ABI in
+types), plus the first "next" row: the completion solver (``complete``,
+Algorithm 2) with GPU-resident sweeps.  All numerics run in hand-written sm_100a CUDA behind the C ABI in
 include/qcur_b200.h; there is no CPU fallback.
 """
 from .errors import (
@@ -30,9 +31,20 @@ from .cur import (
     plan_indices,
     qmcur,
     qmcur_device,
+    stabilized_reconstruct,
     uniform_distributions,
 )
 from .linalg import pseudoinverse
+from .completion import (
+    INDEX_POLICIES,
+    CompletionConfig,
+    CompletionResult,
+    ObservationMask,
+    complete,
+    derive_seed,
+    project_observed,
+    random_mask,
+)
 
 __all__ = [
     "QcurError", "ShapeError", "ParameterError", "FileFormatError", "DegenerateDistributionError",
@@ -40,6 +52,8 @@ __all__ = [
     "QMatrix", "Quaternion", "qmat_matmul", "qmat_conj_transpose", "qmat_frobenius_norm",
     "STRATEGIES", "SamplingPlan", "CURFactors", "length_distributions", "uniform_distributions",
     "default_sample_counts", "make_plan", "draw_indices", "plan_indices", "qmcur", "cur_reconstruct",
-    "cur_relative_error", "cur_psnr", "qmcur_device", "pseudoinverse",
+    "cur_relative_error", "cur_psnr", "qmcur_device", "pseudoinverse", "stabilized_reconstruct",
+    "INDEX_POLICIES", "ObservationMask", "CompletionConfig", "CompletionResult", "random_mask", "project_observed",
+    "complete", "derive_seed",
 ]
 __version__ = "0.1.0"

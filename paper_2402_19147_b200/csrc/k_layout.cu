@@ -60,6 +60,13 @@ __global__ void k3_gather_rows(const double* __restrict__ X, int64_t n, int64_t 
   }
 }
 
+// out = mask ? Y : X per quaternion (project_observed, completion.py:101-111)
+__global__ void k_project_observed(const double* __restrict__ X, const double* __restrict__ Y,
+                                   const unsigned char* __restrict__ mask, int64_t N, double* __restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x)
+    stq(out + t * 4, ldq_nc((mask[t] ? Y : X) + t * 4));
+}
+
 // AH (n x m) = A^H (quat.py:299-302), tiled through shared memory.
 __global__ void k_conj_transpose(const double* __restrict__ A, int64_t m, int64_t n, int64_t lda,
                                  double* __restrict__ AH, int64_t ldah) {
@@ -141,6 +148,11 @@ void launch_gather_rows(const double* X, int64_t n, int64_t ldx, const int64_t* 
                         cudaStream_t st) {
   ++::qcur::g_launches;
   k3_gather_rows<<<grid_for(r * n, 256), 256, 0, st>>>(X, n, ldx, I, r, R);
+}
+void launch_project_observed(const double* X, const double* Y, const unsigned char* mask, int64_t m, int64_t n,
+                             double* out, cudaStream_t st) {
+  ++::qcur::g_launches;
+  k_project_observed<<<grid_for(m * n, 256), 256, 0, st>>>(X, Y, mask, m * n, out);
 }
 void launch_conj_transpose(const double* A, int64_t m, int64_t n, int64_t lda, double* AH, int64_t ldah,
                            cudaStream_t st) {

@@ -104,7 +104,7 @@ __device__ __forceinline__ double flip(double v, unsigned long long m) {
 constexpr unsigned kSignN = 0x3950u;
 constexpr unsigned kSignH = 0x428Eu;
 
-enum { EPI_STORE = 0, EPI_ERR = 1 };
+enum { EPI_STORE = 0, EPI_ERR = 1, EPI_COMPLETE = 2 };
 enum { MODE_STREAMK = 0, MODE_SPLIT = 1, MODE_TILES = 2 };
 
 constexpr int kBKQ = 8;  // quaternions of K per stage
@@ -124,7 +124,7 @@ struct Cfg {
   static constexpr int B_BYTES = kBKQ * BN * 8;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   // EPI_ERR: the epilogue's X tile is staged by TMA too (one BM x BN buffer)
-  static constexpr int X_BYTES = EPI == 1 ? BM * BN * 8 : 0;
+  static constexpr int X_BYTES = EPI != 0 ? BM * BN * 8 : 0;
   static constexpr int STAGES =
       (kSmemBudget - X_BYTES) / STAGE_BYTES > 8 ? 8 : (kSmemBudget - X_BYTES) / STAGE_BYTES;
   static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + X_BYTES + 1024 + (2 * STAGES + 2) * 8;
@@ -141,6 +141,8 @@ struct KParams {
   int64_t ldx;
   double* partials;    // EPI_ERR: [tiles][4]
   double psnr_scale;   // EPI_ERR: > 0 -> also the u8 image statistic at this scale (255)
+  const double* Y;              // EPI_COMPLETE: observed values
+  const unsigned char* mask;    // EPI_COMPLETE: m x n, nonzero = observed
   unsigned* counters;  // per-tile tickets (zero between launches); [65536] + done counters
   double* slots;       // partial tiles [grid][2][BM*BN]
   int b_upper;         // op(B) is upper triangular: tile column j only needs k <= j
@@ -313,7 +315,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, EPI>::THREADS, 1)
         }
         if (OPB == 0) tma_load_2d(Bs, &tmB, jq0 * 4, k0, &full[stage]);  // [8 k][BN reals]
         else tma_load_2d(Bs, &tmB, k0 * 4, jq0, &full[stage]);           // [BN/4 j][8 quaternions]
-        if (EPI == EPI_ERR && kb + 1 == nkb) {  // the tile's X block for the fused error epilogue
+        if (EPI != EPI_STORE && kb + 1 == nkb) {  // the tile's X block for the fused epilogue
           mbar_wait(xempty, xphase ^ 1u);
           mbar_expect_tx(xfull, CF::X_BYTES);
           tma_load_2d(xs, &tmX, tx * BN, i0, xfull);
@@ -530,6 +532,48 @@ __global__ void __launch_bounds__(Cfg<BM, BN, EPI>::THREADS, 1)
             }
           }
         }
+      } else if (EPI == EPI_COMPLETE) {
+        // completion sweep (completion.py:214-219): out = observed ? Y : (P R) written
+        // back, per tile [0] sum (out - X)^2 (the step), [1] sum X^2 (the scale), X being
+        // the current iterate (TMA-staged like the error kernel's X block)
+        double v[2] = {0.0, 0.0};
+        mbar_wait(xfull, xphase);
+        xphase ^= 1u;
+#pragma unroll
+        for (int a = 0; a < CF::FM; ++a) {
+          const int64_t gi = i0 + wm0 + 8 * a + arow;
+#pragma unroll
+          for (int b = 0; b < CF::FN; ++b) {
+            const int64_t gj = jr0 + wn0 + 8 * b + 2 * t4;
+            if (gi < p.Mq && gj < Nr) {
+              const double2 x =
+                  *reinterpret_cast<const double2*>(xs + (wm0 + 8 * a + arow) * BN + wn0 + 8 * b + 2 * t4);
+              double2 o = make_double2(p.alpha * acc[a][b][0], p.alpha * acc[a][b][1]);
+              if (p.mask[gi * p.Nq + (gj >> 2)]) o = __ldg(reinterpret_cast<const double2*>(p.Y + gi * p.ldx * 4 + gj));
+              *reinterpret_cast<double2*>(p.C + gi * p.ldc * 4 + gj) = o;
+              const double d0 = o.x - x.x, d1 = o.y - x.y;
+              v[0] += d0 * d0;
+              v[0] += d1 * d1;
+              v[1] += x.x * x.x;
+              v[1] += x.y * x.y;
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(xempty);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          v[k] = warp_sum(v[k]);
+          if (lane == 0) red[k][warp] = v[k];
+        }
+        consumer_sync<CF::CONSUMERS>();
+        if (tid < 4) {
+          double acc4 = 0.0;
+          if (tid < 2)
+            for (int w2 = 0; w2 < CF::CONSUMERS / 32; ++w2) acc4 += red[tid][w2];
+          p.partials[4 * ct + tid] = acc4;
+        }
+        consumer_sync<CF::CONSUMERS>();
       } else {
         // per tile: [0] sum (X - PR)^2, [1] sum X^2, [2] sum over the imaginary
         // components of (X - PR)^2 (float PSNR), [3] sum of squared differences of
@@ -839,6 +883,42 @@ void launch_cur_error(const double* X, int64_t ldx, const double* P, int64_t ldp
     ok = make_maps<64, 128>(P, ldp, 0, R, ldr, 0, m, n, r, &ta, &tb) &&
          make_map(&tx, X, 4 * n, m, ldx, 128, 64, false);
     if (ok) launch_k<64, 128, 0, 0, EPI_ERR>(ta, tb, tx, kp, grid, st);
+  }
+  if (!ok) cudaLaunchKernel((const void*)nullptr, dim3(1), dim3(1), nullptr, 0, st);
+  launch_reduce_rows(partials, ntiles, 4, out4, st);
+}
+
+void launch_complete_step(const double* X, const double* Y, const unsigned char* mask, int64_t ld, const double* P,
+                          int64_t ldp, const double* R, int64_t ldr, int64_t m, int64_t n, int64_t r, double* out,
+                          double* partials, double* out4, cudaStream_t st) {
+  const int bn = err_bn(n);
+  KParams kp{};
+  kp.Mq = m;
+  kp.Nq = n;
+  kp.Kq = r;
+  kp.alpha = 1.0;
+  kp.X = X;
+  kp.ldx = ld;
+  kp.Y = Y;
+  kp.mask = mask;
+  kp.C = out;
+  kp.ldc = ld;
+  kp.partials = partials;
+  kp.gx = (int)((4 * n + bn - 1) / bn);
+  kp.gy = (int)((m + 64 - 1) / 64);
+  kp.nkb_full = r > 0 ? (int)((r + kBKQ - 1) / kBKQ) : 1;
+  kp.total = (int)((int64_t)kp.gx * kp.gy * kp.nkb_full);
+  kp.mode = MODE_TILES;
+  const int64_t ntiles = (int64_t)kp.gx * kp.gy, G = num_sms();
+  const int grid = (int)(ntiles < G ? ntiles : G);
+  CUtensorMap ta, tb, tx;
+  bool ok;
+  if (bn == 160) {
+    ok = make_maps<64, 160>(P, ldp, 0, R, ldr, 0, m, n, r, &ta, &tb) && make_map(&tx, X, 4 * n, m, ld, 160, 64, false);
+    if (ok) launch_k<64, 160, 0, 0, EPI_COMPLETE>(ta, tb, tx, kp, grid, st);
+  } else {
+    ok = make_maps<64, 128>(P, ldp, 0, R, ldr, 0, m, n, r, &ta, &tb) && make_map(&tx, X, 4 * n, m, ld, 128, 64, false);
+    if (ok) launch_k<64, 128, 0, 0, EPI_COMPLETE>(ta, tb, tx, kp, grid, st);
   }
   if (!ok) cudaLaunchKernel((const void*)nullptr, dim3(1), dim3(1), nullptr, 0, st);
   launch_reduce_rows(partials, ntiles, 4, out4, st);

@@ -89,6 +89,15 @@ void launch_cur_error(const double* X, int64_t ldx, const double* P, int64_t ldp
                       int64_t m, int64_t n, int64_t r, double psnr_scale, double* partials, double* out4,
                       cudaStream_t st);
 
+// Completion sweep (completion.py:214-219): out = mask ? Y : P R (m x n), out4 = {sum (out - X)^2, sum X^2, 0, 0};
+// X, Y, out share the row pitch ld (quaternions); mask is m x n bytes.  partials: err_partials_count(m, n) * 4.
+void launch_complete_step(const double* X, const double* Y, const unsigned char* mask, int64_t ld, const double* P,
+                          int64_t ldp, const double* R, int64_t ldr, int64_t m, int64_t n, int64_t r, double* out,
+                          double* partials, double* out4, cudaStream_t st);
+// out = mask ? Y : X elementwise (project_observed, completion.py:101-111)
+void launch_project_observed(const double* X, const double* Y, const unsigned char* mask, int64_t m, int64_t n,
+                             double* out, cudaStream_t st);
+
 // k_dense.cu : small (q x q) dense factorizations, one CTA each.
 void launch_cholesky(double* G, int64_t q, int64_t ldg, unsigned* status, unsigned fail_bit, cudaStream_t st);
 void launch_tri_inverse_lower(const double* L, int64_t q, int64_t ldl, double* Linv, int64_t ldi, cudaStream_t st);

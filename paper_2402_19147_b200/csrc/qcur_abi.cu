@@ -767,8 +767,9 @@ int error_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, const doubl
 
 int map_status(qcur_ctx* ctx, unsigned bits) {
   ctx->last_info = bits & (ST_CHOL_FAIL_C | ST_CHOL_FAIL_R | ST_DRAW_FALLBACK);
-  if (bits & ST_SAMPLING) return ctx->fail(QCUR_E_SAMPLING, "index draw failed: not enough positive weights");
+  // K1's degenerate distribution precedes (and causes) any failed draw (cur.py:145-146 raises first)
   if (bits & ST_DEGENERATE) return ctx->fail(QCUR_E_DEGENERATE_DISTRIBUTION, "all sampling weights vanish (zero matrix)");
+  if (bits & ST_SAMPLING) return ctx->fail(QCUR_E_SAMPLING, "index draw failed: not enough positive weights");
   return QCUR_OK;
 }
 
@@ -1034,6 +1035,84 @@ int qcur_cur_error(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, con
   int rc = ctx->reserve(error_ws_bytes(m, n, c, r));
   if (rc) return rc;
   return error_impl(ctx, x_dev, m, n, C, c, U, R, r, psnr_scale, out4);
+}
+
+int qcur_cur_given(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, const int64_t* J, int64_t c,
+                   const int64_t* I, int64_t r, double* C, double* U, double* R) {
+  if (m < 1 || n < 1 || c < 1 || r < 1 || c > n || r > m) return ctx->fail(QCUR_E_SHAPE, "cur_given: bad sizes");
+  int rc = ctx->reserve(qmcur_ws_bytes(m, n, c, r) + 4096);
+  if (rc) return rc;
+  if ((rc = reset_status(ctx))) return rc;
+  launch_gather_cols(x_dev, m, n, J, c, C, ctx->stream);
+  launch_gather_rows(x_dev, n, n, I, r, R, ctx->stream);
+  CK_LAUNCH(ctx, "cur_given gather");
+  if ((rc = qmcur_core(ctx, x_dev, m, n, c, r, J, C, U, R, QCUR_CORE_PROJECTION))) return rc;
+  return sync_status(ctx);
+}
+
+int qcur_project_observed(qcur_ctx* ctx, const double* x_dev, const double* y_dev, const unsigned char* mask_dev,
+                          int64_t m, int64_t n, double* out_dev) {
+  if (m < 1 || n < 1) return ctx->fail(QCUR_E_SHAPE, "degenerate matrix shape");
+  launch_project_observed(x_dev, y_dev, mask_dev, m, n, out_dev, ctx->stream);
+  CK_LAUNCH(ctx, "project_observed");
+  return QCUR_OK;
+}
+
+int qcur_complete_sweep(qcur_ctx* ctx, const double* cur_dev, const double* y_dev, const unsigned char* mask_dev,
+                        int64_t m, int64_t n, int strategy, const uint64_t state[4], int64_t count,
+                        const int64_t* fixed_J, const int64_t* fixed_I, int64_t* J_out, int64_t* I_out,
+                        double* out_dev, double* stats4_dev) {
+  const int64_t c = count, r = count;
+  if (m < 1 || n < 1 || c < 1 || c > n || r > m) return ctx->fail(QCUR_E_SHAPE, "complete_sweep: bad sizes");
+  if ((fixed_J == nullptr) != (fixed_I == nullptr))
+    return ctx->fail(QCUR_E_PARAMETER, "fixed_J and fixed_I go together");
+  if (!fixed_J && strategy != QCUR_STRATEGY_LENGTH && strategy != QCUR_STRATEGY_UNIFORM)
+    return ctx->fail(QCUR_E_PARAMETER, "unknown strategy %d", strategy);
+  size_t need = (size_t)(m + n) * 8 + 4096 + qmcur_ws_bytes(m, n, c, r) + error_ws_bytes(m, n, c, r) +
+                qbytes(m, c) + qbytes(c, r) + qbytes(r, n) + (size_t)(c + r) * 8;
+  if (!fixed_J && strategy == QCUR_STRATEGY_LENGTH) need += length_ws_bytes(ctx, m, n);
+  int rc = ctx->reserve(need);
+  if (rc) return rc;
+  if ((rc = reset_status(ctx))) return rc;
+  double* C = ctx->take<double>((size_t)(m * c * 4));
+  double* U = ctx->take<double>((size_t)(c * r * 4));
+  double* R = ctx->take<double>((size_t)(r * n * 4));
+  int64_t* J = J_out ? J_out : ctx->take<int64_t>((size_t)c);
+  int64_t* I = I_out ? I_out : ctx->take<int64_t>((size_t)r);
+  if (!C || !U || !R || !J || !I) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (complete)");
+  cudaStream_t st = ctx->stream;
+  ctx->mark_begin();
+  if (fixed_J) {
+    // stabilized_reconstruct (cur.py:277-286): the same projection core on given index sets
+    if (J != fixed_J) cudaMemcpyAsync(J, fixed_J, (size_t)c * 8, cudaMemcpyDeviceToDevice, st);
+    if (I != fixed_I) cudaMemcpyAsync(I, fixed_I, (size_t)r * 8, cudaMemcpyDeviceToDevice, st);
+    launch_gather_cols(cur_dev, m, n, J, c, C, st);
+    launch_gather_rows(cur_dev, n, n, I, r, R, st);
+    CK_LAUNCH(ctx, "complete gather");
+    if ((rc = qmcur_core(ctx, cur_dev, m, n, c, r, J, C, U, R, QCUR_CORE_PROJECTION))) return rc;
+  } else {
+    // make_plan(current, strategy, rank, seed, count, count) + qmcur (completion.py:207-216)
+    double* colp = ctx->take<double>((size_t)n);
+    double* rowp = ctx->take<double>((size_t)m);
+    if (strategy == QCUR_STRATEGY_LENGTH) {
+      if ((rc = length_distributions_impl(ctx, cur_dev, m, n, colp, rowp))) return rc;
+    } else {
+      launch_fill(colp, n, 1.0 / (double)n, st);
+      launch_fill(rowp, m, 1.0 / (double)m, st);
+    }
+    if ((rc = qmcur_impl(ctx, cur_dev, m, n, colp, rowp, c, r, state, J, I, C, U, R))) return rc;
+  }
+  // approx = C U R with the observed entries restored, and the step / scale sums (completion.py:214-219)
+  double* P = ctx->take<double>((size_t)(m * r * 4));
+  double* parts = ctx->take<double>((size_t)err_partials_count(m, n) * 4);
+  GemmArgs g = gargs(m, r, c, C, c, 0, U, r, 0, P, r);
+  double* gws = ctx->take<double>(qgemm_workspace_bytes(g) / 8 + 16);
+  if (!P || !parts || !gws) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (complete step)");
+  if ((rc = gemm(ctx, g, gws))) return rc;
+  launch_complete_step(cur_dev, y_dev, mask_dev, n, P, r, R, n, m, n, r, out_dev, parts, stats4_dev, st);
+  CK_LAUNCH(ctx, "complete step");
+  ctx->mark("complete");
+  return sync_status(ctx);
 }
 
 int qcur_approx(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int strategy, const uint64_t state[4],

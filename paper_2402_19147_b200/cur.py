@@ -302,6 +302,26 @@ def cur_reconstruct(factors: CURFactors) -> QMatrix:
     return from_device(out, dev)
 
 
+def stabilized_reconstruct(x, row_indices, col_indices) -> QMatrix:
+    """Two-sided projection C pinv(C) X pinv(R) R for given index sets (cur.py:277-286):
+    the qmcur core on the device (qcur_cur_given), then C U R."""
+    dev = _native.device()
+    m, n = (int(v) for v in x.shape)
+    rows = np.array(row_indices, dtype=np.int64).ravel()
+    cols = np.array(col_indices, dtype=np.int64).ravel()
+    c, r = int(cols.size), int(rows.size)
+    if c < 1 or r < 1 or (cols < 0).any() or (cols >= n).any() or (rows < 0).any() or (rows >= m).any():
+        raise ShapeError("index sets out of range")
+    xd = to_device(x, dev)
+    J = dev.torch.from_numpy(cols).to(device=f"cuda:{dev.index}")
+    I = dev.torch.from_numpy(rows).to(device=f"cuda:{dev.index}")
+    C, U, R = dev.empty_q(m, c), dev.empty_q(c, r), dev.empty_q(r, n)
+    dev.call("qcur_cur_given", xd.data_ptr(), m, n, J.data_ptr(), c, I.data_ptr(), r, C.data_ptr(), U.data_ptr(),
+             R.data_ptr())
+    return cur_reconstruct(CURFactors(row_indices=rows, col_indices=cols, c=from_device(C, dev),
+                                      u=from_device(U, dev), r=from_device(R, dev)))
+
+
 def cur_relative_error(x, factors: CURFactors) -> float:
     """||X - C U R||_F / ||X||_F, fused on the GPU (CUR never materialised).
 

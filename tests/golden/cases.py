@@ -30,6 +30,15 @@ DRAW_CASES = {"w_20_12": (20, 12, 99), "w_4000_200": (4000, 200, 1), "w_33_30": 
               "w_1100_1000": (1100, 1000, 8), "w_9_9": (9, 9, 5)}
 PINV_CASES = {"p_10x8": (10, 8, 1), "p_8x10": (8, 10, 2), "p_64x40": (64, 40, 3), "p_1x5": (1, 5, 4)}
 RNG_SEEDS = [0, 1, 7, 12345, 2 ** 40 + 3, 2 ** 70 + 5]
+# completion (completion.py): name: (m, n, rank, gen_seed, missing_ratio, mask_seed,
+#                                    strategy, index_policy, seed, max_iters, rel_tol)
+COMPLETION_CASES = {
+    "comp_uniform_40x36": (40, 36, 3, 21, 0.3, 22, "uniform", "resample_each_iter", 4, 200, 1e-4),
+    "comp_length_30x30": (30, 30, 3, 23, 0.3, 24, "length", "resample_each_iter", 2, 200, 1e-4),
+    "comp_fixed_30x28": (30, 28, 2, 25, 0.4, 26, "length", "fixed", 3, 20, 1e-4),
+    "comp_budget_24x20": (24, 20, 2, 27, 0.5, 28, "uniform", "resample_each_iter", 7, 3, 1e-14),
+}
+DERIVE_SEED_CASES = [(0, ("draw",)), (5, ("sweep", 0)), (5, ("sweep", 17)), (2 ** 63 + 11, ("batch", 3))]
 
 
 def qmcur_input(case):
@@ -55,3 +64,12 @@ def draw_input(case):
 def pinv_input(case):
     m, n, seed = case
     return O.random_planes(np.random.default_rng(100 + seed), m, n)
+
+
+def completion_input(case):
+    """(truth planes, observed mask, y = truth on the observed entries, zeros elsewhere)."""
+    m, n, k, gseed, ratio, mseed = case[:6]
+    truth = O.lowrank_planes(np.random.default_rng(gseed), m, n, k)
+    observed = O.random_mask(m, n, ratio, mseed)
+    y = O.project_observed(tuple(np.zeros((m, n)) for _ in range(4)), observed, truth)
+    return truth, observed, y

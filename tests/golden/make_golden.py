@@ -58,6 +58,23 @@ def main() -> None:
         out[f"{name}/idx"] = qcur.draw_indices(p, count, seed).astype(np.int64)
     for name, case in cases.PINV_CASES.items():
         out[f"{name}/pinv"] = qcur.pseudoinverse(qcur.QMatrix(*cases.pinv_input(case))).to_array()
+    from qcur.bench import derive_seed
+    from qcur.completion import CompletionConfig, ObservationMask, complete, random_mask
+
+    for name, case in cases.COMPLETION_CASES.items():
+        m, n, k, gseed, ratio, mseed, strategy, policy, seed, iters, tol = case
+        truth, observed, y = cases.completion_input(case)
+        mask = random_mask(m, n, ratio, mseed)
+        assert np.array_equal(mask.observed, observed)
+        res = complete(qcur.QMatrix(*y), ObservationMask(observed),
+                       CompletionConfig(rank=k, strategy=strategy, max_iters=iters, rel_tol=tol,
+                                        index_policy=policy, seed=seed))
+        out[f"{name}/mask"] = mask.observed
+        out[f"{name}/history"] = np.array(res.rel_change_history)
+        out[f"{name}/converged"] = np.array([res.converged])
+        out[f"{name}/x_star"] = res.x_star.to_array()
+        print(name, res.iterations_run, res.converged, res.rel_change_history[-1])
+    out["derive_seed"] = np.array([derive_seed(s, *parts) for s, parts in cases.DERIVE_SEED_CASES], dtype=np.uint64)
     for s in cases.RNG_SEEDS:
         out[f"rng/{s}"] = np.random.default_rng(s).random(8)
     out["meta/numpy"] = np.array([np.__version__])

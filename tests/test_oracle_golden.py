@@ -54,3 +54,24 @@ def test_oracle_error_definition():
     e2, x2 = O.cur_error(planes, planes, tuple(np.zeros((8, 8)) + (1.0 if s == 0 else 0.0) * np.eye(8) for s in range(4)),
                          tuple(np.eye(8) * (1.0 if s == 0 else 0.0) for s in range(4)))
     assert e2 == pytest.approx(0.0, abs=1e-24) and math.sqrt(x2) > 0
+
+
+# ---- completion: oracle restatement vs the reference's complete() ----
+@pytest.mark.parametrize("name", sorted(cases.COMPLETION_CASES))
+def test_oracle_completion_matches_reference(name):
+    m, n, k, gseed, ratio, mseed, strategy, policy, seed, iters, tol = cases.COMPLETION_CASES[name]
+    truth, observed, y = cases.completion_input(cases.COMPLETION_CASES[name])
+    assert np.array_equal(observed, G[f"{name}/mask"])  # random_mask, bit for bit
+    x, hist, conv = O.complete(y, observed, k, strategy, iters, tol, policy, seed)
+    ref_hist = G[f"{name}/history"]
+    assert len(hist) == len(ref_hist) and conv == bool(G[f"{name}/converged"][0])
+    # late sweeps measure differences of nearly equal iterates: relative agreement ~1e-7
+    assert np.max(np.abs(np.array(hist) - ref_hist) / np.abs(ref_hist)) <= 1e-6
+    xs = tuple(G[f"{name}/x_star"][i] for i in range(4))
+    assert O.rel_fro(x, xs) <= 1e-8
+    assert all(np.array_equal(a[observed], b[observed]) for a, b in zip(x, xs))
+
+
+def test_oracle_derive_seed_matches_reference():
+    got = [O.derive_seed(s, *parts) for s, parts in cases.DERIVE_SEED_CASES]
+    assert np.array_equal(np.array(got, dtype=np.uint64), G["derive_seed"])
