@@ -315,6 +315,69 @@ def run_rowshard(args, cfg_name: str, cfg: dict, world: int, rank: int, local: i
         print(json.dumps(line), flush=True)
 
 
+COMPLETION = dict(m=512, n=768, rank=20, missing=0.5, mask_seed=1, gen_seed=20240229, noise=0.02, sweeps=30,
+                  strategy="length", seed=0)
+
+
+def run_completion(args) -> None:
+    """--completion: the first "next" row, Algorithm 2 on a Kodak-sized
+    (512 x 768) image-like pure-quaternion matrix with half its entries missing, a fixed number of
+    sweeps (rel_tol below reach).  One JSON line, rank 0, 1 GPU."""
+    import torch
+
+    from paper_2402_19147_b200 import CompletionConfig, QMatrix, _native, complete, random_mask
+    from paper_2402_19147_b200.quat import from_device
+
+    cfgc = dict(COMPLETION)
+    m, n = cfgc["m"], cfgc["n"]
+    dev = _native.device(0)
+    x = dev.empty_q(m, n)
+    dev.call("qcur_synth_image", m, n, 30, cfgc["gen_seed"], cfgc["noise"], x.data_ptr())
+    truth = from_device(x, dev)
+    mask = random_mask(m, n, cfgc["missing"], cfgc["mask_seed"])
+    y = QMatrix(*(np.where(mask.observed, p, 0.0) for p in truth.planes))
+    cc = CompletionConfig(rank=cfgc["rank"], strategy=cfgc["strategy"], max_iters=cfgc["sweeps"], rel_tol=1e-300,
+                          seed=cfgc["seed"])
+    res = None
+    for _ in range(max(args.warmup, 1)):
+        res = complete(y, mask, cc)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(0)
+    with sampler:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            res = complete(y, mask, cc)
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+    sweeps_s = args.steps * res.iterations_run / el
+    cpu = None
+    if not args.no_cpu_baseline:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+
+        k = 3
+        t0 = time.perf_counter()
+        O.complete(tuple(y.planes), mask.observed, cfgc["rank"], cfgc["strategy"], k, 1e-300, "resample_each_iter",
+                   cfgc["seed"])
+        ct = time.perf_counter() - t0
+        cpu = {"value": k / ct, "unit": "sweeps/s", "cores": cpu_threads(), "kind": "port",
+               "sample": f"{k} sweeps of the same solve by oracle/oracle.py:complete"}
+    err = float(np.sqrt(sum(((a - b) ** 2).sum() for a, b in zip(res.x_star.planes, truth.planes)) /
+                        sum((b ** 2).sum() for b in truth.planes)))
+    print(json.dumps({
+        "metric": "completion sweeps/sec (Algorithm 2, completion.py:157-246)", "value": sweeps_s,
+        "unit": "sweeps/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_sweep": 1e3 * el / (args.steps * res.iterations_run), "higher_is_better": True, "dtype": "f64",
+        "data": "synthetic image-like pure quaternion (qcur_synth_image), 50% of entries missing (random_mask)",
+        "config": {"workload": f"completion {m}x{n}, rank {cfgc['rank']}, {cfgc['strategy']} sampling, "
+                               f"{cfgc['sweeps']} sweeps per solve (count = rank + 5 rows / columns)", **cfgc},
+        "e2e": {"value": sweeps_s, "unit": "sweeps/s", "api": "complete(y, mask, cfg) on host QMatrix / mask "
+                "(upload, all sweeps, x_star download inside the timed region)",
+                "h2d_bytes_per_step": 32 * m * n + m * n, "d2h_bytes_per_step": 32 * m * n},
+        "rel_err_vs_truth": err, "clocks": sampler.summary(), "cpu_baseline": cpu,
+    }))
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -327,7 +390,12 @@ def main() -> None:
     ap.add_argument("--c", type=int, default=None, help="override c = r (cfg3: 64, 128 or 256)")
     ap.add_argument("--rowshard", action="store_true",
                     help="shard one matrix by row blocks across the ranks (cfg5 design) instead of replicas")
+    ap.add_argument("--completion", action="store_true",
+                    help="measure the completion solver (Algorithm 2) instead of the QMCUR step")
     args = ap.parse_args()
+    if args.completion:
+        run_completion(args)
+        return
     cfg = dict(CONFIGS[args.config])
     if args.c:
         cfg["c"] = cfg["r"] = args.c
