@@ -30,8 +30,7 @@
 //    tile cut between CTAs is finished by its last contributor (ticket), which
 //    adds the parts in CTA (= k) order.
 //  * split (fewer tiles than SMs/2, equal depth): each tile is cut into S equal
-//    k ranges run at the same time; the S CTAs meet on a ticket and each sums
-//    BM/S rows of the S parts in split order.
+//    k ranges; the last of the S CTAs to finish (ticket) adds the parts in split order.
 // Both orders are fixed, so results are bitwise deterministic run to run
 // (test_cur.py:243-250).
 //
@@ -224,8 +223,7 @@ struct Space {
 //  * stream-K: `waves` rounds of whole tiles (tile w*G + c: CTAs in lock step work on
 //    neighbouring tiles, so each A row block is fetched from HBM once and the other
 //    column tiles hit L2), then one contiguous span of the remaining tiles' iterations.
-__device__ __forceinline__ bool cta_span(const KParams& p, int s, int& sb, int& se) {
-  const int G = gridDim.x, c = blockIdx.x;
+__device__ __forceinline__ bool cta_span(const KParams& p, int G, int c, int s, int& sb, int& se) {
   if (s < p.waves) {
     const int t = c + s * G;
     sb = t * p.nkb_full;
@@ -252,11 +250,25 @@ __device__ __forceinline__ bool cta_span(const KParams& p, int s, int& sb, int& 
   return true;
 }
 
+// A launch carries one or two independent problems of the same shape class (the C and R^H
+// sides of a CholeskyQR2 step): CTAs [0, grid0) run problem 0, the rest problem 1.
+struct KPair {
+  KParams p[2];
+  int grid0;
+};
+
 template <int BM, int BN, int OPA, int OPB, int EPI>
 __global__ void __launch_bounds__(Cfg<BM, BN, EPI>::THREADS, 1)
-    qgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 const __grid_constant__ CUtensorMap tmX, const __grid_constant__ KParams p) {
+    qgemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmB0,
+                 const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
+                 const __grid_constant__ CUtensorMap tmX, const __grid_constant__ KPair pp) {
   using CF = Cfg<BM, BN, EPI>;
+  const bool second = (int)blockIdx.x >= pp.grid0;
+  const KParams& p = pp.p[second ? 1 : 0];
+  const CUtensorMap& tmA = second ? tmA1 : tmA0;
+  const CUtensorMap& tmB = second ? tmB1 : tmB0;
+  const int G = second ? (int)gridDim.x - pp.grid0 : pp.grid0;
+  const int c = second ? (int)blockIdx.x - pp.grid0 : (int)blockIdx.x;
   constexpr int S = CF::STAGES;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte aligned stage ring (swizzle atoms); offsetting the shared array keeps
@@ -274,7 +286,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, EPI>::THREADS, 1)
   const Space<BM, BN> sp(p);
   {
     int sb, se;
-    if (!cta_span(p, 0, sb, se) || sb >= se) return;
+    if (!cta_span(p, G, c, 0, sb, se) || sb >= se) return;
   }
 
   if (tid == 0) {
@@ -295,7 +307,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, EPI>::THREADS, 1)
       int stage = 0;
       unsigned phase = 0, xphase = 0;
       int sb, se;
-      for (int sidx = 0; cta_span(p, sidx, sb, se); ++sidx) {
+      for (int sidx = 0; cta_span(p, G, c, sidx, sb, se); ++sidx) {
       int t, kb, nkb;
       sp.locate(sb, t, kb);
       nkb = sp.tile_nkb(t);
@@ -351,10 +363,9 @@ __global__ void __launch_bounds__(Cfg<BM, BN, EPI>::THREADS, 1)
 
   int stage = 0;
   unsigned phase = 0;
-  const int G = gridDim.x, c = blockIdx.x;
   unsigned xphase = 0;
   int ib, ie;
-  for (int sidx = 0; cta_span(p, sidx, ib, ie); ++sidx) {
+  for (int sidx = 0; cta_span(p, G, c, sidx, ib, ie); ++sidx) {
   int ct, ckb, cnkb;
   sp.locate(ib, ct, ckb);
   cnkb = sp.tile_nkb(ct);
@@ -438,50 +449,46 @@ __global__ void __launch_bounds__(Cfg<BM, BN, EPI>::THREADS, 1)
           __threadfence();
           consumer_sync<CF::CONSUMERS>();
           if (p.mode == MODE_SPLIT) {
-            // all S parts of this tile run concurrently: meet, then each CTA sums BM/S rows
-            const int nsp = p.splits, o = c / nsp, z = c - o * nsp;
-            if (tid == 0) {
-              atomicAdd(&p.counters[ct], 1u);
-              volatile unsigned* vc = &p.counters[ct];
-              while (*vc < (unsigned)nsp) __nanosleep(64);
-            }
+            // the last of the tile's S parts to arrive adds all S in split order (no CTA
+            // ever waits for another, so no co-residency assumption)
+            const int nsp = p.splits, o = c / nsp;
+            if (tid == 0) s_flag = (atomicAdd(&p.counters[ct], 1u) == (unsigned)nsp - 1) ? 1u : 0u;
             consumer_sync<CF::CONSUMERS>();
-            __threadfence();
-            const int r0 = (int)((int64_t)z * BM / nsp), r1 = (int)((int64_t)(z + 1) * BM / nsp);
-            for (int idx = r0 * (BN / 2) + tid; idx < r1 * (BN / 2); idx += CF::CONSUMERS) {
-              const int r = idx / (BN / 2), cc = 2 * (idx % (BN / 2));
-              const int64_t gi = i0 + r, gj = jr0 + cc;
-              if (gi >= p.Mq || gj >= Nr) continue;
-              const double* base = p.slots + (int64_t)(o * nsp) * 2 * (BM * BN) + r * BN + cc;
-              double sx = 0.0, sy = 0.0;
-              for (int k = 0; k < nsp; k += 8) {
-                double2 v[8];
+            if (s_flag) {
+              __threadfence();
+              for (int idx = tid; idx < BM * (BN / 2); idx += CF::CONSUMERS) {
+                const int r = idx / (BN / 2), cc = 2 * (idx % (BN / 2));
+                const int64_t gi = i0 + r, gj = jr0 + cc;
+                if (gi >= p.Mq || gj >= Nr) continue;
+                const double* base = p.slots + (int64_t)(o * nsp) * 2 * (BM * BN) + r * BN + cc;
+                double sx = 0.0, sy = 0.0;
+                for (int k = 0; k < nsp; k += 8) {
+                  double2 v[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
-                  if (k + u < nsp) v[u] = __ldcg(reinterpret_cast<const double2*>(base + (int64_t)(k + u) * 2 * (BM * BN)));
+                  for (int u = 0; u < 8; ++u)
+                    if (k + u < nsp)
+                      v[u] = __ldcg(reinterpret_cast<const double2*>(base + (int64_t)(k + u) * 2 * (BM * BN)));
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
-                  if (k + u < nsp) {
-                    sx += v[u].x;
-                    sy += v[u].y;
-                  }
+                  for (int u = 0; u < 8; ++u)
+                    if (k + u < nsp) {
+                      sx += v[u].x;
+                      sy += v[u].y;
+                    }
+                }
+                double* cp = p.C + gi * p.ldc * 4 + gj;
+                double2 ov = make_double2(p.alpha * sx, p.alpha * sy);
+                if (p.beta != 0.0) {
+                  const double2 old = *reinterpret_cast<const double2*>(cp);
+                  ov.x += p.beta * old.x;
+                  ov.y += p.beta * old.y;
+                }
+                *reinterpret_cast<double2*>(cp) = ov;
               }
-              double* cp = p.C + gi * p.ldc * 4 + gj;
-              double2 ov = make_double2(p.alpha * sx, p.alpha * sy);
-              if (p.beta != 0.0) {
-                const double2 old = *reinterpret_cast<const double2*>(cp);
-                ov.x += p.beta * old.x;
-                ov.y += p.beta * old.y;
-              }
-              *reinterpret_cast<double2*>(cp) = ov;
+              if (tid == 0) p.counters[ct] = 0u;
             }
+            // s_flag is rewritten at this CTA's next partial tile, which a fast warp can
+            // reach while others still read it here (short tiles fit in the stage ring)
             consumer_sync<CF::CONSUMERS>();
-            if (tid == 0) {  // the last CTA through resets the tile's tickets
-              if (atomicAdd(&p.counters[65536 + ct], 1u) == (unsigned)nsp - 1) {
-                p.counters[ct] = 0u;
-                p.counters[65536 + ct] = 0u;
-              }
-            }
           } else {
             if (tid == 0) {
               const unsigned mine = (unsigned)(it + 1 - seg_begin);
@@ -530,6 +537,9 @@ __global__ void __launch_bounds__(Cfg<BM, BN, EPI>::THREADS, 1)
               }
               if (tid == 0) p.counters[ct] = 0u;
             }
+            // s_flag is rewritten at this CTA's next partial tile, which a fast warp can
+            // reach while others still read it here (short tiles fit in the stage ring)
+            consumer_sync<CF::CONSUMERS>();
           }
         }
       } else if (EPI == EPI_COMPLETE) {
@@ -749,7 +759,7 @@ struct Plan {
   size_t slot_bytes;
 };
 
-Plan make_plan(const GemmArgs& g) {
+Plan make_plan(const GemmArgs& g, int64_t gmax = 0) {
   Plan pl{};
   pl.cfg = pick_cfg(g.Mq, g.Nq);
   const TileCfg& c = kCfgs[pl.cfg];
@@ -767,7 +777,7 @@ Plan make_plan(const GemmArgs& g) {
   kp.gy = (int)((g.Mq + c.bm - 1) / c.bm);
   kp.nkb_full = g.Kq > 0 ? (int)((g.Kq + kBKQ - 1) / kBKQ) : 1;
   kp.total = (int)host_total(c, kp.gx, kp.gy, kp.nkb_full, g.b_upper, g.herm_lower);
-  const int64_t G = num_sms();
+  const int64_t G = gmax > 0 ? gmax : num_sms();
   const int64_t ntiles = (int64_t)kp.gx * kp.gy;
   const int64_t active = host_active_tiles(c, kp.gx, kp.gy, g.herm_lower);
   int64_t grid;
@@ -799,8 +809,8 @@ Plan make_plan(const GemmArgs& g) {
 }
 
 template <int BM, int BN, int OPA, int OPB, int EPI>
-void launch_k(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tx, const KParams& kp, int grid,
-              cudaStream_t st) {
+void launch_k2(const CUtensorMap* ta, const CUtensorMap* tb, const CUtensorMap& tx, const KPair& kp, int grid,
+               cudaStream_t st) {
   using CF = Cfg<BM, BN, EPI>;
   auto fn = qgemm_kernel<BM, BN, OPA, OPB, EPI>;
   static bool set = false;
@@ -809,21 +819,44 @@ void launch_k(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& t
     set = true;
   }
   ++::qcur::g_launches;
-  fn<<<grid, CF::THREADS, CF::SMEM, st>>>(ta, tb, tx, kp);
+  fn<<<grid, CF::THREADS, CF::SMEM, st>>>(ta[0], tb[0], ta[1], tb[1], tx, kp);
 }
 
+template <int BM, int BN, int OPA, int OPB, int EPI>
+void launch_k(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tx, const KParams& kp, int grid,
+              cudaStream_t st) {
+  const CUtensorMap a[2] = {ta, ta}, b[2] = {tb, tb};
+  KPair pr;
+  pr.p[0] = pr.p[1] = kp;
+  pr.grid0 = grid;
+  launch_k2<BM, BN, OPA, OPB, EPI>(a, b, tx, pr, grid, st);
+}
+
+// one or two problems (same ops and tile configuration) in one launch
 template <int BM, int BN>
-void launch_cfg(const GemmArgs& g, const KParams& kp, int grid, cudaStream_t st) {
-  CUtensorMap ta, tb;
-  if (!make_maps<BM, BN>(g.A, g.lda, g.opA, g.B, g.ldb, g.opB, g.Mq, g.Nq, g.Kq, &ta, &tb)) {
-    // surfaces through the caller's launch check as a CUDA error
-    cudaLaunchKernel((const void*)nullptr, dim3(1), dim3(1), nullptr, 0, st);
-    return;
+void launch_cfg(const GemmArgs* g, const KParams* kp, const int* grid, int np, cudaStream_t st) {
+  CUtensorMap ta[2], tb[2];
+  for (int k = 0; k < np; ++k)
+    if (!make_maps<BM, BN>(g[k].A, g[k].lda, g[k].opA, g[k].B, g[k].ldb, g[k].opB, g[k].Mq, g[k].Nq, g[k].Kq,
+                           &ta[k], &tb[k])) {
+      // surfaces through the caller's launch check as a CUDA error
+      cudaLaunchKernel((const void*)nullptr, dim3(1), dim3(1), nullptr, 0, st);
+      return;
+    }
+  if (np == 1) {
+    ta[1] = ta[0];
+    tb[1] = tb[0];
   }
-  if (g.opA == 0 && g.opB == 0) launch_k<BM, BN, 0, 0, EPI_STORE>(ta, tb, tb, kp, grid, st);
-  else if (g.opA == 0) launch_k<BM, BN, 0, 1, EPI_STORE>(ta, tb, tb, kp, grid, st);
-  else if (g.opB == 0) launch_k<BM, BN, 1, 0, EPI_STORE>(ta, tb, tb, kp, grid, st);
-  else launch_k<BM, BN, 1, 1, EPI_STORE>(ta, tb, tb, kp, grid, st);
+  KPair pr;
+  pr.p[0] = kp[0];
+  pr.p[1] = kp[np - 1];
+  pr.grid0 = grid[0];
+  const int total = np == 1 ? grid[0] : grid[0] + grid[1];
+  const int opA = g[0].opA, opB = g[0].opB;
+  if (opA == 0 && opB == 0) launch_k2<BM, BN, 0, 0, EPI_STORE>(ta, tb, tb[0], pr, total, st);
+  else if (opA == 0) launch_k2<BM, BN, 0, 1, EPI_STORE>(ta, tb, tb[0], pr, total, st);
+  else if (opB == 0) launch_k2<BM, BN, 1, 0, EPI_STORE>(ta, tb, tb[0], pr, total, st);
+  else launch_k2<BM, BN, 1, 1, EPI_STORE>(ta, tb, tb[0], pr, total, st);
 }
 
 }  // namespace
@@ -839,8 +872,41 @@ void launch_qgemm(const GemmArgs& g, double* workspace, unsigned* counters, cuda
     pl.kp.mode = MODE_STREAMK;
     pl.grid = 1;
   }
-  if (pl.cfg == 1) launch_cfg<64, 160>(g, pl.kp, pl.grid, st);
-  else launch_cfg<64, 128>(g, pl.kp, pl.grid, st);
+  if (pl.cfg == 1) launch_cfg<64, 160>(&g, &pl.kp, &pl.grid, 1, st);
+  else launch_cfg<64, 128>(&g, &pl.kp, &pl.grid, 1, st);
+}
+
+void launch_qgemm_pair(const GemmArgs& g0, double* ws0, const GemmArgs& g1, double* ws1, unsigned* counters,
+                       cudaStream_t st) {
+  static const bool no_pair = getenv("QCUR_NO_PAIR") != nullptr;  // experiments only
+  const bool same = !no_pair && g0.opA == g1.opA && g0.opB == g1.opB && pick_cfg(g0.Mq, g0.Nq) == pick_cfg(g1.Mq, g1.Nq) &&
+                    g0.Mq > 0 && g0.Nq > 0 && g1.Mq > 0 && g1.Nq > 0 && ws0 && ws1 && counters;
+  if (!same) {
+    launch_qgemm(g0, ws0, counters, st);
+    launch_qgemm(g1, ws1, counters, st);
+    return;
+  }
+  // split the SMs in proportion to the two problems' k-block counts
+  const int64_t G = num_sms();
+  const int64_t t0 = make_plan(g0).kp.total, t1 = make_plan(g1).kp.total;
+  int64_t G0 = (G * t0 + (t0 + t1) / 2) / (t0 + t1 > 0 ? t0 + t1 : 1);
+  if (G0 < 1) G0 = 1;
+  if (G0 > G - 1) G0 = G - 1;
+  Plan pl[2] = {make_plan(g0, G0), make_plan(g1, G - G0)};
+  if (pl[0].kp.mode == MODE_TILES || pl[1].kp.mode == MODE_TILES) {
+    launch_qgemm(g0, ws0, counters, st);
+    launch_qgemm(g1, ws1, counters, st);
+    return;
+  }
+  pl[0].kp.counters = counters;
+  pl[1].kp.counters = counters + 32768;  // tickets 32768.., done counters 98304..
+  pl[0].kp.slots = ws0;
+  pl[1].kp.slots = ws1;
+  const GemmArgs g[2] = {g0, g1};
+  const KParams kp[2] = {pl[0].kp, pl[1].kp};
+  const int grid[2] = {pl[0].grid, pl[1].grid};
+  if (pl[0].cfg == 1) launch_cfg<64, 160>(g, kp, grid, 2, st);
+  else launch_cfg<64, 128>(g, kp, grid, 2, st);
 }
 
 // error kernel: 64 x 160 tiles when 4n is a multiple of 160, else 64 x 128

@@ -82,6 +82,10 @@ struct GemmArgs {
 size_t qgemm_workspace_bytes(const GemmArgs& g);
 // counters: >= 65536 zero-initialised uints owned by the caller (split-K tickets)
 void launch_qgemm(const GemmArgs& g, double* workspace, unsigned* counters, cudaStream_t st);
+// two independent products in one launch (SMs split by work); falls back to two launches
+// when their ops or tile configurations differ.  Tile counts < 32768 each.
+void launch_qgemm_pair(const GemmArgs& g0, double* ws0, const GemmArgs& g1, double* ws1, unsigned* counters,
+                       cudaStream_t st);
 // Fused error of X - P R (P: m x r, R: r x n, X: m x n, all interleaved).  out4 =
 // {||X-PR||^2, ||X||^2, imaginary part of ||X-PR||^2, u8-image squared-diff sum at psnr_scale}
 int64_t err_partials_count(int64_t m, int64_t n);  // tiles; the partial buffer needs 4 doubles per tile

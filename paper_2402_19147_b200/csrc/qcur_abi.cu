@@ -402,9 +402,25 @@ struct FactorSpec {
 
 // Factor up to two tall blocks together (C and R^H of one QMCUR step) so the
 // latency-bound small kernels (cluster Cholesky) serve both in one launch.
-int factor_multi(qcur_ctx* ctx, const FactorSpec* specs, int ns) {
+int factor_multi(qcur_ctx* ctx, const FactorSpec* specs_in, int ns) {
   cudaStream_t st = ctx->stream;
   unsigned* status = ctx->status_dev;
+  FactorSpec specs[2];
+  for (int k = 0; k < ns; ++k) specs[k] = specs_in[k];
+  // Two blocks factor in lock step with paired GEMM launches (one launch, the SMs split
+  // between the C and R^H problems).  The pair needs identical ops, so a block given as
+  // src^H (R) is materialised as Z = R^H first (one 32-byte-per-element transpose).
+  if (ns == 2) {
+    for (int k = 0; k < 2; ++k) {
+      if (!specs[k].zh) continue;
+      double* ZH = ctx->take<double>((size_t)(specs[k].p * specs[k].q * 4));
+      if (!ZH) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (factor transpose)");
+      launch_conj_transpose(specs[k].src, specs[k].q, specs[k].p, specs[k].p, ZH, specs[k].q, st);
+      CK_LAUNCH(ctx, "factor transpose");
+      specs[k].src = ZH;
+      specs[k].zh = 0;
+    }
+  }
   struct Bufs {
     double *G1, *L1, *L1i, *G2, *L2, *L2i, *T, *betas, *Zcm, *Qcm, *Tcm, *Vcm, *gws;
   } B[2];
@@ -434,6 +450,20 @@ int factor_multi(qcur_ctx* ctx, const FactorSpec* specs, int ns) {
   int rc;
   bool fast[2] = {false, false};
   for (int k = 0; k < ns; ++k) fast[k] = !(ctx->force_robust || specs[k].cutoff_abs >= 0.0);
+  // one GEMM per fast block: paired into one launch when both blocks are on the fast path
+  auto gemm_each = [&](auto&& args_of) -> int {
+    if (ns == 2 && fast[0] && fast[1]) {
+      launch_qgemm_pair(args_of(0), B[0].gws, args_of(1), B[1].gws, ctx->counters, st);
+      CK_LAUNCH(ctx, "qgemm pair");
+      return QCUR_OK;
+    }
+    for (int k = 0; k < ns; ++k) {
+      if (!fast[k]) continue;
+      const int r2 = gemm(ctx, args_of(k), B[k].gws);
+      if (r2) return r2;
+    }
+    return QCUR_OK;
+  };
   // Cholesky + inverse of each Gram: one cluster launch when both fit, else per problem
   auto chol_inv = [&](bool second) -> int {  // (second pass uses the series below)
     CholJob jobs[2];
@@ -476,57 +506,68 @@ int factor_multi(qcur_ctx* ctx, const FactorSpec* specs, int ns) {
     launch_set_status(status, specs[k].fail_bit, st);
     CK_LAUNCH(ctx, "force robust");
   }
+  auto zsrc = [&](int k) { return specs[k]; };
   // G1 = Z^H Z
-  for (int k = 0; k < ns; ++k) {
-    if (!fast[k]) continue;
-    const FactorSpec& f = specs[k];
-    const int64_t p = f.p, q = f.q;
-    if (!f.zh) rc = gemm(ctx, with_flags(gargs(q, q, p, f.src, q, 1, f.src, q, 0, B[k].G1, q), 0, 1), B[k].gws);
-    else rc = gemm(ctx, with_flags(gargs(q, q, p, f.src, p, 0, f.src, p, 1, B[k].G1, q), 0, 1), B[k].gws);
-    if (rc) return rc;
-  }
+  if ((rc = gemm_each([&](int k) {
+         const FactorSpec f = zsrc(k);
+         const int64_t p = f.p, q = f.q;
+         return f.zh ? with_flags(gargs(q, q, p, f.src, p, 0, f.src, p, 1, B[k].G1, q), 0, 1)
+                     : with_flags(gargs(q, q, p, f.src, q, 1, f.src, q, 0, B[k].G1, q), 0, 1);
+       })))
+    return rc;
   if ((rc = chol_inv(false))) return rc;
   // Q1 = Z L1^{-H} (written straight into the output Q);  G2 = Q1^H Q1
-  for (int k = 0; k < ns; ++k) {
-    if (!fast[k]) continue;
-    const FactorSpec& f = specs[k];
-    const int64_t p = f.p, q = f.q;
-    if (!f.zh) rc = gemm(ctx, with_flags(gargs(p, q, q, f.src, q, 0, B[k].L1i, q, 1, f.out.Q, q), 1, 0), B[k].gws);
-    else rc = gemm(ctx, with_flags(gargs(p, q, q, f.src, p, 1, B[k].L1i, q, 1, f.out.Q, q), 1, 0), B[k].gws);
-    if (rc) return rc;
-    if ((rc = gemm(ctx, with_flags(gargs(q, q, p, f.out.Q, q, 1, f.out.Q, q, 0, B[k].G2, q), 0, 1), B[k].gws)))
-      return rc;
-  }
+  if ((rc = gemm_each([&](int k) {
+         const FactorSpec f = zsrc(k);
+         const int64_t p = f.p, q = f.q;
+         return f.zh ? with_flags(gargs(p, q, q, f.src, p, 1, B[k].L1i, q, 1, f.out.Q, q), 1, 0)
+                     : with_flags(gargs(p, q, q, f.src, q, 0, B[k].L1i, q, 1, f.out.Q, q), 1, 0);
+       })))
+    return rc;
+  if ((rc = gemm_each([&](int k) {
+         const int64_t p = specs[k].p, q = specs[k].q;
+         return with_flags(gargs(q, q, p, specs[k].out.Q, q, 1, specs[k].out.Q, q, 0, B[k].G2, q), 0, 1);
+       })))
+    return rc;
   // second pass: G2 = I + E with E ~ kappa^2 u; L2^{-1} by a second-order series
   // (no sequential Cholesky; blocks with max|E| > 1e-5 take the robust path)
-  for (int k = 0; k < ns; ++k) {
-    if (!fast[k]) continue;
-    const int64_t q = specs[k].q;
-    Bufs& b = B[k];
-    double *M0 = b.L2, *P = b.T, *M1 = b.Tcm, *P2 = b.Vcm;
-    launch_series_lh(b.G2, nullptr, q, M0, status, specs[k].fail_bit, 1e-5, st);
-    if ((rc = gemm(ctx, with_flags(gargs(q, q, q, M0, q, 0, M0, q, 1, P, q), 1, 1), b.gws))) return rc;
-    launch_series_lh(b.G2, P, q, M1, status, specs[k].fail_bit, 1e-5, st);
-    if ((rc = gemm(ctx, gargs(q, q, q, M1, q, 0, M1, q, 0, P2, q), b.gws))) return rc;
-    launch_series_final(M1, P2, q, b.L2i, st);
-    CK_LAUNCH(ctx, "series");
-  }
+  // M0 = lh(E) in b.L2, P = M0 M0^H in b.T, M1 in b.Tcm, P2 = M1 M1 in b.Vcm
+  for (int k = 0; k < ns; ++k)
+    if (fast[k]) launch_series_lh(B[k].G2, nullptr, specs[k].q, B[k].L2, status, specs[k].fail_bit, 1e-5, st);
+  if ((rc = gemm_each([&](int k) {
+         const int64_t q = specs[k].q;
+         return with_flags(gargs(q, q, q, B[k].L2, q, 0, B[k].L2, q, 1, B[k].T, q), 1, 1);
+       })))
+    return rc;
+  for (int k = 0; k < ns; ++k)
+    if (fast[k]) launch_series_lh(B[k].G2, B[k].T, specs[k].q, B[k].Tcm, status, specs[k].fail_bit, 1e-5, st);
+  if ((rc = gemm_each([&](int k) {
+         const int64_t q = specs[k].q;
+         return gargs(q, q, q, B[k].Tcm, q, 0, B[k].Tcm, q, 0, B[k].Vcm, q);
+       })))
+    return rc;
+  for (int k = 0; k < ns; ++k)
+    if (fast[k]) launch_series_final(B[k].Tcm, B[k].Vcm, specs[k].q, B[k].L2i, st);
+  CK_LAUNCH(ctx, "series");
   // Z = Q T with Q = Q1 L2^{-H}, T = L2^H L1^H.  The tall product Q1 L2^{-H} is never
   // formed: pinv(Z) = T^{-1} Q^H = (T^{-1} L2^{-1}) Q1^H, so the factor pair is
   // (Q1, F = T^{-1} L2^{-1}) and every consumer (X Q_R, Q_C^H Y, F Q^H) applies the
   // well-conditioned L2^{-1} (kappa ~ 1 + kappa(Z)^2 u) on the small side instead.
   // kappa_F(T) = ||Z||_F ||T^{-1}||_F = sqrt(tr G1) ||T^{-1}||_F guards the fast path.
-  for (int k = 0; k < ns; ++k) {
-    if (!fast[k]) continue;
-    const FactorSpec& f = specs[k];
-    const int64_t q = f.q;
-    double* Tinv = B[k].T;
-    if ((rc = gemm(ctx, with_flags(gargs(q, q, q, B[k].L1i, q, 1, B[k].L2i, q, 1, Tinv, q), 1, 0), B[k].gws)))
-      return rc;
-    launch_kappa_check(B[k].G1, Tinv, q, ctx->kappa_limit, status, f.fail_bit, st);
-    CK_LAUNCH(ctx, "kappa");
-    if ((rc = gemm(ctx, gargs(q, q, q, Tinv, q, 0, B[k].L2i, q, 0, f.out.F, q), B[k].gws))) return rc;
-  }
+  // (T^{-1} lives in b.T, free again after the series.)
+  if ((rc = gemm_each([&](int k) {
+         const int64_t q = specs[k].q;
+         return with_flags(gargs(q, q, q, B[k].L1i, q, 1, B[k].L2i, q, 1, B[k].T, q), 1, 0);
+       })))
+    return rc;
+  for (int k = 0; k < ns; ++k)
+    if (fast[k]) launch_kappa_check(B[k].G1, B[k].T, specs[k].q, ctx->kappa_limit, status, specs[k].fail_bit, st);
+  CK_LAUNCH(ctx, "kappa");
+  if ((rc = gemm_each([&](int k) {
+         const int64_t q = specs[k].q;
+         return gargs(q, q, q, B[k].T, q, 0, B[k].L2i, q, 0, specs[k].out.F, q);
+       })))
+    return rc;
   // robust path, gated on each fail_bit (no-op launches when the fast path held)
   for (int k = 0; k < ns; ++k) {
     const FactorSpec& f = specs[k];
@@ -576,7 +617,7 @@ size_t qmcur_ws_bytes(int64_t m, int64_t n, int64_t c, int64_t r) {
   b += (size_t)(draw_work_doubles(n) + draw_work_doubles(m)) * 8 + 1024;
   const bool std_shape = m >= c && n >= r;
   if (std_shape) {
-    b += factor_ws_bytes(m, c) + factor_ws_bytes(n, r);
+    b += factor_ws_bytes(m, c) + factor_ws_bytes(n, r) + qbytes(n, r);  // + R^H for the paired factor
     b += qbytes(m, c) + qbytes(c, c) + qbytes(n, r) + qbytes(r, r);  // Q_C F_C Q_R F_R
     b += qbytes(m, r) + qbytes(c, r) * 2;                            // Y, M, W
     GemmArgs g1 = gargs(m, r, n, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0);
