@@ -152,6 +152,7 @@ struct KParams {
   int mode;
   int splits;          // MODE_SPLIT: CTAs per tile
   int waves;           // MODE_STREAMK: rounds of whole tiles before the stream-K tail
+  int cta_G, cta_c;    // device side only: this problem's CTA count and this CTA's index
 };
 
 // Iteration space bookkeeping (closed form).
@@ -264,11 +265,22 @@ __global__ void __launch_bounds__(Cfg<BM, BN, EPI>::THREADS, 1)
                  const __grid_constant__ CUtensorMap tmX, const __grid_constant__ KPair pp) {
   using CF = Cfg<BM, BN, EPI>;
   const bool second = (int)blockIdx.x >= pp.grid0;
-  const KParams& p = pp.p[second ? 1 : 0];
+  // this CTA's problem, copied to shared memory once (uniform LDS instead of generic
+  // loads from the parameter window)
+  __shared__ KParams s_kp;
+  if (threadIdx.x == 0) {
+    s_kp = pp.p[second ? 1 : 0];
+    s_kp.cta_G = second ? (int)gridDim.x - pp.grid0 : pp.grid0;
+    s_kp.cta_c = second ? (int)blockIdx.x - pp.grid0 : (int)blockIdx.x;
+  }
+  __syncthreads();
+  const KParams& p = s_kp;
   const CUtensorMap& tmA = second ? tmA1 : tmA0;
   const CUtensorMap& tmB = second ? tmB1 : tmB0;
-  const int G = second ? (int)gridDim.x - pp.grid0 : pp.grid0;
-  const int c = second ? (int)blockIdx.x - pp.grid0 : (int)blockIdx.x;
+  // (G, c) are read from shared memory where needed: keeping them live across the DMMA
+  // loop costs accumulator registers
+#define G (p.cta_G)
+#define c (p.cta_c)
   constexpr int S = CF::STAGES;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte aligned stage ring (swizzle atoms); offsetting the shared array keeps
@@ -365,7 +377,10 @@ __global__ void __launch_bounds__(Cfg<BM, BN, EPI>::THREADS, 1)
   unsigned phase = 0;
   unsigned xphase = 0;
   int ib, ie;
-  for (int sidx = 0; cta_span(p, G, c, sidx, ib, ie); ++sidx) {
+  // the fused-epilogue kernels run one contiguous span: a constant trip count keeps their
+  // loop as simple as a single-span kernel's
+  constexpr int kMaxSpans = EPI == EPI_STORE ? (1 << 30) : 1;
+  for (int sidx = 0; sidx < kMaxSpans && cta_span(p, G, c, sidx, ib, ie); ++sidx) {
   int ct, ckb, cnkb;
   sp.locate(ib, ct, ckb);
   cnkb = sp.tile_nkb(ct);
@@ -648,6 +663,9 @@ __global__ void __launch_bounds__(Cfg<BM, BN, EPI>::THREADS, 1)
   }
   }
 }
+
+#undef G
+#undef c
 
 // ---------------------------------------------------------------------------
 // host side
