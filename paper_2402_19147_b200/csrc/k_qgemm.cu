@@ -150,7 +150,8 @@ struct KParams {
   int nkb_full;        // k-blocks of a full-depth tile (>= 1)
   int total;           // iterations (sum of k-blocks over tiles, < 2^31)
   int mode;
-  int splits;          // MODE_SPLIT: CTAs per tile
+  int splits;          // MODE_SPLIT: CTAs per tile (the first split_extra tiles get one more)
+  int split_extra;
   int waves;           // MODE_STREAMK: rounds of whole tiles before the stream-K tail
   int cta_G, cta_c;    // device side only: this problem's CTA count and this CTA's index
 };
@@ -224,6 +225,21 @@ struct Space {
 //  * stream-K: `waves` rounds of whole tiles (tile w*G + c: CTAs in lock step work on
 //    neighbouring tiles, so each A row block is fetched from HBM once and the other
 //    column tiles hit L2), then one contiguous span of the remaining tiles' iterations.
+// MODE_SPLIT: tile ordinal o, split z of S for CTA c, and the tile's first CTA
+__device__ __forceinline__ void split_of(const KParams& p, int c, int& o, int& z, int& S, int& first) {
+  const int big = p.split_extra * (p.splits + 1);
+  if (c < big) {
+    S = p.splits + 1;
+    o = c / S;
+    first = o * S;
+  } else {
+    S = p.splits;
+    o = p.split_extra + (c - big) / S;
+    first = big + (o - p.split_extra) * S;
+  }
+  z = c - first;
+}
+
 __device__ __forceinline__ bool cta_span(const KParams& p, int G, int c, int s, int& sb, int& se) {
   if (s < p.waves) {
     const int t = c + s * G;
@@ -239,9 +255,10 @@ __device__ __forceinline__ bool cta_span(const KParams& p, int G, int c, int s, 
     return true;
   }
   if (p.mode == MODE_SPLIT) {
-    const int o = c / p.splits, z = c - o * p.splits;
-    sb = o * p.nkb_full + (int)((int64_t)z * p.nkb_full / p.splits);
-    se = o * p.nkb_full + (int)((int64_t)(z + 1) * p.nkb_full / p.splits);
+    int o, z, S, first;
+    split_of(p, c, o, z, S, first);
+    sb = o * p.nkb_full + (int)((int64_t)z * p.nkb_full / S);
+    se = o * p.nkb_full + (int)((int64_t)(z + 1) * p.nkb_full / S);
     return true;
   }
   const int base = p.waves * G * p.nkb_full;
@@ -466,7 +483,8 @@ __global__ void __launch_bounds__(Cfg<BM, BN, EPI>::THREADS, 1)
           if (p.mode == MODE_SPLIT) {
             // the last of the tile's S parts to arrive adds all S in split order (no CTA
             // ever waits for another, so no co-residency assumption)
-            const int nsp = p.splits, o = c / nsp;
+            int o, z_, nsp, first;
+            split_of(p, c, o, z_, nsp, first);
             if (tid == 0) s_flag = (atomicAdd(&p.counters[ct], 1u) == (unsigned)nsp - 1) ? 1u : 0u;
             consumer_sync<CF::CONSUMERS>();
             if (s_flag) {
@@ -475,7 +493,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, EPI>::THREADS, 1)
                 const int r = idx / (BN / 2), cc = 2 * (idx % (BN / 2));
                 const int64_t gi = i0 + r, gj = jr0 + cc;
                 if (gi >= p.Mq || gj >= Nr) continue;
-                const double* base = p.slots + (int64_t)(o * nsp) * 2 * (BM * BN) + r * BN + cc;
+                const double* base = p.slots + (int64_t)first * 2 * (BM * BN) + r * BN + cc;
                 double sx = 0.0, sy = 0.0;
                 for (int k = 0; k < nsp; k += 8) {
                   double2 v[8];
@@ -770,6 +788,11 @@ int64_t host_active_tiles(const TileCfg& c, int64_t gx, int64_t gy, int herm) {
   return n;
 }
 
+bool no_split() {
+  static const bool v = getenv("QCUR_NO_SPLIT") != nullptr;  // experiments only
+  return v;
+}
+
 struct Plan {
   int cfg;
   KParams kp;
@@ -802,16 +825,21 @@ Plan make_plan(const GemmArgs& g, int64_t gmax = 0) {
   if (ntiles > 65536) {  // beyond the ticket array: whole tiles per CTA (uniform tiles only)
     kp.mode = MODE_TILES;
     grid = (!g.b_upper && !g.herm_lower) ? (ntiles < G ? ntiles : G) : 1;
-  } else if (2 * active <= G && kp.nkb_full >= 2) {
+  } else if (!no_split() && 2 * active <= G && kp.nkb_full >= 2) {
     // few tiles: cut each into equal k ranges.  A triangular op(B) runs at full depth
     // here (its zero triangle is stored as zeros, so the extra products add exact zeros)
     kp.mode = MODE_SPLIT;
     kp.b_upper = 0;
     kp.total = (int)host_total(c, kp.gx, kp.gy, kp.nkb_full, 0, g.herm_lower);
-    int64_t sp = G / active;
-    if (sp > kp.nkb_full) sp = kp.nkb_full;
+    // S_t = G / active splits, one more on the first G % active tiles: every SM busy
+    int64_t sp = G / active, extra = G % active;
+    if (sp >= kp.nkb_full) {
+      sp = kp.nkb_full;
+      extra = 0;
+    }
     kp.splits = (int)sp;
-    grid = active * sp;
+    kp.split_extra = (int)extra;
+    grid = active * sp + extra;
   } else {
     kp.mode = MODE_STREAMK;
     grid = (kp.total + 3) / 4;  // >= 4 k-blocks per CTA
