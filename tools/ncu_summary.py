@@ -6,8 +6,9 @@ import sys
 
 KEYS = [
     ("gpu__time_duration.sum", "time"),
-    ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "fp64 pipe %"),
-    ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "fp64 inst %"),
+    ("sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active", "DMMA pipe % (active)"),
+    ("sm__cycles_active.avg", "sm active cyc"),
+    ("sm__cycles_elapsed.avg", "elapsed cyc"),
     ("dram__bytes_read.sum", "dram rd"),
     ("dram__bytes_write.sum", "dram wr"),
     ("lts__t_sector_hit_rate.pct", "L2 hit %"),
