@@ -116,6 +116,11 @@ int qcur_qmcur_host(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, co
 int qcur_cur_given(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, const int64_t* col_idx_dev,
                    int64_t num_cols, const int64_t* row_idx_dev, int64_t num_rows, double* c_dev, double* u_dev,
                    double* r_dev);
+/* y = op(A) x for a quaternion m x n matrix and quaternion vectors (op: QCUR_OP_N -> y in H^m,
+ * QCUR_OP_H -> y in H^n): the products of the Krylov spectral norm (spectral_norm,
+ * linalg.py:365-367).  HBM-bound, fixed reduction order. */
+int qcur_qgemv(qcur_ctx* ctx, int op, int64_t m, int64_t n, const double* a_dev, int64_t lda, const double* x_dev,
+               double* y_dev);
 /* ---- low-rank completion (Algorithm 2; completion.py) ---- */
 /* out = mask ? y : x elementwise (project_observed, completion.py:101-111); mask: m x n bytes,
  * nonzero = observed. */

@@ -16,7 +16,7 @@ from .errors import (
     SamplingError,
     ShapeError,
 )
-from .quat import QMatrix, Quaternion, qmat_conj_transpose, qmat_frobenius_norm, qmat_matmul
+from .quat import QMatrix, Quaternion, qmat_conj_transpose, qmat_frobenius_norm, qmat_matmul, read_qmat, write_qmat
 from .cur import (
     STRATEGIES,
     CURFactors,
@@ -34,7 +34,7 @@ from .cur import (
     stabilized_reconstruct,
     uniform_distributions,
 )
-from .linalg import pseudoinverse
+from .linalg import pseudoinverse, spectral_norm
 from .completion import (
     INDEX_POLICIES,
     CompletionConfig,
@@ -54,6 +54,6 @@ __all__ = [
     "default_sample_counts", "make_plan", "draw_indices", "plan_indices", "qmcur", "cur_reconstruct",
     "cur_relative_error", "cur_psnr", "qmcur_device", "pseudoinverse", "stabilized_reconstruct",
     "INDEX_POLICIES", "ObservationMask", "CompletionConfig", "CompletionResult", "random_mask", "project_observed",
-    "complete", "derive_seed",
+    "complete", "derive_seed", "read_qmat", "write_qmat", "spectral_norm",
 ]
 __version__ = "0.1.0"

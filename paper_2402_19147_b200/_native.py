@@ -48,7 +48,7 @@ EXPORTS = (
     "qcur_colsums_seq", "qcur_pairwise_sums", "qcur_vec_div", "qcur_gather_cols", "qcur_gather_rows",
     "qcur_qgemm_ex", "qcur_chol_inv", "qcur_series_l2inv", "qcur_kappa_check", "qcur_factor",
     "qcur_synth_lowrank_rows", "qcur_qmcur_ex", "qcur_qmcur_host",
-    "qcur_project_observed", "qcur_complete_sweep", "qcur_cur_given",
+    "qcur_project_observed", "qcur_complete_sweep", "qcur_cur_given", "qcur_qgemv",
 )
 
 _c_dp = ctypes.c_void_p
@@ -101,6 +101,7 @@ def load_library() -> ctypes.CDLL:
             "qcur_qmcur_host": (ctypes.c_int, [_c_dp, _c_dp, _i64, _i64, _c_dp, _c_dp, _i64, _i64, _u64p,
                                                ctypes.c_int, _c_dp, _c_dp, _c_dp, _c_dp, _c_dp, _c_dp, _c_dp,
                                                _c_dp4, _c_dp4, _c_dp4]),
+            "qcur_qgemv": (ctypes.c_int, [_c_dp, ctypes.c_int, _i64, _i64, _c_dp, _i64, _c_dp, _c_dp]),
             "qcur_cur_given": (ctypes.c_int, [_c_dp, _c_dp, _i64, _i64, _c_dp, _i64, _c_dp, _i64, _c_dp, _c_dp, _c_dp]),
             "qcur_project_observed": (ctypes.c_int, [_c_dp, _c_dp, _c_dp, _c_dp, _i64, _i64, _c_dp]),
             "qcur_complete_sweep": (ctypes.c_int, [_c_dp, _c_dp, _c_dp, _c_dp, _i64, _i64, ctypes.c_int, _u64p, _i64,

@@ -102,6 +102,10 @@ void launch_complete_step(const double* X, const double* Y, const unsigned char*
 void launch_project_observed(const double* X, const double* Y, const unsigned char* mask, int64_t m, int64_t n,
                              double* out, cudaStream_t st);
 
+// k_gemv.cu : y = op(A) x for quaternion vectors (op 0 = N, 1 = H), HBM-bound, deterministic
+void launch_qgemv(int op, const double* A, int64_t m, int64_t n, int64_t lda, const double* x, double* y,
+                  cudaStream_t st);
+
 // k_dense.cu : small (q x q) dense factorizations, one CTA each.
 void launch_cholesky(double* G, int64_t q, int64_t ldg, unsigned* status, unsigned fail_bit, cudaStream_t st);
 void launch_tri_inverse_lower(const double* L, int64_t q, int64_t ldl, double* Linv, int64_t ldi, cudaStream_t st);

@@ -1091,6 +1091,15 @@ int qcur_cur_given(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, con
   return sync_status(ctx);
 }
 
+int qcur_qgemv(qcur_ctx* ctx, int op, int64_t m, int64_t n, const double* a_dev, int64_t lda, const double* x_dev,
+               double* y_dev) {
+  if (m < 1 || n < 1 || lda < n) return ctx->fail(QCUR_E_SHAPE, "qgemv: bad sizes");
+  if (op != QCUR_OP_N && op != QCUR_OP_H) return ctx->fail(QCUR_E_PARAMETER, "qgemv: op must be N or H");
+  launch_qgemv(op, a_dev, m, n, lda, x_dev, y_dev, ctx->stream);
+  CK_LAUNCH(ctx, "qgemv");
+  return QCUR_OK;
+}
+
 int qcur_project_observed(qcur_ctx* ctx, const double* x_dev, const double* y_dev, const unsigned char* mask_dev,
                           int64_t m, int64_t n, double* out_dev) {
   if (m < 1 || n < 1) return ctx->fail(QCUR_E_SHAPE, "degenerate matrix shape");

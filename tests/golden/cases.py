@@ -38,6 +38,8 @@ COMPLETION_CASES = {
     "comp_fixed_30x28": (30, 28, 2, 25, 0.4, 26, "length", "fixed", 3, 20, 1e-4),
     "comp_budget_24x20": (24, 20, 2, 27, 0.5, 28, "uniform", "resample_each_iter", 7, 3, 1e-14),
 }
+SPECTRAL_CASES = {"s_30x20": (30, 20, 0, 31), "s_lowrank_40": (40, 40, 3, 32), "s_1x5": (1, 5, 0, 33),
+                  "s_64x12": (64, 12, 0, 34)}
 DERIVE_SEED_CASES = [(0, ("draw",)), (5, ("sweep", 0)), (5, ("sweep", 17)), (2 ** 63 + 11, ("batch", 3))]
 
 
@@ -73,3 +75,12 @@ def completion_input(case):
     observed = O.random_mask(m, n, ratio, mseed)
     y = O.project_observed(tuple(np.zeros((m, n)) for _ in range(4)), observed, truth)
     return truth, observed, y
+
+
+def spectral_input(case):
+    m, n, k, seed = case
+    g = np.random.default_rng(seed)
+    if k:
+        p = O.lowrank_planes(g, m, n, k)
+        return tuple(x + 1e-6 * g.standard_normal(x.shape) for x in p)
+    return O.random_planes(g, m, n)

@@ -74,6 +74,17 @@ def main() -> None:
         out[f"{name}/converged"] = np.array([res.converged])
         out[f"{name}/x_star"] = res.x_star.to_array()
         print(name, res.iterations_run, res.converged, res.rel_change_history[-1])
+    from qcur.linalg import spectral_norm as ref_spectral_norm
+    from qcur.quat import write_qmat as ref_write_qmat
+
+    for name, case in cases.SPECTRAL_CASES.items():
+        out[f"{name}/sigma"] = np.array([ref_spectral_norm(qcur.QMatrix(*cases.spectral_input(case)))])
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "x.qmat")
+        ref_write_qmat(qcur.QMatrix(*cases.spectral_input(cases.SPECTRAL_CASES["s_1x5"])), path)
+        out["qmat/s_1x5_bytes"] = np.frombuffer(open(path, "rb").read(), dtype=np.uint8)
     out["derive_seed"] = np.array([derive_seed(s, *parts) for s, parts in cases.DERIVE_SEED_CASES], dtype=np.uint64)
     for s in cases.RNG_SEEDS:
         out[f"rng/{s}"] = np.random.default_rng(s).random(8)
