@@ -73,6 +73,12 @@ int qcur_rng_seed(const uint32_t* words, int nwords, uint64_t state[4]);
 int qcur_rng_advance(uint64_t state[4], uint64_t delta);
 int qcur_rng_random(uint64_t state[4], int64_t count, double* out);
 
+/* qcur_upload_planar fused with qcur_length_distributions for a host matrix (make_plan's
+ * first use of x, cur.py:132-150): row chunks stream in on a copy stream while the SMs
+ * interleave them and carry numpy's sequential column sums through each chunk; the
+ * pairwise row / flat trees follow.  Same outputs as the two calls; synchronizes. */
+int qcur_upload_length(qcur_ctx* ctx, const double* a0, const double* a1, const double* a2, const double* a3,
+                       int64_t m, int64_t n, double* x_dev, double* col_probs_dev, double* row_probs_dev);
 /* ---- host <-> device (the e2e boundary: reference planar host buffers) --- */
 int qcur_upload_planar(qcur_ctx* ctx, const double* a0, const double* a1, const double* a2, const double* a3,
                        int64_t m, int64_t n, double* x_dev);

@@ -240,15 +240,13 @@ size_t length_ws_bytes(qcur_ctx* ctx, int64_t m, int64_t n) {
 }
 
 // length_distributions on the device (cur.py:132-150); arena must be reserved.
-int length_distributions_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, double* col, double* row) {
+// K1 after the column pass: row / flat pairwise trees and the normalisations (cur.py:144-150)
+int length_tail(qcur_ctx* ctx, const double* sq, const double* colsum, int64_t m, int64_t n, double* col,
+                double* row) {
   cudaStream_t st = ctx->stream;
-  double* sq = ctx->take<double>((size_t)(m * n));
-  double* colsum = ctx->take<double>((size_t)n);
   double* rowsum = ctx->take<double>((size_t)m);
   double* scal = ctx->take<double>(8);  // total, colnorm, rownorm
-  if (!sq || !colsum || !rowsum || !scal) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (length)");
-  launch_colstrip(X, m, n, n, sq, colsum, st);
-  CK_LAUNCH(ctx, "colstrip");
+  if (!rowsum || !scal) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (length)");
   int rc;
   if ((rc = pairwise_sum(ctx, sq, m, n, n, rowsum)) != QCUR_OK) return rc;
   if ((rc = pairwise_sum(ctx, sq, 1, 0, m * n, scal)) != QCUR_OK) return rc;
@@ -263,6 +261,15 @@ int length_distributions_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t
   CK_LAUNCH(ctx, "length scale");
   ctx->mark("length");
   return QCUR_OK;
+}
+
+int length_distributions_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, double* col, double* row) {
+  double* sq = ctx->take<double>((size_t)(m * n));
+  double* colsum = ctx->take<double>((size_t)n);
+  if (!sq || !colsum) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (length)");
+  launch_colstrip(X, m, n, n, sq, colsum, ctx->stream);
+  CK_LAUNCH(ctx, "colstrip");
+  return length_tail(ctx, sq, colsum, m, n, col, row);
 }
 
 // ---------------------------------------------------------------------------
@@ -967,6 +974,60 @@ int qcur_upload_planar(qcur_ctx* ctx, const double* a0, const double* a1, const 
   launch_planar_to_interleaved(planes[0], planes[1], planes[2], planes[3], m, n, x_dev, ctx->stream);
   CK_LAUNCH(ctx, "planar_to_interleaved");
   return QCUR_OK;
+}
+
+int qcur_upload_length(qcur_ctx* ctx, const double* a0, const double* a1, const double* a2, const double* a3,
+                       int64_t m, int64_t n, double* x_dev, double* col_dev, double* row_dev) {
+  if (m < 1 || n < 1) return ctx->fail(QCUR_E_SHAPE, "degenerate matrix shape (%lld, %lld)", (long long)m, (long long)n);
+  // row chunks of ~32 MB per plane: the copy engine streams chunk k+1 while the SMs convert
+  // chunk k and carry numpy's sequential column sums through it (colstrip with acc_in)
+  int64_t rows = (int64_t)((32u << 20) / ((size_t)n * 8));
+  if (rows < 64) rows = 64;
+  if (rows > m) rows = m;
+  const int64_t nchunks = (m + rows - 1) / rows;
+  const size_t stage = (size_t)(rows * n);  // doubles per plane per chunk
+  int rc = ctx->reserve(2 * 4 * stage * 8 + length_ws_bytes(ctx, m, n) + 4096);
+  if (rc) return rc;
+  if ((rc = reset_status(ctx))) return rc;
+  double* buf[2][4];
+  for (int b = 0; b < 2; ++b)
+    for (int k = 0; k < 4; ++k) buf[b][k] = ctx->take<double>(stage);
+  double* sq = ctx->take<double>((size_t)(m * n));
+  double* colsum2[2] = {ctx->take<double>((size_t)n), ctx->take<double>((size_t)n)};  // ping-pong running sums
+  if (!buf[1][3] || !sq || !colsum2[1]) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (upload_length)");
+  cudaStream_t st = ctx->stream, cs = ctx->copy_stream;
+  cudaEvent_t ev_in[2], ev_used[2];
+  for (int b = 0; b < 2; ++b) {
+    cudaEventCreateWithFlags(&ev_in[b], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_used[b], cudaEventDisableTiming);
+  }
+  // the copy stream starts after everything already queued on the main stream
+  cudaEventRecord(ctx->ev_fork, st);
+  cudaStreamWaitEvent(cs, ctx->ev_fork, 0);
+  const double* src[4] = {a0, a1, a2, a3};
+  cudaError_t e = cudaSuccess;
+  for (int64_t c = 0; c < nchunks && e == cudaSuccess; ++c) {
+    const int b = (int)(c & 1);
+    const int64_t r0 = c * rows, nr = (m - r0) < rows ? (m - r0) : rows;
+    if (c >= 2) e = cudaStreamWaitEvent(cs, ev_used[b], 0);  // staging buffer b free again
+    for (int k = 0; k < 4 && e == cudaSuccess; ++k)
+      e = cudaMemcpyAsync(buf[b][k], src[k] + r0 * n, (size_t)(nr * n) * 8, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess) e = cudaEventRecord(ev_in[b], cs);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev_in[b], 0);
+    if (e != cudaSuccess) break;
+    launch_planar_to_interleaved(buf[b][0], buf[b][1], buf[b][2], buf[b][3], nr, n, x_dev + r0 * n * 4, st);
+    cudaEventRecord(ev_used[b], st);
+    launch_colstrip(x_dev + r0 * n * 4, nr, n, n, sq + r0 * n, colsum2[b], st, c == 0 ? nullptr : colsum2[b ^ 1]);
+  }
+  double* colsum = colsum2[(nchunks - 1) & 1];
+  for (int b = 0; b < 2; ++b) {
+    cudaEventDestroy(ev_in[b]);
+    cudaEventDestroy(ev_used[b]);
+  }
+  if (e != cudaSuccess) return ctx->cuda_fail(e, "upload_length H2D");
+  CK_LAUNCH(ctx, "upload_length");
+  if ((rc = length_tail(ctx, sq, colsum, m, n, col_dev, row_dev))) return rc;
+  return sync_status(ctx);
 }
 
 int qcur_download_planar(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int64_t ld, double* a0,

@@ -138,10 +138,19 @@ def length_distributions(x) -> tuple[np.ndarray, np.ndarray]:
     Raises DegenerateDistributionError for the zero matrix."""
     dev = _native.device()
     m, n = (int(v) for v in x.shape)
-    xd = to_device(x, dev)
     col = dev.empty(n)
     row = dev.empty(m)
-    dev.call("qcur_length_distributions", xd.data_ptr(), m, n, col.data_ptr(), row.data_ptr())
+    if isinstance(x, QMatrix) and (x._dev is None or x._dev[0] is not dev):
+        # first use of a host matrix: upload and column pass pipelined (qcur_upload_length);
+        # the device copy stays cached on x for qmcur / the error that follow
+        a0, a1, a2, a3 = (np.ascontiguousarray(p, dtype=np.float64) for p in x.planes)
+        xd = dev.empty_q(m, n)
+        dev.call("qcur_upload_length", a0.ctypes.data, a1.ctypes.data, a2.ctypes.data, a3.ctypes.data, m, n,
+                 xd.data_ptr(), col.data_ptr(), row.data_ptr())
+        x._dev = (dev, xd)
+    else:
+        xd = to_device(x, dev)
+        dev.call("qcur_length_distributions", xd.data_ptr(), m, n, col.data_ptr(), row.data_ptr())
     return col.cpu().numpy(), row.cpu().numpy()
 
 
