@@ -12,7 +12,8 @@
 // from numpy's sequential cumsum only by rounding, bounded by
 // (n + 70) * 2^-53 * total; a draw is accepted only when the uniform sits
 // farther than twice that bound from both neighbouring prefix values, which
-// proves the numpy index.  Otherwise (probability ~1e-12 per draw) the lane
+// proves the numpy index.  Drawn weights leave the tree by subtraction along the
+// path (the margin grows by the per-draw rounding).  Otherwise (probability ~1e-12 per draw) the lane
 // recomputes the exact sequential cumsum — numpy's own order — for that draw.
 // The PCG64 stream is advanced on device (pcg64.h), one double per draw.
 #include "common.cuh"
@@ -177,7 +178,9 @@ __global__ void __launch_bounds__(1024) k2_draw(DrawJobs jobs, unsigned* status)
     int64_t idx = g;
     if (ok) {
       const double tot_est = total * (1.0 + 1e-12);
-      const double delta = 2.0 * ((double)len + 70.0) * u53 * tot_est;  // 2 (n+70) 2^-53 T
+      // 2 (n + 70 + 2 count) 2^-53 T: the fresh tree's prefix error plus one rounding per
+      // level for every earlier removal
+      const double delta = 2.0 * ((double)len + 70.0 + 2.0 * (double)count) * u53 * tot_est;
       ok = (lower <= target - delta) && (upper > target + delta) && (L.lev[0][idx] > 0.0);
     }
     if (!ok) {
@@ -205,15 +208,18 @@ __global__ void __launch_bounds__(1024) k2_draw(DrawJobs jobs, unsigned* status)
       idx = __shfl_sync(0xffffffffu, idx, 0);
     }
     if (lane == 0) {
+      // remove the drawn weight: zero the leaf, subtract it along the path (one rounding per
+      // level and draw; the acceptance margin above covers the accumulated error)
+      const double wgt = L.lev[0][idx];
       job.out[t] = idx;
       L.lev[0][idx] = 0.0;
+      int node = (int)idx;
+      for (int h = 1; h <= L.top; ++h) {
+        node >>= 5;
+        L.lev[h][node] -= wgt;
+      }
     }
     __syncwarp();
-    int node = (int)idx;
-    for (int h = 1; h <= L.top; ++h) {
-      node >>= 5;
-      refresh_node(L, h, node, lane);
-    }
   }
 }
 
