@@ -574,6 +574,36 @@ def main() -> None:
         "steps": e2e_steps,
         "rel_err": e2e_err,
     }
+    # the same work through the throughput API (approx_stream): matrix k+1's H2D overlaps
+    # matrix k's approximation; every step still uploads its 512 MB and reads back its result
+    if batch == 1:
+        from paper_2402_19147_b200 import approx_stream
+
+        nst = max(e2e_steps, 6)
+        seeds = [cfg["plan_seed"]] * (nst + 2)
+        list(approx_stream([xh] * 2, cfg["strategy"], cfg["rank"], seeds[:2], num_rows=r, num_cols=c))
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        res_s = list(approx_stream([xh] * nst, cfg["strategy"], cfg["rank"], seeds[:nst], num_rows=r, num_cols=c))
+        torch.cuda.synchronize()
+        st_s = time.perf_counter() - t0
+        tt = torch.tensor([st_s], dtype=torch.float64, device=f"cuda:{local}")
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        st_s = float(tt.item())
+        single = dict(e2e)
+        # headline e2e = the throughput API (the metric is approximations per second); the
+        # one-call-at-a-time number stays alongside as `single_call`
+        e2e = {
+            "value": world * nst / st_s, "unit": "approx/s", "steps": nst,
+            "h2d_bytes_per_step": 32 * m * n, "d2h_bytes_per_step": 32 * c * r + 8 * (c + r) + 36,
+            "api": "approx_stream over pinned host matrices: each step uploads its 512 MB input (H2D of the next "
+                   "overlapped with the current approximation) and reads back its indices, U and error",
+            "rel_err": res_s[-1].rel_err,
+            "single_call": single,
+        }
 
     # --- CPU baseline: the oracle port on this host (rank 0, N = 1) ---
     cpu = None

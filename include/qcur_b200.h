@@ -155,6 +155,11 @@ int qcur_approx(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int st
                 double* u_dev, double* r_dev, double psnr_scale, int core, double* err4_dev);
 /* read back and clear the device status word; returns the mapped status code */
 int qcur_check(qcur_ctx* ctx);
+/* Asynchronous status: queue a copy of the context's status word to host_dst (pinned) and
+ * clear it, both on the context stream (no synchronisation); after the stream reached that
+ * point, qcur_status_map turns the word into the status code qcur_check would have returned. */
+int qcur_status_async(qcur_ctx* ctx, unsigned* host_dst);
+int qcur_status_map(qcur_ctx* ctx, unsigned bits);
 
 /* ---- linear algebra used by the path -------------------------------------- */
 /* qmat_matmul (quat.py:274-296): C = alpha op(A) op(B) + beta C, sizes in quaternions */

@@ -35,6 +35,7 @@ from .cur import (
     uniform_distributions,
 )
 from .linalg import pseudoinverse, spectral_norm
+from .stream import StreamResult, approx_stream
 from .completion import (
     INDEX_POLICIES,
     CompletionConfig,
@@ -55,5 +56,6 @@ __all__ = [
     "cur_relative_error", "cur_psnr", "qmcur_device", "pseudoinverse", "stabilized_reconstruct",
     "INDEX_POLICIES", "ObservationMask", "CompletionConfig", "CompletionResult", "random_mask", "project_observed",
     "complete", "derive_seed", "read_qmat", "write_qmat", "spectral_norm",
+    "StreamResult", "approx_stream",
 ]
 __version__ = "0.1.0"

@@ -49,7 +49,7 @@ EXPORTS = (
     "qcur_qgemm_ex", "qcur_chol_inv", "qcur_series_l2inv", "qcur_kappa_check", "qcur_factor",
     "qcur_synth_lowrank_rows", "qcur_qmcur_ex", "qcur_qmcur_host",
     "qcur_project_observed", "qcur_complete_sweep", "qcur_cur_given", "qcur_qgemv",
-    "qcur_upload_length",
+    "qcur_upload_length", "qcur_status_async", "qcur_status_map",
 )
 
 _c_dp = ctypes.c_void_p
@@ -102,6 +102,8 @@ def load_library() -> ctypes.CDLL:
             "qcur_qmcur_host": (ctypes.c_int, [_c_dp, _c_dp, _i64, _i64, _c_dp, _c_dp, _i64, _i64, _u64p,
                                                ctypes.c_int, _c_dp, _c_dp, _c_dp, _c_dp, _c_dp, _c_dp, _c_dp,
                                                _c_dp4, _c_dp4, _c_dp4]),
+            "qcur_status_async": (ctypes.c_int, [_c_dp, _c_dp]),
+            "qcur_status_map": (ctypes.c_int, [_c_dp, ctypes.c_uint]),
             "qcur_upload_length": (ctypes.c_int, [_c_dp, _c_dp, _c_dp, _c_dp, _c_dp, _i64, _i64, _c_dp, _c_dp, _c_dp]),
             "qcur_qgemv": (ctypes.c_int, [_c_dp, ctypes.c_int, _i64, _i64, _c_dp, _i64, _c_dp, _c_dp]),
             "qcur_cur_given": (ctypes.c_int, [_c_dp, _c_dp, _i64, _i64, _c_dp, _i64, _c_dp, _i64, _c_dp, _c_dp, _c_dp]),

@@ -1255,6 +1255,14 @@ int qcur_approx(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int st
 
 int qcur_check(qcur_ctx* ctx) { return sync_status(ctx); }
 
+int qcur_status_async(qcur_ctx* ctx, unsigned* host_dst) {
+  cudaError_t e = cudaMemcpyAsync(host_dst, ctx->status_dev, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(ctx->status_dev, 0, sizeof(unsigned), ctx->stream);
+  return e == cudaSuccess ? QCUR_OK : ctx->cuda_fail(e, "status_async");
+}
+
+int qcur_status_map(qcur_ctx* ctx, unsigned bits) { return map_status(ctx, bits); }
+
 int qcur_profile(qcur_ctx* ctx, int on) {
   if (!ctx) return QCUR_E_PARAMETER;
   cudaStreamSynchronize(ctx->stream);
