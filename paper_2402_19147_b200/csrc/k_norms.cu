@@ -98,11 +98,9 @@ __global__ void __launch_bounds__(kChunkThreads) pairwise_chunks(const double* _
   const int pid = pw.chunk_plan[chunk];
   const int len = pw.plan_len[pid];
   const int leaf0 = pw.plan_leaf_ptr[pid], nleaves = pw.plan_leaf_ptr[pid + 1] - leaf0;
-  const double* src = data + seg * seg_stride + pw.chunk_off[chunk];
-  double* vals = sm;            // [len]
-  double* leafv = sm + len;     // [nleaves]
-  for (int t = threadIdx.x; t < len; t += blockDim.x) vals[t] = src[t];
-  __syncthreads();
+  const double* __restrict__ vals = data + seg * seg_stride + pw.chunk_off[chunk];  // leaves read from HBM
+  double* leafv = sm;  // [nleaves + chunk nodes]
+  (void)len;
   const int q = threadIdx.x & 7;
   for (int base = 0; base < nleaves; base += kChunkThreads / 8) {
     const int leaf = base + (threadIdx.x >> 3);
@@ -194,8 +192,8 @@ void launch_pairwise(const double* data, int64_t nseg, int64_t seg_stride, const
     cudaFuncSetAttribute(pairwise_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr_set = true;
   }
-  // dynamic smem only as large as the largest chunk needs
-  size_t need = (size_t)(pw.max_chunk_len + pw.max_chunk_len / 8 + 8) * sizeof(double);
+  // dynamic smem: leaf sums and the chunk's tree nodes only (the data streams from HBM)
+  size_t need = (size_t)(pw.max_chunk_len / 4 + 16) * sizeof(double);
   if (pw.nnodes == 0) {
     // single chunk per segment: write straight to out
     dim3 grid(1, (unsigned)nseg);
