@@ -403,7 +403,26 @@ class DeviceApprox:
         self.R = d.empty_q(r, n)
         self.err4 = d.empty(4)
 
-    def run(self, xd, strategy: str, seed: int, psnr_scale: float = 0.0, core: str = "projection") -> None:
+    def run(self, xd, strategy: str, seed: int, psnr_scale: float = 0.0, core: str = "projection",
+            graph: bool = False) -> None:
+        """One approximation (qcur_approx).  graph=True replays the whole approximation as
+        one CUDA graph (captured on the first call with these arguments after a normal run
+        of the same shape): the ~45 launches go out as a single submission."""
+        if graph:
+            key = (xd.data_ptr(), strategy, int(seed), float(psnr_scale), core)
+            if getattr(self, "_gkey", None) != key:
+                torch = self.dev.torch
+                self.run(xd, strategy, seed, psnr_scale, core)  # sizes the workspace (no allocation inside)
+                self.dev.synchronize()
+                g = torch.cuda.CUDAGraph()
+                before = self.dev.launches()
+                with torch.cuda.graph(g):
+                    self.run(xd, strategy, seed, psnr_scale, core)
+                self._graph, self._gkey = g, key
+                self.graph_kernels = self.dev.launches() - before
+            self._graph.replay()
+            self.graph_replays = getattr(self, "graph_replays", 0) + 1
+            return
         core_code = _check_core(core)
         state = _native.state_from_seed(seed)
         self.dev.call("qcur_approx", xd.data_ptr(), self.m, self.n, _native.STRATEGY_CODES[_check_strategy(strategy)],
