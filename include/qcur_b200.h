@@ -206,6 +206,13 @@ int qcur_gather_rows(qcur_ctx* ctx, const double* x_dev, int64_t n, const int64_
 int qcur_qgemm_ex(qcur_ctx* ctx, int opA, int opB, int64_t M, int64_t N, int64_t K, double alpha, const double* a_dev,
                   int64_t lda, const double* b_dev, int64_t ldb, double beta, double* c_dev, int64_t ldc, int flags);
 /* X = L^{-1} for G = L L^H (cluster kernel, or blocked for q > 304) */
+/* Engine of the X Q_R contraction inside qmcur: 0 auto (INT8 when large), 1 FP64 DMMA, 2 INT8 (Ozaki II).
+   The environment variable QCUR_GEMM=dmma|int8 sets the initial mode of new contexts. */
+int qcur_set_gemm_mode(qcur_ctx* ctx, int mode);
+/* C (M x N) = A (M x K) * B (K x N), op N, on the INT8 tensor cores by exact modular arithmetic
+   (Ozaki scheme II, nmod moduli; 0 = default).  Same contract as qcur_qgemm with alpha = 1, beta = 0. */
+int qcur_qgemm_int8(qcur_ctx* ctx, int64_t M, int64_t N, int64_t K, const double* a_dev, int64_t lda,
+                    const double* b_dev, int64_t ldb, double* c_dev, int64_t ldc, int nmod);
 int qcur_chol_inv(qcur_ctx* ctx, const double* g_dev, int64_t q, double* x_dev);
 /* second CholeskyQR pass: L2^{-1} of G2 = I + E by series */
 int qcur_series_l2inv(qcur_ctx* ctx, const double* g2_dev, int64_t q, double* l2inv_dev);

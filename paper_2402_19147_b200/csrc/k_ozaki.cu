@@ -1,0 +1,791 @@
+// Y = X * B for quaternion matrices on the INT8 tensor cores (tcgen05.mma kind::i8),
+// by exact modular arithmetic (Ozaki scheme II).
+//
+// This is the big contraction of the projection core, Y = X Q_R (cur.py:268 via
+// qmat_matmul, quat.py:274-296): X is m x n, B is n x r, 32 m n r flop.  The FP64
+// tensor path (mma.sync DMMA, k_qgemm.cu) tops out near 37 TFLOP/s on B200; the
+// INT8 tcgen05 path runs at ~4.5 POP/s, so the product is computed exactly in
+// integers instead:
+//
+//  1. Scale each row i of X (as reals, m x 4n) by 2^ex_i and each quaternion
+//     column j of B by 2^fx_j and round to integers X', B' with |X'|, |B'| <= 2^bits.
+//     This is the only rounding of the scheme: relative to the row (column) maximum it is
+//     2^-(bits+1), below the FP64 accumulation error of a K = 4n dot product.
+//  2. The real product Z = X' E(B') (E = the 4x4 Hamilton expansion, E[4k+s][4j+t] =
+//     sign(s,t) b_kj[s^t]) is an integer with |Z| <= 4n 2^(2 bits) < M/2,
+//     M = p_1 ... p_L for L pairwise coprime moduli p_l <= 256.  For every l the
+//     residues X' mod p_l, E(B') mod p_l are signed bytes and Z mod p_l follows from
+//     one int8 GEMM with exact int32 accumulation (|sum| <= 4n 2^14 < 2^31).
+//  3. Z is recovered from its L residues by the Chinese remainder theorem in 128-bit
+//     integer arithmetic and scaled back: Y = 2^-(ex_i + fx_j) Z (one rounding).
+//
+// Kernels: k_oz_xres (row max + residues of X, HBM-bound), k_oz_bmax/k_oz_bres (B,
+// small), k_oz_gemm (tcgen05, TMA, TMEM; persistent, one CTA per SM), k_oz_crt.
+// The GEMM kernel: warp 0 issues TMA loads of 128x128-byte A tiles and BNx128-byte B
+// tiles (128-byte swizzle, K-major) into a 4-stage mbarrier ring; warp 1 (one thread)
+// issues tcgen05.mma.cta_group::1.kind::i8 (M=128, N=BN, K=32) into a double-buffered
+// TMEM accumulator (2 x 256 columns) and commits stage/accumulator barriers; warps 2-5
+// drain the accumulator with tcgen05.ld, reduce it mod p_l and store residue bytes.
+// Work units are (modulus, 128-row block, BN-column block) with the whole K range, so
+// every result is a fixed integer: bitwise deterministic.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstring>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace qcur {
+
+namespace {
+
+constexpr int kOzMaxMod = 20;
+// pairwise coprime, largest first
+constexpr int kOzModuli[kOzMaxMod] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227,
+                                      223, 217, 211, 199, 197, 193, 191, 181, 179, 173};
+constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: x + kMagic rounds x to an integer
+
+struct OzMods {
+  int L;
+  int p[kOzMaxMod];
+  double pd[kOzMaxMod];
+  double pinv[kOzMaxMod];
+};
+
+__device__ __forceinline__ int lo_int(double t) { return __double2loint(t); }
+
+// v: integer-valued double, |v| < 2^51.  Returns r = v mod p as a byte in [-128, 127].
+__device__ __forceinline__ unsigned residue_byte(double v, int l, const OzMods& md) {
+  if (l == 0) return (unsigned)lo_int(v + kMagic) & 0xffu;  // p = 256: the low byte
+  const double q = fma(v, md.pinv[l], kMagic) - kMagic;    // round(v / p), maybe off by one
+  int r = lo_int(fma(-q, md.pd[l], v) + kMagic);           // exact, |r| <= p/2 + 1
+  const int p = md.p[l];
+  r = r > 127 ? r - p : r;
+  r = r < -128 ? r + p : r;
+  return (unsigned)r & 0xffu;
+}
+
+// x * 2^e, exact for every finite x whose result is representable (two steps keep 2^e finite)
+__device__ __forceinline__ double scale2(double x, int e) {
+  const int e1 = e / 2;
+  return x * ldexp(1.0, e1) * ldexp(1.0, e - e1);
+}
+
+// ---------------------------------------------------------------------------
+// residues of X: one CTA per row (K = 4n reals), |X'| <= 2^bits.
+// X' = rint(x 2^e) is split into four signed 13-bit limbs (as exact floats), and for every
+// odd modulus r = sum_i limb_i (2^(13 i) mod p) (exact in fp32, |.| < 2^22) is reduced with
+// one rounded quotient; p = 256 takes the low byte of X'.  All moduli are compile-time
+// constants (template L), so the modulus loop is straight-line FP32 code.
+// ---------------------------------------------------------------------------
+constexpr float kMagicF = 12582912.0f;  // 1.5 * 2^23
+
+__host__ __device__ constexpr int cmod(long long v, int p) {
+  long long r = v % p;
+  if (r < 0) r += p;
+  return (int)(r > p / 2 ? r - p : r);  // centered
+}
+
+
+// residue of the limb sum modulo P; the low byte of the result is r mod 256 (two's complement)
+// Packed FP32 pairs (sm_100 FFMA2 / FADD2): two values per instruction.
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk(float lo, float hi) {
+  return (f32x2)__float_as_uint(lo) | ((f32x2)__float_as_uint(hi) << 32);
+}
+__device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f32x2 fadd2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2 fmul2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// per odd modulus (index l >= 1): 2^13, 2^26, 2^39 mod p (centred), 1/p and -p, each duplicated
+struct OzPairConsts {
+  f32x2 c1[kOzMaxMod], c2[kOzMaxMod], c3[kOzMaxMod], pinv[kOzMaxMod], negp[kOzMaxMod];
+};
+constexpr unsigned f2u(float f) { return __builtin_bit_cast(unsigned, f); }
+constexpr f32x2 dup(float f) { return (f32x2)f2u(f) | ((f32x2)f2u(f) << 32); }
+constexpr OzPairConsts make_pair_consts() {
+  OzPairConsts k{};
+  for (int l = 0; l < kOzMaxMod; ++l) {
+    const int p = kOzModuli[l];
+    k.c1[l] = dup((float)cmod(1ll << 13, p));
+    k.c2[l] = dup((float)cmod(1ll << 26, p));
+    k.c3[l] = dup((float)cmod(1ll << 39, p));
+    k.pinv[l] = dup(1.0f / (float)p);
+    k.negp[l] = dup(-(float)p);
+  }
+  return k;
+}
+__constant__ OzPairConsts c_pair = make_pair_consts();
+
+// residues of a pair of values (limbs f0..f3 as pairs) modulo kOzModuli[l]; the low byte of
+// each 32-bit half is r mod 256 (two's complement)
+template <int l>
+__device__ __forceinline__ f32x2 pair_residue(f32x2 f0, f32x2 f1, f32x2 f2, f32x2 f3, f32x2 mag, f32x2 nmag) {
+  const f32x2 t = ffma2(f3, c_pair.c3[l], ffma2(f2, c_pair.c2[l], ffma2(f1, c_pair.c1[l], f0)));
+  const f32x2 q = fadd2(ffma2(t, c_pair.pinv[l], mag), nmag);  // round(t / p)
+  f32x2 r = ffma2(q, c_pair.negp[l], t);                       // exact, |r| <= p/2 + 1
+  constexpr int P = kOzModuli[l];
+  if constexpr (P > 253) {  // p = 255: r = 128 -> r - p
+    float lo = __uint_as_float((unsigned)r), hi = __uint_as_float((unsigned)(r >> 32));
+    lo = lo > 127.0f ? lo - (float)P : lo;
+    hi = hi > 127.0f ? hi - (float)P : hi;
+    r = pk(lo, hi);
+  }
+  return fadd2(r, mag);
+}
+// low bytes of the four halves of two pairs -> one word
+__device__ __forceinline__ unsigned pack_pairs(f32x2 a, f32x2 b) {
+  return __byte_perm(__byte_perm((unsigned)a, (unsigned)(a >> 32), 0x0040),
+                     __byte_perm((unsigned)b, (unsigned)(b >> 32), 0x0040), 0x5410);
+}
+
+__device__ __forceinline__ double amax4(const double4& v) {
+  return fmax(fmax(fabs(v.x), fabs(v.y)), fmax(fabs(v.z), fabs(v.w)));
+}
+
+template <int L, int NT>
+__global__ void __launch_bounds__(NT, 2) k_oz_xres(const double* __restrict__ X, int64_t K, int64_t ldx, int bits,
+                                                   uint8_t* __restrict__ res, int64_t pitch, int64_t plane,
+                                                   int* __restrict__ ex) {
+  __shared__ double sh[NT / 32];
+  const int64_t row = blockIdx.x;
+  const double* x = X + row * ldx;
+  double mx = 0.0;
+  int64_t k = threadIdx.x * 4;
+  for (; k + 3 * NT * 4 < K; k += 4 * NT * 4) {  // four independent 32-byte loads in flight
+    const double4 v0 = *reinterpret_cast<const double4*>(x + k);
+    const double4 v1 = *reinterpret_cast<const double4*>(x + k + NT * 4);
+    const double4 v2 = *reinterpret_cast<const double4*>(x + k + 2 * NT * 4);
+    const double4 v3 = *reinterpret_cast<const double4*>(x + k + 3 * NT * 4);
+    mx = fmax(mx, fmax(fmax(amax4(v0), amax4(v1)), fmax(amax4(v2), amax4(v3))));
+  }
+  for (; k < K; k += NT * 4) mx = fmax(mx, amax4(*reinterpret_cast<const double4*>(x + k)));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  mx = 0.0;
+#pragma unroll
+  for (int w = 0; w < NT / 32; ++w) mx = fmax(mx, sh[w]);
+  int e = 0;
+  if (mx > 0.0) {
+    int E;
+    frexp(mx, &E);  // mx = f 2^E, f in [0.5, 1)
+    e = bits - E;
+  }
+  if (threadIdx.x == 0) ex[row] = e;
+  const double s1 = ldexp(1.0, e / 2), s2 = ldexp(1.0, e - e / 2);
+  const long long magic_bits = __double_as_longlong(kMagic);
+  const f32x2 mag = dup(kMagicF), nmag = dup(-kMagicF), lmag = dup(-8388608.0f);
+  uint8_t* out = res + row * pitch;
+  for (int64_t k0 = threadIdx.x * 16; k0 < pitch; k0 += NT * 16) {
+    f32x2 f[8][4];  // pair h holds values 2h, 2h+1; limbs 0..3
+    unsigned low[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double4 t = make_double4(0.0, 0.0, 0.0, 0.0);
+      if (k0 + 4 * q < K) t = *reinterpret_cast<const double4*>(x + k0 + 4 * q);
+      const double vv[4] = {t.x, t.y, t.z, t.w};
+      unsigned lb[4], lm[4][4];
+      float sg[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const long long iv = __double_as_longlong(vv[h] * s1 * s2 + kMagic) - magic_bits;  // rint(x 2^e)
+        lb[h] = (unsigned)iv;                                                              // mod 2^32
+        const unsigned long long u = (unsigned long long)(iv < 0 ? -iv : iv);
+        sg[h] = iv < 0 ? -1.0f : 1.0f;
+        lm[h][0] = 0x4B000000u | ((unsigned)u & 0x1fffu);  // limb + 2^23 as a float
+        lm[h][1] = 0x4B000000u | ((unsigned)(u >> 13) & 0x1fffu);
+        lm[h][2] = 0x4B000000u | ((unsigned)(u >> 26) & 0x1fffu);
+        lm[h][3] = 0x4B000000u | (unsigned)(u >> 39);
+      }
+      low[q] = __byte_perm(__byte_perm(lb[0], lb[1], 0x0040), __byte_perm(lb[2], lb[3], 0x0040), 0x5410);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const f32x2 sgn = pk(sg[2 * h], sg[2 * h + 1]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          f[2 * q + h][i] = fmul2(fadd2(((f32x2)lm[2 * h][i]) | ((f32x2)lm[2 * h + 1][i] << 32), lmag), sgn);
+      }
+    }
+    *reinterpret_cast<uint4*>(out + k0) = make_uint4(low[0], low[1], low[2], low[3]);  // p = 256
+#define OZ_PLANE(l)                                                                                     \
+    if constexpr (l < L) {                                                                              \
+      unsigned w[4];                                                                                    \
+      _Pragma("unroll") for (int q = 0; q < 4; ++q) w[q] = pack_pairs(                                  \
+          pair_residue<l>(f[2 * q][0], f[2 * q][1], f[2 * q][2], f[2 * q][3], mag, nmag),               \
+          pair_residue<l>(f[2 * q + 1][0], f[2 * q + 1][1], f[2 * q + 1][2], f[2 * q + 1][3], mag, nmag)); \
+      *reinterpret_cast<uint4*>(out + (l) * plane + k0) = make_uint4(w[0], w[1], w[2], w[3]);           \
+    }
+    OZ_PLANE(1) OZ_PLANE(2) OZ_PLANE(3) OZ_PLANE(4) OZ_PLANE(5) OZ_PLANE(6) OZ_PLANE(7) OZ_PLANE(8)
+    OZ_PLANE(9) OZ_PLANE(10) OZ_PLANE(11) OZ_PLANE(12) OZ_PLANE(13) OZ_PLANE(14) OZ_PLANE(15)
+    OZ_PLANE(16) OZ_PLANE(17) OZ_PLANE(18) OZ_PLANE(19)
+#undef OZ_PLANE
+  }
+}
+
+// column exponents of B (Kq x Nq quaternions): one warp per quaternion column
+__global__ void k_oz_bmax(const double* __restrict__ B, int64_t Kq, int64_t Nq, int64_t ldb, int bits,
+                          int* __restrict__ fx) {
+  const int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (j >= Nq) return;
+  double mx = 0.0;
+  for (int64_t k = lane; k < Kq; k += 32) {
+    const Quat q = ldq_nc(B + (k * ldb + j) * 4);
+    mx = fmax(mx, fmax(fmax(fabs(q.w), fabs(q.x)), fmax(fabs(q.y), fabs(q.z))));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) {
+    int e = 0;
+    if (mx > 0.0) {
+      int E;
+      frexp(mx, &E);
+      e = bits - E;
+    }
+    fx[j] = e;
+  }
+}
+
+// residues of E(B') stored K-major: row 4j+t, byte 4k+s = sign(s,t) b'_kj[s^t] mod p
+__global__ void k_oz_bres(const double* __restrict__ B, int64_t Kq, int64_t Nq, int64_t ldb,
+                          const __grid_constant__ OzMods md, const int* __restrict__ fx, uint8_t* __restrict__ res,
+                          int64_t pitch, int64_t plane) {
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t kq_pad = pitch / 4;
+  if (id >= Nq * kq_pad) return;
+  const int64_t j = id / kq_pad, k = id - j * kq_pad;
+  double b[4] = {0.0, 0.0, 0.0, 0.0};
+  if (k < Kq) {
+    const Quat q = ldq_nc(B + (k * ldb + j) * 4);
+    const int e = fx[j];
+    b[0] = (scale2(q.w, e) + kMagic) - kMagic;
+    b[1] = (scale2(q.x, e) + kMagic) - kMagic;
+    b[2] = (scale2(q.y, e) + kMagic) - kMagic;
+    b[3] = (scale2(q.z, e) + kMagic) - kMagic;
+  }
+  // negative entries of E: (s,t) = (1,0) (2,0) (3,0) (3,1) (1,2) (2,3)
+  for (int l = 0; l < md.L; ++l) {
+    unsigned r[4], n[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      r[u] = residue_byte(b[u], l, md);
+      n[u] = (0u - r[u]) & 0xffu;  // -r: for p = 256, -(-128) wraps to -128 (same residue)
+    }
+    uint8_t* o = res + l * plane + (4 * j) * pitch + 4 * k;
+    // t = 0: s0 +b0, s1 -b1, s2 -b2, s3 -b3
+    *reinterpret_cast<unsigned*>(o) = r[0] | (n[1] << 8) | (n[2] << 16) | (n[3] << 24);
+    // t = 1: s0 +b1, s1 +b0, s2 +b3, s3 -b2
+    *reinterpret_cast<unsigned*>(o + pitch) = r[1] | (r[0] << 8) | (r[3] << 16) | (n[2] << 24);
+    // t = 2: s0 +b2, s1 -b3, s2 +b0, s3 +b1
+    *reinterpret_cast<unsigned*>(o + 2 * pitch) = r[2] | (n[3] << 8) | (r[0] << 16) | (r[1] << 24);
+    // t = 3: s0 +b3, s1 +b2, s2 -b1, s3 +b0
+    *reinterpret_cast<unsigned*>(o + 3 * pitch) = r[3] | (r[2] << 8) | (n[1] << 16) | (r[0] << 24);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// tcgen05 int8 GEMM:  res[l][i][j] = (A_l[i,:] . B_l[j,:]) mod p_l  (bytes in [0, p_l))
+// ---------------------------------------------------------------------------
+// a unit is 256 rows (two M = 128 accumulators sharing every B tile) x BN <= 256 columns
+constexpr int OZ_BM = 256, OZ_BK = 128, OZ_STAGES = 3, OZ_THREADS = 320;
+constexpr int OZ_A_BYTES = OZ_BM * OZ_BK, OZ_B_SLOT = 256 * OZ_BK;
+constexpr int OZ_SMEM = 1024 + OZ_STAGES * (OZ_A_BYTES + OZ_B_SLOT) + 256;
+
+struct OzGemm {
+  int64_t m, N;
+  int L, kblocks, mblocks, nblocks, BN, total;
+  uint32_t idesc;
+  uint8_t* res;
+  int64_t res_pitch, res_plane;
+  int p[kOzMaxMod];
+  double pinv[kOzMaxMod];
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// K-major operand tile with 128-byte rows, 128-byte swizzle, 8-row groups 1024 bytes apart
+__device__ __forceinline__ uint64_t umma_desc(uint32_t addr) {
+  return (uint64_t)((addr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void unit_coords(const OzGemm& P, int u, int& l, int& mb, int& nb) {
+  nb = u % P.nblocks;
+  const int t = u / P.nblocks;
+  mb = t % P.mblocks;
+  l = t / P.mblocks;
+}
+
+__global__ void __launch_bounds__(OZ_THREADS, 1)
+    k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ OzGemm P) {
+  extern __shared__ uint8_t smem_raw[];
+  const unsigned pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+  uint8_t* smem = smem_raw + pad;
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + OZ_STAGES * OZ_A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + OZ_STAGES * OZ_B_SLOT);
+  uint64_t* empty = full + OZ_STAGES;
+  uint64_t* tfull = empty + OZ_STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < OZ_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 8);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tslot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+      const unsigned bytes = OZ_A_BYTES + P.BN * OZ_BK;
+      int stage = 0;
+      unsigned phase = 0;
+      for (int u = blockIdx.x; u < P.total; u += gridDim.x) {
+        int l, mb, nb;
+        unit_coords(P, u, l, mb, nb);
+        for (int kb = 0; kb < P.kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1u);
+          mbar_expect_tx(&full[stage], bytes);
+          tma_load_3d(sA + stage * OZ_A_BYTES, &tmA, kb * OZ_BK, mb * OZ_BM, l, &full[stage]);
+          tma_load_3d(sB + stage * OZ_B_SLOT, &tmB, kb * OZ_BK, nb * P.BN, l, &full[stage]);
+          if (++stage == OZ_STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0;
+      unsigned phase = 0;
+      int t = 0;
+      for (int u = blockIdx.x; u < P.total; u += gridDim.x, ++t) {
+        mbar_wait(tempty, ((unsigned)t & 1u) ^ 1u);  // the epilogue has drained the previous unit
+        tc_fence_after();
+        for (int kb = 0; kb < P.kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * OZ_A_BYTES), b0 = smem_u32(sB + stage * OZ_B_SLOT);
+#pragma unroll
+          for (int k = 0; k < OZ_BK / 32; ++k) {
+            const uint64_t bd = umma_desc(b0 + k * 32);
+            mma_i8(tbase, umma_desc(a0 + k * 32), bd, P.idesc, (kb | k) != 0);                   // rows 0..127
+            mma_i8(tbase + 256, umma_desc(a0 + 128 * OZ_BK + k * 32), bd, P.idesc, (kb | k) != 0);  // 128..255
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == OZ_STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        mma_commit(tfull);
+      }
+    }
+  } else {
+    // 8 epilogue warps: warp w drains TMEM lanes 32 (w % 4) .. +31 of accumulator (w - 2) / 4
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    const int rloc = half * 128 + quarter * 32 + lane;
+    int t = 0;
+    for (int u = blockIdx.x; u < P.total; u += gridDim.x, ++t) {
+      int l, mb, nb;
+      unit_coords(P, u, l, mb, nb);
+      mbar_wait(tfull, (unsigned)t & 1u);
+      tc_fence_after();
+      const int64_t row = (int64_t)mb * OZ_BM + rloc;
+      const int p = P.p[l];
+      const double pinv = P.pinv[l];
+      uint8_t* out = P.res + l * P.res_plane + row * P.res_pitch + (int64_t)nb * P.BN;
+      for (int c0 = 0; c0 < P.BN; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32(tbase + (uint32_t)(half * 256 + c0) + ((uint32_t)(quarter * 32) << 16), v);
+        uint32_t w[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) w[q] = 0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int z = (int)v[i];
+          int r;
+          if (l == 0) {
+            r = z & 255;
+          } else {
+            r = z - (int)floor((double)z * pinv) * p;
+            r = r < 0 ? r + p : r;
+            r = r >= p ? r - p : r;
+          }
+          w[i >> 2] |= (uint32_t)r << (8 * (i & 3));
+        }
+        if (row < P.m) {
+          *reinterpret_cast<uint4*>(out + c0) = make_uint4(w[0], w[1], w[2], w[3]);
+          if (c0 + 32 <= P.BN) *reinterpret_cast<uint4*>(out + c0 + 16) = make_uint4(w[4], w[5], w[6], w[7]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase) : "memory");
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CRT: Z from its residues, Y = 2^-(ex_i + fx_j) Z.  S = sum_l ((r_l w_l) mod p_l) (M / p_l)
+// in 128-bit integers (S < L M), Z = S mod M centred; four outputs per thread.
+// ---------------------------------------------------------------------------
+struct OzCrt {
+  int L;
+  float w[kOzMaxMod];  // (M / p_l)^-1 mod p_l
+  float P[kOzMaxMod], pinv[kOzMaxMod];
+  unsigned long long mi_lo[kOzMaxMod], mi_hi[kOzMaxMod];  // M / p_l
+  unsigned long long M_lo, M_hi;
+  double Md;
+};
+
+template <int L>
+__global__ void __launch_bounds__(256) k_oz_crt(const uint8_t* __restrict__ res, int64_t m, int64_t N, int64_t pitch,
+                                                int64_t plane, const int* __restrict__ ex,
+                                                const int* __restrict__ fx, const __grid_constant__ OzCrt c,
+                                                double* __restrict__ Y, int64_t ldy) {
+  const int64_t nq = N >> 2;  // N = 4 r: one quaternion (4 outputs) per thread
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= m * nq) return;
+  const int64_t i = id / nq, jq = id - i * nq;
+  const uint8_t* rp = res + i * pitch + 4 * jq;
+  unsigned long long lo[4] = {0, 0, 0, 0}, hi[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    const unsigned r4 = __ldg(reinterpret_cast<const unsigned*>(rp + l * plane));
+    const float P = c.P[l], pinv = c.pinv[l];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const float rw = (float)((r4 >> (8 * h)) & 0xffu) * c.w[l];  // < 2^16, exact
+      float t = fmaf(-(fmaf(rw, pinv, kMagicF) - kMagicF), P, rw);
+      t = t < 0.0f ? t + P : t;
+      const unsigned long long tt = (unsigned long long)(unsigned)t;
+      const unsigned long long plo = c.mi_lo[l] * tt, phi = c.mi_hi[l] * tt + __umul64hi(c.mi_lo[l], tt);
+      const unsigned long long nlo = lo[h] + plo;
+      hi[h] += phi + (nlo < plo ? 1ull : 0ull);
+      lo[h] = nlo;
+      // keep S < 2M (< 2^127 for L <= 16): subtract M once it is reached
+      if (hi[h] > c.M_hi || (hi[h] == c.M_hi && lo[h] >= c.M_lo)) {
+        hi[h] -= c.M_hi + (lo[h] < c.M_lo ? 1ull : 0ull);
+        lo[h] -= c.M_lo;
+      }
+    }
+  }
+  const int e = -(ex[i] + fx[jq]);
+  const double s1 = ldexp(1.0, e / 2), s2 = ldexp(1.0, e - e / 2);
+  double out[4];
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    unsigned __int128 S = ((unsigned __int128)hi[h] << 64) | lo[h];
+    const unsigned __int128 M = ((unsigned __int128)c.M_hi << 64) | c.M_lo;
+    const double sd = (double)hi[h] * 18446744073709551616.0 + (double)lo[h];
+    long long q = (long long)floor(sd / c.Md);
+    q = q < 0 ? 0 : q;
+    S -= M * (unsigned long long)q;
+    if ((__int128)S < 0) S += M;  // the estimate was one too large
+    if (S >= M) S -= M;
+    __int128 Z = (__int128)S;
+    if (S > (M >> 1)) Z -= (__int128)M;
+    const double z = (double)(long long)(Z >> 64) * 18446744073709551616.0 + (double)(unsigned long long)Z;
+    out[h] = z * s1 * s2;
+  }
+  double* y = Y + i * ldy + 4 * jq;
+  *reinterpret_cast<double4*>(y) = make_double4(out[0], out[1], out[2], out[3]);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 oz_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+bool oz_map(CUtensorMap* map, const uint8_t* base, int64_t K, int64_t rows, int64_t pitch, int64_t L, int box_rows) {
+  auto enc = oz_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)L};
+  cuuint64_t strides[2] = {(cuuint64_t)pitch, (cuuint64_t)(pitch * rows)};
+  cuuint32_t box[3] = {(cuuint32_t)OZ_BK, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int oz_sms() {
+  static int sms = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+  }();
+  return sms;
+}
+
+struct OzPlan {
+  int L, bits;
+  int64_t K, Kpitch, N, Npitch, BN, nblocks;
+  size_t off_ares, off_bres, off_res, off_ex, off_fx, total;
+};
+
+OzPlan oz_plan(int64_t m, int64_t n, int64_t r, int L) {
+  OzPlan p{};
+  p.L = L;
+  p.K = 4 * n;
+  p.Kpitch = (p.K + 15) / 16 * 16;
+  p.N = 4 * r;
+  p.nblocks = (p.N + 255) / 256;
+  p.BN = 16 * ((p.N + 16 * p.nblocks - 1) / (16 * p.nblocks));
+  p.Npitch = p.nblocks * p.BN;
+  double log2M = 0.0;
+  for (int l = 0; l < L; ++l) log2M += std::log2((double)kOzModuli[l]);
+  // |Z| <= K 2^(2 bits) < M / 2
+  int bits = (int)std::floor((log2M - 1.0 - std::log2((double)p.K) - 1e-6) / 2.0);
+  p.bits = bits > 51 ? 51 : bits;
+  auto al = [](size_t v) { return (v + 255) / 256 * 256; };
+  size_t o = 0;
+  p.off_ares = o;
+  o = al(o + (size_t)L * m * p.Kpitch);
+  p.off_bres = o;
+  o = al(o + (size_t)L * p.N * p.Kpitch);
+  p.off_res = o;
+  o = al(o + (size_t)L * m * p.Npitch);
+  p.off_ex = o;
+  o = al(o + (size_t)m * 4);
+  p.off_fx = o;
+  o = al(o + (size_t)r * 4);
+  p.total = o;
+  return p;
+}
+
+OzMods oz_mods(int L) {
+  OzMods md{};
+  md.L = L;
+  for (int l = 0; l < L; ++l) {
+    md.p[l] = kOzModuli[l];
+    md.pd[l] = (double)kOzModuli[l];
+    md.pinv[l] = 1.0 / (double)kOzModuli[l];
+  }
+  return md;
+}
+
+OzCrt oz_crt(int L) {
+  OzCrt c{};
+  c.L = L;
+  unsigned __int128 M = 1;
+  for (int l = 0; l < L; ++l) M *= (unsigned)kOzModuli[l];
+  c.M_lo = (unsigned long long)M;
+  c.M_hi = (unsigned long long)(M >> 64);
+  c.Md = (double)c.M_hi * 18446744073709551616.0 + (double)c.M_lo;
+  for (int l = 0; l < L; ++l) {
+    const int p = kOzModuli[l];
+    const unsigned __int128 mi = M / (unsigned)p;
+    c.mi_lo[l] = (unsigned long long)mi;
+    c.mi_hi[l] = (unsigned long long)(mi >> 64);
+    const int mr = (int)(mi % (unsigned)p);
+    int w = 1;
+    while ((mr * w) % p != 1) ++w;
+    c.w[l] = (float)w;
+    c.P[l] = (float)p;
+    c.pinv[l] = 1.0f / (float)p;
+  }
+  return c;
+}
+
+}  // namespace
+
+int ozaki_max_moduli() { return kOzMaxMod; }
+
+size_t ozaki_workspace_bytes(int64_t m, int64_t n, int64_t r, int L) { return oz_plan(m, n, r, L).total + 1024; }
+
+bool ozaki_supported(int64_t m, int64_t n, int64_t r) {
+  // int32 accumulation: 4n * 2^14 < 2^31;  TMA: rows and planes < 2^31 bytes apart
+  return m >= 1 && n >= 1 && r >= 1 && 4 * n <= 131068 && (4 * n) % 4 == 0;
+}
+
+// Phase 1 (depends on X only; may run on a side stream): row exponents and residues of X.
+int launch_ozaki_prepare(const double* X, int64_t m, int64_t n, int64_t ldx, int64_t r, int L, void* workspace,
+                         cudaStream_t st) {
+  if (L < 14 || L > 16) return 1;
+  const OzPlan pl = oz_plan(m, n, r, L);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(((uintptr_t)workspace + 255) / 256 * 256);
+  uint8_t* ares = ws + pl.off_ares;
+  int* ex = reinterpret_cast<int*>(ws + pl.off_ex);
+  const int64_t aplane = m * pl.Kpitch;
+  ++::qcur::g_launches;
+  switch (L) {
+    case 14: k_oz_xres<14, 256><<<(unsigned)m, 256, 0, st>>>(X, pl.K, ldx * 4, pl.bits, ares, pl.Kpitch, aplane, ex); break;
+    case 15: k_oz_xres<15, 256><<<(unsigned)m, 256, 0, st>>>(X, pl.K, ldx * 4, pl.bits, ares, pl.Kpitch, aplane, ex); break;
+    default: k_oz_xres<16, 256><<<(unsigned)m, 256, 0, st>>>(X, pl.K, ldx * 4, pl.bits, ares, pl.Kpitch, aplane, ex); break;
+  }
+  return 0;
+}
+
+// Phase 2: residues of E(B), the L int8 GEMMs on tcgen05 and the CRT into Y (m x r).
+int launch_ozaki_finish(int64_t m, int64_t n, const double* B, int64_t r, int64_t ldb, double* Y, int64_t ldy, int L,
+                        void* workspace, cudaStream_t st) {
+  if (L < 14 || L > 16) return 1;
+  const OzPlan pl = oz_plan(m, n, r, L);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(((uintptr_t)workspace + 255) / 256 * 256);
+  uint8_t* ares = ws + pl.off_ares;
+  uint8_t* bres = ws + pl.off_bres;
+  uint8_t* res = ws + pl.off_res;
+  int* ex = reinterpret_cast<int*>(ws + pl.off_ex);
+  int* fx = reinterpret_cast<int*>(ws + pl.off_fx);
+  const OzMods md = oz_mods(L);
+  const int64_t bplane = pl.N * pl.Kpitch, rplane = m * pl.Npitch;
+
+  ++::qcur::g_launches;
+  k_oz_bmax<<<(unsigned)((r + 7) / 8), 256, 0, st>>>(B, n, r, ldb, pl.bits, fx);
+  const int64_t nb_threads = r * (pl.Kpitch / 4);
+  ++::qcur::g_launches;
+  k_oz_bres<<<(unsigned)((nb_threads + 255) / 256), 256, 0, st>>>(B, n, r, ldb, md, fx, bres, pl.Kpitch, bplane);
+
+  CUtensorMap tmA, tmB;
+  if (!oz_map(&tmA, ares, pl.K, m, pl.Kpitch, L, OZ_BM) || !oz_map(&tmB, bres, pl.K, pl.N, pl.Kpitch, L, (int)pl.BN))
+    return 2;
+  OzGemm P{};
+  P.m = m;
+  P.N = pl.N;
+  P.L = L;
+  P.kblocks = (int)((pl.K + OZ_BK - 1) / OZ_BK);
+  P.mblocks = (int)((m + OZ_BM - 1) / OZ_BM);
+  P.nblocks = (int)pl.nblocks;
+  P.BN = (int)pl.BN;
+  P.total = L * P.mblocks * P.nblocks;
+  // kind::i8: D = s32 (bits 4-5 = 2), A/B signed (bits 7-9, 10-12 = 1), K-major, N>>3 at 17, M>>4 at 24
+  P.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(P.BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);  // MMA M = 128 (two per unit)
+  P.res = res;
+  P.res_pitch = pl.Npitch;
+  P.res_plane = rplane;
+  for (int l = 0; l < L; ++l) {
+    P.p[l] = kOzModuli[l];
+    P.pinv[l] = 1.0 / (double)kOzModuli[l];
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_oz_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM);
+    attr = true;
+  }
+  const int grid = P.total < oz_sms() ? P.total : oz_sms();
+  ++::qcur::g_launches;
+  k_oz_gemm<<<grid, OZ_THREADS, OZ_SMEM, st>>>(tmA, tmB, P);
+
+  const OzCrt cc = oz_crt(L);
+  const unsigned cblocks = (unsigned)((m * r + 255) / 256);
+  ++::qcur::g_launches;
+  switch (L) {
+    case 14: k_oz_crt<14><<<cblocks, 256, 0, st>>>(res, m, pl.N, pl.Npitch, rplane, ex, fx, cc, Y, ldy * 4); break;
+    case 15: k_oz_crt<15><<<cblocks, 256, 0, st>>>(res, m, pl.N, pl.Npitch, rplane, ex, fx, cc, Y, ldy * 4); break;
+    default: k_oz_crt<16><<<cblocks, 256, 0, st>>>(res, m, pl.N, pl.Npitch, rplane, ex, fx, cc, Y, ldy * 4); break;
+  }
+  return 0;
+}
+
+// Y (m x r) = X (m x n) * B (n x r), interleaved quaternions (ld in quaternions)
+int launch_ozaki_gemm(const double* X, int64_t m, int64_t n, int64_t ldx, const double* B, int64_t r, int64_t ldb,
+                      double* Y, int64_t ldy, int L, void* workspace, cudaStream_t st) {
+  int rc = launch_ozaki_prepare(X, m, n, ldx, r, L, workspace, st);
+  return rc ? rc : launch_ozaki_finish(m, n, B, r, ldb, Y, ldy, L, workspace, st);
+}
+
+}  // namespace qcur

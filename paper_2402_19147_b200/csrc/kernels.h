@@ -153,6 +153,19 @@ void launch_sumsq(const double* X, int64_t count, double* partials, int64_t npar
 void launch_synth_image(int64_t m, int64_t n, int L, uint64_t seed, double sigma, double* F, double* part,
                         double* X, cudaStream_t st);
 
+// k_ozaki.cu : Y (m x r) = X (m x n) * B (n x r) on the INT8 tensor cores (tcgen05 kind::i8) by exact
+// modular arithmetic over L moduli (Ozaki scheme II); interleaved quaternions, ld in quaternions.
+int ozaki_max_moduli();
+bool ozaki_supported(int64_t m, int64_t n, int64_t r);
+size_t ozaki_workspace_bytes(int64_t m, int64_t n, int64_t r, int L);
+int launch_ozaki_gemm(const double* X, int64_t m, int64_t n, int64_t ldx, const double* B, int64_t r, int64_t ldb,
+                      double* Y, int64_t ldy, int L, void* workspace, cudaStream_t st);
+// the same in two phases: prepare (residues of X; depends on X only) and finish (B, GEMMs, CRT)
+int launch_ozaki_prepare(const double* X, int64_t m, int64_t n, int64_t ldx, int64_t r, int L, void* workspace,
+                         cudaStream_t st);
+int launch_ozaki_finish(int64_t m, int64_t n, const double* B, int64_t r, int64_t ldb, double* Y, int64_t ldy, int L,
+                        void* workspace, cudaStream_t st);
+
 // fp64 peak probe (bench roofline denominator)
 double run_dmma_peak(int sms, cudaStream_t st);
 

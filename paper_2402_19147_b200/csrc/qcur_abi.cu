@@ -2,6 +2,7 @@
 // See include/qcur_b200.h for the contract of every entry point and the
 // reference function it replaces.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -21,6 +22,7 @@ unsigned long long qcur::g_launches = 0;
 namespace {
 
 constexpr double kEps = 2.220446049250313e-16;
+constexpr int kOzakiModuli = 15;  // default modulus count of the INT8 (Ozaki II) GEMM
 
 // Optional phase timing: CUDA events recorded on the launching stream between
 // pipeline phases; harvested (after a sync) by qcur_profile_read.
@@ -67,6 +69,14 @@ struct qcur_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // D2H of finished factors, overlapped with the rest of the pipeline
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t side_stream = nullptr;  // residues of X for the INT8 GEMM, overlapped with the factorizations
+  cudaEvent_t ev_sfork = nullptr, ev_sjoin = nullptr;
+  int gemm_mode = 0;                   // Y = X Q_R: 0 auto, 1 FP64 DMMA, 2 INT8 tcgen05 (Ozaki II)
+  // qcur_approx runs its pipeline on a high-priority stream forked from the caller's, so that
+  // the low-priority side stream (residues of X) only fills SMs the pipeline leaves idle
+  cudaStream_t hi_stream = nullptr;
+  cudaEvent_t ev_hfork = nullptr, ev_hjoin = nullptr;
+  bool prio = true;
   unsigned* status_dev = nullptr;
   unsigned* status_host = nullptr;  // pinned
   unsigned* counters = nullptr;     // split-K tickets for launch_qgemm (kept zero between launches)
@@ -325,6 +335,12 @@ GemmArgs gargs(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, in
   g.alpha = alpha;
   g.beta = beta;
   return g;
+}
+
+// Y = X Q_R on the INT8 tensor cores?  auto: when the product is large enough to pay for the residues
+bool use_int8(const qcur_ctx* ctx, int64_t m, int64_t n, int64_t r) {
+  if (ctx->gemm_mode == 1 || !ozaki_supported(m, n, r)) return false;
+  return ctx->gemm_mode == 2 || (double)m * (double)n * (double)r >= 2e8;
 }
 
 // structure hints: op(B) upper triangular; Hermitian output with only its lower triangle consumed
@@ -631,6 +647,7 @@ size_t qmcur_ws_bytes(int64_t m, int64_t n, int64_t c, int64_t r) {
     GemmArgs g2 = gargs(c, r, m, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0);
     size_t a = qgemm_workspace_bytes(g1), d = qgemm_workspace_bytes(g2);
     b += (a > d ? a : d) + 4096;
+    if (ozaki_supported(m, n, r)) b += ozaki_workspace_bytes(m, n, r, kOzakiModuli) + 4096;
   } else {
     b += pinv_ws_bytes(m, c) + pinv_ws_bytes(r, n) + qbytes(c, m) + qbytes(n, r) + qbytes(m, r);
     GemmArgs g1 = gargs(m, r, n, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0);
@@ -642,7 +659,12 @@ size_t qmcur_ws_bytes(int64_t m, int64_t n, int64_t c, int64_t r) {
 }
 
 int qmcur_core(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, int64_t c, int64_t r, const int64_t* J,
-               const double* C, double* U, const double* R, int core);
+               const double* C, double* U, const double* R, int core, void* oz_ready = nullptr);
+
+// Start the X-only half of the INT8 contraction (residues of X) on the side stream, so that it
+// overlaps the draws and factorizations; the main stream joins before the GEMM.  Returns the
+// workspace holding the residues, or nullptr when the FP64 path will be used.
+void* int8_fork_prepare(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, int64_t r, int* rc);
 
 // Host destinations for qcur_qmcur_host (planar, the reference's QMatrix layout).
 struct HostOut {
@@ -691,7 +713,7 @@ int copy_join(qcur_ctx* ctx) {
 // contraction run; U follows at the end.
 int qmcur_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, const double* colp, const double* rowp,
                int64_t c, int64_t r, const uint64_t state[4], int64_t* J, int64_t* I, double* C, double* U,
-               double* R, int core = QCUR_CORE_PROJECTION, const HostOut* ho = nullptr) {
+               double* R, int core = QCUR_CORE_PROJECTION, const HostOut* ho = nullptr, void* oz_pre = nullptr) {
   cudaStream_t st = ctx->stream;
   // 1. draws: columns first, then rows, one stream (cur.py:251-253)
   Pcg64 g;
@@ -705,6 +727,12 @@ int qmcur_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, const doubl
   jobs[1] = DrawJob{rowp, m, r, g2.state.hi, g2.state.lo, g2.inc.hi, g2.inc.lo, I,
                     ctx->take<double>((size_t)draw_work_doubles(m))};
   if (!jobs[0].work || !jobs[1].work) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (draw)");
+  int rc = QCUR_OK;
+  void* oz = oz_pre;
+  if (!oz && core == QCUR_CORE_PROJECTION && m >= c && n >= r) {
+    oz = int8_fork_prepare(ctx, X, m, n, r, &rc);
+    if (rc) return rc;
+  }
   launch_draw(jobs, 2, ctx->status_dev, st);
   ctx->mark("draw");
   CK_LAUNCH(ctx, "draw");
@@ -713,12 +741,11 @@ int qmcur_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, const doubl
   launch_gather_rows(X, n, n, I, r, R, st);
   CK_LAUNCH(ctx, "gather");
   ctx->mark("gather");
-  int rc;
   if (ho) {
     if ((rc = copy_out(ctx, C, m, c, ho->C, J, c, ho->J, I, r, ho->I))) return rc;
     if ((rc = copy_out(ctx, R, r, n, ho->R, nullptr, 0, nullptr, nullptr, 0, nullptr))) return rc;
   }
-  if ((rc = qmcur_core(ctx, X, m, n, c, r, J, C, U, R, core))) return rc;
+  if ((rc = qmcur_core(ctx, X, m, n, c, r, J, C, U, R, core, oz))) return rc;
   if (ho) {
     if ((rc = copy_out(ctx, U, c, r, ho->U, nullptr, 0, nullptr, nullptr, 0, nullptr))) return rc;
     if ((rc = copy_join(ctx))) return rc;
@@ -727,8 +754,31 @@ int qmcur_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, const doubl
 }
 
 // U from the gathered C, R (projection: pinv(C) X pinv(R); intersection: pinv(R[:, J]))
+void* int8_fork_prepare(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, int64_t r, int* rc) {
+  *rc = QCUR_OK;
+  if (!use_int8(ctx, m, n, r)) return nullptr;
+  void* ozws = ctx->take<uint8_t>(ozaki_workspace_bytes(m, n, r, kOzakiModuli));
+  if (!ozws) {
+    *rc = ctx->fail(QCUR_E_CUDA, "workspace exhausted (int8 gemm)");
+    return nullptr;
+  }
+  cudaError_t e = cudaEventRecord(ctx->ev_sfork, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->side_stream, ctx->ev_sfork, 0);
+  if (e == cudaSuccess && launch_ozaki_prepare(X, m, n, n, r, kOzakiModuli, ozws, ctx->side_stream)) {
+    *rc = ctx->fail(QCUR_E_CUDA, "int8 gemm: bad modulus count");
+    return nullptr;
+  }
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_sjoin, ctx->side_stream);
+  if (e != cudaSuccess) {
+    *rc = ctx->cuda_fail(e, "int8 fork");
+    return nullptr;
+  }
+  return ozws;
+}
+
 int qmcur_core(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, int64_t c, int64_t r, const int64_t* J,
-               const double* C, double* U, const double* R, int core) {
+               const double* C, double* U, const double* R, int core, void* oz_ready) {
   cudaStream_t st = ctx->stream;
   int rc;
   if (core == QCUR_CORE_INTERSECTION) {
@@ -751,6 +801,14 @@ int qmcur_core(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, int64_t c, 
     double* M = ctx->take<double>((size_t)(c * r * 4));
     double* W = ctx->take<double>((size_t)(c * r * 4));
     if (!QC || !FC || !QR || !FR || !Y || !M || !W) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (qmcur)");
+    // INT8 path: the residues of X depend on X alone, so they are computed on the side
+    // stream while the (latency-bound) factorizations run on the main stream
+    void* ozws = oz_ready;
+    if (!ozws) {
+      ozws = int8_fork_prepare(ctx, X, m, n, r, &rc);
+      if (rc) return rc;
+    }
+    const bool i8 = ozws != nullptr;
     // 3. pinv(C) = F_C Q_C^H ; pinv(R) = Q_R F_R^H  (R^H = Q_R T_R)
     FactorSpec specs[2] = {FactorSpec{C, 0, m, c, ST_CHOL_FAIL_C, -1.0, FactorOut{QC, FC}},
                            FactorSpec{R, 1, n, r, ST_CHOL_FAIL_R, -1.0, FactorOut{QR, FR}}};
@@ -762,7 +820,15 @@ int qmcur_core(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, int64_t c, 
     if (!gws) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (qmcur gemm)");
     ctx->mark("factor");
     // 4. Y = X Q_R (m x r) — the big contraction (cur.py:268)
-    if ((rc = gemm(ctx, gargs(m, r, n, X, n, 0, QR, r, 0, Y, r), gws))) return rc;
+    if (i8) {
+      cudaError_t e = cudaStreamWaitEvent(st, ctx->ev_sjoin, 0);
+      if (e != cudaSuccess) return ctx->cuda_fail(e, "int8 join");
+      if (launch_ozaki_finish(m, n, QR, r, r, Y, r, kOzakiModuli, ozws, st))
+        return ctx->fail(QCUR_E_CUDA, "int8 gemm: tensor map encode failed");
+      CK_LAUNCH(ctx, "int8 gemm");
+    } else if ((rc = gemm(ctx, gargs(m, r, n, X, n, 0, QR, r, 0, Y, r), gws))) {
+      return rc;
+    }
     ctx->mark("gemm_xq");
     // 5. M = Q_C^H Y (c x r)
     if ((rc = gemm(ctx, gargs(c, r, m, QC, c, 1, Y, r, 0, M, r), gws))) return rc;
@@ -867,7 +933,18 @@ int qcur_create(int device, qcur_ctx** out) {
     return QCUR_E_CUDA;
   }
   cudaMemset(ctx->counters, 0, (size_t)2 * 65536 * sizeof(unsigned));
-  if (cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+  if (const char* gm = std::getenv("QCUR_GEMM"))
+    ctx->gemm_mode = std::strcmp(gm, "dmma") == 0 ? 1 : std::strcmp(gm, "int8") == 0 ? 2 : 0;
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  if (const char* pe = std::getenv("QCUR_PRIO")) ctx->prio = std::strcmp(pe, "0") != 0;
+  if (cudaStreamCreateWithPriority(&ctx->hi_stream, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_hfork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_hjoin, cudaEventDisableTiming) != cudaSuccess ||
+      cudaStreamCreateWithPriority(&ctx->side_stream, cudaStreamNonBlocking, prio_lo) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_sfork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_sjoin, cudaEventDisableTiming) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
     delete ctx;
@@ -888,6 +965,14 @@ void qcur_destroy(qcur_ctx* ctx) {
   cudaFreeHost(ctx->status_host);
   cudaStreamSynchronize(ctx->copy_stream);
   cudaStreamDestroy(ctx->copy_stream);
+  cudaStreamSynchronize(ctx->side_stream);
+  cudaStreamDestroy(ctx->side_stream);
+  cudaStreamSynchronize(ctx->hi_stream);
+  cudaStreamDestroy(ctx->hi_stream);
+  cudaEventDestroy(ctx->ev_hfork);
+  cudaEventDestroy(ctx->ev_hjoin);
+  cudaEventDestroy(ctx->ev_sfork);
+  cudaEventDestroy(ctx->ev_sjoin);
   cudaEventDestroy(ctx->ev_fork);
   cudaEventDestroy(ctx->ev_join);
   delete ctx;
@@ -1241,16 +1326,36 @@ int qcur_approx(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int st
   if (rc) return rc;
   double* colp = ctx->take<double>((size_t)n);
   double* rowp = ctx->take<double>((size_t)m);
-  ctx->mark_begin();
-  if (strategy == QCUR_STRATEGY_LENGTH) {
-    if ((rc = length_distributions_impl(ctx, x_dev, m, n, colp, rowp))) return rc;
-  } else {
-    launch_fill(colp, n, 1.0 / (double)n, ctx->stream);
-    launch_fill(rowp, m, 1.0 / (double)m, ctx->stream);
-    ctx->mark("dists");
+  // the pipeline runs on the context's high-priority stream, forked from (and joined back
+  // to) the caller's stream; the residues of X start at once on the low-priority side stream
+  cudaStream_t user = ctx->stream;
+  if (ctx->prio) {
+    cudaError_t e = cudaEventRecord(ctx->ev_hfork, user);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->hi_stream, ctx->ev_hfork, 0);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "priority fork");
+    ctx->stream = ctx->hi_stream;
   }
-  if ((rc = qmcur_impl(ctx, x_dev, m, n, colp, rowp, c, r, state, J, I, C, U, R, core))) return rc;
-  return error_impl(ctx, x_dev, m, n, C, c, U, R, r, psnr_scale, err4);
+  ctx->mark_begin();
+  void* oz = nullptr;
+  if (core == QCUR_CORE_PROJECTION && m >= c && n >= r) oz = int8_fork_prepare(ctx, x_dev, m, n, r, &rc);
+  if (!rc) {
+    if (strategy == QCUR_STRATEGY_LENGTH) {
+      rc = length_distributions_impl(ctx, x_dev, m, n, colp, rowp);
+    } else {
+      launch_fill(colp, n, 1.0 / (double)n, ctx->stream);
+      launch_fill(rowp, m, 1.0 / (double)m, ctx->stream);
+      ctx->mark("dists");
+    }
+  }
+  if (!rc) rc = qmcur_impl(ctx, x_dev, m, n, colp, rowp, c, r, state, J, I, C, U, R, core, nullptr, oz);
+  if (!rc) rc = error_impl(ctx, x_dev, m, n, C, c, U, R, r, psnr_scale, err4);
+  if (ctx->prio) {
+    cudaError_t e = cudaEventRecord(ctx->ev_hjoin, ctx->hi_stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(user, ctx->ev_hjoin, 0);
+    ctx->stream = user;
+    if (!rc && e != cudaSuccess) rc = ctx->cuda_fail(e, "priority join");
+  }
+  return rc;
 }
 
 int qcur_check(qcur_ctx* ctx) { return sync_status(ctx); }
@@ -1469,6 +1574,28 @@ int qcur_qgemm_ex(qcur_ctx* ctx, int opA, int opB, int64_t M, int64_t N, int64_t
   int rc = ctx->reserve(qgemm_workspace_bytes(g) + 4096);
   if (rc) return rc;
   return gemm(ctx, g, ctx->take<double>(qgemm_workspace_bytes(g) / 8 + 16));
+}
+
+int qcur_set_gemm_mode(qcur_ctx* ctx, int mode) {
+  if (mode < 0 || mode > 2) return ctx->fail(QCUR_E_PARAMETER, "gemm mode must be 0 (auto), 1 (fp64) or 2 (int8)");
+  ctx->gemm_mode = mode;
+  return QCUR_OK;
+}
+
+int qcur_qgemm_int8(qcur_ctx* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
+                    int64_t ldb, double* C, int64_t ldc, int nmod) {
+  if (nmod == 0) nmod = kOzakiModuli;
+  if (M < 1 || N < 1 || K < 1 || !ozaki_supported(M, K, N)) return ctx->fail(QCUR_E_SHAPE, "qgemm_int8: bad shape");
+  if (nmod < 14 || nmod > 16) return ctx->fail(QCUR_E_PARAMETER, "qgemm_int8: modulus count must be 14..16");
+  const size_t wsb = ozaki_workspace_bytes(M, K, N, nmod);
+  int rc = ctx->reserve(wsb + 4096);
+  if (rc) return rc;
+  void* ws = ctx->take<uint8_t>(wsb);
+  if (!ws) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (qgemm_int8)");
+  if (launch_ozaki_gemm(A, M, K, lda, B, N, ldb, C, ldc, nmod, ws, ctx->stream))
+    return ctx->fail(QCUR_E_CUDA, "qgemm_int8: tensor map encode failed");
+  CK_LAUNCH(ctx, "qgemm_int8");
+  return QCUR_OK;
 }
 
 int qcur_chol_inv(qcur_ctx* ctx, const double* G, int64_t q, double* X) {
