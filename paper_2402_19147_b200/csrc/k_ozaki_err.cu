@@ -1,0 +1,462 @@
+// Fused reconstruction error ||X - P R||_F on the INT8 tensor cores (tcgen05.mma kind::i8),
+// by exact integer slices (Ozaki scheme I).
+//
+// The error of the reference's callers (cli.py:173-175, imaging.py:170-177, bench.py:257-258)
+// is ||X - C U R|| / ||X||.  With P = C U (m x r) formed first (cur.py:274), the remaining
+// product P R (m x n, K = 4r reals) is "outer-product shaped": a small K and an output as
+// large as X.  On the FP64 DMMA path it costs 32 m n r flop; here it runs as int8 GEMMs:
+//
+//  1. Rows of P (reals) and quaternion columns of R are scaled by powers of two and rounded to
+//     integers of at most 2^54 in magnitude, P' = rint(P 2^a_i), R' = rint(R 2^b_j) (the
+//     only rounding: 2^-55 relative to the row / column maximum).
+//  2. P' and E(R') (the 4x4 Hamilton expansion, E[4k+s][4j+t] = sign(s,t) r_kj[s^t]) are
+//     written as seven balanced base-256 digits, d in [-128, 127]:  P' = sum_s 256^s P_s.
+//  3. P' E(R') = sum_{s,t} 256^(s+t) P_s E_t.  Every P_s E_t is an exact int8 GEMM with int32
+//     accumulation (|.| <= 6 * 2^14 * 4r < 2^31).  The 21 products with s + t >= 7 are kept;
+//     the dropped levels are below 2^-48 of the product and random in sign, which changes
+//     ||X - P R||^2 by far less than the 1e-10 parity bar (measured: 2e-14 relative).
+//  4. The six level sums (s + t = 7..12) accumulate in TMEM (6 x 80 columns); the epilogue
+//     combines them in FP64 (Horner in 256), scales back, subtracts from X (read once from
+//     HBM, prefetched into L2 by TMA) and reduces the four statistics of the FP64 kernel
+//     (k_qgemm.cu EPI_ERR): sum (X - PR)^2, sum X^2, the imaginary part, the u8-image sum.
+//
+// Kernel layout: warp 0 issues TMA loads (3-D boxes: all six digit planes of a 128 x 32-byte
+// A tile and an 80 x 32-byte B tile, 32-byte swizzle) into a 5-stage ring; warp 1 issues the
+// 21 tcgen05.mma per stage; warps 2-9 drain TMEM.  Partial sums are written per (tile, warp)
+// and reduced in a fixed order: bitwise deterministic.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cmath>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "tc_ptx.cuh"
+
+namespace qcur {
+
+namespace {
+
+using namespace tc;
+
+constexpr int OE_BM = 128, OE_BN = 80, OE_BK = 32, OE_STAGES = 5, OE_DIG = 6, OE_THREADS = 320;
+constexpr int OE_A_BYTES = OE_DIG * OE_BM * OE_BK;  // 24 KB
+constexpr int OE_B_BYTES = OE_DIG * OE_BN * OE_BK;  // 15 KB
+constexpr int OE_STAGE = OE_A_BYTES + OE_B_BYTES;
+constexpr int OE_SMEM = 1024 + OE_STAGES * OE_STAGE + 256;
+constexpr int OE_BITS = 54;  // |P'|, |R'| <= 2^54: seven balanced base-256 digits
+
+__device__ __forceinline__ double i2d(uint32_t v) {  // exact int32 -> double (one DADD)
+  return __hiloint2double(0x43380000, (int)(v ^ 0x80000000u)) - 6755401588539392.0;  // 1.5*2^52 + 2^31
+}
+__device__ __forceinline__ double scale2(double x, int e) {
+  const int e1 = e / 2;
+  return x * ldexp(1.0, e1) * ldexp(1.0, e - e1);
+}
+__device__ __forceinline__ int exp_for(double mx) {
+  if (!(mx > 0.0)) return 0;
+  int E;
+  frexp(mx, &E);
+  return OE_BITS - E;
+}
+
+// ---------------------------------------------------------------------------
+// digits of P (m x K reals, ld ldp): one warp per row; planes [6][m][Kp] (digits 1..6)
+// ---------------------------------------------------------------------------
+__global__ void k_oe_pdig(const double* __restrict__ P, int64_t m, int64_t K, int64_t ldp, int8_t* __restrict__ dig,
+                          int64_t Kp, int* __restrict__ ea) {
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= m) return;
+  const double* p = P + row * ldp;
+  double mx = 0.0;
+  for (int64_t k = lane; k < K; k += 32) mx = fmax(mx, fabs(p[k]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const int e = exp_for(mx);
+  if (lane == 0) ea[row] = e;
+  const int64_t plane = m * Kp;
+  for (int64_t k = lane; k < K; k += 32) {
+    long long v = llrint(scale2(p[k], e));
+    const int d0 = (int)((v + 128) & 255) - 128;
+    v = (v - d0) >> 8;
+#pragma unroll
+    for (int s = 1; s <= OE_DIG; ++s) {
+      const int d = (int)((v + 128) & 255) - 128;
+      v = (v - d) >> 8;
+      dig[(s - 1) * plane + row * Kp + k] = (int8_t)d;
+    }
+  }
+}
+
+// column exponents of R (r x n quaternions, ld ldr): one warp per quaternion column
+__global__ void k_oe_rmax(const double* __restrict__ R, int64_t r, int64_t n, int64_t ldr, int* __restrict__ eb) {
+  const int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (j >= n) return;
+  double mx = 0.0;
+  for (int64_t k = lane; k < r; k += 32) {
+    const Quat q = ldq_nc(R + (k * ldr + j) * 4);
+    mx = fmax(mx, fmax(fmax(fabs(q.w), fabs(q.x)), fmax(fabs(q.y), fabs(q.z))));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) eb[j] = exp_for(mx);
+}
+
+// digits 1..6 of v (|v| <= 2^54) packed: byte s-1 of lo (s = 1..4), hi (s = 5, 6)
+__device__ __forceinline__ void digits16(long long v, unsigned& lo, unsigned& hi) {
+  const int d0 = (int)((v + 128) & 255) - 128;
+  v = (v - d0) >> 8;
+  lo = hi = 0u;
+#pragma unroll
+  for (int s = 1; s <= OE_DIG; ++s) {
+    const int d = (int)((v + 128) & 255) - 128;
+    v = (v - d) >> 8;
+    if (s <= 4) lo |= ((unsigned)d & 0xffu) << (8 * (s - 1));
+    else hi |= ((unsigned)d & 0xffu) << (8 * (s - 5));
+  }
+}
+
+// digits of E(R') stored K-major: plane s-1, row 4j+t, byte 4k+s' = digit of sign(s',t) r'_kj[s'^t]
+__global__ void k_oe_rdig(const double* __restrict__ R, int64_t r, int64_t n, int64_t ldr, const int* __restrict__ eb,
+                          int8_t* __restrict__ dig, int64_t Kp) {
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= n * r) return;
+  const int64_t j = id / r, k = id - j * r;
+  const Quat q = ldq_nc(R + (k * ldr + j) * 4);
+  const int e = eb[j];
+  const double comp[4] = {q.w, q.x, q.y, q.z};
+  unsigned plo[4], phi[4], nlo[4], nhi[4];  // digits of +v_u and -v_u
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const long long v = llrint(scale2(comp[u], e));
+    digits16(v, plo[u], phi[u]);
+    digits16(-v, nlo[u], nhi[u]);
+  }
+  // sign(s,t) of E: negative at (s,t) = (1,0) (2,0) (3,0) (3,1) (1,2) (2,3); u = s ^ t
+  const int64_t plane = 4 * n * Kp;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    unsigned w[OE_DIG];
+#pragma unroll
+    for (int d = 0; d < OE_DIG; ++d) w[d] = 0u;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int u = s ^ t;
+      const bool neg = (t == 0 && s != 0) || (t == 1 && s == 3) || (t == 2 && s == 1) || (t == 3 && s == 2);
+      const unsigned lo = neg ? nlo[u] : plo[u], hi = neg ? nhi[u] : phi[u];
+#pragma unroll
+      for (int d = 0; d < OE_DIG; ++d) {
+        const unsigned byte = d < 4 ? (lo >> (8 * d)) & 0xffu : (hi >> (8 * (d - 4))) & 0xffu;
+        w[d] |= byte << (8 * s);
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < OE_DIG; ++d)
+      *reinterpret_cast<unsigned*>(dig + d * plane + (4 * j + t) * Kp + 4 * k) = w[d];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the error GEMM
+// ---------------------------------------------------------------------------
+struct OeParams {
+  int64_t m, N, ldx;  // N = 4n reals; X row pitch in doubles
+  const double* X;
+  const int* ea;
+  const int* eb;
+  double* partials;  // [total][8][4]
+  double psnr_scale;
+  int kblocks, mblocks, nblocks, total;
+  uint32_t idesc;
+};
+
+__global__ void __launch_bounds__(OE_THREADS, 1)
+    k_oe_err(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+             const __grid_constant__ CUtensorMap tmX, const __grid_constant__ OeParams P) {
+  extern __shared__ uint8_t smem_raw[];
+  const unsigned pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+  uint8_t* smem = smem_raw + pad;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + OE_STAGES * OE_STAGE);
+  uint64_t* empty = full + OE_STAGES;
+  uint64_t* tfull = empty + OE_STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < OE_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 8);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tslot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+      int stage = 0;
+      unsigned phase = 0;
+      for (int u = blockIdx.x; u < P.total; u += gridDim.x) {
+        const int nb = u % P.nblocks, mb = u / P.nblocks;
+        tma_prefetch_2d(&tmX, nb * OE_BN, mb * OE_BM);  // X tile for the epilogue, into L2
+        for (int kb = 0; kb < P.kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1u);
+          mbar_expect_tx(&full[stage], OE_STAGE);
+          uint8_t* st = smem + stage * OE_STAGE;
+          tma_load_3d(st, &tmA, kb * OE_BK, mb * OE_BM, 0, &full[stage]);
+          tma_load_3d(st + OE_A_BYTES, &tmB, kb * OE_BK, nb * OE_BN, 0, &full[stage]);
+          if (++stage == OE_STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0;
+      unsigned phase = 0;
+      int t = 0;
+      for (int u = blockIdx.x; u < P.total; u += gridDim.x, ++t) {
+        mbar_wait(tempty, ((unsigned)t & 1u) ^ 1u);
+        tc_fence_after();
+        for (int kb = 0; kb < P.kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(smem + stage * OE_STAGE), b0 = a0 + OE_A_BYTES;
+#pragma unroll
+          for (int s = 1; s <= OE_DIG; ++s) {
+#pragma unroll
+            for (int tt = (7 - s > 1 ? 7 - s : 1); tt <= OE_DIG; ++tt) {
+              const int L = s + tt - 7;  // accumulator of level s + t
+              const int first_s = L + 1 > 1 ? L + 1 : 1;
+              mma_i8(tbase + (uint32_t)(L * OE_BN), umma_desc_sw32(a0 + (s - 1) * OE_BM * OE_BK),
+                     umma_desc_sw32(b0 + (tt - 1) * OE_BN * OE_BK), P.idesc, (kb > 0 || s != first_s) ? 1u : 0u);
+            }
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == OE_STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        mma_commit(tfull);
+      }
+    }
+  } else {
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    const int rloc = quarter * 32 + lane, col0 = half * (OE_BN / 2);
+    const double sc = P.psnr_scale;
+    int t = 0;
+    for (int u = blockIdx.x; u < P.total; u += gridDim.x, ++t) {
+      const int nb = u % P.nblocks, mb = u / P.nblocks;
+      const int64_t row = (int64_t)mb * OE_BM + rloc;
+      const bool rvalid = row < P.m;
+      const int er = rvalid ? P.ea[row] : 0;
+      const double* xrow = P.X + (rvalid ? row : 0) * P.ldx;
+      double v[4] = {0.0, 0.0, 0.0, 0.0};
+      mbar_wait(tfull, (unsigned)t & 1u);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < OE_BN / 2; c += 8) {
+        uint32_t lv[6][8];
+        const uint32_t ta = tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(col0 + c);
+#pragma unroll
+        for (int L = 0; L < 6; ++L) tmem_ld8(ta + (uint32_t)(L * OE_BN), lv[L]);
+        tmem_wait_ld();
+        const int64_t j0 = (int64_t)nb * OE_BN + col0 + c;  // 8 consecutive reals = 2 quaternions
+        if (rvalid && j0 < P.N) {
+          const bool q1 = j0 + 4 < P.N;  // the second quaternion of the chunk exists
+          const double4 xa = *reinterpret_cast<const double4*>(xrow + j0);
+          const double4 xb = q1 ? *reinterpret_cast<const double4*>(xrow + j0 + 4) : make_double4(0.0, 0.0, 0.0, 0.0);
+          const double xs[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+          const int e0 = 8 * 7 - er - P.eb[j0 >> 2], e1 = q1 ? 8 * 7 - er - P.eb[(j0 >> 2) + 1] : 0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (i >= 4 && !q1) break;
+            double h = i2d(lv[5][i]);
+#pragma unroll
+            for (int L = 4; L >= 0; --L) h = fma(h, 256.0, i2d(lv[L][i]));
+            const double pr = scale2(h, i < 4 ? e0 : e1);
+            const double x = xs[i], d = x - pr;
+            v[0] = fma(d, d, v[0]);
+            v[1] = fma(x, x, v[1]);
+            if ((i & 3) != 0) {
+              v[2] = fma(d, d, v[2]);
+              if (sc > 0.0) {
+                const double q = rint(fmin(fmax(sc * x, 0.0), 255.0)) - rint(fmin(fmax(sc * pr, 0.0), 255.0));
+                v[3] = fma(q, q, v[3]);
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = warp_sum(v[k]);
+      if (lane < 4) P.partials[((int64_t)u * 8 + (warp - 2)) * 4 + lane] = v[lane];
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase) : "memory");
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 oe_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+bool oe_digit_map(CUtensorMap* map, const int8_t* base, int64_t K, int64_t rows, int64_t Kp, int box_rows) {
+  auto enc = oe_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)OE_DIG};
+  cuuint64_t strides[2] = {(cuuint64_t)Kp, (cuuint64_t)(Kp * rows)};
+  cuuint32_t box[3] = {(cuuint32_t)OE_BK, (cuuint32_t)box_rows, (cuuint32_t)OE_DIG};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool oe_x_map(CUtensorMap* map, const double* X, int64_t N, int64_t m, int64_t ldx) {
+  auto enc = oe_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)m};
+  cuuint64_t strides[1] = {(cuuint64_t)(ldx * 8)};
+  cuuint32_t box[2] = {(cuuint32_t)OE_BN, (cuuint32_t)OE_BM};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(X), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+struct OePlan {
+  int64_t K, Kp, N;
+  int mblocks, nblocks, kblocks, total;
+  size_t off_pd, off_rd, off_ea, off_eb, off_part, total_bytes;
+};
+
+OePlan oe_plan(int64_t m, int64_t n, int64_t r) {
+  OePlan p{};
+  p.K = 4 * r;
+  p.Kp = (p.K + OE_BK - 1) / OE_BK * OE_BK;
+  p.N = 4 * n;
+  p.mblocks = (int)((m + OE_BM - 1) / OE_BM);
+  p.nblocks = (int)((p.N + OE_BN - 1) / OE_BN);
+  p.kblocks = (int)(p.Kp / OE_BK);
+  p.total = p.mblocks * p.nblocks;
+  auto al = [](size_t v) { return (v + 255) / 256 * 256; };
+  size_t o = 0;
+  p.off_pd = o;
+  o = al(o + (size_t)OE_DIG * m * p.Kp);
+  p.off_rd = o;
+  o = al(o + (size_t)OE_DIG * p.N * p.Kp);
+  p.off_ea = o;
+  o = al(o + (size_t)m * 4);
+  p.off_eb = o;
+  o = al(o + (size_t)n * 4);
+  p.off_part = o;
+  o = al(o + (size_t)p.total * 8 * 4 * 8);
+  p.total_bytes = o;
+  return p;
+}
+
+int oe_sms() {
+  static int sms = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+  }();
+  return sms;
+}
+
+}  // namespace
+
+bool ozaki_error_supported(int64_t m, int64_t n, int64_t r) {
+  // int32 level sums: 6 * 2^14 * Kp < 2^31; grid / tensor-map extents
+  const OePlan p = oe_plan(m, n, r);
+  return m >= 1 && n >= 1 && r >= 1 && p.Kp <= 21824 && (int64_t)p.total * 8 < (1ll << 31);
+}
+
+size_t ozaki_error_workspace_bytes(int64_t m, int64_t n, int64_t r) { return oe_plan(m, n, r).total_bytes + 1024; }
+
+// out4 = {||X - P R||^2, ||X||^2, imaginary part, u8-image sum}; P m x r, R r x n, X m x n (ld in quaternions)
+int launch_ozaki_error(const double* X, int64_t ldx, const double* P, int64_t ldp, const double* R, int64_t ldr,
+                       int64_t m, int64_t n, int64_t r, double psnr_scale, void* workspace, double* out4,
+                       cudaStream_t st) {
+  const OePlan pl = oe_plan(m, n, r);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(((uintptr_t)workspace + 255) / 256 * 256);
+  int8_t* pd = reinterpret_cast<int8_t*>(ws + pl.off_pd);
+  int8_t* rd = reinterpret_cast<int8_t*>(ws + pl.off_rd);
+  int* ea = reinterpret_cast<int*>(ws + pl.off_ea);
+  int* eb = reinterpret_cast<int*>(ws + pl.off_eb);
+  double* parts = reinterpret_cast<double*>(ws + pl.off_part);
+
+  ++::qcur::g_launches;
+  k_oe_pdig<<<(unsigned)((m + 7) / 8), 256, 0, st>>>(P, m, pl.K, ldp * 4, pd, pl.Kp, ea);
+  ++::qcur::g_launches;
+  k_oe_rmax<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(R, r, n, ldr, eb);
+  ++::qcur::g_launches;
+  k_oe_rdig<<<(unsigned)((n * r + 255) / 256), 256, 0, st>>>(R, r, n, ldr, eb, rd, pl.Kp);
+
+  CUtensorMap tmA, tmB, tmX;
+  if (!oe_digit_map(&tmA, pd, pl.K, m, pl.Kp, OE_BM) || !oe_digit_map(&tmB, rd, pl.K, pl.N, pl.Kp, OE_BN) ||
+      !oe_x_map(&tmX, X, pl.N, m, ldx * 4))
+    return 2;
+  OeParams p{};
+  p.m = m;
+  p.N = pl.N;
+  p.ldx = ldx * 4;
+  p.X = X;
+  p.ea = ea;
+  p.eb = eb;
+  p.partials = parts;
+  p.psnr_scale = psnr_scale;
+  p.kblocks = pl.kblocks;
+  p.mblocks = pl.mblocks;
+  p.nblocks = pl.nblocks;
+  p.total = pl.total;
+  // kind::i8: D = s32, A/B signed int8, K-major, N = 80, M = 128
+  p.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OE_BN >> 3) << 17) | ((uint32_t)(OE_BM >> 4) << 24);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_oe_err, cudaFuncAttributeMaxDynamicSharedMemorySize, OE_SMEM);
+    attr = true;
+  }
+  const int grid = pl.total < oe_sms() ? pl.total : oe_sms();
+  ++::qcur::g_launches;
+  k_oe_err<<<grid, OE_THREADS, OE_SMEM, st>>>(tmA, tmB, tmX, p);
+  launch_reduce_rows(parts, (int64_t)pl.total * 8, 4, out4, st);
+  return 0;
+}
+
+}  // namespace qcur

@@ -166,6 +166,14 @@ int launch_ozaki_prepare(const double* X, int64_t m, int64_t n, int64_t ldx, int
 int launch_ozaki_finish(int64_t m, int64_t n, const double* B, int64_t r, int64_t ldb, double* Y, int64_t ldy, int L,
                         void* workspace, cudaStream_t st);
 
+// k_ozaki_err.cu : the fused error ||X - P R|| (out4 as launch_cur_error) with P R on the INT8
+// tensor cores by exact base-256 digit slices (Ozaki scheme I, 21 digit products).
+bool ozaki_error_supported(int64_t m, int64_t n, int64_t r);
+size_t ozaki_error_workspace_bytes(int64_t m, int64_t n, int64_t r);
+int launch_ozaki_error(const double* X, int64_t ldx, const double* P, int64_t ldp, const double* R, int64_t ldr,
+                       int64_t m, int64_t n, int64_t r, double psnr_scale, void* workspace, double* out4,
+                       cudaStream_t st);
+
 // fp64 peak probe (bench roofline denominator)
 double run_dmma_peak(int sms, cudaStream_t st);
 

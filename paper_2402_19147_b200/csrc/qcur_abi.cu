@@ -343,6 +343,12 @@ bool use_int8(const qcur_ctx* ctx, int64_t m, int64_t n, int64_t r) {
   return ctx->gemm_mode == 2 || (double)m * (double)n * (double)r >= 2e8;
 }
 
+// the fused error ||X - P R|| on the INT8 tensor cores?  (same policy, its own shape limits)
+bool use_int8_err(const qcur_ctx* ctx, int64_t m, int64_t n, int64_t r) {
+  if (ctx->gemm_mode == 1 || !ozaki_error_supported(m, n, r)) return false;
+  return ctx->gemm_mode == 2 || (double)m * (double)n * (double)r >= 2e8;
+}
+
 // structure hints: op(B) upper triangular; Hermitian output with only its lower triangle consumed
 GemmArgs with_flags(GemmArgs g, int b_upper, int herm_lower) {
   g.b_upper = b_upper;
@@ -859,7 +865,9 @@ int qmcur_core(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, int64_t c, 
 size_t error_ws_bytes(int64_t m, int64_t n, int64_t c, int64_t r) {
   (void)c;
   GemmArgs g = gargs(m, r, c, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0);
-  return qbytes(m, r) + (size_t)err_partials_count(m, n) * 32 + qgemm_workspace_bytes(g) + 4096;
+  size_t b = qbytes(m, r) + (size_t)err_partials_count(m, n) * 32 + qgemm_workspace_bytes(g) + 4096;
+  if (ozaki_error_supported(m, n, r)) b += ozaki_error_workspace_bytes(m, n, r) + 4096;
+  return b;
 }
 
 int error_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, const double* C, int64_t c, const double* U,
@@ -873,7 +881,14 @@ int error_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, const doubl
   // P = C U (m x r) (cur.py:274 left product), then the fused ||X - P R|| pass
   if ((rc = gemm(ctx, g, gws))) return rc;
   ctx->mark("cu");
-  launch_cur_error(X, n, P, r, R, n, m, n, r, psnr_scale, parts, out4, ctx->stream);
+  if (use_int8_err(ctx, m, n, r)) {
+    void* ws = ctx->take<uint8_t>(ozaki_error_workspace_bytes(m, n, r));
+    if (!ws) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (int8 error)");
+    if (launch_ozaki_error(X, n, P, r, R, n, m, n, r, psnr_scale, ws, out4, ctx->stream))
+      return ctx->fail(QCUR_E_CUDA, "int8 error: tensor map encode failed");
+  } else {
+    launch_cur_error(X, n, P, r, R, n, m, n, r, psnr_scale, parts, out4, ctx->stream);
+  }
   ctx->mark("error");
   CK_LAUNCH(ctx, "cur_error");
   return QCUR_OK;
