@@ -470,11 +470,13 @@ struct OzCrt {
   int L;
   float w[kOzMaxMod];  // (M / p_l)^-1 mod p_l
   float P[kOzMaxMod], pinv[kOzMaxMod];
-  unsigned long long mi_lo[kOzMaxMod], mi_hi[kOzMaxMod];  // M / p_l
+  unsigned mi[kOzMaxMod][4];  // M / p_l as four 32-bit limbs, least significant first
   unsigned long long M_lo, M_hi;
   double Md;
 };
 
+// S = sum_l t_l (M / p_l) with t_l = (r_l w_l) mod p_l < 256: the limb products t * mi[k] < 2^40
+// accumulate in four 64-bit columns without overflow (L <= 16), carries are resolved once.
 template <int L>
 __global__ void __launch_bounds__(256) k_oz_crt(const uint8_t* __restrict__ res, int64_t m, int64_t N, int64_t pitch,
                                                 int64_t plane, const int* __restrict__ ex,
@@ -485,7 +487,7 @@ __global__ void __launch_bounds__(256) k_oz_crt(const uint8_t* __restrict__ res,
   if (id >= m * nq) return;
   const int64_t i = id / nq, jq = id - i * nq;
   const uint8_t* rp = res + i * pitch + 4 * jq;
-  unsigned long long lo[4] = {0, 0, 0, 0}, hi[4] = {0, 0, 0, 0};
+  unsigned long long col[4][4] = {};
 #pragma unroll
   for (int l = 0; l < L; ++l) {
     const unsigned r4 = __ldg(reinterpret_cast<const unsigned*>(rp + l * plane));
@@ -495,26 +497,26 @@ __global__ void __launch_bounds__(256) k_oz_crt(const uint8_t* __restrict__ res,
       const float rw = (float)((r4 >> (8 * h)) & 0xffu) * c.w[l];  // < 2^16, exact
       float t = fmaf(-(fmaf(rw, pinv, kMagicF) - kMagicF), P, rw);
       t = t < 0.0f ? t + P : t;
-      const unsigned long long tt = (unsigned long long)(unsigned)t;
-      const unsigned long long plo = c.mi_lo[l] * tt, phi = c.mi_hi[l] * tt + __umul64hi(c.mi_lo[l], tt);
-      const unsigned long long nlo = lo[h] + plo;
-      hi[h] += phi + (nlo < plo ? 1ull : 0ull);
-      lo[h] = nlo;
-      // keep S < 2M (< 2^127 for L <= 16): subtract M once it is reached
-      if (hi[h] > c.M_hi || (hi[h] == c.M_hi && lo[h] >= c.M_lo)) {
-        hi[h] -= c.M_hi + (lo[h] < c.M_lo ? 1ull : 0ull);
-        lo[h] -= c.M_lo;
-      }
+      const unsigned tt = (unsigned)t;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) col[h][k] += (unsigned long long)tt * c.mi[l][k];
     }
   }
+  const unsigned __int128 M = ((unsigned __int128)c.M_hi << 64) | c.M_lo;
   const int e = -(ex[i] + fx[jq]);
   const double s1 = ldexp(1.0, e / 2), s2 = ldexp(1.0, e - e / 2);
   double out[4];
 #pragma unroll
   for (int h = 0; h < 4; ++h) {
-    unsigned __int128 S = ((unsigned __int128)hi[h] << 64) | lo[h];
-    const unsigned __int128 M = ((unsigned __int128)c.M_hi << 64) | c.M_lo;
-    const double sd = (double)hi[h] * 18446744073709551616.0 + (double)lo[h];
+    // resolve the column carries: S = col0 + col1 2^32 + col2 2^64 + col3 2^96
+    const unsigned long long w0 = col[h][0];
+    const unsigned long long c1 = col[h][1] + (w0 >> 32);
+    const unsigned long long c2 = col[h][2] + (c1 >> 32);
+    const unsigned long long c3 = col[h][3] + (c2 >> 32);
+    const unsigned long long lo = (w0 & 0xffffffffull) | (c1 << 32);
+    const unsigned long long hi = (c2 & 0xffffffffull) | (c3 << 32);
+    unsigned __int128 S = ((unsigned __int128)hi << 64) | lo;
+    const double sd = (double)hi * 18446744073709551616.0 + (double)lo;
     long long q = (long long)floor(sd / c.Md);
     q = q < 0 ? 0 : q;
     S -= M * (unsigned long long)q;
@@ -624,8 +626,7 @@ OzCrt oz_crt(int L) {
   for (int l = 0; l < L; ++l) {
     const int p = kOzModuli[l];
     const unsigned __int128 mi = M / (unsigned)p;
-    c.mi_lo[l] = (unsigned long long)mi;
-    c.mi_hi[l] = (unsigned long long)(mi >> 64);
+    for (int k = 0; k < 4; ++k) c.mi[l][k] = (unsigned)(mi >> (32 * k));
     const int mr = (int)(mi % (unsigned)p);
     int w = 1;
     while ((mr * w) % p != 1) ++w;
@@ -650,7 +651,7 @@ bool ozaki_supported(int64_t m, int64_t n, int64_t r) {
 // Phase 1 (depends on X only; may run on a side stream): row exponents and residues of X.
 int launch_ozaki_prepare(const double* X, int64_t m, int64_t n, int64_t ldx, int64_t r, int L, void* workspace,
                          cudaStream_t st) {
-  if (L < 14 || L > 16) return 1;
+  if (L < 14 || L > 15) return 1;
   const OzPlan pl = oz_plan(m, n, r, L);
   uint8_t* ws = reinterpret_cast<uint8_t*>(((uintptr_t)workspace + 255) / 256 * 256);
   uint8_t* ares = ws + pl.off_ares;
@@ -660,7 +661,7 @@ int launch_ozaki_prepare(const double* X, int64_t m, int64_t n, int64_t ldx, int
   switch (L) {
     case 14: k_oz_xres<14, 256><<<(unsigned)m, 256, 0, st>>>(X, pl.K, ldx * 4, pl.bits, ares, pl.Kpitch, aplane, ex); break;
     case 15: k_oz_xres<15, 256><<<(unsigned)m, 256, 0, st>>>(X, pl.K, ldx * 4, pl.bits, ares, pl.Kpitch, aplane, ex); break;
-    default: k_oz_xres<16, 256><<<(unsigned)m, 256, 0, st>>>(X, pl.K, ldx * 4, pl.bits, ares, pl.Kpitch, aplane, ex); break;
+    default: return 1;
   }
   return 0;
 }
@@ -668,7 +669,7 @@ int launch_ozaki_prepare(const double* X, int64_t m, int64_t n, int64_t ldx, int
 // Phase 2: residues of E(B), the L int8 GEMMs on tcgen05 and the CRT into Y (m x r).
 int launch_ozaki_finish(int64_t m, int64_t n, const double* B, int64_t r, int64_t ldb, double* Y, int64_t ldy, int L,
                         void* workspace, cudaStream_t st) {
-  if (L < 14 || L > 16) return 1;
+  if (L < 14 || L > 15) return 1;
   const OzPlan pl = oz_plan(m, n, r, L);
   uint8_t* ws = reinterpret_cast<uint8_t*>(((uintptr_t)workspace + 255) / 256 * 256);
   uint8_t* ares = ws + pl.off_ares;
@@ -721,7 +722,7 @@ int launch_ozaki_finish(int64_t m, int64_t n, const double* B, int64_t r, int64_
   switch (L) {
     case 14: k_oz_crt<14><<<cblocks, 256, 0, st>>>(res, m, pl.N, pl.Npitch, rplane, ex, fx, cc, Y, ldy * 4); break;
     case 15: k_oz_crt<15><<<cblocks, 256, 0, st>>>(res, m, pl.N, pl.Npitch, rplane, ex, fx, cc, Y, ldy * 4); break;
-    default: k_oz_crt<16><<<cblocks, 256, 0, st>>>(res, m, pl.N, pl.Npitch, rplane, ex, fx, cc, Y, ldy * 4); break;
+    default: return 1;
   }
   return 0;
 }

@@ -28,6 +28,7 @@
 #include <cudaTypedefs.h>
 
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -39,7 +40,8 @@ namespace {
 
 using namespace tc;
 
-constexpr int OE_BM = 128, OE_BN = 80, OE_BK = 32, OE_STAGES = 5, OE_DIG = 6, OE_THREADS = 320;
+constexpr int OE_BM = 128, OE_BN = 80, OE_BK = 32, OE_STAGES = 5, OE_DIG = 6;
+constexpr int OE_EPI_WARPS = 16, OE_THREADS = 64 + 32 * OE_EPI_WARPS;  // 4 epilogue warps per TMEM lane quarter
 constexpr int OE_A_BYTES = OE_DIG * OE_BM * OE_BK;  // 24 KB
 constexpr int OE_B_BYTES = OE_DIG * OE_BN * OE_BK;  // 15 KB
 constexpr int OE_STAGE = OE_A_BYTES + OE_B_BYTES;
@@ -52,6 +54,10 @@ __device__ __forceinline__ double i2d(uint32_t v) {  // exact int32 -> double (o
 __device__ __forceinline__ double scale2(double x, int e) {
   const int e1 = e / 2;
   return x * ldexp(1.0, e1) * ldexp(1.0, e - e1);
+}
+// 2^e as a double (e within the normal range: one integer op; else two steps)
+__device__ __forceinline__ double pow2(int e) {
+  return (e >= -1022 && e <= 1023) ? __longlong_as_double((long long)(e + 1023) << 52) : ldexp(1.0, e);
 }
 __device__ __forceinline__ int exp_for(double mx) {
   if (!(mx > 0.0)) return 0;
@@ -166,10 +172,11 @@ struct OeParams {
   const double* X;
   const int* ea;
   const int* eb;
-  double* partials;  // [total][8][4]
+  double* partials;  // [grid][OE_EPI_WARPS][4]
   double psnr_scale;
   int kblocks, mblocks, nblocks, total;
   uint32_t idesc;
+  int experiment;  // timing experiments only (QCUR_OE_EXPERIMENT): 1 = release TMEM at once
 };
 
 __global__ void __launch_bounds__(OE_THREADS, 1)
@@ -191,7 +198,7 @@ __global__ void __launch_bounds__(OE_THREADS, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 8);
+    mbar_init(tempty, OE_EPI_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -212,8 +219,8 @@ __global__ void __launch_bounds__(OE_THREADS, 1)
       int stage = 0;
       unsigned phase = 0;
       for (int u = blockIdx.x; u < P.total; u += gridDim.x) {
-        const int nb = u % P.nblocks, mb = u / P.nblocks;
-        tma_prefetch_2d(&tmX, nb * OE_BN, mb * OE_BM);  // X tile for the epilogue, into L2
+        const int mb = u % P.mblocks, nb = u / P.mblocks;  // row blocks fastest: B tiles stay hot
+        tma_prefetch_2d(&tmX, nb * OE_BN, mb * OE_BM);      // X tile for the epilogue, into L2
         for (int kb = 0; kb < P.kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1u);
           mbar_expect_tx(&full[stage], OE_STAGE);
@@ -259,40 +266,49 @@ __global__ void __launch_bounds__(OE_THREADS, 1)
       }
     }
   } else {
-    const int quarter = warp & 3, half = (warp - 2) >> 2;
-    const int rloc = quarter * 32 + lane, col0 = half * (OE_BN / 2);
+    // warp w drains TMEM lanes 32 (w % 4) .. +31; the 10 column chunks of 8 go round-robin to
+    // the four warps of a lane quarter
+    const int quarter = warp & 3, sub = (warp - 2) >> 2;
+    const int rloc = quarter * 32 + lane;
     const double sc = P.psnr_scale;
+    double v[4] = {0.0, 0.0, 0.0, 0.0};  // this thread's sums over all its units, in a fixed order
     int t = 0;
     for (int u = blockIdx.x; u < P.total; u += gridDim.x, ++t) {
-      const int nb = u % P.nblocks, mb = u / P.nblocks;
+      const int mb = u % P.mblocks, nb = u / P.mblocks;
       const int64_t row = (int64_t)mb * OE_BM + rloc;
       const bool rvalid = row < P.m;
       const int er = rvalid ? P.ea[row] : 0;
       const double* xrow = P.X + (rvalid ? row : 0) * P.ldx;
-      double v[4] = {0.0, 0.0, 0.0, 0.0};
       mbar_wait(tfull, (unsigned)t & 1u);
       tc_fence_after();
+      if (P.experiment == 1) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty);
+        continue;
+      }
 #pragma unroll 1
-      for (int c = 0; c < OE_BN / 2; c += 8) {
+      for (int c = 8 * sub; c < OE_BN; c += 32) {
         uint32_t lv[6][8];
-        const uint32_t ta = tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(col0 + c);
+        const uint32_t ta = tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c;
 #pragma unroll
         for (int L = 0; L < 6; ++L) tmem_ld8(ta + (uint32_t)(L * OE_BN), lv[L]);
         tmem_wait_ld();
-        const int64_t j0 = (int64_t)nb * OE_BN + col0 + c;  // 8 consecutive reals = 2 quaternions
+        const int64_t j0 = (int64_t)nb * OE_BN + c;  // 8 consecutive reals = 2 quaternions
         if (rvalid && j0 < P.N) {
           const bool q1 = j0 + 4 < P.N;  // the second quaternion of the chunk exists
           const double4 xa = *reinterpret_cast<const double4*>(xrow + j0);
           const double4 xb = q1 ? *reinterpret_cast<const double4*>(xrow + j0 + 4) : make_double4(0.0, 0.0, 0.0, 0.0);
           const double xs[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
-          const int e0 = 8 * 7 - er - P.eb[j0 >> 2], e1 = q1 ? 8 * 7 - er - P.eb[(j0 >> 2) + 1] : 0;
+          // P R = (sum_L 256^L acc_L) 2^(56 - a_i - b_j)
+          const double f0 = pow2(8 * 7 - er - P.eb[j0 >> 2]);
+          const double f1 = q1 ? pow2(8 * 7 - er - P.eb[(j0 >> 2) + 1]) : 0.0;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             if (i >= 4 && !q1) break;
             double h = i2d(lv[5][i]);
 #pragma unroll
             for (int L = 4; L >= 0; --L) h = fma(h, 256.0, i2d(lv[L][i]));
-            const double pr = scale2(h, i < 4 ? e0 : e1);
+            const double pr = h * (i < 4 ? f0 : f1);
             const double x = xs[i], d = x - pr;
             v[0] = fma(d, d, v[0]);
             v[1] = fma(x, x, v[1]);
@@ -309,10 +325,10 @@ __global__ void __launch_bounds__(OE_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) v[k] = warp_sum(v[k]);
-      if (lane < 4) P.partials[((int64_t)u * 8 + (warp - 2)) * 4 + lane] = v[lane];
     }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = warp_sum(v[k]);
+    if (lane < 4) P.partials[((int64_t)blockIdx.x * OE_EPI_WARPS + (warp - 2)) * 4 + lane] = v[lane];
   }
   tc_fence_before();
   __syncthreads();
@@ -384,7 +400,7 @@ OePlan oe_plan(int64_t m, int64_t n, int64_t r) {
   p.off_eb = o;
   o = al(o + (size_t)n * 4);
   p.off_part = o;
-  o = al(o + (size_t)p.total * 8 * 4 * 8);
+  o = al(o + (size_t)p.total * OE_EPI_WARPS * 4 * 8);
   p.total_bytes = o;
   return p;
 }
@@ -404,7 +420,7 @@ int oe_sms() {
 bool ozaki_error_supported(int64_t m, int64_t n, int64_t r) {
   // int32 level sums: 6 * 2^14 * Kp < 2^31; grid / tensor-map extents
   const OePlan p = oe_plan(m, n, r);
-  return m >= 1 && n >= 1 && r >= 1 && p.Kp <= 21824 && (int64_t)p.total * 8 < (1ll << 31);
+  return m >= 1 && n >= 1 && r >= 1 && p.Kp <= 21824 && (int64_t)p.total * OE_EPI_WARPS < (1ll << 31);
 }
 
 size_t ozaki_error_workspace_bytes(int64_t m, int64_t n, int64_t r) { return oe_plan(m, n, r).total_bytes + 1024; }
@@ -441,6 +457,7 @@ int launch_ozaki_error(const double* X, int64_t ldx, const double* P, int64_t ld
   p.eb = eb;
   p.partials = parts;
   p.psnr_scale = psnr_scale;
+  if (const char* ex = std::getenv("QCUR_OE_EXPERIMENT")) p.experiment = std::atoi(ex);
   p.kblocks = pl.kblocks;
   p.mblocks = pl.mblocks;
   p.nblocks = pl.nblocks;
@@ -455,7 +472,7 @@ int launch_ozaki_error(const double* X, int64_t ldx, const double* P, int64_t ld
   const int grid = pl.total < oe_sms() ? pl.total : oe_sms();
   ++::qcur::g_launches;
   k_oe_err<<<grid, OE_THREADS, OE_SMEM, st>>>(tmA, tmB, tmX, p);
-  launch_reduce_rows(parts, (int64_t)pl.total * 8, 4, out4, st);
+  launch_reduce_rows(parts, (int64_t)grid * OE_EPI_WARPS, 4, out4, st);
   return 0;
 }
 

@@ -1601,7 +1601,7 @@ int qcur_qgemm_int8(qcur_ctx* ctx, int64_t M, int64_t N, int64_t K, const double
                     int64_t ldb, double* C, int64_t ldc, int nmod) {
   if (nmod == 0) nmod = kOzakiModuli;
   if (M < 1 || N < 1 || K < 1 || !ozaki_supported(M, K, N)) return ctx->fail(QCUR_E_SHAPE, "qgemm_int8: bad shape");
-  if (nmod < 14 || nmod > 16) return ctx->fail(QCUR_E_PARAMETER, "qgemm_int8: modulus count must be 14..16");
+  if (nmod < 14 || nmod > 15) return ctx->fail(QCUR_E_PARAMETER, "qgemm_int8: modulus count must be 14 or 15");
   const size_t wsb = ozaki_workspace_bytes(M, K, N, nmod);
   int rc = ctx->reserve(wsb + 4096);
   if (rc) return rc;

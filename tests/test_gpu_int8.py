@@ -57,7 +57,7 @@ def scaled_err(y, ref, x, b):
 
 @pytest.mark.parametrize("m,n,r", [(1, 1, 1), (5, 3, 2), (8, 8, 4), (129, 257, 52), (300, 500, 40),
                                    (257, 33, 67), (1000, 1000, 40)])
-@pytest.mark.parametrize("nmod", [14, 15, 16])
+@pytest.mark.parametrize("nmod", [14, 15])
 def test_int8_gemm_fp64_accuracy(m, n, r, nmod):
     g = np.random.default_rng(m * 7 + n * 3 + r)
     x, b = g.standard_normal((m, n, 4)), g.standard_normal((n, r, 4))
@@ -92,6 +92,8 @@ def test_int8_gemm_rejects_bad_arguments():
     x = torch.zeros((4, 4, 4), dtype=torch.float64, device="cuda")
     with pytest.raises(q.ParameterError):
         dev.call("qcur_qgemm_int8", 4, 4, 4, x.data_ptr(), 4, x.data_ptr(), 4, x.data_ptr(), 4, 3)
+    with pytest.raises(q.ParameterError):
+        dev.call("qcur_qgemm_int8", 4, 4, 4, x.data_ptr(), 4, x.data_ptr(), 4, x.data_ptr(), 4, 16)
     with pytest.raises(q.ShapeError):
         dev.call("qcur_qgemm_int8", 0, 4, 4, x.data_ptr(), 4, x.data_ptr(), 4, x.data_ptr(), 4, 0)
 
@@ -130,3 +132,57 @@ def test_qmcur_int8_engine_close_to_fp64_engine():
         dev.call("qcur_set_gemm_mode", 0)
     assert np.array_equal(f64.col_indices, f8.col_indices)
     assert O.rel_fro(tuple(f8.u.planes), tuple(f64.u.planes)) <= 1e-11
+
+
+def error_stats(x, c, u, r, mode, psnr_scale=0.0):
+    """{||X - C U R||^2, ||X||^2, imaginary part, u8-image sum} through qcur_cur_error on one engine."""
+    dev = _native.device()
+    m, n = x.shape[0], x.shape[1]
+    cq, rq = c.shape[1], r.shape[0]
+    dx, dc, du, dr = (torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (x, c, u, r))
+    out = dev.empty(4)
+    dev.call("qcur_set_gemm_mode", mode)
+    try:
+        dev.call("qcur_cur_error", dx.data_ptr(), m, n, dc.data_ptr(), cq, du.data_ptr(), dr.data_ptr(), rq,
+                 psnr_scale, out.data_ptr())
+    finally:
+        dev.call("qcur_set_gemm_mode", 0)
+    return out.cpu().numpy()
+
+
+def exact_err2(x, c, u, r):
+    p = ref_product(c, u).astype(np.float64)
+    pr = ref_product(p, r)
+    return float(((x.astype(np.longdouble) - pr) ** 2).sum())
+
+
+@pytest.mark.parametrize("m,n,cq,rq", [(37, 53, 5, 7), (129, 300, 20, 12), (300, 257, 40, 40), (700, 900, 64, 48)])
+def test_int8_error_matches_fp64_engine_and_exact(m, n, cq, rq):
+    g = np.random.default_rng(m + n + cq)
+    x = lowrank(m, n, 6, seed=m, noise=1e-3)
+    xi = np.stack(x.planes, axis=-1)
+    J = g.choice(n, cq, replace=False)
+    I = g.choice(m, rq, replace=False)
+    c, r = xi[:, J], xi[I, :]
+    u = g.standard_normal((cq, rq, 4)) * 1e-2
+    s8 = error_stats(xi, c, u, r, 2)
+    s64 = error_stats(xi, c, u, r, 1)
+    ex = exact_err2(xi, c, u, r)
+    assert abs(s8[0] - ex) <= 1e-12 * ex + 1e-300
+    assert abs(s8[0] - s64[0]) <= 1e-12 * s64[0]
+    assert abs(s8[1] - s64[1]) <= 1e-13 * s64[1]
+    assert abs(s8[2] - s64[2]) <= 1e-12 * s64[2]
+
+
+def test_int8_error_u8_image_statistic():
+    g = np.random.default_rng(3)
+    m, n, k = 96, 130, 8
+    xi = np.clip(np.stack(lowrank(m, n, k, seed=4).planes, axis=-1) * 0.1 + 0.5, 0.0, 1.0)
+    J, I = g.choice(n, 24, replace=False), g.choice(m, 20, replace=False)
+    c, r = xi[:, J], xi[I, :]
+    u = g.standard_normal((24, 20, 4)) * 1e-3
+    s8 = error_stats(xi, c, u, r, 2, psnr_scale=255.0)
+    s64 = error_stats(xi, c, u, r, 1, psnr_scale=255.0)
+    # integer sums of squared u8 differences; a rint() at an exact half-way point may differ
+    assert abs(s8[3] - s64[3]) <= 4.0 * max(1.0, 1e-9 * s64[3])
+    assert abs(s8[0] - s64[0]) <= 1e-12 * s64[0]
