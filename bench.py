@@ -516,22 +516,45 @@ def main() -> None:
     peak_tf = max(peak_live, committed_dmma_peak() or 0.0)
     peaks = load_peaks()
     hbm_peak = peaks.get("hbm_gbs")
+    int8 = "error_digits" in per_approx  # the INT8 tensor-core engine ran (qcur_set_gemm_mode / QCUR_GEMM)
     dom = max(("gemm_xq", "error"), key=lambda k: per_approx.get(k, 0.0))
     dom_ms = per_approx.get(dom, float("nan"))
     dom_flop = counts["gemm_xq_flop"] if dom == "gemm_xq" else counts["error_flop"]
-    achieved = dom_flop / (dom_ms * 1e-3) / 1e12
     traffic, traffic_src = ncu_traffic(args.config, "gemm_xq" if dom == "gemm_xq" else "error")
-    roofline = {
-        "kernel": "qgemm_kernel<EPI_ERR> (fused C U R + error)" if dom == "error" else "qgemm_kernel (Y = X Q_R)",
-        "bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-        "frac": achieved / peak_tf if peak_tf else None, "traffic": traffic, "traffic_source": traffic_src,
-        "peak_source": "FP64 DMMA (mma.sync m8n8k4 f64) peak: max of the live probe (qcur_fp64_peak_tflops) and "
-                       "the committed sustained microbenchmark (profiles/r01_fp64_peak_sustained.jsonl); "
-                       "MEASURED_PEAKS.json has no FP64 figure", "peak_live": peak_live,
-        "algorithmic_flop_per_launch": dom_flop, "avg_launch_ms": dom_ms,
-    }
+    if int8:
+        # INT8 kernels: achieved = the tcgen05 kind::i8 multiply-adds the algorithm needs (x2 ops):
+        # error = 21 digit products of P (m x 4r) by E(R) (4r x 4n); Y = X Q_R = 15 modular
+        # products of X (m x 4n) by E(Q_R) (4n x 4r).  Peak = the live dense kind::i8 probe.
+        peak_i8 = dev.lib.qcur_int8_peak_tops(dev.handle)
+        i8_ops = 2.0 * (21 if dom == "error" else 15) * m * (4 * r) * (4 * n)
+        achieved = i8_ops / (dom_ms * 1e-3) / 1e12
+        roofline = {
+            "kernel": ("k_oe_err (P R by 21 base-256 digit GEMMs on tcgen05 kind::i8, fused error epilogue)"
+                       if dom == "error" else "k_oz_gemm (Y = X Q_R by 15 modular GEMMs on tcgen05 kind::i8)"),
+            "bound": "tensor", "achieved": achieved, "peak": peak_i8, "unit": "TOP/s (int8)",
+            "frac": achieved / peak_i8 if peak_i8 else None, "traffic": traffic, "traffic_source": traffic_src,
+            "peak_source": "live dense INT8 probe (qcur_int8_peak_tops: back-to-back tcgen05.mma kind::i8 M128 N256 "
+                           "K32, one CTA per SM); MEASURED_PEAKS.json has no INT8 figure",
+            "algorithmic_int8_ops_per_launch": i8_ops, "avg_launch_ms": dom_ms,
+            "fp64_equivalent_TFps": dom_flop / (dom_ms * 1e-3) / 1e12,
+            "fp64_dmma_peak_TFps": peak_tf,
+        }
+    else:
+        achieved = dom_flop / (dom_ms * 1e-3) / 1e12
+        roofline = {
+            "kernel": "qgemm_kernel<EPI_ERR> (fused C U R + error)" if dom == "error" else "qgemm_kernel (Y = X Q_R)",
+            "bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+            "frac": achieved / peak_tf if peak_tf else None, "traffic": traffic, "traffic_source": traffic_src,
+            "peak_source": "FP64 DMMA (mma.sync m8n8k4 f64) peak: max of the live probe (qcur_fp64_peak_tflops) and "
+                           "the committed sustained microbenchmark (profiles/r01_fp64_peak_sustained.jsonl); "
+                           "MEASURED_PEAKS.json has no FP64 figure", "peak_live": peak_live,
+            "algorithmic_flop_per_launch": dom_flop, "avg_launch_ms": dom_ms,
+        }
     t_roof = max(counts["flop"] / (peak_tf * 1e12), counts["bytes"] / ((hbm_peak or 6544.3) * 1e9))
-    step_roof = {"flop": counts["flop"], "bytes": counts["bytes"], "t_roofline_ms": t_roof * 1e3,
+    step_roof = {"note": "the reference's algorithmic flops at the FP64 DMMA peak (and its bytes at HBM peak); "
+                         "the INT8 engine computes the big products exactly on the int8 tensor cores, so it can "
+                         "run below this FP64 bound (frac > 1)",
+                 "flop": counts["flop"], "bytes": counts["bytes"], "t_roofline_ms": t_roof * 1e3,
                  "frac": (t_roof * 1e3) / (ms_step / batch)}
     extra_phase = {}
     if "length" in per_approx:

@@ -176,6 +176,7 @@ int qcur_frobenius_sq(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, 
 int qcur_synth_lowrank(qcur_ctx* ctx, int64_t m, int64_t n, int64_t k, uint64_t seed, double noise,
                        int noise_relative, double* x_dev);
 double qcur_fp64_peak_tflops(qcur_ctx* ctx);
+double qcur_int8_peak_tops(qcur_ctx* ctx); /* dense tcgen05 kind::i8 rate, TOP/s (roofline of the INT8 kernels) */
 /* Rows [row0, row0+rows) of the m x n matrix P Q^H + N with noise std
  * noise * sqrt(4k) (relative to the analytic E||S||_F^2 = 16 k m n), so every
  * rank of a row-sharded run generates exactly its block of the same matrix. */

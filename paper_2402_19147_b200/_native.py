@@ -43,7 +43,7 @@ EXPORTS = (
     "qcur_upload_planar", "qcur_download_planar", "qcur_memcpy",
     "qcur_length_distributions", "qcur_uniform_distributions", "qcur_draw_indices", "qcur_qmcur",
     "qcur_cur_error", "qcur_approx", "qcur_check", "qcur_qgemm", "qcur_pseudoinverse",
-    "qcur_frobenius_sq", "qcur_synth_lowrank", "qcur_fp64_peak_tflops",
+    "qcur_frobenius_sq", "qcur_synth_lowrank", "qcur_fp64_peak_tflops", "qcur_int8_peak_tops",
     "qcur_profile", "qcur_profile_read", "qcur_launch_count", "qcur_pairwise_host", "qcur_synth_image",
     "qcur_colsums_seq", "qcur_pairwise_sums", "qcur_vec_div", "qcur_gather_cols", "qcur_gather_rows",
     "qcur_qgemm_ex", "qcur_qgemm_int8", "qcur_set_gemm_mode", "qcur_chol_inv", "qcur_series_l2inv", "qcur_kappa_check", "qcur_factor",
@@ -123,6 +123,7 @@ def load_library() -> ctypes.CDLL:
             "qcur_synth_lowrank": (ctypes.c_int, [_c_dp, _i64, _i64, _i64, ctypes.c_uint64, ctypes.c_double,
                                                   ctypes.c_int, _c_dp]),
             "qcur_fp64_peak_tflops": (ctypes.c_double, [_c_dp]),
+            "qcur_int8_peak_tops": (ctypes.c_double, [_c_dp]),
             "qcur_profile": (ctypes.c_int, [_c_dp, ctypes.c_int]),
             "qcur_profile_read": (ctypes.c_int, [_c_dp, ctypes.c_char_p, ctypes.c_size_t]),
             "qcur_launch_count": (ctypes.c_ulonglong, []),

@@ -241,28 +241,39 @@ __global__ void __launch_bounds__(NT, 2) k_oz_xres(const double* __restrict__ X,
   }
 }
 
-// column exponents of B (Kq x Nq quaternions): one warp per quaternion column
-__global__ void k_oz_bmax(const double* __restrict__ B, int64_t Kq, int64_t Nq, int64_t ldb, int bits,
-                          int* __restrict__ fx) {
-  const int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (j >= Nq) return;
+// column maxima of B (Kq x Nq quaternions): 32 columns x a slab of rows per CTA (coalesced rows,
+// 8 warps striding the slab), one atomicMax per column and CTA on the bits of the non-negative max
+__global__ void k_oz_bmax(const double* __restrict__ B, int64_t Kq, int64_t Nq, int64_t ldb, int64_t rows_per,
+                          unsigned long long* __restrict__ colmax) {
+  __shared__ double sh[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t j = (int64_t)blockIdx.x * 32 + lane;
+  const int64_t k0 = (int64_t)blockIdx.y * rows_per, k1 = k0 + rows_per < Kq ? k0 + rows_per : Kq;
   double mx = 0.0;
-  for (int64_t k = lane; k < Kq; k += 32) {
-    const Quat q = ldq_nc(B + (k * ldb + j) * 4);
-    mx = fmax(mx, fmax(fmax(fabs(q.w), fabs(q.x)), fmax(fabs(q.y), fabs(q.z))));
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if (lane == 0) {
-    int e = 0;
-    if (mx > 0.0) {
-      int E;
-      frexp(mx, &E);
-      e = bits - E;
+  if (j < Nq)
+    for (int64_t k = k0 + w; k < k1; k += 8) {
+      const Quat q = ldq_nc(B + (k * ldb + j) * 4);
+      mx = fmax(mx, fmax(fmax(fabs(q.w), fabs(q.x)), fmax(fabs(q.y), fabs(q.z))));
     }
-    fx[j] = e;
+  sh[w][lane] = mx;
+  __syncthreads();
+  if (w == 0 && j < Nq) {
+    for (int k = 1; k < 8; ++k) mx = fmax(mx, sh[k][lane]);
+    atomicMax(colmax + j, (unsigned long long)__double_as_longlong(mx));
   }
+}
+
+__global__ void k_oz_bexp(const unsigned long long* __restrict__ colmax, int64_t Nq, int bits, int* __restrict__ fx) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= Nq) return;
+  const double mx = __longlong_as_double((long long)colmax[j]);
+  int e = 0;
+  if (mx > 0.0) {
+    int E;
+    frexp(mx, &E);
+    e = bits - E;
+  }
+  fx[j] = e;
 }
 
 // residues of E(B') stored K-major: row 4j+t, byte 4k+s = sign(s,t) b'_kj[s^t] mod p
@@ -571,7 +582,7 @@ int oz_sms() {
 struct OzPlan {
   int L, bits;
   int64_t K, Kpitch, N, Npitch, BN, nblocks;
-  size_t off_ares, off_bres, off_res, off_ex, off_fx, total;
+  size_t off_ares, off_bres, off_res, off_ex, off_fx, off_cmax, total;
 };
 
 OzPlan oz_plan(int64_t m, int64_t n, int64_t r, int L) {
@@ -600,6 +611,8 @@ OzPlan oz_plan(int64_t m, int64_t n, int64_t r, int L) {
   o = al(o + (size_t)m * 4);
   p.off_fx = o;
   o = al(o + (size_t)r * 4);
+  p.off_cmax = o;
+  o = al(o + (size_t)r * 8);
   p.total = o;
   return p;
 }
@@ -637,9 +650,80 @@ OzCrt oz_crt(int L) {
   return c;
 }
 
+// INT8 tensor-core peak probe (roofline denominator): back-to-back tcgen05.mma kind::i8
+// M = 128, N = 256, K = 32 from one pair of shared-memory tiles, one CTA per SM.
+__global__ void __launch_bounds__(128, 1) k_i8_probe(int iters, int* sink) {
+  __shared__ __align__(1024) uint8_t tiles[128 * 128 + 128 * 128];  // B rows 128..255 alias A (values are immaterial)
+  __shared__ __align__(8) uint64_t done;
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < (int)sizeof(tiles) / 4; i += blockDim.x) reinterpret_cast<int*>(tiles)[i] = 0x01010101;
+  if (threadIdx.x == 0) {
+    mbar_init(&done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tslot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tb = tslot;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) | (8u << 24);
+    const uint32_t a0 = smem_u32(tiles), b0 = a0;  // N = 256 rows read from the 32 KB block
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        mma_i8(tb + (uint32_t)((it & 1) * 256), umma_desc(a0 + k * 32), umma_desc(b0 + k * 32), idesc, 1u);
+    mma_commit(&done);
+    mbar_wait(&done, 0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    uint32_t v[32];
+    if (threadIdx.x < 32) tmem_ld32(tb, v);
+    if (threadIdx.x == 0 && v[0] == 0x7fffffffu) *sink = 1;  // keep the result live
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tb) : "memory");
+  }
+}
+
 }  // namespace
 
 int ozaki_max_moduli() { return kOzMaxMod; }
+
+// dense INT8 tensor-core rate of this GPU in TOP/s (2 ops per multiply-add)
+double run_i8_peak(int sms, cudaStream_t st) {
+  int* sink = nullptr;
+  if (cudaMalloc(&sink, 64) != cudaSuccess) return 0.0;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  int iters = 2000;
+  ++::qcur::g_launches;
+  k_i8_probe<<<sms, 128, 0, st>>>(100, sink);
+  float ms = 0.f;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(e0, st);
+    ++::qcur::g_launches;
+    k_i8_probe<<<sms, 128, 0, st>>>(iters, sink);
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < 20.f) iters = (int)(iters * (40.f / (ms > 0.01f ? ms : 0.01f)));
+    else break;
+  }
+  const double ops = 2.0 * 128.0 * 256.0 * 32.0 * 4.0 * (double)iters * (double)sms;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  return ms > 0.f ? ops / ((double)ms * 1e-3) / 1e12 : 0.0;
+}
 
 size_t ozaki_workspace_bytes(int64_t m, int64_t n, int64_t r, int L) { return oz_plan(m, n, r, L).total + 1024; }
 
@@ -666,9 +750,32 @@ int launch_ozaki_prepare(const double* X, int64_t m, int64_t n, int64_t ldx, int
   return 0;
 }
 
-// Phase 2: residues of E(B), the L int8 GEMMs on tcgen05 and the CRT into Y (m x r).
-int launch_ozaki_finish(int64_t m, int64_t n, const double* B, int64_t r, int64_t ldb, double* Y, int64_t ldy, int L,
-                        void* workspace, cudaStream_t st) {
+// Phase 2a: column exponents and residues of E(B).
+int launch_ozaki_prep_b(int64_t m, int64_t n, const double* B, int64_t r, int64_t ldb, int L, void* workspace,
+                        cudaStream_t st) {
+  if (L < 14 || L > 15) return 1;
+  const OzPlan pl = oz_plan(m, n, r, L);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(((uintptr_t)workspace + 255) / 256 * 256);
+  uint8_t* bres = ws + pl.off_bres;
+  int* fx = reinterpret_cast<int*>(ws + pl.off_fx);
+  const OzMods md = oz_mods(L);
+  const int64_t bplane = pl.N * pl.Kpitch;
+  unsigned long long* cmax = reinterpret_cast<unsigned long long*>(ws + pl.off_cmax);
+  cudaMemsetAsync(cmax, 0, (size_t)r * 8, st);
+  const int64_t slabs = (n + 63) / 64 < 64 ? (n + 63) / 64 : 64, rows_per = (n + slabs - 1) / slabs;
+  ++::qcur::g_launches;
+  k_oz_bmax<<<dim3((unsigned)((r + 31) / 32), (unsigned)slabs), 256, 0, st>>>(B, n, r, ldb, rows_per, cmax);
+  ++::qcur::g_launches;
+  k_oz_bexp<<<(unsigned)((r + 255) / 256), 256, 0, st>>>(cmax, r, pl.bits, fx);
+  const int64_t nb_threads = r * (pl.Kpitch / 4);
+  ++::qcur::g_launches;
+  k_oz_bres<<<(unsigned)((nb_threads + 255) / 256), 256, 0, st>>>(B, n, r, ldb, md, fx, bres, pl.Kpitch, bplane);
+  return 0;
+}
+
+// Phase 2b: the L int8 GEMMs on tcgen05 and the CRT into Y (m x r).
+int launch_ozaki_multiply(int64_t m, int64_t n, int64_t r, double* Y, int64_t ldy, int L, void* workspace,
+                          cudaStream_t st) {
   if (L < 14 || L > 15) return 1;
   const OzPlan pl = oz_plan(m, n, r, L);
   uint8_t* ws = reinterpret_cast<uint8_t*>(((uintptr_t)workspace + 255) / 256 * 256);
@@ -677,14 +784,7 @@ int launch_ozaki_finish(int64_t m, int64_t n, const double* B, int64_t r, int64_
   uint8_t* res = ws + pl.off_res;
   int* ex = reinterpret_cast<int*>(ws + pl.off_ex);
   int* fx = reinterpret_cast<int*>(ws + pl.off_fx);
-  const OzMods md = oz_mods(L);
-  const int64_t bplane = pl.N * pl.Kpitch, rplane = m * pl.Npitch;
-
-  ++::qcur::g_launches;
-  k_oz_bmax<<<(unsigned)((r + 7) / 8), 256, 0, st>>>(B, n, r, ldb, pl.bits, fx);
-  const int64_t nb_threads = r * (pl.Kpitch / 4);
-  ++::qcur::g_launches;
-  k_oz_bres<<<(unsigned)((nb_threads + 255) / 256), 256, 0, st>>>(B, n, r, ldb, md, fx, bres, pl.Kpitch, bplane);
+  const int64_t rplane = m * pl.Npitch;
 
   CUtensorMap tmA, tmB;
   if (!oz_map(&tmA, ares, pl.K, m, pl.Kpitch, L, OZ_BM) || !oz_map(&tmB, bres, pl.K, pl.N, pl.Kpitch, L, (int)pl.BN))
@@ -725,6 +825,12 @@ int launch_ozaki_finish(int64_t m, int64_t n, const double* B, int64_t r, int64_
     default: return 1;
   }
   return 0;
+}
+
+int launch_ozaki_finish(int64_t m, int64_t n, const double* B, int64_t r, int64_t ldb, double* Y, int64_t ldy, int L,
+                        void* workspace, cudaStream_t st) {
+  int rc = launch_ozaki_prep_b(m, n, B, r, ldb, L, workspace, st);
+  return rc ? rc : launch_ozaki_multiply(m, n, r, Y, ldy, L, workspace, st);
 }
 
 // Y (m x r) = X (m x n) * B (n x r), interleaved quaternions (ld in quaternions)

@@ -425,10 +425,27 @@ bool ozaki_error_supported(int64_t m, int64_t n, int64_t r) {
 
 size_t ozaki_error_workspace_bytes(int64_t m, int64_t n, int64_t r) { return oe_plan(m, n, r).total_bytes + 1024; }
 
-// out4 = {||X - P R||^2, ||X||^2, imaginary part, u8-image sum}; P m x r, R r x n, X m x n (ld in quaternions)
-int launch_ozaki_error(const double* X, int64_t ldx, const double* P, int64_t ldp, const double* R, int64_t ldr,
-                       int64_t m, int64_t n, int64_t r, double psnr_scale, void* workspace, double* out4,
-                       cudaStream_t st) {
+// the digit planes of P and E(R) and their exponents
+int launch_ozaki_error_digits(const double* P, int64_t ldp, const double* R, int64_t ldr, int64_t m, int64_t n,
+                              int64_t r, void* workspace, cudaStream_t st) {
+  const OePlan pl = oe_plan(m, n, r);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(((uintptr_t)workspace + 255) / 256 * 256);
+  int8_t* pd = reinterpret_cast<int8_t*>(ws + pl.off_pd);
+  int8_t* rd = reinterpret_cast<int8_t*>(ws + pl.off_rd);
+  int* ea = reinterpret_cast<int*>(ws + pl.off_ea);
+  int* eb = reinterpret_cast<int*>(ws + pl.off_eb);
+  ++::qcur::g_launches;
+  k_oe_pdig<<<(unsigned)((m + 7) / 8), 256, 0, st>>>(P, m, pl.K, ldp * 4, pd, pl.Kp, ea);
+  ++::qcur::g_launches;
+  k_oe_rmax<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(R, r, n, ldr, eb);
+  ++::qcur::g_launches;
+  k_oe_rdig<<<(unsigned)((n * r + 255) / 256), 256, 0, st>>>(R, r, n, ldr, eb, rd, pl.Kp);
+  return 0;
+}
+
+// the 21 digit GEMMs with the fused error epilogue, then the fixed-order reduction into out4
+int launch_ozaki_error_gemm(const double* X, int64_t ldx, int64_t m, int64_t n, int64_t r, double psnr_scale,
+                            void* workspace, double* out4, cudaStream_t st) {
   const OePlan pl = oe_plan(m, n, r);
   uint8_t* ws = reinterpret_cast<uint8_t*>(((uintptr_t)workspace + 255) / 256 * 256);
   int8_t* pd = reinterpret_cast<int8_t*>(ws + pl.off_pd);
@@ -436,13 +453,6 @@ int launch_ozaki_error(const double* X, int64_t ldx, const double* P, int64_t ld
   int* ea = reinterpret_cast<int*>(ws + pl.off_ea);
   int* eb = reinterpret_cast<int*>(ws + pl.off_eb);
   double* parts = reinterpret_cast<double*>(ws + pl.off_part);
-
-  ++::qcur::g_launches;
-  k_oe_pdig<<<(unsigned)((m + 7) / 8), 256, 0, st>>>(P, m, pl.K, ldp * 4, pd, pl.Kp, ea);
-  ++::qcur::g_launches;
-  k_oe_rmax<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(R, r, n, ldr, eb);
-  ++::qcur::g_launches;
-  k_oe_rdig<<<(unsigned)((n * r + 255) / 256), 256, 0, st>>>(R, r, n, ldr, eb, rd, pl.Kp);
 
   CUtensorMap tmA, tmB, tmX;
   if (!oe_digit_map(&tmA, pd, pl.K, m, pl.Kp, OE_BM) || !oe_digit_map(&tmB, rd, pl.K, pl.N, pl.Kp, OE_BN) ||
@@ -474,6 +484,14 @@ int launch_ozaki_error(const double* X, int64_t ldx, const double* P, int64_t ld
   k_oe_err<<<grid, OE_THREADS, OE_SMEM, st>>>(tmA, tmB, tmX, p);
   launch_reduce_rows(parts, (int64_t)grid * OE_EPI_WARPS, 4, out4, st);
   return 0;
+}
+
+// out4 = {||X - P R||^2, ||X||^2, imaginary part, u8-image sum}; P m x r, R r x n, X m x n (ld in quaternions)
+int launch_ozaki_error(const double* X, int64_t ldx, const double* P, int64_t ldp, const double* R, int64_t ldr,
+                       int64_t m, int64_t n, int64_t r, double psnr_scale, void* workspace, double* out4,
+                       cudaStream_t st) {
+  int rc = launch_ozaki_error_digits(P, ldp, R, ldr, m, n, r, workspace, st);
+  return rc ? rc : launch_ozaki_error_gemm(X, ldx, m, n, r, psnr_scale, workspace, out4, st);
 }
 
 }  // namespace qcur

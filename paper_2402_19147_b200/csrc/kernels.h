@@ -165,6 +165,11 @@ int launch_ozaki_prepare(const double* X, int64_t m, int64_t n, int64_t ldx, int
                          cudaStream_t st);
 int launch_ozaki_finish(int64_t m, int64_t n, const double* B, int64_t r, int64_t ldb, double* Y, int64_t ldy, int L,
                         void* workspace, cudaStream_t st);
+// finish = prep_b (exponents and residues of E(B)) + multiply (the L GEMMs and the CRT)
+int launch_ozaki_prep_b(int64_t m, int64_t n, const double* B, int64_t r, int64_t ldb, int L, void* workspace,
+                        cudaStream_t st);
+int launch_ozaki_multiply(int64_t m, int64_t n, int64_t r, double* Y, int64_t ldy, int L, void* workspace,
+                          cudaStream_t st);
 
 // k_ozaki_err.cu : the fused error ||X - P R|| (out4 as launch_cur_error) with P R on the INT8
 // tensor cores by exact base-256 digit slices (Ozaki scheme I, 21 digit products).
@@ -173,7 +178,14 @@ size_t ozaki_error_workspace_bytes(int64_t m, int64_t n, int64_t r);
 int launch_ozaki_error(const double* X, int64_t ldx, const double* P, int64_t ldp, const double* R, int64_t ldr,
                        int64_t m, int64_t n, int64_t r, double psnr_scale, void* workspace, double* out4,
                        cudaStream_t st);
+// the same in two steps: digit planes, then the GEMMs with the fused epilogue
+int launch_ozaki_error_digits(const double* P, int64_t ldp, const double* R, int64_t ldr, int64_t m, int64_t n,
+                              int64_t r, void* workspace, cudaStream_t st);
+int launch_ozaki_error_gemm(const double* X, int64_t ldx, int64_t m, int64_t n, int64_t r, double psnr_scale,
+                            void* workspace, double* out4, cudaStream_t st);
 
+// INT8 tensor-core peak probe (TOP/s; bench roofline denominator of the INT8 kernels)
+double run_i8_peak(int sms, cudaStream_t st);
 // fp64 peak probe (bench roofline denominator)
 double run_dmma_peak(int sms, cudaStream_t st);
 

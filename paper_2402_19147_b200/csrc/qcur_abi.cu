@@ -829,7 +829,10 @@ int qmcur_core(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, int64_t c, 
     if (i8) {
       cudaError_t e = cudaStreamWaitEvent(st, ctx->ev_sjoin, 0);
       if (e != cudaSuccess) return ctx->cuda_fail(e, "int8 join");
-      if (launch_ozaki_finish(m, n, QR, r, r, Y, r, kOzakiModuli, ozws, st))
+      if (launch_ozaki_prep_b(m, n, QR, r, r, kOzakiModuli, ozws, st))
+        return ctx->fail(QCUR_E_CUDA, "int8 gemm: bad modulus count");
+      ctx->mark("xq_residues");  // includes the wait for the residues of X (side stream)
+      if (launch_ozaki_multiply(m, n, r, Y, r, kOzakiModuli, ozws, st))
         return ctx->fail(QCUR_E_CUDA, "int8 gemm: tensor map encode failed");
       CK_LAUNCH(ctx, "int8 gemm");
     } else if ((rc = gemm(ctx, gargs(m, r, n, X, n, 0, QR, r, 0, Y, r), gws))) {
@@ -884,7 +887,9 @@ int error_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, const doubl
   if (use_int8_err(ctx, m, n, r)) {
     void* ws = ctx->take<uint8_t>(ozaki_error_workspace_bytes(m, n, r));
     if (!ws) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (int8 error)");
-    if (launch_ozaki_error(X, n, P, r, R, n, m, n, r, psnr_scale, ws, out4, ctx->stream))
+    launch_ozaki_error_digits(P, r, R, n, m, n, r, ws, ctx->stream);
+    ctx->mark("error_digits");
+    if (launch_ozaki_error_gemm(X, n, m, n, r, psnr_scale, ws, out4, ctx->stream))
       return ctx->fail(QCUR_E_CUDA, "int8 error: tensor map encode failed");
   } else {
     launch_cur_error(X, n, P, r, R, n, m, n, r, psnr_scale, parts, out4, ctx->stream);
@@ -1523,6 +1528,7 @@ int qcur_synth_lowrank(qcur_ctx* ctx, int64_t m, int64_t n, int64_t k, uint64_t 
 }
 
 double qcur_fp64_peak_tflops(qcur_ctx* ctx) { return run_dmma_peak(ctx->sms, ctx->stream); }
+double qcur_int8_peak_tops(qcur_ctx* ctx) { return run_i8_peak(ctx->sms, ctx->stream); }
 
 int qcur_synth_lowrank_rows(qcur_ctx* ctx, int64_t m, int64_t n, int64_t k, uint64_t seed, double noise,
                             int64_t row0, int64_t rows, double* x_dev) {

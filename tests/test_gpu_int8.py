@@ -18,6 +18,12 @@ from test_gpu_parity import check_against_oracle
 
 pytestmark = pytest.mark.gpu
 
+
+def default_mode() -> int:
+    """The engine new contexts start with (QCUR_GEMM), restored after a test forces one."""
+    import os
+    return {"dmma": 1, "int8": 2}.get(os.environ.get("QCUR_GEMM", ""), 0)
+
 SIGNS = {0: (1, -1, -1, -1), 1: (1, 1, 1, -1), 2: (1, -1, 1, 1), 3: (1, 1, -1, 1)}
 
 
@@ -103,7 +109,7 @@ def int8_engine():
     dev = _native.device()
     dev.call("qcur_set_gemm_mode", 2)
     yield
-    dev.call("qcur_set_gemm_mode", 0)
+    dev.call("qcur_set_gemm_mode", default_mode())
 
 
 @pytest.mark.parametrize("m,n,k,strategy,seed,counts", [
@@ -129,7 +135,7 @@ def test_qmcur_int8_engine_close_to_fp64_engine():
         dev.call("qcur_set_gemm_mode", 2)
         f8 = q.qmcur(x, plan)
     finally:
-        dev.call("qcur_set_gemm_mode", 0)
+        dev.call("qcur_set_gemm_mode", default_mode())
     assert np.array_equal(f64.col_indices, f8.col_indices)
     assert O.rel_fro(tuple(f8.u.planes), tuple(f64.u.planes)) <= 1e-11
 
@@ -146,7 +152,7 @@ def error_stats(x, c, u, r, mode, psnr_scale=0.0):
         dev.call("qcur_cur_error", dx.data_ptr(), m, n, dc.data_ptr(), cq, du.data_ptr(), dr.data_ptr(), rq,
                  psnr_scale, out.data_ptr())
     finally:
-        dev.call("qcur_set_gemm_mode", 0)
+        dev.call("qcur_set_gemm_mode", default_mode())
     return out.cpu().numpy()
 
 

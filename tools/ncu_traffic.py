@@ -21,8 +21,13 @@ for r in rows[2:]:
     ms = float(r[ix["gpu__time_duration.sum"]]) * TSCALE[units[ix["gpu__time_duration.sum"]]]
     rd = float(r[ix["dram__bytes_read.sum"]]) * SCALE[units[ix["dram__bytes_read.sum"]]]
     wr = float(r[ix["dram__bytes_write.sum"]]) * SCALE[units[ix["dram__bytes_write.sum"]]]
-    epi = "error" if name.rstrip(")").split("(")[0].endswith("1>") else "gemm"
-    key = epi
+    base = name.split("(")[0]
+    if "k_oe_err" in base or base.rstrip(")").endswith("1>"):
+        key = "error"      # INT8 digit-slice error kernel, or the FP64 EPI_ERR GEMM
+    elif "k_oz_gemm" in base or "qgemm_kernel" in base:
+        key = "gemm"       # INT8 modular GEMM of Y = X Q_R, or the FP64 one
+    else:
+        continue
     if key not in best or ms > best[key]["ms"]:
         best[key] = {"kernel": name.split("(")[0].replace("void ", ""), "ms": ms, "dram_read_bytes": rd,
                      "dram_write_bytes": wr, "traffic_bytes": rd + wr}
