@@ -7,6 +7,8 @@ import sys
 KEYS = [
     ("gpu__time_duration.sum", "time"),
     ("sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active", "DMMA pipe % (active)"),
+    ("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", "tensor pipe % (elapsed)"),
+    ("l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "smem->TC % (elapsed)"),
     ("sm__cycles_active.avg", "sm active cyc"),
     ("sm__cycles_elapsed.avg", "elapsed cyc"),
     ("dram__bytes_read.sum", "dram rd"),
