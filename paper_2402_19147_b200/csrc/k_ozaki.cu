@@ -45,6 +45,7 @@ namespace {
 using namespace tc;
 
 constexpr int kOzMaxMod = 20;
+constexpr int kOzMaxModDefault = 15;
 // pairwise coprime, largest first
 constexpr int kOzModuli[kOzMaxMod] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227,
                                       223, 217, 211, 199, 197, 193, 191, 181, 179, 173};
@@ -321,25 +322,36 @@ constexpr int OZ_BM = 256, OZ_BK = 128, OZ_STAGES = 3, OZ_THREADS = 320;
 constexpr int OZ_A_BYTES = OZ_BM * OZ_BK, OZ_B_SLOT = 256 * OZ_BK;
 constexpr int OZ_SMEM = 1024 + OZ_STAGES * (OZ_A_BYTES + OZ_B_SLOT) + 256;
 
-struct OzGemm {
-  int64_t m, N;
-  int L, kblocks, mblocks, nblocks, BN, total;
+struct OzProb {
+  int64_t m, N;  // rows of the A operand; columns (reals) of the product
+  int kblocks, mblocks, nblocks, BN, units;
   uint32_t idesc;
   uint8_t* res;
   int64_t res_pitch, res_plane;
+};
+
+// up to two independent products in one launch (the SMs split by work units)
+struct OzGemm {
+  int L, total;
+  OzProb pr[2];
   int p[kOzMaxMod];
   double pinv[kOzMaxMod];
 };
 
-__device__ __forceinline__ void unit_coords(const OzGemm& P, int u, int& l, int& mb, int& nb) {
-  nb = u % P.nblocks;
-  const int t = u / P.nblocks;
-  mb = t % P.mblocks;
-  l = t / P.mblocks;
+__device__ __forceinline__ int unit_coords(const OzGemm& P, int u, int& l, int& mb, int& nb) {
+  const int k = u < P.pr[0].units ? 0 : 1;
+  const OzProb& q = P.pr[k];
+  u -= k ? P.pr[0].units : 0;
+  nb = u % q.nblocks;
+  const int t = u / q.nblocks;
+  mb = t % q.mblocks;
+  l = t / q.mblocks;
+  return k;
 }
 
 __global__ void __launch_bounds__(OZ_THREADS, 1)
-    k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+    k_oz_gemm(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmB0,
+              const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
               const __grid_constant__ OzGemm P) {
   extern __shared__ uint8_t smem_raw[];
   const unsigned pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
@@ -375,19 +387,22 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-      const unsigned bytes = OZ_A_BYTES + P.BN * OZ_BK;
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA0)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB0)) : "memory");
       int stage = 0;
       unsigned phase = 0;
       for (int u = blockIdx.x; u < P.total; u += gridDim.x) {
         int l, mb, nb;
-        unit_coords(P, u, l, mb, nb);
-        for (int kb = 0; kb < P.kblocks; ++kb) {
+        const int k = unit_coords(P, u, l, mb, nb);
+        const OzProb& q = P.pr[k];
+        const CUtensorMap* ta = k ? &tmA1 : &tmA0;
+        const CUtensorMap* tb = k ? &tmB1 : &tmB0;
+        const unsigned bytes = OZ_A_BYTES + q.BN * OZ_BK;
+        for (int kb = 0; kb < q.kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1u);
           mbar_expect_tx(&full[stage], bytes);
-          tma_load_3d(sA + stage * OZ_A_BYTES, &tmA, kb * OZ_BK, mb * OZ_BM, l, &full[stage]);
-          tma_load_3d(sB + stage * OZ_B_SLOT, &tmB, kb * OZ_BK, nb * P.BN, l, &full[stage]);
+          tma_load_3d(sA + stage * OZ_A_BYTES, ta, kb * OZ_BK, mb * OZ_BM, l, &full[stage]);
+          tma_load_3d(sB + stage * OZ_B_SLOT, tb, kb * OZ_BK, nb * q.BN, l, &full[stage]);
           if (++stage == OZ_STAGES) {
             stage = 0;
             phase ^= 1u;
@@ -401,17 +416,19 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       unsigned phase = 0;
       int t = 0;
       for (int u = blockIdx.x; u < P.total; u += gridDim.x, ++t) {
+        int l, mb, nb;
+        const OzProb& q = P.pr[unit_coords(P, u, l, mb, nb)];
         mbar_wait(tempty, ((unsigned)t & 1u) ^ 1u);  // the epilogue has drained the previous unit
         tc_fence_after();
-        for (int kb = 0; kb < P.kblocks; ++kb) {
+        for (int kb = 0; kb < q.kblocks; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + stage * OZ_A_BYTES), b0 = smem_u32(sB + stage * OZ_B_SLOT);
 #pragma unroll
           for (int k = 0; k < OZ_BK / 32; ++k) {
             const uint64_t bd = umma_desc(b0 + k * 32);
-            mma_i8(tbase, umma_desc(a0 + k * 32), bd, P.idesc, (kb | k) != 0);                   // rows 0..127
-            mma_i8(tbase + 256, umma_desc(a0 + 128 * OZ_BK + k * 32), bd, P.idesc, (kb | k) != 0);  // 128..255
+            mma_i8(tbase, umma_desc(a0 + k * 32), bd, q.idesc, (kb | k) != 0);                   // rows 0..127
+            mma_i8(tbase + 256, umma_desc(a0 + 128 * OZ_BK + k * 32), bd, q.idesc, (kb | k) != 0);  // 128..255
           }
           mma_commit(&empty[stage]);
           if (++stage == OZ_STAGES) {
@@ -429,14 +446,14 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     int t = 0;
     for (int u = blockIdx.x; u < P.total; u += gridDim.x, ++t) {
       int l, mb, nb;
-      unit_coords(P, u, l, mb, nb);
+      const OzProb& q = P.pr[unit_coords(P, u, l, mb, nb)];
       mbar_wait(tfull, (unsigned)t & 1u);
       tc_fence_after();
       const int64_t row = (int64_t)mb * OZ_BM + rloc;
       const int p = P.p[l];
       const double pinv = P.pinv[l];
-      uint8_t* out = P.res + l * P.res_plane + row * P.res_pitch + (int64_t)nb * P.BN;
-      for (int c0 = 0; c0 < P.BN; c0 += 32) {
+      uint8_t* out = q.res + l * q.res_plane + row * q.res_pitch + (int64_t)nb * q.BN;
+      for (int c0 = 0; c0 < q.BN; c0 += 32) {
         uint32_t v[32];
         tmem_ld32(tbase + (uint32_t)(half * 256 + c0) + ((uint32_t)(quarter * 32) << 16), v);
         uint32_t w[8];
@@ -455,9 +472,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           }
           w[i >> 2] |= (uint32_t)r << (8 * (i & 3));
         }
-        if (row < P.m) {
+        if (row < q.m) {
           *reinterpret_cast<uint4*>(out + c0) = make_uint4(w[0], w[1], w[2], w[3]);
-          if (c0 + 32 <= P.BN) *reinterpret_cast<uint4*>(out + c0 + 16) = make_uint4(w[4], w[5], w[6], w[7]);
+          if (c0 + 32 <= q.BN) *reinterpret_cast<uint4*>(out + c0 + 16) = make_uint4(w[4], w[5], w[6], w[7]);
         }
       }
       tc_fence_before();
@@ -562,6 +579,20 @@ bool oz_map(CUtensorMap* map, const uint8_t* base, int64_t K, int64_t rows, int6
   if (!enc) return false;
   cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)L};
   cuuint64_t strides[2] = {(cuuint64_t)pitch, (cuuint64_t)(pitch * rows)};
+  cuuint32_t box[3] = {(cuuint32_t)OZ_BK, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// as oz_map with an explicit row stride and plane stride (bytes)
+bool oz_map_strided(CUtensorMap* map, const uint8_t* base, int64_t K, int64_t rows, int64_t row_stride,
+                    int64_t plane_stride, int64_t L, int box_rows) {
+  auto enc = oz_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)L};
+  cuuint64_t strides[2] = {(cuuint64_t)row_stride, (cuuint64_t)plane_stride};
   cuuint32_t box[3] = {(cuuint32_t)OZ_BK, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(base), dims, strides, box, estr,
@@ -728,8 +759,11 @@ double run_i8_peak(int sms, cudaStream_t st) {
 size_t ozaki_workspace_bytes(int64_t m, int64_t n, int64_t r, int L) { return oz_plan(m, n, r, L).total + 1024; }
 
 bool ozaki_supported(int64_t m, int64_t n, int64_t r) {
-  // int32 accumulation: 4n * 2^14 < 2^31;  TMA: rows and planes < 2^31 bytes apart
-  return m >= 1 && n >= 1 && r >= 1 && 4 * n <= 131068 && (4 * n) % 4 == 0;
+  // int32 accumulation: the odd moduli have residues in [-127, 127], so 4n 127^2 < 2^31; for
+  // p = 256 the accumulator may wrap, which leaves it exact mod 2^32 and hence mod 256.
+  // Residues of X take 15 bytes per real of X (and E(B) 15 bytes per real of E(B)).
+  return m >= 1 && n >= 1 && r >= 1 && 4 * n <= 133140 &&
+         (double)oz_plan(m, n, r, kOzMaxModDefault).total <= 4e9;  // workspace cap (else the FP64 engine)
 }
 
 // Phase 1 (depends on X only; may run on a side stream): row exponents and residues of X.
@@ -773,36 +807,41 @@ int launch_ozaki_prep_b(int64_t m, int64_t n, const double* B, int64_t r, int64_
   return 0;
 }
 
-// Phase 2b: the L int8 GEMMs on tcgen05 and the CRT into Y (m x r).
-int launch_ozaki_multiply(int64_t m, int64_t n, int64_t r, double* Y, int64_t ldy, int L, void* workspace,
-                          cudaStream_t st) {
-  if (L < 14 || L > 15) return 1;
-  const OzPlan pl = oz_plan(m, n, r, L);
-  uint8_t* ws = reinterpret_cast<uint8_t*>(((uintptr_t)workspace + 255) / 256 * 256);
-  uint8_t* ares = ws + pl.off_ares;
-  uint8_t* bres = ws + pl.off_bres;
-  uint8_t* res = ws + pl.off_res;
-  int* ex = reinterpret_cast<int*>(ws + pl.off_ex);
-  int* fx = reinterpret_cast<int*>(ws + pl.off_fx);
-  const int64_t rplane = m * pl.Npitch;
+// one product of a launch: A residues (tensor map over `ares`, rows `arow_stride` bytes apart),
+// B residues, and where the residue bytes of the product go
+struct OzJob {
+  CUtensorMap ta, tb;
+  OzProb pr;
+};
 
-  CUtensorMap tmA, tmB;
-  if (!oz_map(&tmA, ares, pl.K, m, pl.Kpitch, L, OZ_BM) || !oz_map(&tmB, bres, pl.K, pl.N, pl.Kpitch, L, (int)pl.BN))
-    return 2;
+bool oz_job(OzJob& j, const OzPlan& pl, int64_t m, const uint8_t* ares, int64_t arow_stride, const uint8_t* bres,
+            int L, uint8_t* res) {
+  // A planes are m rows of arow_stride bytes (Kpitch for X, 4 Kpitch for the rows 4j of E(A))
+  if (!oz_map_strided(&j.ta, ares, pl.K, m, arow_stride, arow_stride * m, L, OZ_BM) ||
+      !oz_map(&j.tb, bres, pl.K, pl.N, pl.Kpitch, L, (int)pl.BN))
+    return false;
+  OzProb& q = j.pr;
+  q.m = m;
+  q.N = pl.N;
+  q.kblocks = (int)((pl.K + OZ_BK - 1) / OZ_BK);
+  q.mblocks = (int)((m + OZ_BM - 1) / OZ_BM);
+  q.nblocks = (int)pl.nblocks;
+  q.BN = (int)pl.BN;
+  q.units = L * q.mblocks * q.nblocks;
+  // kind::i8: D = s32 (bits 4-5 = 2), A/B signed (bits 7-9, 10-12 = 1), K-major, N>>3 at 17, M>>4 at 24 (M = 128)
+  q.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(q.BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  q.res = res;
+  q.res_pitch = pl.Npitch;
+  q.res_plane = m * pl.Npitch;
+  return true;
+}
+
+void oz_launch_gemm(const OzJob* jobs, int nj, int L, cudaStream_t st) {
   OzGemm P{};
-  P.m = m;
-  P.N = pl.N;
   P.L = L;
-  P.kblocks = (int)((pl.K + OZ_BK - 1) / OZ_BK);
-  P.mblocks = (int)((m + OZ_BM - 1) / OZ_BM);
-  P.nblocks = (int)pl.nblocks;
-  P.BN = (int)pl.BN;
-  P.total = L * P.mblocks * P.nblocks;
-  // kind::i8: D = s32 (bits 4-5 = 2), A/B signed (bits 7-9, 10-12 = 1), K-major, N>>3 at 17, M>>4 at 24
-  P.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(P.BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);  // MMA M = 128 (two per unit)
-  P.res = res;
-  P.res_pitch = pl.Npitch;
-  P.res_plane = rplane;
+  P.pr[0] = jobs[0].pr;
+  P.pr[1] = nj > 1 ? jobs[1].pr : jobs[0].pr;
+  P.total = jobs[0].pr.units + (nj > 1 ? jobs[1].pr.units : 0);
   for (int l = 0; l < L; ++l) {
     P.p[l] = kOzModuli[l];
     P.pinv[l] = 1.0 / (double)kOzModuli[l];
@@ -813,16 +852,59 @@ int launch_ozaki_multiply(int64_t m, int64_t n, int64_t r, double* Y, int64_t ld
     attr = true;
   }
   const int grid = P.total < oz_sms() ? P.total : oz_sms();
+  const OzJob& j1 = nj > 1 ? jobs[1] : jobs[0];
   ++::qcur::g_launches;
-  k_oz_gemm<<<grid, OZ_THREADS, OZ_SMEM, st>>>(tmA, tmB, P);
+  k_oz_gemm<<<grid, OZ_THREADS, OZ_SMEM, st>>>(jobs[0].ta, jobs[0].tb, j1.ta, j1.tb, P);
+}
 
+int oz_launch_crt(const uint8_t* res, int64_t m, const OzPlan& pl, const int* ex, const int* fx, double* Y,
+                  int64_t ldy, int L, cudaStream_t st) {
   const OzCrt cc = oz_crt(L);
-  const unsigned cblocks = (unsigned)((m * r + 255) / 256);
+  const unsigned cblocks = (unsigned)((m * (pl.N / 4) + 255) / 256);
+  const int64_t rplane = m * pl.Npitch;
   ++::qcur::g_launches;
   switch (L) {
     case 14: k_oz_crt<14><<<cblocks, 256, 0, st>>>(res, m, pl.N, pl.Npitch, rplane, ex, fx, cc, Y, ldy * 4); break;
     case 15: k_oz_crt<15><<<cblocks, 256, 0, st>>>(res, m, pl.N, pl.Npitch, rplane, ex, fx, cc, Y, ldy * 4); break;
     default: return 1;
+  }
+  return 0;
+}
+
+// Phase 2b: the L int8 GEMMs on tcgen05 and the CRT into Y (m x r).
+int launch_ozaki_multiply(int64_t m, int64_t n, int64_t r, double* Y, int64_t ldy, int L, void* workspace,
+                          cudaStream_t st) {
+  if (L < 14 || L > 15) return 1;
+  const OzPlan pl = oz_plan(m, n, r, L);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(((uintptr_t)workspace + 255) / 256 * 256);
+  OzJob j;
+  if (!oz_job(j, pl, m, ws + pl.off_ares, pl.Kpitch, ws + pl.off_bres, L, ws + pl.off_res)) return 2;
+  oz_launch_gemm(&j, 1, L, st);
+  return oz_launch_crt(ws + pl.off_res, m, pl, reinterpret_cast<int*>(ws + pl.off_ex),
+                       reinterpret_cast<int*>(ws + pl.off_fx), Y, ldy, L, st);
+}
+
+// Hermitian Grams G_k = A_k^H A_k (A_k: p_k x q_k, ld lda_k; G_k: q_k x q_k, ld ldg_k) for np <= 2
+// problems in one GEMM launch.  Only E(A_k) is formed: its rows 4j (t = 0) hold conj(a_kj), i.e.
+// row j of A_k^H, so they serve as the A operand (row stride 4 rows) with the same exponents.
+int launch_ozaki_gram(const double* const* A, const int64_t* p, const int64_t* q, const int64_t* lda, double* const* G,
+                      const int64_t* ldg, int np, int L, void* const* workspace, cudaStream_t st) {
+  if (L < 14 || L > 15 || np < 1 || np > 2) return 1;
+  OzJob jobs[2];
+  for (int k = 0; k < np; ++k) {
+    int rc = launch_ozaki_prep_b(q[k], p[k], A[k], q[k], lda[k], L, workspace[k], st);
+    if (rc) return rc;
+    const OzPlan pl = oz_plan(q[k], p[k], q[k], L);
+    uint8_t* ws = reinterpret_cast<uint8_t*>(((uintptr_t)workspace[k] + 255) / 256 * 256);
+    if (!oz_job(jobs[k], pl, q[k], ws + pl.off_bres, 4 * pl.Kpitch, ws + pl.off_bres, L, ws + pl.off_res)) return 2;
+  }
+  oz_launch_gemm(jobs, np, L, st);
+  for (int k = 0; k < np; ++k) {
+    const OzPlan pl = oz_plan(q[k], p[k], q[k], L);
+    uint8_t* ws = reinterpret_cast<uint8_t*>(((uintptr_t)workspace[k] + 255) / 256 * 256);
+    const int* fx = reinterpret_cast<int*>(ws + pl.off_fx);
+    int rc = oz_launch_crt(ws + pl.off_res, q[k], pl, fx, fx, G[k], ldg[k], L, st);
+    if (rc) return rc;
   }
   return 0;
 }

@@ -420,7 +420,8 @@ int oe_sms() {
 bool ozaki_error_supported(int64_t m, int64_t n, int64_t r) {
   // int32 level sums: 6 * 2^14 * Kp < 2^31; grid / tensor-map extents
   const OePlan p = oe_plan(m, n, r);
-  return m >= 1 && n >= 1 && r >= 1 && p.Kp <= 21824 && (int64_t)p.total * OE_EPI_WARPS < (1ll << 31);
+  return m >= 1 && n >= 1 && r >= 1 && p.Kp <= 21824 && (int64_t)p.total * OE_EPI_WARPS < (1ll << 31) &&
+         (double)p.total_bytes <= 8e9;  // workspace cap (else the FP64 engine)
 }
 
 size_t ozaki_error_workspace_bytes(int64_t m, int64_t n, int64_t r) { return oe_plan(m, n, r).total_bytes + 1024; }

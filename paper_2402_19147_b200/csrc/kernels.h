@@ -170,6 +170,10 @@ int launch_ozaki_prep_b(int64_t m, int64_t n, const double* B, int64_t r, int64_
                         cudaStream_t st);
 int launch_ozaki_multiply(int64_t m, int64_t n, int64_t r, double* Y, int64_t ldy, int L, void* workspace,
                           cudaStream_t st);
+// Hermitian Grams G_k = A_k^H A_k (A_k p_k x q_k) for up to two problems in one INT8 GEMM launch;
+// workspace[k] >= ozaki_workspace_bytes(q_k, p_k, q_k, L)
+int launch_ozaki_gram(const double* const* A, const int64_t* p, const int64_t* q, const int64_t* lda, double* const* G,
+                      const int64_t* ldg, int np, int L, void* const* workspace, cudaStream_t st);
 
 // k_ozaki_err.cu : the fused error ||X - P R|| (out4 as launch_cur_error) with P R on the INT8
 // tensor cores by exact base-256 digit slices (Ozaki scheme I, 21 digit products).

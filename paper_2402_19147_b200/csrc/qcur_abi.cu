@@ -309,6 +309,7 @@ size_t factor_ws_bytes(int64_t p, int64_t q) {
   b += (w1 > w2 ? w1 : w2) + 4096;
   if (q > 304)  // blocked Cholesky scratch (chol_inv_blocked): A, L, blocks, T and its GEMM slabs
     b += 2 * qbytes(q, q) + 2 * qbytes(256, 256) + qbytes(256, q) + (size_t)16 * q * q * 8 + 8192;
+  if (ozaki_supported(q, p, q)) b += ozaki_workspace_bytes(q, p, q, kOzakiModuli) + 4096;  // INT8 Grams
   return b + 16 * 256;
 }
 
@@ -341,6 +342,12 @@ GemmArgs gargs(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, in
 bool use_int8(const qcur_ctx* ctx, int64_t m, int64_t n, int64_t r) {
   if (ctx->gemm_mode == 1 || !ozaki_supported(m, n, r)) return false;
   return ctx->gemm_mode == 2 || (double)m * (double)n * (double)r >= 2e8;
+}
+
+// the Grams Z^H Z (Z: p x q) of CholeskyQR2 on the INT8 tensor cores?
+bool use_int8_gram(const qcur_ctx* ctx, int64_t p, int64_t q) {
+  if (ctx->gemm_mode == 1 || !ozaki_supported(q, p, q)) return false;
+  return ctx->gemm_mode == 2 || (double)p * (double)q * (double)q >= 5e7;
 }
 
 // the fused error ||X - P R|| on the INT8 tensor cores?  (same policy, its own shape limits)
@@ -479,6 +486,44 @@ int factor_multi(qcur_ctx* ctx, const FactorSpec* specs_in, int ns) {
   int rc;
   bool fast[2] = {false, false};
   for (int k = 0; k < ns; ++k) fast[k] = !(ctx->force_robust || specs[k].cutoff_abs >= 0.0);
+  // Grams on the INT8 tensor cores (Ozaki II, k_ozaki.cu) when every fast block qualifies
+  bool i8gram = true;
+  void* gws8[2] = {nullptr, nullptr};
+  for (int k = 0; k < ns; ++k)
+    if (fast[k] && (specs[k].zh || !use_int8_gram(ctx, specs[k].p, specs[k].q))) i8gram = false;
+  if (i8gram)
+    for (int k = 0; k < ns; ++k) {
+      if (!fast[k]) continue;
+      gws8[k] = ctx->take<uint8_t>(ozaki_workspace_bytes(specs[k].q, specs[k].p, specs[k].q, kOzakiModuli));
+      if (!gws8[k]) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (int8 gram)");
+    }
+  // G = Z^H Z for every fast block (second: Z = Q1), INT8 or FP64 (paired launches either way)
+  auto gram_each = [&](bool second) -> int {
+    if (i8gram) {
+      const double* A[2];
+      int64_t pp[2], qq[2], lda[2], ldg[2];
+      double* G[2];
+      void* w[2];
+      int np = 0;
+      for (int k = 0; k < ns; ++k) {
+        if (!fast[k]) continue;
+        A[np] = second ? specs[k].out.Q : specs[k].src;
+        pp[np] = specs[k].p;
+        qq[np] = specs[k].q;
+        lda[np] = specs[k].q;
+        ldg[np] = specs[k].q;
+        G[np] = second ? B[k].G2 : B[k].G1;
+        w[np] = gws8[k];
+        ++np;
+      }
+      if (np == 0) return QCUR_OK;
+      if (launch_ozaki_gram(A, pp, qq, lda, G, ldg, np, kOzakiModuli, w, st))
+        return ctx->fail(QCUR_E_CUDA, "int8 gram: tensor map encode failed");
+      CK_LAUNCH(ctx, "int8 gram");
+      return QCUR_OK;
+    }
+    return QCUR_E_CUDA + 100;  // caller falls back to the FP64 GEMMs
+  };
   // one GEMM per fast block: paired into one launch when both blocks are on the fast path
   auto gemm_each = [&](auto&& args_of) -> int {
     if (ns == 2 && fast[0] && fast[1]) {
@@ -537,7 +582,9 @@ int factor_multi(qcur_ctx* ctx, const FactorSpec* specs_in, int ns) {
   }
   auto zsrc = [&](int k) { return specs[k]; };
   // G1 = Z^H Z
-  if ((rc = gemm_each([&](int k) {
+  if (i8gram) {
+    if ((rc = gram_each(false))) return rc;
+  } else if ((rc = gemm_each([&](int k) {
          const FactorSpec f = zsrc(k);
          const int64_t p = f.p, q = f.q;
          return f.zh ? with_flags(gargs(q, q, p, f.src, p, 0, f.src, p, 1, B[k].G1, q), 0, 1)
@@ -553,11 +600,14 @@ int factor_multi(qcur_ctx* ctx, const FactorSpec* specs_in, int ns) {
                      : with_flags(gargs(p, q, q, f.src, q, 0, B[k].L1i, q, 1, f.out.Q, q), 1, 0);
        })))
     return rc;
-  if ((rc = gemm_each([&](int k) {
-         const int64_t p = specs[k].p, q = specs[k].q;
-         return with_flags(gargs(q, q, p, specs[k].out.Q, q, 1, specs[k].out.Q, q, 0, B[k].G2, q), 0, 1);
-       })))
+  if (i8gram) {
+    if ((rc = gram_each(true))) return rc;
+  } else if ((rc = gemm_each([&](int k) {
+               const int64_t p = specs[k].p, q = specs[k].q;
+               return with_flags(gargs(q, q, p, specs[k].out.Q, q, 1, specs[k].out.Q, q, 0, B[k].G2, q), 0, 1);
+             }))) {
     return rc;
+  }
   // second pass: G2 = I + E with E ~ kappa^2 u; L2^{-1} by a second-order series
   // (no sequential Cholesky; blocks with max|E| > 1e-5 take the robust path)
   // M0 = lh(E) in b.L2, P = M0 M0^H in b.T, M1 in b.Tcm, P2 = M1 M1 in b.Vcm
@@ -654,6 +704,7 @@ size_t qmcur_ws_bytes(int64_t m, int64_t n, int64_t c, int64_t r) {
     size_t a = qgemm_workspace_bytes(g1), d = qgemm_workspace_bytes(g2);
     b += (a > d ? a : d) + 4096;
     if (ozaki_supported(m, n, r)) b += ozaki_workspace_bytes(m, n, r, kOzakiModuli) + 4096;
+    if (ozaki_supported(c, m, r)) b += qbytes(c, m) + ozaki_workspace_bytes(c, m, r, kOzakiModuli) + 4096;  // Q_C^H Y
   } else {
     b += pinv_ws_bytes(m, c) + pinv_ws_bytes(r, n) + qbytes(c, m) + qbytes(n, r) + qbytes(m, r);
     GemmArgs g1 = gargs(m, r, n, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0);
@@ -839,8 +890,18 @@ int qmcur_core(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, int64_t c, 
       return rc;
     }
     ctx->mark("gemm_xq");
-    // 5. M = Q_C^H Y (c x r)
-    if ((rc = gemm(ctx, gargs(c, r, m, QC, c, 1, Y, r, 0, M, r), gws))) return rc;
+    // 5. M = Q_C^H Y (c x r): INT8 as (Q_C^H materialised) x Y when the engine is on
+    if (i8 && use_int8_gram(ctx, m, c) && ozaki_supported(c, m, r)) {
+      double* QCH = ctx->take<double>((size_t)(c * m * 4));
+      void* ws2 = ctx->take<uint8_t>(ozaki_workspace_bytes(c, m, r, kOzakiModuli));
+      if (!QCH || !ws2) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (int8 Q_C^H Y)");
+      launch_conj_transpose(QC, m, c, c, QCH, m, st);
+      if (launch_ozaki_gemm(QCH, c, m, m, Y, r, r, M, r, kOzakiModuli, ws2, st))
+        return ctx->fail(QCUR_E_CUDA, "int8 Q_C^H Y: tensor map encode failed");
+      CK_LAUNCH(ctx, "int8 Q_C^H Y");
+    } else if ((rc = gemm(ctx, gargs(c, r, m, QC, c, 1, Y, r, 0, M, r), gws))) {
+      return rc;
+    }
     // 6. U = F_C M F_R^H
     if ((rc = gemm(ctx, gargs(c, r, c, FC, c, 0, M, r, 0, W, r), gws))) return rc;
     if ((rc = gemm(ctx, gargs(c, r, r, W, r, 0, FR, r, 1, U, r), gws))) return rc;
