@@ -516,8 +516,9 @@ def main() -> None:
     peak_tf = max(peak_live, committed_dmma_peak() or 0.0)
     peaks = load_peaks()
     hbm_peak = peaks.get("hbm_gbs")
-    int8 = "error_digits" in per_approx  # the INT8 tensor-core engine ran (qcur_set_gemm_mode / QCUR_GEMM)
     dom = max(("gemm_xq", "error"), key=lambda k: per_approx.get(k, 0.0))
+    # did the dominant product run on the INT8 tensor-core engine? (its extra phase marks say so)
+    int8 = ("error_digits" if dom == "error" else "xq_residues") in per_approx
     dom_ms = per_approx.get(dom, float("nan"))
     dom_flop = counts["gemm_xq_flop"] if dom == "gemm_xq" else counts["error_flop"]
     traffic, traffic_src = ncu_traffic(args.config, "gemm_xq" if dom == "gemm_xq" else "error")
@@ -603,7 +604,9 @@ def main() -> None:
     }
     # the same work through the throughput API (approx_stream): matrix k+1's H2D overlaps
     # matrix k's approximation; every step still uploads its 512 MB and reads back its result
-    if batch == 1:
+    # (two device slots of X: skipped when they would not leave room for the pipeline, e.g. cfg5)
+    total_mem = torch.cuda.get_device_properties(local).total_memory
+    if batch == 1 and 2 * 32 * m * n <= 0.25 * total_mem:
         from paper_2402_19147_b200 import approx_stream
 
         nst = max(e2e_steps, 6)
@@ -626,8 +629,8 @@ def main() -> None:
         e2e = {
             "value": world * nst / st_s, "unit": "approx/s", "steps": nst,
             "h2d_bytes_per_step": 32 * m * n, "d2h_bytes_per_step": 32 * c * r + 8 * (c + r) + 36,
-            "api": "approx_stream over pinned host matrices: each step uploads its 512 MB input (H2D of the next "
-                   "overlapped with the current approximation) and reads back its indices, U and error",
+            "api": f"approx_stream over pinned host matrices: each step uploads its {32 * m * n / 1e6:.0f} MB input "
+                   "(H2D of the next overlapped with the current approximation) and reads back its indices, U and error",
             "rel_err": res_s[-1].rel_err,
             "single_call": single,
         }
