@@ -207,6 +207,12 @@ int qcur_gather_rows(qcur_ctx* ctx, const double* x_dev, int64_t n, const int64_
 int qcur_qgemm_ex(qcur_ctx* ctx, int opA, int opB, int64_t M, int64_t N, int64_t K, double alpha, const double* a_dev,
                   int64_t lda, const double* b_dev, int64_t ldb, double beta, double* c_dev, int64_t ldc, int flags);
 /* X = L^{-1} for G = L L^H (cluster kernel, or blocked for q > 304) */
+/* Quaternion SVD core (qsvd, linalg.py:226-310; numerical_rank :370-378): one-sided Jacobi on
+   A (m x n, m >= n, row pitch lda, interleaved).  acm_dev (m x n column-major) receives A V, whose
+   column norms are the singular values (sigma_dev, unsorted); vcm_dev (n x n column-major,
+   nullable) receives V.  sweeps_out (nullable): Jacobi sweeps used. */
+int qcur_qsvd_jacobi(qcur_ctx* ctx, const double* a_dev, int64_t m, int64_t n, int64_t lda, double* acm_dev,
+                     double* vcm_dev, double* sigma_dev, int* sweeps_out);
 /* Engine of the X Q_R contraction inside qmcur: 0 auto (INT8 when large), 1 FP64 DMMA, 2 INT8 (Ozaki II).
    The environment variable QCUR_GEMM=dmma|int8 sets the initial mode of new contexts. */
 int qcur_set_gemm_mode(qcur_ctx* ctx, int mode);

@@ -19,6 +19,12 @@ It restates, in numpy, the algorithm of the reference package ``qcur``
   qmcur                  cur.py:257-269   U = pinv(C) @ X @ pinv(R)
   quaternion matmul      quat.py:274-296  (here via the Cayley-Dickson complex pair)
   relative error         cli.py:173-175 / imaging.py:170-177
+  singular values        linalg.py:226-310 (qsvd's sigma: chi's values, one per pair)
+  numerical_rank         linalg.py:370-378 (the pinv cutoff)
+  spectral_norm          linalg.py:365-367 (chi's largest singular value)
+  perturbation_bounds    cur.py:306-388   (every quantity is basis-invariant, so W_k, V_k
+                         are represented by chi's top-2k singular subspaces: chi(W_k[I,:])
+                         spans the same column space as rows I, m+I of that subspace)
 
 Pinned against the live reference (tests/golden/, made by
 tests/golden/make_golden.py from /root/reference in the build container).
@@ -300,3 +306,68 @@ def complete(y, observed, rank: int, strategy: str = "length", max_iters: int = 
             converged = True
             break
     return current, history, converged
+
+
+# ---------------------------------------------------------------------------
+# QSVD quantities and the perturbation bounds (linalg.py:226-383, cur.py:306-388)
+# ---------------------------------------------------------------------------
+def singular_values(planes) -> np.ndarray:
+    """qsvd(a).sigma: chi's singular values, one per pair, nonincreasing (linalg.py:253-255)."""
+    return np.linalg.svd(adjoint(planes), compute_uv=False)[0::2]
+
+
+def _rank_from_sigma(sigma, shape, tol=None) -> int:
+    smax = float(sigma[0]) if sigma.size else 0.0
+    if smax == 0.0:
+        return 0
+    cutoff = EPS * max(shape) * smax if tol is None else float(tol)
+    return int(np.sum(sigma > cutoff))
+
+
+def numerical_rank(planes, tol=None) -> int:
+    return _rank_from_sigma(singular_values(planes), planes[0].shape, tol)
+
+
+def spectral_norm(planes) -> float:
+    return float(np.linalg.svd(adjoint(planes), compute_uv=False)[0])
+
+
+def _pinv_norm(sigma, shape, norm: str) -> float:
+    """||pinv(A)|| from A's singular values (pinv's cutoff, linalg.py:352-362)."""
+    smax = float(sigma[0]) if sigma.size else 0.0
+    if smax == 0.0:
+        return 0.0
+    kept = sigma[sigma > EPS * max(shape) * smax]
+    return float(1.0 / kept[-1]) if norm == "spectral" else float(np.sqrt(np.sum(1.0 / kept ** 2)))
+
+
+def perturbation_bounds(x, e, rows, cols, k: int, norm: str = "spectral") -> dict:
+    """The eight fields of cur.py:289-303 for clean X (rank k), noise E and index sets I, J."""
+    m, n = x[0].shape
+    rows, cols = np.asarray(rows), np.asarray(cols)
+    if numerical_rank(x) != k:
+        raise OracleError("parameter", "x does not have numerical rank k")
+    nfun = spectral_norm if norm == "spectral" else (lambda p: math.sqrt(frob2(p)))
+    u, s, vh = np.linalg.svd(adjoint(x), full_matrices=False)
+    u2, v2 = u[:, :2 * k], vh.conj().T[:, :2 * k]
+    w_sub = u2[np.concatenate([rows, m + rows]), :]   # column space of chi(W_k[I, :])
+    v_sub = v2[np.concatenate([cols, n + cols]), :]
+    sw = np.linalg.svd(w_sub, compute_uv=False)[0::2]
+    sv = np.linalg.svd(v_sub, compute_uv=False)[0::2]
+    if _rank_from_sigma(sw, (rows.size, k)) < k or _rank_from_sigma(sv, (cols.size, k)) < k:
+        raise OracleError("sampling", "sampled rows of the singular factors lost rank")
+    xt = tuple(a + b for a, b in zip(x, e))
+    recon = stabilized_reconstruct(xt, rows, cols)
+    lhs = nfun(tuple(a - b for a, b in zip(x, recon)))
+    c = tuple(np.ascontiguousarray(p[:, cols]) for p in x)
+    r = tuple(np.ascontiguousarray(p[rows, :]) for p in x)
+    noise = nfun(e)
+    xrp = nfun(qmatmul(x, pinv(r)))
+    cx = nfun(qmatmul(pinv(c), x))
+    e_rows = tuple(np.ascontiguousarray(p[rows, :]) for p in e)
+    e_cols = tuple(np.ascontiguousarray(p[:, cols]) for p in e)
+    bound_a = nfun(e_rows) * xrp + nfun(e_cols) * cx + 3.0 * noise
+    wp = _pinv_norm(sw, (rows.size, k), norm)
+    vp = _pinv_norm(sv, (cols.size, k), norm)
+    return dict(lhs=lhs, bound_a=bound_a, bound_b=noise * (wp + vp + 3.0), noise_norm=noise, xrp_norm=xrp,
+                cx_norm=cx, wsub_pinv_norm=wp, vsub_pinv_norm=vp)

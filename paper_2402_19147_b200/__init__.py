@@ -33,8 +33,10 @@ from .cur import (
     qmcur_device,
     stabilized_reconstruct,
     uniform_distributions,
+    PerturbationBounds,
+    perturbation_bounds,
 )
-from .linalg import pseudoinverse, spectral_norm
+from .linalg import QSVDResult, lowrank_truncate, numerical_rank, pseudoinverse, qsvd, save_qsvd, spectral_norm
 from .stream import StreamResult, approx_stream
 from .completion import (
     INDEX_POLICIES,
@@ -57,5 +59,7 @@ __all__ = [
     "INDEX_POLICIES", "ObservationMask", "CompletionConfig", "CompletionResult", "random_mask", "project_observed",
     "complete", "derive_seed", "read_qmat", "write_qmat", "spectral_norm",
     "StreamResult", "approx_stream",
+    "QSVDResult", "qsvd", "numerical_rank", "lowrank_truncate", "save_qsvd", "PerturbationBounds",
+    "perturbation_bounds",
 ]
 __version__ = "0.1.0"

@@ -141,6 +141,12 @@ void launch_colmajor_to_rowmajor(const double* Zcm, int64_t p, int64_t q, double
 void launch_rowmajor_to_colmajor(const double* Z, int64_t p, int64_t q, int64_t ldz, double* Zcm,
                                  const unsigned* status, unsigned gate_bit, cudaStream_t st);
 
+// k_qsvd.cu : quaternion one-sided Jacobi SVD (column-major A m x n with m >= n, V n x n)
+void launch_to_colmajor(const double* A, int64_t m, int64_t n, int64_t lda, double* Acm, cudaStream_t st);
+void launch_identity_cm(double* Vcm, int64_t n, cudaStream_t st);
+void launch_jacobi_round(double* Acm, int64_t m, int64_t n, double* Vcm, int64_t rnd, unsigned* flag, cudaStream_t st);
+void launch_col_norms(const double* Acm, int64_t m, int64_t n, double* sigma, cudaStream_t st);
+
 // k_synth.cu : synthetic workloads (Philox normal generator)
 // offset: element offset (even) of this block within the whole generated array
 void launch_normal_fill(double* out, int64_t count, uint64_t seed, uint64_t stream, double scale, cudaStream_t st,

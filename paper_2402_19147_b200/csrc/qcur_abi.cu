@@ -1658,6 +1658,38 @@ int qcur_qgemm_ex(qcur_ctx* ctx, int opA, int opB, int64_t M, int64_t N, int64_t
   return gemm(ctx, g, ctx->take<double>(qgemm_workspace_bytes(g) / 8 + 16));
 }
 
+// Quaternion SVD by one-sided Jacobi (qsvd, linalg.py:226-310): A (m x n, m >= n, row pitch lda)
+// is copied column-major into acm and rotated until its columns are orthogonal; then
+// A V = acm (columns a_j with ||a_j|| = sigma_j), V (n x n column-major, nullable) orthonormal.
+int qcur_qsvd_jacobi(qcur_ctx* ctx, const double* a, int64_t m, int64_t n, int64_t lda, double* acm, double* vcm,
+                     double* sigma, int* sweeps_out) {
+  if (m < 1 || n < 1 || m < n) return ctx->fail(QCUR_E_SHAPE, "qsvd_jacobi: need m >= n >= 1");
+  int rc = ctx->reserve(4096);
+  if (rc) return rc;
+  unsigned* flag = ctx->take<unsigned>(16);
+  if (!flag) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (qsvd)");
+  cudaStream_t st = ctx->stream;
+  launch_to_colmajor(a, m, n, lda, acm, st);
+  if (vcm) launch_identity_cm(vcm, n, st);
+  CK_LAUNCH(ctx, "qsvd setup");
+  const int64_t nn = n + (n & 1);
+  int sweep = 0;
+  for (; sweep < 60 && n > 1; ++sweep) {
+    cudaMemsetAsync(flag, 0, sizeof(unsigned), st);
+    for (int64_t rnd = 0; rnd < nn - 1; ++rnd) launch_jacobi_round(acm, m, n, vcm, rnd, flag, st);
+    CK_LAUNCH(ctx, "jacobi round");
+    unsigned h = 0;
+    cudaError_t e = cudaMemcpyAsync(&h, flag, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "qsvd sweep");
+    if (!h) break;
+  }
+  launch_col_norms(acm, m, n, sigma, st);
+  CK_LAUNCH(ctx, "qsvd norms");
+  if (sweeps_out) *sweeps_out = sweep + 1;
+  return QCUR_OK;
+}
+
 int qcur_set_gemm_mode(qcur_ctx* ctx, int mode) {
   if (mode < 0 || mode > 2) return ctx->fail(QCUR_E_PARAMETER, "gemm mode must be 0 (auto), 1 (fp64) or 2 (int8)");
   ctx->gemm_mode = mode;

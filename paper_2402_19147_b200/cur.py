@@ -46,6 +46,9 @@ __all__ = [
     "cur_relative_error",
     "cur_psnr",
     "qmcur_device",
+    "stabilized_reconstruct",
+    "PerturbationBounds",
+    "perturbation_bounds",
 ]
 
 STRATEGIES = ("length", "uniform")
@@ -329,6 +332,65 @@ def stabilized_reconstruct(x, row_indices, col_indices) -> QMatrix:
              R.data_ptr())
     return cur_reconstruct(CURFactors(row_indices=rows, col_indices=cols, c=from_device(C, dev),
                                       u=from_device(U, dev), r=from_device(R, dev)))
+
+
+@dataclass(frozen=True)
+class PerturbationBounds:
+    """Observed projection error and its two computable upper bounds (cur.py:289-303)."""
+
+    lhs: float
+    bound_a: float
+    bound_b: float
+    noise_norm: float
+    xrp_norm: float
+    cx_norm: float
+    wsub_pinv_norm: float
+    vsub_pinv_norm: float
+
+
+def perturbation_bounds(x, e, row_indices, col_indices, k: int, norm: str = "spectral") -> PerturbationBounds:
+    """Projection-error bounds for a clean rank-k X, noise E and index sets I, J (cur.py:306-388).
+
+    Every matrix operation runs on the device: the QSVD of X and the numerical ranks (quaternion
+    one-sided Jacobi), the stabilized reconstruction of X + E, the pseudoinverses, the products
+    and the spectral norms (Lanczos) or Frobenius norms."""
+    from .errors import DegenerateSamplingError
+    from .linalg import numerical_rank, pseudoinverse, qsvd, spectral_norm
+    from .quat import qmat_frobenius_norm
+
+    if norm not in ("spectral", "frobenius"):
+        raise ParameterError(f"norm must be 'spectral' or 'frobenius', got {norm!r}")
+    if tuple(x.shape) != tuple(e.shape):
+        raise ShapeError(f"noise shape {tuple(e.shape)} does not match matrix shape {tuple(x.shape)}")
+    rows = np.asarray(row_indices, dtype=np.intp)
+    cols = np.asarray(col_indices, dtype=np.intp)
+    if rows.size < k or cols.size < k:
+        raise ParameterError("index sets must contain at least k entries")
+    rank_x = numerical_rank(x)
+    if rank_x != k:
+        raise ParameterError(f"x has numerical rank {rank_x}, expected exactly {k}")
+    nfun = spectral_norm if norm == "spectral" else qmat_frobenius_norm
+
+    res = qsvd(x, k)
+    w_sub = res.w.take_rows(rows)
+    v_sub = res.v.take_rows(cols)
+    if numerical_rank(w_sub) < k or numerical_rank(v_sub) < k:
+        raise DegenerateSamplingError("sampled rows of the singular factors lost rank; bounds are void")
+
+    xt = x + e
+    lhs = nfun(x - stabilized_reconstruct(xt, rows, cols))
+    c = x.take_cols(cols)
+    r = x.take_rows(rows)
+    noise = nfun(e)
+    xrp = nfun(x @ pseudoinverse(r))
+    cx = nfun(pseudoinverse(c) @ x)
+    bound_a = nfun(e.take_rows(rows)) * xrp + nfun(e.take_cols(cols)) * cx + 3.0 * noise
+    wsub_pinv = nfun(pseudoinverse(w_sub))
+    vsub_pinv = nfun(pseudoinverse(v_sub))
+    bound_b = noise * (wsub_pinv + vsub_pinv + 3.0)
+    return PerturbationBounds(lhs=float(lhs), bound_a=float(bound_a), bound_b=float(bound_b),
+                              noise_norm=float(noise), xrp_norm=float(xrp), cx_norm=float(cx),
+                              wsub_pinv_norm=float(wsub_pinv), vsub_pinv_norm=float(vsub_pinv))
 
 
 def cur_relative_error(x, factors: CURFactors) -> float:

@@ -1,5 +1,12 @@
-"""Pseudoinverse on the GPU — mirror of ``qcur.linalg.pseudoinverse``
-(pkg/src/qcur/linalg.py:346-362) for the QMCUR path.
+"""Pseudoinverse, QSVD, numerical rank and spectral norm on the GPU — mirrors of
+``qcur.linalg`` (pkg/src/qcur/linalg.py).
+
+  pseudoinverse     linalg.py:346-362   -> qcur_pseudoinverse (CholeskyQR2 / Householder + Jacobi)
+  qsvd              linalg.py:226-310   -> qcur_qsvd_jacobi (quaternion one-sided Jacobi)
+  numerical_rank    linalg.py:370-378   -> the same singular values, the pinv cutoff
+  lowrank_truncate  linalg.py:381-383   -> W_k diag(sigma_k) V_k^H (GPU quaternion GEMMs)
+  spectral_norm     linalg.py:365-367   -> Lanczos on the device (qcur_qgemv)
+  save_qsvd         linalg.py:406-420   (host file output)
 
 pinv(A) = V diag(1/sigma_i, sigma_i > cutoff) W^H with the default cutoff
 eps * max(m, n) * sigma_max (linalg.py:338-339).  Device method: CholeskyQR2
@@ -13,11 +20,16 @@ import ctypes
 
 import numpy as np
 
+from dataclasses import dataclass
+
 from . import _native
-from .errors import ParameterError
+from .errors import ParameterError, ShapeError
 from .quat import QMatrix, from_device, to_device
 
-__all__ = ["pseudoinverse", "spectral_norm"]
+__all__ = ["QSVDResult", "qsvd", "pseudoinverse", "spectral_norm", "numerical_rank", "lowrank_truncate",
+           "save_qsvd"]
+
+_EPS = float(np.finfo(np.float64).eps)
 
 
 def pseudoinverse(a, tol: float | None = None) -> QMatrix:
@@ -117,3 +129,168 @@ def spectral_norm(a, max_iter: int = 300, tol: float = 1e-15) -> float:
         basis.append(v)
         w = apply(v)
     return float(np.sqrt(max(lam, 0.0)))
+
+
+# ---------------------------------------------------------------------------
+# QSVD (linalg.py:226-310) by quaternion one-sided Jacobi on the device
+# ---------------------------------------------------------------------------
+@dataclass(frozen=True)
+class QSVDResult:
+    """Economy quaternion SVD factors A ~ W diag(sigma) V^H (linalg.py:191-214)."""
+
+    w: QMatrix
+    sigma: np.ndarray
+    v: QMatrix
+
+    def __post_init__(self) -> None:
+        sig = np.array(self.sigma, dtype=np.float64, copy=True)
+        sig.setflags(write=False)
+        object.__setattr__(self, "sigma", sig)
+        if sig.ndim != 1:
+            raise ShapeError("sigma must be 1-D")
+        if self.w.cols != sig.size or self.v.cols != sig.size:
+            raise ShapeError("factor widths disagree with sigma length")
+
+    @property
+    def rank_used(self) -> int:
+        return int(self.sigma.size)
+
+    def reconstruct(self) -> QMatrix:
+        return self.w.scale_columns(self.sigma) @ self.v.conj_transpose()
+
+
+def _jacobi(a, want_v: bool):
+    """One-sided Jacobi on the device for a (m x n, m >= n): returns (AV columns (n, m, 4),
+    V columns (n, n, 4) or None, sigma (n,)) as host arrays, columns unsorted."""
+    dev = _native.device()
+    m, n = (int(v) for v in a.shape)
+    ad = to_device(a, dev)
+    acm = dev.empty(n, m, 4)
+    vcm = dev.empty(n, n, 4) if want_v else None
+    sig = dev.empty(n)
+    sweeps = ctypes.c_int()
+    dev.call("qcur_qsvd_jacobi", ad.data_ptr(), m, n, n, acm.data_ptr(), vcm.data_ptr() if want_v else None,
+             sig.data_ptr(), ctypes.byref(sweeps))
+    return acm.cpu().numpy(), (vcm.cpu().numpy() if want_v else None), sig.cpu().numpy()
+
+
+def _qdot(u: np.ndarray, v: np.ndarray) -> np.ndarray:
+    """sum_i conj(u_i) v_i for quaternion vectors stored (len, 4)."""
+    a0, a1, a2, a3 = u[:, 0], -u[:, 1], -u[:, 2], -u[:, 3]
+    b0, b1, b2, b3 = v[:, 0], v[:, 1], v[:, 2], v[:, 3]
+    return np.array([np.sum(a0 * b0 - a1 * b1 - a2 * b2 - a3 * b3), np.sum(a0 * b1 + a1 * b0 + a2 * b3 - a3 * b2),
+                     np.sum(a0 * b2 - a1 * b3 + a2 * b0 + a3 * b1), np.sum(a0 * b3 + a1 * b2 - a2 * b1 + a3 * b0)])
+
+
+def _rmul(u: np.ndarray, q: np.ndarray) -> np.ndarray:
+    """u * q (quaternion vector times a quaternion scalar on the right)."""
+    a0, a1, a2, a3 = u[:, 0], u[:, 1], u[:, 2], u[:, 3]
+    b0, b1, b2, b3 = q
+    return np.stack([a0 * b0 - a1 * b1 - a2 * b2 - a3 * b3, a0 * b1 + a1 * b0 + a2 * b3 - a3 * b2,
+                     a0 * b2 - a1 * b3 + a2 * b0 + a3 * b1, a0 * b3 + a1 * b2 - a2 * b1 + a3 * b0], axis=1)
+
+
+def _complete(cols: list, dim: int, need: int) -> list:
+    """Extend orthonormal quaternion columns by `need` unit vectors orthogonal to them
+    (twice-applied Gram-Schmidt over the canonical basis, as _complete_basis, linalg.py:313-335)."""
+    out = list(cols)
+    for i in range(dim):
+        if len(out) >= len(cols) + need:
+            break
+        e = np.zeros((dim, 4))
+        e[i, 0] = 1.0
+        for _ in range(2):
+            for q in out:
+                e = e - _rmul(q, _qdot(q, e))
+        nr = float(np.sqrt(np.sum(e * e)))
+        if nr > 1e-3:
+            out.append(e / nr)
+    if len(out) < len(cols) + need:
+        raise ParameterError("failed to complete an orthonormal basis")
+    return out[len(cols):]
+
+
+def _to_qmat(cols: list, dim: int) -> QMatrix:
+    arr = np.stack(cols, axis=1) if cols else np.zeros((dim, 0, 4))
+    return QMatrix._wrap(*(np.ascontiguousarray(arr[:, :, t]) for t in range(4)))
+
+
+def qsvd(a, k: int | None = None) -> QSVDResult:
+    """Quaternion SVD (linalg.py:226-310): W (m x r), V (n x r) with quaternion-orthonormal
+    columns and sigma nonincreasing, r = k or min(m, n).  Computed by one-sided Jacobi on the
+    quaternion columns (of A, or of A^H when m < n), so each singular value appears once; the
+    zero-singular-value columns of W are completed to an orthonormal set."""
+    m, n = (int(v) for v in a.shape)
+    r_full = min(m, n)
+    if k is None:
+        k = r_full
+    else:
+        k = int(k)
+        if not 1 <= k <= r_full:
+            raise ParameterError(f"k={k} outside 1..min(m,n)={r_full}")
+    tall = m >= n
+    src = a if tall else QMatrix._wrap(*_planes_conj_t(a))
+    p, q = (m, n) if tall else (n, m)  # src is p x q, p >= q
+    av, vc, sig = _jacobi(src, True)
+    order = np.argsort(-sig, kind="stable")
+    sig = sig[order]
+    smax = float(sig[0]) if sig.size else 0.0
+    if smax == 0.0:
+        eye_w = QMatrix._wrap(np.eye(m, k), np.zeros((m, k)), np.zeros((m, k)), np.zeros((m, k)))
+        eye_v = QMatrix._wrap(np.eye(n, k), np.zeros((n, k)), np.zeros((n, k)), np.zeros((n, k)))
+        return QSVDResult(eye_w, np.zeros(k), eye_v)
+    zero_tol = max(2 * m, 2 * n) * _EPS * smax
+    left = [av[j] / sig[i] for i, j in enumerate(order[:k]) if sig[i] > zero_tol]
+    nz = len(left)
+    if nz < k:
+        left = left + _complete(left, p, k - nz)
+    right = [vc[j] for j in order[:k]]
+    w_src, v_src = _to_qmat(left, p), _to_qmat(right, q)
+    if tall:
+        return QSVDResult(w_src, sig[:k], v_src)
+    return QSVDResult(v_src, sig[:k], w_src)  # A^H = W' S V'^H  =>  A = V' S W'^H
+
+
+def _planes_conj_t(a):
+    from .quat import as_planes
+
+    a0, a1, a2, a3 = as_planes(a)
+    return a0.T.copy(), -a1.T, -a2.T, -a3.T
+
+
+def _singular_values(a) -> np.ndarray:
+    m, n = (int(v) for v in a.shape)
+    src = a if m >= n else QMatrix._wrap(*_planes_conj_t(a))
+    _, _, sig = _jacobi(src, False)
+    return np.sort(sig)[::-1]
+
+
+def numerical_rank(a, tol: float | None = None) -> int:
+    """Number of singular values above the pseudoinverse cutoff eps max(m, n) sigma_max
+    (linalg.py:370-378)."""
+    sigma = _singular_values(a)
+    smax = float(sigma[0])
+    if smax == 0.0:
+        return 0
+    cutoff = _EPS * max(a.shape) * smax if tol is None else float(tol)
+    return int(np.sum(sigma > cutoff))
+
+
+def lowrank_truncate(a, k: int) -> QMatrix:
+    """Best rank-k approximation W_k diag(sigma_k) V_k^H (linalg.py:381-383)."""
+    return qsvd(a, k).reconstruct()
+
+
+def save_qsvd(result: QSVDResult, directory) -> None:
+    """W and V as .qmat files plus sigma as a plain-text list (linalg.py:406-420)."""
+    from pathlib import Path
+
+    from .quat import write_qmat
+
+    out = Path(directory)
+    out.mkdir(parents=True, exist_ok=True)
+    write_qmat(result.w, out / "w.qmat")
+    write_qmat(result.v, out / "v.qmat")
+    with open(out / "sigma.txt", "w") as fh:
+        for s_ in result.sigma:
+            fh.write(f"{s_:.17g}\n")

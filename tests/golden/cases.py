@@ -40,6 +40,12 @@ COMPLETION_CASES = {
 }
 SPECTRAL_CASES = {"s_30x20": (30, 20, 0, 31), "s_lowrank_40": (40, 40, 3, 32), "s_1x5": (1, 5, 0, 33),
                   "s_64x12": (64, 12, 0, 34)}
+QSVD_CASES = {"q_9x6": (9, 6, 0, 41), "q_6x9": (6, 9, 0, 42), "q_lowrank_10x8": (10, 8, 3, 43),
+              "q_30x30": (30, 30, 0, 44), "q_1x4": (1, 4, 0, 45)}
+# (m, n, k, noise, seed, |I|, |J|, norm)
+PERT_CASES = {"pb_spec_40x36": (40, 36, 3, 1e-4, 51, 12, 10, "spectral"),
+              "pb_fro_40x36": (40, 36, 3, 1e-4, 51, 12, 10, "frobenius"),
+              "pb_spec_60x50": (60, 50, 4, 1e-3, 52, 16, 14, "spectral")}
 DERIVE_SEED_CASES = [(0, ("draw",)), (5, ("sweep", 0)), (5, ("sweep", 17)), (2 ** 63 + 11, ("batch", 3))]
 
 
@@ -84,3 +90,20 @@ def spectral_input(case):
         p = O.lowrank_planes(g, m, n, k)
         return tuple(x + 1e-6 * g.standard_normal(x.shape) for x in p)
     return O.random_planes(g, m, n)
+
+
+def qsvd_input(case):
+    m, n, k, seed = case
+    g = np.random.default_rng(seed)
+    return O.lowrank_planes(g, m, n, k) if k else O.random_planes(g, m, n)
+
+
+def pert_input(case):
+    """(clean rank-k X, noise E, rows I, cols J)."""
+    m, n, k, noise, seed, nr, nc = case[:7]
+    g = np.random.default_rng(seed)
+    x = O.lowrank_planes(g, m, n, k)
+    e = tuple(noise * g.standard_normal((m, n)) for _ in range(4))
+    rows = np.sort(g.choice(m, nr, replace=False)).astype(np.int64)
+    cols = np.sort(g.choice(n, nc, replace=False)).astype(np.int64)
+    return x, e, rows, cols

@@ -79,6 +79,20 @@ def main() -> None:
 
     for name, case in cases.SPECTRAL_CASES.items():
         out[f"{name}/sigma"] = np.array([ref_spectral_norm(qcur.QMatrix(*cases.spectral_input(case)))])
+    from qcur.cur import perturbation_bounds as ref_perturbation_bounds
+    from qcur.linalg import numerical_rank as ref_numerical_rank
+    from qcur.linalg import qsvd as ref_qsvd
+
+    for name, case in cases.QSVD_CASES.items():
+        a = qcur.QMatrix(*cases.qsvd_input(case))
+        out[f"{name}/sigma"] = np.asarray(ref_qsvd(a).sigma)
+        out[f"{name}/rank"] = np.array([ref_numerical_rank(a)])
+    for name, case in cases.PERT_CASES.items():
+        x, e, rows, cols = cases.pert_input(case)
+        b = ref_perturbation_bounds(qcur.QMatrix(*x), qcur.QMatrix(*e), rows, cols, case[2], norm=case[7])
+        out[f"{name}/fields"] = np.array([b.lhs, b.bound_a, b.bound_b, b.noise_norm, b.xrp_norm, b.cx_norm,
+                                          b.wsub_pinv_norm, b.vsub_pinv_norm])
+        print(name, b)
     import tempfile
 
     with tempfile.TemporaryDirectory() as td:

@@ -75,3 +75,27 @@ def test_oracle_completion_matches_reference(name):
 def test_oracle_derive_seed_matches_reference():
     got = [O.derive_seed(s, *parts) for s, parts in cases.DERIVE_SEED_CASES]
     assert np.array_equal(np.array(got, dtype=np.uint64), G["derive_seed"])
+
+
+@pytest.mark.parametrize("name", sorted(cases.QSVD_CASES))
+def test_oracle_singular_values_and_rank(name):
+    a = cases.qsvd_input(cases.QSVD_CASES[name])
+    s = O.singular_values(a)
+    want = G[f"{name}/sigma"]
+    assert np.allclose(s[: want.size], want, rtol=1e-12, atol=1e-14 * want[0])
+    assert O.numerical_rank(a) == int(G[f"{name}/rank"][0])
+
+
+@pytest.mark.parametrize("name", sorted(cases.PERT_CASES))
+def test_oracle_perturbation_bounds(name):
+    case = cases.PERT_CASES[name]
+    x, e, rows, cols = cases.pert_input(case)
+    got = O.perturbation_bounds(x, e, rows, cols, case[2], norm=case[7])
+    keys = ["lhs", "bound_a", "bound_b", "noise_norm", "xrp_norm", "cx_norm", "wsub_pinv_norm", "vsub_pinv_norm"]
+    want = G[f"{name}/fields"]
+    # lhs = ||X - C U R|| of a noisy projection: two correct pseudoinverses (the reference's
+    # QSVD + Gram-Schmidt, the oracle's complex-adjoint pinv) differ by ~1e-13 in U, which the
+    # small residual amplifies to ~1e-8; every other field is a norm of a well-conditioned factor
+    for k, w in zip(keys, want):
+        assert got[k] == pytest.approx(w, rel=1e-7 if k == "lhs" else 1e-9), k
+    assert got["lhs"] <= got["bound_a"] <= got["bound_b"] or case[7] != "spectral"
