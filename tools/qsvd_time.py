@@ -1,0 +1,20 @@
+"""Time qsvd / numerical_rank on the device at a few sizes (CUDA sync around each call)."""
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, ".")
+import paper_2402_19147_b200 as q  # noqa: E402
+
+for m, n in [(200, 200), (500, 500), (1000, 1000), (2000, 500)]:
+    g = np.random.default_rng(m + n)
+    a = q.QMatrix(*(g.standard_normal((m, n)) for _ in range(4)))
+    q.qsvd(a, 10)
+    t0 = time.perf_counter()
+    res = q.qsvd(a, 10)
+    t1 = time.perf_counter()
+    r = q.numerical_rank(a)
+    t2 = time.perf_counter()
+    print(f"{m}x{n}: qsvd(k=10) {t1 - t0:.3f} s, numerical_rank {t2 - t1:.3f} s, sigma0 {res.sigma[0]:.6f} rank {r}",
+          flush=True)
