@@ -266,10 +266,13 @@ __global__ void __launch_bounds__(OE_THREADS, 1)
       }
     }
   } else {
-    // warp w drains TMEM lanes 32 (w % 4) .. +31; the 10 column chunks of 8 go round-robin to
-    // the four warps of a lane quarter
+    // warp w drains TMEM lanes 32 (w % 4) .. +31, columns 20 s .. 20 s + 19 (s = (w - 2) / 4:
+    // five quaternions).  Phase A reads the six level accumulators, folds them into the FP64
+    // products and releases TMEM at once, so the next tile's MMAs overlap phase B (X and the
+    // statistics).
     const int quarter = warp & 3, sub = (warp - 2) >> 2;
     const int rloc = quarter * 32 + lane;
+    constexpr int QW = OE_BN / 4 / 4;  // quaternion columns per warp
     const double sc = P.psnr_scale;
     double v[4] = {0.0, 0.0, 0.0, 0.0};  // this thread's sums over all its units, in a fixed order
     int t = 0;
@@ -279,6 +282,8 @@ __global__ void __launch_bounds__(OE_THREADS, 1)
       const bool rvalid = row < P.m;
       const int er = rvalid ? P.ea[row] : 0;
       const double* xrow = P.X + (rvalid ? row : 0) * P.ldx;
+      const int64_t jq0 = ((int64_t)nb * OE_BN + sub * 4 * QW) >> 2;  // first quaternion column
+      double pr[QW][4];
       mbar_wait(tfull, (unsigned)t & 1u);
       tc_fence_after();
       if (P.experiment == 1) {
@@ -286,45 +291,48 @@ __global__ void __launch_bounds__(OE_THREADS, 1)
         if (lane == 0) mbar_arrive(tempty);
         continue;
       }
-#pragma unroll 1
-      for (int c = 8 * sub; c < OE_BN; c += 32) {
-        uint32_t lv[6][8];
-        const uint32_t ta = tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c;
 #pragma unroll
-        for (int L = 0; L < 6; ++L) tmem_ld8(ta + (uint32_t)(L * OE_BN), lv[L]);
+      for (int i = 0; i < QW; ++i) {
+        uint32_t lv[6][4];
+        const uint32_t ta = tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(sub * 4 * QW + 4 * i);
+#pragma unroll
+        for (int L = 0; L < 6; ++L) tmem_ld4(ta + (uint32_t)(L * OE_BN), lv[L]);
         tmem_wait_ld();
-        const int64_t j0 = (int64_t)nb * OE_BN + c;  // 8 consecutive reals = 2 quaternions
-        if (rvalid && j0 < P.N) {
-          const bool q1 = j0 + 4 < P.N;  // the second quaternion of the chunk exists
-          const double4 xa = *reinterpret_cast<const double4*>(xrow + j0);
-          const double4 xb = q1 ? *reinterpret_cast<const double4*>(xrow + j0 + 4) : make_double4(0.0, 0.0, 0.0, 0.0);
-          const double xs[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
-          // P R = (sum_L 256^L acc_L) 2^(56 - a_i - b_j)
-          const double f0 = pow2(8 * 7 - er - P.eb[j0 >> 2]);
-          const double f1 = q1 ? pow2(8 * 7 - er - P.eb[(j0 >> 2) + 1]) : 0.0;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            if (i >= 4 && !q1) break;
-            double h = i2d(lv[5][i]);
+        for (int h = 0; h < 4; ++h) {
+          double acc = i2d(lv[5][h]);
 #pragma unroll
-            for (int L = 4; L >= 0; --L) h = fma(h, 256.0, i2d(lv[L][i]));
-            const double pr = h * (i < 4 ? f0 : f1);
-            const double x = xs[i], d = x - pr;
+          for (int L = 4; L >= 0; --L) acc = fma(acc, 256.0, i2d(lv[L][h]));
+          pr[i][h] = acc;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty);  // TMEM free: the next tile's MMAs start now
+      if (rvalid) {
+#pragma unroll
+        for (int i = 0; i < QW; ++i) {
+          const int64_t jq = jq0 + i;
+          if (4 * jq >= P.N) break;
+          const double4 xq = *reinterpret_cast<const double4*>(xrow + 4 * jq);
+          const double f = pow2(8 * 7 - er - P.eb[jq]);  // P R = (sum_L 256^L acc_L) 2^(56 - a_i - b_j)
+          const double xs[4] = {xq.x, xq.y, xq.z, xq.w};
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const double prh = pr[i][h] * f;
+            const double x = xs[h], d = x - prh;
             v[0] = fma(d, d, v[0]);
             v[1] = fma(x, x, v[1]);
-            if ((i & 3) != 0) {
+            if (h != 0) {
               v[2] = fma(d, d, v[2]);
               if (sc > 0.0) {
-                const double q = rint(fmin(fmax(sc * x, 0.0), 255.0)) - rint(fmin(fmax(sc * pr, 0.0), 255.0));
+                const double q = rint(fmin(fmax(sc * x, 0.0), 255.0)) - rint(fmin(fmax(sc * prh, 0.0), 255.0));
                 v[3] = fma(q, q, v[3]);
               }
             }
           }
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(tempty);
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) v[k] = warp_sum(v[k]);
