@@ -397,6 +397,63 @@ def run_completion(args) -> None:
     }))
 
 
+def run_qsvd(args) -> None:
+    """--qsvd: SURVEY 8(f) rank 4, the truncated QSVD comparator (qsvd(x, k), linalg.py:226-310, as the
+    reference's scaling experiment races it against QMCUR, bench.py:319-352) on a 1000 x 1000
+    rank-10 + noise matrix, k = 10.  CPU baseline: the oracle's complex-adjoint SVD (numpy LAPACK)."""
+    import torch
+
+    import paper_2402_19147_b200 as q
+
+    m = n = 1000
+    k = 10
+    g = np.random.default_rng(20240229)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    # quaternion rank-10 product (on the device GEMM) plus noise
+    pf = q.QMatrix(*(g.standard_normal((m, k)) for _ in range(4)))
+    qf = q.QMatrix(*(g.standard_normal((k, n)) for _ in range(4)))
+    s = pf @ qf
+    planes = [a + 1e-3 * g.standard_normal((m, n)) for a in s.planes]
+    x = q.QMatrix(*planes)
+    res = None
+    for _ in range(max(args.warmup, 1)):
+        res = q.qsvd(x, k)
+    torch.cuda.synchronize()
+    steps = max(1, min(args.steps, 10))
+    sampler = ClockSampler(0)
+    with sampler:
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            res = q.qsvd(x, k)
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+    recon_err = float((x - res.reconstruct()).frobenius_norm() / x.frobenius_norm())
+    cpu = None
+    if not args.no_cpu_baseline:
+        import oracle as O
+
+        t0 = time.perf_counter()
+        _, s_c, _ = np.linalg.svd(O.adjoint(tuple(planes)), full_matrices=False)
+        ct = time.perf_counter() - t0
+        s_ref = s_c[0::2]
+        cpu = {"value": 1.0 / ct, "unit": "qsvd/s", "cores": cpu_threads(), "kind": "port",
+               "sample": "the SVD (with vectors) of the 2000 x 2000 complex adjoint, numpy LAPACK zgesdd: the "
+                         "dominant step of the reference's qsvd (linalg.py:253), without its Gram-Schmidt pull-back",
+               "sigma_rel_diff_top_k": float(np.max(np.abs(s_ref[:k] - res.sigma) / s_ref[0]))}
+    print(json.dumps({
+        "metric": "truncated QSVD per second (qsvd(x, k), linalg.py:226-310)", "value": steps / el,
+        "unit": "qsvd/s", "n_gpus": 1, "steps": steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / steps,
+        "higher_is_better": True, "dtype": "f64",
+        "data": "synthetic host QMatrix: quaternion rank-10 Gaussian product + N(0, 1e-6) noise, seed 20240229",
+        "config": {"workload": f"qsvd {m}x{n}, k = {k} (quaternion one-sided Jacobi on the GPU)", "m": m, "n": n,
+                   "k": k},
+        "e2e": {"value": steps / el, "unit": "qsvd/s", "api": "qsvd(x, k) on a host QMatrix (upload, Jacobi sweeps, "
+                "W / sigma / V download inside the timed region)", "h2d_bytes_per_step": 32 * m * n,
+                "d2h_bytes_per_step": 32 * (m * n + n * n) + 8 * n},
+        "reconstruction_rel_err": recon_err, "clocks": sampler.summary(), "cpu_baseline": cpu,
+    }))
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -409,9 +466,13 @@ def main() -> None:
     ap.add_argument("--c", type=int, default=None, help="override c = r (cfg3: 64, 128 or 256)")
     ap.add_argument("--rowshard", action="store_true",
                     help="shard one matrix by row blocks across the ranks (cfg5 design) instead of replicas")
+    ap.add_argument("--qsvd", action="store_true", help="truncated QSVD comparator (SURVEY 8(f) rank 4)")
     ap.add_argument("--completion", action="store_true",
                     help="measure the completion solver (Algorithm 2) instead of the QMCUR step")
     args = ap.parse_args()
+    if args.qsvd:
+        run_qsvd(args)
+        return
     if args.completion:
         run_completion(args)
         return
