@@ -216,6 +216,10 @@ int qcur_qsvd_jacobi(qcur_ctx* ctx, const double* a_dev, int64_t m, int64_t n, i
 /* Engine of the X Q_R contraction inside qmcur: 0 auto (INT8 when large), 1 FP64 DMMA, 2 INT8 (Ozaki II).
    The environment variable QCUR_GEMM=dmma|int8 sets the initial mode of new contexts. */
 int qcur_set_gemm_mode(qcur_ctx* ctx, int mode);
+/* C (M x N) = A^H B with A (K x M), B (K x N): the Hermitian products of CholeskyQR2 and the core
+   (Z^H Z, Q_C^H Y) on the INT8 tensor cores as 16 real plane products (exact modular arithmetic). */
+int qcur_qgemm_herm_int8(qcur_ctx* ctx, int64_t M, int64_t N, int64_t K, const double* a_dev, int64_t lda,
+                         const double* b_dev, int64_t ldb, double* c_dev, int64_t ldc);
 /* C (M x N) = A (M x K) * B (K x N), op N, on the INT8 tensor cores by exact modular arithmetic
    (Ozaki scheme II, nmod moduli; 0 = default).  Same contract as qcur_qgemm with alpha = 1, beta = 0. */
 int qcur_qgemm_int8(qcur_ctx* ctx, int64_t M, int64_t N, int64_t K, const double* a_dev, int64_t lda,

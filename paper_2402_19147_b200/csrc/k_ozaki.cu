@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         tmem_ld32(tbase + (uint32_t)(half * 256 + c0) + ((uint32_t)(quarter * 32) << 16), v);
         uint32_t w[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) w[q] = 0;
+        for (int z = 0; z < 8; ++z) w[z] = 0;
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           const int z = (int)v[i];
@@ -557,6 +557,143 @@ __global__ void __launch_bounds__(256) k_oz_crt(const uint8_t* __restrict__ res,
   }
   double* y = Y + i * ldy + 4 * jq;
   *reinterpret_cast<double4*>(y) = make_double4(out[0], out[1], out[2], out[3]);
+}
+
+// ---------------------------------------------------------------------------
+// Hermitian products C = A^H B (A: p x qa, B: p x qb quaternions) by real plane products:
+// C_t[i][j] = sum_{a,b} sign_t(a,b) (A_a^T B_b)[i][j], the 16 plane products forming one real
+// GEMM of W_A (4qa x p) by W_B (4qb x p), both K-major stacks of the scaled planes.  No 4x
+// Hamilton expansion of either operand; the signed combination is exact (128-bit integers).
+// ---------------------------------------------------------------------------
+template <int L>
+__global__ void __launch_bounds__(256) k_oz_wres(const double* __restrict__ Z, int64_t p, int64_t q, int64_t ldz,
+                                                 const int* __restrict__ ex, uint8_t* __restrict__ res,
+                                                 int64_t pitch, int64_t plane) {
+  const int64_t k4n = pitch / 4;
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= q * k4n) return;
+  const int64_t i = id / k4n, k0 = 4 * (id - i * k4n);
+  const int e = ex[i];
+  const double s1 = ldexp(1.0, e / 2), s2 = ldexp(1.0, e - e / 2);
+  const long long magic_bits = __double_as_longlong(kMagic);
+  const f32x2 mag = dup(kMagicF), nmag = dup(-kMagicF), lmag = dup(-8388608.0f);
+  // per plane a: limbs of the four values k0..k0+3 as two FP32 pairs, and their low bytes (p = 256)
+  f32x2 f[4][2][4];
+  unsigned low[4];
+  double v[4][4];
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    Quat z = qzero();
+    if (k0 + h < p) z = ldq_nc(Z + ((k0 + h) * ldz + i) * 4);
+    v[0][h] = z.w;
+    v[1][h] = z.x;
+    v[2][h] = z.y;
+    v[3][h] = z.z;
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    unsigned lb[4], lm[4][4];
+    float sg[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const long long iv = __double_as_longlong(v[a][h] * s1 * s2 + kMagic) - magic_bits;  // rint(x 2^e)
+      lb[h] = (unsigned)iv;
+      const unsigned long long u = (unsigned long long)(iv < 0 ? -iv : iv);
+      sg[h] = iv < 0 ? -1.0f : 1.0f;
+      lm[h][0] = 0x4B000000u | ((unsigned)u & 0x1fffu);
+      lm[h][1] = 0x4B000000u | ((unsigned)(u >> 13) & 0x1fffu);
+      lm[h][2] = 0x4B000000u | ((unsigned)(u >> 26) & 0x1fffu);
+      lm[h][3] = 0x4B000000u | (unsigned)(u >> 39);
+    }
+    low[a] = __byte_perm(__byte_perm(lb[0], lb[1], 0x0040), __byte_perm(lb[2], lb[3], 0x0040), 0x5410);
+#pragma unroll
+    for (int hp = 0; hp < 2; ++hp) {
+      const f32x2 sgn = pk(sg[2 * hp], sg[2 * hp + 1]);
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        f[a][hp][t] = fmul2(fadd2(((f32x2)lm[2 * hp][t]) | ((f32x2)lm[2 * hp + 1][t] << 32), lmag), sgn);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) *reinterpret_cast<unsigned*>(res + (a * q + i) * pitch + k0) = low[a];  // p = 256
+#define OZ_WPLANE(l)                                                                                      \
+  if constexpr (l < L) {                                                                                  \
+    _Pragma("unroll") for (int a = 0; a < 4; ++a) {                                                       \
+      const unsigned w = pack_pairs(pair_residue<l>(f[a][0][0], f[a][0][1], f[a][0][2], f[a][0][3], mag, nmag), \
+                                    pair_residue<l>(f[a][1][0], f[a][1][1], f[a][1][2], f[a][1][3], mag, nmag)); \
+      *reinterpret_cast<unsigned*>(res + (l) * plane + (a * q + i) * pitch + k0) = w;                     \
+    }                                                                                                     \
+  }
+  OZ_WPLANE(1) OZ_WPLANE(2) OZ_WPLANE(3) OZ_WPLANE(4) OZ_WPLANE(5) OZ_WPLANE(6) OZ_WPLANE(7) OZ_WPLANE(8)
+  OZ_WPLANE(9) OZ_WPLANE(10) OZ_WPLANE(11) OZ_WPLANE(12) OZ_WPLANE(13) OZ_WPLANE(14) OZ_WPLANE(15)
+#undef OZ_WPLANE
+}
+
+// one product value from its L residue bytes (stride `plane`), centred in (-M/2, M/2]
+template <int L>
+__device__ __forceinline__ __int128 crt_one(const uint8_t* rp, int64_t plane, const OzCrt& c) {
+  unsigned long long col[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    const float rw = (float)rp[l * plane] * c.w[l];
+    float t = fmaf(-(fmaf(rw, c.pinv[l], kMagicF) - kMagicF), c.P[l], rw);
+    t = t < 0.0f ? t + c.P[l] : t;
+    const unsigned tt = (unsigned)t;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) col[k] += (unsigned long long)tt * c.mi[l][k];
+  }
+  const unsigned long long c1 = col[1] + (col[0] >> 32);
+  const unsigned long long c2 = col[2] + (c1 >> 32);
+  const unsigned long long c3 = col[3] + (c2 >> 32);
+  const unsigned long long lo = (col[0] & 0xffffffffull) | (c1 << 32);
+  const unsigned long long hi = (c2 & 0xffffffffull) | (c3 << 32);
+  unsigned __int128 S = ((unsigned __int128)hi << 64) | lo;
+  const unsigned __int128 M = ((unsigned __int128)c.M_hi << 64) | c.M_lo;
+  long long q = (long long)floor(((double)hi * 18446744073709551616.0 + (double)lo) / c.Md);
+  q = q < 0 ? 0 : q;
+  S -= M * (unsigned long long)q;
+  if ((__int128)S < 0) S += M;
+  if (S >= M) S -= M;
+  __int128 Z = (__int128)S;
+  if (S > (M >> 1)) Z -= (__int128)M;
+  return Z;
+}
+
+// C[i][j] from the 16 plane products: conj(x) y = (x0y0 + x1y1 + x2y2 + x3y3) + (x0y1 - x1y0 - x2y3 + x3y2) i
+//   + (x0y2 + x1y3 - x2y0 - x3y1) j + (x0y3 - x1y2 + x2y1 - x3y0) k.  One thread per component t
+// (four exact CRTs, combined in 128-bit integers).
+template <int L>
+__global__ void __launch_bounds__(256) k_oz_hcrt(const uint8_t* __restrict__ res, int64_t qa, int64_t qb,
+                                                 int64_t pitch, int64_t plane, const int* __restrict__ exa,
+                                                 const int* __restrict__ exb, const __grid_constant__ OzCrt c,
+                                                 double* __restrict__ C, int64_t ldc) {
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= qa * qb * 4) return;
+  const int t = (int)(id & 3);
+  const int64_t ij = id >> 2, i = ij / qb, j = ij - i * qb;
+  // (a, b, sign) of the four plane products of component t
+  constexpr int kTerm[4][4][3] = {{{0, 0, 1}, {1, 1, 1}, {2, 2, 1}, {3, 3, 1}},
+                                  {{0, 1, 1}, {1, 0, -1}, {2, 3, -1}, {3, 2, 1}},
+                                  {{0, 2, 1}, {1, 3, 1}, {2, 0, -1}, {3, 1, -1}},
+                                  {{0, 3, 1}, {1, 2, -1}, {2, 1, 1}, {3, 0, -1}}};
+  __int128 g = 0;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    int a = 0, b = 0, sgn = 1;
+#pragma unroll
+    for (int tt = 0; tt < 4; ++tt)
+      if (tt == t) {
+        a = kTerm[tt][u][0];
+        b = kTerm[tt][u][1];
+        sgn = kTerm[tt][u][2];
+      }
+    const __int128 z = crt_one<L>(res + (a * qa + i) * pitch + (b * qb + j), plane, c);
+    g = sgn > 0 ? g + z : g - z;
+  }
+  const int e = -(exa[i] + exb[j]);
+  const double s1 = ldexp(1.0, e / 2), s2 = ldexp(1.0, e - e / 2);
+  C[i * ldc + 4 * j + t] =
+      ((double)(long long)(g >> 64) * 18446744073709551616.0 + (double)(unsigned long long)g) * s1 * s2;
 }
 
 // ---------------------------------------------------------------------------
@@ -724,9 +861,78 @@ __global__ void __launch_bounds__(128, 1) k_i8_probe(int iters, int* sink) {
   }
 }
 
+// plan of C = A^H B: K = p; A operand 4qa rows, B operand 4qb rows (N = 4qb)
+struct OzHPlan {
+  OzPlan g;  // K, Kpitch, N, Npitch, BN, nblocks, bits of the GEMM
+  size_t off_wa, off_wb, off_res, off_exa, off_exb, off_ca, off_cb, total;
+};
+
+OzHPlan oz_hplan(int64_t p, int64_t qa, int64_t qb, int L, bool same) {
+  OzHPlan h{};
+  OzPlan& g = h.g;
+  g.L = L;
+  g.K = p;
+  g.Kpitch = (p + 15) / 16 * 16;
+  g.N = 4 * qb;
+  g.nblocks = (g.N + 255) / 256;
+  g.BN = 16 * ((g.N + 16 * g.nblocks - 1) / (16 * g.nblocks));
+  g.Npitch = g.nblocks * g.BN;
+  double log2M = 0.0;
+  for (int l = 0; l < L; ++l) log2M += std::log2((double)kOzModuli[l]);
+  const int bits = (int)std::floor((log2M - 1.0 - std::log2((double)p) - 1e-6) / 2.0);  // |P_ab| <= p 2^(2 bits)
+  g.bits = bits > 51 ? 51 : bits;
+  auto al = [](size_t v) { return (v + 255) / 256 * 256; };
+  size_t o = 0;
+  h.off_wa = o;
+  o = al(o + (size_t)L * 4 * qa * g.Kpitch);
+  h.off_wb = o;
+  if (!same) o = al(o + (size_t)L * 4 * qb * g.Kpitch);
+  h.off_res = o;
+  o = al(o + (size_t)L * 4 * qa * g.Npitch);
+  h.off_exa = o;
+  o = al(o + (size_t)qa * 4);
+  h.off_exb = o;
+  o = al(o + (size_t)qb * 4);
+  h.off_ca = o;
+  o = al(o + (size_t)qa * 8);
+  h.off_cb = o;
+  o = al(o + (size_t)qb * 8);
+  h.total = o;
+  return h;
+}
+
+// exponents (column maxima) and residues of the planes of Z (p x q) for the Hermitian products
+void oz_planes(const double* Z, int64_t p, int64_t q, int64_t ldz, int L, int bits, unsigned long long* cmax,
+               int* ex, uint8_t* w, int64_t pitch, cudaStream_t st) {
+  cudaMemsetAsync(cmax, 0, (size_t)q * 8, st);
+  const int64_t slabs = (p + 63) / 64 < 64 ? (p + 63) / 64 : 64, rows_per = (p + slabs - 1) / slabs;
+  ++::qcur::g_launches;
+  k_oz_bmax<<<dim3((unsigned)((q + 31) / 32), (unsigned)slabs), 256, 0, st>>>(Z, p, q, ldz, rows_per, cmax);
+  ++::qcur::g_launches;
+  k_oz_bexp<<<(unsigned)((q + 255) / 256), 256, 0, st>>>(cmax, q, bits, ex);
+  const int64_t nthreads = q * (pitch / 4);
+  ++::qcur::g_launches;
+  if (L == 14)
+    k_oz_wres<14><<<(unsigned)((nthreads + 255) / 256), 256, 0, st>>>(Z, p, q, ldz, ex, w, pitch, 4 * q * pitch);
+  else
+    k_oz_wres<15><<<(unsigned)((nthreads + 255) / 256), 256, 0, st>>>(Z, p, q, ldz, ex, w, pitch, 4 * q * pitch);
+}
+
 }  // namespace
 
 int ozaki_max_moduli() { return kOzMaxMod; }
+
+size_t ozaki_herm_workspace_bytes(int64_t p, int64_t qa, int64_t qb, int same) {
+  return oz_hplan(p, qa, qb, kOzMaxModDefault, same != 0).total + 1024;
+}
+
+bool ozaki_herm_supported(int64_t p, int64_t qa, int64_t qb) {
+  // odd-moduli residues in [-127, 127]: p 127^2 < 2^31; workspace cap as the other products
+  return p >= 1 && qa >= 1 && qb >= 1 && p <= 133140 &&
+         (double)oz_hplan(p, qa, qb, kOzMaxModDefault, false).total <= 4e9;
+}
+
+
 
 // dense INT8 tensor-core rate of this GPU in TOP/s (2 ops per multiply-add)
 double run_i8_peak(int sms, cudaStream_t st) {
@@ -884,30 +1090,6 @@ int launch_ozaki_multiply(int64_t m, int64_t n, int64_t r, double* Y, int64_t ld
                        reinterpret_cast<int*>(ws + pl.off_fx), Y, ldy, L, st);
 }
 
-// Hermitian Grams G_k = A_k^H A_k (A_k: p_k x q_k, ld lda_k; G_k: q_k x q_k, ld ldg_k) for np <= 2
-// problems in one GEMM launch.  Only E(A_k) is formed: its rows 4j (t = 0) hold conj(a_kj), i.e.
-// row j of A_k^H, so they serve as the A operand (row stride 4 rows) with the same exponents.
-int launch_ozaki_gram(const double* const* A, const int64_t* p, const int64_t* q, const int64_t* lda, double* const* G,
-                      const int64_t* ldg, int np, int L, void* const* workspace, cudaStream_t st) {
-  if (L < 14 || L > 15 || np < 1 || np > 2) return 1;
-  OzJob jobs[2];
-  for (int k = 0; k < np; ++k) {
-    int rc = launch_ozaki_prep_b(q[k], p[k], A[k], q[k], lda[k], L, workspace[k], st);
-    if (rc) return rc;
-    const OzPlan pl = oz_plan(q[k], p[k], q[k], L);
-    uint8_t* ws = reinterpret_cast<uint8_t*>(((uintptr_t)workspace[k] + 255) / 256 * 256);
-    if (!oz_job(jobs[k], pl, q[k], ws + pl.off_bres, 4 * pl.Kpitch, ws + pl.off_bres, L, ws + pl.off_res)) return 2;
-  }
-  oz_launch_gemm(jobs, np, L, st);
-  for (int k = 0; k < np; ++k) {
-    const OzPlan pl = oz_plan(q[k], p[k], q[k], L);
-    uint8_t* ws = reinterpret_cast<uint8_t*>(((uintptr_t)workspace[k] + 255) / 256 * 256);
-    const int* fx = reinterpret_cast<int*>(ws + pl.off_fx);
-    int rc = oz_launch_crt(ws + pl.off_res, q[k], pl, fx, fx, G[k], ldg[k], L, st);
-    if (rc) return rc;
-  }
-  return 0;
-}
 
 int launch_ozaki_finish(int64_t m, int64_t n, const double* B, int64_t r, int64_t ldb, double* Y, int64_t ldy, int L,
                         void* workspace, cudaStream_t st) {
@@ -920,6 +1102,51 @@ int launch_ozaki_gemm(const double* X, int64_t m, int64_t n, int64_t ldx, const 
                       double* Y, int64_t ldy, int L, void* workspace, cudaStream_t st) {
   int rc = launch_ozaki_prepare(X, m, n, ldx, r, L, workspace, st);
   return rc ? rc : launch_ozaki_finish(m, n, B, r, ldb, Y, ldy, L, workspace, st);
+}
+
+// C_k (qa_k x qb_k) = A_k^H B_k for np <= 2 problems (A_k: p_k x qa_k, B_k: p_k x qb_k, B_k == A_k
+// allowed: its planes are formed once); one INT8 GEMM launch for all of them
+int launch_ozaki_herm(const double* const* A, const double* const* B, const int64_t* p, const int64_t* qa,
+                      const int64_t* qb, const int64_t* lda, const int64_t* ldb, double* const* C,
+                      const int64_t* ldc, int np, int L, void* const* workspace, cudaStream_t st) {
+  if (L < 14 || L > 15 || np < 1 || np > 2) return 1;
+  OzJob jobs[2];
+  OzHPlan hp[2];
+  uint8_t* ws[2];
+  for (int k = 0; k < np; ++k) {
+    const bool same = A[k] == B[k] && qa[k] == qb[k] && lda[k] == ldb[k];
+    hp[k] = oz_hplan(p[k], qa[k], qb[k], L, same);
+    ws[k] = reinterpret_cast<uint8_t*>(((uintptr_t)workspace[k] + 255) / 256 * 256);
+    const OzHPlan& h = hp[k];
+    uint8_t* wa = ws[k] + h.off_wa;
+    uint8_t* wb = same ? wa : ws[k] + h.off_wb;
+    int* exa = reinterpret_cast<int*>(ws[k] + h.off_exa);
+    int* exb = same ? exa : reinterpret_cast<int*>(ws[k] + h.off_exb);
+    oz_planes(A[k], p[k], qa[k], lda[k], L, h.g.bits, reinterpret_cast<unsigned long long*>(ws[k] + h.off_ca), exa,
+              wa, h.g.Kpitch, st);
+    if (!same)
+      oz_planes(B[k], p[k], qb[k], ldb[k], L, h.g.bits, reinterpret_cast<unsigned long long*>(ws[k] + h.off_cb), exb,
+                wb, h.g.Kpitch, st);
+    if (!oz_job(jobs[k], h.g, 4 * qa[k], wa, h.g.Kpitch, wb, L, ws[k] + h.off_res)) return 2;
+  }
+  oz_launch_gemm(jobs, np, L, st);
+  const OzCrt cc = oz_crt(L);
+  for (int k = 0; k < np; ++k) {
+    const OzHPlan& h = hp[k];
+    const bool same = A[k] == B[k] && qa[k] == qb[k] && lda[k] == ldb[k];
+    const int* exa = reinterpret_cast<int*>(ws[k] + h.off_exa);
+    const int* exb = same ? exa : reinterpret_cast<int*>(ws[k] + h.off_exb);
+    const unsigned blocks = (unsigned)((4 * qa[k] * qb[k] + 255) / 256);
+    const int64_t plane = 4 * qa[k] * h.g.Npitch;
+    ++::qcur::g_launches;
+    if (L == 14)
+      k_oz_hcrt<14><<<blocks, 256, 0, st>>>(ws[k] + h.off_res, qa[k], qb[k], h.g.Npitch, plane, exa, exb, cc, C[k],
+                                            ldc[k] * 4);
+    else
+      k_oz_hcrt<15><<<blocks, 256, 0, st>>>(ws[k] + h.off_res, qa[k], qb[k], h.g.Npitch, plane, exa, exb, cc, C[k],
+                                            ldc[k] * 4);
+  }
+  return 0;
 }
 
 }  // namespace qcur

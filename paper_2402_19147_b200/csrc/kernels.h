@@ -176,10 +176,13 @@ int launch_ozaki_prep_b(int64_t m, int64_t n, const double* B, int64_t r, int64_
                         cudaStream_t st);
 int launch_ozaki_multiply(int64_t m, int64_t n, int64_t r, double* Y, int64_t ldy, int L, void* workspace,
                           cudaStream_t st);
-// Hermitian Grams G_k = A_k^H A_k (A_k p_k x q_k) for up to two problems in one INT8 GEMM launch;
-// workspace[k] >= ozaki_workspace_bytes(q_k, p_k, q_k, L)
-int launch_ozaki_gram(const double* const* A, const int64_t* p, const int64_t* q, const int64_t* lda, double* const* G,
-                      const int64_t* ldg, int np, int L, void* const* workspace, cudaStream_t st);
+// C_k = A_k^H B_k (A_k p_k x qa_k, B_k p_k x qb_k; B_k == A_k allowed) for up to two problems in one
+// INT8 GEMM launch, by the 16 real plane products (no Hamilton expansion); ldc in quaternions
+size_t ozaki_herm_workspace_bytes(int64_t p, int64_t qa, int64_t qb, int same);
+bool ozaki_herm_supported(int64_t p, int64_t qa, int64_t qb);
+int launch_ozaki_herm(const double* const* A, const double* const* B, const int64_t* p, const int64_t* qa,
+                      const int64_t* qb, const int64_t* lda, const int64_t* ldb, double* const* C,
+                      const int64_t* ldc, int np, int L, void* const* workspace, cudaStream_t st);
 
 // k_ozaki_err.cu : the fused error ||X - P R|| (out4 as launch_cur_error) with P R on the INT8
 // tensor cores by exact base-256 digit slices (Ozaki scheme I, 21 digit products).

@@ -309,7 +309,7 @@ size_t factor_ws_bytes(int64_t p, int64_t q) {
   b += (w1 > w2 ? w1 : w2) + 4096;
   if (q > 304)  // blocked Cholesky scratch (chol_inv_blocked): A, L, blocks, T and its GEMM slabs
     b += 2 * qbytes(q, q) + 2 * qbytes(256, 256) + qbytes(256, q) + (size_t)16 * q * q * 8 + 8192;
-  if (ozaki_supported(q, p, q)) b += ozaki_workspace_bytes(q, p, q, kOzakiModuli) + 4096;  // INT8 Grams
+  if (ozaki_herm_supported(p, q, q)) b += ozaki_herm_workspace_bytes(p, q, q, 1) + 4096;  // INT8 Grams
   return b + 16 * 256;
 }
 
@@ -346,7 +346,7 @@ bool use_int8(const qcur_ctx* ctx, int64_t m, int64_t n, int64_t r) {
 
 // the Grams Z^H Z (Z: p x q) of CholeskyQR2 on the INT8 tensor cores?
 bool use_int8_gram(const qcur_ctx* ctx, int64_t p, int64_t q) {
-  if (ctx->gemm_mode == 1 || !ozaki_supported(q, p, q)) return false;
+  if (ctx->gemm_mode == 1 || !ozaki_herm_supported(p, q, q)) return false;
   return ctx->gemm_mode == 2 || (double)p * (double)q * (double)q >= 5e7;
 }
 
@@ -494,7 +494,7 @@ int factor_multi(qcur_ctx* ctx, const FactorSpec* specs_in, int ns) {
   if (i8gram)
     for (int k = 0; k < ns; ++k) {
       if (!fast[k]) continue;
-      gws8[k] = ctx->take<uint8_t>(ozaki_workspace_bytes(specs[k].q, specs[k].p, specs[k].q, kOzakiModuli));
+      gws8[k] = ctx->take<uint8_t>(ozaki_herm_workspace_bytes(specs[k].p, specs[k].q, specs[k].q, 1));
       if (!gws8[k]) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (int8 gram)");
     }
   // G = Z^H Z for every fast block (second: Z = Q1), INT8 or FP64 (paired launches either way)
@@ -517,7 +517,7 @@ int factor_multi(qcur_ctx* ctx, const FactorSpec* specs_in, int ns) {
         ++np;
       }
       if (np == 0) return QCUR_OK;
-      if (launch_ozaki_gram(A, pp, qq, lda, G, ldg, np, kOzakiModuli, w, st))
+      if (launch_ozaki_herm(A, A, pp, qq, qq, lda, lda, G, ldg, np, kOzakiModuli, w, st))
         return ctx->fail(QCUR_E_CUDA, "int8 gram: tensor map encode failed");
       CK_LAUNCH(ctx, "int8 gram");
       return QCUR_OK;
@@ -704,7 +704,7 @@ size_t qmcur_ws_bytes(int64_t m, int64_t n, int64_t c, int64_t r) {
     size_t a = qgemm_workspace_bytes(g1), d = qgemm_workspace_bytes(g2);
     b += (a > d ? a : d) + 4096;
     if (ozaki_supported(m, n, r)) b += ozaki_workspace_bytes(m, n, r, kOzakiModuli) + 4096;
-    if (ozaki_supported(c, m, r)) b += qbytes(c, m) + ozaki_workspace_bytes(c, m, r, kOzakiModuli) + 4096;  // Q_C^H Y
+    if (ozaki_herm_supported(m, c, r)) b += ozaki_herm_workspace_bytes(m, c, r, 0) + 4096;  // Q_C^H Y
   } else {
     b += pinv_ws_bytes(m, c) + pinv_ws_bytes(r, n) + qbytes(c, m) + qbytes(n, r) + qbytes(m, r);
     GemmArgs g1 = gargs(m, r, n, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0);
@@ -890,13 +890,15 @@ int qmcur_core(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, int64_t c, 
       return rc;
     }
     ctx->mark("gemm_xq");
-    // 5. M = Q_C^H Y (c x r): INT8 as (Q_C^H materialised) x Y when the engine is on
-    if (i8 && use_int8_gram(ctx, m, c) && ozaki_supported(c, m, r)) {
-      double* QCH = ctx->take<double>((size_t)(c * m * 4));
-      void* ws2 = ctx->take<uint8_t>(ozaki_workspace_bytes(c, m, r, kOzakiModuli));
-      if (!QCH || !ws2) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (int8 Q_C^H Y)");
-      launch_conj_transpose(QC, m, c, c, QCH, m, st);
-      if (launch_ozaki_gemm(QCH, c, m, m, Y, r, r, M, r, kOzakiModuli, ws2, st))
+    // 5. M = Q_C^H Y (c x r): INT8 Hermitian product (plane products) when the engine is on
+    if (i8 && use_int8_gram(ctx, m, c) && ozaki_herm_supported(m, c, r)) {
+      void* ws2 = ctx->take<uint8_t>(ozaki_herm_workspace_bytes(m, c, r, 0));
+      if (!ws2) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (int8 Q_C^H Y)");
+      const double* A1 = QC;
+      const double* B1 = Y;
+      double* C1 = M;
+      const int64_t p1 = m, qa1 = c, qb1 = r, lda1 = c, ldb1 = r, ldc1 = r;
+      if (launch_ozaki_herm(&A1, &B1, &p1, &qa1, &qb1, &lda1, &ldb1, &C1, &ldc1, 1, kOzakiModuli, &ws2, st))
         return ctx->fail(QCUR_E_CUDA, "int8 Q_C^H Y: tensor map encode failed");
       CK_LAUNCH(ctx, "int8 Q_C^H Y");
     } else if ((rc = gemm(ctx, gargs(c, r, m, QC, c, 1, Y, r, 0, M, r), gws))) {
@@ -1693,6 +1695,22 @@ int qcur_qsvd_jacobi(qcur_ctx* ctx, const double* a, int64_t m, int64_t n, int64
 int qcur_set_gemm_mode(qcur_ctx* ctx, int mode) {
   if (mode < 0 || mode > 2) return ctx->fail(QCUR_E_PARAMETER, "gemm mode must be 0 (auto), 1 (fp64) or 2 (int8)");
   ctx->gemm_mode = mode;
+  return QCUR_OK;
+}
+
+int qcur_qgemm_herm_int8(qcur_ctx* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                         const double* B, int64_t ldb, double* C, int64_t ldc) {
+  if (M < 1 || N < 1 || K < 1 || !ozaki_herm_supported(K, M, N))
+    return ctx->fail(QCUR_E_SHAPE, "qgemm_herm_int8: bad shape");
+  const int same = A == B && M == N && lda == ldb;
+  const size_t wsb = ozaki_herm_workspace_bytes(K, M, N, same);
+  int rc = ctx->reserve(wsb + 4096);
+  if (rc) return rc;
+  void* ws = ctx->take<uint8_t>(wsb);
+  if (!ws) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (qgemm_herm_int8)");
+  if (launch_ozaki_herm(&A, &B, &K, &M, &N, &lda, &ldb, &C, &ldc, 1, kOzakiModuli, &ws, ctx->stream))
+    return ctx->fail(QCUR_E_CUDA, "qgemm_herm_int8: tensor map encode failed");
+  CK_LAUNCH(ctx, "qgemm_herm_int8");
   return QCUR_OK;
 }
 

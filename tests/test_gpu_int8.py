@@ -192,3 +192,35 @@ def test_int8_error_u8_image_statistic():
     # integer sums of squared u8 differences; a rint() at an exact half-way point may differ
     assert abs(s8[3] - s64[3]) <= 4.0 * max(1.0, 1e-9 * s64[3])
     assert abs(s8[0] - s64[0]) <= 1e-12 * s64[0]
+
+
+def ref_herm(a, b):
+    """A^H B for (p, qa, 4) and (p, qb, 4) in long double."""
+    x = np.transpose(a.astype(np.longdouble), (1, 0, 2)).copy()
+    x[:, :, 1:] *= -1  # conj(A)^T as a qa x p quaternion matrix
+    bl = b.astype(np.longdouble)
+    y = np.zeros((x.shape[0], b.shape[1], 4), dtype=np.longdouble)
+    for t in range(4):
+        for s in range(4):
+            y[:, :, t] += SIGNS[t][s] * (x[:, :, s] @ bl[:, :, s ^ t])
+    return y
+
+
+@pytest.mark.parametrize("p,qa,qb,same", [(40, 7, 7, True), (300, 40, 40, True), (257, 33, 20, False),
+                                          (1000, 64, 64, True), (4000, 50, 30, False), (5, 1, 1, False)])
+def test_int8_hermitian_product(p, qa, qb, same):
+    g = np.random.default_rng(p + qa + qb)
+    a = g.standard_normal((p, qa, 4))
+    b = a if same else g.standard_normal((p, qb, 4))
+    dev = _native.device()
+    da = torch.from_numpy(a).cuda()
+    db = da if same else torch.from_numpy(b).cuda()
+    c8 = dev.empty_q(qa, qb)
+    dev.call("qcur_qgemm_herm_int8", qa, qb, p, da.data_ptr(), qa, db.data_ptr(), qb, c8.data_ptr(), qb)
+    cd = dev.empty_q(qa, qb)
+    dev.call("qcur_qgemm", 1, 0, qa, qb, p, 1.0, da.data_ptr(), qa, db.data_ptr(), qb, 0.0, cd.data_ptr(), qb)
+    ref = ref_herm(a, b)
+    scale = np.sqrt((a ** 2).sum(axis=(0, 2)))[:, None] * np.sqrt((b ** 2).sum(axis=(0, 2)))[None, :]
+    e8 = float((np.abs(c8.cpu().numpy() - ref).max(axis=2) / scale).max())
+    ed = float((np.abs(cd.cpu().numpy() - ref).max(axis=2) / scale).max())
+    assert e8 <= max(20 * ed, 4e-15), (e8, ed)
