@@ -176,7 +176,6 @@ struct OeParams {
   double psnr_scale;
   int kblocks, mblocks, nblocks, total;
   uint32_t idesc;
-  int experiment;  // timing experiments only (QCUR_OE_EXPERIMENT): 1 = release TMEM at once
 };
 
 __global__ void __launch_bounds__(OE_THREADS, 1)
@@ -286,11 +285,6 @@ __global__ void __launch_bounds__(OE_THREADS, 1)
       double pr[QW][4];
       mbar_wait(tfull, (unsigned)t & 1u);
       tc_fence_after();
-      if (P.experiment == 1) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(tempty);
-        continue;
-      }
 #pragma unroll
       for (int i = 0; i < QW; ++i) {
         uint32_t lv[6][4];
@@ -476,7 +470,6 @@ int launch_ozaki_error_gemm(const double* X, int64_t ldx, int64_t m, int64_t n, 
   p.eb = eb;
   p.partials = parts;
   p.psnr_scale = psnr_scale;
-  if (const char* ex = std::getenv("QCUR_OE_EXPERIMENT")) p.experiment = std::atoi(ex);
   p.kblocks = pl.kblocks;
   p.mblocks = pl.mblocks;
   p.nblocks = pl.nblocks;
