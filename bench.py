@@ -524,15 +524,39 @@ def main() -> None:
     psnr_scale = 255.0 if cfg.get("image") else 0.0
 
     use_graph = batch == 1 and not os.environ.get("QCUR_NO_GRAPH")
+    # Throughput with several independent approximations in flight (single-matrix configs): each
+    # lane has its own native context, stream and resident input (a second matrix of the same
+    # workload, its own generator seed), so one approximation's latency-bound phases (draws,
+    # Cholesky) overlap another's tensor-bound ones.  QCUR_INFLIGHT=1 gives the serial number.
+    inflight = int(os.environ.get("QCUR_INFLIGHT", "2")) if batch == 1 else 1
+    lanes = [(dev, outs, xs, torch.cuda.current_stream())]
+    for k in range(1, inflight):
+        dk = _native.Device(local)
+        xk = dk.empty_q(m, n)
+        if cfg.get("image"):
+            dk.call("qcur_synth_image", m, n, 30, cfg["gen_seed"] + 7919 * rank + 104729 * k, cfg["noise"],
+                    xk.data_ptr())
+        else:
+            dk.call("qcur_synth_lowrank", m, n, cfg["rank"], cfg["gen_seed"] + 7919 * rank + 104729 * k, cfg["noise"],
+                    1 if cfg["relative"] else 0, xk.data_ptr())
+        lanes.append((dk, DeviceApprox(m, n, c, r, dk), [xk], torch.cuda.Stream(local)))
+    lane_pos = [0]
 
     def step(graph=use_graph):
-        for x, b in zip(xs, mine):
-            outs.run(x, cfg["strategy"], cfg["plan_seed"] + b, psnr_scale, graph=graph)
+        d_, o_, xs_, st_ = lanes[lane_pos[0] % len(lanes)]
+        lane_pos[0] += 1
+        with torch.cuda.stream(st_):
+            for x, b in zip(xs_, mine):
+                o_.run(x, cfg["strategy"], cfg["plan_seed"] + b, psnr_scale, graph=graph)
+
+    def replayed():
+        return sum(getattr(o_, "graph_replays", 0) * getattr(o_, "graph_kernels", 0) for _, o_, _, _ in lanes)
 
     stream = torch.cuda.current_stream()
-    for _ in range(max(args.warmup, 3)):
+    for _ in range(max(args.warmup, 3) * len(lanes)):
         step()
-    outs.check()
+    for _, o_, _, _ in lanes:
+        o_.check()
     torch.cuda.synchronize()
 
     # --- timed region: device-resident value ---
@@ -540,20 +564,25 @@ def main() -> None:
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    l0 = dev.launches() + getattr(outs, "graph_replays", 0) * getattr(outs, "graph_kernels", 0)
+    l0 = dev.launches() + replayed()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     with sampler:
         e0.record(stream)
+        for _, _, _, st_ in lanes[1:]:
+            st_.wait_event(e0)
         for _ in range(args.steps):
             step()
+        for _, _, _, st_ in lanes[1:]:
+            stream.wait_stream(st_)
         e1.record(stream)
         torch.cuda.synchronize()
     # kernels launched in the timed region: direct launches plus the kernels of every graph replay
-    launches = dev.launches() + getattr(outs, "graph_replays", 0) * getattr(outs, "graph_kernels", 0) - l0
+    launches = dev.launches() + replayed() - l0
     if world > 1:
         dist.barrier()
-    outs.check()
+    for _, o_, _, _ in lanes:
+        o_.check()
     ms_total = e0.elapsed_time(e1)
     t = torch.tensor([ms_total], dtype=torch.float64, device=f"cuda:{local}")
     if world > 1:
@@ -563,6 +592,18 @@ def main() -> None:
     # units completed by all ranks together / slowest rank's time
     value = (args.steps * batch if batch > 1 else world * args.steps) / (ms_total / 1e3)
     rel_err = outs.rel_error()
+    # the same loop with one approximation in flight (reported beside the headline)
+    serial = None
+    if len(lanes) > 1:
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        s0.record(stream)
+        for _ in range(args.steps):
+            outs.run(xs[0], cfg["strategy"], cfg["plan_seed"], psnr_scale, graph=use_graph)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        serial = args.steps / (s0.elapsed_time(s1) / 1e3)
 
     # --- phase breakdown (events between phases, same stream), separate pass ---
     dev.profile(True)
@@ -730,7 +771,12 @@ def main() -> None:
                        if m * n * 32 > 126e6
                        else "input fits in L2; repeated on the same resident matrix",
                        "launch": "one CUDA graph replay per approximation (captured from the same ABI call)"
-                       if use_graph else "direct stream launches"},
+                       if use_graph else "direct stream launches",
+                       "inflight": len(lanes),
+                       "inflight_note": "approximations in flight: independent resident inputs of this workload, "
+                                        "one native context and stream each, steps round-robin over them; "
+                                        "value_serial is the same loop with one in flight"},
+            "value_serial": serial,
             "gpu_launches": launches, "rel_err": rel_err,
             "psnr": (dict(zip(("u8_db", "float_peak1_db"), outs.psnr())) if psnr_scale else None),
             "roofline": roofline, "step_roofline": step_roof,
