@@ -450,7 +450,8 @@ def run_qsvd(args) -> None:
         "e2e": {"value": steps / el, "unit": "qsvd/s", "api": "qsvd(x, k) on a host QMatrix (upload, Jacobi sweeps, "
                 "W / sigma / V download inside the timed region)", "h2d_bytes_per_step": 32 * m * n,
                 "d2h_bytes_per_step": 32 * (m * n + n * n) + 8 * n},
-        "reconstruction_rel_err": recon_err, "clocks": sampler.summary(), "cpu_baseline": cpu,
+        "reconstruction_rel_err": recon_err, "jacobi_sweeps": q.linalg._last_sweeps, "clocks": sampler.summary(),
+        "cpu_baseline": cpu,
     }))
 
 

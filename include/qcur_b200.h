@@ -213,6 +213,12 @@ int qcur_qgemm_ex(qcur_ctx* ctx, int opA, int opB, int64_t M, int64_t N, int64_t
    nullable) receives V.  sweeps_out (nullable): Jacobi sweeps used. */
 int qcur_qsvd_jacobi(qcur_ctx* ctx, const double* a_dev, int64_t m, int64_t n, int64_t lda, double* acm_dev,
                      double* vcm_dev, double* sigma_dev, int* sweeps_out);
+/* Truncated variant for qsvd(x, k) (linalg.py:226-310): same outputs, but with 0 < k < n the sweeps
+   stop as soon as the k largest columns of A V are certified to be singular triplets (each orthogonal
+   to every other column to max(4, sqrt(m)) eps relative; the rest's Frobenius norm at most half the k-th
+   largest).  k = 0 or k = n: full convergence, as qcur_qsvd_jacobi. */
+int qcur_qsvd_jacobi_top(qcur_ctx* ctx, const double* a_dev, int64_t m, int64_t n, int64_t lda, double* acm_dev,
+                         double* vcm_dev, double* sigma_dev, int64_t k, int* sweeps_out);
 /* Engine of the X Q_R contraction inside qmcur: 0 auto (INT8 when large), 1 FP64 DMMA, 2 INT8 (Ozaki II).
    The environment variable QCUR_GEMM=dmma|int8 sets the initial mode of new contexts. */
 int qcur_set_gemm_mode(qcur_ctx* ctx, int mode);

@@ -46,7 +46,7 @@ EXPORTS = (
     "qcur_frobenius_sq", "qcur_synth_lowrank", "qcur_fp64_peak_tflops", "qcur_int8_peak_tops",
     "qcur_profile", "qcur_profile_read", "qcur_launch_count", "qcur_pairwise_host", "qcur_synth_image",
     "qcur_colsums_seq", "qcur_pairwise_sums", "qcur_vec_div", "qcur_gather_cols", "qcur_gather_rows",
-    "qcur_qgemm_ex", "qcur_qgemm_int8", "qcur_qgemm_herm_int8", "qcur_set_gemm_mode", "qcur_qsvd_jacobi", "qcur_chol_inv", "qcur_series_l2inv", "qcur_kappa_check", "qcur_factor",
+    "qcur_qgemm_ex", "qcur_qgemm_int8", "qcur_qgemm_herm_int8", "qcur_set_gemm_mode", "qcur_qsvd_jacobi", "qcur_qsvd_jacobi_top", "qcur_chol_inv", "qcur_series_l2inv", "qcur_kappa_check", "qcur_factor",
     "qcur_synth_lowrank_rows", "qcur_qmcur_ex", "qcur_qmcur_host",
     "qcur_project_observed", "qcur_complete_sweep", "qcur_cur_given", "qcur_qgemv",
     "qcur_upload_length", "qcur_status_async", "qcur_status_map",
@@ -140,6 +140,8 @@ def load_library() -> ctypes.CDLL:
             "qcur_set_gemm_mode": (ctypes.c_int, [_c_dp, ctypes.c_int]),
             "qcur_qsvd_jacobi": (ctypes.c_int, [_c_dp, _c_dp, _i64, _i64, _i64, _c_dp, _c_dp, _c_dp,
                                                 ctypes.POINTER(ctypes.c_int)]),
+            "qcur_qsvd_jacobi_top": (ctypes.c_int, [_c_dp, _c_dp, _i64, _i64, _i64, _c_dp, _c_dp, _c_dp, _i64,
+                                                    ctypes.POINTER(ctypes.c_int)]),
             "qcur_qgemm_herm_int8": (ctypes.c_int, [_c_dp, _i64, _i64, _i64, _c_dp, _i64, _c_dp, _i64, _c_dp, _i64]),
             "qcur_qgemm_int8": (ctypes.c_int, [_c_dp, _i64, _i64, _i64, _c_dp, _i64, _c_dp, _i64, _c_dp, _i64,
                                                 ctypes.c_int]),

@@ -144,8 +144,11 @@ void launch_rowmajor_to_colmajor(const double* Z, int64_t p, int64_t q, int64_t 
 // k_qsvd.cu : quaternion one-sided Jacobi SVD (column-major A m x n with m >= n, V n x n)
 void launch_to_colmajor(const double* A, int64_t m, int64_t n, int64_t lda, double* Acm, cudaStream_t st);
 void launch_identity_cm(double* Vcm, int64_t n, cudaStream_t st);
+int64_t jacobi_sweep_rounds(int64_t m, int64_t n);
 void launch_jacobi_round(double* Acm, int64_t m, int64_t n, double* Vcm, int64_t rnd, unsigned* flag, cudaStream_t st);
 void launch_col_norms(const double* Acm, int64_t m, int64_t n, double* sigma, cudaStream_t st);
+void launch_jacobi_cert(const double* Acm, int64_t m, int64_t n, const int* top, int k, const double* sigma,
+                        unsigned* flag, cudaStream_t st);
 
 // k_synth.cu : synthetic workloads (Philox normal generator)
 // offset: element offset (even) of this block within the whole generated array

@@ -7,6 +7,7 @@
 #include <cstring>
 #include <map>
 #include <string>
+#include <algorithm>
 #include <vector>
 
 #include "../../include/qcur_b200.h"
@@ -1663,33 +1664,71 @@ int qcur_qgemm_ex(qcur_ctx* ctx, int opA, int opB, int64_t M, int64_t N, int64_t
 // Quaternion SVD by one-sided Jacobi (qsvd, linalg.py:226-310): A (m x n, m >= n, row pitch lda)
 // is copied column-major into acm and rotated until its columns are orthogonal; then
 // A V = acm (columns a_j with ||a_j|| = sigma_j), V (n x n column-major, nullable) orthonormal.
-int qcur_qsvd_jacobi(qcur_ctx* ctx, const double* a, int64_t m, int64_t n, int64_t lda, double* acm, double* vcm,
-                     double* sigma, int* sweeps_out) {
+//
+// Truncated (0 < k < n): the sweeps may stop before the whole matrix has converged, once the k
+// columns of largest norm are certified: every one of them is orthogonal, to the rounding level
+// of an inner product (sqrt(m) eps, relative), to every other column (measured directly, k_jac_cert), and the other columns'
+// Frobenius norm is at most half the k-th largest column norm, so the remaining block cannot
+// hold a singular value that belongs in the top k.  Those k columns then are singular triplets
+// to the same accuracy as after full convergence (qsvd(x, k) returns only them).
+int qcur_qsvd_jacobi_top(qcur_ctx* ctx, const double* a, int64_t m, int64_t n, int64_t lda, double* acm,
+                         double* vcm, double* sigma, int64_t k, int* sweeps_out) {
   if (m < 1 || n < 1 || m < n) return ctx->fail(QCUR_E_SHAPE, "qsvd_jacobi: need m >= n >= 1");
-  int rc = ctx->reserve(4096);
+  if (k < 0 || k > n) return ctx->fail(QCUR_E_PARAMETER, "qsvd_jacobi: need 0 <= k <= n");
+  const bool trunc = k > 0 && k < n;
+  int rc = ctx->reserve(4096 + (trunc ? (size_t)k * sizeof(int) : 0));
   if (rc) return rc;
   unsigned* flag = ctx->take<unsigned>(16);
-  if (!flag) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (qsvd)");
+  int* top_dev = trunc ? ctx->take<int>(k) : nullptr;
+  if (!flag || (trunc && !top_dev)) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (qsvd)");
   cudaStream_t st = ctx->stream;
   launch_to_colmajor(a, m, n, lda, acm, st);
   if (vcm) launch_identity_cm(vcm, n, st);
   CK_LAUNCH(ctx, "qsvd setup");
-  const int64_t nn = n + (n & 1);
+  const int64_t rounds = jacobi_sweep_rounds(m, n);
+  std::vector<double> norms(trunc ? n : 0);
+  std::vector<int> order(trunc ? n : 0);
   int sweep = 0;
   for (; sweep < 60 && n > 1; ++sweep) {
     cudaMemsetAsync(flag, 0, sizeof(unsigned), st);
-    for (int64_t rnd = 0; rnd < nn - 1; ++rnd) launch_jacobi_round(acm, m, n, vcm, rnd, flag, st);
+    for (int64_t rnd = 0; rnd < rounds; ++rnd) launch_jacobi_round(acm, m, n, vcm, rnd, flag, st);
     CK_LAUNCH(ctx, "jacobi round");
     unsigned h = 0;
     cudaError_t e = cudaMemcpyAsync(&h, flag, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && trunc) {
+      launch_col_norms(acm, m, n, sigma, st);
+      e = cudaMemcpyAsync(norms.data(), sigma, n * sizeof(double), cudaMemcpyDeviceToHost, st);
+    }
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return ctx->cuda_fail(e, "qsvd sweep");
+    if (!h) break;
+    if (!trunc) continue;
+    for (int64_t j = 0; j < n; ++j) order[j] = (int)j;
+    std::partial_sort(order.begin(), order.begin() + k, order.end(),
+                      [&](int x, int y) { return norms[x] > norms[y] || (norms[x] == norms[y] && x < y); });
+    const double kth = norms[order[k - 1]];
+    double rest = 0.0;
+    for (int64_t j = k; j < n; ++j) rest += norms[order[j]] * norms[order[j]];
+    if (!(kth > 0.0) || !(rest <= 0.25 * kth * kth)) continue;
+    e = cudaMemcpyAsync(top_dev, order.data(), k * sizeof(int), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(flag, 0, sizeof(unsigned), st);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "qsvd certificate");
+    launch_jacobi_cert(acm, m, n, top_dev, (int)k, sigma, flag, st);
+    CK_LAUNCH(ctx, "qsvd certificate");
+    e = cudaMemcpyAsync(&h, flag, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "qsvd certificate");
     if (!h) break;
   }
   launch_col_norms(acm, m, n, sigma, st);
   CK_LAUNCH(ctx, "qsvd norms");
   if (sweeps_out) *sweeps_out = sweep + 1;
   return QCUR_OK;
+}
+
+int qcur_qsvd_jacobi(qcur_ctx* ctx, const double* a, int64_t m, int64_t n, int64_t lda, double* acm, double* vcm,
+                     double* sigma, int* sweeps_out) {
+  return qcur_qsvd_jacobi_top(ctx, a, m, n, lda, acm, vcm, sigma, 0, sweeps_out);
 }
 
 int qcur_set_gemm_mode(qcur_ctx* ctx, int mode) {

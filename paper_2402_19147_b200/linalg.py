@@ -159,9 +159,13 @@ class QSVDResult:
         return self.w.scale_columns(self.sigma) @ self.v.conj_transpose()
 
 
-def _jacobi(a, want_v: bool):
+_last_sweeps = 0  # sweeps of the last Jacobi run (diagnostics)
+
+
+def _jacobi(a, want_v: bool, k: int = 0):
     """One-sided Jacobi on the device for a (m x n, m >= n): returns (AV columns (n, m, 4),
-    V columns (n, n, 4) or None, sigma (n,)) as host arrays, columns unsorted."""
+    V columns (n, n, 4) or None, sigma (n,)) as host arrays, columns unsorted.  0 < k < n: only
+    the k largest columns are guaranteed converged (qcur_qsvd_jacobi_top)."""
     dev = _native.device()
     m, n = (int(v) for v in a.shape)
     ad = to_device(a, dev)
@@ -169,8 +173,10 @@ def _jacobi(a, want_v: bool):
     vcm = dev.empty(n, n, 4) if want_v else None
     sig = dev.empty(n)
     sweeps = ctypes.c_int()
-    dev.call("qcur_qsvd_jacobi", ad.data_ptr(), m, n, n, acm.data_ptr(), vcm.data_ptr() if want_v else None,
-             sig.data_ptr(), ctypes.byref(sweeps))
+    dev.call("qcur_qsvd_jacobi_top", ad.data_ptr(), m, n, n, acm.data_ptr(), vcm.data_ptr() if want_v else None,
+             sig.data_ptr(), int(k), ctypes.byref(sweeps))
+    global _last_sweeps
+    _last_sweeps = sweeps.value
     return acm.cpu().numpy(), (vcm.cpu().numpy() if want_v else None), sig.cpu().numpy()
 
 
@@ -231,7 +237,7 @@ def qsvd(a, k: int | None = None) -> QSVDResult:
     tall = m >= n
     src = a if tall else QMatrix._wrap(*_planes_conj_t(a))
     p, q = (m, n) if tall else (n, m)  # src is p x q, p >= q
-    av, vc, sig = _jacobi(src, True)
+    av, vc, sig = _jacobi(src, True, k)
     order = np.argsort(-sig, kind="stable")
     sig = sig[order]
     smax = float(sig[0]) if sig.size else 0.0

@@ -123,3 +123,29 @@ def test_perturbation_bounds_errors():
         q.perturbation_bounds(X, E, rows, cols, 4)  # numerical rank is 3
     with pytest.raises(q.ParameterError):
         q.perturbation_bounds(X, E, rows[:2], cols, 3)
+
+
+def test_qsvd_truncated_early_stop_matches_full():
+    """qsvd(x, k) may stop once the top k columns are certified (qcur_qsvd_jacobi_top); the
+    triplets must agree with the fully converged decomposition."""
+    g = np.random.default_rng(41)
+    m, n, r = 160, 120, 6
+    pf = q.QMatrix(*(g.standard_normal((m, r)) for _ in range(4)))
+    qf = q.QMatrix(*(g.standard_normal((r, n)) for _ in range(4)))
+    s = pf @ qf
+    x = q.QMatrix(*(p + 1e-4 * g.standard_normal((m, n)) for p in s.planes))
+    full = q.qsvd(x)
+    sw_full = q.linalg._last_sweeps
+    for k in (1, 3, 6):
+        part = q.qsvd(x, k)
+        sw_part = q.linalg._last_sweeps
+        assert sw_part <= sw_full
+        assert np.allclose(part.sigma, full.sigma[:k], rtol=1e-12, atol=0)
+        assert orth_defect(part.w) < 1e-12 and orth_defect(part.v) < 1e-12
+        # same rank-k truncation (singular vectors up to a unit quaternion phase per column)
+        wk = q.QMatrix(*(p[:, :k].copy() for p in full.w.planes))
+        vk = q.QMatrix(*(p[:, :k].copy() for p in full.v.planes))
+        assert rel_fro_err(part.reconstruct(), q.QSVDResult(wk, full.sigma[:k], vk).reconstruct()) < 1e-10
+    assert q.linalg._last_sweeps < sw_full  # k = 6 (the signal rank) stops early
+    s_ref = O.singular_values(tuple(x.planes))
+    assert np.allclose(q.qsvd(x, 6).sigma, s_ref[:6], rtol=1e-10)
