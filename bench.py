@@ -610,7 +610,12 @@ def main() -> None:
     dev.profile(True)
     nprof = min(args.steps, 10)
     for _ in range(nprof):
-        step(graph=False)  # phase marks are events between direct launches
+        # one approximation at a time on lane 0 (no other lane in flight), so each phase is timed
+        # alone; phase marks are events between direct launches
+        with torch.cuda.stream(lanes[0][3]):
+            for x, b in zip(xs, mine):
+                outs.run(x, cfg["strategy"], cfg["plan_seed"] + b, psnr_scale, graph=False)
+        torch.cuda.synchronize()
     phases = dev.profile_read()
     dev.profile(False)
     per_approx = {k: v[0] / max(v[1], 1) for k, v in phases.items()}

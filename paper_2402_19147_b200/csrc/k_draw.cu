@@ -6,15 +6,24 @@
 // walks back over zero weights, records the index and zeroes its weight.
 //
 // Device design: one CTA per axis (columns and rows run concurrently).  The
-// CTA copies p and builds a 32-ary sum tree over it; one warp then performs
-// the `count` draws, each a root-to-leaf descent of warp scans (O(log32 n)
-// per draw instead of an O(n) cumsum).  The descent's prefix values differ
-// from numpy's sequential cumsum only by rounding, bounded by
-// (n + 70) * 2^-53 * total; a draw is accepted only when the uniform sits
-// farther than twice that bound from both neighbouring prefix values, which
-// proves the numpy index.  Drawn weights leave the tree by subtraction along the
-// path (the margin grows by the per-draw rounding).  Otherwise (probability ~1e-12 per draw) the lane
-// recomputes the exact sequential cumsum — numpy's own order — for that draw.
+// CTA builds a 64-ary PREFIX tree over p: node k of level h holds, for its 64
+// children, the inclusive prefix sums of their totals (every level padded with
+// zeros to a multiple of 64, so a node is one aligned 512-byte run).  One warp
+// then performs the `count` draws; each is a root-to-leaf descent in which
+// every lane loads two adjacent prefix values (one 16-byte load) and a pair of
+// ballots finds the first prefix above the uniform: no scan on the dependent
+// chain, and a 4000-long axis is two levels deep.  A drawn weight leaves the
+// tree by subtracting it from the prefix entries at and after its position in
+// each node of its path, using the values the descent already holds (stores
+// only, all levels independent).  The level pointers and sizes are
+// compile-time-indexed registers (fully unrolled level loops).
+// The descent's prefix values differ from numpy's sequential cumsum only by
+// rounding, bounded by (n + 70) * 2^-53 * total plus one rounding per level
+// and earlier removal; a draw is accepted only when the uniform sits farther
+// than twice that bound from both neighbouring prefix values, which proves
+// the numpy index.  Otherwise (probability ~1e-12 per draw) lane 0 recomputes
+// the exact sequential cumsum — numpy's own order — over the exact weights
+// (a global copy of p with the drawn entries zeroed) for that draw.
 // The PCG64 stream is advanced on device (pcg64.h), one double per draw.
 #include "common.cuh"
 #include "kernels.h"
@@ -22,95 +31,91 @@
 
 namespace qcur {
 
-constexpr int kMaxLevels = 8;
+constexpr int kFan = 64;                    // children per node: two per lane
+constexpr int kMaxL = 5;                    // 64^5 leaves: any axis length up to 2^30
 constexpr int64_t kDrawSmemMaxLen = 24576;  // p (+ its tree) fits the 224 KB dynamic shared memory cap
 
-struct Levels {
-  double* lev[kMaxLevels];
-  int64_t sz[kMaxLevels];
-  int top;  // index of the top level (sz[top] <= 32)
+__host__ __device__ inline int64_t rup64(int64_t x) { return (x + kFan - 1) / kFan * kFan; }
+
+struct Tree {
+  int top;             // index of the top level (sz[top] <= 64)
+  int64_t sz[kMaxL];   // entries per level
+  int64_t off[kMaxL];  // offsets of levels >= 1 in the upper-level buffer (each padded to 64)
+  int64_t upper;       // doubles of the upper-level buffer
+  int64_t root;        // offset of the top level in the upper-level buffer (top >= 1)
 };
 
-__host__ __device__ inline Levels make_levels(double* work, int64_t len) {
-  Levels L;
-  int64_t off = 0;
-  int64_t s = len;
-  int h = 0;
-  L.lev[0] = work;
-  L.sz[0] = len;
-  off = len;
-  while (s > 32 && h + 1 < kMaxLevels) {
-    s = (s + 31) / 32;
-    ++h;
-    L.lev[h] = work + off;
-    L.sz[h] = s;
-    off += s;
+__host__ __device__ inline Tree make_tree(int64_t len) {
+  Tree T;
+  int64_t s = len, off = 0;
+  T.top = 0;
+  T.sz[0] = len;
+  T.off[0] = 0;
+  // fully unrolled (static indices keep the tree in registers)
+#pragma unroll
+  for (int k = 1; k < kMaxL; ++k) {
+    T.off[k] = off;
+    if (s > kFan) {
+      s = (s + kFan - 1) / kFan;
+      T.top = k;
+      T.sz[k] = s;
+      off += rup64(s);
+    } else {
+      T.sz[k] = 0;
+    }
   }
-  L.top = h;
-  return L;
+  T.upper = off;
+  T.root = T.top >= 1 ? off - kFan : 0;  // the top level is one node, allocated last
+  return T;
 }
 
-// work buffer: p (len) | tree levels | 64 slack | uniforms (count <= len)
-__host__ __device__ inline int64_t draw_uniform_offset(int64_t len) {
-  int64_t total = len, s = len;
-  while (s > 32) {
-    s = (s + 31) / 32;
-    total += s;
-  }
-  return total + 64;
-}
+// global work buffer: exact weights p (zeroed as drawn; the fallback's cumsum) | the
+// level-0 prefix entries when they do not fit shared memory | uniforms
+int64_t draw_work_doubles(int64_t len) { return 2 * rup64(len) + len + 64; }
 
-int64_t draw_work_doubles(int64_t len) { return draw_uniform_offset(len) + len; }
-
-// recompute node `node` of level h (h >= 1) from its 32 children; called by a full warp
-__device__ __forceinline__ void refresh_node(const Levels& L, int h, int64_t node, int lane) {
-  const int64_t c = node * 32 + lane;
-  double v = c < L.sz[h - 1] ? L.lev[h - 1][c] : 0.0;
-  v = warp_sum(v);
-  if (lane == 0) L.lev[h][node] = v;
-  __syncwarp();
+// shared memory: level-0 prefixes (when they fit) | levels >= 1 | two node-total buffers
+static int64_t draw_smem_doubles(int64_t len) {
+  const Tree T = make_tree(len);
+  const int64_t nodes0 = rup64((len + kFan - 1) / kFan);
+  return (len <= kDrawSmemMaxLen ? rup64(len) : 0) + T.upper + 2 * nodes0;
 }
 
 struct DrawJobs {
   DrawJob j[2];
 };
 
-__global__ void __launch_bounds__(1024) k2_draw(DrawJobs jobs, unsigned* status) {
+// kLeafSmem: the level-0 prefixes live in shared memory (every job's axis is at most
+// kDrawSmemMaxLen long), so all tree accesses compile to shared-memory loads
+template <bool kLeafSmem>
+__global__ void __launch_bounds__(512, 1) k2_draw(DrawJobs jobs, unsigned* status) {
   const DrawJob job = jobs.j[blockIdx.x];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int64_t len = job.len;
-  // The weights and the sum tree live in shared memory (a draw is a chain of
-  // dependent probes: ~30-cycle smem latency instead of ~600-cycle L2); for
-  // very long axes only the tree does and p stays in the global work buffer.
-  extern __shared__ double sm_draw[];
-  Levels L = make_levels(job.work, len);
-  {
-    const bool p_in_smem = len <= kDrawSmemMaxLen;
-    double* base = p_in_smem ? sm_draw : sm_draw - len;  // tree always follows p's slot in smem
-    Levels S = make_levels(base, len);
-    if (!p_in_smem) S.lev[0] = job.work;
-    L = S;
-  }
-  // copy p and count positives
+  const Tree T = make_tree(len);
+  extern __shared__ __align__(16) double sm_draw[];
+  constexpr bool p_in_smem = kLeafSmem;
+  double* P[kMaxL];
+  P[0] = p_in_smem ? sm_draw : job.work + rup64(len);
+  double* up = p_in_smem ? sm_draw + rup64(len) : sm_draw;
+#pragma unroll
+  for (int h = 1; h < kMaxL; ++h) P[h] = up + T.off[h];
+  const int64_t nodes0 = rup64((len + kFan - 1) / kFan);
+  double* Sb[2] = {up + T.upper, up + T.upper + nodes0};
+  double* pw = job.work;  // exact weights
+  double* uni = job.work + 2 * rup64(len);
+  // exact weights (zero padded) and the count of positives
   __shared__ int s_pos[32];
   int pos = 0;
-  for (int64_t t = tid; t < len; t += blockDim.x) {
-    double v = job.probs[t];
-    L.lev[0][t] = v;
+  for (int64_t t = tid; t < rup64(len); t += blockDim.x) {
+    const double v = t < len ? job.probs[t] : 0.0;
+    pw[t] = v;
     pos += v > 0.0;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) pos += __shfl_xor_sync(0xffffffffu, pos, o);
   if (lane == 0) s_pos[warp] = pos;
-  __syncthreads();
-  // build the sum tree (all warps)
-  for (int h = 1; h <= L.top; ++h) {
-    for (int64_t node = warp; node < L.sz[h]; node += nw) refresh_node(L, h, node, lane);
-    __syncthreads();
-  }
   // the draw's uniforms: uniform t is the stream advanced by t (numpy draws one
   // double per draw, columns first), computed in parallel instead of in the chain
-  double* uni = job.work + draw_uniform_offset(len);
   for (int64_t t = tid; t < job.count; t += blockDim.x) {
     Pcg64 g;
     g.state = u128{job.st_hi, job.st_lo};
@@ -119,6 +124,31 @@ __global__ void __launch_bounds__(1024) k2_draw(DrawJobs jobs, unsigned* status)
     uni[t] = g.next_double();
   }
   __syncthreads();
+  // prefix tree, level by level: a warp per node scans its 64 children (pair sums, then a
+  // fixed-order Hillis-Steele scan); the node's total feeds the level above
+#pragma unroll
+  for (int h = 0; h < kMaxL; ++h) {
+    if (h > T.top) continue;  // (continue, not break: keeps the loop unrolled, P[h] in registers)
+    const double* in = h == 0 ? pw : Sb[(h - 1) & 1];
+    double* tot = Sb[h & 1];
+    const int64_t nnode = rup64(T.sz[h]) / kFan;
+    for (int64_t node = warp; node < nnode; node += nw) {
+      const int64_t c = node * kFan + 2 * lane;
+      const double a = c < T.sz[h] ? in[c] : 0.0;
+      const double b = c + 1 < T.sz[h] ? in[c + 1] : 0.0;
+      double s = __dadd_rn(a, b);
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, s, o);
+        if (lane >= o) s = __dadd_rn(s, y);
+      }
+      double ex = __shfl_up_sync(0xffffffffu, s, 1);
+      if (lane == 0) ex = 0.0;
+      *reinterpret_cast<double2*>(P[h] + c) = make_double2(__dadd_rn(ex, a), s);
+      if (lane == 31 && h < T.top) tot[node] = s;
+    }
+    __syncthreads();
+  }
   if (warp != 0) return;
   int positive = 0;
   for (int w = 0; w < nw; ++w) positive += s_pos[w];
@@ -130,94 +160,117 @@ __global__ void __launch_bounds__(1024) k2_draw(DrawJobs jobs, unsigned* status)
   }
   const double u53 = 1.0 / 9007199254740992.0;
   const int count = (int)job.count;
-  double u_next = uni[0];
+  // tree rounding per earlier removal: one per level
+  const double slack = (double)len + 70.0 + (double)(T.top + 2) * (double)count;
+  // uniforms in registers, 32 draws per block (lane l holds draw 32 b + l), the next block
+  // prefetched a whole block ahead: an L2 round trip per draw would otherwise be the chain's
+  // longest link
+  double ublk = lane < count ? uni[lane] : 0.0;
+  double unext = 32 + lane < count ? uni[32 + lane] : 0.0;
   for (int t = 0; t < count; ++t) {
-    const double u = u_next;  // identical on every lane
-    if (t + 1 < count) u_next = uni[t + 1];
-    // descend; the top level's inclusive scan also yields the total
-    double base = 0.0, lower = 0.0, upper = 0.0, total = 0.0, target = 0.0;
-    int g = 0;
-    bool ok = true;
-    for (int h = L.top; h >= 0; --h) {
-      const int c = g * 32 + lane;
-      const bool valid = c < (int)L.sz[h];
-      double s = valid ? L.lev[h][c] : 0.0;
-      // inclusive Hillis-Steele scan (fixed order)
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        double y = __shfl_up_sync(0xffffffffu, s, o);
-        if (lane >= o) s += y;
-      }
-      if (h == L.top) {
-        total = __shfl_sync(0xffffffffu, s, 31);
-        if (!(total > 0.0)) break;
-        target = u * total;
-      }
-      const double posv = base + s;
-      const unsigned hit = __ballot_sync(0xffffffffu, valid && posv > target);
-      if (hit == 0u) {
-        ok = false;
-        break;
-      }
-      const int k = __ffs(hit) - 1;
-      const double s_prev = __shfl_sync(0xffffffffu, s, (k + 31) & 31);
-      const double s_k = __shfl_sync(0xffffffffu, s, k);
-      const double nb = k > 0 ? base + s_prev : base;
-      if (h == 0) {
-        lower = nb;
-        upper = base + s_k;
-      }
-      base = nb;
-      g = g * 32 + k;
+    if ((t & 31) == 0 && t > 0) {
+      ublk = unext;
+      unext = t + 32 + lane < count ? uni[t + 32 + lane] : 0.0;
     }
+    const double u = __shfl_sync(0xffffffffu, ublk, t & 31);  // identical on every lane
+    const double total = (T.top == 0 ? P[0] : up + T.root)[kFan - 1];  // the root's last inclusive prefix
     if (!(total > 0.0)) {
       if (lane == 0) atomicOr(status, (unsigned)ST_SAMPLING);
       for (int q = t + lane; q < count; q += 32) job.out[q] = 0;
       return;
     }
+    const double target = u * total;
+    double q0[kMaxL], q1[kMaxL];
+    int e_at[kMaxL];
+    double base = 0.0, lower = 0.0, upper = 0.0, wl = 0.0;
+    int64_t g = 0;
+    bool ok = true;
+#pragma unroll
+    for (int h = kMaxL - 1; h >= 0; --h) {
+      q0[h] = q1[h] = 0.0;
+      e_at[h] = 0;
+      if (h > T.top || !ok) continue;
+      const double2 v = *reinterpret_cast<const double2*>(P[h] + g * kFan + 2 * lane);
+      q0[h] = v.x;
+      q1[h] = v.y;
+      const double a0 = base + v.x, a1 = base + v.y;
+      const unsigned b0 = __ballot_sync(0xffffffffu, a0 > target);
+      const unsigned b1 = __ballot_sync(0xffffffffu, a1 > target);
+      if ((b0 | b1) == 0u) {
+        ok = false;
+        continue;
+      }
+      const int k = __ffs(b0 | b1) - 1;
+      const bool first = (b0 >> k) & 1u;
+      const double a0k = __shfl_sync(0xffffffffu, a0, k), a1k = __shfl_sync(0xffffffffu, a1, k);
+      const double a1p = __shfl_sync(0xffffffffu, a1, (k + 31) & 31);
+      const double lo = first ? (k > 0 ? a1p : base) : a0k;
+      if (h == 0) {
+        // the leaf's weight as the tree sees it (within-node prefix difference)
+        const double v0k = __shfl_sync(0xffffffffu, v.x, k), v1k = __shfl_sync(0xffffffffu, v.y, k);
+        const double v1p = __shfl_sync(0xffffffffu, v.y, (k + 31) & 31);
+        wl = first ? (k > 0 ? __dsub_rn(v0k, v1p) : v0k) : __dsub_rn(v1k, v0k);
+        lower = lo;
+        upper = first ? a0k : a1k;
+      }
+      const int e = 2 * k + (first ? 0 : 1);
+      e_at[h] = e;
+      base = lo;
+      g = g * kFan + e;
+    }
     int64_t idx = g;
     if (ok) {
-      const double tot_est = total * (1.0 + 1e-12);
-      // 2 (n + 70 + 2 count) 2^-53 T: the fresh tree's prefix error plus one rounding per
-      // level for every earlier removal
-      const double delta = 2.0 * ((double)len + 70.0 + 2.0 * (double)count) * u53 * tot_est;
-      ok = (lower <= target - delta) && (upper > target + delta) && (L.lev[0][idx] > 0.0);
+      const double delta = 2.0 * slack * u53 * (total * (1.0 + 1e-12));
+      ok = (lower <= target - delta) && (upper > target + delta) && (wl > 0.0);
     }
-    if (!ok) {
+    if (ok) {
+      // remove: entries at and after the path position of every node on the path
+#pragma unroll
+      for (int h = 0; h < kMaxL; ++h) {
+        if (h > T.top) continue;
+        const int e = e_at[h];
+        if (2 * lane + 1 >= e) {
+          const int64_t node = idx >> (6 * (h + 1));
+          const double n0 = 2 * lane >= e ? __dsub_rn(q0[h], wl) : q0[h];
+          *reinterpret_cast<double2*>(P[h] + node * kFan + 2 * lane) = make_double2(n0, __dsub_rn(q1[h], wl));
+        }
+      }
+    } else {
       // exact numpy order: sequential cumsum, searchsorted(side='right'), clamp, zero walk
       if (lane == 0) {
         atomicOr(status, (unsigned)ST_DRAW_FALLBACK);
-        const double* p = L.lev[0];
         double acc = 0.0;
-        for (int64_t i = 0; i < len; ++i) acc = (i == 0) ? p[0] : acc + p[i];
-        const double tot = acc;
-        const double tgt = u * tot;
+        for (int64_t i = 0; i < len; ++i) acc = (i == 0) ? pw[0] : acc + pw[i];
+        const double tgt = u * acc;
         acc = 0.0;
         int64_t found = len;
         for (int64_t i = 0; i < len; ++i) {
-          acc = (i == 0) ? p[0] : acc + p[i];
+          acc = (i == 0) ? pw[0] : acc + pw[i];
           if (acc > tgt) {
             found = i;
             break;
           }
         }
         if (found > len - 1) found = len - 1;
-        while (found > 0 && p[found] == 0.0) --found;
+        while (found > 0 && pw[found] == 0.0) --found;
         idx = found;
       }
       idx = __shfl_sync(0xffffffffu, idx, 0);
+      const double w = pw[idx];
+      // remove the exact weight along idx's path (reload: the descent may have left it)
+#pragma unroll
+      for (int h = 0; h < kMaxL; ++h) {
+        if (h > T.top) continue;
+        const int e = (int)((idx >> (6 * h)) & (kFan - 1));
+        const int64_t node = idx >> (6 * (h + 1));
+        double2* at = reinterpret_cast<double2*>(P[h] + node * kFan + 2 * lane);
+        const double2 v = *at;
+        if (2 * lane + 1 >= e) *at = make_double2(2 * lane >= e ? __dsub_rn(v.x, w) : v.x, __dsub_rn(v.y, w));
+      }
     }
     if (lane == 0) {
-      // remove the drawn weight: zero the leaf, subtract it along the path (one rounding per
-      // level and draw; the acceptance margin above covers the accumulated error)
-      const double wgt = L.lev[0][idx];
       job.out[t] = idx;
-      L.lev[0][idx] = 0.0;
-      int node = (int)idx;
-      for (int h = 1; h <= L.top; ++h) {
-        node >>= 5;
-        L.lev[h][node] -= wgt;
-      }
+      pw[idx] = 0.0;
     }
     __syncwarp();
   }
@@ -229,19 +282,24 @@ void launch_draw(const DrawJob* jobs, int njobs, unsigned* status, cudaStream_t 
   for (int k = 0; k < njobs && k < 2; ++k) {
     j.j[k] = jobs[k];
     const int64_t len = jobs[k].len;
-    const int64_t tree = draw_uniform_offset(len) - len;  // levels >= 1 (+ slack)
-    const int64_t need = (len <= kDrawSmemMaxLen ? len : 0) + tree;
+    const int64_t need = draw_smem_doubles(len);
     if ((size_t)need * sizeof(double) > smem) smem = (size_t)need * sizeof(double);
   }
+  bool leaf_smem = true;
+  for (int k = 0; k < njobs && k < 2; ++k) leaf_smem = leaf_smem && jobs[k].len <= kDrawSmemMaxLen;
   static bool attr = false;
   if (!attr) {
     // 227 KB minus the kernel's static shared memory (a failing attribute call
     // would otherwise surface as the launch's error)
-    cudaFuncSetAttribute(k2_draw, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);
+    cudaFuncSetAttribute(k2_draw<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);
+    cudaFuncSetAttribute(k2_draw<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);
     attr = true;
   }
   ++::qcur::g_launches;
-  k2_draw<<<njobs, 1024, smem, st>>>(j, status);
+  if (leaf_smem)
+    k2_draw<true><<<njobs, 512, smem, st>>>(j, status);
+  else
+    k2_draw<false><<<njobs, 512, smem, st>>>(j, status);
 }
 
 }  // namespace qcur

@@ -86,24 +86,20 @@ __global__ void __launch_bounds__(kStripThreads) k1_colstrip(const double* __res
 // Pass B: numpy pairwise trees.
 // ---------------------------------------------------------------------------
 constexpr int kChunkThreads = 256;
+constexpr int kFinThreads = 1024;
 
-// One CTA evaluates one chunk (<= kChunkMax elements) of one segment.
-// out[seg * out_stride + chunk]
-__global__ void __launch_bounds__(kChunkThreads) pairwise_chunks(const double* __restrict__ data, int64_t seg_stride,
-                                                                 DevPairwise pw, double* __restrict__ out,
-                                                                 int64_t out_stride) {
-  extern __shared__ double sm[];
-  const int chunk = blockIdx.x;
-  const int64_t seg = blockIdx.y;
+// All threads of a CTA evaluate chunk `chunk` of numpy's pairwise tree over
+// `vals` (the segment's data: HBM or shared memory), using `leafv` (shared,
+// nleaves + chunk nodes) for the leaf sums and inner nodes.  Returns the chunk
+// sum in every thread.
+__device__ __forceinline__ double chunk_eval(const double* __restrict__ vals, const DevPairwise& pw, int chunk,
+                                             double* leafv) {
   const int pid = pw.chunk_plan[chunk];
-  const int len = pw.plan_len[pid];
   const int leaf0 = pw.plan_leaf_ptr[pid], nleaves = pw.plan_leaf_ptr[pid + 1] - leaf0;
-  const double* __restrict__ vals = data + seg * seg_stride + pw.chunk_off[chunk];  // leaves read from HBM
-  double* leafv = sm;  // [nleaves + chunk nodes]
-  (void)len;
+  vals += pw.chunk_off[chunk];
   const int q = threadIdx.x & 7;
-  for (int base = 0; base < nleaves; base += kChunkThreads / 8) {
-    const int leaf = base + (threadIdx.x >> 3);
+  for (int base = 0; base < nleaves; base += (int)blockDim.x / 8) {
+    const int leaf = base + ((int)threadIdx.x >> 3);
     const bool active = leaf < nleaves;
     int off = 0, ln = 0;
     if (active) {
@@ -144,7 +140,66 @@ __global__ void __launch_bounds__(kChunkThreads) pairwise_chunks(const double* _
     prev = end;
     __syncthreads();
   }
-  if (threadIdx.x == 0) out[seg * out_stride + chunk] = nl > 0 ? leafv[nleaves + prev - 1] : leafv[0];
+  const double sum = nl > 0 ? leafv[nleaves + prev - 1] : leafv[0];
+  __syncthreads();  // leafv may be reused by the caller
+  return sum;
+}
+
+// One CTA evaluates one chunk (<= kChunkMax elements) of one segment.
+// out[seg * out_stride + chunk].  reverse: segments in descending order (the
+// row pass right after the column strips finds the last-written rows of sq in L2).
+__global__ void __launch_bounds__(kChunkThreads) pairwise_chunks(const double* __restrict__ data, int64_t seg_stride,
+                                                                 DevPairwise pw, double* __restrict__ out,
+                                                                 int64_t out_stride, int reverse) {
+  extern __shared__ double sm[];
+  const int chunk = blockIdx.x;
+  const int64_t seg = reverse ? (int64_t)gridDim.y - 1 - blockIdx.y : (int64_t)blockIdx.y;
+  const double v = chunk_eval(data + seg * seg_stride, pw, chunk, sm);  // leaves read from HBM
+  if (threadIdx.x == 0) out[seg * out_stride + chunk] = v;
+}
+
+// Fused tail of length_distributions (cur.py:144-150) for axes of at most one
+// pairwise chunk: CTA 0 handles the columns, CTA 1 the rows.  Each CTA
+//   1. evaluates the flat top tree over the chunk sums of sq.ravel() in shared
+//      memory -> total (both CTAs alike, bit-identical);
+//   2. sc = axis_sum / total  (col = sq.sum(axis=0) / total), kept in shared memory;
+//   3. s = pairwise(sc)  (col.sum()), numpy's tree;
+//   4. out = sc / s.
+// Same divisions in the same order as the unfused launches, so the same bits.
+struct FinalizeAxis {
+  const double* sum;  // colsum or rowsum
+  double* out;        // col or row
+  DevPairwise pw;     // the axis length's program (a single chunk)
+};
+
+__global__ void __launch_bounds__(kFinThreads) k1_finalize(const double* __restrict__ flat, DevPairwise fpw,
+                                                           FinalizeAxis ax0, FinalizeAxis ax1, unsigned* status) {
+  extern __shared__ double sm[];
+  const FinalizeAxis& ax = blockIdx.x == 0 ? ax0 : ax1;
+  double total;
+  if (fpw.nnodes == 0) {
+    total = flat[0];
+  } else {
+    double* v = sm;
+    for (int k = threadIdx.x; k < fpw.nchunks; k += blockDim.x) v[k] = flat[k];
+    __syncthreads();
+    for (int h = 1; h <= fpw.maxh; ++h) {
+      const int a = fpw.level_ptr[h], b = fpw.level_ptr[h + 1];
+      for (int k = a + threadIdx.x; k < b; k += blockDim.x)
+        v[fpw.nchunks + k] = __dadd_rn(v[fpw.node_l[k]], v[fpw.node_r[k]]);
+      __syncthreads();
+    }
+    total = v[fpw.nchunks + fpw.nnodes - 1];
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && !(total > 0.0)) atomicOr(status, (unsigned)ST_DEGENERATE);
+  const int64_t len = ax.pw.length;
+  double* sc = sm;
+  double* leafv = sm + ((len + 31) & ~(int64_t)31);
+  for (int64_t t = threadIdx.x; t < len; t += blockDim.x) sc[t] = __ddiv_rn(ax.sum[t], total);
+  __syncthreads();
+  const double s = chunk_eval(sc, ax.pw, 0, leafv);
+  for (int64_t t = threadIdx.x; t < len; t += blockDim.x) ax.out[t] = __ddiv_rn(sc[t], s);
 }
 
 // Top tree over chunk sums; one CTA per segment.  vals: [nseg][nchunks+nnodes]
@@ -185,7 +240,7 @@ void launch_colstrip(const double* X, int64_t m, int64_t n, int64_t ldx, double*
 }
 
 void launch_pairwise(const double* data, int64_t nseg, int64_t seg_stride, const DevPairwise& pw, double* scratch,
-                     double* out, cudaStream_t st) {
+                     double* out, cudaStream_t st, bool with_top, bool reverse) {
   size_t smem = (size_t)(kChunkMax + kChunkMax / 8 + 8) * sizeof(double);
   static bool attr_set = false;
   if (!attr_set) {
@@ -198,15 +253,41 @@ void launch_pairwise(const double* data, int64_t nseg, int64_t seg_stride, const
     // single chunk per segment: write straight to out
     dim3 grid(1, (unsigned)nseg);
     ++::qcur::g_launches;
-    pairwise_chunks<<<grid, kChunkThreads, need, st>>>(data, seg_stride, pw, out, 1);
+    pairwise_chunks<<<grid, kChunkThreads, need, st>>>(data, seg_stride, pw, out, 1, reverse ? 1 : 0);
     return;
   }
   const int64_t w = (int64_t)pw.nchunks + pw.nnodes;
   dim3 grid((unsigned)pw.nchunks, (unsigned)nseg);
   ++::qcur::g_launches;
-  pairwise_chunks<<<grid, kChunkThreads, need, st>>>(data, seg_stride, pw, scratch, w);
+  pairwise_chunks<<<grid, kChunkThreads, need, st>>>(data, seg_stride, pw, scratch, w, reverse ? 1 : 0);
+  if (!with_top) return;
   ++::qcur::g_launches;
   pairwise_top<<<(unsigned)nseg, 256, 0, st>>>(scratch, pw, out);
+}
+
+static size_t finalize_smem(const DevPairwise& fpw, int64_t n, int64_t m) {
+  const int64_t top = fpw.nnodes == 0 ? 0 : (int64_t)fpw.nchunks + fpw.nnodes;
+  const int64_t len = n > m ? n : m;
+  const int64_t axis = ((len + 31) & ~(int64_t)31) + len / 4 + 64;
+  return (size_t)(top > axis ? top : axis) * sizeof(double);
+}
+
+bool finalize_supported(const DevPairwise& fpw, const DevPairwise& cpw, const DevPairwise& rpw) {
+  return cpw.nnodes == 0 && cpw.nchunks == 1 && rpw.nnodes == 0 && rpw.nchunks == 1 &&
+         finalize_smem(fpw, cpw.length, rpw.length) <= (size_t)200 * 1024;
+}
+
+void launch_finalize(const double* flat, const DevPairwise& fpw, const double* colsum, const DevPairwise& cpw,
+                     double* col, const double* rowsum, const DevPairwise& rpw, double* row, unsigned* status,
+                     cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k1_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
+  }
+  ++::qcur::g_launches;
+  k1_finalize<<<2, kFinThreads, finalize_smem(fpw, cpw.length, rpw.length), st>>>(
+      flat, fpw, FinalizeAxis{colsum, col, cpw}, FinalizeAxis{rowsum, row, rpw}, status);
 }
 
 void launch_scale(const double* in, int64_t len, const double* denom, double* out, unsigned* status,

@@ -32,7 +32,12 @@ struct DevPairwise {
 void launch_colstrip(const double* X, int64_t m, int64_t n, int64_t ldx, double* sq, double* colsum, cudaStream_t st,
                      const double* acc_in = nullptr);
 void launch_pairwise(const double* data, int64_t nseg, int64_t seg_stride, const DevPairwise& pw, double* scratch,
-                     double* out, cudaStream_t st);
+                     double* out, cudaStream_t st, bool with_top = true, bool reverse = false);
+// fused tail of the length distributions (axes of one pairwise chunk; see k_norms.cu)
+bool finalize_supported(const DevPairwise& fpw, const DevPairwise& cpw, const DevPairwise& rpw);
+void launch_finalize(const double* flat, const DevPairwise& fpw, const double* colsum, const DevPairwise& cpw,
+                     double* col, const double* rowsum, const DevPairwise& rpw, double* row, unsigned* status,
+                     cudaStream_t st);
 void launch_scale(const double* in, int64_t len, const double* denom, double* out, unsigned* status,
                   unsigned check_bit, cudaStream_t st);
 void launch_fill(double* out, int64_t len, double v, cudaStream_t st);

@@ -78,6 +78,7 @@ struct qcur_ctx {
   cudaStream_t hi_stream = nullptr;
   cudaEvent_t ev_hfork = nullptr, ev_hjoin = nullptr;
   bool prio = true;
+  int xres_fork = 1;  // where the residues of X fork: 0 before the length pass, 1 after it, 2 after the draw
   unsigned* status_dev = nullptr;
   unsigned* status_host = nullptr;  // pinned
   unsigned* counters = nullptr;     // split-K tickets for launch_qgemm (kept zero between launches)
@@ -259,6 +260,25 @@ int length_tail(qcur_ctx* ctx, const double* sq, const double* colsum, int64_t m
   double* scal = ctx->take<double>(8);  // total, colnorm, rownorm
   if (!rowsum || !scal) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (length)");
   int rc;
+  const DevProgram* pc = ctx->program(n);
+  const DevProgram* pr = ctx->program(m);
+  const DevProgram* pf = ctx->program(m * n);
+  if (!pc || !pr || !pf) return ctx->fail(QCUR_E_CUDA, "pairwise program allocation failed");
+  if (finalize_supported(pf->d, pc->d, pr->d)) {
+    // rows bottom-up (the column strips wrote the bottom rows of sq last: L2 hits), then the
+    // flat chunks top-down (the rows pass touched the top rows last), then one fused tail
+    double* flat = scal;
+    if (pf->d.nnodes > 0) {
+      flat = ctx->take<double>((size_t)pf->scratch_len);
+      if (!flat) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (length)");
+    }
+    launch_pairwise(sq, m, n, pc->d, nullptr, rowsum, st, true, true);  // m rows of length n
+    launch_pairwise(sq, 1, 0, pf->d, flat, flat, st, false, false);
+    launch_finalize(flat, pf->d, colsum, pc->d, col, rowsum, pr->d, row, ctx->status_dev, st);
+    CK_LAUNCH(ctx, "length tail");
+    ctx->mark("length");
+    return QCUR_OK;
+  }
   if ((rc = pairwise_sum(ctx, sq, m, n, n, rowsum)) != QCUR_OK) return rc;
   if ((rc = pairwise_sum(ctx, sq, 1, 0, m * n, scal)) != QCUR_OK) return rc;
   // col = colsum / total ; row = rowsum / total   (cur.py:147-148); total <= 0 -> degenerate
@@ -787,7 +807,7 @@ int qmcur_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, const doubl
   if (!jobs[0].work || !jobs[1].work) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (draw)");
   int rc = QCUR_OK;
   void* oz = oz_pre;
-  if (!oz && core == QCUR_CORE_PROJECTION && m >= c && n >= r) {
+  if (!oz && ctx->xres_fork < 2 && core == QCUR_CORE_PROJECTION && m >= c && n >= r) {
     oz = int8_fork_prepare(ctx, X, m, n, r, &rc);
     if (rc) return rc;
   }
@@ -1022,6 +1042,7 @@ int qcur_create(int device, qcur_ctx** out) {
   int prio_lo = 0, prio_hi = 0;
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   if (const char* pe = std::getenv("QCUR_PRIO")) ctx->prio = std::strcmp(pe, "0") != 0;
+  if (const char* xf = std::getenv("QCUR_XRES_FORK")) ctx->xres_fork = std::atoi(xf);
   if (cudaStreamCreateWithPriority(&ctx->hi_stream, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_hfork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_hjoin, cudaEventDisableTiming) != cudaSuccess ||
@@ -1421,7 +1442,8 @@ int qcur_approx(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int st
   }
   ctx->mark_begin();
   void* oz = nullptr;
-  if (core == QCUR_CORE_PROJECTION && m >= c && n >= r) oz = int8_fork_prepare(ctx, x_dev, m, n, r, &rc);
+  const bool fork_ok = core == QCUR_CORE_PROJECTION && m >= c && n >= r;
+  if (fork_ok && ctx->xres_fork == 0) oz = int8_fork_prepare(ctx, x_dev, m, n, r, &rc);
   if (!rc) {
     if (strategy == QCUR_STRATEGY_LENGTH) {
       rc = length_distributions_impl(ctx, x_dev, m, n, colp, rowp);
@@ -1431,6 +1453,7 @@ int qcur_approx(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int st
       ctx->mark("dists");
     }
   }
+  if (!rc && fork_ok && ctx->xres_fork == 1) oz = int8_fork_prepare(ctx, x_dev, m, n, r, &rc);
   if (!rc) rc = qmcur_impl(ctx, x_dev, m, n, colp, rowp, c, r, state, J, I, C, U, R, core, nullptr, oz);
   if (!rc) rc = error_impl(ctx, x_dev, m, n, C, c, U, R, r, psnr_scale, err4);
   if (ctx->prio) {
