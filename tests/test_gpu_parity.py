@@ -283,3 +283,41 @@ def test_unknown_core_rejected():
     x = lowrank(10, 8, 2, seed=1)
     with pytest.raises(q.ParameterError):
         q.qmcur(x, q.make_plan(x, "length", 2, 0), core="bogus")
+
+
+# 64-ary prefix tree (k_draw.cu): lengths at level boundaries (64, 64^2, 64^3), the
+# shared/global leaf boundary (24576) and draws that exhaust every positive weight
+@pytest.mark.parametrize("size,count", [(1, 1), (2, 2), (63, 20), (64, 64), (65, 40), (127, 100), (128, 7),
+                                        (129, 129), (4095, 300), (4096, 200), (4097, 200), (24576, 100),
+                                        (24577, 100), (262145, 40)])
+def test_draw_tree_level_boundaries(size, count):
+    rng = np.random.default_rng(size + count)
+    p = rng.random(size) ** 4
+    p /= p.sum()
+    got = q.draw_indices(p, count, size)
+    want = O.draw_indices(p, count, np.random.default_rng(size))
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("size,npos", [(70, 5), (5000, 64), (4097, 4097)])
+def test_draw_exhausts_sparse_positive_weights(size, npos):
+    # count == number of positive weights: every positive index is drawn, zeros never
+    rng = np.random.default_rng(npos)
+    p = np.zeros(size)
+    pos = rng.choice(size, npos, replace=False)
+    p[pos] = rng.random(npos) + 1e-3
+    p /= p.sum()
+    got = q.draw_indices(p, npos, 11)
+    want = O.draw_indices(p, npos, np.random.default_rng(11))
+    assert np.array_equal(got, want)
+    assert set(got.tolist()) == set(pos.tolist())
+
+
+def test_draw_tied_weights():
+    # equal weights put every cumsum boundary on a multiple of 1/n: draws near ties are
+    # decided by the exact fallback when the tree cannot prove the index
+    for n, seed in ((10, 3), (1000, 5), (4096, 9)):
+        p = np.full(n, 1.0 / n)
+        got = q.draw_indices(p, min(n, 300), seed)
+        want = O.draw_indices(p, min(n, 300), np.random.default_rng(seed))
+        assert np.array_equal(got, want)
