@@ -78,7 +78,6 @@ struct qcur_ctx {
   cudaStream_t hi_stream = nullptr;
   cudaEvent_t ev_hfork = nullptr, ev_hjoin = nullptr;
   bool prio = true;
-  int xres_fork = 1;  // where the residues of X fork: 0 before the length pass, 1 after it, 2 after the draw
   unsigned* status_dev = nullptr;
   unsigned* status_host = nullptr;  // pinned
   unsigned* counters = nullptr;     // split-K tickets for launch_qgemm (kept zero between launches)
@@ -807,7 +806,7 @@ int qmcur_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, const doubl
   if (!jobs[0].work || !jobs[1].work) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (draw)");
   int rc = QCUR_OK;
   void* oz = oz_pre;
-  if (!oz && ctx->xres_fork < 2 && core == QCUR_CORE_PROJECTION && m >= c && n >= r) {
+  if (!oz && core == QCUR_CORE_PROJECTION && m >= c && n >= r) {
     oz = int8_fork_prepare(ctx, X, m, n, r, &rc);
     if (rc) return rc;
   }
@@ -1042,7 +1041,6 @@ int qcur_create(int device, qcur_ctx** out) {
   int prio_lo = 0, prio_hi = 0;
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   if (const char* pe = std::getenv("QCUR_PRIO")) ctx->prio = std::strcmp(pe, "0") != 0;
-  if (const char* xf = std::getenv("QCUR_XRES_FORK")) ctx->xres_fork = std::atoi(xf);
   if (cudaStreamCreateWithPriority(&ctx->hi_stream, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_hfork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_hjoin, cudaEventDisableTiming) != cudaSuccess ||
@@ -1432,7 +1430,7 @@ int qcur_approx(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int st
   double* colp = ctx->take<double>((size_t)n);
   double* rowp = ctx->take<double>((size_t)m);
   // the pipeline runs on the context's high-priority stream, forked from (and joined back
-  // to) the caller's stream; the residues of X start at once on the low-priority side stream
+  // to) the caller's stream; the residues of X start after the length pass on the low-priority side stream
   cudaStream_t user = ctx->stream;
   if (ctx->prio) {
     cudaError_t e = cudaEventRecord(ctx->ev_hfork, user);
@@ -1442,8 +1440,6 @@ int qcur_approx(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int st
   }
   ctx->mark_begin();
   void* oz = nullptr;
-  const bool fork_ok = core == QCUR_CORE_PROJECTION && m >= c && n >= r;
-  if (fork_ok && ctx->xres_fork == 0) oz = int8_fork_prepare(ctx, x_dev, m, n, r, &rc);
   if (!rc) {
     if (strategy == QCUR_STRATEGY_LENGTH) {
       rc = length_distributions_impl(ctx, x_dev, m, n, colp, rowp);
@@ -1453,7 +1449,9 @@ int qcur_approx(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int st
       ctx->mark("dists");
     }
   }
-  if (!rc && fork_ok && ctx->xres_fork == 1) oz = int8_fork_prepare(ctx, x_dev, m, n, r, &rc);
+  // the residues of X fork after the length pass: overlapping it (both HBM-bound) gained nothing,
+  // overlapping the latency-bound draws and factorizations does
+  if (!rc && core == QCUR_CORE_PROJECTION && m >= c && n >= r) oz = int8_fork_prepare(ctx, x_dev, m, n, r, &rc);
   if (!rc) rc = qmcur_impl(ctx, x_dev, m, n, colp, rowp, c, r, state, J, I, C, U, R, core, nullptr, oz);
   if (!rc) rc = error_impl(ctx, x_dev, m, n, C, c, U, R, r, psnr_scale, err4);
   if (ctx->prio) {
