@@ -158,6 +158,28 @@ __global__ void __launch_bounds__(kChunkThreads) pairwise_chunks(const double* _
   if (threadIdx.x == 0) out[seg * out_stride + chunk] = v;
 }
 
+// The row pass and the flat pass in one launch, scheduled by position: job list entries
+// >= 0 are rows (rowsum[i] = pairwise(sq[i, :])), entries < 0 are flat chunks -(k+1)
+// (chunk sums of sq.ravel()); each row is followed by the flat chunks that start inside it,
+// so the second reader of every stretch of sq finds it in L2.  Jobs run bottom-up (the
+// column strips wrote the bottom rows last).
+__global__ void __launch_bounds__(kChunkThreads) pairwise_rows_flat(const double* __restrict__ sq, int64_t n,
+                                                                    DevPairwise rpw, DevPairwise fpw,
+                                                                    const int32_t* __restrict__ sched,
+                                                                    double* __restrict__ rowsum,
+                                                                    double* __restrict__ flat) {
+  extern __shared__ double sm[];
+  const int job = sched[gridDim.x - 1 - blockIdx.x];
+  if (job >= 0) {
+    const double v = chunk_eval(sq + (int64_t)job * n, rpw, 0, sm);
+    if (threadIdx.x == 0) rowsum[job] = v;
+  } else {
+    const int chunk = -job - 1;
+    const double v = chunk_eval(sq, fpw, chunk, sm);
+    if (threadIdx.x == 0) flat[chunk] = v;
+  }
+}
+
 // Fused tail of length_distributions (cur.py:144-150) for axes of at most one
 // pairwise chunk: CTA 0 handles the columns, CTA 1 the rows.  Each CTA
 //   1. evaluates the flat top tree over the chunk sums of sq.ravel() in shared
@@ -270,6 +292,14 @@ static size_t finalize_smem(const DevPairwise& fpw, int64_t n, int64_t m) {
   const int64_t len = n > m ? n : m;
   const int64_t axis = ((len + 31) & ~(int64_t)31) + len / 4 + 64;
   return (size_t)(top > axis ? top : axis) * sizeof(double);
+}
+
+void launch_rows_flat(const double* sq, int64_t m, int64_t n, const DevPairwise& rpw, const DevPairwise& fpw,
+                      const int32_t* sched, double* rowsum, double* flat, cudaStream_t st) {
+  const int64_t mc = rpw.max_chunk_len > fpw.max_chunk_len ? rpw.max_chunk_len : fpw.max_chunk_len;
+  const size_t need = (size_t)(mc / 4 + 16) * sizeof(double);
+  ++::qcur::g_launches;
+  pairwise_rows_flat<<<(unsigned)(m + fpw.nchunks), kChunkThreads, need, st>>>(sq, n, rpw, fpw, sched, rowsum, flat);
 }
 
 bool finalize_supported(const DevPairwise& fpw, const DevPairwise& cpw, const DevPairwise& rpw) {

@@ -34,6 +34,8 @@ void launch_colstrip(const double* X, int64_t m, int64_t n, int64_t ldx, double*
 void launch_pairwise(const double* data, int64_t nseg, int64_t seg_stride, const DevPairwise& pw, double* scratch,
                      double* out, cudaStream_t st, bool with_top = true, bool reverse = false);
 // fused tail of the length distributions (axes of one pairwise chunk; see k_norms.cu)
+void launch_rows_flat(const double* sq, int64_t m, int64_t n, const DevPairwise& rpw, const DevPairwise& fpw,
+                      const int32_t* sched, double* rowsum, double* flat, cudaStream_t st);
 bool finalize_supported(const DevPairwise& fpw, const DevPairwise& cpw, const DevPairwise& rpw);
 void launch_finalize(const double* flat, const DevPairwise& fpw, const double* colsum, const DevPairwise& cpw,
                      double* col, const double* rowsum, const DevPairwise& rpw, double* row, unsigned* status,

@@ -86,6 +86,7 @@ struct qcur_ctx {
   bool force_robust = false;
   Arena arena;
   std::map<int64_t, DevProgram> programs;
+  std::map<std::pair<int64_t, int64_t>, int32_t*> rf_sched;  // rows + flat chunk job lists (length tail)
   std::string err;
   Profiler prof;
 
@@ -252,6 +253,26 @@ size_t length_ws_bytes(qcur_ctx* ctx, int64_t m, int64_t n) {
 
 // length_distributions on the device (cur.py:132-150); arena must be reserved.
 // K1 after the column pass: row / flat pairwise trees and the normalisations (cur.py:144-150)
+// Job list of pairwise_rows_flat: row i, then the flat chunks of sq.ravel() starting in row i.
+const int32_t* rows_flat_schedule(qcur_ctx* ctx, int64_t m, int64_t n) {
+  auto key = std::make_pair(m, n);
+  auto it = ctx->rf_sched.find(key);
+  if (it != ctx->rf_sched.end()) return it->second;
+  const PairwiseProgram pp = compile_pairwise(m * n);
+  std::vector<int32_t> jobs;
+  jobs.reserve((size_t)m + pp.chunk_off.size());
+  size_t k = 0;
+  for (int64_t i = 0; i < m; ++i) {
+    jobs.push_back((int32_t)i);
+    while (k < pp.chunk_off.size() && pp.chunk_off[k] < (i + 1) * n) jobs.push_back(-(int32_t)(k++) - 1);
+  }
+  int32_t* d = nullptr;
+  if (cudaMalloc(&d, jobs.size() * sizeof(int32_t)) != cudaSuccess) return nullptr;
+  cudaMemcpy(d, jobs.data(), jobs.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+  ctx->rf_sched[key] = d;
+  return d;
+}
+
 int length_tail(qcur_ctx* ctx, const double* sq, const double* colsum, int64_t m, int64_t n, double* col,
                 double* row) {
   cudaStream_t st = ctx->stream;
@@ -264,15 +285,16 @@ int length_tail(qcur_ctx* ctx, const double* sq, const double* colsum, int64_t m
   const DevProgram* pf = ctx->program(m * n);
   if (!pc || !pr || !pf) return ctx->fail(QCUR_E_CUDA, "pairwise program allocation failed");
   if (finalize_supported(pf->d, pc->d, pr->d)) {
-    // rows bottom-up (the column strips wrote the bottom rows of sq last: L2 hits), then the
-    // flat chunks top-down (the rows pass touched the top rows last), then one fused tail
+    // rows and flat chunks in one launch, interleaved by position and bottom-up (L2 reuse of sq),
+    // then one fused tail
     double* flat = scal;
     if (pf->d.nnodes > 0) {
       flat = ctx->take<double>((size_t)pf->scratch_len);
       if (!flat) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (length)");
     }
-    launch_pairwise(sq, m, n, pc->d, nullptr, rowsum, st, true, true);  // m rows of length n
-    launch_pairwise(sq, 1, 0, pf->d, flat, flat, st, false, false);
+    const int32_t* sched = rows_flat_schedule(ctx, m, n);
+    if (!sched) return ctx->fail(QCUR_E_CUDA, "length schedule allocation failed");
+    launch_rows_flat(sq, m, n, pc->d, pf->d, sched, rowsum, flat, st);
     launch_finalize(flat, pf->d, colsum, pc->d, col, rowsum, pr->d, row, ctx->status_dev, st);
     CK_LAUNCH(ctx, "length tail");
     ctx->mark("length");
@@ -1062,6 +1084,7 @@ void qcur_destroy(qcur_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   for (auto& kv : ctx->programs) cudaFree(kv.second.buf);
+  for (auto& kv : ctx->rf_sched) cudaFree(kv.second);
   if (ctx->arena.base) cudaFree(ctx->arena.base);
   cudaFree(ctx->status_dev);
   cudaFree(ctx->counters);
