@@ -33,7 +33,8 @@ namespace qcur {
 
 constexpr int kFan = 64;                    // children per node: two per lane
 constexpr int kMaxL = 5;                    // 64^5 leaves: any axis length up to 2^30
-constexpr int64_t kDrawSmemMaxLen = 24576;  // p (+ its tree) fits the 224 KB dynamic shared memory cap
+constexpr int64_t kDrawSmemMaxLen = 24576;         // leaf prefixes (+ upper levels) fit the 224 KB smem cap
+constexpr int64_t kMaxDrawLen = (int64_t)1 << 30;  // 64^5: the deepest tree kMaxL levels hold
 
 __host__ __device__ inline int64_t rup64(int64_t x) { return (x + kFan - 1) / kFan * kFan; }
 
@@ -276,7 +277,9 @@ __global__ void __launch_bounds__(512, 1) k2_draw(DrawJobs jobs, unsigned* statu
   }
 }
 
-void launch_draw(const DrawJob* jobs, int njobs, unsigned* status, cudaStream_t st) {
+bool launch_draw(const DrawJob* jobs, int njobs, unsigned* status, cudaStream_t st) {
+  for (int k = 0; k < njobs && k < 2; ++k)
+    if (jobs[k].len > kMaxDrawLen) return false;
   DrawJobs j{};
   size_t smem = 0;
   for (int k = 0; k < njobs && k < 2; ++k) {
@@ -300,6 +303,7 @@ void launch_draw(const DrawJob* jobs, int njobs, unsigned* status, cudaStream_t 
     k2_draw<true><<<njobs, 512, smem, st>>>(j, status);
   else
     k2_draw<false><<<njobs, 512, smem, st>>>(j, status);
+  return true;
 }
 
 }  // namespace qcur

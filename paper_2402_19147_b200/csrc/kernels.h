@@ -54,7 +54,8 @@ struct DrawJob {
   double* work;                           // >= draw_work_doubles(len)
 };
 int64_t draw_work_doubles(int64_t len);
-void launch_draw(const DrawJob* jobs_host, int njobs, unsigned* status, cudaStream_t st);  // njobs <= 2
+// njobs <= 2; false (nothing launched) for an axis longer than the draw tree holds (64^5 entries)
+bool launch_draw(const DrawJob* jobs_host, int njobs, unsigned* status, cudaStream_t st);
 
 // k_layout.cu
 void launch_planar_to_interleaved(const double* a0, const double* a1, const double* a2, const double* a3, int64_t m,

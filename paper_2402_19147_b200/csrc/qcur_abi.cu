@@ -832,7 +832,8 @@ int qmcur_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, const doubl
     oz = int8_fork_prepare(ctx, X, m, n, r, &rc);
     if (rc) return rc;
   }
-  launch_draw(jobs, 2, ctx->status_dev, st);
+  if (!launch_draw(jobs, 2, ctx->status_dev, st))
+    return ctx->fail(QCUR_E_PARAMETER, "draw: axis longer than 2^30 entries");
   ctx->mark("draw");
   CK_LAUNCH(ctx, "draw");
   // 2. gathers (quat.py:215-225)
@@ -1286,7 +1287,8 @@ int qcur_draw_indices(qcur_ctx* ctx, const double* probs, int64_t size, int64_t 
   if ((rc = reset_status(ctx))) return rc;
   DrawJob job{probs, size, count, state[0], state[1], state[2], state[3], out,
               ctx->take<double>((size_t)draw_work_doubles(size))};
-  launch_draw(&job, 1, ctx->status_dev, ctx->stream);
+  if (!launch_draw(&job, 1, ctx->status_dev, ctx->stream))
+    return ctx->fail(QCUR_E_PARAMETER, "draw: axis longer than 2^30 entries");
   CK_LAUNCH(ctx, "draw");
   qcur_rng_advance(state, (uint64_t)count);
   return sync_status(ctx);
