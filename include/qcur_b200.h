@@ -93,7 +93,8 @@ int qcur_length_distributions(qcur_ctx* ctx, const double* x_dev, int64_t m, int
 /* uniform_distributions (cur.py:153-157) */
 int qcur_uniform_distributions(qcur_ctx* ctx, int64_t m, int64_t n, double* col_probs_dev, double* row_probs_dev);
 /* draw_indices (cur.py:202-242): `count` distinct indices, index-exact vs numpy,
- * consuming `count` doubles of the stream `state` (advanced on return). */
+ * consuming `count` doubles of the stream `state` (advanced on return).
+ * QCUR_E_PARAMETER for size > 2^30 (the 64-ary draw tree's capacity). */
 int qcur_draw_indices(qcur_ctx* ctx, const double* probs_dev, int64_t size, int64_t count, uint64_t state[4],
                       int64_t* out_dev);
 /* qmcur (cur.py:257-269) + plan_indices (cur.py:245-254):
