@@ -7,8 +7,8 @@
 //   row   = pairwise sum along each row                              (cur.py:148)
 //   col/total, row/total, then divided by their own pairwise sums    (cur.py:150)
 //
-// Pass A (k1_colstrip): one CTA per 32-column strip streams its strip of X
-// top to bottom (coalesced 1 KB row segments, register double-buffered),
+// Pass A (k1_colstrip): one CTA per 16-column strip streams its strip of X
+// top to bottom (coalesced 512-byte row segments, register double-buffered),
 // computes sq, writes it row-major for pass B and keeps the exact sequential
 // column accumulator in one lane per column.
 // Pass B (pairwise_chunks / pairwise_top): numpy's pairwise tree over each row
@@ -22,28 +22,30 @@ namespace qcur {
 // ---------------------------------------------------------------------------
 // Pass A: sq + exact sequential column sums.
 // ---------------------------------------------------------------------------
-constexpr int kStripW = 32;   // quaternion columns per CTA (one warp lane each)
-constexpr int kStripRB = 64;  // rows per pipeline stage (8 quaternions in flight per thread)
+constexpr int kStripW = 16;    // quaternion columns per CTA (half a warp per row: 512-byte segments)
+constexpr int kStripRB = 128;  // rows per pipeline stage (8 quaternions in flight per thread)
 constexpr int kStripThreads = 256;
 
 // acc_in (nullable): running column sums of the rows above this block, so a
 // row-sharded matrix continues numpy's sequential axis-0 order across ranks.
+// 16-column strips: n / 16 CTAs (250 at n = 4000) cover every SM, where 32-column
+// strips left 23 of 148 idle.
 __global__ void __launch_bounds__(kStripThreads) k1_colstrip(const double* __restrict__ X, int64_t m, int64_t n,
                                                              int64_t ldx, double* __restrict__ sq,
                                                              double* __restrict__ colsum,
                                                              const double* __restrict__ acc_in) {
   __shared__ double sqs[2][kStripRB][kStripW];
   const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  const int wrow = tid >> 5;  // 0..7
-  const int64_t j = (int64_t)blockIdx.x * kStripW + lane;
+  const int lane = tid & 31, col = lane & (kStripW - 1);
+  const int prow = (tid >> 5) * 2 + (lane >> 4);  // 0..15: row within a 16-row pass
+  const int64_t j = (int64_t)blockIdx.x * kStripW + col;
   const bool jok = j < n;
-  constexpr int kPer = kStripRB / 8;  // rows per thread per stage
+  constexpr int kPer = kStripRB / 16;  // rows per thread per stage
   Quat buf[kPer];
   auto load_stage = [&](int64_t r0) {
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
-      int64_t i = r0 + wrow + 8 * k;
+      int64_t i = r0 + prow + 16 * k;
       if (jok && i < m)
         buf[k] = ldq_nc(X + (i * ldx + j) * 4);
       else
@@ -64,22 +66,22 @@ __global__ void __launch_bounds__(kStripThreads) k1_colstrip(const double* __res
       v = __dadd_rn(v, __dmul_rn(q.x, q.x));
       v = __dadd_rn(v, __dmul_rn(q.y, q.y));
       v = __dadd_rn(v, __dmul_rn(q.z, q.z));
-      const int rr = wrow + 8 * k;
-      sqs[b][rr][lane] = v;
+      const int rr = prow + 16 * k;
+      sqs[b][rr][col] = v;
       const int64_t i = r0 + rr;
       if (jok && i < m) sq[i * n + j] = v;
     }
     if (s + 1 < nstages) load_stage(r0 + kStripRB);
     __syncthreads();
-    if (wrow == 0) {
+    if (tid < kStripW) {
       const int rows = (int)((m - r0) < kStripRB ? (m - r0) : kStripRB);
-      for (int rr = 0; rr < rows; ++rr) acc = __dadd_rn(acc, sqs[b][rr][lane]);
+      for (int rr = 0; rr < rows; ++rr) acc = __dadd_rn(acc, sqs[b][rr][col]);
     }
     // the double buffer lets the next stage's sq writes proceed while warp 0
     // accumulates; a second barrier is only needed before a buffer is reused,
     // which the barrier of the following stage provides.
   }
-  if (wrow == 0 && jok) colsum[j] = acc;
+  if (tid < kStripW && jok) colsum[j] = acc;
 }
 
 // ---------------------------------------------------------------------------
