@@ -204,13 +204,22 @@ __global__ void __launch_bounds__(kFinThreads) k1_finalize(const double* __restr
   if (fpw.nnodes == 0) {
     total = flat[0];
   } else {
+    // the tree program is staged in shared memory with the chunk sums (one round trip
+    // instead of one per level)
     double* v = sm;
+    int32_t* nl = reinterpret_cast<int32_t*>(v + fpw.nchunks + fpw.nnodes);
+    int32_t* nr = nl + fpw.nnodes;
+    int32_t* lp = nr + fpw.nnodes;
     for (int k = threadIdx.x; k < fpw.nchunks; k += blockDim.x) v[k] = flat[k];
+    for (int k = threadIdx.x; k < fpw.nnodes; k += blockDim.x) {
+      nl[k] = fpw.node_l[k];
+      nr[k] = fpw.node_r[k];
+    }
+    for (int k = threadIdx.x; k < fpw.maxh + 2; k += blockDim.x) lp[k] = fpw.level_ptr[k];
     __syncthreads();
     for (int h = 1; h <= fpw.maxh; ++h) {
-      const int a = fpw.level_ptr[h], b = fpw.level_ptr[h + 1];
-      for (int k = a + threadIdx.x; k < b; k += blockDim.x)
-        v[fpw.nchunks + k] = __dadd_rn(v[fpw.node_l[k]], v[fpw.node_r[k]]);
+      const int a = lp[h], b = lp[h + 1];
+      for (int k = a + threadIdx.x; k < b; k += blockDim.x) v[fpw.nchunks + k] = __dadd_rn(v[nl[k]], v[nr[k]]);
       __syncthreads();
     }
     total = v[fpw.nchunks + fpw.nnodes - 1];
@@ -290,7 +299,8 @@ void launch_pairwise(const double* data, int64_t nseg, int64_t seg_stride, const
 }
 
 static size_t finalize_smem(const DevPairwise& fpw, int64_t n, int64_t m) {
-  const int64_t top = fpw.nnodes == 0 ? 0 : (int64_t)fpw.nchunks + fpw.nnodes;
+  // chunk sums and nodes (doubles) + node_l, node_r, level_ptr (int32)
+  const int64_t top = fpw.nnodes == 0 ? 0 : (int64_t)fpw.nchunks + fpw.nnodes + (2 * (int64_t)fpw.nnodes + fpw.maxh + 3) / 2;
   const int64_t len = n > m ? n : m;
   const int64_t axis = ((len + 31) & ~(int64_t)31) + len / 4 + 64;
   return (size_t)(top > axis ? top : axis) * sizeof(double);
