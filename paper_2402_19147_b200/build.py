@@ -6,6 +6,7 @@ travels with the repo snapshot to the GPU box.  Invoked by
 """
 from __future__ import annotations
 
+import hashlib
 import os
 import subprocess
 import sys
@@ -14,6 +15,7 @@ from pathlib import Path
 HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
 LIB = CSRC / "libqcur_b200.so"
+STAMP = CSRC / "libqcur_b200.so.sha256"  # hash of the sources + flags the library was built from
 SOURCES = ["qcur_abi.cu", "k_norms.cu", "k_draw.cu", "k_layout.cu", "k_qgemm.cu", "k_dense.cu", "k_synth.cu",
            "k_chol_cluster.cu", "k_gemv.cu", "k_ozaki.cu", "k_ozaki_err.cu", "k_qsvd.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -27,13 +29,30 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(verbose: bool = False, jobs: int | None = None) -> Path:
-    objdir = CSRC / "build"
-    objdir.mkdir(exist_ok=True)
+def source_hash() -> str:
+    """sha256 over every source, header and the compile flags (not mtimes: a copied tree keeps a
+    stale library's mtime newer than its sources, so time stamps cannot prove freshness)."""
+    h = hashlib.sha256(" ".join(SOURCES + ARCH + FLAGS).encode())
     deps = sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h"))
     deps.append(HERE.parent / "include" / "qcur_b200.h")
-    newest = max(p.stat().st_mtime for p in deps)
-    if LIB.exists() and LIB.stat().st_mtime >= newest:
+    for p in deps:
+        h.update(p.name.encode())
+        h.update(p.read_bytes())
+    return h.hexdigest()
+
+
+def build_info() -> dict:
+    """Which binary the package loads: its path, the source hash it was built from and
+    whether that hash matches the sources in the tree."""
+    stamp = STAMP.read_text().strip() if STAMP.exists() else None
+    return {"lib": str(LIB), "exists": LIB.exists(), "built_from": stamp, "fresh": stamp == source_hash()}
+
+
+def build(verbose: bool = False, jobs: int | None = None, force: bool = False) -> Path:
+    objdir = CSRC / "build"
+    objdir.mkdir(exist_ok=True)
+    want = source_hash()
+    if not force and LIB.exists() and STAMP.exists() and STAMP.read_text().strip() == want:
         return LIB
     procs = []
     objs = []
@@ -56,8 +75,9 @@ def build(verbose: bool = False, jobs: int | None = None) -> Path:
         raise RuntimeError(f"nvcc failed:\n{msg}")
     cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *map(str, objs)]
     subprocess.run(cmd, check=True)
+    STAMP.write_text(want + "\n")
     return LIB
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv))
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))

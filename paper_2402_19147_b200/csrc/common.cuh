@@ -8,7 +8,20 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 namespace qcur {
+
+// True the first time it is called on the current device for this flag: kernel
+// attributes (cudaFuncSetAttribute) are per device, so a process driving several
+// GPUs sets them once on each.
+inline bool first_on_device(std::atomic<unsigned>& done) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned bit = 1u << (dev & 31);
+  return !(done.fetch_or(bit) & bit);
+}
+
 
 struct __align__(32) Quat {
   double w, x, y, z;

@@ -225,11 +225,10 @@ void launch_chol_inv_cluster(const CholJob* jobs, int njobs, int64_t q, unsigned
   P.q = q;
   P.status = status;
   const size_t smem = chol_cluster_smem(q);
-  static bool set = false;
-  if (!set) {
+  static std::atomic<unsigned> set{0};
+  if (first_on_device(set)) {
     cudaFuncSetAttribute(k_chol_inv_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(k_chol_inv_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    set = true;
   }
   ++::qcur::g_launches;
   k_chol_inv_cluster<<<kCl * njobs, kThreads, smem, st>>>(P);

@@ -18,12 +18,18 @@
 // only, all levels independent).  The level pointers and sizes are
 // compile-time-indexed registers (fully unrolled level loops).
 // The descent's prefix values differ from numpy's sequential cumsum only by
-// rounding, bounded by (n + 70) * 2^-53 * total plus one rounding per level
-// and earlier removal; a draw is accepted only when the uniform sits farther
-// than twice that bound from both neighbouring prefix values, which proves
-// the numpy index.  Otherwise (probability ~1e-12 per draw) lane 0 recomputes
-// the exact sequential cumsum — numpy's own order — over the exact weights
-// (a global copy of p with the drawn entries zeroed) for that draw.
+// rounding.  numpy's own cumsum is within (n + 2) * 2^-53 * total of the exact
+// prefix; the tree's entries carry their build rounding (relative to the total
+// the tree was BUILT at) plus one rounding per level for every earlier removal
+// (relative to the total at THAT removal, which can be far above today's total
+// when a dominant weight was drawn).  The kernel keeps that running bound and
+// accepts a draw only when the uniform sits farther than twice the sum from
+// both neighbouring prefix values, which proves the numpy index.  When the
+// tree's accumulated bound outgrows numpy's own term the tree is rebuilt from
+// the exact remaining weights (drawn entries exactly zero), so a dominant
+// weight costs one rebuild, not a run of fallbacks.  A draw that cannot be
+// proved (probability ~1e-12 for ordinary weights) is made by lane 0 with the
+// exact sequential cumsum — numpy's own order — over the exact weights.
 // The PCG64 stream is advanced on device (pcg64.h), one double per draw.
 #include "common.cuh"
 #include "kernels.h"
@@ -71,62 +77,32 @@ __host__ __device__ inline Tree make_tree(int64_t len) {
 }
 
 // global work buffer: exact weights p (zeroed as drawn; the fallback's cumsum) | the
-// level-0 prefix entries when they do not fit shared memory | uniforms
-int64_t draw_work_doubles(int64_t len) { return 2 * rup64(len) + len + 64; }
+// level-0 prefix entries when they do not fit shared memory | uniforms | the upper
+// levels and node-total buffers when even those do not fit shared memory
+static int64_t draw_upper_doubles(int64_t len) {
+  const Tree T = make_tree(len);
+  return T.upper + 2 * rup64((len + kFan - 1) / kFan);
+}
+int64_t draw_work_doubles(int64_t len) { return 3 * rup64(len) + draw_upper_doubles(len) + 64; }
+
+static constexpr size_t kDrawSmemCap = 224 * 1024;
 
 // shared memory: level-0 prefixes (when they fit) | levels >= 1 | two node-total buffers
 static int64_t draw_smem_doubles(int64_t len) {
-  const Tree T = make_tree(len);
-  const int64_t nodes0 = rup64((len + kFan - 1) / kFan);
-  return (len <= kDrawSmemMaxLen ? rup64(len) : 0) + T.upper + 2 * nodes0;
+  const int64_t need = (len <= kDrawSmemMaxLen ? rup64(len) : 0) + draw_upper_doubles(len);
+  return (size_t)need * 8 <= kDrawSmemCap ? need : 0;  // 0: everything in global memory
 }
 
 struct DrawJobs {
   DrawJob j[2];
 };
 
-// kLeafSmem: the level-0 prefixes live in shared memory (every job's axis is at most
-// kDrawSmemMaxLen long), so all tree accesses compile to shared-memory loads
-template <bool kLeafSmem>
-__global__ void __launch_bounds__(512, 1) k2_draw(DrawJobs jobs, unsigned* status) {
-  const DrawJob job = jobs.j[blockIdx.x];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  const int64_t len = job.len;
-  const Tree T = make_tree(len);
-  extern __shared__ __align__(16) double sm_draw[];
-  constexpr bool p_in_smem = kLeafSmem;
-  double* P[kMaxL];
-  P[0] = p_in_smem ? sm_draw : job.work + rup64(len);
-  double* up = p_in_smem ? sm_draw + rup64(len) : sm_draw;
-#pragma unroll
-  for (int h = 1; h < kMaxL; ++h) P[h] = up + T.off[h];
-  const int64_t nodes0 = rup64((len + kFan - 1) / kFan);
-  double* Sb[2] = {up + T.upper, up + T.upper + nodes0};
-  double* pw = job.work;  // exact weights
-  double* uni = job.work + 2 * rup64(len);
-  // exact weights (zero padded) and the count of positives
-  __shared__ int s_pos[32];
-  int pos = 0;
-  for (int64_t t = tid; t < rup64(len); t += blockDim.x) {
-    const double v = t < len ? job.probs[t] : 0.0;
-    pw[t] = v;
-    pos += v > 0.0;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) pos += __shfl_xor_sync(0xffffffffu, pos, o);
-  if (lane == 0) s_pos[warp] = pos;
-  // the draw's uniforms: uniform t is the stream advanced by t (numpy draws one
-  // double per draw, columns first), computed in parallel instead of in the chain
-  for (int64_t t = tid; t < job.count; t += blockDim.x) {
-    Pcg64 g;
-    g.state = u128{job.st_hi, job.st_lo};
-    g.inc = u128{job.inc_hi, job.inc_lo};
-    g.advance((uint64_t)t);
-    uni[t] = g.next_double();
-  }
-  __syncthreads();
-  // prefix tree, level by level: a warp per node scans its 64 children (pair sums, then a
-  // fixed-order Hillis-Steele scan); the node's total feeds the level above
+// The prefix tree over the exact weights pw, level by level: a warp per node scans its 64
+// children (pair sums, then a fixed-order Hillis-Steele scan); the node's total feeds the
+// level above.  Run by the whole block (block = true) or, for a rebuild, by warp 0 alone.
+template <bool kBlock>
+__device__ __forceinline__ void build_tree(const Tree& T, double* const* P, double* const* Sb, const double* pw,
+                                           int warp, int nw, int lane) {
 #pragma unroll
   for (int h = 0; h < kMaxL; ++h) {
     if (h > T.top) continue;  // (continue, not break: keeps the loop unrolled, P[h] in registers)
@@ -148,8 +124,57 @@ __global__ void __launch_bounds__(512, 1) k2_draw(DrawJobs jobs, unsigned* statu
       *reinterpret_cast<double2*>(P[h] + c) = make_double2(__dadd_rn(ex, a), s);
       if (lane == 31 && h < T.top) tot[node] = s;
     }
-    __syncthreads();
+    if (kBlock)
+      __syncthreads();
+    else
+      __syncwarp();
   }
+}
+
+// kLeafSmem: the level-0 prefixes live in shared memory (every job's axis is at most
+// kDrawSmemMaxLen long), so all tree accesses compile to shared-memory loads.
+// up_global: the upper levels do not fit shared memory either (axes beyond ~1.7M entries).
+template <bool kLeafSmem>
+__global__ void __launch_bounds__(512, 1) k2_draw(DrawJobs jobs, unsigned* status, int up_global) {
+  const DrawJob job = jobs.j[blockIdx.x];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int64_t len = job.len;
+  const Tree T = make_tree(len);
+  extern __shared__ __align__(16) double sm_draw[];
+  constexpr bool p_in_smem = kLeafSmem;
+  double* P[kMaxL];
+  P[0] = p_in_smem ? sm_draw : job.work + rup64(len);
+  double* up = p_in_smem ? sm_draw + rup64(len) : (up_global ? job.work + 3 * rup64(len) : sm_draw);
+#pragma unroll
+  for (int h = 1; h < kMaxL; ++h) P[h] = up + T.off[h];
+  const int64_t nodes0 = rup64((len + kFan - 1) / kFan);
+  double* Sb[2] = {up + T.upper, up + T.upper + nodes0};
+  double* pw = job.work;  // exact weights
+  double* uni = job.work + 2 * rup64(len);
+  // exact weights (zero padded) and the count of positives
+  __shared__ int s_pos[32];
+  int pos = 0;
+  for (int64_t t = tid; t < rup64(len); t += blockDim.x) {
+    const double v = t < len ? job.probs[t] : 0.0;
+    pw[t] = v;
+    pos += v > 0.0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) pos += __shfl_xor_sync(0xffffffffu, pos, o);
+  if (lane == 0) s_pos[warp] = pos;
+  // the draw's uniforms: uniform t is the stream advanced by t (numpy draws one
+  // double per draw, columns first), computed in parallel instead of in the chain.
+  // count > len always fails the positives check below, so len uniforms suffice.
+  const int64_t nuni = job.count < len ? job.count : len;
+  for (int64_t t = tid; t < nuni; t += blockDim.x) {
+    Pcg64 g;
+    g.state = u128{job.st_hi, job.st_lo};
+    g.inc = u128{job.inc_hi, job.inc_lo};
+    g.advance((uint64_t)t);
+    uni[t] = g.next_double();
+  }
+  __syncthreads();
+  build_tree<true>(T, P, Sb, pw, warp, nw, lane);
   if (warp != 0) return;
   int positive = 0;
   for (int w = 0; w < nw; ++w) positive += s_pos[w];
@@ -161,8 +186,20 @@ __global__ void __launch_bounds__(512, 1) k2_draw(DrawJobs jobs, unsigned* statu
   }
   const double u53 = 1.0 / 9007199254740992.0;
   const int count = (int)job.count;
-  // tree rounding per earlier removal: one per level
-  const double slack = (double)len + 70.0 + (double)(T.top + 2) * (double)count;
+  const double* rootp = (T.top == 0 ? P[0] : up + T.root) + (kFan - 1);  // the root's last inclusive prefix
+  // Error bookkeeping, in units of 2^-53 (module header).  Let E bound |tree prefix - exact
+  // prefix| over every position.  The build leaves at most 7 roundings per stored prefix per
+  // level, inherited upward: E0 = c_build * total0 (total0 = the total the tree was built at).
+  // A removal subtracts the leaf's prefix difference wl from the entries after it on every
+  // level: the drawn leaf's own build error (two adjacent within-node prefixes, <= 14 * total0)
+  // leaves with it, and every level adds one rounding of entries no larger than the current
+  // total (plus wl's own): E += 14 * total0 + c_rem * total.  numpy's sequential cumsum is within
+  // (len + 2) * total of the exact prefix and the descent adds one rounding per level (c_np).
+  // A draw is proved when the uniform is 2 (c_np * total + E) away from both neighbours.
+  const double c_build = 4.0 * (T.top + 1) * (T.top + 2) + 16.0;
+  const double c_rem = (double)(T.top + 3);
+  const double c_np = (double)len + 2.0 + (double)(T.top + 2);
+  double total0 = *rootp, err_acc = c_build * total0;
   // uniforms in registers, 32 draws per block (lane l holds draw 32 b + l), the next block
   // prefetched a whole block ahead: an L2 round trip per draw would otherwise be the chain's
   // longest link
@@ -174,7 +211,15 @@ __global__ void __launch_bounds__(512, 1) k2_draw(DrawJobs jobs, unsigned* statu
       unext = t + 32 + lane < count ? uni[t + 32 + lane] : 0.0;
     }
     const double u = __shfl_sync(0xffffffffu, ublk, t & 31);  // identical on every lane
-    const double total = (T.top == 0 ? P[0] : up + T.root)[kFan - 1];  // the root's last inclusive prefix
+    double total = *rootp;
+    if (err_acc > c_np * total && total > 0.0) {
+      // the tree's rounding (from heavier, already drawn weights) outweighs numpy's own:
+      // rebuild it from the exact remaining weights
+      build_tree<false>(T, P, Sb, pw, 0, 1, lane);
+      total = *rootp;
+      total0 = total;
+      err_acc = c_build * total0;
+    }
     if (!(total > 0.0)) {
       if (lane == 0) atomicOr(status, (unsigned)ST_SAMPLING);
       for (int q = t + lane; q < count; q += 32) job.out[q] = 0;
@@ -221,9 +266,10 @@ __global__ void __launch_bounds__(512, 1) k2_draw(DrawJobs jobs, unsigned* statu
     }
     int64_t idx = g;
     if (ok) {
-      const double delta = 2.0 * slack * u53 * (total * (1.0 + 1e-12));
+      const double delta = 2.0 * u53 * (c_np * total + err_acc) * (1.0 + 1e-9);
       ok = (lower <= target - delta) && (upper > target + delta) && (wl > 0.0);
     }
+    err_acc += (14.0 * total0 + c_rem * total) * (1.0 + 1e-9);
     if (ok) {
       // remove: entries at and after the path position of every node on the path
 #pragma unroll
@@ -282,27 +328,29 @@ bool launch_draw(const DrawJob* jobs, int njobs, unsigned* status, cudaStream_t 
     if (jobs[k].len > kMaxDrawLen) return false;
   DrawJobs j{};
   size_t smem = 0;
+  bool leaf_smem = true, up_global = false;
   for (int k = 0; k < njobs && k < 2; ++k) {
     j.j[k] = jobs[k];
     const int64_t len = jobs[k].len;
     const int64_t need = draw_smem_doubles(len);
+    if (need == 0) up_global = true;
     if ((size_t)need * sizeof(double) > smem) smem = (size_t)need * sizeof(double);
+    leaf_smem = leaf_smem && len <= kDrawSmemMaxLen;
   }
-  bool leaf_smem = true;
-  for (int k = 0; k < njobs && k < 2; ++k) leaf_smem = leaf_smem && jobs[k].len <= kDrawSmemMaxLen;
-  static bool attr = false;
-  if (!attr) {
+  if (up_global) smem = 0;  // one launch, one layout: both jobs keep their tree in global memory
+  // the large-shared-memory attribute, once per device (cudaFuncSetAttribute is per device)
+  static std::atomic<unsigned> attr_done{0};
+  if (first_on_device(attr_done)) {
     // 227 KB minus the kernel's static shared memory (a failing attribute call
     // would otherwise surface as the launch's error)
-    cudaFuncSetAttribute(k2_draw<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);
-    cudaFuncSetAttribute(k2_draw<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);
-    attr = true;
+    cudaFuncSetAttribute(k2_draw<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDrawSmemCap);
+    cudaFuncSetAttribute(k2_draw<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDrawSmemCap);
   }
   ++::qcur::g_launches;
-  if (leaf_smem)
-    k2_draw<true><<<njobs, 512, smem, st>>>(j, status);
+  if (leaf_smem && !up_global)
+    k2_draw<true><<<njobs, 512, smem, st>>>(j, status, 0);
   else
-    k2_draw<false><<<njobs, 512, smem, st>>>(j, status);
+    k2_draw<false><<<njobs, 512, smem, st>>>(j, status, up_global ? 1 : 0);
   return true;
 }
 

@@ -275,10 +275,9 @@ void launch_colstrip(const double* X, int64_t m, int64_t n, int64_t ldx, double*
 void launch_pairwise(const double* data, int64_t nseg, int64_t seg_stride, const DevPairwise& pw, double* scratch,
                      double* out, cudaStream_t st, bool with_top, bool reverse) {
   size_t smem = (size_t)(kChunkMax + kChunkMax / 8 + 8) * sizeof(double);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<unsigned> attr_set{0};
+  if (first_on_device(attr_set)) {
     cudaFuncSetAttribute(pairwise_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_set = true;
   }
   // dynamic smem: leaf sums and the chunk's tree nodes only (the data streams from HBM)
   size_t need = (size_t)(pw.max_chunk_len / 4 + 16) * sizeof(double);
@@ -322,10 +321,9 @@ bool finalize_supported(const DevPairwise& fpw, const DevPairwise& cpw, const De
 void launch_finalize(const double* flat, const DevPairwise& fpw, const double* colsum, const DevPairwise& cpw,
                      double* col, const double* rowsum, const DevPairwise& rpw, double* row, unsigned* status,
                      cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<unsigned> attr_set{0};
+  if (first_on_device(attr_set)) {
     cudaFuncSetAttribute(k1_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
   }
   ++::qcur::g_launches;
   k1_finalize<<<2, kFinThreads, finalize_smem(fpw, cpw.length, rpw.length), st>>>(

@@ -1052,10 +1052,9 @@ void oz_launch_gemm(const OzJob* jobs, int nj, int L, cudaStream_t st) {
     P.p[l] = kOzModuli[l];
     P.pinv[l] = 1.0 / (double)kOzModuli[l];
   }
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned> attr{0};
+  if (first_on_device(attr)) {
     cudaFuncSetAttribute(k_oz_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM);
-    attr = true;
   }
   const int grid = P.total < oz_sms() ? P.total : oz_sms();
   const OzJob& j1 = nj > 1 ? jobs[1] : jobs[0];

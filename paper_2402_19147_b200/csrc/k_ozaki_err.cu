@@ -476,10 +476,9 @@ int launch_ozaki_error_gemm(const double* X, int64_t ldx, int64_t m, int64_t n, 
   p.total = pl.total;
   // kind::i8: D = s32, A/B signed int8, K-major, N = 80, M = 128
   p.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OE_BN >> 3) << 17) | ((uint32_t)(OE_BM >> 4) << 24);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned> attr{0};
+  if (first_on_device(attr)) {
     cudaFuncSetAttribute(k_oe_err, cudaFuncAttributeMaxDynamicSharedMemorySize, OE_SMEM);
-    attr = true;
   }
   const int grid = pl.total < oe_sms() ? pl.total : oe_sms();
   ++::qcur::g_launches;

@@ -859,10 +859,9 @@ void launch_k2(const CUtensorMap* ta, const CUtensorMap* tb, const CUtensorMap& 
                cudaStream_t st) {
   using CF = Cfg<BM, BN, EPI>;
   auto fn = qgemm_kernel<BM, BN, OPA, OPB, EPI>;
-  static bool set = false;
-  if (!set) {
+  static std::atomic<unsigned> set{0};
+  if (first_on_device(set)) {
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM);
-    set = true;
   }
   ++::qcur::g_launches;
   fn<<<grid, CF::THREADS, CF::SMEM, st>>>(ta[0], tb[0], ta[1], tb[1], tx, kp);

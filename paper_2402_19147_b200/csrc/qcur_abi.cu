@@ -1032,6 +1032,23 @@ int reset_status(qcur_ctx* ctx) {
 
 }  // namespace
 
+// Every entry point runs on its context's device and leaves the caller's current
+// device as it found it (a process may drive several GPUs from one thread).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(const qcur_ctx* ctx) {
+    if (!ctx) return;
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != ctx->device) cudaSetDevice(ctx->device);
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 // ===========================================================================
 // extern "C"
 // ===========================================================================
@@ -1045,7 +1062,14 @@ int qcur_create(int device, qcur_ctx** out) {
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0) return QCUR_E_CUDA;
   if (device < 0 || device >= ndev) return QCUR_E_PARAMETER;
+  int prev_device = 0;
+  cudaGetDevice(&prev_device);
   if (cudaSetDevice(device) != cudaSuccess) return QCUR_E_CUDA;
+  // restore the caller's device however this function returns
+  struct Restore {
+    int d;
+    ~Restore() { cudaSetDevice(d); }
+  } restore{prev_device};
   qcur_ctx* ctx = new qcur_ctx();
   ctx->device = device;
   cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
@@ -1081,6 +1105,7 @@ int qcur_create(int device, qcur_ctx** out) {
 }
 
 void qcur_destroy(qcur_ctx* ctx) {
+  DeviceGuard device_guard_(ctx);
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
@@ -1116,22 +1141,26 @@ unsigned qcur_last_info(const qcur_ctx* ctx) {
 }
 
 int qcur_set_stream(qcur_ctx* ctx, void* s) {
+  DeviceGuard device_guard_(ctx);
   if (!ctx) return QCUR_E_PARAMETER;
   ctx->stream = (cudaStream_t)s;
   return QCUR_OK;
 }
 
 int qcur_synchronize(qcur_ctx* ctx) {
+  DeviceGuard device_guard_(ctx);
   cudaError_t e = cudaStreamSynchronize(ctx->stream);
   return e == cudaSuccess ? QCUR_OK : ctx->cuda_fail(e, "synchronize");
 }
 
 int qcur_set_kappa_limit(qcur_ctx* ctx, double limit) {
+  DeviceGuard device_guard_(ctx);
   if (!ctx || !(limit > 0.0)) return QCUR_E_PARAMETER;
   ctx->kappa_limit = limit;
   return QCUR_OK;
 }
 int qcur_force_robust(qcur_ctx* ctx, int on) {
+  DeviceGuard device_guard_(ctx);
   if (!ctx) return QCUR_E_PARAMETER;
   ctx->force_robust = on != 0;
   return QCUR_OK;
@@ -1166,12 +1195,14 @@ int qcur_rng_random(uint64_t state[4], int64_t count, double* out) {
 }
 
 int qcur_memcpy(qcur_ctx* ctx, void* dst, const void* src, size_t bytes, int kind) {
+  DeviceGuard device_guard_(ctx);
   cudaError_t e = cudaMemcpyAsync(dst, src, bytes, (cudaMemcpyKind)kind, ctx->stream);
   return e == cudaSuccess ? QCUR_OK : ctx->cuda_fail(e, "memcpy");
 }
 
 int qcur_upload_planar(qcur_ctx* ctx, const double* a0, const double* a1, const double* a2, const double* a3,
                        int64_t m, int64_t n, double* x_dev) {
+  DeviceGuard device_guard_(ctx);
   if (m < 1 || n < 1) return ctx->fail(QCUR_E_SHAPE, "degenerate matrix shape (%lld, %lld)", (long long)m, (long long)n);
   const size_t pb = (size_t)(m * n) * sizeof(double);
   int rc = ctx->reserve(4 * pb + 1024);
@@ -1190,6 +1221,7 @@ int qcur_upload_planar(qcur_ctx* ctx, const double* a0, const double* a1, const 
 
 int qcur_upload_length(qcur_ctx* ctx, const double* a0, const double* a1, const double* a2, const double* a3,
                        int64_t m, int64_t n, double* x_dev, double* col_dev, double* row_dev) {
+  DeviceGuard device_guard_(ctx);
   if (m < 1 || n < 1) return ctx->fail(QCUR_E_SHAPE, "degenerate matrix shape (%lld, %lld)", (long long)m, (long long)n);
   // row chunks of ~32 MB per plane: the copy engine streams chunk k+1 while the SMs convert
   // chunk k and carry numpy's sequential column sums through it (colstrip with acc_in)
@@ -1244,6 +1276,7 @@ int qcur_upload_length(qcur_ctx* ctx, const double* a0, const double* a1, const 
 
 int qcur_download_planar(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int64_t ld, double* a0,
                          double* a1, double* a2, double* a3) {
+  DeviceGuard device_guard_(ctx);
   const size_t pb = (size_t)(m * n) * sizeof(double);
   int rc = ctx->reserve(4 * pb + 1024);
   if (rc) return rc;
@@ -1261,6 +1294,7 @@ int qcur_download_planar(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t 
 }
 
 int qcur_length_distributions(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, double* col, double* row) {
+  DeviceGuard device_guard_(ctx);
   if (m < 1 || n < 1) return ctx->fail(QCUR_E_SHAPE, "degenerate matrix shape");
   int rc = ctx->reserve(length_ws_bytes(ctx, m, n));
   if (rc) return rc;
@@ -1270,6 +1304,7 @@ int qcur_length_distributions(qcur_ctx* ctx, const double* x_dev, int64_t m, int
 }
 
 int qcur_uniform_distributions(qcur_ctx* ctx, int64_t m, int64_t n, double* col, double* row) {
+  DeviceGuard device_guard_(ctx);
   if (m < 1 || n < 1) return ctx->fail(QCUR_E_PARAMETER, "dimensions must be positive, got (%lld, %lld)",
                                        (long long)m, (long long)n);
   launch_fill(col, n, 1.0 / (double)n, ctx->stream);
@@ -1280,6 +1315,7 @@ int qcur_uniform_distributions(qcur_ctx* ctx, int64_t m, int64_t n, double* col,
 
 int qcur_draw_indices(qcur_ctx* ctx, const double* probs, int64_t size, int64_t count, uint64_t state[4],
                       int64_t* out) {
+  DeviceGuard device_guard_(ctx);
   if (size < 1) return ctx->fail(QCUR_E_SHAPE, "probs must be a non-empty 1-D array");
   if (count < 1) return ctx->fail(QCUR_E_PARAMETER, "count must be positive, got %lld", (long long)count);
   int rc = ctx->reserve((size_t)draw_work_doubles(size) * 8 + 4096);
@@ -1297,6 +1333,7 @@ int qcur_draw_indices(qcur_ctx* ctx, const double* probs, int64_t size, int64_t 
 int qcur_qmcur(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, const double* colp, const double* rowp,
                int64_t c, int64_t r, const uint64_t state[4], int64_t* J, int64_t* I, double* C, double* U,
                double* R) {
+  DeviceGuard device_guard_(ctx);
   if (m < 1 || n < 1 || c < 1 || r < 1 || c > n || r > m)
     return ctx->fail(QCUR_E_SHAPE, "qmcur: bad sizes m=%lld n=%lld c=%lld r=%lld", (long long)m, (long long)n,
                      (long long)c, (long long)r);
@@ -1310,6 +1347,7 @@ int qcur_qmcur(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, const d
 int qcur_qmcur_ex(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, const double* colp, const double* rowp,
                   int64_t c, int64_t r, const uint64_t state[4], int core, int64_t* J, int64_t* I, double* C,
                   double* U, double* R) {
+  DeviceGuard device_guard_(ctx);
   if (core != QCUR_CORE_PROJECTION && core != QCUR_CORE_INTERSECTION)
     return ctx->fail(QCUR_E_PARAMETER, "unknown core mode %d", core);
   if (m < 1 || n < 1 || c < 1 || r < 1 || c > n || r > m) return ctx->fail(QCUR_E_SHAPE, "qmcur: bad sizes");
@@ -1324,6 +1362,7 @@ int qcur_qmcur_host(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, co
                     const double* rowp, int64_t c, int64_t r, const uint64_t state[4], int core, int64_t* J,
                     int64_t* I, double* C, double* U, double* R, int64_t* J_host, int64_t* I_host,
                     double* const C_host[4], double* const U_host[4], double* const R_host[4]) {
+  DeviceGuard device_guard_(ctx);
   if (core != QCUR_CORE_PROJECTION && core != QCUR_CORE_INTERSECTION)
     return ctx->fail(QCUR_E_PARAMETER, "unknown core mode %d", core);
   if (m < 1 || n < 1 || c < 1 || r < 1 || c > n || r > m) return ctx->fail(QCUR_E_SHAPE, "qmcur: bad sizes");
@@ -1347,6 +1386,7 @@ int qcur_qmcur_host(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, co
 
 int qcur_cur_error(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, const double* C, int64_t c,
                    const double* U, const double* R, int64_t r, double psnr_scale, double* out4) {
+  DeviceGuard device_guard_(ctx);
   int rc = ctx->reserve(error_ws_bytes(m, n, c, r));
   if (rc) return rc;
   return error_impl(ctx, x_dev, m, n, C, c, U, R, r, psnr_scale, out4);
@@ -1354,6 +1394,7 @@ int qcur_cur_error(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, con
 
 int qcur_cur_given(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, const int64_t* J, int64_t c,
                    const int64_t* I, int64_t r, double* C, double* U, double* R) {
+  DeviceGuard device_guard_(ctx);
   if (m < 1 || n < 1 || c < 1 || r < 1 || c > n || r > m) return ctx->fail(QCUR_E_SHAPE, "cur_given: bad sizes");
   int rc = ctx->reserve(qmcur_ws_bytes(m, n, c, r) + 4096);
   if (rc) return rc;
@@ -1367,6 +1408,7 @@ int qcur_cur_given(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, con
 
 int qcur_qgemv(qcur_ctx* ctx, int op, int64_t m, int64_t n, const double* a_dev, int64_t lda, const double* x_dev,
                double* y_dev) {
+  DeviceGuard device_guard_(ctx);
   if (m < 1 || n < 1 || lda < n) return ctx->fail(QCUR_E_SHAPE, "qgemv: bad sizes");
   if (op != QCUR_OP_N && op != QCUR_OP_H) return ctx->fail(QCUR_E_PARAMETER, "qgemv: op must be N or H");
   launch_qgemv(op, a_dev, m, n, lda, x_dev, y_dev, ctx->stream);
@@ -1376,6 +1418,7 @@ int qcur_qgemv(qcur_ctx* ctx, int op, int64_t m, int64_t n, const double* a_dev,
 
 int qcur_project_observed(qcur_ctx* ctx, const double* x_dev, const double* y_dev, const unsigned char* mask_dev,
                           int64_t m, int64_t n, double* out_dev) {
+  DeviceGuard device_guard_(ctx);
   if (m < 1 || n < 1) return ctx->fail(QCUR_E_SHAPE, "degenerate matrix shape");
   launch_project_observed(x_dev, y_dev, mask_dev, m, n, out_dev, ctx->stream);
   CK_LAUNCH(ctx, "project_observed");
@@ -1386,6 +1429,7 @@ int qcur_complete_sweep(qcur_ctx* ctx, const double* cur_dev, const double* y_de
                         int64_t m, int64_t n, int strategy, const uint64_t state[4], int64_t count,
                         const int64_t* fixed_J, const int64_t* fixed_I, int64_t* J_out, int64_t* I_out,
                         double* out_dev, double* stats4_dev) {
+  DeviceGuard device_guard_(ctx);
   const int64_t c = count, r = count;
   if (m < 1 || n < 1 || c < 1 || c > n || r > m) return ctx->fail(QCUR_E_SHAPE, "complete_sweep: bad sizes");
   if ((fixed_J == nullptr) != (fixed_I == nullptr))
@@ -1442,6 +1486,7 @@ int qcur_complete_sweep(qcur_ctx* ctx, const double* cur_dev, const double* y_de
 int qcur_approx(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int strategy, const uint64_t state[4],
                 int64_t c, int64_t r, int64_t* J, int64_t* I, double* C, double* U, double* R, double psnr_scale,
                 int core, double* err4) {
+  DeviceGuard device_guard_(ctx);
   if (m < 1 || n < 1 || c < 1 || r < 1 || c > n || r > m) return ctx->fail(QCUR_E_SHAPE, "qcur_approx: bad sizes");
   if (strategy != QCUR_STRATEGY_LENGTH && strategy != QCUR_STRATEGY_UNIFORM)
     return ctx->fail(QCUR_E_PARAMETER, "unknown strategy %d", strategy);
@@ -1488,17 +1533,21 @@ int qcur_approx(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int st
   return rc;
 }
 
-int qcur_check(qcur_ctx* ctx) { return sync_status(ctx); }
+int qcur_check(qcur_ctx* ctx) {
+  DeviceGuard device_guard_(ctx); return sync_status(ctx); }
 
 int qcur_status_async(qcur_ctx* ctx, unsigned* host_dst) {
+  DeviceGuard device_guard_(ctx);
   cudaError_t e = cudaMemcpyAsync(host_dst, ctx->status_dev, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(ctx->status_dev, 0, sizeof(unsigned), ctx->stream);
   return e == cudaSuccess ? QCUR_OK : ctx->cuda_fail(e, "status_async");
 }
 
-int qcur_status_map(qcur_ctx* ctx, unsigned bits) { return map_status(ctx, bits); }
+int qcur_status_map(qcur_ctx* ctx, unsigned bits) {
+  DeviceGuard device_guard_(ctx); return map_status(ctx, bits); }
 
 int qcur_profile(qcur_ctx* ctx, int on) {
+  DeviceGuard device_guard_(ctx);
   if (!ctx) return QCUR_E_PARAMETER;
   cudaStreamSynchronize(ctx->stream);
   ctx->prof.marks.clear();
@@ -1510,6 +1559,7 @@ int qcur_profile(qcur_ctx* ctx, int on) {
 }
 
 int qcur_profile_read(qcur_ctx* ctx, char* buf, size_t len) {
+  DeviceGuard device_guard_(ctx);
   if (!ctx || !buf || len == 0) return QCUR_E_PARAMETER;
   cudaError_t e = cudaStreamSynchronize(ctx->stream);
   if (e != cudaSuccess) return ctx->cuda_fail(e, "profile sync");
@@ -1568,6 +1618,7 @@ int qcur_pairwise_host(const double* data, int64_t n, double* out) {
 
 int qcur_qgemm(qcur_ctx* ctx, int opA, int opB, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
                int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
+  DeviceGuard device_guard_(ctx);
   if (M < 0 || N < 0 || K < 0) return ctx->fail(QCUR_E_SHAPE, "negative gemm size");
   GemmArgs g = gargs(M, N, K, A, lda, opA, B, ldb, opB, C, ldc, alpha, beta);
   int rc = ctx->reserve(qgemm_workspace_bytes(g) + 4096);
@@ -1586,6 +1637,7 @@ int qcur_qgemm(qcur_ctx* ctx, int opA, int opB, int64_t M, int64_t N, int64_t K,
 }
 
 int qcur_pseudoinverse(qcur_ctx* ctx, const double* a_dev, int64_t m, int64_t n, double tol, double* out_dev) {
+  DeviceGuard device_guard_(ctx);
   if (m < 1 || n < 1) return ctx->fail(QCUR_E_SHAPE, "degenerate matrix shape");
   int rc = ctx->reserve(pinv_ws_bytes(m, n) + 4096);
   if (rc) return rc;
@@ -1595,6 +1647,7 @@ int qcur_pseudoinverse(qcur_ctx* ctx, const double* a_dev, int64_t m, int64_t n,
 }
 
 int qcur_frobenius_sq(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, double* out_host) {
+  DeviceGuard device_guard_(ctx);
   const int64_t nparts = 296;
   int rc = ctx->reserve((size_t)nparts * 16 + 1024);
   if (rc) return rc;
@@ -1609,6 +1662,7 @@ int qcur_frobenius_sq(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, 
 
 int qcur_synth_lowrank(qcur_ctx* ctx, int64_t m, int64_t n, int64_t k, uint64_t seed, double noise,
                        int noise_relative, double* x_dev) {
+  DeviceGuard device_guard_(ctx);
   if (m < 1 || n < 1 || k < 1) return ctx->fail(QCUR_E_PARAMETER, "synth: bad sizes");
   const int64_t nparts = 296;
   GemmArgs gprobe = gargs(m, n, k, nullptr, 0, 0, nullptr, 0, 1, nullptr, 0);
@@ -1637,11 +1691,14 @@ int qcur_synth_lowrank(qcur_ctx* ctx, int64_t m, int64_t n, int64_t k, uint64_t 
   return QCUR_OK;
 }
 
-double qcur_fp64_peak_tflops(qcur_ctx* ctx) { return run_dmma_peak(ctx->sms, ctx->stream); }
-double qcur_int8_peak_tops(qcur_ctx* ctx) { return run_i8_peak(ctx->sms, ctx->stream); }
+double qcur_fp64_peak_tflops(qcur_ctx* ctx) {
+  DeviceGuard device_guard_(ctx); return run_dmma_peak(ctx->sms, ctx->stream); }
+double qcur_int8_peak_tops(qcur_ctx* ctx) {
+  DeviceGuard device_guard_(ctx); return run_i8_peak(ctx->sms, ctx->stream); }
 
 int qcur_synth_lowrank_rows(qcur_ctx* ctx, int64_t m, int64_t n, int64_t k, uint64_t seed, double noise,
                             int64_t row0, int64_t rows, double* x_dev) {
+  DeviceGuard device_guard_(ctx);
   if (m < 1 || n < 1 || k < 1 || row0 < 0 || rows < 1 || row0 + rows > m)
     return ctx->fail(QCUR_E_PARAMETER, "synth_lowrank_rows: bad sizes");
   GemmArgs gprobe = gargs(rows, n, k, nullptr, 0, 0, nullptr, 0, 1, nullptr, 0);
@@ -1666,6 +1723,7 @@ int qcur_synth_lowrank_rows(qcur_ctx* ctx, int64_t m, int64_t n, int64_t k, uint
 // ---- phase-level entry points (row-block sharded QMCUR, paper_2402_19147_b200/rowshard.py) ----
 int qcur_colsums_seq(qcur_ctx* ctx, const double* x_dev, int64_t rows, int64_t n, const double* acc_in,
                      double* colsum_out, double* sq_out) {
+  DeviceGuard device_guard_(ctx);
   if (rows < 1 || n < 1) return ctx->fail(QCUR_E_SHAPE, "colsums_seq: bad sizes");
   launch_colstrip(x_dev, rows, n, n, sq_out, colsum_out, ctx->stream, acc_in);
   CK_LAUNCH(ctx, "colsums_seq");
@@ -1674,6 +1732,7 @@ int qcur_colsums_seq(qcur_ctx* ctx, const double* x_dev, int64_t rows, int64_t n
 
 int qcur_pairwise_sums(qcur_ctx* ctx, const double* data, int64_t nseg, int64_t stride, int64_t length,
                        double* out) {
+  DeviceGuard device_guard_(ctx);
   if (nseg < 1 || length < 0) return ctx->fail(QCUR_E_SHAPE, "pairwise_sums: bad sizes");
   int rc = ctx->reserve(pairwise_scratch_bytes(ctx, nseg, length) + 4096);
   if (rc) return rc;
@@ -1681,6 +1740,7 @@ int qcur_pairwise_sums(qcur_ctx* ctx, const double* data, int64_t nseg, int64_t 
 }
 
 int qcur_vec_div(qcur_ctx* ctx, const double* in, int64_t len, const double* denom, double* out) {
+  DeviceGuard device_guard_(ctx);
   launch_scale(in, len, denom, out, ctx->status_dev, ST_DEGENERATE, ctx->stream);
   CK_LAUNCH(ctx, "vec_div");
   return QCUR_OK;
@@ -1688,12 +1748,14 @@ int qcur_vec_div(qcur_ctx* ctx, const double* in, int64_t len, const double* den
 
 int qcur_gather_cols(qcur_ctx* ctx, const double* x_dev, int64_t rows, int64_t n, const int64_t* J, int64_t c,
                      double* out) {
+  DeviceGuard device_guard_(ctx);
   launch_gather_cols(x_dev, rows, n, J, c, out, ctx->stream);
   CK_LAUNCH(ctx, "gather_cols");
   return QCUR_OK;
 }
 
 int qcur_gather_rows(qcur_ctx* ctx, const double* x_dev, int64_t n, const int64_t* I, int64_t r, double* out) {
+  DeviceGuard device_guard_(ctx);
   launch_gather_rows(x_dev, n, n, I, r, out, ctx->stream);
   CK_LAUNCH(ctx, "gather_rows");
   return QCUR_OK;
@@ -1701,6 +1763,7 @@ int qcur_gather_rows(qcur_ctx* ctx, const double* x_dev, int64_t n, const int64_
 
 int qcur_qgemm_ex(qcur_ctx* ctx, int opA, int opB, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
                   int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, int flags) {
+  DeviceGuard device_guard_(ctx);
   GemmArgs g = with_flags(gargs(M, N, K, A, lda, opA, B, ldb, opB, C, ldc, alpha, beta), flags & 1, (flags >> 1) & 1);
   int rc = ctx->reserve(qgemm_workspace_bytes(g) + 4096);
   if (rc) return rc;
@@ -1719,6 +1782,7 @@ int qcur_qgemm_ex(qcur_ctx* ctx, int opA, int opB, int64_t M, int64_t N, int64_t
 // to the same accuracy as after full convergence (qsvd(x, k) returns only them).
 int qcur_qsvd_jacobi_top(qcur_ctx* ctx, const double* a, int64_t m, int64_t n, int64_t lda, double* acm,
                          double* vcm, double* sigma, int64_t k, int* sweeps_out) {
+  DeviceGuard device_guard_(ctx);
   if (m < 1 || n < 1 || m < n) return ctx->fail(QCUR_E_SHAPE, "qsvd_jacobi: need m >= n >= 1");
   if (k < 0 || k > n) return ctx->fail(QCUR_E_PARAMETER, "qsvd_jacobi: need 0 <= k <= n");
   const bool trunc = k > 0 && k < n;
@@ -1774,10 +1838,12 @@ int qcur_qsvd_jacobi_top(qcur_ctx* ctx, const double* a, int64_t m, int64_t n, i
 
 int qcur_qsvd_jacobi(qcur_ctx* ctx, const double* a, int64_t m, int64_t n, int64_t lda, double* acm, double* vcm,
                      double* sigma, int* sweeps_out) {
+  DeviceGuard device_guard_(ctx);
   return qcur_qsvd_jacobi_top(ctx, a, m, n, lda, acm, vcm, sigma, 0, sweeps_out);
 }
 
 int qcur_set_gemm_mode(qcur_ctx* ctx, int mode) {
+  DeviceGuard device_guard_(ctx);
   if (mode < 0 || mode > 2) return ctx->fail(QCUR_E_PARAMETER, "gemm mode must be 0 (auto), 1 (fp64) or 2 (int8)");
   ctx->gemm_mode = mode;
   return QCUR_OK;
@@ -1785,6 +1851,7 @@ int qcur_set_gemm_mode(qcur_ctx* ctx, int mode) {
 
 int qcur_qgemm_herm_int8(qcur_ctx* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                          const double* B, int64_t ldb, double* C, int64_t ldc) {
+  DeviceGuard device_guard_(ctx);
   if (M < 1 || N < 1 || K < 1 || !ozaki_herm_supported(K, M, N))
     return ctx->fail(QCUR_E_SHAPE, "qgemm_herm_int8: bad shape");
   const int same = A == B && M == N && lda == ldb;
@@ -1801,6 +1868,7 @@ int qcur_qgemm_herm_int8(qcur_ctx* ctx, int64_t M, int64_t N, int64_t K, const d
 
 int qcur_qgemm_int8(qcur_ctx* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
                     int64_t ldb, double* C, int64_t ldc, int nmod) {
+  DeviceGuard device_guard_(ctx);
   if (nmod == 0) nmod = kOzakiModuli;
   if (M < 1 || N < 1 || K < 1 || !ozaki_supported(M, K, N)) return ctx->fail(QCUR_E_SHAPE, "qgemm_int8: bad shape");
   if (nmod < 14 || nmod > 15) return ctx->fail(QCUR_E_PARAMETER, "qgemm_int8: modulus count must be 14 or 15");
@@ -1816,6 +1884,7 @@ int qcur_qgemm_int8(qcur_ctx* ctx, int64_t M, int64_t N, int64_t K, const double
 }
 
 int qcur_chol_inv(qcur_ctx* ctx, const double* G, int64_t q, double* X) {
+  DeviceGuard device_guard_(ctx);
   if (q < 1) return ctx->fail(QCUR_E_SHAPE, "chol_inv: bad size");
   if (q <= chol_cluster_qmax()) {
     CholJob j{G, nullptr, X, ST_CHOL_FAIL_C};
@@ -1829,6 +1898,7 @@ int qcur_chol_inv(qcur_ctx* ctx, const double* G, int64_t q, double* X) {
 }
 
 int qcur_series_l2inv(qcur_ctx* ctx, const double* G2, int64_t q, double* L2inv) {
+  DeviceGuard device_guard_(ctx);
   GemmArgs probe = gargs(q, q, q, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0);
   int rc = ctx->reserve(4 * qbytes(q, q) + qgemm_workspace_bytes(probe) + 8192);
   if (rc) return rc;
@@ -1845,12 +1915,14 @@ int qcur_series_l2inv(qcur_ctx* ctx, const double* G2, int64_t q, double* L2inv)
 }
 
 int qcur_kappa_check(qcur_ctx* ctx, const double* G1, const double* F, int64_t q) {
+  DeviceGuard device_guard_(ctx);
   launch_kappa_check(G1, F, q, ctx->kappa_limit, ctx->status_dev, ST_CHOL_FAIL_C, ctx->stream);
   CK_LAUNCH(ctx, "kappa");
   return QCUR_OK;
 }
 
 int qcur_factor(qcur_ctx* ctx, const double* src, int zh, int64_t p, int64_t q, double* Q, double* F) {
+  DeviceGuard device_guard_(ctx);
   if (p < q || q < 1) return ctx->fail(QCUR_E_SHAPE, "factor: needs a tall block (p >= q)");
   int rc = ctx->reserve(factor_ws_bytes(p, q) + 4096);
   if (rc) return rc;
@@ -1859,6 +1931,7 @@ int qcur_factor(qcur_ctx* ctx, const double* src, int zh, int64_t p, int64_t q, 
 
 int qcur_synth_image(qcur_ctx* ctx, int64_t m, int64_t n, int nterms, uint64_t seed, double noise_std,
                      double* x_dev) {
+  DeviceGuard device_guard_(ctx);
   if (m < 1 || n < 1 || nterms < 1) return ctx->fail(QCUR_E_PARAMETER, "synth_image: bad sizes");
   const int64_t maxlen = m > n ? m : n;
   int rc = ctx->reserve((size_t)(6 * nterms * maxlen + 296 * 6) * 8 + 4096);

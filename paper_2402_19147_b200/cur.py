@@ -314,16 +314,28 @@ def cur_reconstruct(factors: CURFactors) -> QMatrix:
     return from_device(out, dev)
 
 
+def _fancy_index(indices, size: int, what: str, axis: int) -> np.ndarray:
+    """Indices as numpy fancy indexing along an axis of length `size` resolves them."""
+    idx = np.asarray(indices, dtype=np.intp)
+    if idx.ndim != 1 or idx.size == 0:
+        raise ShapeError(f"{what} selection must be a non-empty 1-D index list")
+    bad = (idx < -size) | (idx >= size)
+    if bad.any():
+        raise IndexError(f"index {int(idx[bad][0])} is out of bounds for axis {axis} with size {size}")
+    return np.where(idx < 0, idx + size, idx).astype(np.int64)
+
+
 def stabilized_reconstruct(x, row_indices, col_indices) -> QMatrix:
     """Two-sided projection C pinv(C) X pinv(R) R for given index sets (cur.py:277-286):
     the qmcur core on the device (qcur_cur_given), then C U R."""
     dev = _native.device()
     m, n = (int(v) for v in x.shape)
-    rows = np.array(row_indices, dtype=np.int64).ravel()
-    cols = np.array(col_indices, dtype=np.int64).ravel()
+    # the reference selects through take_cols / take_rows (quat.py:215-225): a 1-D non-empty
+    # index list (else ShapeError), numpy fancy indexing (negative indices wrap, out of range
+    # raises IndexError); columns are taken first (cur.py:282-283)
+    cols = _fancy_index(col_indices, n, "column", 1)
+    rows = _fancy_index(row_indices, m, "row", 0)
     c, r = int(cols.size), int(rows.size)
-    if c < 1 or r < 1 or (cols < 0).any() or (cols >= n).any() or (rows < 0).any() or (rows >= m).any():
-        raise ShapeError("index sets out of range")
     xd = to_device(x, dev)
     J = dev.torch.from_numpy(cols).to(device=f"cuda:{dev.index}")
     I = dev.torch.from_numpy(rows).to(device=f"cuda:{dev.index}")

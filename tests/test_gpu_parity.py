@@ -76,6 +76,36 @@ def test_draw_indices_exact(size, count, seed):
     assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("kind,n,count,plans", [("dominant", 64, 40, 400), ("geometric", 64, 40, 200),
+                                                 ("dominant", 4000, 200, 40), ("geometric", 4000, 200, 20),
+                                                 ("dominant", 40000, 300, 4)])
+def test_draw_dynamic_range(kind, n, count, plans):
+    """Weights spanning 13-30 decades (advisor round 1): the tree's rounding follows the heaviest
+    totals already drawn; every index must still equal numpy's sequential-cumsum draw."""
+    for s in range(plans):
+        g = np.random.default_rng(s)
+        if kind == "dominant":
+            p = g.random(n)
+            p[g.integers(n)] *= 1e13
+        else:
+            p = 10.0 ** (-g.random(n) * 30)
+        p /= p.sum()
+        got = q.draw_indices(p, count, 500 + s)
+        want = O.draw_indices(p, count, np.random.default_rng(500 + s))
+        assert np.array_equal(got, want), (kind, n, s)
+
+
+@pytest.mark.parametrize("size", [1 << 20, 2_000_000])
+def test_draw_long_axis(size):
+    """Axes whose upper tree levels no longer fit shared memory (> ~0.6M entries) keep the tree
+    in global memory instead of failing the launch (advisor round 1)."""
+    p = np.random.default_rng(size).random(size) ** 2
+    p /= p.sum()
+    got = q.draw_indices(p, 64, 9)
+    want = O.draw_indices(p, 64, np.random.default_rng(9))
+    assert np.array_equal(got, want)
+
+
 def test_draw_generator_stream_advances_like_numpy():
     rng_a = np.random.default_rng(7)
     rng_b = np.random.default_rng(7)
