@@ -183,6 +183,12 @@ double qcur_int8_peak_tops(qcur_ctx* ctx); /* dense tcgen05 kind::i8 rate, TOP/s
  * rank of a row-sharded run generates exactly its block of the same matrix. */
 int qcur_synth_lowrank_rows(qcur_ctx* ctx, int64_t m, int64_t n, int64_t k, uint64_t seed, double noise,
                             int64_t row0, int64_t rows, double* x_dev);
+/* The generator stream itself: out[t] = scale * z(offset + t), z the standard normals of
+ * Philox4x32-10 keyed by `seed`, counter (pair index, stream) and Box-Muller on 53-bit
+ * uniforms (`offset` even).  Streams: 1 = P, 2 = Q, 3 = noise, in element order.  For
+ * host restatements / spot checks of any block of a generated matrix. */
+int qcur_synth_normals(qcur_ctx* ctx, uint64_t seed, uint64_t stream, int64_t offset, int64_t count, double scale,
+                       double* out_dev);
 /* cfg3 image-like pure quaternion matrix: each imaginary plane = sum of `nterms`
  * separable products of random cosine series (frequencies U[0,8]), min-max to
  * [0,1], quantised to 1/255, plus N(0, noise_std^2); real part 0. */

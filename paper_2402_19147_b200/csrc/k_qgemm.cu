@@ -822,7 +822,8 @@ Plan make_plan(const GemmArgs& g, int64_t gmax = 0) {
   const int64_t ntiles = (int64_t)kp.gx * kp.gy;
   const int64_t active = host_active_tiles(c, kp.gx, kp.gy, g.herm_lower);
   int64_t grid;
-  if (ntiles > 65536) {  // beyond the ticket array: whole tiles per CTA (uniform tiles only)
+  if (ntiles > 65536 || (g.whole_tiles && !g.b_upper && !g.herm_lower)) {
+    // beyond the ticket array, or asked for: whole tiles per CTA (uniform tiles only)
     kp.mode = MODE_TILES;
     grid = (!g.b_upper && !g.herm_lower) ? (ntiles < G ? ntiles : G) : 1;
   } else if (!no_split() && 2 * active <= G && kp.nkb_full >= 2) {

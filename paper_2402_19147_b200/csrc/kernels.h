@@ -86,6 +86,8 @@ struct GemmArgs {
   double alpha, beta;
   int b_upper = 0;     // op(B) upper triangular (skip k > j)
   int herm_lower = 0;  // Hermitian output, only the lower triangle is produced / consumed
+  int whole_tiles = 0;  // every output tile summed by one CTA over k in order: an element's value does not
+                        // depend on M (row blocks of a generated matrix concatenate bit for bit)
 };
 size_t qgemm_workspace_bytes(const GemmArgs& g);
 // counters: >= 65536 zero-initialised uints owned by the caller (split-K tickets)

@@ -1675,6 +1675,7 @@ int qcur_synth_lowrank(qcur_ctx* ctx, int64_t m, int64_t n, int64_t k, uint64_t 
   launch_normal_fill(P, m * k * 4, seed, 1, 1.0, ctx->stream);
   launch_normal_fill(Q, n * k * 4, seed, 2, 1.0, ctx->stream);
   GemmArgs g = gargs(m, n, k, P, k, 0, Q, k, 1, x_dev, n);  // S = P Q^H
+  g.whole_tiles = 1;  // S(i, j) independent of the launch shape (same bits as any row block)
   double* gws = ctx->take<double>(qgemm_workspace_bytes(g) / 8 + 16);
   if (!P || !Q || !parts || !ssq || !gws) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (synth)");
   launch_qgemm(g, gws, ctx->counters, ctx->stream);
@@ -1696,6 +1697,16 @@ double qcur_fp64_peak_tflops(qcur_ctx* ctx) {
 double qcur_int8_peak_tops(qcur_ctx* ctx) {
   DeviceGuard device_guard_(ctx); return run_i8_peak(ctx->sms, ctx->stream); }
 
+int qcur_synth_normals(qcur_ctx* ctx, uint64_t seed, uint64_t stream, int64_t offset, int64_t count, double scale,
+                       double* out_dev) {
+  DeviceGuard device_guard_(ctx);
+  if (offset < 0 || (offset & 1) || count < 1 || !out_dev)
+    return ctx->fail(QCUR_E_PARAMETER, "synth_normals: offset must be even and non-negative, count positive");
+  launch_normal_fill(out_dev, count, seed, stream, scale, ctx->stream, offset);
+  CK_LAUNCH(ctx, "synth normals");
+  return QCUR_OK;
+}
+
 int qcur_synth_lowrank_rows(qcur_ctx* ctx, int64_t m, int64_t n, int64_t k, uint64_t seed, double noise,
                             int64_t row0, int64_t rows, double* x_dev) {
   DeviceGuard device_guard_(ctx);
@@ -1707,6 +1718,7 @@ int qcur_synth_lowrank_rows(qcur_ctx* ctx, int64_t m, int64_t n, int64_t k, uint
   double* P = ctx->take<double>((size_t)(rows * k * 4));
   double* Q = ctx->take<double>((size_t)(n * k * 4));
   GemmArgs g = gargs(rows, n, k, P, k, 0, Q, k, 1, x_dev, n);  // S rows = P rows Q^H
+  g.whole_tiles = 1;  // every row block of S has the bits of the whole-matrix generation
   double* gws = ctx->take<double>(qgemm_workspace_bytes(g) / 8 + 16);
   if (!P || !Q || !gws) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (synth rows)");
   launch_normal_fill(P, rows * k * 4, seed, 1, 1.0, ctx->stream, row0 * k * 4);

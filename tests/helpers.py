@@ -48,8 +48,19 @@ def exact_rel_error(x, c, u, r) -> float:
 
 
 def assert_error_parity(got: float, ref: float, exact_got: float, exact_ref: float, tol: float = 1e-10) -> None:
-    """North-star error bar (1e-10 relative, fp64): our value within tol of the
-    exact error of our factors, and within tol of the reference's fp64 value up to
-    the reference's own rounding (|ref - exact_ref|)."""
-    assert abs(got - exact_got) <= tol * exact_got, (got, exact_got)
-    assert abs(got - ref) <= tol * ref + abs(ref - exact_ref) + abs(exact_got - exact_ref), (got, ref, exact_ref)
+    """North-star error bar (1e-10 relative, fp64), as two separate claims plus a report:
+
+    1. our fp64 value is within tol of the exact error of OUR factors (evaluation accuracy);
+    2. the exact error of our factors is within tol of the exact error of the REFERENCE's factors
+       (factor quality).  U = C^+ X R^+ minimises ||X - C U R||_F over U, so the true error is
+       stationary in U: two cores within the 1e-9 U bar differ in true error only to second
+       order, far below tol.
+    The raw |got - ref| / ref is printed; by 1 and 2 it is at most 2 tol plus the reference's
+    own fp64 rounding |ref - exact_ref|, which is not ours to bound (it reaches 8e-11 on the
+    golden wide_40x300 case)."""
+    raw = abs(got - ref) / ref if ref else abs(got - ref)
+    print(f"error parity: got {got:.15e} ref {ref:.15e} raw rel diff {raw:.3e}; "
+          f"|got - exact_got| / exact_got {abs(got - exact_got) / exact_got if exact_got else 0.0:.3e}; "
+          f"|exact_got - exact_ref| / exact_ref {abs(exact_got - exact_ref) / exact_ref if exact_ref else 0.0:.3e}")
+    assert abs(got - exact_got) <= tol * exact_got, ("evaluation", got, exact_got)
+    assert abs(exact_got - exact_ref) <= tol * exact_ref, ("factors", exact_got, exact_ref)
