@@ -245,14 +245,28 @@ __global__ void __launch_bounds__(OE_THREADS, 1)
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(smem + stage * OE_STAGE), b0 = a0 + OE_A_BYTES;
+          // A digit s is shared by its 7 - max(1, 7 - s) products: it is read from shared
+          // memory once (collector::a fill / use / lastuse), so a k-block moves 6 A tiles and
+          // 21 B tiles through the shared-memory port instead of 21 + 21
 #pragma unroll
           for (int s = 1; s <= OE_DIG; ++s) {
+            const int t0 = 7 - s > 1 ? 7 - s : 1;
 #pragma unroll
-            for (int tt = (7 - s > 1 ? 7 - s : 1); tt <= OE_DIG; ++tt) {
+            for (int tt = t0; tt <= OE_DIG; ++tt) {
               const int L = s + tt - 7;  // accumulator of level s + t
               const int first_s = L + 1 > 1 ? L + 1 : 1;
-              mma_i8(tbase + (uint32_t)(L * OE_BN), umma_desc_sw32(a0 + (s - 1) * OE_BM * OE_BK),
-                     umma_desc_sw32(b0 + (tt - 1) * OE_BN * OE_BK), P.idesc, (kb > 0 || s != first_s) ? 1u : 0u);
+              const uint32_t d = tbase + (uint32_t)(L * OE_BN);
+              const uint64_t ad = umma_desc_sw32(a0 + (s - 1) * OE_BM * OE_BK);
+              const uint64_t bd = umma_desc_sw32(b0 + (tt - 1) * OE_BN * OE_BK);
+              const uint32_t acc = (kb > 0 || s != first_s) ? 1u : 0u;
+              if (t0 == OE_DIG)
+                mma_i8(d, ad, bd, P.idesc, acc);
+              else if (tt == t0)
+                mma_i8_coll<1>(d, ad, bd, P.idesc, acc);
+              else if (tt == OE_DIG)
+                mma_i8_coll<3>(d, ad, bd, P.idesc, acc);
+              else
+                mma_i8_coll<2>(d, ad, bd, P.idesc, acc);
             }
           }
           mma_commit(&empty[stage]);
