@@ -350,6 +350,7 @@ def run_reference(args, cfg_name: str, cfg: dict) -> None:
         "steps": len(times), "warmup": warm, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (numpy host generator)",
         "config": {"workload": workload_name(cfg_name, cfg)}, "rel_err": rel_err,
+        "world_size": int(os.environ.get("WORLD_SIZE", "1")),
         "cpu_baseline": {"value": value, "unit": "approx/s", "cores": cores_used, "kind": kind, "sample": sample},
         "port": port,
         "e2e": {"value": value, "unit": "approx/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -720,6 +721,25 @@ def main() -> None:
         torch.cuda.synchronize()
         serial = args.steps / (s0.elapsed_time(s1) / 1e3)
 
+    # --- batch configs: every rank's per-matrix results (error, J, I) assembled on every rank
+    # (no collective between approximations, one at the end) ---
+    batch_results = None
+    if batch > 1:
+        from paper_2402_19147_b200.sharding import run_batch_split
+
+        pos = {b: k for k, b in enumerate(mine)}
+
+        def approx_one(b):
+            outs.run(xs[pos[b]], cfg["strategy"], cfg["plan_seed"] + b, psnr_scale, graph=False)
+            return np.concatenate([[outs.rel_error()], outs.J.cpu().numpy(), outs.I.cpu().numpy()])
+
+        table = run_batch_split(batch, approx_one, 1 + c + r, device=f"cuda:{local}")
+        errs = table[:, 0]
+        batch_results = {"matrices": int(batch), "rel_err_min": float(errs.min()), "rel_err_max": float(errs.max()),
+                         "rel_err_mean": float(errs.mean()),
+                         "complete": bool(np.isfinite(table).all()),
+                         "gathered_by": "one all-reduce of the (batch, 1 + c + r) table of errors and index sets"}
+
     # --- phase breakdown (events between phases, same stream), separate pass ---
     dev.profile(True)
     nprof = min(args.steps, 10)
@@ -914,7 +934,7 @@ def main() -> None:
                                         "one native context and stream each, steps round-robin over them; "
                                         "value_serial is the same loop with one in flight"},
             "value_serial": serial,
-            "gpu_launches": launches, "rel_err": rel_err,
+            "gpu_launches": launches, "rel_err": rel_err, "batch_results": batch_results,
             "psnr": (dict(zip(("u8_db", "float_peak1_db"), outs.psnr())) if psnr_scale else None),
             "roofline": roofline, "step_roofline": step_roof,
             "phases_ms_per_approx": per_approx, "phase_rates": extra_phase,

@@ -237,6 +237,13 @@ int qcur_qgemm_herm_int8(qcur_ctx* ctx, int64_t M, int64_t N, int64_t K, const d
    (Ozaki scheme II, nmod moduli; 0 = default).  Same contract as qcur_qgemm with alpha = 1, beta = 0. */
 int qcur_qgemm_int8(qcur_ctx* ctx, int64_t M, int64_t N, int64_t K, const double* a_dev, int64_t lda,
                     const double* b_dev, int64_t ldb, double* c_dev, int64_t ldc, int nmod);
+/* Y (m x r) = X (m x n, row pitch ldx) Q_R (n x r): the big contraction of qmcur (cur.py:268) with
+   qmcur's engine policy: INT8 in one shot, INT8 one chunk of rows at a time when the residue planes
+   exceed the one-shot workspace (cfg5), else the FP64 DMMA GEMM.  Used by the row-sharded path. */
+int qcur_xq(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int64_t ldx, const double* qr_dev, int64_t r,
+            double* y_dev);
+/* to_complex_adjoint (linalg.py:151-164): chi(A), 2m x 2n complex128 row-major (re, im interleaved) */
+int qcur_complex_adjoint(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, double* chi_dev);
 int qcur_chol_inv(qcur_ctx* ctx, const double* g_dev, int64_t q, double* x_dev);
 /* second CholeskyQR pass: L2^{-1} of G2 = I + E by series */
 int qcur_series_l2inv(qcur_ctx* ctx, const double* g2_dev, int64_t q, double* l2inv_dev);

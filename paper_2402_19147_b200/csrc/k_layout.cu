@@ -154,6 +154,27 @@ void launch_project_observed(const double* X, const double* Y, const unsigned ch
   ++::qcur::g_launches;
   k_project_observed<<<grid_for(m * n, 256), 256, 0, st>>>(X, Y, mask, m * n, out);
 }
+// chi(A) (linalg.py:151-164): the 2m x 2n complex adjoint, row-major complex128 (re, im pairs):
+// [[A_a, A_b], [-conj(A_b), conj(A_a)]] with A_a = a0 + i a1, A_b = a2 + i a3.  Sign flips only.
+__global__ void k_complex_adjoint(const double* __restrict__ X, int64_t m, int64_t n, double* __restrict__ chi) {
+  const int64_t ld = 4 * n;  // doubles per row of chi (2n complex)
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m * n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / n, j = t - i * n;
+    const Quat q = ldq_nc(X + t * 4);
+    double* top = chi + i * ld;
+    double* bot = chi + (m + i) * ld;
+    *reinterpret_cast<double2*>(top + 2 * j) = make_double2(q.w, q.x);
+    *reinterpret_cast<double2*>(top + 2 * (n + j)) = make_double2(q.y, q.z);
+    *reinterpret_cast<double2*>(bot + 2 * j) = make_double2(-q.y, q.z);
+    *reinterpret_cast<double2*>(bot + 2 * (n + j)) = make_double2(q.w, -q.x);
+  }
+}
+
+void launch_complex_adjoint(const double* X, int64_t m, int64_t n, double* chi, cudaStream_t st) {
+  ++::qcur::g_launches;
+  k_complex_adjoint<<<grid_for(m * n, 256), 256, 0, st>>>(X, m, n, chi);
+}
+
 void launch_conj_transpose(const double* A, int64_t m, int64_t n, int64_t lda, double* AH, int64_t ldah,
                            cudaStream_t st) {
   dim3 grid((unsigned)((n + 31) / 32), (unsigned)((m + 31) / 32));

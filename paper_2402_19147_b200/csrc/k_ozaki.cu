@@ -964,6 +964,19 @@ double run_i8_peak(int sms, cudaStream_t st) {
 
 size_t ozaki_workspace_bytes(int64_t m, int64_t n, int64_t r, int L) { return oz_plan(m, n, r, L).total + 1024; }
 
+// Rows per chunk for a product whose whole-matrix workspace exceeds the cap: the residues of X
+// are produced and consumed one chunk of rows at a time (rows are independent: each row's
+// scale comes from its own maximum), E(B)'s residues once.  0 when no chunk of 256 rows fits.
+int64_t ozaki_chunk_rows(int64_t m, int64_t n, int64_t r, double cap_bytes) {
+  if (m < 1 || n < 1 || r < 1 || 4 * n > 133140) return 0;
+  const double fixed = (double)oz_plan(0, n, r, kOzMaxModDefault).total;
+  const double per_row = (double)oz_plan(256, n, r, kOzMaxModDefault).total / 256.0 - fixed / 256.0;
+  if (!(per_row > 0.0) || fixed + 256.0 * per_row > cap_bytes) return 0;
+  int64_t rows = (int64_t)((cap_bytes - fixed) / per_row) / 256 * 256;
+  if (rows > m) rows = m;
+  return rows;
+}
+
 bool ozaki_supported(int64_t m, int64_t n, int64_t r) {
   // int32 accumulation: the odd moduli have residues in [-127, 127], so 4n 127^2 < 2^31; for
   // p = 256 the accumulator may wrap, which leaves it exact mod 2^32 and hence mod 256.

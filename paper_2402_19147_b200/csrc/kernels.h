@@ -66,6 +66,7 @@ void launch_gather_cols(const double* X, int64_t m, int64_t ldx, const int64_t* 
                         cudaStream_t st);
 void launch_gather_rows(const double* X, int64_t n, int64_t ldx, const int64_t* I, int64_t r, double* R,
                         cudaStream_t st);
+void launch_complex_adjoint(const double* X, int64_t m, int64_t n, double* chi, cudaStream_t st);
 void launch_conj_transpose(const double* A, int64_t m, int64_t n, int64_t lda, double* AH, int64_t ldah,
                            cudaStream_t st);
 void launch_reduce_pairs(const double* parts, int64_t nparts, double* out2, cudaStream_t st);
@@ -177,6 +178,7 @@ void launch_synth_image(int64_t m, int64_t n, int L, uint64_t seed, double sigma
 int ozaki_max_moduli();
 bool ozaki_supported(int64_t m, int64_t n, int64_t r);
 size_t ozaki_workspace_bytes(int64_t m, int64_t n, int64_t r, int L);
+int64_t ozaki_chunk_rows(int64_t m, int64_t n, int64_t r, double cap_bytes);
 int launch_ozaki_gemm(const double* X, int64_t m, int64_t n, int64_t ldx, const double* B, int64_t r, int64_t ldb,
                       double* Y, int64_t ldy, int L, void* workspace, cudaStream_t st);
 // the same in two phases: prepare (residues of X; depends on X only) and finish (B, GEMMs, CRT)

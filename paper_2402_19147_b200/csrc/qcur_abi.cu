@@ -386,6 +386,15 @@ bool use_int8(const qcur_ctx* ctx, int64_t m, int64_t n, int64_t r) {
   return ctx->gemm_mode == 2 || (double)m * (double)n * (double)r >= 2e8;
 }
 
+// Y = X Q_R on the INT8 tensor cores one chunk of rows at a time (a product whose residues
+// exceed the one-shot workspace cap, e.g. cfg5's 32768^2 X: 64 GB of residue planes)?
+constexpr double kOzChunkCap = 24e9;  // bytes of INT8 workspace for the chunked product
+int64_t int8_chunk_rows(const qcur_ctx* ctx, int64_t m, int64_t n, int64_t r) {
+  if (ctx->gemm_mode == 1 || ozaki_supported(m, n, r)) return 0;
+  if (!(ctx->gemm_mode == 2 || (double)m * (double)n * (double)r >= 2e8)) return 0;
+  return ozaki_chunk_rows(m, n, r, kOzChunkCap);
+}
+
 // the Grams Z^H Z (Z: p x q) of CholeskyQR2 on the INT8 tensor cores?
 bool use_int8_gram(const qcur_ctx* ctx, int64_t p, int64_t q) {
   if (ctx->gemm_mode == 1 || !ozaki_herm_supported(p, q, q)) return false;
@@ -746,6 +755,7 @@ size_t qmcur_ws_bytes(int64_t m, int64_t n, int64_t c, int64_t r) {
     size_t a = qgemm_workspace_bytes(g1), d = qgemm_workspace_bytes(g2);
     b += (a > d ? a : d) + 4096;
     if (ozaki_supported(m, n, r)) b += ozaki_workspace_bytes(m, n, r, kOzakiModuli) + 4096;
+    else if (int64_t mc = ozaki_chunk_rows(m, n, r, kOzChunkCap)) b += ozaki_workspace_bytes(mc, n, r, kOzakiModuli) + 4096;
     if (ozaki_herm_supported(m, c, r)) b += ozaki_herm_workspace_bytes(m, c, r, 0) + 4096;  // Q_C^H Y
   } else {
     b += pinv_ws_bytes(m, c) + pinv_ws_bytes(r, n) + qbytes(c, m) + qbytes(n, r) + qbytes(m, r);
@@ -877,6 +887,37 @@ void* int8_fork_prepare(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, in
   return ozws;
 }
 
+// Y = X Q_R (m x r) with the engine policy of qmcur when no residues were forked: INT8 in
+// one shot, INT8 in row chunks, or the FP64 DMMA GEMM (gws: its workspace, or nullptr to take it).
+int xq_product(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, int64_t ldx, const double* QR, int64_t r,
+               double* Y, double* gws) {
+  cudaStream_t st = ctx->stream;
+  const int64_t mc = int8_chunk_rows(ctx, m, n, r);
+  if (use_int8(ctx, m, n, r) || mc > 0) {
+    const int64_t rows = mc > 0 ? mc : m;
+    void* ws = ctx->take<uint8_t>(ozaki_workspace_bytes(rows, n, r, kOzakiModuli));
+    if (!ws) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (int8 X Q_R)");
+    if (launch_ozaki_prep_b(rows, n, QR, r, r, kOzakiModuli, ws, st))
+      return ctx->fail(QCUR_E_CUDA, "int8 gemm: bad modulus count");
+    // chunks of `rows` rows; the last one ends at row m and may overlap its predecessor (rows are
+    // independent, so the overlap is recomputed to the same bits)
+    for (int64_t i0 = 0; i0 < m; i0 += rows) {
+      const int64_t a = i0 + rows <= m ? i0 : m - rows;
+      if (launch_ozaki_prepare(X + a * ldx * 4, rows, n, ldx, r, kOzakiModuli, ws, st) ||
+          launch_ozaki_multiply(rows, n, r, Y + a * r * 4, r, kOzakiModuli, ws, st))
+        return ctx->fail(QCUR_E_CUDA, "int8 gemm: tensor map encode failed");
+    }
+    CK_LAUNCH(ctx, "int8 X Q_R");
+    return QCUR_OK;
+  }
+  GemmArgs g = gargs(m, r, n, X, ldx, 0, QR, r, 0, Y, r);
+  if (!gws) {
+    gws = ctx->take<double>(qgemm_workspace_bytes(g) / 8 + 16);
+    if (!gws) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (X Q_R)");
+  }
+  return gemm(ctx, g, gws);
+}
+
 int qmcur_core(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, int64_t c, int64_t r, const int64_t* J,
                const double* C, double* U, const double* R, int core, void* oz_ready) {
   cudaStream_t st = ctx->stream;
@@ -929,7 +970,7 @@ int qmcur_core(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, int64_t c, 
       if (launch_ozaki_multiply(m, n, r, Y, r, kOzakiModuli, ozws, st))
         return ctx->fail(QCUR_E_CUDA, "int8 gemm: tensor map encode failed");
       CK_LAUNCH(ctx, "int8 gemm");
-    } else if ((rc = gemm(ctx, gargs(m, r, n, X, n, 0, QR, r, 0, Y, r), gws))) {
+    } else if ((rc = xq_product(ctx, X, m, n, n, QR, r, Y, gws))) {
       return rc;
     }
     ctx->mark("gemm_xq");
@@ -1406,6 +1447,14 @@ int qcur_cur_given(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, con
   return sync_status(ctx);
 }
 
+int qcur_complex_adjoint(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, double* chi_dev) {
+  DeviceGuard device_guard_(ctx);
+  if (m < 1 || n < 1) return ctx->fail(QCUR_E_SHAPE, "complex_adjoint: bad sizes");
+  launch_complex_adjoint(x_dev, m, n, chi_dev, ctx->stream);
+  CK_LAUNCH(ctx, "complex_adjoint");
+  return QCUR_OK;
+}
+
 int qcur_qgemv(qcur_ctx* ctx, int op, int64_t m, int64_t n, const double* a_dev, int64_t lda, const double* x_dev,
                double* y_dev) {
   DeviceGuard device_guard_(ctx);
@@ -1876,6 +1925,20 @@ int qcur_qgemm_herm_int8(qcur_ctx* ctx, int64_t M, int64_t N, int64_t K, const d
     return ctx->fail(QCUR_E_CUDA, "qgemm_herm_int8: tensor map encode failed");
   CK_LAUNCH(ctx, "qgemm_herm_int8");
   return QCUR_OK;
+}
+
+int qcur_xq(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int64_t ldx, const double* qr_dev, int64_t r,
+            double* y_dev) {
+  DeviceGuard device_guard_(ctx);
+  if (m < 1 || n < 1 || r < 1 || ldx < n) return ctx->fail(QCUR_E_SHAPE, "xq: bad sizes");
+  const int64_t mc = int8_chunk_rows(ctx, m, n, r);
+  const int64_t rows = mc > 0 ? mc : m;
+  GemmArgs g = gargs(m, r, n, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0);
+  size_t b = qgemm_workspace_bytes(g) + 4096;
+  if (use_int8(ctx, m, n, r) || mc > 0) b += ozaki_workspace_bytes(rows, n, r, kOzakiModuli) + 4096;
+  int rc = ctx->reserve(b);
+  if (rc) return rc;
+  return xq_product(ctx, x_dev, m, n, ldx, qr_dev, r, y_dev, nullptr);
 }
 
 int qcur_qgemm_int8(qcur_ctx* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,

@@ -27,7 +27,7 @@ from .errors import ParameterError, ShapeError
 from .quat import QMatrix, from_device, to_device
 
 __all__ = ["QSVDResult", "qsvd", "pseudoinverse", "spectral_norm", "numerical_rank", "lowrank_truncate",
-           "save_qsvd"]
+           "save_qsvd", "ComplexAdjoint", "to_complex_adjoint", "orthonormalize_columns"]
 
 _EPS = float(np.finfo(np.float64).eps)
 
@@ -300,3 +300,62 @@ def save_qsvd(result: QSVDResult, directory) -> None:
     with open(out / "sigma.txt", "w") as fh:
         for s_ in result.sigma:
             fh.write(f"{s_:.17g}\n")
+
+
+# ---------------------------------------------------------------------------
+# the complex adjoint and column orthonormalisation (linalg.py:136-164, 385-404)
+# ---------------------------------------------------------------------------
+@dataclass(frozen=True)
+class ComplexAdjoint:
+    """The 2m-by-2n complex image chi(A) of an m-by-n quaternion matrix (linalg.py:136-148)."""
+
+    matrix: np.ndarray
+    source_rows: int
+    source_cols: int
+
+    def __post_init__(self) -> None:
+        self.matrix.setflags(write=False)
+
+    @property
+    def shape(self) -> tuple[int, int]:
+        return self.matrix.shape
+
+
+def to_complex_adjoint(a) -> ComplexAdjoint:
+    """chi(A) = [[A_a, A_b], [-conj(A_b), conj(A_a)]] built on the device (k_complex_adjoint;
+    sign flips only, so the block relations hold bit for bit as in linalg.py:151-164)."""
+    dev = _native.device()
+    m, n = (int(v) for v in a.shape)
+    ad = to_device(a, dev)
+    chi = dev.empty((2 * m, 2 * n, 2))
+    dev.call("qcur_complex_adjoint", ad.data_ptr(), m, n, chi.data_ptr())
+    out = chi.cpu().numpy().view(np.complex128).reshape(2 * m, 2 * n).copy()
+    return ComplexAdjoint(out, m, n)
+
+
+def orthonormalize_columns(a) -> QMatrix:
+    """An orthonormal basis of A's columns, the Q of A = Q T with T upper triangular and a positive
+    real diagonal (the frame the reference's twice-applied Gram-Schmidt produces, linalg.py:385-404;
+    QR with a positive diagonal is unique).  On the device: CholeskyQR2 (qcur_factor), the
+    Householder path when the kappa guard trips.  ShapeError for more columns than rows;
+    ParameterError when a column is numerically dependent on the others."""
+    m, n = (int(v) for v in a.shape)
+    if n > m:
+        raise ShapeError(f"cannot orthonormalize {n} columns in dimension {m}")
+    sigma = _singular_values(a)
+    from .quat import as_planes
+
+    colnorm2 = sum(p * p for p in as_planes(a)).sum(axis=0)
+    scale = max(float(np.sqrt(colnorm2.max())), 1.0)
+    if not float(sigma[-1]) > 1e-12 * scale:
+        raise ParameterError("columns are numerically dependent on earlier columns")
+    dev = _native.device()
+    z = to_device(a, dev)
+    # qcur_factor returns pinv(Z) = F Q^H with Q = Z L1^-H (one Cholesky pass, orthonormal to
+    # kappa^2 u); factoring that Q once more gives Z (L' L1)^-H, orthonormal to u
+    for _ in range(2):
+        Q, F = dev.empty_q(m, n), dev.empty_q(n, n)
+        dev.call("qcur_factor", z.data_ptr(), 0, m, n, Q.data_ptr(), F.data_ptr())
+        z = Q
+    dev.call("qcur_check")
+    return from_device(Q, dev)

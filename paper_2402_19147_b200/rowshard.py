@@ -12,11 +12,12 @@ torch.distributed collective on device buffers (NCCL over NVLink):
                       combined in the tree's own order -> bit-identical to numpy;
       row normaliser  all-gather of the m row weights.
   K2  draws           identical on every rank (same weights, same PCG64 stream).
-  K3  C = X[:, J]     rows local;  R = X[I, :]: owners copy their rows, all-gather
-                      (byte copies, no arithmetic -> bit-exact).
+  K3  C = X[:, J]     rows local;  R = X[I, :]: owners copy their rows, all-gather,
+                      one device gather by an owner-slot table (byte copies -> bit-exact).
   K4  pinv(C)         distributed CholeskyQR2: all-reduce of the c x c Grams;
       pinv(R)         R replicated -> factored redundantly.
-  K6  Y_g = X_g Q_R;  M = sum_g Q_C,g^H Y_g (all-reduce of c x r);  U replicated.
+  K6  Y_g = X_g Q_R (qcur_xq: INT8 tensor cores, in row chunks when the residues are large);
+      M = sum_g Q_C,g^H Y_g (all-reduce of c x r);  U replicated.
   K9  error partials  local fused kernel; 4 statistics all-gathered and summed
                       in rank order.
 
@@ -218,6 +219,12 @@ class GpuOps:
                       int(B.shape[1]), 0.0, out.data_ptr(), N, int(flags))
         return out
 
+    def xq(self, xb, QR):
+        rows, n, r = int(xb.shape[0]), int(xb.shape[1]), int(QR.shape[1])
+        out = self.dev.empty_q(rows, r)
+        self.dev.call("qcur_xq", xb.data_ptr(), rows, n, n, QR.data_ptr(), r, out.data_ptr())
+        return out
+
     def chol_inv(self, G):
         q = int(G.shape[0])
         out = self.dev.empty_q(q, q)
@@ -302,18 +309,20 @@ def approx_rowsharded(ops, comm, xb, m: int, strategy: str, seed: int, c: int, r
     owned = [t for t in range(r) if row0 <= int(I_host[t]) < row0 + rows_b]
     kmax = comm.all_max(len(owned))
     Rown = ops.gather_rows(xb, ops.index_tensor([int(I_host[t]) - row0 for t in owned]))
-    if kmax > 0:
-        import torch
+    import torch
 
-        buf = torch.zeros((kmax, n, 4), dtype=torch.float64, device=Rown.device)
-        buf[: len(owned)] = Rown
-        allrows = comm.all_gather_cat(buf)  # (G*kmax, n, 4)
-        R = torch.empty((r, n, 4), dtype=torch.float64, device=Rown.device)
-        for owner in range(G):
-            lo, hi = owner * rows_b, (owner + 1) * rows_b
-            ts = [t for t in range(r) if lo <= int(I_host[t]) < hi]
-            for k, t in enumerate(ts):
-                R[t] = allrows[owner * kmax + k]
+    buf = torch.zeros((kmax, n, 4), dtype=torch.float64, device=Rown.device)
+    buf[: len(owned)] = Rown
+    allrows = comm.all_gather_cat(buf)  # (G*kmax, n, 4): owner g's rows at [g*kmax, g*kmax + #owned_g)
+    # one device gather puts row t of R (drawn index I[t]) in place: its slot in the gathered
+    # buffer is (owner of I[t]) * kmax + (its rank among that owner's draws, in draw order)
+    slot = np.empty(r, dtype=np.int64)
+    seen = np.zeros(G, dtype=np.int64)
+    for t in range(r):
+        owner = int(I_host[t]) // rows_b
+        slot[t] = owner * kmax + seen[owner]
+        seen[owner] += 1
+    R = ops.gather_rows(allrows, ops.index_tensor(slot))
     # ---- K4: pinv(C) by distributed CholeskyQR2, pinv(R) replicated ------
     G1 = comm.all_reduce_sum(ops.gemm(Cb, Cb, opA=1, flags=2))
     X1 = ops.chol_inv(G1)
@@ -333,7 +342,7 @@ def approx_rowsharded(ops, comm, xb, m: int, strategy: str, seed: int, c: int, r
         QC = QCfull[row0:row0 + rows_b]
     QR, FR = ops.factor(R, 1)
     # ---- K6/K7: U ----------------------------------------------------------
-    Yb = ops.gemm(xb, QR)
+    Yb = ops.xq(xb, QR)  # the big contraction on qmcur's engine (INT8 tensor cores when large)
     M = comm.all_reduce_sum(ops.gemm(QC, Yb, opA=1))
     U = ops.gemm(ops.gemm(FC, M), FR, opB=1)
     # ---- K8/K9: fused error, partials in rank order -------------------------

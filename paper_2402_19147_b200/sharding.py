@@ -47,3 +47,31 @@ def gather_results(local: dict[int, float], total: int, device=None) -> list[flo
         out[mask] = -float("inf")
         dist.all_reduce(out, op=dist.ReduceOp.MAX)
     return [float(v) for v in out.cpu()]
+
+
+def gather_rows(local: dict, total: int, width: int, device=None):
+    """Assemble per-unit fixed-width rows {unit: sequence of `width` numbers} from every rank
+    into a (total, width) float64 numpy array ordered by unit (index sets, statistics)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    out = torch.full((total, width), -float("inf"), dtype=torch.float64, device=device)
+    for k, v in local.items():
+        out[k] = torch.as_tensor(np.asarray(v, dtype=np.float64), device=out.device)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(out, op=dist.ReduceOp.MAX)  # each row has exactly one owner
+    return out.cpu().numpy()
+
+
+def run_batch_split(total: int, approx_one, width: int, device=None):
+    """cfg4's by-matrix split: this rank approximates its contiguous block of the
+    `total` matrices with approx_one(b) -> row of `width` numbers (relative error, indices ...),
+    and every rank receives the (total, width) table of all results.  No collective runs between
+    the approximations; one all-reduce assembles the table at the end."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
+    rank = dist.get_rank() if world > 1 else 0
+    local = {b: approx_one(b) for b in shard_range(total, world, rank)}
+    return gather_rows(local, total, width, device=device)

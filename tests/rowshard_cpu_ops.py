@@ -114,6 +114,9 @@ class CpuOps:
             b = O.conj_t(b)
         return stack(tuple(alpha * p for p in O.qmatmul(a, b)))
 
+    def xq(self, xb, QR):
+        return self.gemm(xb, QR)
+
     def chol_inv(self, G):
         return stack(qchol_inv(planes(G)))
 

@@ -58,3 +58,54 @@ def test_gloo_world2_batch_split_and_timing():
     for _, _, allres, slowest in out:
         assert allres == [float(b * b) for b in range(64)]
         assert slowest == 11.0
+
+
+CFG4_SMALL = dict(m=96, n=80, rank=6, noise=1e-4, relative=True, strategy="uniform", c=12, r=12, plan_seed=0,
+                  gen_seed=20240301, batch=16)
+
+
+def cfg4_row(b):
+    """One matrix of bench.py's cfg4 recipe (reduced size) through the CPU oracle stand-in:
+    (relative error, J, I)."""
+    import sys
+    import numpy as np
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path[:0] = [root, os.path.join(root, "oracle")]
+    import bench
+    import oracle as O
+
+    cfg = CFG4_SMALL
+    planes = bench.host_lowrank(cfg, cfg["gen_seed"] + 1000 * b)
+    res = O.approx(planes, cfg["strategy"], cfg["rank"], cfg["plan_seed"] + b, cfg["c"], cfg["r"])
+    return np.concatenate([[res["rel_err"]], res["cols"], res["rows"]])
+
+
+def _split_worker(rank: int, world: int, port: int, q):
+    import torch.distributed as dist
+
+    from paper_2402_19147_b200.sharding import run_batch_split
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    table = run_batch_split(CFG4_SMALL["batch"], cfg4_row, 1 + CFG4_SMALL["c"] + CFG4_SMALL["r"])
+    q.put((rank, table))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_cfg4_split_end_to_end():
+    """The bench's cfg4 split end to end with CPU stand-ins: each of 2 gloo ranks approximates its
+    half of the batch; both receive the full table, equal to a single-process run."""
+    import numpy as np
+
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_split_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    want = np.stack([cfg4_row(b) for b in range(CFG4_SMALL["batch"])])
+    for _, table in out:
+        assert np.array_equal(table, want)
