@@ -645,6 +645,8 @@ def main() -> None:
     # workload, its own generator seed), so one approximation's latency-bound phases (draws,
     # Cholesky) overlap another's tensor-bound ones.  QCUR_INFLIGHT=1 gives the serial number.
     inflight = int(os.environ.get("QCUR_INFLIGHT", "2")) if batch == 1 else 1
+    if 32 * m * n > 8e9:  # cfg5: one 34 GB matrix and its workspace fill the GPU; one in flight
+        inflight = 1
     lanes = [(dev, outs, xs, torch.cuda.current_stream())]
     for k in range(1, inflight):
         dk = _native.Device(local)

@@ -9,6 +9,7 @@ device, :func:`device` raises.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
@@ -75,7 +76,9 @@ def load_library() -> ctypes.CDLL:
                 f"{LIB_PATH} is not built; run `python -m paper_2402_19147_b200.build` "
                 "(there is no CPU fallback for the QMCUR path)"
             )
-        lib = ctypes.CDLL(str(LIB_PATH))
+        # experiments only: time another build of the library against this one (A/B runs)
+        ab = os.environ.get("QCUR_LIB_AB")
+        lib = ctypes.CDLL(ab if ab else str(LIB_PATH))
         sig = {
             "qcur_abi_version": (ctypes.c_int, []),
             "qcur_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
@@ -157,6 +160,8 @@ def load_library() -> ctypes.CDLL:
                                                   ctypes.c_double, _c_dp]),
         }
         for name, (res, args) in sig.items():
+            if ab and not hasattr(lib, name):
+                continue
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

@@ -411,33 +411,39 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      int stage = 0;
-      unsigned phase = 0;
-      int t = 0;
-      for (int u = blockIdx.x; u < P.total; u += gridDim.x, ++t) {
-        int l, mb, nb;
-        const OzProb& q = P.pr[unit_coords(P, u, l, mb, nb)];
-        mbar_wait(tempty, ((unsigned)t & 1u) ^ 1u);  // the epilogue has drained the previous unit
+    // the whole warp runs the issue loop (uniform registers, no per-MMA election loops); one
+    // elected lane issues each k-block's MMAs and commits
+    const uint64_t adesc0 = umma_desc(smem_u32(sA)), bdesc0 = umma_desc(smem_u32(sB));
+    int stage = 0;
+    unsigned phase = 0;
+    int t = 0;
+    for (int u = blockIdx.x; u < P.total; u += gridDim.x, ++t) {
+      int l, mb, nb;
+      const OzProb& q = P.pr[unit_coords(P, u, l, mb, nb)];
+      mbar_wait(tempty, ((unsigned)t & 1u) ^ 1u);  // the epilogue has drained the previous unit
+      tc_fence_after();
+      for (int kb = 0; kb < q.kblocks; ++kb) {
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
-        for (int kb = 0; kb < q.kblocks; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + stage * OZ_A_BYTES), b0 = smem_u32(sB + stage * OZ_B_SLOT);
+        const uint64_t ad = adesc0 + (uint64_t)((stage * OZ_A_BYTES) >> 4);
+        const uint64_t bd0 = bdesc0 + (uint64_t)((stage * OZ_B_SLOT) >> 4);
+        if (elect_one_sync()) {
 #pragma unroll
           for (int k = 0; k < OZ_BK / 32; ++k) {
-            const uint64_t bd = umma_desc(b0 + k * 32);
-            mma_i8(tbase, umma_desc(a0 + k * 32), bd, q.idesc, (kb | k) != 0);                   // rows 0..127
-            mma_i8(tbase + 256, umma_desc(a0 + 128 * OZ_BK + k * 32), bd, q.idesc, (kb | k) != 0);  // 128..255
+            const uint64_t bd = bd0 + (uint64_t)(k * 2);  // +32 bytes along K
+            mma_i8(tbase, ad + (uint64_t)(k * 2), bd, q.idesc, (kb | k) != 0);                          // rows 0..127
+            mma_i8(tbase + 256, ad + (uint64_t)((128 * OZ_BK + k * 32) >> 4), bd, q.idesc, (kb | k) != 0);  // 128..255
           }
           mma_commit(&empty[stage]);
-          if (++stage == OZ_STAGES) {
-            stage = 0;
-            phase ^= 1u;
-          }
         }
-        mma_commit(tfull);
+        __syncwarp();
+        if (++stage == OZ_STAGES) {
+          stage = 0;
+          phase ^= 1u;
+        }
       }
+      if (elect_one_sync()) mma_commit(tfull);
+      __syncwarp();
     }
   } else {
     // 8 epilogue warps: warp w drains TMEM lanes 32 (w % 4) .. +31 of accumulator (w - 2) / 4

@@ -46,7 +46,8 @@ constexpr int OE_A_BYTES = OE_DIG * OE_BM * OE_BK;  // 24 KB
 constexpr int OE_B_BYTES = OE_DIG * OE_BN * OE_BK;  // 15 KB
 constexpr int OE_STAGE = OE_A_BYTES + OE_B_BYTES;
 constexpr int OE_SMEM = 1024 + OE_STAGES * OE_STAGE + 256;
-constexpr int OE_BITS = 54;  // |P'|, |R'| <= 2^54: seven balanced base-256 digits
+constexpr int OE_BITS = 54;
+constexpr int kOeCluster = 2;  // CTAs per cluster sharing the A digit tile by TMA multicast  // |P'|, |R'| <= 2^54: seven balanced base-256 digits
 
 __device__ __forceinline__ double i2d(uint32_t v) {  // exact int32 -> double (one DADD)
   return __hiloint2double(0x43380000, (int)(v ^ 0x80000000u)) - 6755401588539392.0;  // 1.5*2^52 + 2^31
@@ -175,9 +176,16 @@ struct OeParams {
   double* partials;  // [grid][OE_EPI_WARPS][4]
   double psnr_scale;
   int kblocks, mblocks, nblocks, total;
+  int groups;  // (row block, group of CL column blocks) work units of a cluster
   uint32_t idesc;
 };
 
+// CL CTAs per cluster work on one row block and CL adjacent column blocks: the A digit tile
+// (6 planes x 128 rows x 32 bytes per k-block) is the same for all of them, so each CTA loads
+// a share of its digit planes and multicasts it to the whole cluster (L2 -> SM traffic for A
+// divided by CL); every CTA still loads its own B tile.  A stage may be refilled only when all
+// CL CTAs have consumed it: the MMA warps commit to the stage's "empty" barrier of every CTA.
+template <int CL>
 __global__ void __launch_bounds__(OE_THREADS, 1)
     k_oe_err(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
              const __grid_constant__ CUtensorMap tmX, const __grid_constant__ OeParams P) {
@@ -191,10 +199,14 @@ __global__ void __launch_bounds__(OE_THREADS, 1)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int crank = CL > 1 ? (int)cluster_ctarank() : 0;
+  const int cid = CL > 1 ? (int)cluster_id_x() : (int)blockIdx.x;
+  const int ncl = CL > 1 ? (int)ncluster_x() : (int)gridDim.x;
+  constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1u);
   if (threadIdx.x == 0) {
     for (int s = 0; s < OE_STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL);  // one commit from each CTA of the cluster
     }
     mbar_init(tfull, 1);
     mbar_init(tempty, OE_EPI_WARPS);
@@ -207,7 +219,10 @@ __global__ void __launch_bounds__(OE_THREADS, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CL > 1)
+    cluster_sync_all();  // every CTA's barriers initialised before any multicast reaches them
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
 
@@ -217,14 +232,20 @@ __global__ void __launch_bounds__(OE_THREADS, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
       int stage = 0;
       unsigned phase = 0;
-      for (int u = blockIdx.x; u < P.total; u += gridDim.x) {
-        const int mb = u % P.mblocks, nb = u / P.mblocks;  // row blocks fastest: B tiles stay hot
-        tma_prefetch_2d(&tmX, nb * OE_BN, mb * OE_BM);      // X tile for the epilogue, into L2
+      for (int g = cid; g < P.groups; g += ncl) {
+        const int mb = g % P.mblocks, nb = (g / P.mblocks) * CL + crank;  // row blocks fastest
+        if (nb < P.nblocks) tma_prefetch_2d(&tmX, nb * OE_BN, mb * OE_BM);  // X tile for the epilogue
         for (int kb = 0; kb < P.kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1u);
           mbar_expect_tx(&full[stage], OE_STAGE);
           uint8_t* st = smem + stage * OE_STAGE;
-          tma_load_3d(st, &tmA, kb * OE_BK, mb * OE_BM, 0, &full[stage]);
+          if constexpr (CL == 1) {
+            tma_load_3d(st, &tmA, kb * OE_BK, mb * OE_BM, 0, &full[stage]);
+          } else {
+            // this CTA's share of the digit planes, into every CTA of the cluster
+            for (int d = crank; d < OE_DIG; d += CL)
+              tma_load_3d_mc(st + d * OE_BM * OE_BK, &tmA, kb * OE_BK, mb * OE_BM, d, &full[stage], kMask);
+          }
           tma_load_3d(st + OE_A_BYTES, &tmB, kb * OE_BK, nb * OE_BN, 0, &full[stage]);
           if (++stage == OE_STAGES) {
             stage = 0;
@@ -234,17 +255,22 @@ __global__ void __launch_bounds__(OE_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      int stage = 0;
-      unsigned phase = 0;
-      int t = 0;
-      for (int u = blockIdx.x; u < P.total; u += gridDim.x, ++t) {
-        mbar_wait(tempty, ((unsigned)t & 1u) ^ 1u);
+    // the whole warp runs the issue loop (uniform control flow: descriptors and counters live in
+    // uniform registers, no per-MMA lane election loops); one elected lane issues each k-block's
+    // 21 MMAs and its commit
+    const uint64_t adesc0 = umma_desc_sw32(smem_u32(smem));
+    int stage = 0;
+    unsigned phase = 0;
+    int t = 0;
+    for (int g = cid; g < P.groups; g += ncl, ++t) {
+      mbar_wait(tempty, ((unsigned)t & 1u) ^ 1u);
+      tc_fence_after();
+      for (int kb = 0; kb < P.kblocks; ++kb) {
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
-        for (int kb = 0; kb < P.kblocks; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t a0 = smem_u32(smem + stage * OE_STAGE), b0 = a0 + OE_A_BYTES;
+        const uint64_t ad0 = adesc0 + (uint64_t)((stage * OE_STAGE) >> 4);
+        const uint64_t bd0 = ad0 + (uint64_t)(OE_A_BYTES >> 4);
+        if (elect_one_sync()) {
           // A digit s is shared by its 7 - max(1, 7 - s) products: it is read from shared
           // memory once (collector::a fill / use / lastuse), so a k-block moves 6 A tiles and
           // 21 B tiles through the shared-memory port instead of 21 + 21
@@ -256,8 +282,8 @@ __global__ void __launch_bounds__(OE_THREADS, 1)
               const int L = s + tt - 7;  // accumulator of level s + t
               const int first_s = L + 1 > 1 ? L + 1 : 1;
               const uint32_t d = tbase + (uint32_t)(L * OE_BN);
-              const uint64_t ad = umma_desc_sw32(a0 + (s - 1) * OE_BM * OE_BK);
-              const uint64_t bd = umma_desc_sw32(b0 + (tt - 1) * OE_BN * OE_BK);
+              const uint64_t ad = ad0 + (uint64_t)(((s - 1) * OE_BM * OE_BK) >> 4);
+              const uint64_t bd = bd0 + (uint64_t)(((tt - 1) * OE_BN * OE_BK) >> 4);
               const uint32_t acc = (kb > 0 || s != first_s) ? 1u : 0u;
               if (t0 == OE_DIG)
                 mma_i8(d, ad, bd, P.idesc, acc);
@@ -269,14 +295,19 @@ __global__ void __launch_bounds__(OE_THREADS, 1)
                 mma_i8_coll<2>(d, ad, bd, P.idesc, acc);
             }
           }
-          mma_commit(&empty[stage]);
-          if (++stage == OE_STAGES) {
-            stage = 0;
-            phase ^= 1u;
-          }
+          if constexpr (CL == 1)
+            mma_commit(&empty[stage]);
+          else
+            mma_commit_mc(&empty[stage], kMask);  // the stage is free in every CTA's ring
         }
-        mma_commit(tfull);
+        __syncwarp();
+        if (++stage == OE_STAGES) {
+          stage = 0;
+          phase ^= 1u;
+        }
       }
+      if (elect_one_sync()) mma_commit(tfull);
+      __syncwarp();
     }
   } else {
     // warp w drains TMEM lanes 32 (w % 4) .. +31, columns 20 s .. 20 s + 19 (s = (w - 2) / 4:
@@ -289,10 +320,10 @@ __global__ void __launch_bounds__(OE_THREADS, 1)
     const double sc = P.psnr_scale;
     double v[4] = {0.0, 0.0, 0.0, 0.0};  // this thread's sums over all its units, in a fixed order
     int t = 0;
-    for (int u = blockIdx.x; u < P.total; u += gridDim.x, ++t) {
-      const int mb = u % P.mblocks, nb = u / P.mblocks;
+    for (int g = cid; g < P.groups; g += ncl, ++t) {
+      const int mb = g % P.mblocks, nb = (g / P.mblocks) * CL + crank;
       const int64_t row = (int64_t)mb * OE_BM + rloc;
-      const bool rvalid = row < P.m;
+      const bool rvalid = row < P.m && nb < P.nblocks;
       const int er = rvalid ? P.ea[row] : 0;
       const double* xrow = P.X + (rvalid ? row : 0) * P.ldx;
       const int64_t jq0 = ((int64_t)nb * OE_BN + sub * 4 * QW) >> 2;  // first quaternion column
@@ -352,6 +383,8 @@ __global__ void __launch_bounds__(OE_THREADS, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase) : "memory");
   }
+  // no CTA may leave while a peer can still multicast into its shared memory or barriers
+  if constexpr (CL > 1) cluster_sync_all();
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 oe_encode() {
@@ -366,12 +399,13 @@ PFN_cuTensorMapEncodeTiled_v12000 oe_encode() {
   return fn;
 }
 
-bool oe_digit_map(CUtensorMap* map, const int8_t* base, int64_t K, int64_t rows, int64_t Kp, int box_rows) {
+bool oe_digit_map(CUtensorMap* map, const int8_t* base, int64_t K, int64_t rows, int64_t Kp, int box_rows,
+                  int box_digits = OE_DIG) {
   auto enc = oe_encode();
   if (!enc) return false;
   cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)OE_DIG};
   cuuint64_t strides[2] = {(cuuint64_t)Kp, (cuuint64_t)(Kp * rows)};
-  cuuint32_t box[3] = {(cuuint32_t)OE_BK, (cuuint32_t)box_rows, (cuuint32_t)OE_DIG};
+  cuuint32_t box[3] = {(cuuint32_t)OE_BK, (cuuint32_t)box_rows, (cuuint32_t)box_digits};
   cuuint32_t estr[3] = {1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -471,9 +505,16 @@ int launch_ozaki_error_gemm(const double* X, int64_t ldx, int64_t m, int64_t n, 
   int* eb = reinterpret_cast<int*>(ws + pl.off_eb);
   double* parts = reinterpret_cast<double*>(ws + pl.off_part);
 
+  // cluster size: CTAs of one row block sharing the A digit tile (QCUR_OE_CLUSTER overrides)
+  static const int cl_env = [] {
+    const char* e = std::getenv("QCUR_OE_CLUSTER");
+    return e ? std::atoi(e) : 0;
+  }();
+  int CL = cl_env > 0 ? cl_env : kOeCluster;
+  if (CL != 1 && CL != 2 && CL != 4) CL = kOeCluster;
   CUtensorMap tmA, tmB, tmX;
-  if (!oe_digit_map(&tmA, pd, pl.K, m, pl.Kp, OE_BM) || !oe_digit_map(&tmB, rd, pl.K, pl.N, pl.Kp, OE_BN) ||
-      !oe_x_map(&tmX, X, pl.N, m, ldx * 4))
+  if (!oe_digit_map(&tmA, pd, pl.K, m, pl.Kp, OE_BM, CL == 1 ? OE_DIG : 1) ||
+      !oe_digit_map(&tmB, rd, pl.K, pl.N, pl.Kp, OE_BN) || !oe_x_map(&tmX, X, pl.N, m, ldx * 4))
     return 2;
   OeParams p{};
   p.m = m;
@@ -488,15 +529,52 @@ int launch_ozaki_error_gemm(const double* X, int64_t ldx, int64_t m, int64_t n, 
   p.mblocks = pl.mblocks;
   p.nblocks = pl.nblocks;
   p.total = pl.total;
+  p.groups = pl.mblocks * ((pl.nblocks + CL - 1) / CL);
   // kind::i8: D = s32, A/B signed int8, K-major, N = 80, M = 128
   p.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OE_BN >> 3) << 17) | ((uint32_t)(OE_BM >> 4) << 24);
   static std::atomic<unsigned> attr{0};
   if (first_on_device(attr)) {
-    cudaFuncSetAttribute(k_oe_err, cudaFuncAttributeMaxDynamicSharedMemorySize, OE_SMEM);
+    cudaFuncSetAttribute(k_oe_err<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, OE_SMEM);
+    cudaFuncSetAttribute(k_oe_err<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, OE_SMEM);
+    cudaFuncSetAttribute(k_oe_err<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, OE_SMEM);
   }
-  const int grid = pl.total < oe_sms() ? pl.total : oe_sms();
+  cudaLaunchConfig_t cfg{};
+  cfg.blockDim = dim3(OE_THREADS);
+  cfg.dynamicSmemBytes = OE_SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  // persistent grid: as many clusters as can be resident at once (clusters live inside one GPC,
+  // so CL > 1 may leave a few SMs of a GPC idle), never a second wave
+  int nclusters_max = oe_sms() / CL;
+  if (CL > 1) {
+    static int max_active[5] = {0, 0, 0, 0, 0};
+    if (!max_active[CL]) {
+      int nc = 0;
+      cfg.gridDim = dim3((unsigned)(nclusters_max * CL));
+      const cudaError_t e = CL == 2 ? cudaOccupancyMaxActiveClusters(&nc, k_oe_err<2>, &cfg)
+                                    : cudaOccupancyMaxActiveClusters(&nc, k_oe_err<4>, &cfg);
+      max_active[CL] = (e == cudaSuccess && nc > 0) ? nc : nclusters_max;
+      (void)cudaGetLastError();
+    }
+    if (max_active[CL] < nclusters_max) nclusters_max = max_active[CL];
+  }
+  const int nclusters = p.groups < nclusters_max ? p.groups : nclusters_max;
+  const int grid = nclusters * CL;
   ++::qcur::g_launches;
-  k_oe_err<<<grid, OE_THREADS, OE_SMEM, st>>>(tmA, tmB, tmX, p);
+  if (CL == 1) {
+    k_oe_err<1><<<grid, OE_THREADS, OE_SMEM, st>>>(tmA, tmB, tmX, p);
+  } else {
+    cfg.gridDim = dim3((unsigned)grid);
+    const cudaError_t e = CL == 2 ? cudaLaunchKernelEx(&cfg, k_oe_err<2>, tmA, tmB, tmX, p)
+                                  : cudaLaunchKernelEx(&cfg, k_oe_err<4>, tmA, tmB, tmX, p);
+    if (e != cudaSuccess) return 3;
+  }
   launch_reduce_rows(parts, (int64_t)grid * OE_EPI_WARPS, 4, out4, st);
   return 0;
 }

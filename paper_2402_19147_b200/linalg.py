@@ -327,7 +327,7 @@ def to_complex_adjoint(a) -> ComplexAdjoint:
     dev = _native.device()
     m, n = (int(v) for v in a.shape)
     ad = to_device(a, dev)
-    chi = dev.empty((2 * m, 2 * n, 2))
+    chi = dev.empty(2 * m, 2 * n, 2)
     dev.call("qcur_complex_adjoint", ad.data_ptr(), m, n, chi.data_ptr())
     out = chi.cpu().numpy().view(np.complex128).reshape(2 * m, 2 * n).copy()
     return ComplexAdjoint(out, m, n)
