@@ -154,6 +154,16 @@ int qcur_cur_error(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, con
 int qcur_approx(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int strategy, const uint64_t state[4],
                 int64_t num_cols, int64_t num_rows, int64_t* col_idx_dev, int64_t* row_idx_dev, double* c_dev,
                 double* u_dev, double* r_dev, double psnr_scale, int core, double* err4_dev);
+/* Batched: `batch` independent m x n matrices x_devs[b] (device pointers, host array) through the
+ * pipeline of qcur_approx, matrix b with PCG64 state states[4b..4b+3]; outputs packed per matrix
+ * (col_idx batch x num_cols, c batch x m x num_cols, ..., err4 batch x 4).  Matrices run on `lanes`
+ * (1..8; 0 = 4) internal lane contexts overlapping one another; fork/join on the context stream,
+ * capturable into one CUDA graph.  The caller's shape: the per-matrix make_plan + qmcur loop of
+ * the reference's scaling experiment (pkg/src/qcur/bench.py:346-351). */
+int qcur_approx_batched(qcur_ctx* ctx, int64_t batch, const double* const* x_devs, int64_t m, int64_t n, int strategy,
+                        const uint64_t* states, int64_t num_cols, int64_t num_rows, int64_t* col_idx_dev,
+                        int64_t* row_idx_dev, double* c_dev, double* u_dev, double* r_dev, double psnr_scale,
+                        int core, double* err4_dev, int lanes);
 /* read back and clear the device status word; returns the mapped status code */
 int qcur_check(qcur_ctx* ctx);
 /* Asynchronous status: queue a copy of the context's status word to host_dst (pinned) and

@@ -83,6 +83,30 @@ __global__ void k_conj_transpose(const double* __restrict__ A, int64_t m, int64_
   }
 }
 
+// status words of a batch's lane contexts OR-ed into the caller's, then cleared
+struct StatusSrc {
+  unsigned* p[8];
+  int n;
+};
+__global__ void k_status_or(unsigned* dst, StatusSrc src) {
+  if (threadIdx.x == 0) {
+    unsigned v = 0;
+    for (int k = 0; k < src.n; ++k) {
+      v |= *src.p[k];
+      *src.p[k] = 0u;
+    }
+    *dst |= v;
+  }
+}
+
+void launch_status_or(unsigned* dst, unsigned* const* srcs, int n, cudaStream_t st) {
+  StatusSrc s{};
+  s.n = n < 8 ? n : 8;
+  for (int k = 0; k < s.n; ++k) s.p[k] = srcs[k];
+  ++::qcur::g_launches;
+  k_status_or<<<1, 32, 0, st>>>(dst, s);
+}
+
 // Deterministic fixed-order reduction of (a, b) pairs: out2 = (sum a, sum b).
 __global__ void k_reduce_pairs(const double* __restrict__ parts, int64_t nparts, double* __restrict__ out2) {
   __shared__ double sa[1024], sb[1024];

@@ -333,6 +333,7 @@ struct OzProb {
 // up to two independent products in one launch (the SMs split by work units)
 struct OzGemm {
   int L, total;
+  int exp;  // timing experiments only (QCUR_OZ_EXP=1: the epilogue releases TMEM without reading it)
   OzProb pr[2];
   int p[kOzMaxMod];
   double pinv[kOzMaxMod];
@@ -455,6 +456,12 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       const OzProb& q = P.pr[unit_coords(P, u, l, mb, nb)];
       mbar_wait(tfull, (unsigned)t & 1u);
       tc_fence_after();
+      if (P.exp) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty);
+        continue;
+      }
       const int64_t row = (int64_t)mb * OZ_BM + rloc;
       const int p = P.p[l];
       const double pinv = P.pinv[l];
@@ -1075,6 +1082,11 @@ void oz_launch_gemm(const OzJob* jobs, int nj, int L, cudaStream_t st) {
   if (first_on_device(attr)) {
     cudaFuncSetAttribute(k_oz_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM);
   }
+  static const int exp_env = [] {
+    const char* e = std::getenv("QCUR_OZ_EXP");
+    return e ? std::atoi(e) : 0;
+  }();
+  P.exp = exp_env;
   const int grid = P.total < oz_sms() ? P.total : oz_sms();
   const OzJob& j1 = nj > 1 ? jobs[1] : jobs[0];
   ++::qcur::g_launches;

@@ -40,10 +40,13 @@ namespace {
 
 using namespace tc;
 
-constexpr int OE_BM = 128, OE_BN = 80, OE_BK = 32, OE_STAGES = 5, OE_DIG = 6;
+// K = 64 bytes per stage (64-byte swizzle): TMA delivers 64-byte row segments, twice the rate of
+// 32-byte ones (tools/tma_probe.cu: 14.5 vs 9.2 TB/s), so the 21 x 2 MMAs of a stage are no longer
+// starved; two 78 KB stages fill shared memory
+constexpr int OE_BM = 128, OE_BN = 80, OE_BK = 64, OE_STAGES = 2, OE_DIG = 6;
 constexpr int OE_EPI_WARPS = 16, OE_THREADS = 64 + 32 * OE_EPI_WARPS;  // 4 epilogue warps per TMEM lane quarter
-constexpr int OE_A_BYTES = OE_DIG * OE_BM * OE_BK;  // 24 KB
-constexpr int OE_B_BYTES = OE_DIG * OE_BN * OE_BK;  // 15 KB
+constexpr int OE_A_BYTES = OE_DIG * OE_BM * OE_BK;  // 48 KB
+constexpr int OE_B_BYTES = OE_DIG * OE_BN * OE_BK;  // 30 KB
 constexpr int OE_STAGE = OE_A_BYTES + OE_B_BYTES;
 constexpr int OE_SMEM = 1024 + OE_STAGES * OE_STAGE + 256;
 constexpr int OE_BITS = 54;
@@ -178,6 +181,7 @@ struct OeParams {
   int kblocks, mblocks, nblocks, total;
   int groups;  // (row block, group of CL column blocks) work units of a cluster
   uint32_t idesc;
+  int exp;  // timing experiments only (QCUR_OE_EXP): 1 = epilogue skips TMEM, 2 = and skips X / statistics
 };
 
 // CL CTAs per cluster work on one row block and CL adjacent column blocks: the A digit tile
@@ -258,7 +262,7 @@ __global__ void __launch_bounds__(OE_THREADS, 1)
     // the whole warp runs the issue loop (uniform control flow: descriptors and counters live in
     // uniform registers, no per-MMA lane election loops); one elected lane issues each k-block's
     // 21 MMAs and its commit
-    const uint64_t adesc0 = umma_desc_sw32(smem_u32(smem));
+    const uint64_t adesc0 = umma_desc_sw64(smem_u32(smem));
     int stage = 0;
     unsigned phase = 0;
     int t = 0;
@@ -272,27 +276,29 @@ __global__ void __launch_bounds__(OE_THREADS, 1)
         const uint64_t bd0 = ad0 + (uint64_t)(OE_A_BYTES >> 4);
         if (elect_one_sync()) {
           // A digit s is shared by its 7 - max(1, 7 - s) products: it is read from shared
-          // memory once (collector::a fill / use / lastuse), so a k-block moves 6 A tiles and
-          // 21 B tiles through the shared-memory port instead of 21 + 21
+          // memory once per K half (collector::a fill / use / lastuse)
 #pragma unroll
-          for (int s = 1; s <= OE_DIG; ++s) {
-            const int t0 = 7 - s > 1 ? 7 - s : 1;
+          for (int kk = 0; kk < OE_BK / 32; ++kk) {
 #pragma unroll
-            for (int tt = t0; tt <= OE_DIG; ++tt) {
-              const int L = s + tt - 7;  // accumulator of level s + t
-              const int first_s = L + 1 > 1 ? L + 1 : 1;
-              const uint32_t d = tbase + (uint32_t)(L * OE_BN);
-              const uint64_t ad = ad0 + (uint64_t)(((s - 1) * OE_BM * OE_BK) >> 4);
-              const uint64_t bd = bd0 + (uint64_t)(((tt - 1) * OE_BN * OE_BK) >> 4);
-              const uint32_t acc = (kb > 0 || s != first_s) ? 1u : 0u;
-              if (t0 == OE_DIG)
-                mma_i8(d, ad, bd, P.idesc, acc);
-              else if (tt == t0)
-                mma_i8_coll<1>(d, ad, bd, P.idesc, acc);
-              else if (tt == OE_DIG)
-                mma_i8_coll<3>(d, ad, bd, P.idesc, acc);
-              else
-                mma_i8_coll<2>(d, ad, bd, P.idesc, acc);
+            for (int s = 1; s <= OE_DIG; ++s) {
+              const int t0 = 7 - s > 1 ? 7 - s : 1;
+#pragma unroll
+              for (int tt = t0; tt <= OE_DIG; ++tt) {
+                const int L = s + tt - 7;  // accumulator of level s + t
+                const int first_s = L + 1 > 1 ? L + 1 : 1;
+                const uint32_t d = tbase + (uint32_t)(L * OE_BN);
+                const uint64_t ad = ad0 + (uint64_t)((((s - 1) * OE_BM * OE_BK) + kk * 32) >> 4);
+                const uint64_t bd = bd0 + (uint64_t)((((tt - 1) * OE_BN * OE_BK) + kk * 32) >> 4);
+                const uint32_t acc = (kb > 0 || kk > 0 || s != first_s) ? 1u : 0u;
+                if (t0 == OE_DIG)
+                  mma_i8(d, ad, bd, P.idesc, acc);
+                else if (tt == t0)
+                  mma_i8_coll<1>(d, ad, bd, P.idesc, acc);
+                else if (tt == OE_DIG)
+                  mma_i8_coll<3>(d, ad, bd, P.idesc, acc);
+                else
+                  mma_i8_coll<2>(d, ad, bd, P.idesc, acc);
+              }
             }
           }
           if constexpr (CL == 1)
@@ -330,6 +336,16 @@ __global__ void __launch_bounds__(OE_THREADS, 1)
       double pr[QW][4];
       mbar_wait(tfull, (unsigned)t & 1u);
       tc_fence_after();
+      if (P.exp) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty);
+        if (P.exp == 2) continue;
+#pragma unroll
+        for (int i = 0; i < QW; ++i)
+#pragma unroll
+          for (int h = 0; h < 4; ++h) pr[i][h] = 0.0;
+      } else
 #pragma unroll
       for (int i = 0; i < QW; ++i) {
         uint32_t lv[6][4];
@@ -345,9 +361,11 @@ __global__ void __launch_bounds__(OE_THREADS, 1)
           pr[i][h] = acc;
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(tempty);  // TMEM free: the next tile's MMAs start now
+      if (!P.exp) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty);  // TMEM free: the next tile's MMAs start now
+      }
       if (rvalid) {
 #pragma unroll
         for (int i = 0; i < QW; ++i) {
@@ -408,7 +426,7 @@ bool oe_digit_map(CUtensorMap* map, const int8_t* base, int64_t K, int64_t rows,
   cuuint32_t box[3] = {(cuuint32_t)OE_BK, (cuuint32_t)box_rows, (cuuint32_t)box_digits};
   cuuint32_t estr[3] = {1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -530,6 +548,11 @@ int launch_ozaki_error_gemm(const double* X, int64_t ldx, int64_t m, int64_t n, 
   p.nblocks = pl.nblocks;
   p.total = pl.total;
   p.groups = pl.mblocks * ((pl.nblocks + CL - 1) / CL);
+  static const int exp_env = [] {
+    const char* e = std::getenv("QCUR_OE_EXP");
+    return e ? std::atoi(e) : 0;
+  }();
+  p.exp = exp_env;
   // kind::i8: D = s32, A/B signed int8, K-major, N = 80, M = 128
   p.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OE_BN >> 3) << 17) | ((uint32_t)(OE_BM >> 4) << 24);
   static std::atomic<unsigned> attr{0};

@@ -66,6 +66,7 @@ void launch_gather_cols(const double* X, int64_t m, int64_t ldx, const int64_t* 
                         cudaStream_t st);
 void launch_gather_rows(const double* X, int64_t n, int64_t ldx, const int64_t* I, int64_t r, double* R,
                         cudaStream_t st);
+void launch_status_or(unsigned* dst, unsigned* const* srcs, int n, cudaStream_t st);
 void launch_complex_adjoint(const double* X, int64_t m, int64_t n, double* chi, cudaStream_t st);
 void launch_conj_transpose(const double* A, int64_t m, int64_t n, int64_t lda, double* AH, int64_t ldah,
                            cudaStream_t st);

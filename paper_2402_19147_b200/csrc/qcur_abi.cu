@@ -89,6 +89,10 @@ struct qcur_ctx {
   std::map<std::pair<int64_t, int64_t>, int32_t*> rf_sched;  // rows + flat chunk job lists (length tail)
   std::string err;
   Profiler prof;
+  // qcur_approx_batched: child contexts (own streams, workspace, status), one per concurrent lane
+  std::vector<qcur_ctx*> lanes;
+  std::vector<cudaEvent_t> lane_ev;
+  cudaEvent_t ev_bfork = nullptr;
 
   // mark the end of a named phase (no-op unless profiling)
   void mark(const char* name) {
@@ -1150,6 +1154,13 @@ void qcur_destroy(qcur_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  for (size_t k = 0; k < ctx->lanes.size(); ++k) {
+    cudaStream_t ls = ctx->lanes[k]->stream;
+    qcur_destroy(ctx->lanes[k]);
+    cudaStreamDestroy(ls);
+    cudaEventDestroy(ctx->lane_ev[k]);
+  }
+  if (ctx->ev_bfork) cudaEventDestroy(ctx->ev_bfork);
   for (auto& kv : ctx->programs) cudaFree(kv.second.buf);
   for (auto& kv : ctx->rf_sched) cudaFree(kv.second);
   if (ctx->arena.base) cudaFree(ctx->arena.base);
@@ -1580,6 +1591,67 @@ int qcur_approx(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int st
     if (!rc && e != cudaSuccess) rc = ctx->cuda_fail(e, "priority join");
   }
   return rc;
+}
+
+// Batched approximations (cfg4; caller shape /root/reference/pkg/src/qcur/bench.py:346-351, one
+// make_plan + qmcur per matrix): `batch` independent m x n matrices through the whole pipeline of
+// qcur_approx.  Matrix b runs on lane b % L (L child contexts with their own stream, workspace and
+// status word), forked from and joined back to the caller's stream, so one matrix's
+// latency-bound phases (draws, Cholesky, small products) overlap the others' tensor-bound ones.
+// Capturable into one CUDA graph (event fork / join only).  Lane status words are OR-ed into the
+// context's own, so qcur_check reports the batch.
+int qcur_approx_batched(qcur_ctx* ctx, int64_t batch, const double* const* x_devs, int64_t m, int64_t n, int strategy,
+                        const uint64_t* states, int64_t c, int64_t r, int64_t* J, int64_t* I, double* C, double* U,
+                        double* R, double psnr_scale, int core, double* err4, int lanes) {
+  DeviceGuard device_guard_(ctx);
+  if (batch < 1 || !x_devs || !states) return ctx->fail(QCUR_E_PARAMETER, "approx_batched: empty batch");
+  if (lanes < 1) lanes = 4;
+  if (lanes > 8) lanes = 8;
+  if (lanes > batch) lanes = (int)batch;
+  cudaError_t e = cudaSuccess;
+  if (!ctx->ev_bfork) e = cudaEventCreateWithFlags(&ctx->ev_bfork, cudaEventDisableTiming);
+  while (e == cudaSuccess && (int)ctx->lanes.size() < lanes) {
+    qcur_ctx* child = nullptr;
+    const int rc = qcur_create(ctx->device, &child);
+    if (rc) return ctx->fail(rc, "approx_batched: lane context creation failed");
+    cudaStream_t ls = nullptr;
+    cudaEvent_t ev = nullptr;
+    e = cudaStreamCreateWithFlags(&ls, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    child->stream = ls;
+    child->gemm_mode = ctx->gemm_mode;
+    child->prio = ctx->prio;
+    child->kappa_limit = ctx->kappa_limit;
+    child->force_robust = ctx->force_robust;
+    ctx->lanes.push_back(child);
+    ctx->lane_ev.push_back(ev);
+  }
+  if (e != cudaSuccess) return ctx->cuda_fail(e, "approx_batched lanes");
+  if ((e = cudaEventRecord(ctx->ev_bfork, ctx->stream)) != cudaSuccess) return ctx->cuda_fail(e, "batch fork");
+  for (int k = 0; k < lanes; ++k) {
+    qcur_ctx* L = ctx->lanes[k];
+    L->gemm_mode = ctx->gemm_mode;
+    L->force_robust = ctx->force_robust;
+    L->kappa_limit = ctx->kappa_limit;
+    if ((e = cudaStreamWaitEvent(L->stream, ctx->ev_bfork, 0)) != cudaSuccess) return ctx->cuda_fail(e, "batch fork");
+  }
+  for (int64_t b = 0; b < batch; ++b) {
+    qcur_ctx* L = ctx->lanes[b % lanes];
+    const int rc = qcur_approx(L, x_devs[b], m, n, strategy, states + 4 * b, c, r, J + b * c, I + b * r,
+                               C + b * m * c * 4, U + b * c * r * 4, R + b * r * n * 4, psnr_scale, core, err4 + 4 * b);
+    if (rc) return ctx->fail(rc, "approx_batched: matrix %lld: %s", (long long)b, L->err.c_str());
+  }
+  unsigned* st[8] = {};
+  for (int k = 0; k < lanes; ++k) {
+    qcur_ctx* L = ctx->lanes[k];
+    if ((e = cudaEventRecord(ctx->lane_ev[k], L->stream)) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(ctx->stream, ctx->lane_ev[k], 0)) != cudaSuccess)
+      return ctx->cuda_fail(e, "batch join");
+    st[k] = L->status_dev;
+  }
+  launch_status_or(ctx->status_dev, st, lanes, ctx->stream);
+  CK_LAUNCH(ctx, "batch status");
+  return QCUR_OK;
 }
 
 int qcur_check(qcur_ctx* ctx) {

@@ -96,6 +96,12 @@ __device__ __forceinline__ uint64_t umma_desc_sw32(uint32_t addr) {
   return (uint64_t)((addr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(256 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)6 << 61);
 }
+// K-major operand tile with 64-byte rows, 64-byte swizzle, 8-row groups 512 bytes apart; the second
+// 32-byte K half of a row is addressed by advancing the start address 32 bytes
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t addr) {
+  return (uint64_t)((addr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
+}
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])

@@ -519,6 +519,59 @@ class DeviceApprox:
         return psnr_from_stats(u8_sq, imag_sq, self.m, self.n)
 
 
+class DeviceBatch:
+    """Preallocated outputs for repeated batched approximations of same-shape device matrices
+    (qcur_approx_batched): the per-matrix make_plan + qmcur loop of the reference's scaling
+    experiment (pkg/src/qcur/bench.py:346-351) as one ABI call whose matrices overlap on
+    internal lanes; graph=True replays the whole batch as one CUDA graph."""
+
+    def __init__(self, batch: int, m: int, n: int, c: int, r: int, dev=None, lanes: int = 4):
+        self.dev = dev or _native.device()
+        d = self.dev
+        self.batch, self.m, self.n, self.c, self.r, self.lanes = batch, m, n, c, r, lanes
+        self.J = d.empty(batch, c, dtype=d.torch.int64)
+        self.I = d.empty(batch, r, dtype=d.torch.int64)
+        self.C = d.empty(batch, m, c, 4)
+        self.U = d.empty(batch, c, r, 4)
+        self.R = d.empty(batch, r, n, 4)
+        self.err4 = d.empty(batch, 4)
+
+    def run(self, xds, strategy: str, seeds, psnr_scale: float = 0.0, core: str = "projection",
+            graph: bool = False) -> None:
+        if len(xds) != self.batch or len(seeds) != self.batch:
+            raise ShapeError(f"batch of {self.batch} matrices expected, got {len(xds)} / {len(seeds)} seeds")
+        if graph:
+            key = (tuple(x.data_ptr() for x in xds), strategy, tuple(int(s) for s in seeds), float(psnr_scale), core)
+            if getattr(self, "_gkey", None) != key:
+                torch = self.dev.torch
+                self.run(xds, strategy, seeds, psnr_scale, core)  # sizes every lane's workspace first
+                self.dev.synchronize()
+                g = torch.cuda.CUDAGraph()
+                before = self.dev.launches()
+                with torch.cuda.graph(g):
+                    self.run(xds, strategy, seeds, psnr_scale, core)
+                self._graph, self._gkey = g, key
+                self.graph_kernels = self.dev.launches() - before
+            self._graph.replay()
+            self.graph_replays = getattr(self, "graph_replays", 0) + 1
+            return
+        core_code = _check_core(core)
+        states = np.concatenate([_native.state_from_seed(int(sd)) for sd in seeds]).astype(np.uint64)
+        ptrs = (ctypes.c_void_p * self.batch)(*[x.data_ptr() for x in xds])
+        self._keep = (states, ptrs)
+        self.dev.call("qcur_approx_batched", self.batch, ptrs, self.m, self.n,
+                      _native.STRATEGY_CODES[_check_strategy(strategy)], states.ctypes.data_as(_native._u64p),
+                      self.c, self.r, self.J.data_ptr(), self.I.data_ptr(), self.C.data_ptr(), self.U.data_ptr(),
+                      self.R.data_ptr(), float(psnr_scale), core_code, self.err4.data_ptr(), int(self.lanes))
+
+    def check(self) -> None:
+        self.dev.call("qcur_check")
+
+    def rel_errors(self) -> np.ndarray:
+        e = self.err4.cpu().numpy()
+        return np.sqrt(e[:, 0]) / np.sqrt(e[:, 1])
+
+
 def qmcur_device(xd, strategy: str, rank: int, seed: int, num_rows: int, num_cols: int) -> DeviceApprox:
     """One whole approximation on a device-resident interleaved X (m, n, 4)."""
     m, n = int(xd.shape[0]), int(xd.shape[1])
