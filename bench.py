@@ -666,7 +666,7 @@ def main() -> None:
     if batch > 1:
         from paper_2402_19147_b200.cur import DeviceBatch
 
-        bt = DeviceBatch(len(mine), m, n, c, r, dev, lanes=int(os.environ.get("QCUR_BATCH_LANES", "4")))
+        bt = DeviceBatch(len(mine), m, n, c, r, dev, lanes=int(os.environ.get("QCUR_BATCH_LANES", "8")))
         lanes = [(dev, bt, xs, torch.cuda.current_stream())]
 
     def step(graph=use_graph):

@@ -213,6 +213,11 @@ int qcur_synth_image(qcur_ctx* ctx, int64_t m, int64_t n, int nterms, uint64_t s
 /* sq of a row block and numpy's sequential column sums continued from acc_in (nullable) */
 int qcur_colsums_seq(qcur_ctx* ctx, const double* x_dev, int64_t rows, int64_t n, const double* acc_in_dev,
                      double* colsum_out_dev, double* sq_out_dev);
+/* The same over a slice of columns: x_dev points at the slice's first column (row pitch ldx
+ * quaternions), sq_out at its first column in the full sq rows (pitch ldsq): the row-sharded
+ * path pipelines numpy's sequential column chain across ranks chunk by chunk. */
+int qcur_colsums_seq_ex(qcur_ctx* ctx, const double* x_dev, int64_t rows, int64_t ncols, int64_t ldx,
+                        const double* acc_in, double* colsum_out, double* sq_out, int64_t ldsq);
 /* numpy pairwise sums of nseg segments of `length` doubles (stride apart) */
 int qcur_pairwise_sums(qcur_ctx* ctx, const double* data_dev, int64_t nseg, int64_t stride, int64_t length,
                        double* out_dev);

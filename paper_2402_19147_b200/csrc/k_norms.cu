@@ -33,7 +33,7 @@ constexpr int kStripThreads = 256;
 __global__ void __launch_bounds__(kStripThreads) k1_colstrip(const double* __restrict__ X, int64_t m, int64_t n,
                                                              int64_t ldx, double* __restrict__ sq,
                                                              double* __restrict__ colsum,
-                                                             const double* __restrict__ acc_in) {
+                                                             const double* __restrict__ acc_in, int64_t ldsq) {
   __shared__ double sqs[2][kStripRB][kStripW];
   const int tid = threadIdx.x;
   const int lane = tid & 31, col = lane & (kStripW - 1);
@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(kStripThreads) k1_colstrip(const double* __res
       const int rr = prow + 16 * k;
       sqs[b][rr][col] = v;
       const int64_t i = r0 + rr;
-      if (jok && i < m) sq[i * n + j] = v;
+      if (jok && i < m) sq[i * ldsq + j] = v;
     }
     if (s + 1 < nstages) load_stage(r0 + kStripRB);
     __syncthreads();
@@ -266,10 +266,10 @@ __global__ void k_fill(double* __restrict__ out, int64_t len, double v) {
 // host launchers
 // ---------------------------------------------------------------------------
 void launch_colstrip(const double* X, int64_t m, int64_t n, int64_t ldx, double* sq, double* colsum,
-                     cudaStream_t st, const double* acc_in) {
+                     cudaStream_t st, const double* acc_in, int64_t ldsq) {
   dim3 grid((unsigned)((n + kStripW - 1) / kStripW));
   ++::qcur::g_launches;
-  k1_colstrip<<<grid, kStripThreads, 0, st>>>(X, m, n, ldx, sq, colsum, acc_in);
+  k1_colstrip<<<grid, kStripThreads, 0, st>>>(X, m, n, ldx, sq, colsum, acc_in, ldsq > 0 ? ldsq : n);
 }
 
 void launch_pairwise(const double* data, int64_t nseg, int64_t seg_stride, const DevPairwise& pw, double* scratch,

@@ -464,7 +464,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       }
       const int64_t row = (int64_t)mb * OZ_BM + rloc;
       const int p = P.p[l];
-      const double pinv = P.pinv[l];
+      const float pinvf = (float)P.pinv[l];
       uint8_t* out = q.res + l * q.res_plane + row * q.res_pitch + (int64_t)nb * q.BN;
       for (int c0 = 0; c0 < q.BN; c0 += 32) {
         uint32_t v[32];
@@ -479,9 +479,14 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           if (l == 0) {
             r = z & 255;
           } else {
-            r = z - (int)floor((double)z * pinv) * p;
-            r = r < 0 ? r + p : r;
-            r = r >= p ? r - p : r;
+            // quotient in FP32 (full-rate pipe): |z| < 2^31 and p >= 197 put the float quotient
+            // within 2 of the true one, so r = z - q p (exact in int32) needs at most two
+            // corrections either way
+            r = z - __float2int_rd(__int2float_rn(z) * pinvf) * p;
+            r += r < 0 ? p : 0;
+            r += r < 0 ? p : 0;
+            r -= r >= p ? p : 0;
+            r -= r >= p ? p : 0;
           }
           w[i >> 2] |= (uint32_t)r << (8 * (i & 3));
         }

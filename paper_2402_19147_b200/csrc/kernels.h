@@ -29,8 +29,9 @@ struct DevPairwise {
 };
 
 // k_norms.cu
+// ldsq: row pitch of sq (0 = n): a column slice of X writes its slice of the full sq rows
 void launch_colstrip(const double* X, int64_t m, int64_t n, int64_t ldx, double* sq, double* colsum, cudaStream_t st,
-                     const double* acc_in = nullptr);
+                     const double* acc_in = nullptr, int64_t ldsq = 0);
 void launch_pairwise(const double* data, int64_t nseg, int64_t seg_stride, const DevPairwise& pw, double* scratch,
                      double* out, cudaStream_t st, bool with_top = true, bool reverse = false);
 // fused tail of the length distributions (axes of one pairwise chunk; see k_norms.cu)

@@ -1863,6 +1863,15 @@ int qcur_colsums_seq(qcur_ctx* ctx, const double* x_dev, int64_t rows, int64_t n
   return QCUR_OK;
 }
 
+int qcur_colsums_seq_ex(qcur_ctx* ctx, const double* x_dev, int64_t rows, int64_t ncols, int64_t ldx,
+                        const double* acc_in, double* colsum_out, double* sq_out, int64_t ldsq) {
+  DeviceGuard device_guard_(ctx);
+  if (rows < 1 || ncols < 1 || ldx < ncols || ldsq < ncols) return ctx->fail(QCUR_E_SHAPE, "colsums_seq_ex: bad sizes");
+  launch_colstrip(x_dev, rows, ncols, ldx, sq_out, colsum_out, ctx->stream, acc_in, ldsq);
+  CK_LAUNCH(ctx, "colsums_seq_ex");
+  return QCUR_OK;
+}
+
 int qcur_pairwise_sums(qcur_ctx* ctx, const double* data, int64_t nseg, int64_t stride, int64_t length,
                        double* out) {
   DeviceGuard device_guard_(ctx);

@@ -525,7 +525,7 @@ class DeviceBatch:
     experiment (pkg/src/qcur/bench.py:346-351) as one ABI call whose matrices overlap on
     internal lanes; graph=True replays the whole batch as one CUDA graph."""
 
-    def __init__(self, batch: int, m: int, n: int, c: int, r: int, dev=None, lanes: int = 4):
+    def __init__(self, batch: int, m: int, n: int, c: int, r: int, dev=None, lanes: int = 8):
         self.dev = dev or _native.device()
         d = self.dev
         self.batch, self.m, self.n, self.c, self.r, self.lanes = batch, m, n, c, r, lanes

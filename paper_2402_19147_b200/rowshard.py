@@ -5,7 +5,7 @@ Rank g of G owns rows [g m/G, (g+1) m/G) of X (generated or loaded locally; a
 torch.distributed collective on device buffers (NCCL over NVLink):
 
   K1  column sums     numpy's *sequential* axis-0 order continued rank to rank
-                      (send/recv chain of n doubles), then broadcast;
+                      (send/recv chain pipelined by column chunks), then broadcast;
       row sums        local (rows are whole);
       flat total      each rank's rows are one complete subtree of numpy's
                       pairwise tree (checked); G partials all-gathered and
@@ -164,6 +164,12 @@ class GpuOps:
                       col.data_ptr(), sq.data_ptr())
         return sq, col
 
+    def colsums_chunk(self, xb, c0, c1, acc, colsum, sq):
+        """Columns [c0, c1) of the sequential chain: colsum[c0:c1] and sq[:, c0:c1] (row pitch n)."""
+        rows, n = int(xb.shape[0]), int(xb.shape[1])
+        self.dev.call("qcur_colsums_seq_ex", xb.data_ptr() + 32 * c0, rows, c1 - c0, n,
+                      0 if acc is None else acc.data_ptr(), colsum.data_ptr() + 8 * c0, sq.data_ptr() + 8 * c0, n)
+
     def pairwise(self, data, nseg, length):
         out = self.dev.empty(int(nseg))
         self.dev.call("qcur_pairwise_sums", data.data_ptr(), int(nseg), int(length), int(length), out.data_ptr())
@@ -280,10 +286,18 @@ def approx_rowsharded(ops, comm, xb, m: int, strategy: str, seed: int, c: int, r
         if not subtree_aligned(m * n, G):
             raise NotImplementedError(
                 f"numpy's pairwise tree over {m}x{n} does not split at the row blocks of {G} ranks")
-        acc = None if g == 0 else comm.recv_like(ops.vec(n), g - 1)
-        sq, colsum = ops.colsums_seq(xb, acc)
-        if g < G - 1:
-            comm.send(colsum, g + 1)
+        # numpy's sequential column chain continued rank to rank, pipelined by column chunks: rank
+        # g works on chunk k as soon as rank g-1 has passed it on (a wavefront: G + K - 1 chunk
+        # times instead of G whole passes)
+        nchunks = 1 if G == 1 else max(1, min(4 * G, n // 64))
+        bounds = [n * k // nchunks for k in range(nchunks + 1)]
+        sq, colsum = ops.vec(rows_b * n), ops.vec(n)
+        for k in range(nchunks):
+            c0, c1 = bounds[k], bounds[k + 1]
+            acc = None if g == 0 else comm.recv_like(ops.vec(c1 - c0), g - 1)
+            ops.colsums_chunk(xb, c0, c1, acc, colsum, sq)
+            if g < G - 1:
+                comm.send(colsum[c0:c1], g + 1)
         colsum = comm.broadcast(colsum, G - 1)
         rowsum = ops.pairwise(sq, rows_b, n)
         part = ops.pairwise(sq, 1, rows_b * n)

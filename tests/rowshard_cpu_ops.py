@@ -71,6 +71,16 @@ class CpuOps:
             col = col + sq[i]
         return torch.from_numpy(np.ascontiguousarray(sq.ravel())), torch.from_numpy(col)
 
+    def colsums_chunk(self, xb, c0, c1, acc, colsum, sq):
+        a0, a1, a2, a3 = planes(xb[:, c0:c1])
+        blk = ((a0 * a0 + a1 * a1) + a2 * a2) + a3 * a3
+        col = np.zeros(c1 - c0) if acc is None else acc.numpy().copy()
+        for i in range(blk.shape[0]):  # numpy's sequential axis-0 order
+            col = col + blk[i]
+        colsum[c0:c1] = torch.from_numpy(col)
+        n = xb.shape[1]
+        sq.view(xb.shape[0], n)[:, c0:c1] = torch.from_numpy(np.ascontiguousarray(blk))
+
     def pairwise(self, data, nseg, length):
         return torch.from_numpy(np.ascontiguousarray(data.numpy().reshape(nseg, length).sum(axis=1)))
 
