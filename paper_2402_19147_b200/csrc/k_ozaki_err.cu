@@ -49,8 +49,9 @@ constexpr int OE_A_BYTES = OE_DIG * OE_BM * OE_BK;  // 48 KB
 constexpr int OE_B_BYTES = OE_DIG * OE_BN * OE_BK;  // 30 KB
 constexpr int OE_STAGE = OE_A_BYTES + OE_B_BYTES;
 constexpr int OE_SMEM = 1024 + OE_STAGES * OE_STAGE + 256;
-constexpr int OE_BITS = 54;
-constexpr int kOeCluster = 2;  // CTAs per cluster sharing the A digit tile by TMA multicast  // |P'|, |R'| <= 2^54: seven balanced base-256 digits
+constexpr int OE_BITS = 54;            // |P'|, |R'| <= 2^54: seven balanced base-256 digits
+constexpr int kOeCluster = 2;          // CTAs per cluster sharing the A digit tile by TMA multicast
+constexpr bool kOePairDefault = false;  // CTA-pair (cta_group::2) kernel by default
 
 __device__ __forceinline__ double i2d(uint32_t v) {  // exact int32 -> double (one DADD)
   return __hiloint2double(0x43380000, (int)(v ^ 0x80000000u)) - 6755401588539392.0;  // 1.5*2^52 + 2^31
@@ -405,6 +406,206 @@ __global__ void __launch_bounds__(OE_THREADS, 1)
   if constexpr (CL > 1) cluster_sync_all();
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant (tcgen05.mma.cta_group::2, M = 256): the two CTAs of a cluster compute a
+// 256 x 80 tile; each loads its own 128 rows of the A digits and 40 of the 80 B rows, so a CTA's
+// stage is 63 KB instead of 78 KB (three stages fit shared memory instead of two) and the
+// MMA instruction count halves.  CTA 0 issues every MMA; the operand bytes of both CTAs complete
+// on CTA 0's "full" barrier, MMA completions are committed to both CTAs' "empty" / "tfull"
+// barriers, and both CTAs' epilogue warps release TMEM on CTA 0's "tempty" barrier.
+// ---------------------------------------------------------------------------
+constexpr int OE2_BNH = OE_BN / 2;  // B rows per CTA
+constexpr int OE2_STAGES = 3;
+constexpr int OE2_A_BYTES = OE_DIG * OE_BM * OE_BK;     // 48 KB
+constexpr int OE2_B_BYTES = OE_DIG * OE2_BNH * OE_BK;   // 15 KB
+constexpr int OE2_STAGE = OE2_A_BYTES + OE2_B_BYTES;
+constexpr int OE2_SMEM = 1024 + OE2_STAGES * OE2_STAGE + 256;
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OE_THREADS, 1)
+    k_oe_err_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                  const __grid_constant__ CUtensorMap tmX, const __grid_constant__ OeParams P) {
+  extern __shared__ uint8_t smem_raw[];
+  const unsigned pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+  uint8_t* smem = smem_raw + pad;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + OE2_STAGES * OE2_STAGE);
+  uint64_t* empty = full + OE2_STAGES;
+  uint64_t* tfull = empty + OE2_STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int crank = (int)cluster_ctarank();
+  const int cid = (int)cluster_id_x(), ncl = (int)ncluster_x();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < OE2_STAGES; ++s) {
+      mbar_init(&full[s], 1);   // CTA 0's producer arrive (+ both CTAs' transaction bytes)
+      mbar_init(&empty[s], 1);  // CTA 0's MMA commit, multicast to both CTAs
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 2 * OE_EPI_WARPS);  // the epilogue warps of both CTAs (used in CTA 0)
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {  // the same warp in both CTAs allocates the pair's TMEM
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tslot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+      int stage = 0;
+      unsigned phase = 0;
+      for (int g = cid; g < P.groups; g += ncl) {
+        const int mb = g % P.mblocks, nb = g / P.mblocks;  // 256-row blocks fastest
+        tma_prefetch_2d(&tmX, nb * OE_BN, mb * 2 * OE_BM + crank * OE_BM);
+        for (int kb = 0; kb < P.kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1u);
+          if (crank == 0) mbar_expect_tx(&full[stage], 2 * OE2_STAGE);
+          uint8_t* st = smem + stage * OE2_STAGE;
+          tma_load_3d_2sm(st, &tmA, kb * OE_BK, mb * 2 * OE_BM + crank * OE_BM, 0, &full[stage]);
+          tma_load_3d_2sm(st + OE2_A_BYTES, &tmB, kb * OE_BK, nb * OE_BN + crank * OE2_BNH, 0, &full[stage]);
+          if (++stage == OE2_STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (crank == 0) {
+      const uint64_t adesc0 = umma_desc_sw64(smem_u32(smem));
+      int stage = 0;
+      unsigned phase = 0;
+      int t = 0;
+      for (int g = cid; g < P.groups; g += ncl, ++t) {
+        mbar_wait(tempty, ((unsigned)t & 1u) ^ 1u);
+        tc_fence_after();
+        for (int kb = 0; kb < P.kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t ad0 = adesc0 + (uint64_t)((stage * OE2_STAGE) >> 4);
+          const uint64_t bd0 = ad0 + (uint64_t)(OE2_A_BYTES >> 4);
+          if (elect_one_sync()) {
+#pragma unroll
+            for (int kk = 0; kk < OE_BK / 32; ++kk) {
+#pragma unroll
+              for (int s = 1; s <= OE_DIG; ++s) {
+                const int t0 = 7 - s > 1 ? 7 - s : 1;
+#pragma unroll
+                for (int tt = t0; tt <= OE_DIG; ++tt) {
+                  const int L = s + tt - 7;
+                  const int first_s = L + 1 > 1 ? L + 1 : 1;
+                  const uint32_t d = tbase + (uint32_t)(L * OE_BN);
+                  const uint64_t ad = ad0 + (uint64_t)((((s - 1) * OE_BM * OE_BK) + kk * 32) >> 4);
+                  const uint64_t bd = bd0 + (uint64_t)((((tt - 1) * OE2_BNH * OE_BK) + kk * 32) >> 4);
+                  const uint32_t acc = (kb > 0 || kk > 0 || s != first_s) ? 1u : 0u;
+                  if (t0 == OE_DIG)
+                    mma_i8_2sm<0>(d, ad, bd, P.idesc, acc);
+                  else if (tt == t0)
+                    mma_i8_2sm<1>(d, ad, bd, P.idesc, acc);
+                  else if (tt == OE_DIG)
+                    mma_i8_2sm<3>(d, ad, bd, P.idesc, acc);
+                  else
+                    mma_i8_2sm<2>(d, ad, bd, P.idesc, acc);
+                }
+              }
+            }
+            mma_commit_2sm_mc(&empty[stage], 3);  // the stage is free in both CTAs
+          }
+          __syncwarp();
+          if (++stage == OE2_STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        if (elect_one_sync()) mma_commit_2sm_mc(tfull, 3);
+        __syncwarp();
+      }
+    }
+  } else {
+    const int quarter = warp & 3, sub = (warp - 2) >> 2;
+    const int rloc = quarter * 32 + lane;
+    constexpr int QW = OE_BN / 4 / 4;
+    const double sc = P.psnr_scale;
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    int t = 0;
+    for (int g = cid; g < P.groups; g += ncl, ++t) {
+      const int mb = g % P.mblocks, nb = g / P.mblocks;
+      const int64_t row = (int64_t)mb * 2 * OE_BM + crank * OE_BM + rloc;
+      const bool rvalid = row < P.m;
+      const int er = rvalid ? P.ea[row] : 0;
+      const double* xrow = P.X + (rvalid ? row : 0) * P.ldx;
+      const int64_t jq0 = ((int64_t)nb * OE_BN + sub * 4 * QW) >> 2;
+      double pr[QW][4];
+      mbar_wait(tfull, (unsigned)t & 1u);
+      tc_fence_after();
+#pragma unroll
+      for (int i = 0; i < QW; ++i) {
+        uint32_t lv[6][4];
+        const uint32_t ta = tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(sub * 4 * QW + 4 * i);
+#pragma unroll
+        for (int L = 0; L < 6; ++L) tmem_ld4(ta + (uint32_t)(L * OE_BN), lv[L]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          double acc = i2d(lv[5][h]);
+#pragma unroll
+          for (int L = 4; L >= 0; --L) acc = fma(acc, 256.0, i2d(lv[L][h]));
+          pr[i][h] = acc;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {  // TMEM of this CTA drained: CTA 0's MMA warp may start the next tile
+        if (crank == 0)
+          mbar_arrive(tempty);
+        else
+          mbar_arrive_cluster(tempty, 0);
+      }
+      if (rvalid) {
+#pragma unroll
+        for (int i = 0; i < QW; ++i) {
+          const int64_t jq = jq0 + i;
+          if (4 * jq >= P.N) break;
+          const double4 xq = *reinterpret_cast<const double4*>(xrow + 4 * jq);
+          const double f = pow2(8 * 7 - er - P.eb[jq]);
+          const double xs[4] = {xq.x, xq.y, xq.z, xq.w};
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const double prh = pr[i][h] * f;
+            const double x = xs[h], d = x - prh;
+            v[0] = fma(d, d, v[0]);
+            v[1] = fma(x, x, v[1]);
+            if (h != 0) {
+              v[2] = fma(d, d, v[2]);
+              if (sc > 0.0) {
+                const double q = rint(fmin(fmax(sc * x, 0.0), 255.0)) - rint(fmin(fmax(sc * prh, 0.0), 255.0));
+                v[3] = fma(q, q, v[3]);
+              }
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = warp_sum(v[k]);
+    if (lane < 4) P.partials[((int64_t)blockIdx.x * OE_EPI_WARPS + (warp - 2)) * 4 + lane] = v[lane];
+  }
+  tc_fence_before();
+  cluster_sync_all();  // both CTAs done: no barrier or TMEM of the pair is used any more
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tbase) : "memory");
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 oe_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* f = nullptr;
@@ -560,6 +761,40 @@ int launch_ozaki_error_gemm(const double* X, int64_t ldx, int64_t m, int64_t n, 
     cudaFuncSetAttribute(k_oe_err<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, OE_SMEM);
     cudaFuncSetAttribute(k_oe_err<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, OE_SMEM);
     cudaFuncSetAttribute(k_oe_err<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, OE_SMEM);
+  }
+  static const int pair_env = [] {
+    const char* e = std::getenv("QCUR_OE_PAIR");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (pair_env == 1 || (pair_env < 0 && kOePairDefault)) {
+    // CTA pairs: 256-row blocks x 80-column blocks; A maps of 128 rows, B maps of 40 rows
+    CUtensorMap tmA2, tmB2;
+    if (!oe_digit_map(&tmA2, pd, pl.K, m, pl.Kp, OE_BM) || !oe_digit_map(&tmB2, rd, pl.K, pl.N, pl.Kp, OE2_BNH))
+      return 2;
+    const int mb2 = (int)((m + 2 * OE_BM - 1) / (2 * OE_BM));
+    p.mblocks = mb2;
+    p.groups = mb2 * pl.nblocks;
+    p.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OE_BN >> 3) << 17) | ((uint32_t)((2 * OE_BM) >> 4) << 24);
+    static std::atomic<unsigned> attr2{0};
+    if (first_on_device(attr2))
+      cudaFuncSetAttribute(k_oe_err_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, OE2_SMEM);
+    static int max_pairs = 0;
+    if (!max_pairs) {
+      cudaLaunchConfig_t qc{};
+      qc.gridDim = dim3((unsigned)(oe_sms() / 2 * 2));
+      qc.blockDim = dim3(OE_THREADS);
+      qc.dynamicSmemBytes = OE2_SMEM;
+      int nc = 0;
+      max_pairs = (cudaOccupancyMaxActiveClusters(&nc, k_oe_err_pair, &qc) == cudaSuccess && nc > 0) ? nc
+                                                                                                     : oe_sms() / 2;
+      (void)cudaGetLastError();
+    }
+    const int npairs = p.groups < max_pairs ? p.groups : max_pairs;
+    const int grid = 2 * npairs;
+    ++::qcur::g_launches;
+    k_oe_err_pair<<<grid, OE_THREADS, OE2_SMEM, st>>>(tmA2, tmB2, tmX, p);
+    launch_reduce_rows(parts, (int64_t)grid * OE_EPI_WARPS, 4, out4, st);
+    return 0;
   }
   cudaLaunchConfig_t cfg{};
   cfg.blockDim = dim3(OE_THREADS);
