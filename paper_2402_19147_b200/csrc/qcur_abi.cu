@@ -73,6 +73,8 @@ struct qcur_ctx {
   cudaStream_t side_stream = nullptr;  // residues of X for the INT8 GEMM, overlapped with the factorizations
   cudaEvent_t ev_sfork = nullptr, ev_sjoin = nullptr;
   int gemm_mode = 0;                   // Y = X Q_R: 0 auto, 1 FP64 DMMA, 2 INT8 tcgen05 (Ozaki II)
+  int xq_moduli = 15;                  // moduli of the INT8 X Q_R product (14 or 15; env QCUR_XQ_MODULI)
+  int herm_moduli = 15;                // moduli of the INT8 Hermitian products (Grams, Q_C^H Y; QCUR_HERM_MODULI)
   // qcur_approx runs its pipeline on a high-priority stream forked from the caller's, so that
   // the low-priority side stream (residues of X) only fills SMs the pipeline leaves idle
   cudaStream_t hi_stream = nullptr;
@@ -572,7 +574,7 @@ int factor_multi(qcur_ctx* ctx, const FactorSpec* specs_in, int ns) {
         ++np;
       }
       if (np == 0) return QCUR_OK;
-      if (launch_ozaki_herm(A, A, pp, qq, qq, lda, lda, G, ldg, np, kOzakiModuli, w, st))
+      if (launch_ozaki_herm(A, A, pp, qq, qq, lda, lda, G, ldg, np, ctx->herm_moduli, w, st))
         return ctx->fail(QCUR_E_CUDA, "int8 gram: tensor map encode failed");
       CK_LAUNCH(ctx, "int8 gram");
       return QCUR_OK;
@@ -878,7 +880,7 @@ void* int8_fork_prepare(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, in
   }
   cudaError_t e = cudaEventRecord(ctx->ev_sfork, ctx->stream);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->side_stream, ctx->ev_sfork, 0);
-  if (e == cudaSuccess && launch_ozaki_prepare(X, m, n, n, r, kOzakiModuli, ozws, ctx->side_stream)) {
+  if (e == cudaSuccess && launch_ozaki_prepare(X, m, n, n, r, ctx->xq_moduli, ozws, ctx->side_stream)) {
     *rc = ctx->fail(QCUR_E_CUDA, "int8 gemm: bad modulus count");
     return nullptr;
   }
@@ -901,14 +903,14 @@ int xq_product(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, int64_t ldx
     const int64_t rows = mc > 0 ? mc : m;
     void* ws = ctx->take<uint8_t>(ozaki_workspace_bytes(rows, n, r, kOzakiModuli));
     if (!ws) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (int8 X Q_R)");
-    if (launch_ozaki_prep_b(rows, n, QR, r, r, kOzakiModuli, ws, st))
+    if (launch_ozaki_prep_b(rows, n, QR, r, r, ctx->xq_moduli, ws, st))
       return ctx->fail(QCUR_E_CUDA, "int8 gemm: bad modulus count");
     // chunks of `rows` rows; the last one ends at row m and may overlap its predecessor (rows are
     // independent, so the overlap is recomputed to the same bits)
     for (int64_t i0 = 0; i0 < m; i0 += rows) {
       const int64_t a = i0 + rows <= m ? i0 : m - rows;
-      if (launch_ozaki_prepare(X + a * ldx * 4, rows, n, ldx, r, kOzakiModuli, ws, st) ||
-          launch_ozaki_multiply(rows, n, r, Y + a * r * 4, r, kOzakiModuli, ws, st))
+      if (launch_ozaki_prepare(X + a * ldx * 4, rows, n, ldx, r, ctx->xq_moduli, ws, st) ||
+          launch_ozaki_multiply(rows, n, r, Y + a * r * 4, r, ctx->xq_moduli, ws, st))
         return ctx->fail(QCUR_E_CUDA, "int8 gemm: tensor map encode failed");
     }
     CK_LAUNCH(ctx, "int8 X Q_R");
@@ -968,10 +970,10 @@ int qmcur_core(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, int64_t c, 
     if (i8) {
       cudaError_t e = cudaStreamWaitEvent(st, ctx->ev_sjoin, 0);
       if (e != cudaSuccess) return ctx->cuda_fail(e, "int8 join");
-      if (launch_ozaki_prep_b(m, n, QR, r, r, kOzakiModuli, ozws, st))
+      if (launch_ozaki_prep_b(m, n, QR, r, r, ctx->xq_moduli, ozws, st))
         return ctx->fail(QCUR_E_CUDA, "int8 gemm: bad modulus count");
       ctx->mark("xq_residues");  // includes the wait for the residues of X (side stream)
-      if (launch_ozaki_multiply(m, n, r, Y, r, kOzakiModuli, ozws, st))
+      if (launch_ozaki_multiply(m, n, r, Y, r, ctx->xq_moduli, ozws, st))
         return ctx->fail(QCUR_E_CUDA, "int8 gemm: tensor map encode failed");
       CK_LAUNCH(ctx, "int8 gemm");
     } else if ((rc = xq_product(ctx, X, m, n, n, QR, r, Y, gws))) {
@@ -986,7 +988,7 @@ int qmcur_core(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, int64_t c, 
       const double* B1 = Y;
       double* C1 = M;
       const int64_t p1 = m, qa1 = c, qb1 = r, lda1 = c, ldb1 = r, ldc1 = r;
-      if (launch_ozaki_herm(&A1, &B1, &p1, &qa1, &qb1, &lda1, &ldb1, &C1, &ldc1, 1, kOzakiModuli, &ws2, st))
+      if (launch_ozaki_herm(&A1, &B1, &p1, &qa1, &qb1, &lda1, &ldb1, &C1, &ldc1, 1, ctx->herm_moduli, &ws2, st))
         return ctx->fail(QCUR_E_CUDA, "int8 Q_C^H Y: tensor map encode failed");
       CK_LAUNCH(ctx, "int8 Q_C^H Y");
     } else if ((rc = gemm(ctx, gargs(c, r, m, QC, c, 1, Y, r, 0, M, r), gws))) {
@@ -1128,6 +1130,8 @@ int qcur_create(int device, qcur_ctx** out) {
     return QCUR_E_CUDA;
   }
   cudaMemset(ctx->counters, 0, (size_t)2 * 65536 * sizeof(unsigned));
+  if (const char* xm = std::getenv("QCUR_XQ_MODULI")) ctx->xq_moduli = std::atoi(xm) == 14 ? 14 : 15;
+  if (const char* hm = std::getenv("QCUR_HERM_MODULI")) ctx->herm_moduli = std::atoi(hm) == 14 ? 14 : 15;
   if (const char* gm = std::getenv("QCUR_GEMM"))
     ctx->gemm_mode = std::strcmp(gm, "dmma") == 0 ? 1 : std::strcmp(gm, "int8") == 0 ? 2 : 0;
   int prio_lo = 0, prio_hi = 0;
