@@ -21,6 +21,8 @@
 // (C and R^H) run as two clusters of one launch.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -32,6 +34,7 @@ namespace {
 constexpr int kCl = 16;  // CTAs per cluster (non-portable size, supported on B200)
 constexpr int kThreads = 512;
 constexpr int kClusterQMax = 304;  // compact triangles + 3 column buffers within 227 KB of smem
+constexpr bool kCholTwoColumnDefault = false;  // two columns per cluster exchange (QCUR_CHOL_B2)
 
 __device__ __forceinline__ Quat ldQ(const double* p) { return *reinterpret_cast<const Quat*>(p); }
 __device__ __forceinline__ void stQ(double* p, const Quat& q) { *reinterpret_cast<Quat*>(p) = q; }
@@ -204,6 +207,212 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1) k_cho
   cluster_barrier();
 }
 
+// ---------------------------------------------------------------------------
+// Two columns per exchange.  The one-column kernel above pays one DSMEM round trip per column
+// (q sequential exchanges, ~1.8 us each at q = 200).  Here every CTA also keeps a replicated
+// first sub-diagonal sub[i] = G'(i+1, i) next to the replicated diagonal, so at block (j, j+1)
+// every CTA forms the 2 x 2 diagonal factor itself:
+//   l0 = sqrt(d_j),  L10 = G'(j+1, j) / l0,  l1 = sqrt(d_{j+1} - |L10|^2),
+// and its own rows' entries of BOTH columns:
+//   L_ij = G'(i, j) / l0,   L_i,j+1 = (G'(i, j+1) - L_ij conj(L10)) / l1     (i > j + 1),
+// which go out in one exchange: q/2 round trips.  After the exchange the block's rank-2 update
+// is applied (look-ahead columns j+2, j+3 first, with the replicated d and sub of rows j+2,
+// j+3, then the next block is sent, then the bulk), and the inverse columns take the two
+// elimination steps j and j+1 locally.  The arithmetic per element is the same as the
+// one-column kernel's (the rank-2 update is two rank-1 updates, in column order).
+// ---------------------------------------------------------------------------
+constexpr int kClusterQMax2 = 288;  // compact triangles + 3 two-column buffers + sub within 227 KB
+
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1) k_chol_inv_cluster2(CholProblems P) {
+  const int c = (int)cg::this_cluster().block_rank();
+  const CholJob pr = P.p[blockIdx.x / kCl];
+  const int q = (int)P.q;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int kWarps = kThreads / 32;
+  const int nown = (q - c + kCl - 1) / kCl;
+  extern __shared__ __align__(32) double sm[];
+  double* colbuf = sm;                           // [3][2][q] quaternions: the two columns of a block
+  double* sub = colbuf + 6 * (size_t)q * 4;      // [q] quaternions: replicated G'(i+1, i)
+  double* diag = sub + (size_t)q * 4;            // [q] replicated running diagonal
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(diag + q + (q & 1));
+  double* rows = reinterpret_cast<double*>(mbar + 4);
+  auto rowbase = [&](int s) -> size_t { return (size_t)s * (c + 1) + (size_t)8 * s * (s - 1); };
+  auto colbase = [&](int u) -> size_t { return (size_t)u * (q - c) - (size_t)8 * u * (u - 1); };
+  double* wcol = rows + rowbase(nown) * 4;
+  auto G_at = [&](int s, int k) -> double* { return rows + (rowbase(s) + k) * 4; };  // own row c + 16 s, col k
+
+  for (int s = 0; s < nown; ++s) {
+    const int i = c + kCl * s;
+    double* row = rows + rowbase(s) * 4;
+    for (int k = tid; k <= i; k += kThreads) stQ(row + (size_t)k * 4, ldQ(pr.G + ((size_t)i * q + k) * 4));
+    double* col = wcol + colbase(s) * 4;
+    for (int r = i + tid; r < q; r += kThreads) stQ(col + (size_t)(r - i) * 4, Quat{r == i ? 1.0 : 0.0, 0.0, 0.0, 0.0});
+  }
+  for (int i = tid; i < q; i += kThreads) {
+    diag[i] = pr.G[((size_t)i * q + i) * 4];
+    stQ(sub + (size_t)i * 4, i + 1 < q ? ldQ(pr.G + ((size_t)(i + 1) * q + i) * 4) : qzero());
+  }
+  if (tid == 0) {
+    for (int k = 0; k < 3; ++k) mbar_init(&mbar[k], kCl + 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  cluster_barrier();
+
+  // the 2 x 2 diagonal factor of block j (identical in every CTA); false on breakdown
+  auto diag_factor = [&](int j, double& inv0, Quat& L10, double& inv1) -> bool {
+    const double d0 = diag[j];
+    if (!(d0 > 0.0) || !isfinite(d0)) return false;
+    inv0 = 1.0 / sqrt(d0);
+    if (j + 1 < q) {
+      L10 = qscale(ldQ(sub + (size_t)j * 4), inv0);
+      const double d1 = diag[j + 1] - qnorm2(L10);
+      if (!(d1 > 0.0) || !isfinite(d1)) return false;
+      inv1 = 1.0 / sqrt(d1);
+    }
+    return true;
+  };
+  // send the own rows' entries of columns j, j+1 (rows i > j + 1) to every CTA; L10 (row j+1 of
+  // column j) every CTA writes itself
+  auto produce = [&](int j) -> bool {
+    double inv0 = 0.0, inv1 = 0.0;
+    Quat L10 = qzero();
+    if (!diag_factor(j, inv0, L10, inv1)) return false;
+    const int b = (j >> 1) % 3;
+    double* cb = colbuf + (size_t)b * 2 * q * 4;
+    const unsigned nsend = (unsigned)(q - 2 - j > 0 ? q - 2 - j : 0);
+    if (tid == 0) {
+      mbar_expect_tx(&mbar[b], 2u * 32u * nsend);
+      if (j + 1 < q) stQ(cb + (size_t)(j + 1) * 4, L10);  // column j, row j + 1 (local)
+    }
+    const uint32_t cb_u = smem_u32(cb), mb_u = smem_u32(&mbar[b]);
+    for (int t = tid; t < nown * kCl; t += kThreads) {
+      const int s = t / kCl, dst = t - s * kCl;
+      const int i = c + kCl * s;
+      if (i <= j + 1) continue;
+      const Quat lij = qscale(ldQ(G_at(s, j)), inv0);
+      const Quat lij1 = qscale(qsub(ldQ(G_at(s, j + 1)), qmul(lij, qconj(L10))), inv1);
+      st_async_quat(mapa(cb_u + 32u * (unsigned)i, dst), lij, mapa(mb_u, dst));
+      st_async_quat(mapa(cb_u + 32u * (unsigned)(q + i), dst), lij1, mapa(mb_u, dst));
+    }
+    if (tid < kCl) mbar_arrive_remote(mapa(mb_u, tid));
+    return true;
+  };
+
+  bool ok = produce(0);
+  for (int j = 0; ok && j < q; j += 2) {
+    const int b = (j >> 1) % 3;
+    const double* c0 = colbuf + (size_t)b * 2 * q * 4;  // column j of L
+    const double* c1 = c0 + (size_t)q * 4;               // column j+1 of L
+    const bool two = j + 1 < q;
+    mbar_wait(&mbar[b], (unsigned)(j / 6) & 1u);
+    double inv0 = 0.0, inv1 = 0.0;
+    Quat L10 = qzero();
+    diag_factor(j, inv0, L10, inv1);  // succeeded in produce (same replicated data)
+    // look-ahead: columns j+2, j+3 of the own rows and the replicated d / sub of rows j+2, j+3,
+    // then send block j+2 so its exchange overlaps this block's bulk update
+    if (j + 2 < q) {
+      const Quat a2 = ldQ(c0 + (size_t)(j + 2) * 4), b2 = two ? ldQ(c1 + (size_t)(j + 2) * 4) : qzero();
+      const bool has3 = j + 3 < q;
+      const Quat a3 = has3 ? ldQ(c0 + (size_t)(j + 3) * 4) : qzero(), b3 = has3 ? ldQ(c1 + (size_t)(j + 3) * 4) : qzero();
+      for (int s = tid; s < nown; s += kThreads) {
+        const int i = c + kCl * s;
+        if (i <= j + 1) continue;
+        const Quat lij = ldQ(c0 + (size_t)i * 4), lij1 = ldQ(c1 + (size_t)i * 4);
+        if (i > j + 2) {  // entry (i, j+2)
+          double* e = G_at(s, j + 2);
+          Quat v = qsub(ldQ(e), qmul(lij, qconj(a2)));
+          if (two) v = qsub(v, qmul(lij1, qconj(b2)));
+          stQ(e, v);
+        }
+        if (has3 && i > j + 3) {  // entry (i, j+3)
+          double* e = G_at(s, j + 3);
+          Quat v = qsub(ldQ(e), qmul(lij, qconj(a3)));
+          if (two) v = qsub(v, qmul(lij1, qconj(b3)));
+          stQ(e, v);
+        }
+      }
+      if (tid == 0) {
+        diag[j + 2] = diag[j + 2] - qnorm2(a2) - qnorm2(b2);
+        if (has3) {
+          diag[j + 3] = diag[j + 3] - qnorm2(a3) - qnorm2(b3);
+          Quat v = qsub(ldQ(sub + (size_t)(j + 2) * 4), qmul(a3, qconj(a2)));
+          if (two) v = qsub(v, qmul(b3, qconj(b2)));
+          stQ(sub + (size_t)(j + 2) * 4, v);
+        }
+      }
+      __syncthreads();
+      ok = produce(j + 2);
+    }
+    // bulk rank-2 update of the own rows, columns k >= j+4 (j+2, j+3 done above): one warp per row
+    for (int s = warp; s < nown; s += kWarps) {
+      const int i = c + kCl * s;
+      if (i <= j + 3) continue;
+      const Quat lij = ldQ(c0 + (size_t)i * 4), lij1 = two ? ldQ(c1 + (size_t)i * 4) : qzero();
+      double* row = rows + rowbase(s) * 4;
+      for (int k = j + 4 + lane; k <= i; k += 32) {
+        Quat v = qsub(ldQ(row + (size_t)k * 4), qmul(lij, qconj(ldQ(c0 + (size_t)k * 4))));
+        if (two) v = qsub(v, qmul(lij1, qconj(ldQ(c1 + (size_t)k * 4))));
+        stQ(row + (size_t)k * 4, v);
+      }
+    }
+    // inverse, own columns: elimination steps j and j+1
+    for (int u = warp; u < nown; u += kWarps) {
+      const int k = c + kCl * u;
+      if (k > j + 1 || (!two && k > j)) continue;
+      double* w = wcol + colbase(u) * 4 - (size_t)k * 4;  // w + i*4 addresses W_ik (i >= k)
+      if (k <= j) {
+        const Quat xjk = qscale(ldQ(w + (size_t)j * 4), inv0);
+        __syncwarp();
+        if (lane == 0) stQ(w + (size_t)j * 4, xjk);
+        for (int i = j + 1 + lane; i < q; i += 32) stQ(w + (size_t)i * 4, qsub(ldQ(w + (size_t)i * 4), qmul(ldQ(c0 + (size_t)i * 4), xjk)));
+        __syncwarp();
+      }
+      if (two) {
+        const Quat xj1 = qscale(ldQ(w + (size_t)(j + 1) * 4), inv1);
+        __syncwarp();
+        if (lane == 0) stQ(w + (size_t)(j + 1) * 4, xj1);
+        for (int i = j + 2 + lane; i < q; i += 32) stQ(w + (size_t)i * 4, qsub(ldQ(w + (size_t)i * 4), qmul(ldQ(c1 + (size_t)i * 4), xj1)));
+        __syncwarp();
+      }
+    }
+    // replicated diagonal and sub-diagonal of the rows below the look-ahead
+    for (int i = j + 4 + tid; i < q; i += kThreads) {
+      const Quat ai = ldQ(c0 + (size_t)i * 4), bi = two ? ldQ(c1 + (size_t)i * 4) : qzero();
+      diag[i] = diag[i] - qnorm2(ai) - qnorm2(bi);
+    }
+    for (int i = j + 3 + tid; i + 1 < q; i += kThreads) {  // sub[i] = G'(i+1, i)
+      const Quat ai = ldQ(c0 + (size_t)i * 4), ai1 = ldQ(c0 + (size_t)(i + 1) * 4);
+      Quat v = qsub(ldQ(sub + (size_t)i * 4), qmul(ai1, qconj(ai)));
+      if (two) v = qsub(v, qmul(ldQ(c1 + (size_t)(i + 1) * 4), qconj(ldQ(c1 + (size_t)i * 4))));
+      stQ(sub + (size_t)i * 4, v);
+    }
+    __syncthreads();
+  }
+  if (!ok) {
+    if (c == 0 && tid == 0) atomicOr(P.status, pr.fail_bit);
+    cluster_barrier();
+    return;
+  }
+  for (int u = 0; u < nown; ++u) {
+    const int k = c + kCl * u;
+    const double* w = wcol + colbase(u) * 4;
+    for (int i = tid; i < q; i += kThreads) stQ(pr.X + ((size_t)i * q + k) * 4, i >= k ? ldQ(w + (size_t)(i - k) * 4) : qzero());
+  }
+  cluster_barrier();
+}
+
+static size_t chol_cluster_smem2(int64_t q) {
+  size_t best = 0;
+  for (int c = 0; c < kCl; ++c) {
+    const int64_t nown = (q - c + kCl - 1) / kCl;
+    const int64_t rows = nown * (c + 1) + 8 * nown * (nown - 1);
+    const int64_t cols = nown * (q - c) - 8 * nown * (nown - 1);
+    const size_t b = (size_t)(6 * q * 4 + q * 4 + q + (q & 1) + 4 + 4 * (rows + cols)) * sizeof(double);
+    best = b > best ? b : best;
+  }
+  return best;
+}
+
 int chol_cluster_qmax() { return kClusterQMax; }
 
 // dynamic shared memory of the CTA with the largest triangles (rank 0)
@@ -229,6 +438,22 @@ void launch_chol_inv_cluster(const CholJob* jobs, int njobs, int64_t q, unsigned
   if (first_on_device(set)) {
     cudaFuncSetAttribute(k_chol_inv_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(k_chol_inv_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  }
+  static const int b2_env = [] {
+    const char* e = std::getenv("QCUR_CHOL_B2");
+    return e ? std::atoi(e) : -1;
+  }();
+  const bool two = (b2_env == 1 || (b2_env < 0 && kCholTwoColumnDefault)) && q <= kClusterQMax2 &&
+                   chol_cluster_smem2(q) <= 227 * 1024;
+  if (two) {
+    static std::atomic<unsigned> set2{0};
+    if (first_on_device(set2)) {
+      cudaFuncSetAttribute(k_chol_inv_cluster2, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(k_chol_inv_cluster2, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    }
+    ++::qcur::g_launches;
+    k_chol_inv_cluster2<<<kCl * njobs, kThreads, chol_cluster_smem2(q), st>>>(P);
+    return;
   }
   ++::qcur::g_launches;
   k_chol_inv_cluster<<<kCl * njobs, kThreads, smem, st>>>(P);

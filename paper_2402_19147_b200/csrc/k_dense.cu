@@ -134,6 +134,36 @@ __global__ void k_series_lh(const double* __restrict__ G2, const double* __restr
   if (bad) atomicOr(status, fail_bit);
 }
 
+// G2^{-1} by its series for the factor F = L1^{-H} G2^{-1} (round 2): from the lower triangle of the
+// Hermitian G2 = I + E, the full E and S = I - E (S later gains E E: S = I - E + E^2, accurate to
+// |E|^3 <= 1e-15 under the 1e-5 gate); raises fail_bit when max|E| > thresh (robust path).
+__global__ void k_series_inv_prep(const double* __restrict__ G2, int64_t q, double* __restrict__ E,
+                                  double* __restrict__ S, unsigned* status, unsigned fail_bit, double thresh) {
+  int bad = 0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < q * q; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / q, k = t - i * q;
+    Quat e = k <= i ? ldQ(G2 + t * 4) : qconj(ldQ(G2 + (k * q + i) * 4));
+    if (i == k) e = Quat{e.w - 1.0, 0.0, 0.0, 0.0};
+    if (k <= i) {
+      const double mx = fmax(fmax(fabs(e.w), fabs(e.x)), fmax(fabs(e.y), fabs(e.z)));
+      if (!(mx <= thresh)) bad = 1;
+    }
+    stQ(E + t * 4, e);
+    Quat sv = qscale(e, -1.0);
+    if (i == k) sv.w += 1.0;
+    stQ(S + t * 4, sv);
+  }
+  if (bad) atomicOr(status, fail_bit);
+}
+
+void launch_series_inv_prep(const double* G2, int64_t q, double* E, double* S, unsigned* status, unsigned fail_bit,
+                            double thresh, cudaStream_t st) {
+  int blocks = (int)((q * q + 255) / 256);
+  if (blocks > 592) blocks = 592;
+  ++::qcur::g_launches;
+  k_series_inv_prep<<<blocks, 256, 0, st>>>(G2, q, E, S, status, fail_bit, thresh);
+}
+
 // L2inv = I - M1 + P2 (P2 = M1 M1, lower triangular)
 __global__ void k_series_final(const double* __restrict__ M1, const double* __restrict__ P2, int64_t q,
                                double* __restrict__ L2inv) {

@@ -140,6 +140,9 @@ int chol_cluster_qmax();
 void launch_series_lh(const double* G2, const double* P, int64_t q, double* M, unsigned* status, unsigned fail_bit,
                       double thresh, cudaStream_t st);
 void launch_series_final(const double* M1, const double* P2, int64_t q, double* L2inv, cudaStream_t st);
+// E = G2 - I and S = I - E, both full (from G2's lower triangle); fail_bit when max|E| > thresh
+void launch_series_inv_prep(const double* G2, int64_t q, double* E, double* S, unsigned* status, unsigned fail_bit,
+                            double thresh, cudaStream_t st);
 void launch_chol_inv_cluster(const CholJob* jobs, int njobs, int64_t q, unsigned* status, cudaStream_t st);
 // robust path (runs only when `status & gate_bit`, otherwise returns immediately)
 void launch_householder_qr(double* Zcm, int64_t p, int64_t q, double* alpha, double* Qcm, double* T, int64_t ldt,

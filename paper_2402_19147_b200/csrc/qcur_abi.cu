@@ -665,6 +665,33 @@ int factor_multi(qcur_ctx* ctx, const FactorSpec* specs_in, int ns) {
              }))) {
     return rc;
   }
+  // second pass, round 2: Z = Q T with Q = Q1 L2^{-H}, T = L2^H L1^H and G2 = L2 L2^H, so
+  // pinv(Z) = T^{-1} Q^H = L1^{-H} L2^{-H} L2^{-1} Q1^H = (L1^{-H} G2^{-1}) Q1^H: the factor is
+  // F = L1^{-H} (I - E + E^2) with E = G2 - I ~ kappa^2 u (gate max|E| <= 1e-5, dropped term
+  // |E|^3 <= 1e-15), two small GEMMs instead of the series for L2^{-1}, T and T L2^{-1} (four).
+  // The kappa_F guard uses ||L1^{-1}||_F (= ||T^{-1}||_F up to 1 + |E|).
+  static const int series_env = [] {
+    const char* e = std::getenv("QCUR_SERIES_INV");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (series_env != 0) {
+    for (int k = 0; k < ns; ++k)
+      if (fast[k]) launch_series_inv_prep(B[k].G2, specs[k].q, B[k].Tcm, B[k].Vcm, status, specs[k].fail_bit, 1e-5, st);
+    CK_LAUNCH(ctx, "series prep");
+    if ((rc = gemm_each([&](int k) {  // S += E E  (S = I - E + E^2)
+           const int64_t q = specs[k].q;
+           return gargs(q, q, q, B[k].Tcm, q, 0, B[k].Tcm, q, 0, B[k].Vcm, q, 1.0, 1.0);
+         })))
+      return rc;
+    for (int k = 0; k < ns; ++k)
+      if (fast[k]) launch_kappa_check(B[k].G1, B[k].L1i, specs[k].q, ctx->kappa_limit, status, specs[k].fail_bit, st);
+    CK_LAUNCH(ctx, "kappa");
+    if ((rc = gemm_each([&](int k) {  // F = L1^{-H} S
+           const int64_t q = specs[k].q;
+           return gargs(q, q, q, B[k].L1i, q, 1, B[k].Vcm, q, 0, specs[k].out.F, q);
+         })))
+      return rc;
+  } else {
   // second pass: G2 = I + E with E ~ kappa^2 u; L2^{-1} by a second-order series
   // (no sequential Cholesky; blocks with max|E| > 1e-5 take the robust path)
   // M0 = lh(E) in b.L2, P = M0 M0^H in b.T, M1 in b.Tcm, P2 = M1 M1 in b.Vcm
@@ -704,6 +731,7 @@ int factor_multi(qcur_ctx* ctx, const FactorSpec* specs_in, int ns) {
          return gargs(q, q, q, B[k].T, q, 0, B[k].L2i, q, 0, specs[k].out.F, q);
        })))
     return rc;
+  }
   // robust path, gated on each fail_bit (no-op launches when the fast path held)
   for (int k = 0; k < ns; ++k) {
     const FactorSpec& f = specs[k];
