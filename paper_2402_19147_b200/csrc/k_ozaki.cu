@@ -319,6 +319,7 @@ __global__ void k_oz_bres(const double* __restrict__ B, int64_t Kq, int64_t Nq, 
 // ---------------------------------------------------------------------------
 // a unit is 256 rows (two M = 128 accumulators sharing every B tile) x BN <= 256 columns
 constexpr int OZ_BM = 256, OZ_BK = 128, OZ_STAGES = 3, OZ_THREADS = 320;
+constexpr int kOzCluster = 1;  // CTAs per cluster sharing the A tile by TMA multicast (QCUR_OZ_CLUSTER)
 constexpr int OZ_A_BYTES = OZ_BM * OZ_BK, OZ_B_SLOT = 256 * OZ_BK;
 constexpr int OZ_SMEM = 1024 + OZ_STAGES * (OZ_A_BYTES + OZ_B_SLOT) + 256;
 
@@ -339,17 +340,25 @@ struct OzGemm {
   double pinv[kOzMaxMod];
 };
 
-__device__ __forceinline__ int unit_coords(const OzGemm& P, int u, int& l, int& mb, int& nb) {
+// unit u of the launch -> (problem, modulus l, row block mb, column block nb).  With clusters of CL
+// CTAs a unit is a group of CL adjacent column blocks (this CTA's is nb = group * CL + rank).
+template <int CL>
+__device__ __forceinline__ int unit_coords(const OzGemm& P, int u, int& l, int& mb, int& nb, int crank) {
   const int k = u < P.pr[0].units ? 0 : 1;
   const OzProb& q = P.pr[k];
   u -= k ? P.pr[0].units : 0;
-  nb = u % q.nblocks;
-  const int t = u / q.nblocks;
+  const int ngroups = (q.nblocks + CL - 1) / CL;
+  nb = (u % ngroups) * CL + crank;
+  const int t = u / ngroups;
   mb = t % q.mblocks;
   l = t / q.mblocks;
   return k;
 }
 
+// CL = 2: the two CTAs of a cluster take the same (modulus, row block) and two adjacent column
+// blocks; each loads one 128-row half of the shared A tile and multicasts it to both, and loads
+// its own B tile; a stage is released by a multicast commit to both CTAs' "empty" barriers.
+template <int CL>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
     k_oz_gemm(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmB0,
               const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
@@ -366,10 +375,14 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int crank = CL > 1 ? (int)cluster_ctarank() : 0;
+  const int cid = CL > 1 ? (int)cluster_id_x() : (int)blockIdx.x;
+  const int ncl = CL > 1 ? (int)ncluster_x() : (int)gridDim.x;
+  constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1u);
   if (threadIdx.x == 0) {
     for (int s = 0; s < OZ_STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL);  // one commit from each CTA of the cluster
     }
     mbar_init(tfull, 1);
     mbar_init(tempty, 8);
@@ -382,7 +395,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CL > 1)
+    cluster_sync_all();  // every CTA's barriers initialised before any multicast reaches them
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
 
@@ -392,9 +408,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB0)) : "memory");
       int stage = 0;
       unsigned phase = 0;
-      for (int u = blockIdx.x; u < P.total; u += gridDim.x) {
+      for (int u = cid; u < P.total; u += ncl) {
         int l, mb, nb;
-        const int k = unit_coords(P, u, l, mb, nb);
+        const int k = unit_coords<CL>(P, u, l, mb, nb, crank);
         const OzProb& q = P.pr[k];
         const CUtensorMap* ta = k ? &tmA1 : &tmA0;
         const CUtensorMap* tb = k ? &tmB1 : &tmB0;
@@ -402,7 +418,15 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         for (int kb = 0; kb < q.kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1u);
           mbar_expect_tx(&full[stage], bytes);
-          tma_load_3d(sA + stage * OZ_A_BYTES, ta, kb * OZ_BK, mb * OZ_BM, l, &full[stage]);
+          // A tile = two 128-row boxes (with CL = 2: this CTA's half, multicast to both CTAs)
+          if constexpr (CL == 1) {
+            tma_load_3d(sA + stage * OZ_A_BYTES, ta, kb * OZ_BK, mb * OZ_BM, l, &full[stage]);
+            tma_load_3d(sA + stage * OZ_A_BYTES + OZ_A_BYTES / 2, ta, kb * OZ_BK, mb * OZ_BM + OZ_BM / 2, l,
+                        &full[stage]);
+          } else {
+            tma_load_3d_mc(sA + stage * OZ_A_BYTES + crank * (OZ_A_BYTES / 2), ta, kb * OZ_BK,
+                           mb * OZ_BM + crank * (OZ_BM / 2), l, &full[stage], kMask);
+          }
           tma_load_3d(sB + stage * OZ_B_SLOT, tb, kb * OZ_BK, nb * q.BN, l, &full[stage]);
           if (++stage == OZ_STAGES) {
             stage = 0;
@@ -418,9 +442,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     int stage = 0;
     unsigned phase = 0;
     int t = 0;
-    for (int u = blockIdx.x; u < P.total; u += gridDim.x, ++t) {
+    for (int u = cid; u < P.total; u += ncl, ++t) {
       int l, mb, nb;
-      const OzProb& q = P.pr[unit_coords(P, u, l, mb, nb)];
+      const OzProb& q = P.pr[unit_coords<CL>(P, u, l, mb, nb, crank)];
       mbar_wait(tempty, ((unsigned)t & 1u) ^ 1u);  // the epilogue has drained the previous unit
       tc_fence_after();
       for (int kb = 0; kb < q.kblocks; ++kb) {
@@ -435,7 +459,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
             mma_i8(tbase, ad + (uint64_t)(k * 2), bd, q.idesc, (kb | k) != 0);                          // rows 0..127
             mma_i8(tbase + 256, ad + (uint64_t)((128 * OZ_BK + k * 32) >> 4), bd, q.idesc, (kb | k) != 0);  // 128..255
           }
-          mma_commit(&empty[stage]);
+          if constexpr (CL == 1)
+            mma_commit(&empty[stage]);
+          else
+            mma_commit_mc(&empty[stage], kMask);  // the stage is free in both CTAs' rings
         }
         __syncwarp();
         if (++stage == OZ_STAGES) {
@@ -451,9 +478,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     const int quarter = warp & 3, half = (warp - 2) >> 2;
     const int rloc = half * 128 + quarter * 32 + lane;
     int t = 0;
-    for (int u = blockIdx.x; u < P.total; u += gridDim.x, ++t) {
+    for (int u = cid; u < P.total; u += ncl, ++t) {
       int l, mb, nb;
-      const OzProb& q = P.pr[unit_coords(P, u, l, mb, nb)];
+      const OzProb& q = P.pr[unit_coords<CL>(P, u, l, mb, nb, crank)];
       mbar_wait(tfull, (unsigned)t & 1u);
       tc_fence_after();
       if (P.exp) {
@@ -490,7 +517,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           }
           w[i >> 2] |= (uint32_t)r << (8 * (i & 3));
         }
-        if (row < q.m) {
+        if (row < q.m && nb < q.nblocks) {
           *reinterpret_cast<uint4*>(out + c0) = make_uint4(w[0], w[1], w[2], w[3]);
           if (c0 + 32 <= q.BN) *reinterpret_cast<uint4*>(out + c0 + 16) = make_uint4(w[4], w[5], w[6], w[7]);
         }
@@ -506,6 +533,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase) : "memory");
   }
+  // no CTA may leave while its peer can still multicast into its shared memory or barriers
+  if constexpr (CL > 1) cluster_sync_all();
 }
 
 // ---------------------------------------------------------------------------
@@ -919,6 +948,77 @@ OzHPlan oz_hplan(int64_t p, int64_t qa, int64_t qb, int L, bool same) {
   return h;
 }
 
+// The same residues, tiled (round 2): a CTA stages a 32-row x 32-column tile of Z through shared
+// memory, so the reads are whole 1 KB row segments (the per-thread column walk of k_oz_wres read one
+// 32-byte quaternion per row, 4 rows apart) and each thread then packs four rows of one column:
+// eight threads write a contiguous 32-byte run of each residue row.
+template <int L>
+__global__ void __launch_bounds__(256) k_oz_wres_tiled(const double* __restrict__ Z, int64_t p, int64_t q, int64_t ldz,
+                                                       const int* __restrict__ ex, uint8_t* __restrict__ res,
+                                                       int64_t pitch, int64_t plane) {
+  __shared__ double tile[32][33][4];  // [row][column (+1 pad)][component]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t i0 = (int64_t)blockIdx.x * 32, k00 = (int64_t)blockIdx.y * 32;
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr) {
+    const int r = warp + 8 * rr;
+    const int64_t k = k00 + r, i = i0 + lane;
+    const Quat z = (k < p && i < q) ? ldq_nc(Z + (k * ldz + i) * 4) : qzero();
+    tile[r][lane][0] = z.w;
+    tile[r][lane][1] = z.x;
+    tile[r][lane][2] = z.y;
+    tile[r][lane][3] = z.z;
+  }
+  __syncthreads();
+  const int il = tid >> 3, kq = tid & 7;
+  const int64_t i = i0 + il, k0 = k00 + 4 * kq;
+  if (i >= q || k0 >= pitch) return;
+  const int e = ex[i];
+  const double s1 = ldexp(1.0, e / 2), s2 = ldexp(1.0, e - e / 2);
+  const long long magic_bits = __double_as_longlong(kMagic);
+  const f32x2 mag = dup(kMagicF), nmag = dup(-kMagicF), lmag = dup(-8388608.0f);
+  f32x2 f[4][2][4];
+  unsigned low[4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    unsigned lb[4], lm[4][4];
+    float sg[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const double v = tile[4 * kq + h][il][a];
+      const long long iv = __double_as_longlong(v * s1 * s2 + kMagic) - magic_bits;  // rint(x 2^e)
+      lb[h] = (unsigned)iv;
+      const unsigned long long u = (unsigned long long)(iv < 0 ? -iv : iv);
+      sg[h] = iv < 0 ? -1.0f : 1.0f;
+      lm[h][0] = 0x4B000000u | ((unsigned)u & 0x1fffu);
+      lm[h][1] = 0x4B000000u | ((unsigned)(u >> 13) & 0x1fffu);
+      lm[h][2] = 0x4B000000u | ((unsigned)(u >> 26) & 0x1fffu);
+      lm[h][3] = 0x4B000000u | (unsigned)(u >> 39);
+    }
+    low[a] = __byte_perm(__byte_perm(lb[0], lb[1], 0x0040), __byte_perm(lb[2], lb[3], 0x0040), 0x5410);
+#pragma unroll
+    for (int hp = 0; hp < 2; ++hp) {
+      const f32x2 sgn = pk(sg[2 * hp], sg[2 * hp + 1]);
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        f[a][hp][t] = fmul2(fadd2(((f32x2)lm[2 * hp][t]) | ((f32x2)lm[2 * hp + 1][t] << 32), lmag), sgn);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) *reinterpret_cast<unsigned*>(res + (a * q + i) * pitch + k0) = low[a];  // p = 256
+#define OZ_WPLANE(l)                                                                                      \
+  if constexpr (l < L) {                                                                                  \
+    _Pragma("unroll") for (int a = 0; a < 4; ++a) {                                                       \
+      const unsigned w = pack_pairs(pair_residue<l>(f[a][0][0], f[a][0][1], f[a][0][2], f[a][0][3], mag, nmag), \
+                                    pair_residue<l>(f[a][1][0], f[a][1][1], f[a][1][2], f[a][1][3], mag, nmag)); \
+      *reinterpret_cast<unsigned*>(res + (l) * plane + (a * q + i) * pitch + k0) = w;                     \
+    }                                                                                                     \
+  }
+  OZ_WPLANE(1) OZ_WPLANE(2) OZ_WPLANE(3) OZ_WPLANE(4) OZ_WPLANE(5) OZ_WPLANE(6) OZ_WPLANE(7) OZ_WPLANE(8)
+  OZ_WPLANE(9) OZ_WPLANE(10) OZ_WPLANE(11) OZ_WPLANE(12) OZ_WPLANE(13) OZ_WPLANE(14) OZ_WPLANE(15)
+#undef OZ_WPLANE
+}
+
 // exponents (column maxima) and residues of the planes of Z (p x q) for the Hermitian products
 void oz_planes(const double* Z, int64_t p, int64_t q, int64_t ldz, int L, int bits, unsigned long long* cmax,
                int* ex, uint8_t* w, int64_t pitch, cudaStream_t st) {
@@ -930,6 +1030,18 @@ void oz_planes(const double* Z, int64_t p, int64_t q, int64_t ldz, int L, int bi
   k_oz_bexp<<<(unsigned)((q + 255) / 256), 256, 0, st>>>(cmax, q, bits, ex);
   const int64_t nthreads = q * (pitch / 4);
   ++::qcur::g_launches;
+  static const int tiled_env = [] {
+    const char* e = std::getenv("QCUR_WRES_TILED");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (tiled_env) {
+    const dim3 grid((unsigned)((q + 31) / 32), (unsigned)((pitch + 31) / 32));
+    if (L == 14)
+      k_oz_wres_tiled<14><<<grid, 256, 0, st>>>(Z, p, q, ldz, ex, w, pitch, 4 * q * pitch);
+    else
+      k_oz_wres_tiled<15><<<grid, 256, 0, st>>>(Z, p, q, ldz, ex, w, pitch, 4 * q * pitch);
+    return;
+  }
   if (L == 14)
     k_oz_wres<14><<<(unsigned)((nthreads + 255) / 256), 256, 0, st>>>(Z, p, q, ldz, ex, w, pitch, 4 * q * pitch);
   else
@@ -1054,7 +1166,7 @@ struct OzJob {
 bool oz_job(OzJob& j, const OzPlan& pl, int64_t m, const uint8_t* ares, int64_t arow_stride, const uint8_t* bres,
             int L, uint8_t* res) {
   // A planes are m rows of arow_stride bytes (Kpitch for X, 4 Kpitch for the rows 4j of E(A))
-  if (!oz_map_strided(&j.ta, ares, pl.K, m, arow_stride, arow_stride * m, L, OZ_BM) ||
+  if (!oz_map_strided(&j.ta, ares, pl.K, m, arow_stride, arow_stride * m, L, OZ_BM / 2) ||
       !oz_map(&j.tb, bres, pl.K, pl.N, pl.Kpitch, L, (int)pl.BN))
     return false;
   OzProb& q = j.pr;
@@ -1085,17 +1197,50 @@ void oz_launch_gemm(const OzJob* jobs, int nj, int L, cudaStream_t st) {
   }
   static std::atomic<unsigned> attr{0};
   if (first_on_device(attr)) {
-    cudaFuncSetAttribute(k_oz_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM);
+    cudaFuncSetAttribute(k_oz_gemm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM);
+    cudaFuncSetAttribute(k_oz_gemm<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM);
   }
   static const int exp_env = [] {
     const char* e = std::getenv("QCUR_OZ_EXP");
     return e ? std::atoi(e) : 0;
   }();
   P.exp = exp_env;
-  const int grid = P.total < oz_sms() ? P.total : oz_sms();
+  static const int cl_env = [] {
+    const char* e = std::getenv("QCUR_OZ_CLUSTER");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int CL = cl_env == 1 || cl_env == 2 ? cl_env : kOzCluster;
   const OzJob& j1 = nj > 1 ? jobs[1] : jobs[0];
   ++::qcur::g_launches;
-  k_oz_gemm<<<grid, OZ_THREADS, OZ_SMEM, st>>>(jobs[0].ta, jobs[0].tb, j1.ta, j1.tb, P);
+  if (CL == 1) {
+    const int grid = P.total < oz_sms() ? P.total : oz_sms();
+    k_oz_gemm<1><<<grid, OZ_THREADS, OZ_SMEM, st>>>(jobs[0].ta, jobs[0].tb, j1.ta, j1.tb, P);
+    return;
+  }
+  // clusters of two CTAs over pairs of column blocks: units count the pairs
+  for (int k = 0; k < 2; ++k) P.pr[k].units = L * P.pr[k].mblocks * ((P.pr[k].nblocks + 1) / 2);
+  P.total = P.pr[0].units + (nj > 1 ? P.pr[1].units : 0);
+  cudaLaunchConfig_t cfg{};
+  cfg.blockDim = dim3(OZ_THREADS);
+  cfg.dynamicSmemBytes = OZ_SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  static int max_active = 0;
+  if (!max_active) {
+    int nc = 0;
+    cfg.gridDim = dim3((unsigned)(oz_sms() / 2 * 2));
+    max_active = (cudaOccupancyMaxActiveClusters(&nc, k_oz_gemm<2>, &cfg) == cudaSuccess && nc > 0) ? nc : oz_sms() / 2;
+    (void)cudaGetLastError();
+  }
+  const int nclusters = P.total < max_active ? P.total : max_active;
+  cfg.gridDim = dim3((unsigned)(2 * nclusters));
+  cudaLaunchKernelEx(&cfg, k_oz_gemm<2>, jobs[0].ta, jobs[0].tb, j1.ta, j1.tb, P);
 }
 
 int oz_launch_crt(const uint8_t* res, int64_t m, const OzPlan& pl, const int* ex, const int* fx, double* Y,
