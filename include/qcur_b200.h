@@ -157,7 +157,7 @@ int qcur_approx(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int st
 /* Batched: `batch` independent m x n matrices x_devs[b] (device pointers, host array) through the
  * pipeline of qcur_approx, matrix b with PCG64 state states[4b..4b+3]; outputs packed per matrix
  * (col_idx batch x num_cols, c batch x m x num_cols, ..., err4 batch x 4).  Matrices run on `lanes`
- * (1..8; 0 = 4) internal lane contexts overlapping one another; fork/join on the context stream,
+ * (1..16; 0 = 4) internal lane contexts overlapping one another; fork/join on the context stream,
  * capturable into one CUDA graph.  The caller's shape: the per-matrix make_plan + qmcur loop of
  * the reference's scaling experiment (pkg/src/qcur/bench.py:346-351). */
 int qcur_approx_batched(qcur_ctx* ctx, int64_t batch, const double* const* x_devs, int64_t m, int64_t n, int strategy,

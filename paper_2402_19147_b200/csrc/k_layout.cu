@@ -85,7 +85,7 @@ __global__ void k_conj_transpose(const double* __restrict__ A, int64_t m, int64_
 
 // status words of a batch's lane contexts OR-ed into the caller's, then cleared
 struct StatusSrc {
-  unsigned* p[8];
+  unsigned* p[16];
   int n;
 };
 __global__ void k_status_or(unsigned* dst, StatusSrc src) {
@@ -101,7 +101,7 @@ __global__ void k_status_or(unsigned* dst, StatusSrc src) {
 
 void launch_status_or(unsigned* dst, unsigned* const* srcs, int n, cudaStream_t st) {
   StatusSrc s{};
-  s.n = n < 8 ? n : 8;
+  s.n = n < 16 ? n : 16;
   for (int k = 0; k < s.n; ++k) s.p[k] = srcs[k];
   ++::qcur::g_launches;
   k_status_or<<<1, 32, 0, st>>>(dst, s);

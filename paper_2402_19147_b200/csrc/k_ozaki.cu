@@ -948,77 +948,6 @@ OzHPlan oz_hplan(int64_t p, int64_t qa, int64_t qb, int L, bool same) {
   return h;
 }
 
-// The same residues, tiled (round 2): a CTA stages a 32-row x 32-column tile of Z through shared
-// memory, so the reads are whole 1 KB row segments (the per-thread column walk of k_oz_wres read one
-// 32-byte quaternion per row, 4 rows apart) and each thread then packs four rows of one column:
-// eight threads write a contiguous 32-byte run of each residue row.
-template <int L>
-__global__ void __launch_bounds__(256) k_oz_wres_tiled(const double* __restrict__ Z, int64_t p, int64_t q, int64_t ldz,
-                                                       const int* __restrict__ ex, uint8_t* __restrict__ res,
-                                                       int64_t pitch, int64_t plane) {
-  __shared__ double tile[32][33][4];  // [row][column (+1 pad)][component]
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t i0 = (int64_t)blockIdx.x * 32, k00 = (int64_t)blockIdx.y * 32;
-#pragma unroll
-  for (int rr = 0; rr < 4; ++rr) {
-    const int r = warp + 8 * rr;
-    const int64_t k = k00 + r, i = i0 + lane;
-    const Quat z = (k < p && i < q) ? ldq_nc(Z + (k * ldz + i) * 4) : qzero();
-    tile[r][lane][0] = z.w;
-    tile[r][lane][1] = z.x;
-    tile[r][lane][2] = z.y;
-    tile[r][lane][3] = z.z;
-  }
-  __syncthreads();
-  const int il = tid >> 3, kq = tid & 7;
-  const int64_t i = i0 + il, k0 = k00 + 4 * kq;
-  if (i >= q || k0 >= pitch) return;
-  const int e = ex[i];
-  const double s1 = ldexp(1.0, e / 2), s2 = ldexp(1.0, e - e / 2);
-  const long long magic_bits = __double_as_longlong(kMagic);
-  const f32x2 mag = dup(kMagicF), nmag = dup(-kMagicF), lmag = dup(-8388608.0f);
-  f32x2 f[4][2][4];
-  unsigned low[4];
-#pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    unsigned lb[4], lm[4][4];
-    float sg[4];
-#pragma unroll
-    for (int h = 0; h < 4; ++h) {
-      const double v = tile[4 * kq + h][il][a];
-      const long long iv = __double_as_longlong(v * s1 * s2 + kMagic) - magic_bits;  // rint(x 2^e)
-      lb[h] = (unsigned)iv;
-      const unsigned long long u = (unsigned long long)(iv < 0 ? -iv : iv);
-      sg[h] = iv < 0 ? -1.0f : 1.0f;
-      lm[h][0] = 0x4B000000u | ((unsigned)u & 0x1fffu);
-      lm[h][1] = 0x4B000000u | ((unsigned)(u >> 13) & 0x1fffu);
-      lm[h][2] = 0x4B000000u | ((unsigned)(u >> 26) & 0x1fffu);
-      lm[h][3] = 0x4B000000u | (unsigned)(u >> 39);
-    }
-    low[a] = __byte_perm(__byte_perm(lb[0], lb[1], 0x0040), __byte_perm(lb[2], lb[3], 0x0040), 0x5410);
-#pragma unroll
-    for (int hp = 0; hp < 2; ++hp) {
-      const f32x2 sgn = pk(sg[2 * hp], sg[2 * hp + 1]);
-#pragma unroll
-      for (int t = 0; t < 4; ++t)
-        f[a][hp][t] = fmul2(fadd2(((f32x2)lm[2 * hp][t]) | ((f32x2)lm[2 * hp + 1][t] << 32), lmag), sgn);
-    }
-  }
-#pragma unroll
-  for (int a = 0; a < 4; ++a) *reinterpret_cast<unsigned*>(res + (a * q + i) * pitch + k0) = low[a];  // p = 256
-#define OZ_WPLANE(l)                                                                                      \
-  if constexpr (l < L) {                                                                                  \
-    _Pragma("unroll") for (int a = 0; a < 4; ++a) {                                                       \
-      const unsigned w = pack_pairs(pair_residue<l>(f[a][0][0], f[a][0][1], f[a][0][2], f[a][0][3], mag, nmag), \
-                                    pair_residue<l>(f[a][1][0], f[a][1][1], f[a][1][2], f[a][1][3], mag, nmag)); \
-      *reinterpret_cast<unsigned*>(res + (l) * plane + (a * q + i) * pitch + k0) = w;                     \
-    }                                                                                                     \
-  }
-  OZ_WPLANE(1) OZ_WPLANE(2) OZ_WPLANE(3) OZ_WPLANE(4) OZ_WPLANE(5) OZ_WPLANE(6) OZ_WPLANE(7) OZ_WPLANE(8)
-  OZ_WPLANE(9) OZ_WPLANE(10) OZ_WPLANE(11) OZ_WPLANE(12) OZ_WPLANE(13) OZ_WPLANE(14) OZ_WPLANE(15)
-#undef OZ_WPLANE
-}
-
 // exponents (column maxima) and residues of the planes of Z (p x q) for the Hermitian products
 void oz_planes(const double* Z, int64_t p, int64_t q, int64_t ldz, int L, int bits, unsigned long long* cmax,
                int* ex, uint8_t* w, int64_t pitch, cudaStream_t st) {
@@ -1030,18 +959,6 @@ void oz_planes(const double* Z, int64_t p, int64_t q, int64_t ldz, int L, int bi
   k_oz_bexp<<<(unsigned)((q + 255) / 256), 256, 0, st>>>(cmax, q, bits, ex);
   const int64_t nthreads = q * (pitch / 4);
   ++::qcur::g_launches;
-  static const int tiled_env = [] {
-    const char* e = std::getenv("QCUR_WRES_TILED");
-    return e ? std::atoi(e) : 1;
-  }();
-  if (tiled_env) {
-    const dim3 grid((unsigned)((q + 31) / 32), (unsigned)((pitch + 31) / 32));
-    if (L == 14)
-      k_oz_wres_tiled<14><<<grid, 256, 0, st>>>(Z, p, q, ldz, ex, w, pitch, 4 * q * pitch);
-    else
-      k_oz_wres_tiled<15><<<grid, 256, 0, st>>>(Z, p, q, ldz, ex, w, pitch, 4 * q * pitch);
-    return;
-  }
   if (L == 14)
     k_oz_wres<14><<<(unsigned)((nthreads + 255) / 256), 256, 0, st>>>(Z, p, q, ldz, ex, w, pitch, 4 * q * pitch);
   else

@@ -1638,7 +1638,7 @@ int qcur_approx_batched(qcur_ctx* ctx, int64_t batch, const double* const* x_dev
   DeviceGuard device_guard_(ctx);
   if (batch < 1 || !x_devs || !states) return ctx->fail(QCUR_E_PARAMETER, "approx_batched: empty batch");
   if (lanes < 1) lanes = 4;
-  if (lanes > 8) lanes = 8;
+  if (lanes > 16) lanes = 16;
   if (lanes > batch) lanes = (int)batch;
   cudaError_t e = cudaSuccess;
   if (!ctx->ev_bfork) e = cudaEventCreateWithFlags(&ctx->ev_bfork, cudaEventDisableTiming);
@@ -1673,7 +1673,7 @@ int qcur_approx_batched(qcur_ctx* ctx, int64_t batch, const double* const* x_dev
                                C + b * m * c * 4, U + b * c * r * 4, R + b * r * n * 4, psnr_scale, core, err4 + 4 * b);
     if (rc) return ctx->fail(rc, "approx_batched: matrix %lld: %s", (long long)b, L->err.c_str());
   }
-  unsigned* st[8] = {};
+  unsigned* st[16] = {};
   for (int k = 0; k < lanes; ++k) {
     qcur_ctx* L = ctx->lanes[k];
     if ((e = cudaEventRecord(ctx->lane_ev[k], L->stream)) != cudaSuccess ||
