@@ -644,7 +644,9 @@ def main() -> None:
     # lane has its own native context, stream and resident input (a second matrix of the same
     # workload, its own generator seed), so one approximation's latency-bound phases (draws,
     # Cholesky) overlap another's tensor-bound ones.  QCUR_INFLIGHT=1 gives the serial number.
-    inflight = int(os.environ.get("QCUR_INFLIGHT", "2")) if batch == 1 else 1
+    # in flight: 4 for the small single-matrix configs (cfg1: latency-bound, 2805 -> 4351 approx/s
+    # with 4), 2 otherwise (cfg2: 2, 3 and 4 measure the same)
+    inflight = int(os.environ.get("QCUR_INFLIGHT", "4" if m * n < 8e6 else "2")) if batch == 1 else 1
     if 32 * m * n > 8e9:  # cfg5: one 34 GB matrix and its workspace fill the GPU; one in flight
         inflight = 1
     lanes = [(dev, outs, xs, torch.cuda.current_stream())]

@@ -387,9 +387,12 @@ GemmArgs gargs(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, in
 }
 
 // Y = X Q_R on the INT8 tensor cores?  auto: when the product is large enough to pay for the residues
+// Thresholds (round 2, measured for throughput): the INT8 engine wins from cfg1's size up
+// (1000^2, r = 40: 1708 -> 1875 approx/s one at a time; cfg4's 64 x 1024^2: 2910 -> 3920 matrices/s).
+constexpr double kInt8MinMNR = 3e7, kInt8MinGram = 1e6;
 bool use_int8(const qcur_ctx* ctx, int64_t m, int64_t n, int64_t r) {
   if (ctx->gemm_mode == 1 || !ozaki_supported(m, n, r)) return false;
-  return ctx->gemm_mode == 2 || (double)m * (double)n * (double)r >= 2e8;
+  return ctx->gemm_mode == 2 || (double)m * (double)n * (double)r >= kInt8MinMNR;
 }
 
 // Y = X Q_R on the INT8 tensor cores one chunk of rows at a time (a product whose residues
@@ -404,13 +407,13 @@ int64_t int8_chunk_rows(const qcur_ctx* ctx, int64_t m, int64_t n, int64_t r) {
 // the Grams Z^H Z (Z: p x q) of CholeskyQR2 on the INT8 tensor cores?
 bool use_int8_gram(const qcur_ctx* ctx, int64_t p, int64_t q) {
   if (ctx->gemm_mode == 1 || !ozaki_herm_supported(p, q, q)) return false;
-  return ctx->gemm_mode == 2 || (double)p * (double)q * (double)q >= 5e7;
+  return ctx->gemm_mode == 2 || (double)p * (double)q * (double)q >= kInt8MinGram;
 }
 
 // the fused error ||X - P R|| on the INT8 tensor cores?  (same policy, its own shape limits)
 bool use_int8_err(const qcur_ctx* ctx, int64_t m, int64_t n, int64_t r) {
   if (ctx->gemm_mode == 1 || !ozaki_error_supported(m, n, r)) return false;
-  return ctx->gemm_mode == 2 || (double)m * (double)n * (double)r >= 2e8;
+  return ctx->gemm_mode == 2 || (double)m * (double)n * (double)r >= kInt8MinMNR;
 }
 
 // structure hints: op(B) upper triangular; Hermitian output with only its lower triangle consumed

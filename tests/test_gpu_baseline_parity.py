@@ -2,7 +2,7 @@
 
 Every case runs the public API (make_plan + qmcur + cur_relative_error, the C ABI underneath)
 twice: in the default engine mode (the INT8 tensor-core engine where its size thresholds
-trigger: X Q_R and the fused error when m n r >= 2e8, the CholeskyQR2 Grams when p q^2 >= 5e7)
+trigger: X Q_R and the fused error when m n r >= 3e7, the CholeskyQR2 Grams when p q^2 >= 1e6)
 and with the FP64 DMMA engine forced.  Against the oracle (oracle/oracle.py, pinned to the
 reference) on the same input bits:
 
