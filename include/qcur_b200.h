@@ -262,6 +262,8 @@ int qcur_complex_adjoint(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t 
 int qcur_chol_inv(qcur_ctx* ctx, const double* g_dev, int64_t q, double* x_dev);
 /* second CholeskyQR pass: L2^{-1} of G2 = I + E by series */
 int qcur_series_l2inv(qcur_ctx* ctx, const double* g2_dev, int64_t q, double* l2inv_dev);
+/* S = I - E + E^2 ~ G2^{-1} with E = G2 - I (the second CholeskyQR pass: F = L1^{-H} S) */
+int qcur_series_inv(qcur_ctx* ctx, const double* g2_dev, int64_t q, double* s_dev);
 int qcur_kappa_check(qcur_ctx* ctx, const double* g1_dev, const double* f_dev, int64_t q);
 /* local factorisation of a tall block Z = src (zh=0) or src^H (zh=1): pinv(Z) = F Q^H */
 int qcur_factor(qcur_ctx* ctx, const double* src_dev, int zh, int64_t p, int64_t q, double* q_dev, double* f_dev);

@@ -48,7 +48,7 @@ EXPORTS = (
     "qcur_profile", "qcur_profile_read", "qcur_launch_count", "qcur_pairwise_host", "qcur_synth_image",
     "qcur_colsums_seq", "qcur_pairwise_sums", "qcur_vec_div", "qcur_gather_cols", "qcur_gather_rows",
     "qcur_qgemm_ex", "qcur_qgemm_int8", "qcur_qgemm_herm_int8", "qcur_set_gemm_mode", "qcur_qsvd_jacobi", "qcur_qsvd_jacobi_top", "qcur_chol_inv", "qcur_series_l2inv", "qcur_kappa_check", "qcur_factor",
-    "qcur_synth_lowrank_rows", "qcur_synth_normals", "qcur_xq", "qcur_complex_adjoint", "qcur_approx_batched", "qcur_colsums_seq_ex", "qcur_qmcur_ex", "qcur_qmcur_host",
+    "qcur_synth_lowrank_rows", "qcur_synth_normals", "qcur_xq", "qcur_complex_adjoint", "qcur_approx_batched", "qcur_colsums_seq_ex", "qcur_series_inv", "qcur_qmcur_ex", "qcur_qmcur_host",
     "qcur_project_observed", "qcur_complete_sweep", "qcur_cur_given", "qcur_qgemv",
     "qcur_upload_length", "qcur_status_async", "qcur_status_map",
 )
@@ -154,6 +154,7 @@ def load_library() -> ctypes.CDLL:
             "qcur_factor": (ctypes.c_int, [_c_dp, _c_dp, ctypes.c_int, _i64, _i64, _c_dp, _c_dp]),
             "qcur_synth_lowrank_rows": (ctypes.c_int, [_c_dp, _i64, _i64, _i64, ctypes.c_uint64, ctypes.c_double,
                                                        _i64, _i64, _c_dp]),
+            "qcur_series_inv": (ctypes.c_int, [_c_dp, _c_dp, _i64, _c_dp]),
             "qcur_colsums_seq_ex": (ctypes.c_int, [_c_dp, _c_dp, _i64, _i64, _i64, _c_dp, _c_dp, _c_dp, _i64]),
             "qcur_approx_batched": (ctypes.c_int, [_c_dp, _i64, ctypes.POINTER(ctypes.c_void_p), _i64, _i64,
                                                    ctypes.c_int, _u64p, _i64, _i64, _c_dp, _c_dp, _c_dp, _c_dp,

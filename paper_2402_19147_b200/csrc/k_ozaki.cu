@@ -445,6 +445,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     for (int u = cid; u < P.total; u += ncl, ++t) {
       int l, mb, nb;
       const OzProb& q = P.pr[unit_coords<CL>(P, u, l, mb, nb, crank)];
+      const bool second_half = (int64_t)mb * OZ_BM + OZ_BM / 2 < q.m;
       mbar_wait(tempty, ((unsigned)t & 1u) ^ 1u);  // the epilogue has drained the previous unit
       tc_fence_after();
       for (int kb = 0; kb < q.kblocks; ++kb) {
@@ -456,8 +457,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < OZ_BK / 32; ++k) {
             const uint64_t bd = bd0 + (uint64_t)(k * 2);  // +32 bytes along K
-            mma_i8(tbase, ad + (uint64_t)(k * 2), bd, q.idesc, (kb | k) != 0);                          // rows 0..127
-            mma_i8(tbase + 256, ad + (uint64_t)((128 * OZ_BK + k * 32) >> 4), bd, q.idesc, (kb | k) != 0);  // 128..255
+            mma_i8(tbase, ad + (uint64_t)(k * 2), bd, q.idesc, (kb | k) != 0);  // rows 0..127
+            // rows 128..255 only when the block has any (the 800-row outputs of the Hermitian
+            // products end 32 rows into their fourth block: its second half is all padding)
+            if (second_half)
+              mma_i8(tbase + 256, ad + (uint64_t)((128 * OZ_BK + k * 32) >> 4), bd, q.idesc, (kb | k) != 0);
           }
           if constexpr (CL == 1)
             mma_commit(&empty[stage]);
@@ -490,6 +494,12 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         continue;
       }
       const int64_t row = (int64_t)mb * OZ_BM + rloc;
+      if ((int64_t)mb * OZ_BM + half * (OZ_BM / 2) >= q.m) {  // an all-padding half (no MMA was issued)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty);
+        continue;
+      }
       const int p = P.p[l];
       const float pinvf = (float)P.pinv[l];
       uint8_t* out = q.res + l * q.res_plane + row * q.res_pitch + (int64_t)nb * q.BN;

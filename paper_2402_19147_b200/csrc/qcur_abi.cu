@@ -2105,6 +2105,20 @@ int qcur_series_l2inv(qcur_ctx* ctx, const double* G2, int64_t q, double* L2inv)
   return QCUR_OK;
 }
 
+// G2^{-1} ~ S = I - E + E^2, E = G2 - I (the second CholeskyQR pass of factor_multi: the factor is
+// F = L1^{-H} S); raises the fast-path failure bit when max|E| > 1e-5
+int qcur_series_inv(qcur_ctx* ctx, const double* G2, int64_t q, double* S) {
+  DeviceGuard device_guard_(ctx);
+  GemmArgs probe = gargs(q, q, q, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0);
+  int rc = ctx->reserve(qbytes(q, q) + qgemm_workspace_bytes(probe) + 8192);
+  if (rc) return rc;
+  double* E = ctx->take<double>((size_t)(q * q * 4));
+  double* gws = ctx->take<double>(qgemm_workspace_bytes(probe) / 8 + 16);
+  launch_series_inv_prep(G2, q, E, S, ctx->status_dev, ST_CHOL_FAIL_C, 1e-5, ctx->stream);
+  CK_LAUNCH(ctx, "series prep");
+  return gemm(ctx, gargs(q, q, q, E, q, 0, E, q, 0, S, q, 1.0, 1.0), gws);
+}
+
 int qcur_kappa_check(qcur_ctx* ctx, const double* G1, const double* F, int64_t q) {
   DeviceGuard device_guard_(ctx);
   launch_kappa_check(G1, F, q, ctx->kappa_limit, ctx->status_dev, ST_CHOL_FAIL_C, ctx->stream);

@@ -243,6 +243,12 @@ class GpuOps:
         self.dev.call("qcur_series_l2inv", G2.data_ptr(), q, out.data_ptr())
         return out
 
+    def series_inv(self, G2):
+        q = int(G2.shape[0])
+        out = self.dev.empty_q(q, q)
+        self.dev.call("qcur_series_inv", G2.data_ptr(), q, out.data_ptr())
+        return out
+
     def kappa(self, G1, F):
         self.dev.call("qcur_kappa_check", G1.data_ptr(), F.data_ptr(), int(G1.shape[0]))
 
@@ -342,13 +348,12 @@ def approx_rowsharded(ops, comm, xb, m: int, strategy: str, seed: int, c: int, r
     X1 = ops.chol_inv(G1)
     Q1 = ops.gemm(Cb, X1, opB=1, flags=1)
     G2 = comm.all_reduce_sum(ops.gemm(Q1, Q1, opA=1, flags=2))
-    L2i = ops.series(G2)
-    # (Q1, T^-1 L2^-1) as in the monolithic factor (qcur_abi.cu factor_multi): the tall
-    # product Q1 L2^-H is never formed
+    # as the monolithic factor (qcur_abi.cu factor_multi): pinv(C) = F Q1^H with
+    # F = L1^-H G2^-1 = L1^-H (I - E + E^2), E = G2 - I; the kappa guard on ||L1^-1||_F
     QC = Q1
-    Tinv = ops.gemm(X1, L2i, opA=1, opB=1, flags=1)
-    ops.kappa(G1, Tinv)
-    FC = ops.gemm(Tinv, L2i)
+    S = ops.series_inv(G2)
+    ops.kappa(G1, X1)
+    FC = ops.gemm(X1, S, opA=1)
     failed = ops.fast_failed()
     if comm.all_max(1 if failed else 0):  # robust path: factor the gathered C locally
         Cfull = comm.all_gather_cat(Cb)

@@ -142,6 +142,16 @@ class CpuOps:
         out = (out[0] + np.eye(q),) + out[1:]
         return stack(tuple(np.tril(x) for x in out))
 
+    def series_inv(self, G2):
+        g = planes(G2)
+        q = g[0].shape[0]
+        lo = tuple(np.tril(x) for x in g)  # Hermitian from the lower triangle
+        full = tuple(l + (np.tril(l, -1).T * (1 if k == 0 else -1)) for k, l in enumerate(lo))
+        e = (full[0] - np.eye(q),) + full[1:]
+        e2 = O.qmatmul(e, e)
+        s = tuple(-a + b for a, b in zip(e, e2))
+        return stack((s[0] + np.eye(q),) + s[1:])
+
     def kappa(self, G1, F):
         return None
 
