@@ -43,7 +43,13 @@ using namespace tc;
 // K = 64 bytes per stage (64-byte swizzle): TMA delivers 64-byte row segments, twice the rate of
 // 32-byte ones (tools/tma_probe.cu: 14.5 vs 9.2 TB/s), so the 21 x 2 MMAs of a stage are no longer
 // starved; two 78 KB stages fill shared memory
-constexpr int OE_BM = 128, OE_BN = 80, OE_BK = 64, OE_STAGES = 2, OE_DIG = 6;
+#ifndef QCUR_OE_BN  // build-time variants for A/B timing (tools: nvcc -DQCUR_OE_BN=64 -DQCUR_OE_STAGES=3)
+#define QCUR_OE_BN 80
+#endif
+#ifndef QCUR_OE_STAGES
+#define QCUR_OE_STAGES 2
+#endif
+constexpr int OE_BM = 128, OE_BN = QCUR_OE_BN, OE_BK = 64, OE_STAGES = QCUR_OE_STAGES, OE_DIG = 6;
 constexpr int OE_EPI_WARPS = 16, OE_THREADS = 64 + 32 * OE_EPI_WARPS;  // 4 epilogue warps per TMEM lane quarter
 constexpr int OE_A_BYTES = OE_DIG * OE_BM * OE_BK;  // 48 KB
 constexpr int OE_B_BYTES = OE_DIG * OE_BN * OE_BK;  // 30 KB
