@@ -32,7 +32,10 @@ namespace qcur {
 
 namespace {
 constexpr int kCl = 16;  // CTAs per cluster (non-portable size, supported on B200)
-constexpr int kThreads = 512;
+#ifndef QCUR_CHOL_THREADS  // build-time variant for A/B timing
+#define QCUR_CHOL_THREADS 512
+#endif
+constexpr int kThreads = QCUR_CHOL_THREADS;
 constexpr int kClusterQMax = 304;  // compact triangles + 3 column buffers within 227 KB of smem
 constexpr bool kCholTwoColumnDefault = false;  // two columns per cluster exchange (QCUR_CHOL_B2)
 

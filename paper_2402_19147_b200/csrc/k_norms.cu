@@ -111,8 +111,15 @@ __device__ __forceinline__ double chunk_eval(const double* __restrict__ vals, co
     double r = 0.0;
     const int body = ln - (ln & 7);
     if (active && ln >= 8) {
-      r = vals[off + q];
-      for (int i = 8; i < body; i += 8) r = __dadd_rn(r, vals[off + i + q]);
+      // a numpy leaf holds at most 128 values (PW_BLOCKSIZE), so this lane's <= 16 are loaded
+      // first (independent loads in flight) and then added in numpy's order
+      double buf[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) buf[t] = 8 * t < body ? vals[off + 8 * t + q] : 0.0;
+      r = buf[0];
+#pragma unroll
+      for (int t = 1; t < 16; ++t)
+        if (8 * t < body) r = __dadd_rn(r, buf[t]);
     }
     // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) in lane group order
     double t1 = __shfl_xor_sync(0xffffffffu, r, 1);
