@@ -1038,8 +1038,11 @@ bool ozaki_supported(int64_t m, int64_t n, int64_t r) {
   // int32 accumulation: the odd moduli have residues in [-127, 127], so 4n 127^2 < 2^31; for
   // p = 256 the accumulator may wrap, which leaves it exact mod 2^32 and hence mod 256.
   // Residues of X take 15 bytes per real of X (and E(B) 15 bytes per real of E(B)).
-  return m >= 1 && n >= 1 && r >= 1 && 4 * n <= 133140 &&
-         (double)oz_plan(m, n, r, kOzMaxModDefault).total <= 4e9;  // workspace cap (else the FP64 engine)
+  // workspace cap of the one-shot product (else row chunks or the FP64 engine); QCUR_OZ_ONESHOT_CAP
+  // lowers it for tests of the chunked path
+  const char* cap_env = std::getenv("QCUR_OZ_ONESHOT_CAP");
+  const double cap = cap_env ? std::atof(cap_env) : 4e9;
+  return m >= 1 && n >= 1 && r >= 1 && 4 * n <= 133140 && (double)oz_plan(m, n, r, kOzMaxModDefault).total <= cap;
 }
 
 // Phase 1 (depends on X only; may run on a side stream): row exponents and residues of X.

@@ -397,11 +397,15 @@ bool use_int8(const qcur_ctx* ctx, int64_t m, int64_t n, int64_t r) {
 
 // Y = X Q_R on the INT8 tensor cores one chunk of rows at a time (a product whose residues
 // exceed the one-shot workspace cap, e.g. cfg5's 32768^2 X: 64 GB of residue planes)?
-constexpr double kOzChunkCap = 24e9;  // bytes of INT8 workspace for the chunked product
+// bytes of INT8 workspace for the chunked product (QCUR_OZ_CHUNK_CAP lowers it for tests)
+double oz_chunk_cap() {
+  const char* e = std::getenv("QCUR_OZ_CHUNK_CAP");
+  return e ? std::atof(e) : 24e9;
+}
 int64_t int8_chunk_rows(const qcur_ctx* ctx, int64_t m, int64_t n, int64_t r) {
   if (ctx->gemm_mode == 1 || ozaki_supported(m, n, r)) return 0;
   if (!(ctx->gemm_mode == 2 || (double)m * (double)n * (double)r >= 2e8)) return 0;
-  return ozaki_chunk_rows(m, n, r, kOzChunkCap);
+  return ozaki_chunk_rows(m, n, r, oz_chunk_cap());
 }
 
 // the Grams Z^H Z (Z: p x q) of CholeskyQR2 on the INT8 tensor cores?
@@ -792,7 +796,7 @@ size_t qmcur_ws_bytes(int64_t m, int64_t n, int64_t c, int64_t r) {
     size_t a = qgemm_workspace_bytes(g1), d = qgemm_workspace_bytes(g2);
     b += (a > d ? a : d) + 4096;
     if (ozaki_supported(m, n, r)) b += ozaki_workspace_bytes(m, n, r, kOzakiModuli) + 4096;
-    else if (int64_t mc = ozaki_chunk_rows(m, n, r, kOzChunkCap)) b += ozaki_workspace_bytes(mc, n, r, kOzakiModuli) + 4096;
+    else if (int64_t mc = ozaki_chunk_rows(m, n, r, oz_chunk_cap())) b += ozaki_workspace_bytes(mc, n, r, kOzakiModuli) + 4096;
     if (ozaki_herm_supported(m, c, r)) b += ozaki_herm_workspace_bytes(m, c, r, 0) + 4096;  // Q_C^H Y
   } else {
     b += pinv_ws_bytes(m, c) + pinv_ws_bytes(r, n) + qbytes(c, m) + qbytes(n, r) + qbytes(m, r);
