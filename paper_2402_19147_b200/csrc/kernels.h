@@ -145,6 +145,11 @@ void launch_series_inv_prep(const double* G2, int64_t q, double* E, double* S, u
                             double thresh, cudaStream_t st);
 void launch_chol_inv_cluster(const CholJob* jobs, int njobs, int64_t q, unsigned* status, cudaStream_t st);
 // robust path (runs only when `status & gate_bit`, otherwise returns immediately)
+// robust factor on a 16-CTA cluster (k_robust.cu): one-sided Jacobi on Zcm (p x q, column-major, overwritten),
+// Q = W (row-major, ld ldq), F = V Sigma^+ (row-major, ld ldf); gated on `status & gate_bit`
+void launch_robust_jacobi(double* Zcm, int64_t p, int64_t q, double* Vcm, double* Q, int64_t ldq, double* F,
+                          int64_t ldf, double cutoff_scale, double cutoff_abs, const unsigned* status, unsigned gate_bit,
+                          cudaStream_t st);
 void launch_householder_qr(double* Zcm, int64_t p, int64_t q, double* alpha, double* Qcm, double* T, int64_t ldt,
                            const unsigned* status, unsigned gate_bit, cudaStream_t st);
 // cutoff = cutoff_abs if cutoff_abs >= 0 else cutoff_scale * sigma_max; Vcm needs q*q*4 + q doubles

@@ -746,11 +746,22 @@ int factor_multi(qcur_ctx* ctx, const FactorSpec* specs_in, int ns) {
     Bufs& b = B[k];
     if (!f.zh) launch_rowmajor_to_colmajor(f.src, p, q, q, b.Zcm, status, f.fail_bit, st);
     else launch_conj_copy(f.src, p * q, b.Zcm, status, f.fail_bit, st);
-    launch_householder_qr(b.Zcm, p, q, b.betas, b.Qcm, b.T, q, status, f.fail_bit, st);
-    launch_colmajor_to_rowmajor(b.Qcm, p, q, f.out.Q, q, status, f.fail_bit, 0, st);
-    launch_rowmajor_to_colmajor(b.T, q, q, q, b.Tcm, status, f.fail_bit, st);
-    launch_jacobi_pinv_factor(b.Tcm, b.Vcm, q, kEps * (double)(p > q ? p : q), f.cutoff_abs, f.out.F, q, status,
-                              f.fail_bit, st);
+    // round 2: one-sided Jacobi on Z itself on a 16-CTA cluster (the single-CTA Householder QR +
+    // Jacobi of the triangular factor took 340 ms per side at cfg2; QCUR_ROBUST_HH=1 restores it)
+    static const int hh_env = [] {
+      const char* e = std::getenv("QCUR_ROBUST_HH");
+      return e ? std::atoi(e) : 0;
+    }();
+    if (hh_env) {
+      launch_householder_qr(b.Zcm, p, q, b.betas, b.Qcm, b.T, q, status, f.fail_bit, st);
+      launch_colmajor_to_rowmajor(b.Qcm, p, q, f.out.Q, q, status, f.fail_bit, 0, st);
+      launch_rowmajor_to_colmajor(b.T, q, q, q, b.Tcm, status, f.fail_bit, st);
+      launch_jacobi_pinv_factor(b.Tcm, b.Vcm, q, kEps * (double)(p > q ? p : q), f.cutoff_abs, f.out.F, q, status,
+                                f.fail_bit, st);
+    } else {
+      launch_robust_jacobi(b.Zcm, p, q, b.Vcm, f.out.Q, q, f.out.F, q, kEps * (double)(p > q ? p : q), f.cutoff_abs,
+                           status, f.fail_bit, st);
+    }
     CK_LAUNCH(ctx, "robust factor");
   }
   return QCUR_OK;

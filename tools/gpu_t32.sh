@@ -1,0 +1,4 @@
+cd $GRAFT_REPO_ROOT
+TAG=${1:-t32}
+timeout 2400 python -m pytest tests -q -m gpu -p no:cacheprovider --durations=10 > gpurun_out/${TAG}_tests.log 2>&1
+echo "rc=$?" >> gpurun_out/${TAG}_tests.log
