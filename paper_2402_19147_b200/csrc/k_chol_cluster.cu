@@ -33,14 +33,26 @@ namespace qcur {
 namespace {
 constexpr int kCl = 16;  // CTAs per cluster (non-portable size, supported on B200)
 #ifndef QCUR_CHOL_THREADS  // build-time variant for A/B timing
-#define QCUR_CHOL_THREADS 512
+#define QCUR_CHOL_THREADS 256
 #endif
 constexpr int kThreads = QCUR_CHOL_THREADS;
 constexpr int kClusterQMax = 304;  // compact triangles + 3 column buffers within 227 KB of smem
-constexpr bool kCholTwoColumnDefault = false;  // two columns per cluster exchange (QCUR_CHOL_B2)
+constexpr bool kCholTwoColumnDefault = false;
+#ifndef QCUR_CHOL_BATCH  // entries per lane loaded before they are updated (V2 bulk)
+#define QCUR_CHOL_BATCH 2
+#endif
+constexpr int kCB = QCUR_CHOL_BATCH;  // two columns per cluster exchange (QCUR_CHOL_B2)
 
 __device__ __forceinline__ Quat ldQ(const double* p) { return *reinterpret_cast<const Quat*>(p); }
 __device__ __forceinline__ void stQ(double* p, const Quat& q) { *reinterpret_cast<Quat*>(p) = q; }
+
+#ifdef QCUR_CHOL_TRACE  // per-step phase clocks of CTA 0, thread 0 (tools/test_chol_cluster.cu)
+__device__ long long g_chol_trace[512][6];
+#define CHOL_T(j, k) \
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (j) < 512) g_chol_trace[j][k] = clock64();
+#else
+#define CHOL_T(j, k)
+#endif
 
 struct CholProblems {
   CholJob p[2];
@@ -87,6 +99,14 @@ __device__ __forceinline__ void st_async_quat(uint32_t remote, const Quat& v, ui
 }
 }  // namespace
 
+// V2: (a) the look-ahead column is formed and sent in one pass by the sending threads themselves
+// (no write-back to the Gram row, no barrier between them; the final pivot of the next step is kept
+// in a local array), (b) the bulk updates are spread over all warps as work items (own Cholesky rows,
+// own inverse columns), each lane loading its next kCB entries before updating them (the one-warp-per-
+// row loops stored and reloaded through possibly-aliasing shared-memory pointers, serialising every
+// iteration: measured 1.8k cycles per step at q = 200, tools/test_chol_cluster.cu with
+// QCUR_CHOL_TRACE).  Same operations on every element in the same order: bit-identical factors.
+template <bool V2>
 __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1) k_chol_inv_cluster(CholProblems P) {
   const int c = (int)cg::this_cluster().block_rank();
   const CholJob pr = P.p[blockIdx.x / kCl];
@@ -106,6 +126,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1) k_cho
   auto rowbase = [&](int s) -> size_t { return (size_t)s * (c + 1) + (size_t)8 * s * (s - 1); };
   auto colbase = [&](int u) -> size_t { return (size_t)u * (q - c) - (size_t)8 * u * (u - 1); };
   double* wcol = rows + rowbase(nown) * 4;
+  double* dfin = wcol + colbase(nown) * 4;  // [q] final pivots (V2, local)
   (void)nmax;
 
   for (int s = 0; s < nown; ++s) {
@@ -116,6 +137,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1) k_cho
     for (int r = i + tid; r < q; r += kThreads) stQ(col + (size_t)(r - i) * 4, Quat{r == i ? 1.0 : 0.0, 0.0, 0.0, 0.0});
   }
   for (int i = tid; i < q; i += kThreads) diag[i] = pr.G[((size_t)i * q + i) * 4];
+  if (V2 && tid == 0) dfin[0] = pr.G[0];
   if (tid == 0) {
     for (int k = 0; k < 3; ++k) mbar_init(&mbar[k], kCl + 1);  // 16 producer arrives + local expect_tx
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -146,55 +168,142 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1) k_cho
   for (int j = 0; ok && j < q; ++j) {
     const int b = j % 3;
     double* cb = colbuf + (size_t)b * q * 4;
+    CHOL_T(j, 0)
     mbar_wait(&mbar[b], (unsigned)(j / 3) & 1u);
-    const double inv = 1.0 / sqrt(diag[j]);
-    // look-ahead: finish column j+1 first and send it, so its transfer overlaps
-    // the bulk of this step's update
-    if (j + 1 < q) {
-      const Quat lj1 = ldQ(cb + (size_t)(j + 1) * 4);
-      for (int s = tid; s < nown; s += kThreads) {
+    CHOL_T(j, 1)
+    if constexpr (!V2) {
+      const double inv = 1.0 / sqrt(diag[j]);
+      // look-ahead: finish column j+1 first and send it, so its transfer overlaps
+      // the bulk of this step's update
+      if (j + 1 < q) {
+        const Quat lj1 = ldQ(cb + (size_t)(j + 1) * 4);
+        for (int s = tid; s < nown; s += kThreads) {
+          const int i = c + kCl * s;
+          if (i <= j + 1) continue;
+          double* e = rows + (rowbase(s) + j + 1) * 4;
+          stQ(e, qsub(ldQ(e), qmul(ldQ(cb + (size_t)i * 4), qconj(lj1))));
+        }
+        if (tid == 0) diag[j + 1] = diag[j + 1] - qnorm2(lj1);
+        __syncthreads();
+        CHOL_T(j, 2)
+        ok = produce(j + 1);
+      }
+      CHOL_T(j, 3)
+      // bulk Cholesky update (k = j+1 done above): one warp per own row
+      for (int s = warp; s < nown; s += kWarps) {
         const int i = c + kCl * s;
         if (i <= j + 1) continue;
-        double* e = rows + (rowbase(s) + j + 1) * 4;
-        stQ(e, qsub(ldQ(e), qmul(ldQ(cb + (size_t)i * 4), qconj(lj1))));
+        const Quat lij = ldQ(cb + (size_t)i * 4);
+        double* row = rows + rowbase(s) * 4;
+        int k = j + 2 + lane;
+        for (; k + 32 <= i; k += 64) {  // two independent updates in flight
+          const Quat a0 = ldQ(row + (size_t)k * 4), b0 = ldQ(cb + (size_t)k * 4);
+          const Quat a1 = ldQ(row + (size_t)(k + 32) * 4), b1 = ldQ(cb + (size_t)(k + 32) * 4);
+          stQ(row + (size_t)k * 4, qsub(a0, qmul(lij, qconj(b0))));
+          stQ(row + (size_t)(k + 32) * 4, qsub(a1, qmul(lij, qconj(b1))));
+        }
+        if (k <= i) stQ(row + (size_t)k * 4, qsub(ldQ(row + (size_t)k * 4), qmul(lij, qconj(ldQ(cb + (size_t)k * 4)))));
       }
-      if (tid == 0) diag[j + 1] = diag[j + 1] - qnorm2(lj1);
-      __syncthreads();
-      ok = produce(j + 1);
-    }
-    // bulk Cholesky update (k = j+1 done above): one warp per own row
-    for (int s = warp; s < nown; s += kWarps) {
-      const int i = c + kCl * s;
-      if (i <= j + 1) continue;
-      const Quat lij = ldQ(cb + (size_t)i * 4);
-      double* row = rows + rowbase(s) * 4;
-      int k = j + 2 + lane;
-      for (; k + 32 <= i; k += 64) {  // two independent updates in flight
-        const Quat a0 = ldQ(row + (size_t)k * 4), b0 = ldQ(cb + (size_t)k * 4);
-        const Quat a1 = ldQ(row + (size_t)(k + 32) * 4), b1 = ldQ(cb + (size_t)(k + 32) * 4);
-        stQ(row + (size_t)k * 4, qsub(a0, qmul(lij, qconj(b0))));
-        stQ(row + (size_t)(k + 32) * 4, qsub(a1, qmul(lij, qconj(b1))));
+      // inverse, own columns k <= j: X_jk = W_jk / l_jj;  W_ik -= L_ij X_jk (i > j)
+      for (int u = warp; u < nown; u += kWarps) {
+        const int k = c + kCl * u;
+        if (k > j) continue;
+        double* w = wcol + colbase(u) * 4 - (size_t)k * 4;  // w + i*4 addresses W_ik (i >= k)
+        const Quat xjk = qscale(ldQ(w + (size_t)j * 4), inv);
+        if (lane == 0) stQ(w + (size_t)j * 4, xjk);
+        int i = j + 1 + lane;
+        for (; i + 32 < q; i += 64) {
+          const Quat a0 = ldQ(w + (size_t)i * 4), b0 = ldQ(cb + (size_t)i * 4);
+          const Quat a1 = ldQ(w + (size_t)(i + 32) * 4), b1 = ldQ(cb + (size_t)(i + 32) * 4);
+          stQ(w + (size_t)i * 4, qsub(a0, qmul(b0, xjk)));
+          stQ(w + (size_t)(i + 32) * 4, qsub(a1, qmul(b1, xjk)));
+        }
+        if (i < q) stQ(w + (size_t)i * 4, qsub(ldQ(w + (size_t)i * 4), qmul(ldQ(cb + (size_t)i * 4), xjk)));
       }
-      if (k <= i) stQ(row + (size_t)k * 4, qsub(ldQ(row + (size_t)k * 4), qmul(lij, qconj(ldQ(cb + (size_t)k * 4)))));
-    }
-    // inverse, own columns k <= j: X_jk = W_jk / l_jj;  W_ik -= L_ij X_jk (i > j)
-    for (int u = warp; u < nown; u += kWarps) {
-      const int k = c + kCl * u;
-      if (k > j) continue;
-      double* w = wcol + colbase(u) * 4 - (size_t)k * 4;  // w + i*4 addresses W_ik (i >= k)
-      const Quat xjk = qscale(ldQ(w + (size_t)j * 4), inv);
-      if (lane == 0) stQ(w + (size_t)j * 4, xjk);
-      int i = j + 1 + lane;
-      for (; i + 32 < q; i += 64) {
-        const Quat a0 = ldQ(w + (size_t)i * 4), b0 = ldQ(cb + (size_t)i * 4);
-        const Quat a1 = ldQ(w + (size_t)(i + 32) * 4), b1 = ldQ(cb + (size_t)(i + 32) * 4);
-        stQ(w + (size_t)i * 4, qsub(a0, qmul(b0, xjk)));
-        stQ(w + (size_t)(i + 32) * 4, qsub(a1, qmul(b1, xjk)));
+    } else {
+      const double inv = 1.0 / sqrt(dfin[j]);
+      // look-ahead: the senders form column j+1 of their rows themselves and send it at once
+      if (j + 1 < q) {
+        const Quat lj1 = ldQ(cb + (size_t)(j + 1) * 4);
+        const double d1 = diag[j + 1] - qnorm2(lj1);
+        if (!(d1 > 0.0) || !isfinite(d1)) {
+          ok = false;  // every CTA alike (replicated diagonal)
+        } else {
+          const double inv1 = 1.0 / sqrt(d1);
+          const int b1 = (j + 1) % 3;
+          if (tid == 0) {
+            dfin[j + 1] = d1;
+            mbar_expect_tx(&mbar[b1], 32u * (unsigned)(q - 2 - j));
+          }
+          const uint32_t cb_u = smem_u32(colbuf + (size_t)b1 * q * 4), mb_u = smem_u32(&mbar[b1]);
+          for (int t = tid; t < nown * kCl; t += kThreads) {
+            const int s = t / kCl, dst = t - s * kCl;
+            const int i = c + kCl * s;
+            if (i <= j + 1) continue;
+            const Quat v = qsub(ldQ(rows + (rowbase(s) + j + 1) * 4), qmul(ldQ(cb + (size_t)i * 4), qconj(lj1)));
+            st_async_quat(mapa(cb_u + 32u * (unsigned)i, dst), qscale(v, inv1), mapa(mb_u, dst));
+          }
+          if (tid < kCl) mbar_arrive_remote(mapa(mb_u, tid));
+        }
       }
-      if (i < q) stQ(w + (size_t)i * 4, qsub(ldQ(w + (size_t)i * 4), qmul(ldQ(cb + (size_t)i * 4), xjk)));
+      CHOL_T(j, 2)
+      CHOL_T(j, 3)
+      // bulk: items = own Cholesky rows i > j+1 (entries k in [j+2, i]) and own inverse columns
+      // k <= j (entries i in [j+1, q)), one warp per item, kCB entries per lane loaded first
+      const int s0 = j + 1 < c ? 0 : (j + 1 - c) / kCl + 1;
+      const int nrow = nown > s0 ? nown - s0 : 0;
+      const int ncol = j < c ? 0 : ((j - c) / kCl + 1 < nown ? (j - c) / kCl + 1 : nown);
+      // the senders of the look-ahead column are the low warps: the bulk starts from the high ones
+      for (int it = kWarps - 1 - warp; it < nrow + ncol; it += kWarps) {
+        if (it < nrow) {
+          const int s = s0 + it, i = c + kCl * s;
+          const Quat lij = ldQ(cb + (size_t)i * 4);
+          double* row = rows + rowbase(s) * 4;
+          for (int k0 = j + 2; k0 <= i; k0 += 32 * kCB) {
+            Quat av[kCB], bv[kCB];
+#pragma unroll
+            for (int u = 0; u < kCB; ++u) {
+              const int k = k0 + lane + 32 * u;
+              if (k <= i) {
+                av[u] = ldQ(row + (size_t)k * 4);
+                bv[u] = ldQ(cb + (size_t)k * 4);
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < kCB; ++u) {
+              const int k = k0 + lane + 32 * u;
+              if (k <= i) stQ(row + (size_t)k * 4, qsub(av[u], qmul(lij, qconj(bv[u]))));
+            }
+          }
+        } else {
+          const int u0 = it - nrow, k = c + kCl * u0;
+          double* w = wcol + colbase(u0) * 4 - (size_t)k * 4;  // w + i*4 addresses W_ik (i >= k)
+          const Quat xjk = qscale(ldQ(w + (size_t)j * 4), inv);
+          __syncwarp();
+          if (lane == 0) stQ(w + (size_t)j * 4, xjk);
+          for (int i0 = j + 1; i0 < q; i0 += 32 * kCB) {
+            Quat av[kCB], bv[kCB];
+#pragma unroll
+            for (int u = 0; u < kCB; ++u) {
+              const int i = i0 + lane + 32 * u;
+              if (i < q) {
+                av[u] = ldQ(w + (size_t)i * 4);
+                bv[u] = ldQ(cb + (size_t)i * 4);
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < kCB; ++u) {
+              const int i = i0 + lane + 32 * u;
+              if (i < q) stQ(w + (size_t)i * 4, qsub(av[u], qmul(bv[u], xjk)));
+            }
+          }
+        }
+      }
     }
+    CHOL_T(j, 4)
     for (int i = j + 2 + tid; i < q; i += kThreads) diag[i] = diag[i] - qnorm2(ldQ(cb + (size_t)i * 4));
     __syncthreads();
+    CHOL_T(j, 5)
   }
   if (!ok) {  // identical in every CTA (replicated diagonal): no transfer is left in flight
     if (c == 0 && tid == 0) atomicOr(P.status, pr.fail_bit);
@@ -205,7 +314,11 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1) k_cho
   for (int u = 0; u < nown; ++u) {
     const int k = c + kCl * u;
     const double* w = wcol + colbase(u) * 4;
-    for (int i = tid; i < q; i += kThreads) stQ(pr.X + ((size_t)i * q + k) * 4, i >= k ? ldQ(w + (size_t)(i - k) * 4) : qzero());
+    for (int i = tid; i < q; i += kThreads) {
+      Quat v = qzero();
+      if (i >= k) v = ldQ(w + (size_t)(i - k) * 4);
+      stQ(pr.X + ((size_t)i * q + k) * 4, v);
+    }
   }
   cluster_barrier();
 }
@@ -418,6 +531,10 @@ static size_t chol_cluster_smem2(int64_t q) {
 
 int chol_cluster_qmax() { return kClusterQMax; }
 
+#ifdef QCUR_CHOL_TRACE
+void chol_trace_read(long long* out) { cudaMemcpyFromSymbol(out, g_chol_trace, sizeof(g_chol_trace)); }
+#endif
+
 // dynamic shared memory of the CTA with the largest triangles (rank 0)
 static size_t chol_cluster_smem(int64_t q) {
   size_t best = 0;
@@ -425,7 +542,7 @@ static size_t chol_cluster_smem(int64_t q) {
     const int64_t nown = (q - c + kCl - 1) / kCl;
     const int64_t rows = nown * (c + 1) + 8 * nown * (nown - 1);
     const int64_t cols = nown * (q - c) - 8 * nown * (nown - 1);
-    const size_t b = (size_t)(3 * q * 4 + q + (q & 1) + 4 + 4 * (rows + cols)) * sizeof(double);
+    const size_t b = (size_t)(3 * q * 4 + q + (q & 1) + 4 + 4 * (rows + cols) + q) * sizeof(double);  // + V2 pivots
     best = b > best ? b : best;
   }
   return best;
@@ -439,9 +556,15 @@ void launch_chol_inv_cluster(const CholJob* jobs, int njobs, int64_t q, unsigned
   const size_t smem = chol_cluster_smem(q);
   static std::atomic<unsigned> set{0};
   if (first_on_device(set)) {
-    cudaFuncSetAttribute(k_chol_inv_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(k_chol_inv_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_chol_inv_cluster<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k_chol_inv_cluster<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_chol_inv_cluster<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k_chol_inv_cluster<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   }
+  static const int v2_env = [] {
+    const char* e = std::getenv("QCUR_CHOL_V2");
+    return e ? std::atoi(e) : 1;
+  }();
   static const int b2_env = [] {
     const char* e = std::getenv("QCUR_CHOL_B2");
     return e ? std::atoi(e) : -1;
@@ -459,7 +582,10 @@ void launch_chol_inv_cluster(const CholJob* jobs, int njobs, int64_t q, unsigned
     return;
   }
   ++::qcur::g_launches;
-  k_chol_inv_cluster<<<kCl * njobs, kThreads, smem, st>>>(P);
+  if (v2_env)
+    k_chol_inv_cluster<true><<<kCl * njobs, kThreads, smem, st>>>(P);
+  else
+    k_chol_inv_cluster<false><<<kCl * njobs, kThreads, smem, st>>>(P);
 }
 
 }  // namespace qcur

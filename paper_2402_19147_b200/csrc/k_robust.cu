@@ -95,7 +95,10 @@ __device__ bool rotate_pair(double* A, int64_t p, double* V, int64_t q, int64_t 
   }
   __syncthreads();  // red is reused by the next pair
   const double gn = sqrt(qnorm2(g));
-  if (!(gn > 4.0 * DBL_EPSILON * sqrt(al) * sqrt(be)) || !(al > 0.0) || !(be > 0.0)) return false;
+  // rotation threshold: a few ulps of the pair's norms, growing like sqrt(p) with the rounding of the
+  // p-term inner product (a fixed 4 eps kept some pairs rotating on their own rounding noise)
+  const double tol = fmax(4.0, sqrt((double)p)) * DBL_EPSILON;
+  if (!(gn > tol * sqrt(al) * sqrt(be)) || !(al > 0.0) || !(be > 0.0)) return false;
   const Quat mu_bar = qconj(qscale(g, 1.0 / gn));
   const double zeta = (be - al) / (2.0 * gn);
   const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
@@ -219,14 +222,10 @@ void launch_rj(double* A, int64_t p, int64_t q, double* V, double* Q, int64_t ld
 void launch_robust_jacobi(double* Zcm, int64_t p, int64_t q, double* Vcm, double* Q, int64_t ldq, double* F,
                           int64_t ldf, double cutoff_scale, double cutoff_abs, const unsigned* status, unsigned gate_bit,
                           cudaStream_t st) {
-  if (p <= 1 * kRThreads)
+  // R = 1 keeps a thread's rows of the pair in registers; larger R spills at 1024 threads (64 registers), so
+  // taller blocks stream their rows twice (measured: cfg2 p = 4000 streaming 520 ms, R = 4 slower)
+  if (p <= kRThreads)
     launch_rj<1>(Zcm, p, q, Vcm, Q, ldq, F, ldf, cutoff_scale, cutoff_abs, status, gate_bit, st);
-  else if (p <= 2 * kRThreads)
-    launch_rj<2>(Zcm, p, q, Vcm, Q, ldq, F, ldf, cutoff_scale, cutoff_abs, status, gate_bit, st);
-  else if (p <= 4 * kRThreads)
-    launch_rj<4>(Zcm, p, q, Vcm, Q, ldq, F, ldf, cutoff_scale, cutoff_abs, status, gate_bit, st);
-  else if (p <= 8 * kRThreads)
-    launch_rj<8>(Zcm, p, q, Vcm, Q, ldq, F, ldf, cutoff_scale, cutoff_abs, status, gate_bit, st);
   else
     launch_rj<0>(Zcm, p, q, Vcm, Q, ldq, F, ldf, cutoff_scale, cutoff_abs, status, gate_bit, st);
 }

@@ -6,6 +6,9 @@
 #include "../paper_2402_19147_b200/csrc/common.cuh"
 #include "../paper_2402_19147_b200/csrc/kernels.h"
 unsigned long long qcur::g_launches = 0;
+#ifdef QCUR_CHOL_TRACE
+namespace qcur { void chol_trace_read(long long* out); }
+#endif
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at line %d\n", cudaGetErrorString(e), __LINE__); return 1; } } while (0)
 struct Q { double w, x, y, z; };
 static Q mul(Q a, Q b) { return {a.w*b.w-a.x*b.x-a.y*b.y-a.z*b.z, a.w*b.x+a.x*b.w+a.y*b.z-a.z*b.y, a.w*b.y-a.x*b.z+a.y*b.w+a.z*b.x, a.w*b.z+a.x*b.y-a.y*b.x+a.z*b.w}; }
@@ -37,6 +40,21 @@ int main() {
     double gn = 1.0;
     float ms; cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
     cudaEventRecord(a); for (int r = 0; r < 10; ++r) qcur::launch_chol_inv_cluster(jobs, 2, q, st, 0); cudaEventRecord(b); CK(cudaEventSynchronize(b)); cudaEventElapsedTime(&ms, a, b);
+#ifdef QCUR_CHOL_TRACE
+    {
+      long long tr[512][6];
+      qcur::chol_trace_read(&tr[0][0]);
+      double acc[6] = {0};
+      int steps = q - 1 < 511 ? q - 1 : 511;
+      for (int j = 1; j < steps; ++j) {
+        for (int k = 1; k < 6; ++k) acc[k] += (double)(tr[j][k] - tr[j][k - 1]);
+        acc[0] += (double)(tr[j + 1][0] - tr[j][5]);
+      }
+      printf("q=%d per-step cycles: wait %.0f lookahead %.0f produce %.0f bulk %.0f diag+sync %.0f loop %.0f  total/step %.0f\n", q,
+             acc[1] / steps, acc[2] / steps, acc[3] / steps, acc[4] / steps, acc[5] / steps, acc[0] / steps,
+             (double)(tr[steps][5] - tr[1][0]) / (steps - 1));
+    }
+#endif
     printf("q=%d status=%u |XGX^H-I|=%.2e upper(X)=%.2e  time(2 problems)=%.1f us\n", q, hs, e1/gn, e2, ms*100);
   }
   return 0;
