@@ -326,6 +326,11 @@ constexpr int OZ_SMEM = 1024 + OZ_STAGES * (OZ_A_BYTES + OZ_B_SLOT) + 256;
 struct OzProb {
   int64_t m, N;  // rows of the A operand; columns (reals) of the product
   int kblocks, mblocks, nblocks, BN, units;
+  // lower: a symmetric product (A = B, the plane Grams of CholeskyQR2): only the tiles meeting the
+  // lower triangle are computed (the CRT reads the mirror entry of the others).  tiles per modulus,
+  // of which the first `fulls` have both 128-row halves (the last row block's may be all-padding
+  // in its second half and costs half).
+  int lower, tiles, fulls;
   uint32_t idesc;
   uint8_t* res;
   int64_t res_pitch, res_plane;
@@ -334,16 +339,59 @@ struct OzProb {
 // up to two independent products in one launch (the SMs split by work units)
 struct OzGemm {
   int L, total;
+  int nfull;  // units of full cost (both problems), scheduled before the half-cost ones
   int exp;  // timing experiments only (QCUR_OZ_EXP=1: the epilogue releases TMEM without reading it)
   OzProb pr[2];
   int p[kOzMaxMod];
+  int bm[kOzMaxMod];  // floor(2^32 / p) for the Barrett reduction of the epilogue
   double pinv[kOzMaxMod];
 };
 
 // unit u of the launch -> (problem, modulus l, row block mb, column block nb).  With clusters of CL
 // CTAs a unit is a group of CL adjacent column blocks (this CTA's is nb = group * CL + rank).
+// tiles of row block mb (lower products: those meeting the lower triangle)
+__host__ __device__ __forceinline__ int oz_row_tiles(const OzProb& q, int mb) {
+  if (!q.lower) return q.nblocks;
+  const int t = (mb * OZ_BM + OZ_BM - 1) / q.BN + 1;
+  return t < q.nblocks ? t : q.nblocks;
+}
+
+// CL = 1: units sorted by cost (every full-cost unit of both problems first, then the half-cost
+// ones), within a class by modulus then tile (row block, column block) so that concurrently running
+// CTAs share A tiles in L2; round-robin over the CTAs then leaves at most one half unit of imbalance.
 template <int CL>
 __device__ __forceinline__ int unit_coords(const OzGemm& P, int u, int& l, int& mb, int& nb, int crank) {
+  if constexpr (CL == 1) {
+    const int L = P.L;
+    int k, tile;
+    if (u < P.nfull) {
+      const int f0 = L * P.pr[0].fulls;
+      k = u < f0 ? 0 : 1;
+      const int tl = u - (k ? f0 : 0), F = P.pr[k].fulls;
+      l = tl / F;
+      tile = tl - l * F;
+    } else {
+      const int v = u - P.nfull, h0 = L * (P.pr[0].tiles - P.pr[0].fulls);
+      k = v < h0 ? 0 : 1;
+      const int tl = v - (k ? h0 : 0), H = P.pr[k].tiles - P.pr[k].fulls;
+      l = tl / H;
+      tile = P.pr[k].fulls + (tl - l * H);
+    }
+    const OzProb& q = P.pr[k];
+    if (!q.lower) {
+      mb = tile / q.nblocks;
+      nb = tile - mb * q.nblocks;
+    } else {
+      mb = 0;
+      for (int c = oz_row_tiles(q, 0); tile >= c; c = oz_row_tiles(q, mb)) {
+        tile -= c;
+        ++mb;
+      }
+      nb = tile;
+    }
+    (void)crank;
+    return k;
+  }
   const int k = u < P.pr[0].units ? 0 : 1;
   const OzProb& q = P.pr[k];
   u -= k ? P.pr[0].units : 0;
@@ -501,35 +549,49 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         continue;
       }
       const int p = P.p[l];
-      const float pinvf = (float)P.pinv[l];
+      const int bm = P.bm[l];  // floor(2^32 / p)
       uint8_t* out = q.res + l * q.res_plane + row * q.res_pitch + (int64_t)nb * q.BN;
-      for (int c0 = 0; c0 < q.BN; c0 += 32) {
-        uint32_t v[32];
-        tmem_ld32(tbase + (uint32_t)(half * 256 + c0) + ((uint32_t)(quarter * 32) << 16), v);
+      const bool store = row < q.m && nb < q.nblocks;
+      // residues of 32 accumulator columns: p = 256 the low byte; odd p by Barrett reduction with
+      // the 32-bit high product (q = floor(z floor(2^32/p) / 2^32) is floor(z/p) or one off either
+      // way for |z| < 2^31, so r = z - q p needs one correction each way; integer pipes only)
+      auto emit = [&](const uint32_t(&v)[32], int c0) {
         uint32_t w[8];
 #pragma unroll
         for (int z = 0; z < 8; ++z) w[z] = 0;
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          const int z = (int)v[i];
-          int r;
+          uint32_t r;
           if (l == 0) {
-            r = z & 255;
+            r = v[i] & 255u;
           } else {
-            // quotient in FP32 (full-rate pipe): |z| < 2^31 and p >= 197 put the float quotient
-            // within 2 of the true one, so r = z - q p (exact in int32) needs at most two
-            // corrections either way
-            r = z - __float2int_rd(__int2float_rn(z) * pinvf) * p;
-            r += r < 0 ? p : 0;
-            r += r < 0 ? p : 0;
-            r -= r >= p ? p : 0;
-            r -= r >= p ? p : 0;
+            const int z = (int)v[i];
+            int rr = (int)(v[i] - (uint32_t)__mulhi(z, bm) * (uint32_t)p);
+            rr += rr < 0 ? p : 0;
+            rr -= rr >= p ? p : 0;
+            r = (uint32_t)rr;
           }
-          w[i >> 2] |= (uint32_t)r << (8 * (i & 3));
+          w[i >> 2] |= r << (8 * (i & 3));
         }
-        if (row < q.m && nb < q.nblocks) {
+        if (store) {
           *reinterpret_cast<uint4*>(out + c0) = make_uint4(w[0], w[1], w[2], w[3]);
           if (c0 + 32 <= q.BN) *reinterpret_cast<uint4*>(out + c0 + 16) = make_uint4(w[4], w[5], w[6], w[7]);
+        }
+      };
+      // TMEM loads one chunk ahead of the arithmetic (two register buffers)
+      const uint32_t taddr = tbase + (uint32_t)(half * 256) + ((uint32_t)(quarter * 32) << 16);
+      const int nch = (q.BN + 31) / 32;
+      uint32_t va[32], vb[32];
+      tmem_ld32_async(taddr, va);
+      tmem_wait_ld();
+      for (int ch = 0; ch < nch; ch += 2) {
+        if (ch + 1 < nch) tmem_ld32_async(taddr + (uint32_t)((ch + 1) * 32), vb);
+        emit(va, ch * 32);
+        tmem_wait_ld();
+        if (ch + 1 < nch) {
+          if (ch + 2 < nch) tmem_ld32_async(taddr + (uint32_t)((ch + 2) * 32), va);
+          emit(vb, (ch + 1) * 32);
+          tmem_wait_ld();
         }
       }
       tc_fence_before();
@@ -716,14 +778,14 @@ __device__ __forceinline__ __int128 crt_one(const uint8_t* rp, int64_t plane, co
   return Z;
 }
 
-// C[i][j] from the 16 plane products: conj(x) y = (x0y0 + x1y1 + x2y2 + x3y3) + (x0y1 - x1y0 - x2y3 + x3y2) i
+// C[i][j] from the 16 plane products (of the lower tiles only when lower_bn > 0): conj(x) y = (x0y0 + x1y1 + x2y2 + x3y3) + (x0y1 - x1y0 - x2y3 + x3y2) i
 //   + (x0y2 + x1y3 - x2y0 - x3y1) j + (x0y3 - x1y2 + x2y1 - x3y0) k.  One thread per component t
 // (four exact CRTs, combined in 128-bit integers).
 template <int L>
 __global__ void __launch_bounds__(256) k_oz_hcrt(const uint8_t* __restrict__ res, int64_t qa, int64_t qb,
                                                  int64_t pitch, int64_t plane, const int* __restrict__ exa,
                                                  const int* __restrict__ exb, const __grid_constant__ OzCrt c,
-                                                 double* __restrict__ C, int64_t ldc) {
+                                                 double* __restrict__ C, int64_t ldc, int lower_bn) {
   const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= qa * qb * 4) return;
   const int t = (int)(id & 3);
@@ -744,7 +806,15 @@ __global__ void __launch_bounds__(256) k_oz_hcrt(const uint8_t* __restrict__ res
         b = kTerm[tt][u][1];
         sgn = kTerm[tt][u][2];
       }
-    const __int128 z = crt_one<L>(res + (a * qa + i) * pitch + (b * qb + j), plane, c);
+    int64_t row = a * qa + i, col = b * qb + j;
+    // lower products (lower_bn = BN): a tile above the lower triangle was not computed; the plane
+    // Gram is symmetric, so its mirror entry holds the same residues
+    if (lower_bn && (col / lower_bn) * lower_bn > (row / OZ_BM) * OZ_BM + OZ_BM - 1) {
+      const int64_t t = row;
+      row = col;
+      col = t;
+    }
+    const __int128 z = crt_one<L>(res + row * pitch + col, plane, c);
     g = sgn > 0 ? g + z : g - z;
   }
   const int e = -(exa[i] + exb[j]);
@@ -1093,6 +1163,17 @@ struct OzJob {
   OzProb pr;
 };
 
+// a symmetric product (A = B): keep only the tiles meeting the lower triangle
+void oz_job_lower(OzJob& j, int L) {
+  OzProb& q = j.pr;
+  q.lower = 1;
+  q.tiles = 0;
+  for (int mb = 0; mb < q.mblocks; ++mb) q.tiles += oz_row_tiles(q, mb);
+  const bool last_half = !((int64_t)(q.mblocks - 1) * OZ_BM + OZ_BM / 2 < q.m);
+  q.fulls = last_half ? q.tiles - oz_row_tiles(q, q.mblocks - 1) : q.tiles;
+  q.units = L * q.tiles;
+}
+
 bool oz_job(OzJob& j, const OzPlan& pl, int64_t m, const uint8_t* ares, int64_t arow_stride, const uint8_t* bres,
             int L, uint8_t* res) {
   // A planes are m rows of arow_stride bytes (Kpitch for X, 4 Kpitch for the rows 4j of E(A))
@@ -1106,7 +1187,10 @@ bool oz_job(OzJob& j, const OzPlan& pl, int64_t m, const uint8_t* ares, int64_t 
   q.mblocks = (int)((m + OZ_BM - 1) / OZ_BM);
   q.nblocks = (int)pl.nblocks;
   q.BN = (int)pl.BN;
-  q.units = L * q.mblocks * q.nblocks;
+  q.lower = 0;
+  q.tiles = q.mblocks * q.nblocks;
+  q.fulls = (int64_t)(q.mblocks - 1) * OZ_BM + OZ_BM / 2 < m ? q.tiles : q.tiles - q.nblocks;
+  q.units = L * q.tiles;
   // kind::i8: D = s32 (bits 4-5 = 2), A/B signed (bits 7-9, 10-12 = 1), K-major, N>>3 at 17, M>>4 at 24 (M = 128)
   q.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(q.BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   q.res = res;
@@ -1121,8 +1205,10 @@ void oz_launch_gemm(const OzJob* jobs, int nj, int L, cudaStream_t st) {
   P.pr[0] = jobs[0].pr;
   P.pr[1] = nj > 1 ? jobs[1].pr : jobs[0].pr;
   P.total = jobs[0].pr.units + (nj > 1 ? jobs[1].pr.units : 0);
+  P.nfull = L * (jobs[0].pr.fulls + (nj > 1 ? jobs[1].pr.fulls : 0));
   for (int l = 0; l < L; ++l) {
     P.p[l] = kOzModuli[l];
+    P.bm[l] = (int)((1ull << 32) / (unsigned long long)kOzModuli[l]);  // < 2^31 for p >= 3 (p = 256 unused)
     P.pinv[l] = 1.0 / (double)kOzModuli[l];
   }
   static std::atomic<unsigned> attr{0};
@@ -1139,7 +1225,8 @@ void oz_launch_gemm(const OzJob* jobs, int nj, int L, cudaStream_t st) {
     const char* e = std::getenv("QCUR_OZ_CLUSTER");
     return e ? std::atoi(e) : 0;
   }();
-  const int CL = cl_env == 1 || cl_env == 2 ? cl_env : kOzCluster;
+  const bool any_lower = jobs[0].pr.lower || (nj > 1 && jobs[1].pr.lower);
+  const int CL = any_lower ? 1 : cl_env == 1 || cl_env == 2 ? cl_env : kOzCluster;
   const OzJob& j1 = nj > 1 ? jobs[1] : jobs[0];
   ++::qcur::g_launches;
   if (CL == 1) {
@@ -1220,6 +1307,10 @@ int launch_ozaki_herm(const double* const* A, const double* const* B, const int6
                       const int64_t* qb, const int64_t* lda, const int64_t* ldb, double* const* C,
                       const int64_t* ldc, int np, int L, void* const* workspace, cudaStream_t st) {
   if (L < 14 || L > 15 || np < 1 || np > 2) return 1;
+  static const int lower_env = [] {  // QCUR_OZ_LOWER=0: full plane Grams (A/B timing)
+    const char* e = std::getenv("QCUR_OZ_LOWER");
+    return e ? std::atoi(e) : 1;
+  }();
   OzJob jobs[2];
   OzHPlan hp[2];
   uint8_t* ws[2];
@@ -1238,6 +1329,7 @@ int launch_ozaki_herm(const double* const* A, const double* const* B, const int6
       oz_planes(B[k], p[k], qb[k], ldb[k], L, h.g.bits, reinterpret_cast<unsigned long long*>(ws[k] + h.off_cb), exb,
                 wb, h.g.Kpitch, st);
     if (!oz_job(jobs[k], h.g, 4 * qa[k], wa, h.g.Kpitch, wb, L, ws[k] + h.off_res)) return 2;
+    if (same && lower_env) oz_job_lower(jobs[k], L);
   }
   oz_launch_gemm(jobs, np, L, st);
   const OzCrt cc = oz_crt(L);
@@ -1249,12 +1341,13 @@ int launch_ozaki_herm(const double* const* A, const double* const* B, const int6
     const unsigned blocks = (unsigned)((4 * qa[k] * qb[k] + 255) / 256);
     const int64_t plane = 4 * qa[k] * h.g.Npitch;
     ++::qcur::g_launches;
+    const int lbn = jobs[k].pr.lower ? jobs[k].pr.BN : 0;
     if (L == 14)
       k_oz_hcrt<14><<<blocks, 256, 0, st>>>(ws[k] + h.off_res, qa[k], qb[k], h.g.Npitch, plane, exa, exb, cc, C[k],
-                                            ldc[k] * 4);
+                                            ldc[k] * 4, lbn);
     else
       k_oz_hcrt<15><<<blocks, 256, 0, st>>>(ws[k] + h.off_res, qa[k], qb[k], h.g.Npitch, plane, exa, exb, cc, C[k],
-                                            ldc[k] * 4);
+                                            ldc[k] * 4, lbn);
   }
   return 0;
 }
