@@ -318,7 +318,11 @@ __global__ void k_oz_bres(const double* __restrict__ B, int64_t Kq, int64_t Nq, 
 // tcgen05 int8 GEMM:  res[l][i][j] = (A_l[i,:] . B_l[j,:]) mod p_l  (bytes in [0, p_l))
 // ---------------------------------------------------------------------------
 // a unit is 256 rows (two M = 128 accumulators sharing every B tile) x BN <= 256 columns
-constexpr int OZ_BM = 256, OZ_BK = 128, OZ_STAGES = 3, OZ_THREADS = 320;
+#ifndef QCUR_OZ_EPI_WARPS  // epilogue warps: 8 (one per TMEM lane quarter and accumulator) or 16 (columns split)
+#define QCUR_OZ_EPI_WARPS 16
+#endif
+constexpr int OZ_EPI = QCUR_OZ_EPI_WARPS;
+constexpr int OZ_BM = 256, OZ_BK = 128, OZ_STAGES = 3, OZ_THREADS = 64 + 32 * OZ_EPI;
 constexpr int kOzCluster = 1;  // CTAs per cluster sharing the A tile by TMA multicast (QCUR_OZ_CLUSTER)
 constexpr int OZ_A_BYTES = OZ_BM * OZ_BK, OZ_B_SLOT = 256 * OZ_BK;
 constexpr int OZ_SMEM = 1024 + OZ_STAGES * (OZ_A_BYTES + OZ_B_SLOT) + 256;
@@ -433,7 +437,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       mbar_init(&empty[s], CL);  // one commit from each CTA of the cluster
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 8);
+    mbar_init(tempty, OZ_EPI);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -526,8 +530,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       __syncwarp();
     }
   } else {
-    // 8 epilogue warps: warp w drains TMEM lanes 32 (w % 4) .. +31 of accumulator (w - 2) / 4
-    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    // epilogue warps: warp w drains TMEM lanes 32 (w % 4) .. +31 of accumulator ((w - 2) / 4) % 2,
+    // with 16 warps the column chunks split in two parts ((w - 2) / 8)
+    const int quarter = warp & 3, half = ((warp - 2) >> 2) & 1, cpart = OZ_EPI == 16 ? (warp - 2) >> 3 : 0;
     const int rloc = half * 128 + quarter * 32 + lane;
     int t = 0;
     for (int u = cid; u < P.total; u += ncl, ++t) {
@@ -580,18 +585,21 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       };
       // TMEM loads one chunk ahead of the arithmetic (two register buffers)
       const uint32_t taddr = tbase + (uint32_t)(half * 256) + ((uint32_t)(quarter * 32) << 16);
-      const int nch = (q.BN + 31) / 32;
-      uint32_t va[32], vb[32];
-      tmem_ld32_async(taddr, va);
-      tmem_wait_ld();
-      for (int ch = 0; ch < nch; ch += 2) {
-        if (ch + 1 < nch) tmem_ld32_async(taddr + (uint32_t)((ch + 1) * 32), vb);
-        emit(va, ch * 32);
+      const int nall = (q.BN + 31) / 32, nfirst = OZ_EPI == 16 ? (nall + 1) / 2 : nall;
+      const int ch0 = cpart ? nfirst : 0, nch = cpart ? nall : nfirst;
+      if (ch0 < nch) {
+        uint32_t va[32], vb[32];
+        tmem_ld32_async(taddr + (uint32_t)(ch0 * 32), va);
         tmem_wait_ld();
-        if (ch + 1 < nch) {
-          if (ch + 2 < nch) tmem_ld32_async(taddr + (uint32_t)((ch + 2) * 32), va);
-          emit(vb, (ch + 1) * 32);
+        for (int ch = ch0; ch < nch; ch += 2) {
+          if (ch + 1 < nch) tmem_ld32_async(taddr + (uint32_t)((ch + 1) * 32), vb);
+          emit(va, ch * 32);
           tmem_wait_ld();
+          if (ch + 1 < nch) {
+            if (ch + 2 < nch) tmem_ld32_async(taddr + (uint32_t)((ch + 2) * 32), va);
+            emit(vb, (ch + 1) * 32);
+            tmem_wait_ld();
+          }
         }
       }
       tc_fence_before();
