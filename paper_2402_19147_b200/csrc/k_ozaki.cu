@@ -786,49 +786,112 @@ __device__ __forceinline__ __int128 crt_one(const uint8_t* rp, int64_t plane, co
   return Z;
 }
 
-// C[i][j] from the 16 plane products (of the lower tiles only when lower_bn > 0): conj(x) y = (x0y0 + x1y1 + x2y2 + x3y3) + (x0y1 - x1y0 - x2y3 + x3y2) i
-//   + (x0y2 + x1y3 - x2y0 - x3y1) j + (x0y3 - x1y2 + x2y1 - x3y0) k.  One thread per component t
-// (four exact CRTs, combined in 128-bit integers).
+// C[i][j] from the 16 plane products: conj(x) y = (x0y0 + x1y1 + x2y2 + x3y3) + (x0y1 - x1y0 - x2y3 + x3y2) i
+//   + (x0y2 + x1y3 - x2y0 - x3y1) j + (x0y3 - x1y2 + x2y1 - x3y0) k.
+// One CTA per 16 x 16 block of (i, j) and component t, a thread per output.  One thread TMA-loads,
+// for each of t's four plane products, the residue block of every modulus (a 3-D box, 32 columns from
+// the 16-byte aligned start: a TMA box must begin on a 16-byte boundary, tools/tma3d_probe.cu), and
+// for lower products (lower_bn = BN of the GEMM: the plane Grams of CholeskyQR2 computed only the
+// tiles meeting the lower triangle) also the mirror block; each thread then takes its element from
+// the direct block, or from the mirror when its tile was not computed, forms the signed residue sum
+// and accumulates one CRT (CRT is linear, and the exact integer sum obeys |sum| <= 4 p 2^(2 bits)
+// < M / 2).
+constexpr int kHB = 16;  // output block edge
+
+__device__ __forceinline__ bool oz_tile_computed(int row, int col, int lower_bn) {  // 32-bit: cheap divisions
+  return !lower_bn || (unsigned)col / (unsigned)lower_bn * (unsigned)lower_bn <= ((unsigned)row & ~(unsigned)(OZ_BM - 1)) + OZ_BM - 1;
+}
+
+// a TMA box starts on a 16-byte column boundary: boxes are 32 columns wide from the aligned start
+constexpr int kHBW = 32;
+constexpr int kOzHcrtSmem = 8 * kOzMaxModDefault * kHB * kHBW + 64;  // [u | mirror u + 4][modulus][row][32]
+
 template <int L>
-__global__ void __launch_bounds__(256) k_oz_hcrt(const uint8_t* __restrict__ res, int64_t qa, int64_t qb,
-                                                 int64_t pitch, int64_t plane, const int* __restrict__ exa,
-                                                 const int* __restrict__ exb, const __grid_constant__ OzCrt c,
-                                                 double* __restrict__ C, int64_t ldc, int lower_bn) {
-  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (id >= qa * qb * 4) return;
-  const int t = (int)(id & 3);
-  const int64_t ij = id >> 2, i = ij / qb, j = ij - i * qb;
+__global__ void __launch_bounds__(kHB * kHB) k_oz_hcrt(const __grid_constant__ CUtensorMap tm, int64_t qa, int64_t qb,
+                                                       const int* __restrict__ exa, const int* __restrict__ exb,
+                                                       const __grid_constant__ OzCrt c, double* __restrict__ C,
+                                                       int64_t ldc, int lower_bn) {
+  extern __shared__ __align__(128) uint8_t hsm[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(hsm + 8 * L * kHB * kHBW);
+  auto blk = [&](int box, int l, int row, int col) -> uint8_t {
+    return hsm[((box * L + l) * kHB + row) * kHBW + col];
+  };
+  const int tx = threadIdx.x % kHB, ty = threadIdx.x / kHB;
+  const int t = (int)blockIdx.z;
+  const int i0 = (int)blockIdx.y * kHB, j0 = (int)blockIdx.x * kHB;
   // (a, b, sign) of the four plane products of component t
   constexpr int kTerm[4][4][3] = {{{0, 0, 1}, {1, 1, 1}, {2, 2, 1}, {3, 3, 1}},
                                   {{0, 1, 1}, {1, 0, -1}, {2, 3, -1}, {3, 2, 1}},
                                   {{0, 2, 1}, {1, 3, 1}, {2, 0, -1}, {3, 1, -1}},
                                   {{0, 3, 1}, {1, 2, -1}, {2, 1, 1}, {3, 0, -1}}};
-  __int128 g = 0;
+  const int iqa = (int)qa, iqb = (int)qb;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int nb = lower_bn ? 8 : 4;
+    mbar_expect_tx(bar, (unsigned)(nb * L * kHB * kHBW));
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int a = kTerm[t][u][0], b = kTerm[t][u][1];
+      const int xd = b * iqb + j0, xm = a * iqa + i0;  // first column of the direct / mirror block
+      tma_load_3d(hsm + u * L * kHB * kHBW, &tm, xd & ~15, a * iqa + i0, 0, bar);  // x = column, y = row
+      if (lower_bn) tma_load_3d(hsm + (4 + u) * L * kHB * kHBW, &tm, xm & ~15, b * iqb + j0, 0, bar);
+    }
+  }
+  const int i = i0 + ty, j = j0 + tx;
+  int sg[4], cd[4], cm[4];
+  bool dir[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
-    int a = 0, b = 0, sgn = 1;
-#pragma unroll
-    for (int tt = 0; tt < 4; ++tt)
-      if (tt == t) {
-        a = kTerm[tt][u][0];
-        b = kTerm[tt][u][1];
-        sgn = kTerm[tt][u][2];
-      }
-    int64_t row = a * qa + i, col = b * qb + j;
-    // lower products (lower_bn = BN): a tile above the lower triangle was not computed; the plane
-    // Gram is symmetric, so its mirror entry holds the same residues
-    if (lower_bn && (col / lower_bn) * lower_bn > (row / OZ_BM) * OZ_BM + OZ_BM - 1) {
-      const int64_t t = row;
-      row = col;
-      col = t;
-    }
-    const __int128 z = crt_one<L>(res + row * pitch + col, plane, c);
-    g = sgn > 0 ? g + z : g - z;
+    const int a = kTerm[t][u][0], b = kTerm[t][u][1];
+    sg[u] = kTerm[t][u][2];
+    dir[u] = oz_tile_computed(a * iqa + i, b * iqb + j, lower_bn);
+    cd[u] = ((b * iqb + j0) & 15) + tx;  // column of the element in the direct block (row ty)
+    cm[u] = ((a * iqa + i0) & 15) + ty;  // column of the element in the mirror block (row tx)
   }
+  mbar_wait(bar, 0);
+  unsigned long long col[4] = {};
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    int sum = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) sum += sg[u] * (int)(dir[u] ? blk(u, l, ty, cd[u]) : blk(4 + u, l, tx, cm[u]));
+    const float P = c.P[l], pinv = c.pinv[l];
+    // (sum mod p) w mod p, exact in FP32: |sum| < 1024, (sum mod p) w < 2^16
+    const float sf = (float)sum;
+    float sm = fmaf(-(fmaf(sf, pinv, kMagicF) - kMagicF), P, sf);
+    sm = sm < 0.0f ? sm + P : sm;
+    sm = sm >= P ? sm - P : sm;
+    const float rw = sm * c.w[l];
+    float tq = fmaf(-(fmaf(rw, pinv, kMagicF) - kMagicF), P, rw);
+    tq = tq < 0.0f ? tq + P : tq;
+    const unsigned tt = (unsigned)tq;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) col[k] += (unsigned long long)tt * c.mi[l][k];
+  }
+  if (i >= iqa || j >= iqb) return;
+  const unsigned __int128 M = ((unsigned __int128)c.M_hi << 64) | c.M_lo;
+  const unsigned long long w0 = col[0];
+  const unsigned long long c1 = col[1] + (w0 >> 32);
+  const unsigned long long c2 = col[2] + (c1 >> 32);
+  const unsigned long long c3 = col[3] + (c2 >> 32);
+  const unsigned long long lo = (w0 & 0xffffffffull) | (c1 << 32);
+  const unsigned long long hi = (c2 & 0xffffffffull) | (c3 << 32);
+  unsigned __int128 S = ((unsigned __int128)hi << 64) | lo;
+  long long q = (long long)floor(((double)hi * 18446744073709551616.0 + (double)lo) / c.Md);
+  q = q < 0 ? 0 : q;
+  S -= M * (unsigned long long)q;
+  if ((__int128)S < 0) S += M;
+  if (S >= M) S -= M;
+  __int128 Z = (__int128)S;
+  if (S > (M >> 1)) Z -= (__int128)M;
   const int e = -(exa[i] + exb[j]);
   const double s1 = ldexp(1.0, e / 2), s2 = ldexp(1.0, e - e / 2);
-  C[i * ldc + 4 * j + t] =
-      ((double)(long long)(g >> 64) * 18446744073709551616.0 + (double)(unsigned long long)g) * s1 * s2;
+  C[(int64_t)i * ldc + 4 * j + t] =
+      ((double)(long long)(Z >> 64) * 18446744073709551616.0 + (double)(unsigned long long)Z) * s1 * s2;
 }
 
 // ---------------------------------------------------------------------------
@@ -1014,7 +1077,9 @@ OzHPlan oz_hplan(int64_t p, int64_t qa, int64_t qb, int L, bool same) {
   g.Npitch = g.nblocks * g.BN;
   double log2M = 0.0;
   for (int l = 0; l < L; ++l) log2M += std::log2((double)kOzModuli[l]);
-  const int bits = (int)std::floor((log2M - 1.0 - std::log2((double)p) - 1e-6) / 2.0);  // |P_ab| <= p 2^(2 bits)
+  // |P_ab| <= p 2^(2 bits), and the signed sum of four of them (one quaternion component, recovered
+  // by a single CRT) stays below M / 2
+  const int bits = (int)std::floor((log2M - 3.0 - std::log2((double)p) - 1e-6) / 2.0);
   g.bits = bits > 51 ? 51 : bits;
   auto al = [](size_t v) { return (v + 255) / 256 * 256; };
   size_t o = 0;
@@ -1346,16 +1411,31 @@ int launch_ozaki_herm(const double* const* A, const double* const* B, const int6
     const bool same = A[k] == B[k] && qa[k] == qb[k] && lda[k] == ldb[k];
     const int* exa = reinterpret_cast<int*>(ws[k] + h.off_exa);
     const int* exb = same ? exa : reinterpret_cast<int*>(ws[k] + h.off_exb);
-    const unsigned blocks = (unsigned)((4 * qa[k] * qb[k] + 255) / 256);
-    const int64_t plane = 4 * qa[k] * h.g.Npitch;
-    ++::qcur::g_launches;
+    const dim3 grid((unsigned)((qb[k] + kHB - 1) / kHB), (unsigned)((qa[k] + kHB - 1) / kHB), 4);
     const int lbn = jobs[k].pr.lower ? jobs[k].pr.BN : 0;
+    // residue planes as a 3-D tensor: columns (Npitch bytes), rows (4 qa), moduli; 16 x 16 x L boxes
+    CUtensorMap tm;
+    {
+      auto enc = oz_encode();
+      cuuint64_t dims[3] = {(cuuint64_t)h.g.Npitch, (cuuint64_t)(4 * qa[k]), (cuuint64_t)L};
+      cuuint64_t strides[2] = {(cuuint64_t)h.g.Npitch, (cuuint64_t)(4 * qa[k] * h.g.Npitch)};
+      cuuint32_t box[3] = {(cuuint32_t)kHBW, (cuuint32_t)kHB, (cuuint32_t)L};
+      cuuint32_t estr[3] = {1, 1, 1};
+      if (!enc || enc(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, ws[k] + h.off_res, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return 2;
+    }
+    static std::atomic<unsigned> hattr{0};
+    if (first_on_device(hattr)) {
+      cudaFuncSetAttribute(k_oz_hcrt<14>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOzHcrtSmem);
+      cudaFuncSetAttribute(k_oz_hcrt<15>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOzHcrtSmem);
+    }
+    ++::qcur::g_launches;
     if (L == 14)
-      k_oz_hcrt<14><<<blocks, 256, 0, st>>>(ws[k] + h.off_res, qa[k], qb[k], h.g.Npitch, plane, exa, exb, cc, C[k],
-                                            ldc[k] * 4, lbn);
+      k_oz_hcrt<14><<<grid, kHB * kHB, kOzHcrtSmem, st>>>(tm, qa[k], qb[k], exa, exb, cc, C[k], ldc[k] * 4, lbn);
     else
-      k_oz_hcrt<15><<<blocks, 256, 0, st>>>(ws[k] + h.off_res, qa[k], qb[k], h.g.Npitch, plane, exa, exb, cc, C[k],
-                                            ldc[k] * 4, lbn);
+      k_oz_hcrt<15><<<grid, kHB * kHB, kOzHcrtSmem, st>>>(tm, qa[k], qb[k], exa, exb, cc, C[k], ldc[k] * 4, lbn);
   }
   return 0;
 }
