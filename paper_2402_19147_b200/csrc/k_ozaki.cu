@@ -31,6 +31,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 
@@ -692,15 +693,11 @@ __global__ void __launch_bounds__(256) k_oz_crt(const uint8_t* __restrict__ res,
 // GEMM of W_A (4qa x p) by W_B (4qb x p), both K-major stacks of the scaled planes.  No 4x
 // Hamilton expansion of either operand; the signed combination is exact (128-bit integers).
 // ---------------------------------------------------------------------------
+// the plane residues of rows k0..k0+3 of column i of Z (scaled by 2^e)
 template <int L>
-__global__ void __launch_bounds__(256) k_oz_wres(const double* __restrict__ Z, int64_t p, int64_t q, int64_t ldz,
-                                                 const int* __restrict__ ex, uint8_t* __restrict__ res,
-                                                 int64_t pitch, int64_t plane) {
-  const int64_t k4n = pitch / 4;
-  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (id >= q * k4n) return;
-  const int64_t i = id / k4n, k0 = 4 * (id - i * k4n);
-  const int e = ex[i];
+__device__ __forceinline__ void oz_wres_body(const double* __restrict__ Z, int64_t p, int64_t q, int64_t ldz, int e,
+                                             uint8_t* __restrict__ res, int64_t pitch, int64_t plane, int64_t i,
+                                             int64_t k0) {
   const double s1 = ldexp(1.0, e / 2), s2 = ldexp(1.0, e - e / 2);
   const long long magic_bits = __double_as_longlong(kMagic);
   const f32x2 mag = dup(kMagicF), nmag = dup(-kMagicF), lmag = dup(-8388608.0f);
@@ -754,6 +751,60 @@ __global__ void __launch_bounds__(256) k_oz_wres(const double* __restrict__ Z, i
   OZ_WPLANE(1) OZ_WPLANE(2) OZ_WPLANE(3) OZ_WPLANE(4) OZ_WPLANE(5) OZ_WPLANE(6) OZ_WPLANE(7) OZ_WPLANE(8)
   OZ_WPLANE(9) OZ_WPLANE(10) OZ_WPLANE(11) OZ_WPLANE(12) OZ_WPLANE(13) OZ_WPLANE(14) OZ_WPLANE(15)
 #undef OZ_WPLANE
+}
+
+// Up to four operands' plane residues in two launches (the Hermitian products of one factorization
+// step: C and R^H, or A and B): column maxima (k_oz_pmax, one atomicMax per column and slab), then
+// exponents and residues (k_oz_pres: the thread of row block 0 also stores the column's exponent).
+struct OzPlaneJob {
+  const double* Z;
+  int64_t p, q, ldz, rows_per, pitch, plane;
+  int slabs, bits;
+  unsigned long long* cmax;
+  int* ex;
+  uint8_t* w;
+};
+struct OzPlaneJobs {
+  OzPlaneJob j[4];
+};
+
+__global__ void k_oz_pmax(const __grid_constant__ OzPlaneJobs J) {
+  const OzPlaneJob& jb = J.j[blockIdx.z];
+  if ((int64_t)blockIdx.x * 32 >= jb.q || (int)blockIdx.y >= jb.slabs) return;
+  __shared__ double sh[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t j = (int64_t)blockIdx.x * 32 + lane;
+  const int64_t k0 = (int64_t)blockIdx.y * jb.rows_per, k1 = k0 + jb.rows_per < jb.p ? k0 + jb.rows_per : jb.p;
+  double mx = 0.0;
+  if (j < jb.q)
+    for (int64_t k = k0 + w; k < k1; k += 8) {
+      const Quat z = ldq_nc(jb.Z + (k * jb.ldz + j) * 4);
+      mx = fmax(mx, fmax(fmax(fabs(z.w), fabs(z.x)), fmax(fabs(z.y), fabs(z.z))));
+    }
+  sh[w][lane] = mx;
+  __syncthreads();
+  if (w == 0 && j < jb.q) {
+    for (int k = 1; k < 8; ++k) mx = fmax(mx, sh[k][lane]);
+    atomicMax(jb.cmax + j, (unsigned long long)__double_as_longlong(mx));
+  }
+}
+
+template <int L>
+__global__ void __launch_bounds__(256) k_oz_pres(const __grid_constant__ OzPlaneJobs J) {
+  const OzPlaneJob& jb = J.j[blockIdx.y];
+  const int64_t k4n = jb.pitch / 4;
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= jb.q * k4n) return;
+  const int64_t i = id / k4n, k0 = 4 * (id - i * k4n);
+  const double mx = __longlong_as_double((long long)jb.cmax[i]);
+  int e = 0;
+  if (mx > 0.0) {
+    int E;
+    frexp(mx, &E);
+    e = jb.bits - E;
+  }
+  if (k0 == 0) jb.ex[i] = e;
+  oz_wres_body<L>(jb.Z, jb.p, jb.q, jb.ldz, e, jb.w, jb.pitch, jb.plane, i, k0);
 }
 
 // one product value from its L residue bytes (stride `plane`), centred in (-M/2, M/2]
@@ -1102,20 +1153,41 @@ OzHPlan oz_hplan(int64_t p, int64_t qa, int64_t qb, int L, bool same) {
 }
 
 // exponents (column maxima) and residues of the planes of Z (p x q) for the Hermitian products
-void oz_planes(const double* Z, int64_t p, int64_t q, int64_t ldz, int L, int bits, unsigned long long* cmax,
-               int* ex, uint8_t* w, int64_t pitch, cudaStream_t st) {
-  cudaMemsetAsync(cmax, 0, (size_t)q * 8, st);
-  const int64_t slabs = (p + 63) / 64 < 64 ? (p + 63) / 64 : 64, rows_per = (p + slabs - 1) / slabs;
+OzPlaneJob oz_plane_job(const double* Z, int64_t p, int64_t q, int64_t ldz, int bits, unsigned long long* cmax,
+                        int* ex, uint8_t* w, int64_t pitch) {
+  OzPlaneJob j{};
+  j.Z = Z;
+  j.p = p;
+  j.q = q;
+  j.ldz = ldz;
+  j.slabs = (int)((p + 63) / 64 < 64 ? (p + 63) / 64 : 64);
+  j.rows_per = (p + j.slabs - 1) / j.slabs;
+  j.pitch = pitch;
+  j.plane = 4 * q * pitch;
+  j.bits = bits;
+  j.cmax = cmax;
+  j.ex = ex;
+  j.w = w;
+  return j;
+}
+
+void oz_planes_launch(const OzPlaneJob* jobs, int n, int L, cudaStream_t st) {
+  OzPlaneJobs J{};
+  unsigned cb = 1, sl = 1, rb = 1;
+  for (int k = 0; k < n; ++k) {
+    J.j[k] = jobs[k];
+    cudaMemsetAsync(jobs[k].cmax, 0, (size_t)jobs[k].q * 8, st);
+    cb = std::max(cb, (unsigned)((jobs[k].q + 31) / 32));
+    sl = std::max(sl, (unsigned)jobs[k].slabs);
+    rb = std::max(rb, (unsigned)((jobs[k].q * (jobs[k].pitch / 4) + 255) / 256));
+  }
   ++::qcur::g_launches;
-  k_oz_bmax<<<dim3((unsigned)((q + 31) / 32), (unsigned)slabs), 256, 0, st>>>(Z, p, q, ldz, rows_per, cmax);
-  ++::qcur::g_launches;
-  k_oz_bexp<<<(unsigned)((q + 255) / 256), 256, 0, st>>>(cmax, q, bits, ex);
-  const int64_t nthreads = q * (pitch / 4);
+  k_oz_pmax<<<dim3(cb, sl, (unsigned)n), 256, 0, st>>>(J);
   ++::qcur::g_launches;
   if (L == 14)
-    k_oz_wres<14><<<(unsigned)((nthreads + 255) / 256), 256, 0, st>>>(Z, p, q, ldz, ex, w, pitch, 4 * q * pitch);
+    k_oz_pres<14><<<dim3(rb, (unsigned)n), 256, 0, st>>>(J);
   else
-    k_oz_wres<15><<<(unsigned)((nthreads + 255) / 256), 256, 0, st>>>(Z, p, q, ldz, ex, w, pitch, 4 * q * pitch);
+    k_oz_pres<15><<<dim3(rb, (unsigned)n), 256, 0, st>>>(J);
 }
 
 }  // namespace
@@ -1387,6 +1459,8 @@ int launch_ozaki_herm(const double* const* A, const double* const* B, const int6
   OzJob jobs[2];
   OzHPlan hp[2];
   uint8_t* ws[2];
+  OzPlaneJob pj[4];
+  int npj = 0;
   for (int k = 0; k < np; ++k) {
     const bool same = A[k] == B[k] && qa[k] == qb[k] && lda[k] == ldb[k];
     hp[k] = oz_hplan(p[k], qa[k], qb[k], L, same);
@@ -1396,14 +1470,15 @@ int launch_ozaki_herm(const double* const* A, const double* const* B, const int6
     uint8_t* wb = same ? wa : ws[k] + h.off_wb;
     int* exa = reinterpret_cast<int*>(ws[k] + h.off_exa);
     int* exb = same ? exa : reinterpret_cast<int*>(ws[k] + h.off_exb);
-    oz_planes(A[k], p[k], qa[k], lda[k], L, h.g.bits, reinterpret_cast<unsigned long long*>(ws[k] + h.off_ca), exa,
-              wa, h.g.Kpitch, st);
+    pj[npj++] = oz_plane_job(A[k], p[k], qa[k], lda[k], h.g.bits,
+                             reinterpret_cast<unsigned long long*>(ws[k] + h.off_ca), exa, wa, h.g.Kpitch);
     if (!same)
-      oz_planes(B[k], p[k], qb[k], ldb[k], L, h.g.bits, reinterpret_cast<unsigned long long*>(ws[k] + h.off_cb), exb,
-                wb, h.g.Kpitch, st);
+      pj[npj++] = oz_plane_job(B[k], p[k], qb[k], ldb[k], h.g.bits,
+                               reinterpret_cast<unsigned long long*>(ws[k] + h.off_cb), exb, wb, h.g.Kpitch);
     if (!oz_job(jobs[k], h.g, 4 * qa[k], wa, h.g.Kpitch, wb, L, ws[k] + h.off_res)) return 2;
     if (same && lower_env) oz_job_lower(jobs[k], L);
   }
+  oz_planes_launch(pj, npj, L, st);
   oz_launch_gemm(jobs, np, L, st);
   const OzCrt cc = oz_crt(L);
   for (int k = 0; k < np; ++k) {

@@ -389,7 +389,14 @@ GemmArgs gargs(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, in
 // Y = X Q_R on the INT8 tensor cores?  auto: when the product is large enough to pay for the residues
 // Thresholds (round 2, measured for throughput): the INT8 engine wins from cfg1's size up
 // (1000^2, r = 40: 1708 -> 1875 approx/s one at a time; cfg4's 64 x 1024^2: 2910 -> 3920 matrices/s).
-constexpr double kInt8MinMNR = 3e7, kInt8MinGram = 1e6;
+constexpr double kInt8MinMNRDefault = 3e7, kInt8MinGramDefault = 1e6;
+// QCUR_INT8_MIN_MNR / QCUR_INT8_MIN_GRAM override the thresholds (A/B timing)
+double env_or(const char* name, double v) {
+  const char* e = std::getenv(name);
+  return e ? std::atof(e) : v;
+}
+const double kInt8MinMNR = env_or("QCUR_INT8_MIN_MNR", kInt8MinMNRDefault);
+const double kInt8MinGram = env_or("QCUR_INT8_MIN_GRAM", kInt8MinGramDefault);
 bool use_int8(const qcur_ctx* ctx, int64_t m, int64_t n, int64_t r) {
   if (ctx->gemm_mode == 1 || !ozaki_supported(m, n, r)) return false;
   return ctx->gemm_mode == 2 || (double)m * (double)n * (double)r >= kInt8MinMNR;
