@@ -147,6 +147,12 @@ void launch_chol_inv_cluster(const CholJob* jobs, int njobs, int64_t q, unsigned
 // robust path (runs only when `status & gate_bit`, otherwise returns immediately)
 // robust factor on a 16-CTA cluster (k_robust.cu): one-sided Jacobi on Zcm (p x q, column-major, overwritten),
 // Q = W (row-major, ld ldq), F = V Sigma^+ (row-major, ld ldf); gated on `status & gate_bit`
+// robust factorization by Householder QR + one-sided Jacobi pinv of the triangular factor, both on
+// 16-CTA clusters (k_robust.cu): Q (p x q row-major), F = T^+ (q x q row-major); gated on gate_bit
+bool robust_qr_supported(int64_t p, int64_t q);
+void launch_robust_qr_pinv(double* Zcm, int64_t p, int64_t q, double* betas, double* Ycm, double* Q, int64_t ldq,
+                           double* Tcm, double* Vcm, double* F, int64_t ldf, double cutoff_scale, double cutoff_abs,
+                           const unsigned* status, unsigned gate_bit, cudaStream_t st);
 void launch_robust_jacobi(double* Zcm, int64_t p, int64_t q, double* Vcm, double* Q, int64_t ldq, double* F,
                           int64_t ldf, double cutoff_scale, double cutoff_abs, const unsigned* status, unsigned gate_bit,
                           cudaStream_t st);

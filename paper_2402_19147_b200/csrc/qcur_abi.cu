@@ -753,21 +753,26 @@ int factor_multi(qcur_ctx* ctx, const FactorSpec* specs_in, int ns) {
     Bufs& b = B[k];
     if (!f.zh) launch_rowmajor_to_colmajor(f.src, p, q, q, b.Zcm, status, f.fail_bit, st);
     else launch_conj_copy(f.src, p * q, b.Zcm, status, f.fail_bit, st);
-    // round 2: one-sided Jacobi on Z itself on a 16-CTA cluster (the single-CTA Householder QR +
-    // Jacobi of the triangular factor took 340 ms per side at cfg2; QCUR_ROBUST_HH=1 restores it)
-    static const int hh_env = [] {
-      const char* e = std::getenv("QCUR_ROBUST_HH");
-      return e ? std::atoi(e) : 0;
+    // round 2: Householder QR and the one-sided Jacobi pinv of its triangular factor, each on a
+    // 16-CTA cluster (k_robust.cu).  QCUR_ROBUST=jacobi: one-sided Jacobi on Z itself (cluster);
+    // QCUR_ROBUST=hh: round 1's single-CTA Householder QR + Jacobi (340 ms per side at cfg2).
+    static const int mode_env = [] {
+      const char* e = std::getenv("QCUR_ROBUST");
+      if (!e) return 0;
+      return std::string(e) == "jacobi" ? 1 : std::string(e) == "hh" ? 2 : 0;
     }();
-    if (hh_env) {
+    const double cutoff_scale = kEps * (double)(p > q ? p : q);
+    if (mode_env == 2) {
       launch_householder_qr(b.Zcm, p, q, b.betas, b.Qcm, b.T, q, status, f.fail_bit, st);
       launch_colmajor_to_rowmajor(b.Qcm, p, q, f.out.Q, q, status, f.fail_bit, 0, st);
       launch_rowmajor_to_colmajor(b.T, q, q, q, b.Tcm, status, f.fail_bit, st);
-      launch_jacobi_pinv_factor(b.Tcm, b.Vcm, q, kEps * (double)(p > q ? p : q), f.cutoff_abs, f.out.F, q, status,
-                                f.fail_bit, st);
+      launch_jacobi_pinv_factor(b.Tcm, b.Vcm, q, cutoff_scale, f.cutoff_abs, f.out.F, q, status, f.fail_bit, st);
+    } else if (mode_env == 0 && robust_qr_supported(p, q)) {
+      launch_robust_qr_pinv(b.Zcm, p, q, b.betas, b.Qcm, f.out.Q, q, b.Tcm, b.Vcm, f.out.F, q, cutoff_scale,
+                            f.cutoff_abs, status, f.fail_bit, st);
     } else {
-      launch_robust_jacobi(b.Zcm, p, q, b.Vcm, f.out.Q, q, f.out.F, q, kEps * (double)(p > q ? p : q), f.cutoff_abs,
-                           status, f.fail_bit, st);
+      launch_robust_jacobi(b.Zcm, p, q, b.Vcm, f.out.Q, q, f.out.F, q, cutoff_scale, f.cutoff_abs, status, f.fail_bit,
+                           st);
     }
     CK_LAUNCH(ctx, "robust factor");
   }
