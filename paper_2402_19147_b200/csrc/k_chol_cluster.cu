@@ -165,10 +165,18 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1) k_cho
   };
 
   bool ok = produce(0);
+  double inv_cur = V2 ? 1.0 / sqrt(pr.G[0]) : 0.0;  // V2: 1 / l_jj of the current step (G[0] > 0 when ok)
   for (int j = 0; ok && j < q; ++j) {
     const int b = j % 3;
     double* cb = colbuf + (size_t)b * q * 4;
     CHOL_T(j, 0)
+    Quat pre = qzero();  // V2: this sender's Gram entry (own row, column j+1), final since the last bulk
+    if constexpr (V2) {
+      if (tid < nown * kCl && j + 1 < q) {
+        const int s = tid / kCl;
+        if (c + kCl * s > j + 1) pre = ldQ(rows + (rowbase(s) + j + 1) * 4);
+      }
+    }
     mbar_wait(&mbar[b], (unsigned)(j / 3) & 1u);
     CHOL_T(j, 1)
     if constexpr (!V2) {
@@ -221,7 +229,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1) k_cho
         if (i < q) stQ(w + (size_t)i * 4, qsub(ldQ(w + (size_t)i * 4), qmul(ldQ(cb + (size_t)i * 4), xjk)));
       }
     } else {
-      const double inv = 1.0 / sqrt(dfin[j]);
+      const double inv = inv_cur;
       // look-ahead: the senders form column j+1 of their rows themselves and send it at once
       if (j + 1 < q) {
         const Quat lj1 = ldQ(cb + (size_t)(j + 1) * 4);
@@ -230,6 +238,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1) k_cho
           ok = false;  // every CTA alike (replicated diagonal)
         } else {
           const double inv1 = 1.0 / sqrt(d1);
+          inv_cur = inv1;
           const int b1 = (j + 1) % 3;
           if (tid == 0) {
             dfin[j + 1] = d1;
@@ -240,7 +249,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1) k_cho
             const int s = t / kCl, dst = t - s * kCl;
             const int i = c + kCl * s;
             if (i <= j + 1) continue;
-            const Quat v = qsub(ldQ(rows + (rowbase(s) + j + 1) * 4), qmul(ldQ(cb + (size_t)i * 4), qconj(lj1)));
+            const Quat v = qsub(t == tid ? pre : ldQ(rows + (rowbase(s) + j + 1) * 4), qmul(ldQ(cb + (size_t)i * 4), qconj(lj1)));
             st_async_quat(mapa(cb_u + 32u * (unsigned)i, dst), qscale(v, inv1), mapa(mb_u, dst));
           }
           if (tid < kCl) mbar_arrive_remote(mapa(mb_u, tid));
@@ -459,36 +468,80 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1) k_cho
       __syncthreads();
       ok = produce(j + 2);
     }
-    // bulk rank-2 update of the own rows, columns k >= j+4 (j+2, j+3 done above): one warp per row
-    for (int s = warp; s < nown; s += kWarps) {
-      const int i = c + kCl * s;
-      if (i <= j + 3) continue;
-      const Quat lij = ldQ(c0 + (size_t)i * 4), lij1 = two ? ldQ(c1 + (size_t)i * 4) : qzero();
-      double* row = rows + rowbase(s) * 4;
-      for (int k = j + 4 + lane; k <= i; k += 32) {
-        Quat v = qsub(ldQ(row + (size_t)k * 4), qmul(lij, qconj(ldQ(c0 + (size_t)k * 4))));
-        if (two) v = qsub(v, qmul(lij1, qconj(ldQ(c1 + (size_t)k * 4))));
-        stQ(row + (size_t)k * 4, v);
-      }
-    }
-    // inverse, own columns: elimination steps j and j+1
-    for (int u = warp; u < nown; u += kWarps) {
-      const int k = c + kCl * u;
-      if (k > j + 1 || (!two && k > j)) continue;
-      double* w = wcol + colbase(u) * 4 - (size_t)k * 4;  // w + i*4 addresses W_ik (i >= k)
-      if (k <= j) {
-        const Quat xjk = qscale(ldQ(w + (size_t)j * 4), inv0);
-        __syncwarp();
-        if (lane == 0) stQ(w + (size_t)j * 4, xjk);
-        for (int i = j + 1 + lane; i < q; i += 32) stQ(w + (size_t)i * 4, qsub(ldQ(w + (size_t)i * 4), qmul(ldQ(c0 + (size_t)i * 4), xjk)));
-        __syncwarp();
-      }
-      if (two) {
-        const Quat xj1 = qscale(ldQ(w + (size_t)(j + 1) * 4), inv1);
-        __syncwarp();
-        if (lane == 0) stQ(w + (size_t)(j + 1) * 4, xj1);
-        for (int i = j + 2 + lane; i < q; i += 32) stQ(w + (size_t)i * 4, qsub(ldQ(w + (size_t)i * 4), qmul(ldQ(c1 + (size_t)i * 4), xj1)));
-        __syncwarp();
+    // bulk: items = own rows i > j+3 (rank-2 update of columns k in [j+4, i]) and own inverse columns
+    // k <= j+1 (elimination steps j and j+1 fused per entry, same operation order), one warp per item
+    // from the high warps down (the senders are the low ones), kCB entries per lane loaded first
+    {
+      const int s0 = j + 3 < c ? 0 : (j + 3 - c) / kCl + 1;
+      const int nrow = nown > s0 ? nown - s0 : 0;
+      const int kmax = two ? j + 1 : j;
+      const int ncol = kmax < c ? 0 : ((kmax - c) / kCl + 1 < nown ? (kmax - c) / kCl + 1 : nown);
+      for (int it = kWarps - 1 - warp; it < nrow + ncol; it += kWarps) {
+        if (it < nrow) {
+          const int sr = s0 + it, i = c + kCl * sr;
+          const Quat lij = ldQ(c0 + (size_t)i * 4), lij1 = two ? ldQ(c1 + (size_t)i * 4) : qzero();
+          double* row = rows + rowbase(sr) * 4;
+          for (int k0 = j + 4; k0 <= i; k0 += 32 * kCB) {
+            Quat av[kCB], bv[kCB], dv[kCB];
+#pragma unroll
+            for (int u = 0; u < kCB; ++u) {
+              const int k = k0 + lane + 32 * u;
+              if (k <= i) {
+                av[u] = ldQ(row + (size_t)k * 4);
+                bv[u] = ldQ(c0 + (size_t)k * 4);
+                dv[u] = two ? ldQ(c1 + (size_t)k * 4) : qzero();
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < kCB; ++u) {
+              const int k = k0 + lane + 32 * u;
+              if (k <= i) {
+                Quat v = qsub(av[u], qmul(lij, qconj(bv[u])));
+                if (two) v = qsub(v, qmul(lij1, qconj(dv[u])));
+                stQ(row + (size_t)k * 4, v);
+              }
+            }
+          }
+        } else {
+          const int u0 = it - nrow, k = c + kCl * u0;
+          double* w = wcol + colbase(u0) * 4 - (size_t)k * 4;  // w + i*4 addresses W_ik (i >= k)
+          const bool stepj = k <= j;
+          const Quat xjk = stepj ? qscale(ldQ(w + (size_t)j * 4), inv0) : qzero();
+          Quat xj1 = qzero();
+          if (two) {
+            Quat wj1 = ldQ(w + (size_t)(j + 1) * 4);
+            if (stepj) wj1 = qsub(wj1, qmul(ldQ(c0 + (size_t)(j + 1) * 4), xjk));
+            xj1 = qscale(wj1, inv1);
+          }
+          __syncwarp();
+          if (lane == 0) {
+            if (stepj) stQ(w + (size_t)j * 4, xjk);
+            if (two) stQ(w + (size_t)(j + 1) * 4, xj1);
+          }
+          for (int i0 = j + 2; i0 < q; i0 += 32 * kCB) {
+            Quat av[kCB], bv[kCB], dv[kCB];
+#pragma unroll
+            for (int u = 0; u < kCB; ++u) {
+              const int i = i0 + lane + 32 * u;
+              if (i < q) {
+                av[u] = ldQ(w + (size_t)i * 4);
+                bv[u] = ldQ(c0 + (size_t)i * 4);
+                dv[u] = two ? ldQ(c1 + (size_t)i * 4) : qzero();
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < kCB; ++u) {
+              const int i = i0 + lane + 32 * u;
+              if (i < q) {
+                Quat v = av[u];
+                if (stepj) v = qsub(v, qmul(bv[u], xjk));
+                if (two) v = qsub(v, qmul(dv[u], xj1));
+                stQ(w + (size_t)i * 4, v);
+              }
+            }
+          }
+          __syncwarp();
+        }
       }
     }
     // replicated diagonal and sub-diagonal of the rows below the look-ahead
