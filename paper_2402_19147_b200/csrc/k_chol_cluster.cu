@@ -85,6 +85,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mb, unsigned parity) {
         : "r"(a), "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* mb) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(mb)) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t remote_mb) {
   asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_mb) : "memory");
 }
@@ -588,6 +591,200 @@ int chol_cluster_qmax() { return kClusterQMax; }
 void chol_trace_read(long long* out) { cudaMemcpyFromSymbol(out, g_chol_trace, sizeof(g_chol_trace)); }
 #endif
 
+// ---------------------------------------------------------------------------
+// Pipelined variant (QCUR_CHOL_PIPE): warp-specialised.  Sender warps (S) run the critical chain:
+// wait for column j, form and send column j+1 of the own rows, then apply step j to column j+2
+// (entries and replicated pivot) once the bulk warps have finished step j-1.  Bulk warps (B) apply
+// step j to the columns k >= j+3 of the own rows and to the inverse, one step behind the senders, so
+// the exchange of column j+1 overlaps the bulk of step j instead of following it.  Four column
+// buffers: a peer can be at most two columns ahead of this CTA's bulk.  The operations on every
+// element are the one-column kernel's, in the same order: bit-identical factors.
+// ---------------------------------------------------------------------------
+#ifndef QCUR_CHOL_PB
+#define QCUR_CHOL_PB 8
+#endif
+constexpr int kPS = 4, kPB = QCUR_CHOL_PB, kPThreads = 32 * (kPS + kPB), kPBuf = 4;
+
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPThreads, 1) k_chol_inv_pipe(CholProblems P) {
+  const int c = (int)cg::this_cluster().block_rank();
+  const CholJob pr = P.p[blockIdx.x / kCl];
+  const int q = (int)P.q;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nown = (q - c + kCl - 1) / kCl;
+  extern __shared__ __align__(32) double sm[];
+  double* colbuf = sm;                                   // [4][q] columns of L in flight
+  double* diag = colbuf + kPBuf * (size_t)q * 4;         // [q] replicated running diagonal
+  double* invs = diag + q;                               // [q] 1 / l_jj
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(invs + q + 2);  // [4] column arrival, [4] bulk done
+  uint64_t* bdone = mbar + kPBuf;
+  double* rows = reinterpret_cast<double*>(mbar + 2 * kPBuf);
+  auto rowbase = [&](int s) -> size_t { return (size_t)s * (c + 1) + (size_t)8 * s * (s - 1); };
+  auto colbase = [&](int u) -> size_t { return (size_t)u * (q - c) - (size_t)8 * u * (u - 1); };
+  double* wcol = rows + rowbase(nown) * 4;
+  __shared__ int s_fail;
+
+  for (int s = 0; s < nown; ++s) {
+    const int i = c + kCl * s;
+    double* row = rows + rowbase(s) * 4;
+    for (int k = tid; k <= i; k += kPThreads) stQ(row + (size_t)k * 4, ldQ(pr.G + ((size_t)i * q + k) * 4));
+    double* col = wcol + colbase(s) * 4;
+    for (int r = i + tid; r < q; r += kPThreads) stQ(col + (size_t)(r - i) * 4, Quat{r == i ? 1.0 : 0.0, 0.0, 0.0, 0.0});
+  }
+  for (int i = tid; i < q; i += kPThreads) diag[i] = pr.G[((size_t)i * q + i) * 4];
+  if (tid == 0) {
+    for (int k = 0; k < kPBuf; ++k) mbar_init(&mbar[k], kCl + 1);  // 16 producer arrives + local expect_tx
+    mbar_init(bdone, 1);                                          // one arrive per bulk step
+    s_fail = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  cluster_barrier();
+
+  if (warp < kPS) {
+    // ---------------- senders ----------------
+    const int st = tid;  // 0 .. 32 kPS - 1
+    bool fail = false;
+    // send column j (own rows i > j, entry value v(s) supplied by the caller), scaled by inv
+    auto send = [&](int j, double inv, auto&& value) {
+      const int b = j % kPBuf;
+      if (st == 0) {
+        invs[j] = inv;  // before the local arrive: the bulk warps read it after this column's phase
+        mbar_expect_tx(&mbar[b], 32u * (unsigned)(q - 1 - j));
+      }
+      const uint32_t cb_u = smem_u32(colbuf + (size_t)b * q * 4), mb_u = smem_u32(&mbar[b]);
+      for (int t = st; t < nown * kCl; t += 32 * kPS) {
+        const int s = t / kCl, dst = t - s * kCl;
+        const int i = c + kCl * s;
+        if (i <= j) continue;
+        st_async_quat(mapa(cb_u + 32u * (unsigned)i, dst), fail ? qzero() : qscale(value(s), inv), mapa(mb_u, dst));
+      }
+      if (st < kCl) mbar_arrive_remote(mapa(mb_u, st));
+    };
+    {
+      const double d = diag[0];
+      fail = !(d > 0.0) || !isfinite(d);
+      send(0, fail ? 0.0 : 1.0 / sqrt(d), [&](int s) { return ldQ(rows + (rowbase(s) + 0) * 4); });
+    }
+    for (int j = 0; j < q; ++j) {
+      const int b = j % kPBuf;
+      const double* cb = colbuf + (size_t)b * q * 4;
+      mbar_wait(&mbar[b], (unsigned)(j / kPBuf) & 1u);
+      if (j + 1 < q) {
+        const Quat lj1 = ldQ(cb + (size_t)(j + 1) * 4);
+        const double d1 = diag[j + 1] - qnorm2(lj1);
+        if (!(d1 > 0.0) || !isfinite(d1)) fail = true;  // every CTA alike (replicated diagonal)
+        send(j + 1, fail ? 0.0 : 1.0 / sqrt(d1), [&](int s) {
+          const int i = c + kCl * s;
+          return qsub(ldQ(rows + (rowbase(s) + j + 1) * 4), qmul(ldQ(cb + (size_t)i * 4), qconj(lj1)));
+        });
+      }
+      if (j + 2 < q) {
+        if (j >= 1) mbar_wait(bdone, (unsigned)(j - 1) & 1u);  // the bulk of step j-1 is done
+        if (!fail) {
+          const Quat lj2 = ldQ(cb + (size_t)(j + 2) * 4);
+          for (int s = st; s < nown; s += 32 * kPS) {
+            const int i = c + kCl * s;
+            if (i <= j + 2) continue;
+            double* e = rows + (rowbase(s) + j + 2) * 4;
+            stQ(e, qsub(ldQ(e), qmul(ldQ(cb + (size_t)i * 4), qconj(lj2))));
+          }
+          if (st == 0) diag[j + 2] = diag[j + 2] - qnorm2(lj2);
+        }
+      }
+      named_sync(1, 32 * kPS);  // the next step's senders read the entries and pivot written above
+    }
+    if (st == 0 && fail) s_fail = 1;
+  } else {
+    // ---------------- bulk ----------------
+    const int bw = warp - kPS, bt = tid - 32 * kPS;
+    for (int j = 0; j < q; ++j) {
+      const int b = j % kPBuf;
+      const double* cb = colbuf + (size_t)b * q * 4;
+      mbar_wait(&mbar[b], (unsigned)(j / kPBuf) & 1u);
+      const double inv = invs[j];
+      const int s0 = j + 2 < c ? 0 : (j + 2 - c) / kCl + 1;  // own rows i > j + 2
+      const int nrow = nown > s0 ? nown - s0 : 0;
+      const int ncol = j < c ? 0 : ((j - c) / kCl + 1 < nown ? (j - c) / kCl + 1 : nown);
+      for (int it = kPB - 1 - bw; it < nrow + ncol; it += kPB) {
+        if (it < nrow) {
+          const int sr = s0 + it, i = c + kCl * sr;
+          const Quat lij = ldQ(cb + (size_t)i * 4);
+          double* row = rows + rowbase(sr) * 4;
+          for (int k0 = j + 3; k0 <= i; k0 += 32 * kCB) {
+            Quat av[kCB], bv[kCB];
+#pragma unroll
+            for (int u = 0; u < kCB; ++u) {
+              const int k = k0 + lane + 32 * u;
+              if (k <= i) {
+                av[u] = ldQ(row + (size_t)k * 4);
+                bv[u] = ldQ(cb + (size_t)k * 4);
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < kCB; ++u) {
+              const int k = k0 + lane + 32 * u;
+              if (k <= i) stQ(row + (size_t)k * 4, qsub(av[u], qmul(lij, qconj(bv[u]))));
+            }
+          }
+        } else {
+          const int u0 = it - nrow, k = c + kCl * u0;
+          double* w = wcol + colbase(u0) * 4 - (size_t)k * 4;  // w + i*4 addresses W_ik (i >= k)
+          const Quat xjk = qscale(ldQ(w + (size_t)j * 4), inv);
+          __syncwarp();
+          if (lane == 0) stQ(w + (size_t)j * 4, xjk);
+          for (int i0 = j + 1; i0 < q; i0 += 32 * kCB) {
+            Quat av[kCB], bv[kCB];
+#pragma unroll
+            for (int u = 0; u < kCB; ++u) {
+              const int i = i0 + lane + 32 * u;
+              if (i < q) {
+                av[u] = ldQ(w + (size_t)i * 4);
+                bv[u] = ldQ(cb + (size_t)i * 4);
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < kCB; ++u) {
+              const int i = i0 + lane + 32 * u;
+              if (i < q) stQ(w + (size_t)i * 4, qsub(av[u], qmul(bv[u], xjk)));
+            }
+          }
+          __syncwarp();
+        }
+      }
+      for (int i = j + 3 + bt; i < q; i += 32 * kPB) diag[i] = diag[i] - qnorm2(ldQ(cb + (size_t)i * 4));
+      named_sync(2, 32 * kPB);  // every bulk warp is done with step j
+      if (bt == 0) mbar_arrive(bdone);
+    }
+  }
+  __syncthreads();
+  if (s_fail) {  // identical in every CTA (replicated diagonal)
+    if (c == 0 && tid == 0) atomicOr(P.status, pr.fail_bit);
+    cluster_barrier();
+    return;
+  }
+  for (int u = 0; u < nown; ++u) {
+    const int k = c + kCl * u;
+    const double* w = wcol + colbase(u) * 4;
+    for (int i = tid; i < q; i += kPThreads) stQ(pr.X + ((size_t)i * q + k) * 4, i >= k ? ldQ(w + (size_t)(i - k) * 4) : qzero());
+  }
+  cluster_barrier();
+}
+
+static size_t chol_pipe_smem(int64_t q) {
+  size_t best = 0;
+  for (int c = 0; c < kCl; ++c) {
+    const int64_t nown = (q - c + kCl - 1) / kCl;
+    const int64_t rows = nown * (c + 1) + 8 * nown * (nown - 1);
+    const int64_t cols = nown * (q - c) - 8 * nown * (nown - 1);
+    const size_t b = (size_t)(kPBuf * q * 4 + 2 * q + 2 + 2 * kPBuf + 4 * (rows + cols)) * sizeof(double);
+    best = b > best ? b : best;
+  }
+  return best;
+}
+
 // dynamic shared memory of the CTA with the largest triangles (rank 0)
 static size_t chol_cluster_smem(int64_t q) {
   size_t best = 0;
@@ -632,6 +829,20 @@ void launch_chol_inv_cluster(const CholJob* jobs, int njobs, int64_t q, unsigned
     }
     ++::qcur::g_launches;
     k_chol_inv_cluster2<<<kCl * njobs, kThreads, chol_cluster_smem2(q), st>>>(P);
+    return;
+  }
+  static const int pipe_env = [] {
+    const char* e = std::getenv("QCUR_CHOL_PIPE");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (pipe_env && chol_pipe_smem(q) <= 226 * 1024) {
+    static std::atomic<unsigned> setp{0};
+    if (first_on_device(setp)) {
+      cudaFuncSetAttribute(k_chol_inv_pipe, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(k_chol_inv_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
+    }
+    ++::qcur::g_launches;
+    k_chol_inv_pipe<<<kCl * njobs, kPThreads, chol_pipe_smem(q), st>>>(P);
     return;
   }
   ++::qcur::g_launches;
