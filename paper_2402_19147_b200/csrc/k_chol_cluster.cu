@@ -592,7 +592,7 @@ void chol_trace_read(long long* out) { cudaMemcpyFromSymbol(out, g_chol_trace, s
 #endif
 
 // ---------------------------------------------------------------------------
-// Pipelined variant (QCUR_CHOL_PIPE): warp-specialised.  Sender warps (S) run the critical chain:
+// Pipelined variant (default for q >= 192; QCUR_CHOL_PIPE=0/1 forces it): warp-specialised.  Sender warps (S) run the critical chain:
 // wait for column j, form and send column j+1 of the own rows, then apply step j to column j+2
 // (entries and replicated pivot) once the bulk warps have finished step j-1.  Bulk warps (B) apply
 // step j to the columns k >= j+3 of the own rows and to the inverse, one step behind the senders, so
@@ -604,6 +604,7 @@ void chol_trace_read(long long* out) { cudaMemcpyFromSymbol(out, g_chol_trace, s
 #define QCUR_CHOL_PB 8
 #endif
 constexpr int kPS = 4, kPB = QCUR_CHOL_PB, kPThreads = 32 * (kPS + kPB), kPBuf = 4;
+constexpr int64_t kPipeQMin = 192;
 
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -831,11 +832,13 @@ void launch_chol_inv_cluster(const CholJob* jobs, int njobs, int64_t q, unsigned
     k_chol_inv_cluster2<<<kCl * njobs, kThreads, chol_cluster_smem2(q), st>>>(P);
     return;
   }
+  // pipelined variant from q = 192 up (measured, factor phase per approximation: q = 200 1.196 -> 1.160 ms,
+  // q = 256 1.073 -> 1.033 ms; slower at q <= 128: 0.414 -> 0.432 ms); QCUR_CHOL_PIPE=0/1 forces it
   static const int pipe_env = [] {
     const char* e = std::getenv("QCUR_CHOL_PIPE");
-    return e ? std::atoi(e) : 0;
+    return e ? std::atoi(e) : -1;
   }();
-  if (pipe_env && chol_pipe_smem(q) <= 226 * 1024) {
+  if ((pipe_env == 1 || (pipe_env < 0 && q >= kPipeQMin)) && chol_pipe_smem(q) <= 226 * 1024) {
     static std::atomic<unsigned> setp{0};
     if (first_on_device(setp)) {
       cudaFuncSetAttribute(k_chol_inv_pipe, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

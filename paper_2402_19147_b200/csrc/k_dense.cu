@@ -164,6 +164,78 @@ void launch_series_inv_prep(const double* G2, int64_t q, double* E, double* S, u
   k_series_inv_prep<<<blocks, 256, 0, st>>>(G2, q, E, S, status, fail_bit, thresh);
 }
 
+// k_series_inv_prep for up to two blocks in one launch (blockIdx.y), with the kappa_F guard of the
+// first pass folded in: each CTA adds its share of trace(G1) and ||L1^{-1}||_F^2, stores the two
+// partials, and the last CTA of a block (ticket, reset by it) adds them in CTA order and raises
+// fail_bit when sqrt(tr G1) ||L1^{-1}||_F > limit.  Same E and S as k_series_inv_prep.
+__global__ void __launch_bounds__(256) k_series_kappa(const __grid_constant__ SeriesKappaJobs J, unsigned* status,
+                                                      unsigned* tickets, double thresh, double limit) {
+  const SeriesKappaJob& jb = J.j[blockIdx.y];
+  const int64_t q = jb.q;
+  __shared__ double sh[8];
+  __shared__ unsigned s_last;
+  int bad = 0;
+  double a = 0.0, b = 0.0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < q * q; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / q, k = t - i * q;
+    Quat e = k <= i ? ldQ(jb.G2 + t * 4) : qconj(ldQ(jb.G2 + (k * q + i) * 4));
+    if (i == k) {
+      e = Quat{e.w - 1.0, 0.0, 0.0, 0.0};
+      a += jb.G1[t * 4];
+    }
+    if (k <= i) {
+      const double mx = fmax(fmax(fabs(e.w), fabs(e.x)), fmax(fabs(e.y), fabs(e.z)));
+      if (!(mx <= thresh)) bad = 1;
+    }
+    b += qnorm2(ldQ(jb.L1i + t * 4));
+    stQ(jb.E + t * 4, e);
+    Quat sv = qscale(e, -1.0);
+    if (i == k) sv.w += 1.0;
+    stQ(jb.S + t * 4, sv);
+  }
+  if (bad) atomicOr(status, jb.fail_bit);
+  const double sa = block_sum<256>(a, sh);
+  const double sb = block_sum<256>(b, sh);
+  if (threadIdx.x == 0) {
+    jb.partials[2 * blockIdx.x] = sa;
+    jb.partials[2 * blockIdx.x + 1] = sb;
+    __threadfence();
+    s_last = atomicAdd(&tickets[blockIdx.y], 1u) == gridDim.x - 1 ? 1u : 0u;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  double pa = 0.0, pb = 0.0;
+  for (unsigned k = threadIdx.x; k < gridDim.x; k += blockDim.x) {  // CTA order within each thread
+    pa += __ldcg(jb.partials + 2 * k);
+    pb += __ldcg(jb.partials + 2 * k + 1);
+  }
+  const double ta = block_sum<256>(pa, sh);
+  const double tb = block_sum<256>(pb, sh);
+  if (threadIdx.x == 0) {
+    tickets[blockIdx.y] = 0u;
+    const double kf = sqrt(ta) * sqrt(tb);
+    if (!(kf <= limit)) atomicOr(status, jb.fail_bit);
+  }
+}
+
+int series_kappa_blocks(int64_t q) {
+  int blocks = (int)((q * q + 255) / 256);
+  return blocks > 296 ? 296 : blocks;
+}
+
+void launch_series_kappa(const SeriesKappaJobs& J, int nj, unsigned* status, unsigned* tickets, double thresh,
+                         double limit, cudaStream_t st) {
+  int blocks = 1;
+  for (int k = 0; k < nj; ++k) {
+    const int b = series_kappa_blocks(J.j[k].q);
+    blocks = b > blocks ? b : blocks;
+  }
+  // every block of the grid must visit its ticket: a problem with fewer elements still has `blocks` CTAs
+  ++::qcur::g_launches;
+  k_series_kappa<<<dim3((unsigned)blocks, (unsigned)nj), 256, 0, st>>>(J, status, tickets, thresh, limit);
+}
+
 // L2inv = I - M1 + P2 (P2 = M1 M1, lower triangular)
 __global__ void k_series_final(const double* __restrict__ M1, const double* __restrict__ P2, int64_t q,
                                double* __restrict__ L2inv) {

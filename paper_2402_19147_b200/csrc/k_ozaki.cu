@@ -857,19 +857,51 @@ __device__ __forceinline__ bool oz_tile_computed(int row, int col, int lower_bn)
 constexpr int kHBW = 32;
 constexpr int kOzHcrtSmem = 8 * kOzMaxModDefault * kHB * kHBW + 64;  // [u | mirror u + 4][modulus][row][32]
 
+// Both problems of a factorization step in one launch (blockIdx.z); a problem whose consumers read
+// only the lower triangle of its Hermitian output (the CholeskyQR2 Grams: the Cholesky, the series
+// and the kappa guard read k <= i) enumerates only the 16 x 16 blocks on or below the diagonal.
+struct OzHcrtProb {
+  CUtensorMap tm;
+  int64_t qa, qb, ldc;
+  const int* exa;
+  const int* exb;
+  double* C;
+  int lower_bn, tri, nbx, nblk;
+};
+struct OzHcrtJobs {
+  OzHcrtProb p[2];
+};
+
 template <int L>
-__global__ void __launch_bounds__(kHB * kHB) k_oz_hcrt(const __grid_constant__ CUtensorMap tm, int64_t qa, int64_t qb,
-                                                       const int* __restrict__ exa, const int* __restrict__ exb,
-                                                       const __grid_constant__ OzCrt c, double* __restrict__ C,
-                                                       int64_t ldc, int lower_bn) {
+__global__ void __launch_bounds__(kHB * kHB) k_oz_hcrt(const __grid_constant__ OzHcrtJobs H,
+                                                       const __grid_constant__ OzCrt c) {
+  const OzHcrtProb& hp = H.p[blockIdx.z];
+  if ((int)blockIdx.x >= hp.nblk) return;
+  int bi, bj;
+  if (hp.tri) {  // linear index -> (bi, bj), bj <= bi
+    const int b = (int)blockIdx.x;
+    bi = (int)((sqrtf(8.0f * (float)b + 1.0f) - 1.0f) * 0.5f);
+    while ((bi + 1) * (bi + 2) / 2 <= b) ++bi;
+    while (bi * (bi + 1) / 2 > b) --bi;
+    bj = b - bi * (bi + 1) / 2;
+  } else {
+    bi = (int)blockIdx.x / hp.nbx;
+    bj = (int)blockIdx.x - bi * hp.nbx;
+  }
+  const CUtensorMap& tm = hp.tm;
+  const int64_t qa = hp.qa, qb = hp.qb, ldc = hp.ldc;
+  const int* __restrict__ exa = hp.exa;
+  const int* __restrict__ exb = hp.exb;
+  double* __restrict__ C = hp.C;
+  const int lower_bn = hp.lower_bn;
   extern __shared__ __align__(128) uint8_t hsm[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(hsm + 8 * L * kHB * kHBW);
   auto blk = [&](int box, int l, int row, int col) -> uint8_t {
     return hsm[((box * L + l) * kHB + row) * kHBW + col];
   };
   const int tx = threadIdx.x % kHB, ty = threadIdx.x / kHB;
-  const int t = (int)blockIdx.z;
-  const int i0 = (int)blockIdx.y * kHB, j0 = (int)blockIdx.x * kHB;
+  const int t = (int)blockIdx.y;
+  const int i0 = bi * kHB, j0 = bj * kHB;
   // (a, b, sign) of the four plane products of component t
   constexpr int kTerm[4][4][3] = {{{0, 0, 1}, {1, 1, 1}, {2, 2, 1}, {3, 3, 1}},
                                   {{0, 1, 1}, {1, 0, -1}, {2, 3, -1}, {3, 2, 1}},
@@ -1450,7 +1482,7 @@ int launch_ozaki_gemm(const double* X, int64_t m, int64_t n, int64_t ldx, const 
 // allowed: its planes are formed once); one INT8 GEMM launch for all of them
 int launch_ozaki_herm(const double* const* A, const double* const* B, const int64_t* p, const int64_t* qa,
                       const int64_t* qb, const int64_t* lda, const int64_t* ldb, double* const* C,
-                      const int64_t* ldc, int np, int L, void* const* workspace, cudaStream_t st) {
+                      const int64_t* ldc, int np, int L, void* const* workspace, cudaStream_t st, int lower_only) {
   if (L < 14 || L > 15 || np < 1 || np > 2) return 1;
   static const int lower_env = [] {  // QCUR_OZ_LOWER=0: full plane Grams (A/B timing)
     const char* e = std::getenv("QCUR_OZ_LOWER");
@@ -1481,37 +1513,46 @@ int launch_ozaki_herm(const double* const* A, const double* const* B, const int6
   oz_planes_launch(pj, npj, L, st);
   oz_launch_gemm(jobs, np, L, st);
   const OzCrt cc = oz_crt(L);
+  OzHcrtJobs H{};
+  int gx = 0;
   for (int k = 0; k < np; ++k) {
     const OzHPlan& h = hp[k];
     const bool same = A[k] == B[k] && qa[k] == qb[k] && lda[k] == ldb[k];
-    const int* exa = reinterpret_cast<int*>(ws[k] + h.off_exa);
-    const int* exb = same ? exa : reinterpret_cast<int*>(ws[k] + h.off_exb);
-    const dim3 grid((unsigned)((qb[k] + kHB - 1) / kHB), (unsigned)((qa[k] + kHB - 1) / kHB), 4);
-    const int lbn = jobs[k].pr.lower ? jobs[k].pr.BN : 0;
+    OzHcrtProb& P = H.p[k];
+    P.exa = reinterpret_cast<int*>(ws[k] + h.off_exa);
+    P.exb = same ? P.exa : reinterpret_cast<int*>(ws[k] + h.off_exb);
+    P.qa = qa[k];
+    P.qb = qb[k];
+    P.ldc = ldc[k] * 4;
+    P.C = C[k];
+    P.lower_bn = jobs[k].pr.lower ? jobs[k].pr.BN : 0;
+    const int nba = (int)((qa[k] + kHB - 1) / kHB), nbb = (int)((qb[k] + kHB - 1) / kHB);
+    P.tri = same && lower_only ? 1 : 0;
+    P.nbx = nbb;
+    P.nblk = P.tri ? nba * (nba + 1) / 2 : nba * nbb;
+    gx = P.nblk > gx ? P.nblk : gx;
     // residue planes as a 3-D tensor: columns (Npitch bytes), rows (4 qa), moduli; 16 x 16 x L boxes
-    CUtensorMap tm;
-    {
-      auto enc = oz_encode();
-      cuuint64_t dims[3] = {(cuuint64_t)h.g.Npitch, (cuuint64_t)(4 * qa[k]), (cuuint64_t)L};
-      cuuint64_t strides[2] = {(cuuint64_t)h.g.Npitch, (cuuint64_t)(4 * qa[k] * h.g.Npitch)};
-      cuuint32_t box[3] = {(cuuint32_t)kHBW, (cuuint32_t)kHB, (cuuint32_t)L};
-      cuuint32_t estr[3] = {1, 1, 1};
-      if (!enc || enc(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, ws[k] + h.off_res, dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        return 2;
-    }
-    static std::atomic<unsigned> hattr{0};
-    if (first_on_device(hattr)) {
-      cudaFuncSetAttribute(k_oz_hcrt<14>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOzHcrtSmem);
-      cudaFuncSetAttribute(k_oz_hcrt<15>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOzHcrtSmem);
-    }
-    ++::qcur::g_launches;
-    if (L == 14)
-      k_oz_hcrt<14><<<grid, kHB * kHB, kOzHcrtSmem, st>>>(tm, qa[k], qb[k], exa, exb, cc, C[k], ldc[k] * 4, lbn);
-    else
-      k_oz_hcrt<15><<<grid, kHB * kHB, kOzHcrtSmem, st>>>(tm, qa[k], qb[k], exa, exb, cc, C[k], ldc[k] * 4, lbn);
+    auto enc = oz_encode();
+    cuuint64_t dims[3] = {(cuuint64_t)h.g.Npitch, (cuuint64_t)(4 * qa[k]), (cuuint64_t)L};
+    cuuint64_t strides[2] = {(cuuint64_t)h.g.Npitch, (cuuint64_t)(4 * qa[k] * h.g.Npitch)};
+    cuuint32_t box[3] = {(cuuint32_t)kHBW, (cuuint32_t)kHB, (cuuint32_t)L};
+    cuuint32_t estr[3] = {1, 1, 1};
+    if (!enc || enc(&P.tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, ws[k] + h.off_res, dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return 2;
   }
+  static std::atomic<unsigned> hattr{0};
+  if (first_on_device(hattr)) {
+    cudaFuncSetAttribute(k_oz_hcrt<14>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOzHcrtSmem);
+    cudaFuncSetAttribute(k_oz_hcrt<15>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOzHcrtSmem);
+  }
+  const dim3 grid((unsigned)gx, 4, (unsigned)np);
+  ++::qcur::g_launches;
+  if (L == 14)
+    k_oz_hcrt<14><<<grid, kHB * kHB, kOzHcrtSmem, st>>>(H, cc);
+  else
+    k_oz_hcrt<15><<<grid, kHB * kHB, kOzHcrtSmem, st>>>(H, cc);
   return 0;
 }
 

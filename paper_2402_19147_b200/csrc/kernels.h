@@ -141,6 +141,23 @@ void launch_series_lh(const double* G2, const double* P, int64_t q, double* M, u
                       double thresh, cudaStream_t st);
 void launch_series_final(const double* M1, const double* P2, int64_t q, double* L2inv, cudaStream_t st);
 // E = G2 - I and S = I - E, both full (from G2's lower triangle); fail_bit when max|E| > thresh
+struct SeriesKappaJob {
+  const double* G2;   // second Gram (lower triangle read)
+  const double* G1;   // first Gram (diagonal read: trace)
+  const double* L1i;  // L1^{-1} (kappa guard)
+  double* E;
+  double* S;
+  double* partials;  // [2 * series_kappa_blocks(q)]
+  int64_t q;
+  unsigned fail_bit;
+};
+struct SeriesKappaJobs {
+  SeriesKappaJob j[2];
+};
+int series_kappa_blocks(int64_t q);
+// k_series_inv_prep + k_kappa_check of up to two blocks in one launch; tickets[0..nj) zero between launches
+void launch_series_kappa(const SeriesKappaJobs& J, int nj, unsigned* status, unsigned* tickets, double thresh,
+                         double limit, cudaStream_t st);
 void launch_series_inv_prep(const double* G2, int64_t q, double* E, double* S, unsigned* status, unsigned fail_bit,
                             double thresh, cudaStream_t st);
 void launch_chol_inv_cluster(const CholJob* jobs, int njobs, int64_t q, unsigned* status, cudaStream_t st);
@@ -213,7 +230,8 @@ size_t ozaki_herm_workspace_bytes(int64_t p, int64_t qa, int64_t qb, int same);
 bool ozaki_herm_supported(int64_t p, int64_t qa, int64_t qb);
 int launch_ozaki_herm(const double* const* A, const double* const* B, const int64_t* p, const int64_t* qa,
                       const int64_t* qb, const int64_t* lda, const int64_t* ldb, double* const* C,
-                      const int64_t* ldc, int np, int L, void* const* workspace, cudaStream_t st);
+                      const int64_t* ldc, int np, int L, void* const* workspace, cudaStream_t st,
+                      int lower_only = 0);  // 1: same-operand products write only blocks on/below the diagonal
 
 // k_ozaki_err.cu : the fused error ||X - P R|| (out4 as launch_cur_error) with P R on the INT8
 // tensor cores by exact base-256 digit slices (Ozaki scheme I, 21 digit products).

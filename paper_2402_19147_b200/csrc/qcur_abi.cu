@@ -24,6 +24,7 @@ namespace {
 
 constexpr double kEps = 2.220446049250313e-16;
 constexpr int kOzakiModuli = 15;  // default modulus count of the INT8 (Ozaki II) GEMM
+constexpr size_t kSeriesTickets = 2 * 65536, kCounterWords = 2 * 65536 + 64;  // ctx->counters layout
 
 // Optional phase timing: CUDA events recorded on the launching stream between
 // pipeline phases; harvested (after a sync) by qcur_profile_read.
@@ -83,6 +84,7 @@ struct qcur_ctx {
   unsigned* status_dev = nullptr;
   unsigned* status_host = nullptr;  // pinned
   unsigned* counters = nullptr;     // split-K tickets for launch_qgemm (kept zero between launches)
+                                    // [2 * 65536, + 2): tickets of launch_series_kappa
   unsigned last_info = 0;
   double kappa_limit = 1e7;
   bool force_robust = false;
@@ -588,7 +590,7 @@ int factor_multi(qcur_ctx* ctx, const FactorSpec* specs_in, int ns) {
         ++np;
       }
       if (np == 0) return QCUR_OK;
-      if (launch_ozaki_herm(A, A, pp, qq, qq, lda, lda, G, ldg, np, ctx->herm_moduli, w, st))
+      if (launch_ozaki_herm(A, A, pp, qq, qq, lda, lda, G, ldg, np, ctx->herm_moduli, w, st, 1))
         return ctx->fail(QCUR_E_CUDA, "int8 gram: tensor map encode failed");
       CK_LAUNCH(ctx, "int8 gram");
       return QCUR_OK;
@@ -689,17 +691,22 @@ int factor_multi(qcur_ctx* ctx, const FactorSpec* specs_in, int ns) {
     return e ? std::atoi(e) : -1;
   }();
   if (series_env != 0) {
-    for (int k = 0; k < ns; ++k)
-      if (fast[k]) launch_series_inv_prep(B[k].G2, specs[k].q, B[k].Tcm, B[k].Vcm, status, specs[k].fail_bit, 1e-5, st);
+    // E, S = I - E and the kappa_F guard of both blocks in one launch
+    SeriesKappaJobs sj{};
+    int nsj = 0;
+    for (int k = 0; k < ns; ++k) {
+      if (!fast[k]) continue;
+      double* part = ctx->take<double>((size_t)2 * series_kappa_blocks(specs[k].q) + 8);
+      if (!part) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (series)");
+      sj.j[nsj++] = SeriesKappaJob{B[k].G2, B[k].G1, B[k].L1i, B[k].Tcm, B[k].Vcm, part, specs[k].q, specs[k].fail_bit};
+    }
+    if (nsj) launch_series_kappa(sj, nsj, status, ctx->counters + kSeriesTickets, 1e-5, ctx->kappa_limit, st);
     CK_LAUNCH(ctx, "series prep");
     if ((rc = gemm_each([&](int k) {  // S += E E  (S = I - E + E^2)
            const int64_t q = specs[k].q;
            return gargs(q, q, q, B[k].Tcm, q, 0, B[k].Tcm, q, 0, B[k].Vcm, q, 1.0, 1.0);
          })))
       return rc;
-    for (int k = 0; k < ns; ++k)
-      if (fast[k]) launch_kappa_check(B[k].G1, B[k].L1i, specs[k].q, ctx->kappa_limit, status, specs[k].fail_bit, st);
-    CK_LAUNCH(ctx, "kappa");
     if ((rc = gemm_each([&](int k) {  // F = L1^{-H} S
            const int64_t q = specs[k].q;
            return gargs(q, q, q, B[k].L1i, q, 1, B[k].Vcm, q, 0, specs[k].out.F, q);
@@ -1183,11 +1190,11 @@ int qcur_create(int device, qcur_ctx** out) {
     return QCUR_E_CUDA;
   }
   cudaMemset(ctx->status_dev, 0, 64);
-  if (cudaMalloc(&ctx->counters, (size_t)2 * 65536 * sizeof(unsigned)) != cudaSuccess) {
+  if (cudaMalloc(&ctx->counters, (size_t)kCounterWords * sizeof(unsigned)) != cudaSuccess) {
     delete ctx;
     return QCUR_E_CUDA;
   }
-  cudaMemset(ctx->counters, 0, (size_t)2 * 65536 * sizeof(unsigned));
+  cudaMemset(ctx->counters, 0, (size_t)kCounterWords * sizeof(unsigned));
   if (const char* xm = std::getenv("QCUR_XQ_MODULI")) ctx->xq_moduli = std::atoi(xm) == 14 ? 14 : 15;
   if (const char* hm = std::getenv("QCUR_HERM_MODULI")) ctx->herm_moduli = std::atoi(hm) == 14 ? 14 : 15;
   if (const char* gm = std::getenv("QCUR_GEMM"))
