@@ -315,6 +315,78 @@ __global__ void k_oz_bres(const double* __restrict__ B, int64_t Kq, int64_t Nq, 
   }
 }
 
+// The small right operand of a factorization product (Q_1 = Z L_1^{-H}: B = L_1^{-H}, q x q) for up to
+// two problems in one launch: one CTA per quaternion column j of B reduces the column maximum, stores
+// the exponent and writes the residues of E(B') for that column (k_oz_bmax + k_oz_bexp + k_oz_bres
+// without the atomics and the two extra launches).  conjT: B = A^H, read from A's row j (contiguous).
+struct OzBColJob {
+  const double* B;
+  int64_t Kq, Nq, ldb, pitch, plane;
+  int conjT, bits;
+  int* fx;
+  uint8_t* res;
+};
+struct OzBColJobs {
+  OzBColJob j[2];
+};
+
+__global__ void __launch_bounds__(256) k_oz_bcol(const __grid_constant__ OzBColJobs J, const __grid_constant__ OzMods md) {
+  const OzBColJob& jb = J.j[blockIdx.y];
+  const int64_t j = blockIdx.x;
+  if (j >= jb.Nq) return;
+  auto ld = [&](int64_t k) -> Quat {
+    if (jb.conjT) {
+      const Quat a = ldq_nc(jb.B + (j * jb.ldb + k) * 4);
+      return Quat{a.w, -a.x, -a.y, -a.z};
+    }
+    return ldq_nc(jb.B + (k * jb.ldb + j) * 4);
+  };
+  __shared__ double sh[8];
+  double mx = 0.0;
+  for (int64_t k = threadIdx.x; k < jb.Kq; k += 256) {
+    const Quat q = ld(k);
+    mx = fmax(mx, fmax(fmax(fabs(q.w), fabs(q.x)), fmax(fabs(q.y), fabs(q.z))));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  mx = 0.0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) mx = fmax(mx, sh[w]);
+  int e = 0;
+  if (mx > 0.0) {
+    int E;
+    frexp(mx, &E);
+    e = jb.bits - E;
+  }
+  if (threadIdx.x == 0) jb.fx[j] = e;
+  const int64_t kq_pad = jb.pitch / 4;
+  for (int64_t k = threadIdx.x; k < kq_pad; k += 256) {
+    double b[4] = {0.0, 0.0, 0.0, 0.0};
+    if (k < jb.Kq) {
+      const Quat q = ld(k);
+      b[0] = (scale2(q.w, e) + kMagic) - kMagic;
+      b[1] = (scale2(q.x, e) + kMagic) - kMagic;
+      b[2] = (scale2(q.y, e) + kMagic) - kMagic;
+      b[3] = (scale2(q.z, e) + kMagic) - kMagic;
+    }
+    for (int l = 0; l < md.L; ++l) {  // the layout and signs of k_oz_bres
+      unsigned r[4], n[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        r[u] = residue_byte(b[u], l, md);
+        n[u] = (0u - r[u]) & 0xffu;
+      }
+      uint8_t* o = jb.res + l * jb.plane + (4 * j) * jb.pitch + 4 * k;
+      *reinterpret_cast<unsigned*>(o) = r[0] | (n[1] << 8) | (n[2] << 16) | (n[3] << 24);
+      *reinterpret_cast<unsigned*>(o + jb.pitch) = r[1] | (r[0] << 8) | (r[3] << 16) | (n[2] << 24);
+      *reinterpret_cast<unsigned*>(o + 2 * jb.pitch) = r[2] | (n[3] << 8) | (r[0] << 16) | (r[1] << 24);
+      *reinterpret_cast<unsigned*>(o + 3 * jb.pitch) = r[3] | (r[2] << 8) | (n[1] << 16) | (r[0] << 24);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // tcgen05 int8 GEMM:  res[l][i][j] = (A_l[i,:] . B_l[j,:]) mod p_l  (bytes in [0, p_l))
 // ---------------------------------------------------------------------------
@@ -1476,6 +1548,47 @@ int launch_ozaki_gemm(const double* X, int64_t m, int64_t n, int64_t ldx, const 
                       double* Y, int64_t ldy, int L, void* workspace, cudaStream_t st) {
   int rc = launch_ozaki_prepare(X, m, n, ldx, r, L, workspace, st);
   return rc ? rc : launch_ozaki_finish(m, n, B, r, ldb, Y, ldy, L, workspace, st);
+}
+
+// Y_k (m_k x r_k) = X_k (m_k x n_k) op(B_k) for np <= 2 problems with small right operands (the
+// triangular products Q_1 = Z L_1^{-H} of a factorization step): residues of each X_k (one CTA per
+// row), of every op(B_k) in one k_oz_bcol launch, one tcgen05 launch for all products, one CRT each.
+// conjT[k]: op(B_k) = B_k^H (B_k is r_k x n_k).  workspace[k]: ozaki_workspace_bytes(m_k, n_k, r_k, L).
+int launch_ozaki_pair(const double* const* X, const int64_t* m, const int64_t* n, const int64_t* ldx,
+                      const double* const* B, const int64_t* r, const int64_t* ldb, const int* conjT, double* const* Y,
+                      const int64_t* ldy, int np, int L, void* const* workspace, cudaStream_t st) {
+  if (L < 14 || L > 15 || np < 1 || np > 2) return 1;
+  OzJob jobs[2];
+  OzPlan pl[2];
+  uint8_t* ws[2];
+  OzBColJobs bj{};
+  int64_t rmax = 0;
+  for (int k = 0; k < np; ++k) {
+    pl[k] = oz_plan(m[k], n[k], r[k], L);
+    ws[k] = reinterpret_cast<uint8_t*>(((uintptr_t)workspace[k] + 255) / 256 * 256);
+    uint8_t* ares = ws[k] + pl[k].off_ares;
+    int* ex = reinterpret_cast<int*>(ws[k] + pl[k].off_ex);
+    ++::qcur::g_launches;
+    if (L == 14)
+      k_oz_xres<14, 256><<<(unsigned)m[k], 256, 0, st>>>(X[k], pl[k].K, ldx[k] * 4, pl[k].bits, ares, pl[k].Kpitch,
+                                                         m[k] * pl[k].Kpitch, ex);
+    else
+      k_oz_xres<15, 256><<<(unsigned)m[k], 256, 0, st>>>(X[k], pl[k].K, ldx[k] * 4, pl[k].bits, ares, pl[k].Kpitch,
+                                                         m[k] * pl[k].Kpitch, ex);
+    bj.j[k] = OzBColJob{B[k], n[k], r[k], ldb[k], pl[k].Kpitch, pl[k].N * pl[k].Kpitch, conjT[k], pl[k].bits,
+                        reinterpret_cast<int*>(ws[k] + pl[k].off_fx), ws[k] + pl[k].off_bres};
+    rmax = r[k] > rmax ? r[k] : rmax;
+    if (!oz_job(jobs[k], pl[k], m[k], ares, pl[k].Kpitch, ws[k] + pl[k].off_bres, L, ws[k] + pl[k].off_res)) return 2;
+  }
+  ++::qcur::g_launches;
+  k_oz_bcol<<<dim3((unsigned)rmax, (unsigned)np), 256, 0, st>>>(bj, oz_mods(L));
+  oz_launch_gemm(jobs, np, L, st);
+  for (int k = 0; k < np; ++k) {
+    const int rc = oz_launch_crt(ws[k] + pl[k].off_res, m[k], pl[k], reinterpret_cast<int*>(ws[k] + pl[k].off_ex),
+                                 reinterpret_cast<int*>(ws[k] + pl[k].off_fx), Y[k], ldy[k], L, st);
+    if (rc) return rc;
+  }
+  return 0;
 }
 
 // C_k (qa_k x qb_k) = A_k^H B_k for np <= 2 problems (A_k: p_k x qa_k, B_k: p_k x qb_k, B_k == A_k

@@ -342,6 +342,8 @@ struct FactorOut {
   double* F;  // q x q
 };
 
+bool int8_q1_fits(int64_t p, int64_t q);
+
 size_t factor_ws_bytes(int64_t p, int64_t q) {
   size_t b = 0;
   b += qbytes(p, q) * 2;        // Zcm, Qcm
@@ -360,6 +362,7 @@ size_t factor_ws_bytes(int64_t p, int64_t q) {
   if (q > 304)  // blocked Cholesky scratch (chol_inv_blocked): A, L, blocks, T and its GEMM slabs
     b += 2 * qbytes(q, q) + 2 * qbytes(256, 256) + qbytes(256, q) + (size_t)16 * q * q * 8 + 8192;
   if (ozaki_herm_supported(p, q, q)) b += ozaki_herm_workspace_bytes(p, q, q, 1) + 4096;  // INT8 Grams
+  if (int8_q1_fits(p, q)) b += ozaki_workspace_bytes(p, q, q, 15) + 4096;                   // INT8 Q1
   return b + 16 * 256;
 }
 
@@ -421,6 +424,20 @@ int64_t int8_chunk_rows(const qcur_ctx* ctx, int64_t m, int64_t n, int64_t r) {
 bool use_int8_gram(const qcur_ctx* ctx, int64_t p, int64_t q) {
   if (ctx->gemm_mode == 1 || !ozaki_herm_supported(p, q, q)) return false;
   return ctx->gemm_mode == 2 || (double)p * (double)q * (double)q >= kInt8MinGram;
+}
+
+// the triangular product Q1 = Z L1^{-H} (Z: p x q) of CholeskyQR2 on the INT8 tensor cores?  Off by
+// default: measured slower than the FP64 DMMA GEMM at every BASELINE size (cfg2 pair: residues 2 x 59,
+// GEMM 155, CRT 2 x 52 = 386 us against 230 us on DMMA; factor phase 1.162 -> 1.327 ms).
+// QCUR_INT8_MIN_Q1 (a p q^2 threshold) turns it on for A/B timing and tests.
+const double kInt8MinQ1 = env_or("QCUR_INT8_MIN_Q1", 1e300);
+constexpr double kInt8Q1WorkspaceCap = 2e9;  // bytes per block (cfg5's q = 1000 stays on DMMA)
+bool int8_q1_fits(int64_t p, int64_t q) {
+  return ozaki_supported(p, q, q) && (double)ozaki_workspace_bytes(p, q, q, 15) <= kInt8Q1WorkspaceCap;
+}
+bool use_int8_q1(const qcur_ctx* ctx, int64_t p, int64_t q) {
+  if (ctx->gemm_mode == 1 || !int8_q1_fits(p, q)) return false;
+  return ctx->gemm_mode == 2 || (double)p * (double)q * (double)q >= kInt8MinQ1;
 }
 
 // the fused error ||X - P R|| on the INT8 tensor cores?  (same policy, its own shape limits)
@@ -666,7 +683,35 @@ int factor_multi(qcur_ctx* ctx, const FactorSpec* specs_in, int ns) {
     return rc;
   if ((rc = chol_inv(false))) return rc;
   // Q1 = Z L1^{-H} (written straight into the output Q);  G2 = Q1^H Q1
-  if ((rc = gemm_each([&](int k) {
+  // Q1 on the INT8 tensor cores (Ozaki II, both blocks in shared launches) next to INT8 Grams
+  bool i8q1 = i8gram;
+  for (int k = 0; k < ns; ++k)
+    if (fast[k] && !use_int8_q1(ctx, specs[k].p, specs[k].q)) i8q1 = false;
+  if (i8q1) {
+    const double* X[2];
+    const double* Bm[2];
+    int64_t mm[2], nn[2], ld[2];
+    int cj[2];
+    double* Y[2];
+    void* w[2];
+    int np = 0;
+    for (int k = 0; k < ns; ++k) {
+      if (!fast[k]) continue;
+      X[np] = specs[k].src;
+      Bm[np] = B[k].L1i;
+      mm[np] = specs[k].p;
+      nn[np] = specs[k].q;
+      ld[np] = specs[k].q;
+      cj[np] = 1;
+      Y[np] = specs[k].out.Q;
+      w[np] = ctx->take<uint8_t>(ozaki_workspace_bytes(specs[k].p, specs[k].q, specs[k].q, ctx->herm_moduli));
+      if (!w[np]) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (int8 Q1)");
+      ++np;
+    }
+    if (np && launch_ozaki_pair(X, mm, nn, ld, Bm, nn, ld, cj, Y, ld, np, ctx->herm_moduli, w, st))
+      return ctx->fail(QCUR_E_CUDA, "int8 Q1: tensor map encode failed");
+    CK_LAUNCH(ctx, "int8 Q1");
+  } else if ((rc = gemm_each([&](int k) {
          const FactorSpec f = zsrc(k);
          const int64_t p = f.p, q = f.q;
          return f.zh ? with_flags(gargs(p, q, q, f.src, p, 1, B[k].L1i, q, 1, f.out.Q, q), 1, 0)
