@@ -532,6 +532,40 @@ void launch_conj_copy(const double* src, int64_t count_q, double* dst, const uns
   ++::qcur::g_launches;
   k_conj_copy<<<blocks, 256, 0, st>>>(src, count_q, dst, status, gate_bit);
 }
+struct RowToColJobs {
+  const double* Z[2];
+  double* Zcm[2];
+  int64_t p[2], q[2], ldz[2];
+  unsigned bit[2];
+};
+__global__ void k_row_to_col2(const __grid_constant__ RowToColJobs J, const unsigned* status) {
+  const int k = blockIdx.y;
+  if (!(*status & J.bit[k])) return;
+  const int64_t p = J.p[k], q = J.q[k], ldz = J.ldz[k];
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < p * q; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = t / p, i = t - j * p;
+    stQ(J.Zcm[k] + t * 4, ldQ(J.Z[k] + (i * ldz + j) * 4));
+  }
+}
+void launch_rowmajor_to_colmajor2(const double* const* Z, const int64_t* p, const int64_t* q, const int64_t* ldz,
+                                  double* const* Zcm, int nj, const unsigned* status, const unsigned* gate_bit,
+                                  cudaStream_t st) {
+  RowToColJobs J{};
+  int64_t most = 1;
+  for (int k = 0; k < nj; ++k) {
+    J.Z[k] = Z[k];
+    J.Zcm[k] = Zcm[k];
+    J.p[k] = p[k];
+    J.q[k] = q[k];
+    J.ldz[k] = ldz[k];
+    J.bit[k] = gate_bit[k];
+    most = p[k] * q[k] > most ? p[k] * q[k] : most;
+  }
+  int blocks = (int)((most + 255) / 256);
+  if (blocks > 592) blocks = 592;
+  ++::qcur::g_launches;
+  k_row_to_col2<<<dim3((unsigned)blocks, (unsigned)nj), 256, 0, st>>>(J, status);
+}
 void launch_rowmajor_to_colmajor(const double* Z, int64_t p, int64_t q, int64_t ldz, double* Zcm,
                                  const unsigned* status, unsigned gate_bit, cudaStream_t st) {
   int blocks = (int)((p * q + 255) / 256);

@@ -250,7 +250,13 @@ struct HqrArgs {
   unsigned gate_bit;
 };
 
-__global__ void __cluster_dims__(kRCl, 1, 1) __launch_bounds__(kHThreads, 1) k_robust_hqr(const HqrArgs A) {
+// both blocks of a factorization step in one launch: cluster b = blockIdx.x / kRCl takes A.a[b]
+struct HqrPair {
+  HqrArgs a[2];
+};
+
+__global__ void __cluster_dims__(kRCl, 1, 1) __launch_bounds__(kHThreads, 1) k_robust_hqr(const __grid_constant__ HqrPair P) {
+  const HqrArgs& A = P.a[blockIdx.x / kRCl];
   if (!(*A.status & A.gate_bit)) return;
   cg::cluster_group cl = cg::this_cluster();
   const int c = (int)cl.block_rank();
@@ -383,9 +389,31 @@ __global__ void __cluster_dims__(kRCl, 1, 1) __launch_bounds__(kHThreads, 1) k_r
 // ---------------------------------------------------------------------------
 constexpr int kSmallQ = 256, kSThreads = 256, kSWarps = kSThreads / 32, kSR = kSmallQ / 32;
 
+struct TpinvArgs {
+  double* Tcm;
+  int64_t q;
+  double* Vcm;
+  double* F;
+  int64_t ldf;
+  double cutoff_scale, cutoff_abs;
+  const unsigned* status;
+  unsigned gate_bit;
+};
+struct TpinvPair {
+  TpinvArgs a[2];
+};
+
 __global__ void __cluster_dims__(kRCl, 1, 1) __launch_bounds__(kSThreads, 1)
-    k_robust_tpinv(double* Tcm, int64_t q, double* Vcm, double* F, int64_t ldf, double cutoff_scale, double cutoff_abs,
-                   const unsigned* status, unsigned gate_bit) {
+    k_robust_tpinv(const __grid_constant__ TpinvPair P) {
+  const TpinvArgs& A = P.a[blockIdx.x / kRCl];
+  double* Tcm = A.Tcm;
+  const int64_t q = A.q;
+  double* Vcm = A.Vcm;
+  double* F = A.F;
+  const int64_t ldf = A.ldf;
+  const double cutoff_scale = A.cutoff_scale, cutoff_abs = A.cutoff_abs;
+  const unsigned* status = A.status;
+  const unsigned gate_bit = A.gate_bit;
   if (!(*status & gate_bit)) return;
   cg::cluster_group cl = cg::this_cluster();
   const int c = (int)cl.block_rank();
@@ -517,20 +545,34 @@ bool robust_qr_supported(int64_t p, int64_t q) {
   return q <= kSmallQ && p >= q && robust_hqr_smem(q) <= 200 * 1024;
 }
 
-void launch_robust_qr_pinv(double* Zcm, int64_t p, int64_t q, double* betas, double* Ycm, double* Q, int64_t ldq,
-                           double* Tcm, double* Vcm, double* F, int64_t ldf, double cutoff_scale, double cutoff_abs,
-                           const unsigned* status, unsigned gate_bit, cudaStream_t st) {
+void launch_robust_qr_pinv_multi(const RobustQrJob* J, int nj, cudaStream_t st) {
   static std::atomic<unsigned> attr{0};
   if (first_on_device(attr)) {
     cudaFuncSetAttribute(k_robust_hqr, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(k_robust_hqr, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_robust_tpinv, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   }
-  HqrArgs A{Zcm, p, q, betas, Ycm, Q, ldq, Tcm, status, gate_bit};
+  HqrPair H{};
+  TpinvPair T{};
+  size_t smem = 0;
+  for (int k = 0; k < nj; ++k) {
+    const RobustQrJob& a = J[k];
+    H.a[k] = HqrArgs{a.Zcm, a.p, a.q, a.betas, a.Ycm, a.Q, a.ldq, a.Tcm, a.status, a.gate_bit};
+    T.a[k] = TpinvArgs{a.Tcm, a.q, a.Vcm, a.F, a.ldf, a.cutoff_scale, a.cutoff_abs, a.status, a.gate_bit};
+    const size_t b = robust_hqr_smem(a.q);
+    smem = b > smem ? b : smem;
+  }
   ++::qcur::g_launches;
-  k_robust_hqr<<<kRCl, kHThreads, robust_hqr_smem(q), st>>>(A);
+  k_robust_hqr<<<kRCl * nj, kHThreads, smem, st>>>(H);
   ++::qcur::g_launches;
-  k_robust_tpinv<<<kRCl, kSThreads, 0, st>>>(Tcm, q, Vcm, F, ldf, cutoff_scale, cutoff_abs, status, gate_bit);
+  k_robust_tpinv<<<kRCl * nj, kSThreads, 0, st>>>(T);
+}
+
+void launch_robust_qr_pinv(double* Zcm, int64_t p, int64_t q, double* betas, double* Ycm, double* Q, int64_t ldq,
+                           double* Tcm, double* Vcm, double* F, int64_t ldf, double cutoff_scale, double cutoff_abs,
+                           const unsigned* status, unsigned gate_bit, cudaStream_t st) {
+  RobustQrJob j{Zcm, p, q, betas, Ycm, Q, ldq, Tcm, Vcm, F, ldf, cutoff_scale, cutoff_abs, status, gate_bit};
+  launch_robust_qr_pinv_multi(&j, 1, st);
 }
 
 }  // namespace qcur

@@ -167,6 +167,28 @@ void launch_chol_inv_cluster(const CholJob* jobs, int njobs, int64_t q, unsigned
 // robust factorization by Householder QR + one-sided Jacobi pinv of the triangular factor, both on
 // 16-CTA clusters (k_robust.cu): Q (p x q row-major), F = T^+ (q x q row-major); gated on gate_bit
 bool robust_qr_supported(int64_t p, int64_t q);
+struct RobustQrJob {
+  double* Zcm;
+  int64_t p, q;
+  double* betas;
+  double* Ycm;
+  double* Q;
+  int64_t ldq;
+  double* Tcm;
+  double* Vcm;
+  double* F;
+  int64_t ldf;
+  double cutoff_scale, cutoff_abs;
+  const unsigned* status;
+  unsigned gate_bit;
+};
+// launch_robust_qr_pinv for up to two blocks (each gated on its own bit) in two launches
+void launch_robust_qr_pinv_multi(const RobustQrJob* J, int nj, cudaStream_t st);
+// row-major -> column-major copies of up to two blocks in one launch (each gated on its bit)
+void launch_rowmajor_to_colmajor2(const double* const* Z, const int64_t* p, const int64_t* q, const int64_t* ldz,
+                                  double* const* Zcm, int nj, const unsigned* status, const unsigned* gate_bit,
+                                  cudaStream_t st);
+
 void launch_robust_qr_pinv(double* Zcm, int64_t p, int64_t q, double* betas, double* Ycm, double* Q, int64_t ldq,
                            double* Tcm, double* Vcm, double* F, int64_t ldf, double cutoff_scale, double cutoff_abs,
                            const unsigned* status, unsigned gate_bit, cudaStream_t st);

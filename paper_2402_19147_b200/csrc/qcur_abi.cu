@@ -799,6 +799,36 @@ int factor_multi(qcur_ctx* ctx, const FactorSpec* specs_in, int ns) {
     return rc;
   }
   // robust path, gated on each fail_bit (no-op launches when the fast path held)
+  static const int mode_env = [] {
+    const char* e = std::getenv("QCUR_ROBUST");
+    if (!e) return 0;
+    return std::string(e) == "jacobi" ? 1 : std::string(e) == "hh" ? 2 : 0;
+  }();
+  bool merged = mode_env == 0;
+  for (int k = 0; k < ns; ++k)
+    if (specs[k].zh || !robust_qr_supported(specs[k].p, specs[k].q)) merged = false;
+  if (merged) {  // both blocks' gated copies, Householder QRs and triangular pinvs in three launches
+    const double* Z[2];
+    double* Zc[2];
+    int64_t pp[2], qq[2];
+    unsigned bits[2];
+    RobustQrJob rj[2];
+    for (int k = 0; k < ns; ++k) {
+      const FactorSpec& f = specs[k];
+      Bufs& b = B[k];
+      Z[k] = f.src;
+      Zc[k] = b.Zcm;
+      pp[k] = f.p;
+      qq[k] = f.q;
+      bits[k] = f.fail_bit;
+      rj[k] = RobustQrJob{b.Zcm, f.p, f.q, b.betas, b.Qcm, f.out.Q, f.q, b.Tcm, b.Vcm, f.out.F, f.q,
+                          kEps * (double)(f.p > f.q ? f.p : f.q), f.cutoff_abs, status, f.fail_bit};
+    }
+    launch_rowmajor_to_colmajor2(Z, pp, qq, qq, Zc, ns, status, bits, st);
+    launch_robust_qr_pinv_multi(rj, ns, st);
+    CK_LAUNCH(ctx, "robust factor");
+    return QCUR_OK;
+  }
   for (int k = 0; k < ns; ++k) {
     const FactorSpec& f = specs[k];
     const int64_t p = f.p, q = f.q;
@@ -808,11 +838,6 @@ int factor_multi(qcur_ctx* ctx, const FactorSpec* specs_in, int ns) {
     // round 2: Householder QR and the one-sided Jacobi pinv of its triangular factor, each on a
     // 16-CTA cluster (k_robust.cu).  QCUR_ROBUST=jacobi: one-sided Jacobi on Z itself (cluster);
     // QCUR_ROBUST=hh: round 1's single-CTA Householder QR + Jacobi (340 ms per side at cfg2).
-    static const int mode_env = [] {
-      const char* e = std::getenv("QCUR_ROBUST");
-      if (!e) return 0;
-      return std::string(e) == "jacobi" ? 1 : std::string(e) == "hh" ? 2 : 0;
-    }();
     const double cutoff_scale = kEps * (double)(p > q ? p : q);
     if (mode_env == 2) {
       launch_householder_qr(b.Zcm, p, q, b.betas, b.Qcm, b.T, q, status, f.fail_bit, st);

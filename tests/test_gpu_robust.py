@@ -25,7 +25,8 @@ class forced_robust:
 
 
 @pytest.mark.parametrize("m,n,k,c,r,strategy", [(300, 260, 12, 36, 48, "length"), (1000, 1000, 10, 40, 40, "uniform"),
-                                                (1200, 1100, 30, 120, 110, "length")])
+                                                (1200, 1100, 30, 120, 110, "length"),
+                                                (1000, 900, 20, 200, 196, "length")])
 def test_forced_robust_qmcur_matches_oracle(m, n, k, c, r, strategy):
     x = lowrank(m, n, k, seed=m + k, noise=1e-3)
     plan = q.make_plan(x, strategy, k, 7, num_rows=r, num_cols=c)
@@ -55,3 +56,17 @@ def test_exact_recovery_through_robust_path():
     plan = q.make_plan(x, "length", 5, 3, num_rows=12, num_cols=12)
     f = q.qmcur(x, plan)
     assert q.cur_relative_error(x, f) <= 1e-10
+
+
+@pytest.mark.parametrize("c,r", [(200, 200), (160, 240)])
+def test_rank_deficient_large_blocks_reach_robust_path(c, r):
+    # rank 40, c, r >= 160: the Grams are singular, so the cluster Cholesky (the pipelined variant from
+    # q = 192) breaks down or the kappa guard trips, and both blocks go through the merged robust launches
+    x = lowrank(900, 800, 40, seed=2024)
+    plan = q.make_plan(x, "length", 40, 11, num_rows=r, num_cols=c)
+    f = q.qmcur(x, plan)
+    err = q.cur_relative_error(x, f)
+    rows, cols, C, U, R = O.qmcur(tuple(x.planes), plan.col_probs, plan.row_probs, c, r, 11)
+    assert np.array_equal(f.col_indices, cols) and np.array_equal(f.row_indices, rows)
+    assert O.rel_fro(tuple(f.u.planes), U) <= 1e-9
+    assert err <= 1e-10
