@@ -17,7 +17,7 @@ CSRC = HERE / "csrc"
 LIB = CSRC / "libqcur_b200.so"
 STAMP = CSRC / "libqcur_b200.so.sha256"  # hash of the sources + flags the library was built from
 SOURCES = ["qcur_abi.cu", "k_norms.cu", "k_draw.cu", "k_layout.cu", "k_qgemm.cu", "k_dense.cu", "k_synth.cu",
-           "k_chol_cluster.cu", "k_gemv.cu", "k_ozaki.cu", "k_ozaki_err.cu", "k_qsvd.cu", "k_robust.cu"]
+           "k_chol_cluster.cu", "k_gemv.cu", "k_ozaki.cu", "k_ozaki_err.cu", "k_qsvd.cu", "k_robust.cu", "k_qgemm_small.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-cudart", "static"]
 

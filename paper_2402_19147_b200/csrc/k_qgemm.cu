@@ -911,6 +911,10 @@ size_t qgemm_workspace_bytes(const GemmArgs& g) { return make_plan(g).slot_bytes
 
 void launch_qgemm(const GemmArgs& g, double* workspace, unsigned* counters, cudaStream_t st) {
   if (g.Mq <= 0 || g.Nq <= 0) return;
+  if (g.Kq > 0 && qgemm_small_ok(g)) {  // q x q products: one cluster per 32 x 32 tile (k_qgemm_small.cu)
+    launch_qgemm_small(&g, 1, st);
+    return;
+  }
   Plan pl = make_plan(g);
   pl.kp.counters = counters;
   pl.kp.slots = workspace;
@@ -924,6 +928,11 @@ void launch_qgemm(const GemmArgs& g, double* workspace, unsigned* counters, cuda
 
 void launch_qgemm_pair(const GemmArgs& g0, double* ws0, const GemmArgs& g1, double* ws1, unsigned* counters,
                        cudaStream_t st) {
+  if (qgemm_small_ok(g0) && qgemm_small_ok(g1) && g0.Kq > 0 && g1.Kq > 0 && g0.opA == g1.opA && g0.opB == g1.opB) {
+    const GemmArgs g[2] = {g0, g1};
+    launch_qgemm_small(g, 2, st);
+    return;
+  }
   static const bool no_pair = getenv("QCUR_NO_PAIR") != nullptr;  // experiments only
   const bool same = !no_pair && g0.opA == g1.opA && g0.opB == g1.opB && pick_cfg(g0.Mq, g0.Nq) == pick_cfg(g1.Mq, g1.Nq) &&
                     g0.Mq > 0 && g0.Nq > 0 && g1.Mq > 0 && g1.Nq > 0 && ws0 && ws1 && counters;

@@ -93,6 +93,10 @@ struct GemmArgs {
                         // depend on M (row blocks of a generated matrix concatenate bit for bit)
 };
 size_t qgemm_workspace_bytes(const GemmArgs& g);
+// small products (M, N, K <= 256, not whole_tiles): launch_qgemm / launch_qgemm_pair route them to
+// k_qgemm_small (no workspace or counters used)
+bool qgemm_small_ok(const GemmArgs& g);
+void launch_qgemm_small(const GemmArgs* g, int np, cudaStream_t st);
 // counters: >= 65536 zero-initialised uints owned by the caller (split-K tickets)
 void launch_qgemm(const GemmArgs& g, double* workspace, unsigned* counters, cudaStream_t st);
 // two independent products in one launch (SMs split by work); falls back to two launches
