@@ -162,10 +162,14 @@ __device__ __forceinline__ double amax4(const double4& v) {
   return fmax(fmax(fabs(v.x), fabs(v.y)), fmax(fabs(v.z), fabs(v.w)));
 }
 
-template <int L, int NT>
+// VPT: values of X per thread and pass (16: uint4 residue stores; 8: uint2 stores, half the limb
+// registers: no spills under the two-CTAs-per-SM register cap)
+template <int L, int NT, int VPT = 16>
 __global__ void __launch_bounds__(NT, 2) k_oz_xres(const double* __restrict__ X, int64_t K, int64_t ldx, int bits,
                                                    uint8_t* __restrict__ res, int64_t pitch, int64_t plane,
                                                    int* __restrict__ ex) {
+  static_assert(VPT == 16 || VPT == 8, "values per thread");
+  constexpr int NQ = VPT / 4;  // 32-byte loads per pass
   __shared__ double sh[NT / 32];
   const int64_t row = blockIdx.x;
   const double* x = X + row * ldx;
@@ -197,11 +201,11 @@ __global__ void __launch_bounds__(NT, 2) k_oz_xres(const double* __restrict__ X,
   const long long magic_bits = __double_as_longlong(kMagic);
   const f32x2 mag = dup(kMagicF), nmag = dup(-kMagicF), lmag = dup(-8388608.0f);
   uint8_t* out = res + row * pitch;
-  for (int64_t k0 = threadIdx.x * 16; k0 < pitch; k0 += NT * 16) {
-    f32x2 f[8][4];  // pair h holds values 2h, 2h+1; limbs 0..3
-    unsigned low[4];
+  for (int64_t k0 = threadIdx.x * VPT; k0 < pitch; k0 += NT * VPT) {
+    f32x2 f[VPT / 2][4];  // pair h holds values 2h, 2h+1; limbs 0..3
+    unsigned low[NQ];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < NQ; ++q) {
       double4 t = make_double4(0.0, 0.0, 0.0, 0.0);
       if (k0 + 4 * q < K) t = *reinterpret_cast<const double4*>(x + k0 + 4 * q);
       const double vv[4] = {t.x, t.y, t.z, t.w};
@@ -227,14 +231,18 @@ __global__ void __launch_bounds__(NT, 2) k_oz_xres(const double* __restrict__ X,
           f[2 * q + h][i] = fmul2(fadd2(((f32x2)lm[2 * h][i]) | ((f32x2)lm[2 * h + 1][i] << 32), lmag), sgn);
       }
     }
-    *reinterpret_cast<uint4*>(out + k0) = make_uint4(low[0], low[1], low[2], low[3]);  // p = 256
+    if constexpr (VPT == 16) *reinterpret_cast<uint4*>(out + k0) = make_uint4(low[0], low[1], low[2], low[3]);  // p = 256
+    else *reinterpret_cast<uint2*>(out + k0) = make_uint2(low[0], low[1]);
 #define OZ_PLANE(l)                                                                                     \
     if constexpr (l < L) {                                                                              \
-      unsigned w[4];                                                                                    \
-      _Pragma("unroll") for (int q = 0; q < 4; ++q) w[q] = pack_pairs(                                  \
+      unsigned w[NQ];                                                                                   \
+      _Pragma("unroll") for (int q = 0; q < NQ; ++q) w[q] = pack_pairs(                                 \
           pair_residue<l>(f[2 * q][0], f[2 * q][1], f[2 * q][2], f[2 * q][3], mag, nmag),               \
           pair_residue<l>(f[2 * q + 1][0], f[2 * q + 1][1], f[2 * q + 1][2], f[2 * q + 1][3], mag, nmag)); \
-      *reinterpret_cast<uint4*>(out + (l) * plane + k0) = make_uint4(w[0], w[1], w[2], w[3]);           \
+      if constexpr (VPT == 16)                                                                          \
+        *reinterpret_cast<uint4*>(out + (l) * plane + k0) = make_uint4(w[0], w[1], w[2], w[3]);         \
+      else                                                                                              \
+        *reinterpret_cast<uint2*>(out + (l) * plane + k0) = make_uint2(w[0], w[1]);                     \
     }
     OZ_PLANE(1) OZ_PLANE(2) OZ_PLANE(3) OZ_PLANE(4) OZ_PLANE(5) OZ_PLANE(6) OZ_PLANE(7) OZ_PLANE(8)
     OZ_PLANE(9) OZ_PLANE(10) OZ_PLANE(11) OZ_PLANE(12) OZ_PLANE(13) OZ_PLANE(14) OZ_PLANE(15)
@@ -1364,6 +1372,15 @@ bool ozaki_supported(int64_t m, int64_t n, int64_t r) {
   return m >= 1 && n >= 1 && r >= 1 && 4 * n <= 133140 && (double)oz_plan(m, n, r, kOzMaxModDefault).total <= cap;
 }
 
+// values per thread of k_oz_xres: 8 (no spills; cfg2 385.6 -> 367.5 us, ncu); QCUR_XRES_VPT=16 for A/B timing
+int xres_vpt() {
+  static const int v = [] {
+    const char* e = std::getenv("QCUR_XRES_VPT");
+    return e && std::atoi(e) == 16 ? 16 : 8;
+  }();
+  return v;
+}
+
 // Phase 1 (depends on X only; may run on a side stream): row exponents and residues of X.
 int launch_ozaki_prepare(const double* X, int64_t m, int64_t n, int64_t ldx, int64_t r, int L, void* workspace,
                          cudaStream_t st) {
@@ -1376,7 +1393,12 @@ int launch_ozaki_prepare(const double* X, int64_t m, int64_t n, int64_t ldx, int
   ++::qcur::g_launches;
   switch (L) {
     case 14: k_oz_xres<14, 256><<<(unsigned)m, 256, 0, st>>>(X, pl.K, ldx * 4, pl.bits, ares, pl.Kpitch, aplane, ex); break;
-    case 15: k_oz_xres<15, 256><<<(unsigned)m, 256, 0, st>>>(X, pl.K, ldx * 4, pl.bits, ares, pl.Kpitch, aplane, ex); break;
+    case 15:
+      if (xres_vpt() == 8)
+        k_oz_xres<15, 256, 8><<<(unsigned)m, 256, 0, st>>>(X, pl.K, ldx * 4, pl.bits, ares, pl.Kpitch, aplane, ex);
+      else
+        k_oz_xres<15, 256><<<(unsigned)m, 256, 0, st>>>(X, pl.K, ldx * 4, pl.bits, ares, pl.Kpitch, aplane, ex);
+      break;
     default: return 1;
   }
   return 0;
