@@ -982,11 +982,9 @@ __global__ void __launch_bounds__(kHB * kHB) k_oz_hcrt(const __grid_constant__ O
   const int tx = threadIdx.x % kHB, ty = threadIdx.x / kHB;
   const int t = (int)blockIdx.y;
   const int i0 = bi * kHB, j0 = bj * kHB;
-  // (a, b, sign) of the four plane products of component t
-  constexpr int kTerm[4][4][3] = {{{0, 0, 1}, {1, 1, 1}, {2, 2, 1}, {3, 3, 1}},
-                                  {{0, 1, 1}, {1, 0, -1}, {2, 3, -1}, {3, 2, 1}},
-                                  {{0, 2, 1}, {1, 3, 1}, {2, 0, -1}, {3, 1, -1}},
-                                  {{0, 3, 1}, {1, 2, -1}, {2, 1, 1}, {3, 0, -1}}};
+  // plane product u of component t is A_u^T B_(u^t) with sign -1 where bit u of nibble t of 0xAC60 is set:
+  // t = 0: + + + +,  t = 1: + - - +,  t = 2: + + - -,  t = 3: + - + -  (no runtime-indexed local table)
+  const unsigned neg = (0xAC60u >> (4 * t)) & 0xFu;
   const int iqa = (int)qa, iqb = (int)qb;
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
@@ -998,7 +996,7 @@ __global__ void __launch_bounds__(kHB * kHB) k_oz_hcrt(const __grid_constant__ O
     mbar_expect_tx(bar, (unsigned)(nb * L * kHB * kHBW));
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int a = kTerm[t][u][0], b = kTerm[t][u][1];
+      const int a = u, b = u ^ t;
       const int xd = b * iqb + j0, xm = a * iqa + i0;  // first column of the direct / mirror block
       tma_load_3d(hsm + u * L * kHB * kHBW, &tm, xd & ~15, a * iqa + i0, 0, bar);  // x = column, y = row
       if (lower_bn) tma_load_3d(hsm + (4 + u) * L * kHB * kHBW, &tm, xm & ~15, b * iqb + j0, 0, bar);
@@ -1009,8 +1007,8 @@ __global__ void __launch_bounds__(kHB * kHB) k_oz_hcrt(const __grid_constant__ O
   bool dir[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
-    const int a = kTerm[t][u][0], b = kTerm[t][u][1];
-    sg[u] = kTerm[t][u][2];
+    const int a = u, b = u ^ t;
+    sg[u] = (neg >> u) & 1u ? -1 : 1;
     dir[u] = oz_tile_computed(a * iqa + i, b * iqb + j, lower_bn);
     cd[u] = ((b * iqb + j0) & 15) + tx;  // column of the element in the direct block (row ty)
     cm[u] = ((a * iqa + i0) & 15) + ty;  // column of the element in the mirror block (row tx)
