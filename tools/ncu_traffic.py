@@ -22,8 +22,8 @@ for r in rows[2:]:
     rd = float(r[ix["dram__bytes_read.sum"]]) * SCALE[units[ix["dram__bytes_read.sum"]]]
     wr = float(r[ix["dram__bytes_write.sum"]]) * SCALE[units[ix["dram__bytes_write.sum"]]]
     base = name.split("(")[0]
-    if "k_oe_err" in base or base.rstrip(")").endswith("1>"):
-        key = "error"      # INT8 digit-slice error kernel, or the FP64 EPI_ERR GEMM
+    if "k_oe_err" in base or ("qgemm_kernel" in base and base.rstrip(")").endswith("1>")):
+        key = "error"      # INT8 digit-slice error kernel, or the FP64 EPI_ERR GEMM (qgemm_kernel<.., 1>)
     elif "k_oz_gemm" in base or "qgemm_kernel" in base:
         key = "gemm"       # INT8 modular GEMM of Y = X Q_R, or the FP64 one
     else:
