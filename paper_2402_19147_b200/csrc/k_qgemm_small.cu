@@ -72,6 +72,45 @@ __device__ __forceinline__ void qmac(Quat& c, const Quat& a, const Quat& b) {
   c.z = fma(az, b.w, c.z);
 }
 
+// the eight products acc[u][v] += op(a_u) op(b_v), issued step by step across all 32 accumulators
+// (four rounds of 32 independent FMAs instead of 32 chains of four dependent ones: at one or two
+// warps per scheduler the chains stalled on the FMA latency).  Each accumulator sees the same
+// operations in the same order as qmac: identical bits.
+template <bool CA, bool CB>
+__device__ __forceinline__ void qmac8(Quat (&acc)[2][4], const Quat (&a)[2], const Quat (&b)[4]) {
+  double A[2][4], B[4][4];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    A[u][0] = a[u].w;
+    A[u][1] = CA ? -a[u].x : a[u].x;
+    A[u][2] = CA ? -a[u].y : a[u].y;
+    A[u][3] = CA ? -a[u].z : a[u].z;
+  }
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    B[v][0] = b[v].w;
+    B[v][1] = CB ? -b[v].x : b[v].x;
+    B[v][2] = CB ? -b[v].y : b[v].y;
+    B[v][3] = CB ? -b[v].z : b[v].z;
+  }
+  // component t, step s: c_t += sg * A[ia] * B[ib]   (the Hamilton table of qmac, row by row)
+  constexpr int kIa[4][4] = {{0, 1, 2, 3}, {0, 1, 2, 3}, {0, 1, 2, 3}, {0, 1, 2, 3}};
+  constexpr int kIb[4][4] = {{0, 1, 2, 3}, {1, 0, 3, 2}, {2, 3, 0, 1}, {3, 2, 1, 0}};
+  constexpr int kSg[4][4] = {{1, -1, -1, -1}, {1, 1, 1, -1}, {1, -1, 1, 1}, {1, 1, -1, 1}};
+#pragma unroll
+  for (int st = 0; st < 4; ++st)
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        Quat& c = acc[u][v];
+        c.w = fma(kSg[0][st] * A[u][kIa[0][st]], B[v][kIb[0][st]], c.w);
+        c.x = fma(kSg[1][st] * A[u][kIa[1][st]], B[v][kIb[1][st]], c.x);
+        c.y = fma(kSg[2][st] * A[u][kIa[2][st]], B[v][kIb[2][st]], c.y);
+        c.z = fma(kSg[3][st] * A[u][kIa[3][st]], B[v][kIb[3][st]], c.z);
+      }
+}
+
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
   const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(valid ? 16 : 0) : "memory");
@@ -151,11 +190,7 @@ __global__ void __launch_bounds__(kThreadsS) k_qgemm_small(const __grid_constant
 #pragma unroll
       for (int v = 0; v < 4; ++v)
         b[v] = OPB == 0 ? ldq(Bs + (kk * (kT + 1) + tj + 8 * v) * 4) : ldq(Bs + ((tj + 8 * v) * (kKC + 1) + kk) * 4);
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        qmac<OPA != 0, OPB != 0>(acc[0][v], a[0], b[v]);
-        qmac<OPA != 0, OPB != 0>(acc[1][v], a[1], b[v]);
-      }
+      qmac8<OPA != 0, OPB != 0>(acc, a, b);
     }
     __syncthreads();  // the buffer is refilled by the next iteration's prefetch
     buf ^= 1;
