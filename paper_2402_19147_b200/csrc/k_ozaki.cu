@@ -699,6 +699,204 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------
+// Round 2: the modular GEMM on CTA pairs sharing B, with double-buffered accumulators.
+// The two CTAs of a cluster take the two 128-row halves of one 256-row unit; each loads its own
+// 128 A rows and one half of the B tile (BN / 2 rows), multicast to both, so the L2 -> SM bytes per
+// MAC equal the single-CTA kernel's (its 256-row unit reads both A halves itself).  A CTA's
+// accumulator is one M = 128 x BN block, so two of them fit TMEM (2 x 256 columns): the MMAs of
+// unit t + 1 run while the epilogue drains unit t (the single-CTA kernel's two 128-row halves fill
+// TMEM and its MMAs wait for every drain: ncu with the epilogue skipped, Gram 84 -> 58 us, X Q_R
+// 560 -> 511 us).  A stage is 16 KB of A + up to 32 KB of B: four stages.  Measured: bit-identical
+// results, no faster (Gram 82-85 us, X Q_R 588 us against 563): the drain was not what the skipped
+// epilogue saved.  Off by default (QCUR_OZ_BMC=1).
+// ---------------------------------------------------------------------------
+constexpr int OZB_STAGES = 4, OZB_A = 128 * OZ_BK, OZB_B = 256 * OZ_BK;
+constexpr int OZB_SMEM = 1024 + OZB_STAGES * (OZB_A + OZB_B) + 256;
+static_assert(OZB_SMEM <= OZ_SMEM + 4096, "B-multicast stages");
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ_THREADS, 1)
+    k_oz_gemm_bmc(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmB0,
+                  const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
+                  const __grid_constant__ OzGemm P) {
+  extern __shared__ uint8_t smem_raw[];
+  const unsigned pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+  uint8_t* smem = smem_raw + pad;
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + OZB_STAGES * OZB_A;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + OZB_STAGES * OZB_B);
+  uint64_t* empty = full + OZB_STAGES;
+  uint64_t* tfull = empty + OZB_STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;          // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int crank = (int)cluster_ctarank();
+  const int cid = (int)cluster_id_x(), ncl = (int)ncluster_x();
+  constexpr uint16_t kMask = 3;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < OZB_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 2);  // one commit from each CTA: both have consumed their copy of B
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], OZ_EPI);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tslot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();  // every CTA's barriers initialised before any multicast reaches them
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA0)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB0)) : "memory");
+      int stage = 0;
+      unsigned phase = 0;
+      for (int u = cid; u < P.total; u += ncl) {
+        int l, mb, nb;
+        const int k = unit_coords<1>(P, u, l, mb, nb, 0);
+        const OzProb& q = P.pr[k];
+        const CUtensorMap* ta = k ? &tmA1 : &tmA0;
+        const CUtensorMap* tb = k ? &tmB1 : &tmB0;  // boxes of BN / 2 rows
+        const int hb = q.BN / 2;
+        const unsigned bytes = OZB_A + q.BN * OZ_BK;  // own A + both halves of B
+        for (int kb = 0; kb < q.kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1u);
+          mbar_expect_tx(&full[stage], bytes);
+          tma_load_3d(sA + stage * OZB_A, ta, kb * OZ_BK, mb * OZ_BM + crank * (OZ_BM / 2), l, &full[stage]);
+          tma_load_3d_mc(sB + stage * OZB_B + crank * hb * OZ_BK, tb, kb * OZ_BK, nb * q.BN + crank * hb, l,
+                         &full[stage], kMask);
+          if (++stage == OZB_STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    const uint64_t adesc0 = umma_desc(smem_u32(sA)), bdesc0 = umma_desc(smem_u32(sB));
+    int stage = 0;
+    unsigned phase = 0;
+    int t = 0;
+    for (int u = cid; u < P.total; u += ncl, ++t) {
+      int l, mb, nb;
+      const OzProb& q = P.pr[unit_coords<1>(P, u, l, mb, nb, 0)];
+      const bool mine = (int64_t)mb * OZ_BM + crank * (OZ_BM / 2) < q.m;  // any valid row in this CTA's half
+      const int buf = t & 1;
+      mbar_wait(&tempty[buf], (((unsigned)t >> 1) & 1u) ^ 1u);  // the epilogue has drained unit t - 2
+      tc_fence_after();
+      const uint32_t d = tbase + (uint32_t)(buf * 256);
+      for (int kb = 0; kb < q.kblocks; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint64_t ad = adesc0 + (uint64_t)((stage * OZB_A) >> 4);
+        const uint64_t bd0 = bdesc0 + (uint64_t)((stage * OZB_B) >> 4);
+        if (elect_one_sync()) {
+          if (mine) {
+#pragma unroll
+            for (int kk = 0; kk < OZ_BK / 32; ++kk)
+              mma_i8(d, ad + (uint64_t)(kk * 2), bd0 + (uint64_t)(kk * 2), q.idesc, (kb | kk) != 0);
+          }
+          mma_commit_mc(&empty[stage], kMask);  // this CTA's copy of the stage is consumed
+        }
+        __syncwarp();
+        if (++stage == OZB_STAGES) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+      if (elect_one_sync()) mma_commit(&tfull[buf]);
+      __syncwarp();
+    }
+  } else {
+    // epilogue: warp w drains TMEM lanes 32 (w % 4) .. +31 and column part (w - 2) / 4 of OZ_EPI / 4
+    constexpr int kParts = OZ_EPI / 4;
+    const int quarter = warp & 3, cpart = (warp - 2) >> 2;
+    const int rloc = crank * (OZ_BM / 2) + quarter * 32 + lane;
+    int t = 0;
+    for (int u = cid; u < P.total; u += ncl, ++t) {
+      int l, mb, nb;
+      const OzProb& q = P.pr[unit_coords<1>(P, u, l, mb, nb, 0)];
+      const int buf = t & 1;
+      mbar_wait(&tfull[buf], ((unsigned)t >> 1) & 1u);
+      tc_fence_after();
+      const bool mine = (int64_t)mb * OZ_BM + crank * (OZ_BM / 2) < q.m;
+      if (P.exp || !mine) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
+        continue;
+      }
+      const int64_t row = (int64_t)mb * OZ_BM + rloc;
+      const int p = P.p[l];
+      const int bm = P.bm[l];
+      uint8_t* out = q.res + l * q.res_plane + row * q.res_pitch + (int64_t)nb * q.BN;
+      const bool store = row < q.m && nb < q.nblocks;
+      auto emit = [&](const uint32_t(&v)[32], int c0) {  // as k_oz_gemm's epilogue
+        uint32_t w[8];
+#pragma unroll
+        for (int z = 0; z < 8; ++z) w[z] = 0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          uint32_t r;
+          if (l == 0) {
+            r = v[i] & 255u;
+          } else {
+            const int z = (int)v[i];
+            int rr = (int)(v[i] - (uint32_t)__mulhi(z, bm) * (uint32_t)p);
+            rr += rr < 0 ? p : 0;
+            rr -= rr >= p ? p : 0;
+            r = (uint32_t)rr;
+          }
+          w[i >> 2] |= r << (8 * (i & 3));
+        }
+        if (store) {
+          *reinterpret_cast<uint4*>(out + c0) = make_uint4(w[0], w[1], w[2], w[3]);
+          if (c0 + 32 <= q.BN) *reinterpret_cast<uint4*>(out + c0 + 16) = make_uint4(w[4], w[5], w[6], w[7]);
+        }
+      };
+      const uint32_t taddr = tbase + (uint32_t)(buf * 256) + ((uint32_t)(quarter * 32) << 16);
+      const int nall = (q.BN + 31) / 32;
+      const int ch0 = cpart * nall / kParts, nch = (cpart + 1) * nall / kParts;
+      if (ch0 < nch) {
+        uint32_t va[32], vb[32];
+        tmem_ld32_async(taddr + (uint32_t)(ch0 * 32), va);
+        tmem_wait_ld();
+        for (int ch = ch0; ch < nch; ch += 2) {
+          if (ch + 1 < nch) tmem_ld32_async(taddr + (uint32_t)((ch + 1) * 32), vb);
+          emit(va, ch * 32);
+          tmem_wait_ld();
+          if (ch + 1 < nch) {
+            if (ch + 2 < nch) tmem_ld32_async(taddr + (uint32_t)((ch + 2) * 32), va);
+            emit(vb, (ch + 1) * 32);
+            tmem_wait_ld();
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase) : "memory");
+  }
+  cluster_sync_all();  // no CTA leaves while its peer can still multicast into it
+}
+
+// ---------------------------------------------------------------------------
 // CRT: Z from its residues, Y = 2^-(ex_i + fx_j) Z.  S = sum_l ((r_l w_l) mod p_l) (M / p_l)
 // in 128-bit integers (S < L M), Z = S mod M centred; four outputs per thread.
 // ---------------------------------------------------------------------------
@@ -709,7 +907,21 @@ struct OzCrt {
   unsigned mi[kOzMaxMod][4];  // M / p_l as four 32-bit limbs, least significant first
   unsigned long long M_lo, M_hi;
   double Md;
+  double Mr;  // 1 / Md: the quotient estimate by one multiply (corrected both ways below)
 };
+
+// Exact small-integer <-> float conversions on the FMA / integer pipes instead of the conversion
+// unit (I2F / F2I run at a quarter of the FMA rate or less; the CRT kernels issued 120 of them per
+// thread, ncu: 40 % of k_oz_crt's time).
+__device__ __forceinline__ float byte_to_float(unsigned word, int h) {  // byte h of word, exact
+  return __uint_as_float(__byte_perm(word, 0x4B000000u, 0x7650u | (unsigned)h)) - 8388608.0f;
+}
+__device__ __forceinline__ unsigned small_float_to_uint(float t) {  // t integer-valued in [0, 2^23)
+  return __float_as_uint(t + 8388608.0f) - 0x4B000000u;
+}
+__device__ __forceinline__ float small_int_to_float(int v) {  // |v| < 2^22, exact
+  return __int_as_float(0x4B400000 + v) - 12582912.0f;
+}
 
 // S = sum_l t_l (M / p_l) with t_l = (r_l w_l) mod p_l < 256: the limb products t * mi[k] < 2^40
 // accumulate in four 64-bit columns without overflow (L <= 16), carries are resolved once.
@@ -730,10 +942,10 @@ __global__ void __launch_bounds__(256) k_oz_crt(const uint8_t* __restrict__ res,
     const float P = c.P[l], pinv = c.pinv[l];
 #pragma unroll
     for (int h = 0; h < 4; ++h) {
-      const float rw = (float)((r4 >> (8 * h)) & 0xffu) * c.w[l];  // < 2^16, exact
+      const float rw = byte_to_float(r4, h) * c.w[l];  // < 2^16, exact
       float t = fmaf(-(fmaf(rw, pinv, kMagicF) - kMagicF), P, rw);
       t = t < 0.0f ? t + P : t;
-      const unsigned tt = (unsigned)t;
+      const unsigned tt = small_float_to_uint(t);
 #pragma unroll
       for (int k = 0; k < 4; ++k) col[h][k] += (unsigned long long)tt * c.mi[l][k];
     }
@@ -753,7 +965,7 @@ __global__ void __launch_bounds__(256) k_oz_crt(const uint8_t* __restrict__ res,
     const unsigned long long hi = (c2 & 0xffffffffull) | (c3 << 32);
     unsigned __int128 S = ((unsigned __int128)hi << 64) | lo;
     const double sd = (double)hi * 18446744073709551616.0 + (double)lo;
-    long long q = (long long)floor(sd / c.Md);
+    long long q = (long long)floor(sd * c.Mr);
     q = q < 0 ? 0 : q;
     S -= M * (unsigned long long)q;
     if ((__int128)S < 0) S += M;  // the estimate was one too large
@@ -893,10 +1105,10 @@ __device__ __forceinline__ __int128 crt_one(const uint8_t* rp, int64_t plane, co
   unsigned long long col[4] = {0, 0, 0, 0};
 #pragma unroll
   for (int l = 0; l < L; ++l) {
-    const float rw = (float)rp[l * plane] * c.w[l];
+    const float rw = small_int_to_float((int)rp[l * plane]) * c.w[l];
     float t = fmaf(-(fmaf(rw, c.pinv[l], kMagicF) - kMagicF), c.P[l], rw);
     t = t < 0.0f ? t + c.P[l] : t;
-    const unsigned tt = (unsigned)t;
+    const unsigned tt = small_float_to_uint(t);
 #pragma unroll
     for (int k = 0; k < 4; ++k) col[k] += (unsigned long long)tt * c.mi[l][k];
   }
@@ -907,7 +1119,7 @@ __device__ __forceinline__ __int128 crt_one(const uint8_t* rp, int64_t plane, co
   const unsigned long long hi = (c2 & 0xffffffffull) | (c3 << 32);
   unsigned __int128 S = ((unsigned __int128)hi << 64) | lo;
   const unsigned __int128 M = ((unsigned __int128)c.M_hi << 64) | c.M_lo;
-  long long q = (long long)floor(((double)hi * 18446744073709551616.0 + (double)lo) / c.Md);
+  long long q = (long long)floor(((double)hi * 18446744073709551616.0 + (double)lo) * c.Mr);
   q = q < 0 ? 0 : q;
   S -= M * (unsigned long long)q;
   if ((__int128)S < 0) S += M;
@@ -1022,14 +1234,14 @@ __global__ void __launch_bounds__(kHB * kHB) k_oz_hcrt(const __grid_constant__ O
     for (int u = 0; u < 4; ++u) sum += sg[u] * (int)(dir[u] ? blk(u, l, ty, cd[u]) : blk(4 + u, l, tx, cm[u]));
     const float P = c.P[l], pinv = c.pinv[l];
     // (sum mod p) w mod p, exact in FP32: |sum| < 1024, (sum mod p) w < 2^16
-    const float sf = (float)sum;
+    const float sf = small_int_to_float(sum);
     float sm = fmaf(-(fmaf(sf, pinv, kMagicF) - kMagicF), P, sf);
     sm = sm < 0.0f ? sm + P : sm;
     sm = sm >= P ? sm - P : sm;
     const float rw = sm * c.w[l];
     float tq = fmaf(-(fmaf(rw, pinv, kMagicF) - kMagicF), P, rw);
     tq = tq < 0.0f ? tq + P : tq;
-    const unsigned tt = (unsigned)tq;
+    const unsigned tt = small_float_to_uint(tq);
 #pragma unroll
     for (int k = 0; k < 4; ++k) col[k] += (unsigned long long)tt * c.mi[l][k];
   }
@@ -1042,7 +1254,7 @@ __global__ void __launch_bounds__(kHB * kHB) k_oz_hcrt(const __grid_constant__ O
   const unsigned long long lo = (w0 & 0xffffffffull) | (c1 << 32);
   const unsigned long long hi = (c2 & 0xffffffffull) | (c3 << 32);
   unsigned __int128 S = ((unsigned __int128)hi << 64) | lo;
-  long long q = (long long)floor(((double)hi * 18446744073709551616.0 + (double)lo) / c.Md);
+  long long q = (long long)floor(((double)hi * 18446744073709551616.0 + (double)lo) * c.Mr);
   q = q < 0 ? 0 : q;
   S -= M * (unsigned long long)q;
   if ((__int128)S < 0) S += M;
@@ -1163,6 +1375,7 @@ OzCrt oz_crt(int L) {
   c.M_lo = (unsigned long long)M;
   c.M_hi = (unsigned long long)(M >> 64);
   c.Md = (double)c.M_hi * 18446744073709551616.0 + (double)c.M_lo;
+  c.Mr = 1.0 / c.Md;
   for (int l = 0; l < L; ++l) {
     const int p = kOzModuli[l];
     const unsigned __int128 mi = M / (unsigned)p;
@@ -1429,6 +1642,7 @@ int launch_ozaki_prep_b(int64_t m, int64_t n, const double* B, int64_t r, int64_
 // B residues, and where the residue bytes of the product go
 struct OzJob {
   CUtensorMap ta, tb;
+  CUtensorMap tbh;  // B in boxes of BN / 2 rows (k_oz_gemm_bmc: each CTA of a pair loads one half)
   OzProb pr;
 };
 
@@ -1447,7 +1661,8 @@ bool oz_job(OzJob& j, const OzPlan& pl, int64_t m, const uint8_t* ares, int64_t 
             int L, uint8_t* res) {
   // A planes are m rows of arow_stride bytes (Kpitch for X, 4 Kpitch for the rows 4j of E(A))
   if (!oz_map_strided(&j.ta, ares, pl.K, m, arow_stride, arow_stride * m, L, OZ_BM / 2) ||
-      !oz_map(&j.tb, bres, pl.K, pl.N, pl.Kpitch, L, (int)pl.BN))
+      !oz_map(&j.tb, bres, pl.K, pl.N, pl.Kpitch, L, (int)pl.BN) ||
+      !oz_map(&j.tbh, bres, pl.K, pl.N, pl.Kpitch, L, (int)pl.BN / 2))
     return false;
   OzProb& q = j.pr;
   q.m = m;
@@ -1497,6 +1712,31 @@ void oz_launch_gemm(const OzJob* jobs, int nj, int L, cudaStream_t st) {
   const bool any_lower = jobs[0].pr.lower || (nj > 1 && jobs[1].pr.lower);
   const int CL = any_lower ? 1 : cl_env == 1 || cl_env == 2 ? cl_env : kOzCluster;
   const OzJob& j1 = nj > 1 ? jobs[1] : jobs[0];
+  static const int bmc_env = [] {  // QCUR_OZ_BMC=1: the B-multicast pair kernel (correct, bit-identical; measured
+    const char* e = std::getenv("QCUR_OZ_BMC");  // no faster: Gram 84 -> 82-85 us, X Q_R 563 -> 588 us)
+    return e ? std::atoi(e) : 0;
+  }();
+  if (bmc_env && cl_env == 0) {
+    static std::atomic<unsigned> battr{0};
+    static int max_clusters = 0;
+    cudaLaunchConfig_t cfg{};
+    cfg.blockDim = dim3(OZ_THREADS);
+    cfg.dynamicSmemBytes = OZB_SMEM;
+    cfg.stream = st;
+    if (first_on_device(battr)) {
+      cudaFuncSetAttribute(k_oz_gemm_bmc, cudaFuncAttributeMaxDynamicSharedMemorySize, OZB_SMEM);
+      int nc = 0;
+      cfg.gridDim = dim3((unsigned)(oz_sms() / 2 * 2));
+      max_clusters = (cudaOccupancyMaxActiveClusters(&nc, k_oz_gemm_bmc, &cfg) == cudaSuccess && nc > 0) ? nc
+                                                                                                         : oz_sms() / 2;
+      (void)cudaGetLastError();
+    }
+    const int ncl = P.total < max_clusters ? P.total : max_clusters;
+    cfg.gridDim = dim3((unsigned)(2 * ncl));
+    ++::qcur::g_launches;
+    cudaLaunchKernelEx(&cfg, k_oz_gemm_bmc, jobs[0].ta, jobs[0].tbh, j1.ta, j1.tbh, P);
+    return;
+  }
   ++::qcur::g_launches;
   if (CL == 1) {
     const int grid = P.total < oz_sms() ? P.total : oz_sms();

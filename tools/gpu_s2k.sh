@@ -1,0 +1,9 @@
+# CRT kernels without conversion-unit instructions: INT8 tests + parity, launch list, bench
+cd $GRAFT_REPO_ROOT
+TAG=${1:-s2k}
+timeout 900 python -m pytest tests/test_gpu_int8.py tests/test_gpu_parity.py tests/test_gpu_baseline_parity.py tests/test_gpu_golden.py -q -x -p no:cacheprovider > gpurun_out/${TAG}_tests.log 2>&1
+echo "rc=$?" >> gpurun_out/${TAG}_tests.log
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
+    --log-file gpurun_out/${TAG}_ll.csv python tools/profile_step.py cfg2 > gpurun_out/${TAG}_ll.log 2>&1
+python tools/launch_list.py gpurun_out/${TAG}_ll.csv --order > gpurun_out/${TAG}_ll.txt
+timeout 600 python tools/chol_ab.py cfg1 cfg4 cfg3:128 cfg2 > gpurun_out/${TAG}_ab.jsonl 2> gpurun_out/${TAG}_ab.err
