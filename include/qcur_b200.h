@@ -272,8 +272,11 @@ int qcur_factor(qcur_ctx* ctx, const double* src_dev, int zh, int64_t p, int64_t
  * qcur_profile(ctx, 1) records CUDA events on the context stream at the end of
  * every pipeline phase (length, draw, gather, factor_c, factor_r, gemm_xq,
  * core_u, cu, error); qcur_profile_read synchronises and writes
- * "phase:total_ms:count;..." into buf.  qcur_launch_count is the number of
- * kernels this library has launched in the process. */
+ * "phase:total_ms:count;..." into buf.  qcur_profile(ctx, 2): the same, for a
+ * call captured into a CUDA graph (the phase events become external event
+ * nodes); the marks persist, so call qcur_profile_read after every replay.
+ * qcur_launch_count is the number of kernels this library has launched in the
+ * process. */
 int qcur_profile(qcur_ctx* ctx, int on);
 int qcur_profile_read(qcur_ctx* ctx, char* buf, size_t len);
 unsigned long long qcur_launch_count(void);

@@ -272,8 +272,10 @@ class Device:
     def info(self) -> int:
         return int(self.lib.qcur_last_info(self.handle))
 
-    def profile(self, on: bool) -> None:
-        self.call("qcur_profile", 1 if on else 0)
+    def profile(self, on) -> None:
+        """on: False/0 off, True/1 phase events between direct launches, 2 events captured into a
+        CUDA graph (kept across replays: call profile_read after every replay)."""
+        self.call("qcur_profile", int(on) if not isinstance(on, bool) else (1 if on else 0))
 
     def profile_read(self) -> dict[str, tuple[float, int]]:
         """{phase: (total_ms, count)} accumulated since profile(True)."""

@@ -164,14 +164,17 @@ __device__ __forceinline__ double amax4(const double4& v) {
 
 // VPT: values of X per thread and pass (16: uint4 residue stores; 8: uint2 stores, half the limb
 // registers: no spills under the two-CTAs-per-SM register cap)
-template <int L, int NT, int VPT = 16>
-__global__ void __launch_bounds__(NT, 2) k_oz_xres(const double* __restrict__ X, int64_t K, int64_t ldx, int bits,
-                                                   uint8_t* __restrict__ res, int64_t pitch, int64_t plane,
-                                                   int* __restrict__ ex) {
+// Rows are taken grid-stride (row = blockIdx.x, += gridDim.x up to M): with QCUR_XRES_RESERVE=n the
+// side-stream launch uses one 512-thread CTA per SM on all but n SMs, so the latency-bound main-stream
+// kernels beside it (the draws, the cluster Cholesky) find whole SMs free (measured: no net gain).
+template <int L, int NT, int VPT = 16, int MINB = 2>
+__global__ void __launch_bounds__(NT, MINB) k_oz_xres(const double* __restrict__ X, int64_t K, int64_t ldx, int bits,
+                                                      uint8_t* __restrict__ res, int64_t pitch, int64_t plane,
+                                                      int* __restrict__ ex, int64_t M) {
   static_assert(VPT == 16 || VPT == 8, "values per thread");
   constexpr int NQ = VPT / 4;  // 32-byte loads per pass
   __shared__ double sh[NT / 32];
-  const int64_t row = blockIdx.x;
+  for (int64_t row = blockIdx.x; row < M; row += gridDim.x) {
   const double* x = X + row * ldx;
   double mx = 0.0;
   int64_t k = threadIdx.x * 4;
@@ -248,6 +251,8 @@ __global__ void __launch_bounds__(NT, 2) k_oz_xres(const double* __restrict__ X,
     OZ_PLANE(9) OZ_PLANE(10) OZ_PLANE(11) OZ_PLANE(12) OZ_PLANE(13) OZ_PLANE(14) OZ_PLANE(15)
     OZ_PLANE(16) OZ_PLANE(17) OZ_PLANE(18) OZ_PLANE(19)
 #undef OZ_PLANE
+  }
+  __syncthreads();  // sh is rewritten by the next row's maximum
   }
 }
 
@@ -1583,6 +1588,18 @@ bool ozaki_supported(int64_t m, int64_t n, int64_t r) {
   return m >= 1 && n >= 1 && r >= 1 && 4 * n <= 133140 && (double)oz_plan(m, n, r, kOzMaxModDefault).total <= cap;
 }
 
+// SMs the side-stream residues of X leave free for the main stream (QCUR_XRES_RESERVE=n; default 0: one
+// 256-thread CTA per row, two per SM, on every SM).  Measured at cfg2 with n = 28: the graph's draw phase
+// 191 -> 121 us, but the residues then stretch over the factorization (1.09 -> 1.17 ms): one at a time
+// 298 -> 293 approx/s, cfg1 in flight 6066 -> 5645, cfg4 4534 -> 4276; so off.
+int xres_reserve() {
+  static const int v = [] {
+    const char* e = std::getenv("QCUR_XRES_RESERVE");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
 // values per thread of k_oz_xres: 8 (no spills; cfg2 385.6 -> 367.5 us, ncu); QCUR_XRES_VPT=16 for A/B timing
 int xres_vpt() {
   static const int v = [] {
@@ -1603,13 +1620,19 @@ int launch_ozaki_prepare(const double* X, int64_t m, int64_t n, int64_t ldx, int
   const int64_t aplane = m * pl.Kpitch;
   ++::qcur::g_launches;
   switch (L) {
-    case 14: k_oz_xres<14, 256><<<(unsigned)m, 256, 0, st>>>(X, pl.K, ldx * 4, pl.bits, ares, pl.Kpitch, aplane, ex); break;
-    case 15:
-      if (xres_vpt() == 8)
-        k_oz_xres<15, 256, 8><<<(unsigned)m, 256, 0, st>>>(X, pl.K, ldx * 4, pl.bits, ares, pl.Kpitch, aplane, ex);
-      else
-        k_oz_xres<15, 256><<<(unsigned)m, 256, 0, st>>>(X, pl.K, ldx * 4, pl.bits, ares, pl.Kpitch, aplane, ex);
+    case 14: k_oz_xres<14, 256><<<(unsigned)m, 256, 0, st>>>(X, pl.K, ldx * 4, pl.bits, ares, pl.Kpitch, aplane, ex, m); break;
+    case 15: {
+      const int reserve = xres_reserve();
+      if (reserve > 0 && m > oz_sms() - reserve) {
+        const int grid = oz_sms() - reserve;
+        k_oz_xres<15, 512, 8, 1><<<(unsigned)grid, 512, 0, st>>>(X, pl.K, ldx * 4, pl.bits, ares, pl.Kpitch, aplane, ex, m);
+      } else if (xres_vpt() == 8) {
+        k_oz_xres<15, 256, 8><<<(unsigned)m, 256, 0, st>>>(X, pl.K, ldx * 4, pl.bits, ares, pl.Kpitch, aplane, ex, m);
+      } else {
+        k_oz_xres<15, 256><<<(unsigned)m, 256, 0, st>>>(X, pl.K, ldx * 4, pl.bits, ares, pl.Kpitch, aplane, ex, m);
+      }
       break;
+    }
     default: return 1;
   }
   return 0;
@@ -1831,10 +1854,10 @@ int launch_ozaki_pair(const double* const* X, const int64_t* m, const int64_t* n
     ++::qcur::g_launches;
     if (L == 14)
       k_oz_xres<14, 256><<<(unsigned)m[k], 256, 0, st>>>(X[k], pl[k].K, ldx[k] * 4, pl[k].bits, ares, pl[k].Kpitch,
-                                                         m[k] * pl[k].Kpitch, ex);
+                                                         m[k] * pl[k].Kpitch, ex, m[k]);
     else
       k_oz_xres<15, 256><<<(unsigned)m[k], 256, 0, st>>>(X[k], pl[k].K, ldx[k] * 4, pl[k].bits, ares, pl[k].Kpitch,
-                                                         m[k] * pl[k].Kpitch, ex);
+                                                         m[k] * pl[k].Kpitch, ex, m[k]);
     bj.j[k] = OzBColJob{B[k], n[k], r[k], ldb[k], pl[k].Kpitch, pl[k].N * pl[k].Kpitch, conjT[k], pl[k].bits,
                         reinterpret_cast<int*>(ws[k] + pl[k].off_fx), ws[k] + pl[k].off_bres};
     rmax = r[k] > rmax ? r[k] : rmax;

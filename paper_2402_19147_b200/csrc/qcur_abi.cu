@@ -30,6 +30,8 @@ constexpr size_t kSeriesTickets = 2 * 65536, kCounterWords = 2 * 65536 + 64;  //
 // pipeline phases; harvested (after a sync) by qcur_profile_read.
 struct Profiler {
   bool on = false;
+  bool keep = false;  // qcur_profile(ctx, 2): marks captured into a CUDA graph persist across harvests
+                      // (each replay re-records the same events; harvest after every replay)
   std::vector<cudaEvent_t> pool;
   size_t used = 0;
   std::vector<std::pair<std::string, cudaEvent_t>> marks;  // phase name ends at this event
@@ -98,22 +100,29 @@ struct qcur_ctx {
   std::vector<cudaEvent_t> lane_ev;
   cudaEvent_t ev_bfork = nullptr;
 
-  // mark the end of a named phase (no-op unless profiling)
+  // mark the end of a named phase (no-op unless profiling).  Inside a stream capture the record
+  // becomes an external event node of the graph, so replays time the phases as the graph runs them.
+  void record(cudaEvent_t e) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(stream, &cs);
+    if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(e, stream, cudaEventRecordExternal);
+    else cudaEventRecord(e, stream);
+  }
   void mark(const char* name) {
     if (!prof.on) return;
     if (!prof.start) {
       prof.start = prof.next();
-      cudaEventRecord(prof.start, stream);
+      record(prof.start);
     }
     cudaEvent_t e = prof.next();
-    cudaEventRecord(e, stream);
+    record(e);
     prof.marks.emplace_back(name, e);
   }
   void mark_begin() {
     if (!prof.on) return;
     if (!prof.start) {
       prof.start = prof.next();
-      cudaEventRecord(prof.start, stream);
+      record(prof.start);
     }
   }
   void harvest() {
@@ -126,6 +135,7 @@ struct qcur_ctx {
       a.second += 1;
       prev = mk.second;
     }
+    if (prof.keep) return;
     prof.marks.clear();
     prof.start = nullptr;
     prof.used = 0;
@@ -1815,6 +1825,7 @@ int qcur_profile(qcur_ctx* ctx, int on) {
   ctx->prof.used = 0;
   ctx->prof.acc.clear();
   ctx->prof.on = on != 0;
+  ctx->prof.keep = on == 2;
   return QCUR_OK;
 }
 
