@@ -849,6 +849,12 @@ def main() -> None:
         extra_phase["gather_GBps"] = counts["gather_bytes"] / (per_approx["gather"] * 1e-3) / 1e9
     extra_phase["gemm_xq_TFps"] = counts["gemm_xq_flop"] / (per_approx.get("gemm_xq", float("nan")) * 1e-3) / 1e12
     extra_phase["error_TFps"] = counts["error_flop"] / (per_approx.get("error", float("nan")) * 1e-3) / 1e12
+    gp = graph_phases if isinstance(graph_phases, dict) else {}
+    if isinstance(gp.get("length"), float) and gp["length"] > 0:  # the same rates as the graph replays run them
+        extra_phase["length_GBps_in_graph"] = counts["length_bytes"] / (gp["length"] * 1e-3) / 1e9
+        extra_phase["length_frac_hbm_in_graph"] = extra_phase["length_GBps_in_graph"] / (hbm_peak or 6544.3)
+    if isinstance(gp.get("gather"), float) and gp["gather"] > 0:
+        extra_phase["gather_GBps_in_graph"] = counts["gather_bytes"] / (gp["gather"] * 1e-3) / 1e9
 
     # --- e2e through the public API with pinned host buffers ---
     e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
