@@ -925,6 +925,14 @@ int qmcur_core(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, int64_t c, 
 // overlaps the draws and factorizations; the main stream joins before the GEMM.  Returns the
 // workspace holding the residues, or nullptr when the FP64 path will be used.
 void* int8_fork_prepare(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, int64_t r, int* rc);
+// QCUR_XRES_FORK=draw: the residues of X fork after the draws instead of after the length pass
+bool xres_fork_after_draw() {
+  static const bool v = [] {
+    const char* e = std::getenv("QCUR_XRES_FORK");
+    return e && std::string(e) == "draw";
+  }();
+  return v;
+}
 
 // Host destinations for qcur_qmcur_host (planar, the reference's QMatrix layout).
 struct HostOut {
@@ -989,12 +997,17 @@ int qmcur_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, const doubl
   if (!jobs[0].work || !jobs[1].work) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (draw)");
   int rc = QCUR_OK;
   void* oz = oz_pre;
-  if (!oz && core == QCUR_CORE_PROJECTION && m >= c && n >= r) {
+  const bool fork_late = xres_fork_after_draw();
+  if (!oz && !fork_late && core == QCUR_CORE_PROJECTION && m >= c && n >= r) {
     oz = int8_fork_prepare(ctx, X, m, n, r, &rc);
     if (rc) return rc;
   }
   if (!launch_draw(jobs, 2, ctx->status_dev, st))
     return ctx->fail(QCUR_E_PARAMETER, "draw: axis longer than 2^30 entries");
+  if (!oz && fork_late && core == QCUR_CORE_PROJECTION && m >= c && n >= r) {
+    oz = int8_fork_prepare(ctx, X, m, n, r, &rc);  // the draws' two CTAs get their SMs first
+    if (rc) return rc;
+  }
   ctx->mark("draw");
   CK_LAUNCH(ctx, "draw");
   // 2. gathers (quat.py:215-225)
@@ -1730,7 +1743,8 @@ int qcur_approx(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int st
   }
   // the residues of X fork after the length pass: overlapping it (both HBM-bound) gained nothing,
   // overlapping the latency-bound draws and factorizations does
-  if (!rc && core == QCUR_CORE_PROJECTION && m >= c && n >= r) oz = int8_fork_prepare(ctx, x_dev, m, n, r, &rc);
+  if (!rc && !xres_fork_after_draw() && core == QCUR_CORE_PROJECTION && m >= c && n >= r)
+    oz = int8_fork_prepare(ctx, x_dev, m, n, r, &rc);
   if (!rc) rc = qmcur_impl(ctx, x_dev, m, n, colp, rowp, c, r, state, J, I, C, U, R, core, nullptr, oz);
   if (!rc) rc = error_impl(ctx, x_dev, m, n, C, c, U, R, r, psnr_scale, err4);
   if (ctx->prio) {
