@@ -781,17 +781,15 @@ def main() -> None:
                 ga.run(gx, cfg["strategy"], cfg["plan_seed"], psnr_scale)  # sizes the workspace
             torch.cuda.synchronize()
             dev.profile(2)
-            gg = torch.cuda.CUDAGraph()
             with torch.cuda.stream(lanes[0][3]):
-                with torch.cuda.graph(gg):
-                    ga.run(gx, cfg["strategy"], cfg["plan_seed"], psnr_scale)
-            for _ in range(nprof):
-                gg.replay()
-                torch.cuda.synchronize()
-                gph = dev.profile_read()
+                ga.capture(gx, cfg["strategy"], cfg["plan_seed"], psnr_scale)
+                for _ in range(nprof):
+                    ga.run(gx, cfg["strategy"], cfg["plan_seed"], psnr_scale, graph=True)
+                    torch.cuda.synchronize()
+                    gph = dev.profile_read()
             dev.profile(False)
             graph_phases = {k: v[0] / max(v[1], 1) for k, v in gph.items()}
-            del gg
+            ga._drop_graph()
         except Exception as exc:  # pragma: no cover - measurement extra, never fatal
             dev.profile(False)
             graph_phases = {"unavailable": str(exc)[:200]}

@@ -277,6 +277,15 @@ int qcur_factor(qcur_ctx* ctx, const double* src_dev, int zh, int64_t p, int64_t
  * nodes); the marks persist, so call qcur_profile_read after every replay.
  * qcur_launch_count is the number of kernels this library has launched in the
  * process. */
+/* CUDA graphs of captured calls with node priorities (the main chain high, the side stream's
+ * residues of X low), instantiated with cudaGraphInstantiateFlagUseNodePriority:
+ * qcur_graph_begin starts capturing the context stream (not the legacy default stream), the
+ * captured ABI calls follow, qcur_graph_end closes the capture and returns the executable graph,
+ * qcur_graph_launch replays it on the context stream, qcur_graph_destroy frees it. */
+int qcur_graph_begin(qcur_ctx* ctx);
+int qcur_graph_end(qcur_ctx* ctx, void** exec_out);
+int qcur_graph_launch(qcur_ctx* ctx, void* exec);
+int qcur_graph_destroy(void* exec);
 int qcur_profile(qcur_ctx* ctx, int on);
 int qcur_profile_read(qcur_ctx* ctx, char* buf, size_t len);
 unsigned long long qcur_launch_count(void);

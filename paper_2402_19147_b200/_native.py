@@ -51,6 +51,7 @@ EXPORTS = (
     "qcur_synth_lowrank_rows", "qcur_synth_normals", "qcur_xq", "qcur_complex_adjoint", "qcur_approx_batched", "qcur_colsums_seq_ex", "qcur_series_inv", "qcur_qmcur_ex", "qcur_qmcur_host",
     "qcur_project_observed", "qcur_complete_sweep", "qcur_cur_given", "qcur_qgemv",
     "qcur_upload_length", "qcur_status_async", "qcur_status_map",
+    "qcur_graph_begin", "qcur_graph_end", "qcur_graph_launch", "qcur_graph_destroy",
 )
 
 _c_dp = ctypes.c_void_p
@@ -128,6 +129,10 @@ def load_library() -> ctypes.CDLL:
             "qcur_fp64_peak_tflops": (ctypes.c_double, [_c_dp]),
             "qcur_int8_peak_tops": (ctypes.c_double, [_c_dp]),
             "qcur_profile": (ctypes.c_int, [_c_dp, ctypes.c_int]),
+            "qcur_graph_begin": (ctypes.c_int, [_c_dp]),
+            "qcur_graph_end": (ctypes.c_int, [_c_dp, ctypes.POINTER(ctypes.c_void_p)]),
+            "qcur_graph_launch": (ctypes.c_int, [_c_dp, _c_dp]),
+            "qcur_graph_destroy": (ctypes.c_int, [_c_dp]),
             "qcur_profile_read": (ctypes.c_int, [_c_dp, ctypes.c_char_p, ctypes.c_size_t]),
             "qcur_launch_count": (ctypes.c_ulonglong, []),
             "qcur_pairwise_host": (ctypes.c_int, [_c_dp, _i64, ctypes.POINTER(ctypes.c_double)]),

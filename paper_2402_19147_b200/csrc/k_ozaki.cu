@@ -1522,6 +1522,13 @@ void oz_planes_launch(const OzPlaneJob* jobs, int n, int L, cudaStream_t st) {
 
 int ozaki_max_moduli() { return kOzMaxMod; }
 
+// the residues of X run on the context's low-priority side stream: a captured graph gives their nodes
+// the low priority explicitly (graph replays otherwise run every node at the launch stream's priority)
+bool ozaki_side_kernel(const void* f) {
+  return f == (const void*)k_oz_xres<15, 256, 8, 2> || f == (const void*)k_oz_xres<15, 256, 16, 2> ||
+         f == (const void*)k_oz_xres<14, 256, 16, 2> || f == (const void*)k_oz_xres<15, 512, 8, 1>;
+}
+
 size_t ozaki_herm_workspace_bytes(int64_t p, int64_t qa, int64_t qb, int same) {
   return oz_hplan(p, qa, qb, kOzMaxModDefault, same != 0).total + 1024;
 }

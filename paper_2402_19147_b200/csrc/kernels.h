@@ -254,6 +254,7 @@ int launch_ozaki_multiply(int64_t m, int64_t n, int64_t r, double* Y, int64_t ld
 // INT8 GEMM launch, by the 16 real plane products (no Hamilton expansion); ldc in quaternions
 size_t ozaki_herm_workspace_bytes(int64_t p, int64_t qa, int64_t qb, int same);
 bool ozaki_herm_supported(int64_t p, int64_t qa, int64_t qb);
+bool ozaki_side_kernel(const void* f);  // kernels of the low-priority side stream (graph node priorities)
 int launch_ozaki_pair(const double* const* X, const int64_t* m, const int64_t* n, const int64_t* ldx,
                       const double* const* B, const int64_t* r, const int64_t* ldb, const int* conjT, double* const* Y,
                       const int64_t* ldy, int np, int L, void* const* workspace, cudaStream_t st);

@@ -1361,6 +1361,62 @@ int qcur_set_stream(qcur_ctx* ctx, void* s) {
   return QCUR_OK;
 }
 
+// Native CUDA graphs of a captured ABI call (bench / DeviceApprox graph replays).  Replays of a graph
+// run every kernel at the priority of the stream they are launched into unless the graph is
+// instantiated with node priorities: the capture is closed here, every kernel node gets the
+// context's high priority except the side stream's residues of X (low), and the graph is
+// instantiated with cudaGraphInstantiateFlagUseNodePriority, so the latency-bound main chain (the
+// draws, the cluster Cholesky) is scheduled ahead of the residue CTAs as in direct launches.
+int qcur_graph_begin(qcur_ctx* ctx) {
+  DeviceGuard device_guard_(ctx);
+  if (!ctx) return QCUR_E_PARAMETER;
+  cudaError_t e = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal);
+  return e == cudaSuccess ? QCUR_OK : ctx->cuda_fail(e, "graph capture begin");
+}
+
+int qcur_graph_end(qcur_ctx* ctx, void** exec_out) {
+  DeviceGuard device_guard_(ctx);
+  if (!ctx || !exec_out) return QCUR_E_PARAMETER;
+  *exec_out = nullptr;
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+  if (e != cudaSuccess) return ctx->cuda_fail(e, "graph capture end");
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  size_t n = 0;
+  cudaGraphGetNodes(g, nullptr, &n);
+  std::vector<cudaGraphNode_t> nodes(n);
+  if (n) cudaGraphGetNodes(g, nodes.data(), &n);
+  for (cudaGraphNode_t node : nodes) {
+    cudaGraphNodeType t;
+    if (cudaGraphNodeGetType(node, &t) != cudaSuccess || t != cudaGraphNodeTypeKernel) continue;
+    cudaKernelNodeParams kp{};
+    if (cudaGraphKernelNodeGetParams(node, &kp) != cudaSuccess) continue;
+    cudaLaunchAttributeValue v{};
+    v.priority = ozaki_side_kernel(kp.func) ? lo : hi;
+    cudaGraphKernelNodeSetAttribute(node, cudaLaunchAttributePriority, &v);
+  }
+  (void)cudaGetLastError();
+  cudaGraphExec_t ex = nullptr;
+  e = cudaGraphInstantiateWithFlags(&ex, g, cudaGraphInstantiateFlagUseNodePriority);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return ctx->cuda_fail(e, "graph instantiate");
+  *exec_out = ex;
+  return QCUR_OK;
+}
+
+int qcur_graph_launch(qcur_ctx* ctx, void* exec) {
+  DeviceGuard device_guard_(ctx);
+  if (!ctx || !exec) return QCUR_E_PARAMETER;
+  cudaError_t e = cudaGraphLaunch((cudaGraphExec_t)exec, ctx->stream);
+  return e == cudaSuccess ? QCUR_OK : ctx->cuda_fail(e, "graph launch");
+}
+
+int qcur_graph_destroy(void* exec) {
+  if (!exec) return QCUR_E_PARAMETER;
+  return cudaGraphExecDestroy((cudaGraphExec_t)exec) == cudaSuccess ? QCUR_OK : QCUR_E_CUDA;
+}
+
 int qcur_synchronize(qcur_ctx* ctx) {
   DeviceGuard device_guard_(ctx);
   cudaError_t e = cudaStreamSynchronize(ctx->stream);
