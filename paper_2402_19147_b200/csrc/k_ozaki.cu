@@ -343,7 +343,8 @@ struct OzBColJobs {
   OzBColJob j[2];
 };
 
-__global__ void __launch_bounds__(256) k_oz_bcol(const __grid_constant__ OzBColJobs J, const __grid_constant__ OzMods md) {
+template <int NT>
+__global__ void __launch_bounds__(NT) k_oz_bcol(const __grid_constant__ OzBColJobs J, const __grid_constant__ OzMods md) {
   const OzBColJob& jb = J.j[blockIdx.y];
   const int64_t j = blockIdx.x;
   if (j >= jb.Nq) return;
@@ -354,9 +355,9 @@ __global__ void __launch_bounds__(256) k_oz_bcol(const __grid_constant__ OzBColJ
     }
     return ldq_nc(jb.B + (k * jb.ldb + j) * 4);
   };
-  __shared__ double sh[8];
+  __shared__ double sh[NT / 32];
   double mx = 0.0;
-  for (int64_t k = threadIdx.x; k < jb.Kq; k += 256) {
+  for (int64_t k = threadIdx.x; k < jb.Kq; k += NT) {
     const Quat q = ld(k);
     mx = fmax(mx, fmax(fmax(fabs(q.w), fabs(q.x)), fmax(fabs(q.y), fabs(q.z))));
   }
@@ -366,7 +367,7 @@ __global__ void __launch_bounds__(256) k_oz_bcol(const __grid_constant__ OzBColJ
   __syncthreads();
   mx = 0.0;
 #pragma unroll
-  for (int w = 0; w < 8; ++w) mx = fmax(mx, sh[w]);
+  for (int w = 0; w < NT / 32; ++w) mx = fmax(mx, sh[w]);
   int e = 0;
   if (mx > 0.0) {
     int E;
@@ -375,7 +376,7 @@ __global__ void __launch_bounds__(256) k_oz_bcol(const __grid_constant__ OzBColJ
   }
   if (threadIdx.x == 0) jb.fx[j] = e;
   const int64_t kq_pad = jb.pitch / 4;
-  for (int64_t k = threadIdx.x; k < kq_pad; k += 256) {
+  for (int64_t k = threadIdx.x; k < kq_pad; k += NT) {
     double b[4] = {0.0, 0.0, 0.0, 0.0};
     if (k < jb.Kq) {
       const Quat q = ld(k);
@@ -1655,6 +1656,20 @@ int launch_ozaki_prep_b(int64_t m, int64_t n, const double* B, int64_t r, int64_
   int* fx = reinterpret_cast<int*>(ws + pl.off_fx);
   const OzMods md = oz_mods(L);
   const int64_t bplane = pl.N * pl.Kpitch;
+  // one launch (a 1024-thread CTA per quaternion column of B: maximum, exponent, residues) for small B:
+  // measured per approximation cfg1 22.6 -> 16.9 us, cfg4 23.1 -> 16.9, cfg3 c = 128 31.2 -> 25.9, but at
+  // cfg2 (n r = 8e5, 200 CTAs) 66 -> 82 us; bit-identical.  QCUR_PREPB_BCOL=0/1 forces either way.
+  static const int bcol_env = [] {
+    const char* e = std::getenv("QCUR_PREPB_BCOL");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (bcol_env == 1 || (bcol_env < 0 && (double)n * (double)r <= 4e5)) {
+    OzBColJobs bj{};
+    bj.j[0] = OzBColJob{B, n, r, ldb, pl.Kpitch, bplane, 0, pl.bits, fx, bres};
+    ++::qcur::g_launches;
+    k_oz_bcol<1024><<<dim3((unsigned)r, 1), 1024, 0, st>>>(bj, md);
+    return 0;
+  }
   unsigned long long* cmax = reinterpret_cast<unsigned long long*>(ws + pl.off_cmax);
   cudaMemsetAsync(cmax, 0, (size_t)r * 8, st);
   const int64_t slabs = (n + 63) / 64 < 64 ? (n + 63) / 64 : 64, rows_per = (n + slabs - 1) / slabs;
@@ -1871,7 +1886,7 @@ int launch_ozaki_pair(const double* const* X, const int64_t* m, const int64_t* n
     if (!oz_job(jobs[k], pl[k], m[k], ares, pl[k].Kpitch, ws[k] + pl[k].off_bres, L, ws[k] + pl[k].off_res)) return 2;
   }
   ++::qcur::g_launches;
-  k_oz_bcol<<<dim3((unsigned)rmax, (unsigned)np), 256, 0, st>>>(bj, oz_mods(L));
+  k_oz_bcol<256><<<dim3((unsigned)rmax, (unsigned)np), 256, 0, st>>>(bj, oz_mods(L));
   oz_launch_gemm(jobs, np, L, st);
   for (int k = 0; k < np; ++k) {
     const int rc = oz_launch_crt(ws[k] + pl[k].off_res, m[k], pl[k], reinterpret_cast<int*>(ws[k] + pl[k].off_ex),
