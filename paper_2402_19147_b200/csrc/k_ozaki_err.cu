@@ -702,20 +702,30 @@ bool ozaki_error_supported(int64_t m, int64_t n, int64_t r) {
 size_t ozaki_error_workspace_bytes(int64_t m, int64_t n, int64_t r) { return oe_plan(m, n, r).total_bytes + 1024; }
 
 // the digit planes of P and E(R) and their exponents
-int launch_ozaki_error_digits(const double* P, int64_t ldp, const double* R, int64_t ldr, int64_t m, int64_t n,
-                              int64_t r, void* workspace, cudaStream_t st) {
+// the digit planes of E(R) and their exponents (R alone: may run as soon as R is gathered)
+int launch_ozaki_error_rdigits(const double* R, int64_t ldr, int64_t m, int64_t n, int64_t r, void* workspace,
+                               cudaStream_t st) {
   const OePlan pl = oe_plan(m, n, r);
   uint8_t* ws = reinterpret_cast<uint8_t*>(((uintptr_t)workspace + 255) / 256 * 256);
-  int8_t* pd = reinterpret_cast<int8_t*>(ws + pl.off_pd);
   int8_t* rd = reinterpret_cast<int8_t*>(ws + pl.off_rd);
-  int* ea = reinterpret_cast<int*>(ws + pl.off_ea);
   int* eb = reinterpret_cast<int*>(ws + pl.off_eb);
-  ++::qcur::g_launches;
-  k_oe_pdig<<<(unsigned)((m + 7) / 8), 256, 0, st>>>(P, m, pl.K, ldp * 4, pd, pl.Kp, ea);
   ++::qcur::g_launches;
   k_oe_rmax<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(R, r, n, ldr, eb);
   ++::qcur::g_launches;
   k_oe_rdig<<<(unsigned)((n * r + 255) / 256), 256, 0, st>>>(R, r, n, ldr, eb, rd, pl.Kp);
+  return 0;
+}
+
+// the digit planes of P (and of E(R) unless with_r == 0: formed earlier by launch_ozaki_error_rdigits)
+int launch_ozaki_error_digits(const double* P, int64_t ldp, const double* R, int64_t ldr, int64_t m, int64_t n,
+                              int64_t r, void* workspace, cudaStream_t st, int with_r) {
+  const OePlan pl = oe_plan(m, n, r);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(((uintptr_t)workspace + 255) / 256 * 256);
+  int8_t* pd = reinterpret_cast<int8_t*>(ws + pl.off_pd);
+  int* ea = reinterpret_cast<int*>(ws + pl.off_ea);
+  ++::qcur::g_launches;
+  k_oe_pdig<<<(unsigned)((m + 7) / 8), 256, 0, st>>>(P, m, pl.K, ldp * 4, pd, pl.Kp, ea);
+  if (with_r) return launch_ozaki_error_rdigits(R, ldr, m, n, r, workspace, st);
   return 0;
 }
 

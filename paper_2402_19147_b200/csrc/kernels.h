@@ -272,7 +272,9 @@ int launch_ozaki_error(const double* X, int64_t ldx, const double* P, int64_t ld
                        cudaStream_t st);
 // the same in two steps: digit planes, then the GEMMs with the fused epilogue
 int launch_ozaki_error_digits(const double* P, int64_t ldp, const double* R, int64_t ldr, int64_t m, int64_t n,
-                              int64_t r, void* workspace, cudaStream_t st);
+                              int64_t r, void* workspace, cudaStream_t st, int with_r = 1);
+int launch_ozaki_error_rdigits(const double* R, int64_t ldr, int64_t m, int64_t n, int64_t r, void* workspace,
+                               cudaStream_t st);
 int launch_ozaki_error_gemm(const double* X, int64_t ldx, int64_t m, int64_t n, int64_t r, double psnr_scale,
                             void* workspace, double* out4, cudaStream_t st);
 

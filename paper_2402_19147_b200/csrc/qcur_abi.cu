@@ -75,6 +75,7 @@ struct qcur_ctx {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaStream_t side_stream = nullptr;  // residues of X for the INT8 GEMM, overlapped with the factorizations
   cudaEvent_t ev_sfork = nullptr, ev_sjoin = nullptr;
+  cudaEvent_t ev_rjoin = nullptr;  // E(R)'s error digits, formed on the side stream after the gathers
   int gemm_mode = 0;                   // Y = X Q_R: 0 auto, 1 FP64 DMMA, 2 INT8 tcgen05 (Ozaki II)
   int xq_moduli = 15;                  // moduli of the INT8 X Q_R product (14 or 15; env QCUR_XQ_MODULI)
   int herm_moduli = 15;                // moduli of the INT8 Hermitian products (Grams, Q_C^H Y; QCUR_HERM_MODULI)
@@ -925,6 +926,15 @@ int qmcur_core(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, int64_t c, 
 // overlaps the draws and factorizations; the main stream joins before the GEMM.  Returns the
 // workspace holding the residues, or nullptr when the FP64 path will be used.
 void* int8_fork_prepare(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, int64_t r, int* rc);
+// qcur_approx forms E(R)'s error digits on the side stream right after the gathers (QCUR_RDIG_EARLY=0: with
+// the digits of P, just before the error kernel)
+bool rdigits_early() {
+  static const bool v = [] {
+    const char* e = std::getenv("QCUR_RDIG_EARLY");
+    return !(e && std::string(e) == "0");
+  }();
+  return v;
+}
 // QCUR_XRES_FORK=draw: the residues of X fork after the draws instead of after the length pass
 bool xres_fork_after_draw() {
   static const bool v = [] {
@@ -981,7 +991,8 @@ int copy_join(qcur_ctx* ctx) {
 // contraction run; U follows at the end.
 int qmcur_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, const double* colp, const double* rowp,
                int64_t c, int64_t r, const uint64_t state[4], int64_t* J, int64_t* I, double* C, double* U,
-               double* R, int core = QCUR_CORE_PROJECTION, const HostOut* ho = nullptr, void* oz_pre = nullptr) {
+               double* R, int core = QCUR_CORE_PROJECTION, const HostOut* ho = nullptr, void* oz_pre = nullptr,
+               void* rdig_ws = nullptr) {
   cudaStream_t st = ctx->stream;
   // 1. draws: columns first, then rows, one stream (cur.py:251-253)
   Pcg64 g;
@@ -1015,6 +1026,14 @@ int qmcur_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, const doubl
   launch_gather_rows(X, n, n, I, r, R, st);
   CK_LAUNCH(ctx, "gather");
   ctx->mark("gather");
+  if (rdig_ws) {  // E(R)'s digits for the error kernel depend on R alone: side stream, joined by error_impl
+    cudaError_t e = cudaEventRecord(ctx->ev_sfork, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->side_stream, ctx->ev_sfork, 0);
+    if (e == cudaSuccess) launch_ozaki_error_rdigits(R, n, m, n, r, rdig_ws, ctx->side_stream);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_rjoin, ctx->side_stream);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "error digits fork");
+  }
   if (ho) {
     if ((rc = copy_out(ctx, C, m, c, ho->C, J, c, ho->J, I, r, ho->I))) return rc;
     if ((rc = copy_out(ctx, R, r, n, ho->R, nullptr, 0, nullptr, nullptr, 0, nullptr))) return rc;
@@ -1185,7 +1204,7 @@ size_t error_ws_bytes(int64_t m, int64_t n, int64_t c, int64_t r) {
 }
 
 int error_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, const double* C, int64_t c, const double* U,
-               const double* R, int64_t r, double psnr_scale, double* out4) {
+               const double* R, int64_t r, double psnr_scale, double* out4, void* rdig_ws = nullptr) {
   double* P = ctx->take<double>((size_t)(m * r * 4));
   double* parts = ctx->take<double>((size_t)err_partials_count(m, n) * 4);
   GemmArgs g = gargs(m, r, c, C, c, 0, U, r, 0, P, r);
@@ -1196,9 +1215,13 @@ int error_impl(qcur_ctx* ctx, const double* X, int64_t m, int64_t n, const doubl
   if ((rc = gemm(ctx, g, gws))) return rc;
   ctx->mark("cu");
   if (use_int8_err(ctx, m, n, r)) {
-    void* ws = ctx->take<uint8_t>(ozaki_error_workspace_bytes(m, n, r));
+    void* ws = rdig_ws ? rdig_ws : ctx->take<uint8_t>(ozaki_error_workspace_bytes(m, n, r));
     if (!ws) return ctx->fail(QCUR_E_CUDA, "workspace exhausted (int8 error)");
-    launch_ozaki_error_digits(P, r, R, n, m, n, r, ws, ctx->stream);
+    launch_ozaki_error_digits(P, r, R, n, m, n, r, ws, ctx->stream, rdig_ws ? 0 : 1);
+    if (rdig_ws) {  // E(R)'s digits were formed on the side stream after the gathers
+      cudaError_t e = cudaStreamWaitEvent(ctx->stream, ctx->ev_rjoin, 0);
+      if (e != cudaSuccess) return ctx->cuda_fail(e, "error digits join");
+    }
     ctx->mark("error_digits");
     if (launch_ozaki_error_gemm(X, n, m, n, r, psnr_scale, ws, out4, ctx->stream))
       return ctx->fail(QCUR_E_CUDA, "int8 error: tensor map encode failed");
@@ -1301,6 +1324,7 @@ int qcur_create(int device, qcur_ctx** out) {
       cudaStreamCreateWithPriority(&ctx->side_stream, cudaStreamNonBlocking, prio_lo) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_sfork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_sjoin, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_rjoin, cudaEventDisableTiming) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
@@ -1339,6 +1363,7 @@ void qcur_destroy(qcur_ctx* ctx) {
   cudaEventDestroy(ctx->ev_hjoin);
   cudaEventDestroy(ctx->ev_sfork);
   cudaEventDestroy(ctx->ev_sjoin);
+  cudaEventDestroy(ctx->ev_rjoin);
   cudaEventDestroy(ctx->ev_fork);
   cudaEventDestroy(ctx->ev_join);
   delete ctx;
@@ -1801,8 +1826,13 @@ int qcur_approx(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int st
   // overlapping the latency-bound draws and factorizations does
   if (!rc && !xres_fork_after_draw() && core == QCUR_CORE_PROJECTION && m >= c && n >= r)
     oz = int8_fork_prepare(ctx, x_dev, m, n, r, &rc);
-  if (!rc) rc = qmcur_impl(ctx, x_dev, m, n, colp, rowp, c, r, state, J, I, C, U, R, core, nullptr, oz);
-  if (!rc) rc = error_impl(ctx, x_dev, m, n, C, c, U, R, r, psnr_scale, err4);
+  void* rdig = nullptr;
+  if (!rc && use_int8_err(ctx, m, n, r) && rdigits_early()) {
+    rdig = ctx->take<uint8_t>(ozaki_error_workspace_bytes(m, n, r));
+    if (!rdig) rc = ctx->fail(QCUR_E_CUDA, "workspace exhausted (int8 error)");
+  }
+  if (!rc) rc = qmcur_impl(ctx, x_dev, m, n, colp, rowp, c, r, state, J, I, C, U, R, core, nullptr, oz, rdig);
+  if (!rc) rc = error_impl(ctx, x_dev, m, n, C, c, U, R, r, psnr_scale, err4, rdig);
   if (ctx->prio) {
     cudaError_t e = cudaEventRecord(ctx->ev_hjoin, ctx->hi_stream);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(user, ctx->ev_hjoin, 0);
