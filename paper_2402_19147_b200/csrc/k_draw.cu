@@ -97,6 +97,15 @@ struct DrawJobs {
   DrawJob j[2];
 };
 
+#ifdef QCUR_DRAW_TRACE  // per-draw clocks of CTA 0, lane 0 (tools/test_draw_trace.cu)
+__device__ long long g_draw_trace[1026][3];
+#define DRAW_T(t, k) \
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (t) < 1026) g_draw_trace[t][k] = clock64();
+void draw_trace_read(long long* out) { cudaMemcpyFromSymbol(out, g_draw_trace, sizeof(g_draw_trace)); }
+#else
+#define DRAW_T(t, k)
+#endif
+
 // The prefix tree over the exact weights pw, level by level: a warp per node scans its 64
 // children (pair sums, then a fixed-order Hillis-Steele scan); the node's total feeds the
 // level above.  Run by the whole block (block = true) or, for a rebuild, by warp 0 alone.
@@ -139,6 +148,7 @@ __global__ void __launch_bounds__(512, 1) k2_draw(DrawJobs jobs, unsigned* statu
   const DrawJob job = jobs.j[blockIdx.x];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int64_t len = job.len;
+  DRAW_T(1024, 0)
   const Tree T = make_tree(len);
   extern __shared__ __align__(16) double sm_draw[];
   constexpr bool p_in_smem = kLeafSmem;
@@ -174,7 +184,9 @@ __global__ void __launch_bounds__(512, 1) k2_draw(DrawJobs jobs, unsigned* statu
     uni[t] = g.next_double();
   }
   __syncthreads();
+  DRAW_T(1024, 1)
   build_tree<true>(T, P, Sb, pw, warp, nw, lane);
+  DRAW_T(1024, 2)
   if (warp != 0) return;
   int positive = 0;
   for (int w = 0; w < nw; ++w) positive += s_pos[w];
@@ -206,6 +218,7 @@ __global__ void __launch_bounds__(512, 1) k2_draw(DrawJobs jobs, unsigned* statu
   double ublk = lane < count ? uni[lane] : 0.0;
   double unext = 32 + lane < count ? uni[32 + lane] : 0.0;
   for (int t = 0; t < count; ++t) {
+    DRAW_T(t, 0)
     if ((t & 31) == 0 && t > 0) {
       ublk = unext;
       unext = t + 32 + lane < count ? uni[t + 32 + lane] : 0.0;
@@ -264,6 +277,7 @@ __global__ void __launch_bounds__(512, 1) k2_draw(DrawJobs jobs, unsigned* statu
       base = lo;
       g = g * kFan + e;
     }
+    DRAW_T(t, 1)
     int64_t idx = g;
     if (ok) {
       const double delta = 2.0 * u53 * (c_np * total + err_acc) * (1.0 + 1e-9);
@@ -320,7 +334,9 @@ __global__ void __launch_bounds__(512, 1) k2_draw(DrawJobs jobs, unsigned* statu
       pw[idx] = 0.0;
     }
     __syncwarp();
+    DRAW_T(t, 2)
   }
+  DRAW_T(1025, 0)
 }
 
 bool launch_draw(const DrawJob* jobs, int njobs, unsigned* status, cudaStream_t st) {
