@@ -672,7 +672,9 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPThreads, 1) k_ch
     for (int j = 0; j < q; ++j) {
       const int b = j % kPBuf;
       const double* cb = colbuf + (size_t)b * q * 4;
+      CHOL_T(j, 0)
       mbar_wait(&mbar[b], (unsigned)(j / kPBuf) & 1u);
+      CHOL_T(j, 1)
       if (j + 1 < q) {
         const Quat lj1 = ldQ(cb + (size_t)(j + 1) * 4);
         const double d1 = diag[j + 1] - qnorm2(lj1);
@@ -682,8 +684,10 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPThreads, 1) k_ch
           return qsub(ldQ(rows + (rowbase(s) + j + 1) * 4), qmul(ldQ(cb + (size_t)i * 4), qconj(lj1)));
         });
       }
+      CHOL_T(j, 2)
       if (j + 2 < q) {
         if (j >= 1) mbar_wait(bdone, (unsigned)(j - 1) & 1u);  // the bulk of step j-1 is done
+        CHOL_T(j, 3)
         if (!fail) {
           const Quat lj2 = ldQ(cb + (size_t)(j + 2) * 4);
           for (int s = st; s < nown; s += 32 * kPS) {
@@ -695,7 +699,9 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPThreads, 1) k_ch
           if (st == 0) diag[j + 2] = diag[j + 2] - qnorm2(lj2);
         }
       }
+      CHOL_T(j, 4)
       named_sync(1, 32 * kPS);  // the next step's senders read the entries and pivot written above
+      CHOL_T(j, 5)
     }
     if (st == 0 && fail) s_fail = 1;
   } else {
