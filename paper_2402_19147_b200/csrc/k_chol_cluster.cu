@@ -606,19 +606,35 @@ void chol_trace_read(long long* out) { cudaMemcpyFromSymbol(out, g_chol_trace, s
 constexpr int kPS = 4, kPB = QCUR_CHOL_PB, kPThreads = 32 * (kPS + kPB), kPBuf = 4;
 constexpr int64_t kPipeQMin = 192;
 
+__host__ __device__ inline int chol_bulk_ns(int64_t q) {  // slots per owner: ceil(q / 16), odd
+  const int n = (int)((q + kCl - 1) / kCl);
+  return n | 1;
+}
+
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// BULK (round 2): the column exchange as one bulk copy per destination.  A column buffer is laid out
+// by owner (entry i at slot (i mod 16) NS + i / 16, NS = ceil(q / 16) rounded up to odd: a warp reading 32
+// consecutive entries still touches every 32-byte bank group once), so an owner's entries of a column
+// are contiguous: the senders write them into their own buffer and each destination receives them with
+// one cp.async.bulk (shared::cta -> shared::cluster, complete_tx on the destination's barrier) instead
+// of 2 (q - j) / 16 st.async per destination (traced: the send took ~1000 of the 2800 cycles of a step).
+// Measured slower (the small bulk copies cost more than the st.async they replace): opt-in only.
+template <bool BULK>
 __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPThreads, 1) k_chol_inv_pipe(CholProblems P) {
   const int c = (int)cg::this_cluster().block_rank();
   const CholJob pr = P.p[blockIdx.x / kCl];
   const int q = (int)P.q;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nown = (q - c + kCl - 1) / kCl;
+  const int NS = chol_bulk_ns(q);                        // slots per owner (BULK)
+  const int CS = BULK ? kCl * NS : q;                    // quaternions per column buffer
+  auto slot = [&](int i) -> int { return BULK ? (i & (kCl - 1)) * NS + (i >> 4) : i; };
   extern __shared__ __align__(32) double sm[];
-  double* colbuf = sm;                                   // [4][q] columns of L in flight
-  double* diag = colbuf + kPBuf * (size_t)q * 4;         // [q] replicated running diagonal
+  double* colbuf = sm;                                   // [4][CS] columns of L in flight
+  double* diag = colbuf + kPBuf * (size_t)CS * 4;        // [q] replicated running diagonal
   double* invs = diag + q;                               // [q] 1 / l_jj
   uint64_t* mbar = reinterpret_cast<uint64_t*>(invs + q + 2);  // [4] column arrival, [4] bulk done
   uint64_t* bdone = mbar + kPBuf;
@@ -651,18 +667,62 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPThreads, 1) k_ch
     // send column j (own rows i > j, entry value v(s) supplied by the caller), scaled by inv
     auto send = [&](int j, double inv, auto&& value) {
       const int b = j % kPBuf;
-      if (st == 0) {
-        invs[j] = inv;  // before the local arrive: the bulk warps read it after this column's phase
-        mbar_expect_tx(&mbar[b], 32u * (unsigned)(q - 1 - j));
+      if constexpr (BULK) {
+        double* cbw = colbuf + (size_t)b * CS * 4;
+        const int s0 = j < c ? 0 : (j - c) / kCl + 1;  // own entries i = c + 16 s > j
+        const int cnt = nown > s0 ? nown - s0 : 0;
+        for (int sr = s0 + st; sr < nown; sr += 32 * kPS)
+          stQ(cbw + (size_t)(c * NS + sr) * 4, fail ? qzero() : qscale(value(sr), inv));
+        if (st == 0) {
+          invs[j] = inv;
+          mbar_expect_tx(&mbar[b], 32u * (unsigned)((q - 1 - j) - cnt));  // the other owners' entries
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> bulk copy reads
+        named_sync(3, 32 * kPS);
+        if (st < kCl) {
+          const uint32_t mb_u = smem_u32(&mbar[b]);
+          if (st != c) {
+            if (cnt > 0) {
+              const uint32_t src = smem_u32(cbw + (size_t)(c * NS + s0) * 4);
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                      mapa(src, st)),
+                  "r"(src), "r"(32u * (unsigned)cnt), "r"(mapa(mb_u, st))
+                  : "memory");
+            }
+            mbar_arrive_remote(mapa(mb_u, st));
+          } else {
+            mbar_arrive(&mbar[b]);  // release: this CTA's own entries are plain stores
+          }
+        }
+      } else {
+        if (st == 0) {
+          invs[j] = inv;  // before the local arrive: the bulk warps read it after this column's phase
+          mbar_expect_tx(&mbar[b], 32u * (unsigned)(q - 1 - j));
+        }
+        const uint32_t cb_u = smem_u32(colbuf + (size_t)b * CS * 4), mb_u = smem_u32(&mbar[b]);
+        // a thread's (entry, destination) pairs: all values first (independent loads and products in
+        // flight together), then the stores (same values, same order per destination)
+        constexpr int kPairs = ((kClusterQMax + kCl - 1) / kCl * kCl + 32 * kPS - 1) / (32 * kPS);
+        Quat val[kPairs];
+        bool act[kPairs];
+#pragma unroll
+        for (int u = 0; u < kPairs; ++u) {
+          const int t = st + u * 32 * kPS;
+          const int sr = t / kCl;
+          act[u] = t < nown * kCl && c + kCl * sr > j;
+          val[u] = act[u] && !fail ? qscale(value(sr), inv) : qzero();
+        }
+#pragma unroll
+        for (int u = 0; u < kPairs; ++u) {
+          if (!act[u]) continue;
+          const int t = st + u * 32 * kPS;
+          const int sr = t / kCl, dst = t - sr * kCl;
+          const int i = c + kCl * sr;
+          st_async_quat(mapa(cb_u + 32u * (unsigned)i, dst), val[u], mapa(mb_u, dst));
+        }
+        if (st < kCl) mbar_arrive_remote(mapa(mb_u, st));
       }
-      const uint32_t cb_u = smem_u32(colbuf + (size_t)b * q * 4), mb_u = smem_u32(&mbar[b]);
-      for (int t = st; t < nown * kCl; t += 32 * kPS) {
-        const int s = t / kCl, dst = t - s * kCl;
-        const int i = c + kCl * s;
-        if (i <= j) continue;
-        st_async_quat(mapa(cb_u + 32u * (unsigned)i, dst), fail ? qzero() : qscale(value(s), inv), mapa(mb_u, dst));
-      }
-      if (st < kCl) mbar_arrive_remote(mapa(mb_u, st));
     };
     {
       const double d = diag[0];
@@ -671,17 +731,17 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPThreads, 1) k_ch
     }
     for (int j = 0; j < q; ++j) {
       const int b = j % kPBuf;
-      const double* cb = colbuf + (size_t)b * q * 4;
+      const double* cb = colbuf + (size_t)b * CS * 4;
       CHOL_T(j, 0)
       mbar_wait(&mbar[b], (unsigned)(j / kPBuf) & 1u);
       CHOL_T(j, 1)
       if (j + 1 < q) {
-        const Quat lj1 = ldQ(cb + (size_t)(j + 1) * 4);
+        const Quat lj1 = ldQ(cb + (size_t)slot(j + 1) * 4);
         const double d1 = diag[j + 1] - qnorm2(lj1);
         if (!(d1 > 0.0) || !isfinite(d1)) fail = true;  // every CTA alike (replicated diagonal)
         send(j + 1, fail ? 0.0 : 1.0 / sqrt(d1), [&](int s) {
           const int i = c + kCl * s;
-          return qsub(ldQ(rows + (rowbase(s) + j + 1) * 4), qmul(ldQ(cb + (size_t)i * 4), qconj(lj1)));
+          return qsub(ldQ(rows + (rowbase(s) + j + 1) * 4), qmul(ldQ(cb + (size_t)slot(i) * 4), qconj(lj1)));
         });
       }
       CHOL_T(j, 2)
@@ -689,12 +749,12 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPThreads, 1) k_ch
         if (j >= 1) mbar_wait(bdone, (unsigned)(j - 1) & 1u);  // the bulk of step j-1 is done
         CHOL_T(j, 3)
         if (!fail) {
-          const Quat lj2 = ldQ(cb + (size_t)(j + 2) * 4);
+          const Quat lj2 = ldQ(cb + (size_t)slot(j + 2) * 4);
           for (int s = st; s < nown; s += 32 * kPS) {
             const int i = c + kCl * s;
             if (i <= j + 2) continue;
             double* e = rows + (rowbase(s) + j + 2) * 4;
-            stQ(e, qsub(ldQ(e), qmul(ldQ(cb + (size_t)i * 4), qconj(lj2))));
+            stQ(e, qsub(ldQ(e), qmul(ldQ(cb + (size_t)slot(i) * 4), qconj(lj2))));
           }
           if (st == 0) diag[j + 2] = diag[j + 2] - qnorm2(lj2);
         }
@@ -709,7 +769,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPThreads, 1) k_ch
     const int bw = warp - kPS, bt = tid - 32 * kPS;
     for (int j = 0; j < q; ++j) {
       const int b = j % kPBuf;
-      const double* cb = colbuf + (size_t)b * q * 4;
+      const double* cb = colbuf + (size_t)b * CS * 4;
       mbar_wait(&mbar[b], (unsigned)(j / kPBuf) & 1u);
       const double inv = invs[j];
       const int s0 = j + 2 < c ? 0 : (j + 2 - c) / kCl + 1;  // own rows i > j + 2
@@ -718,7 +778,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPThreads, 1) k_ch
       for (int it = kPB - 1 - bw; it < nrow + ncol; it += kPB) {
         if (it < nrow) {
           const int sr = s0 + it, i = c + kCl * sr;
-          const Quat lij = ldQ(cb + (size_t)i * 4);
+          const Quat lij = ldQ(cb + (size_t)slot(i) * 4);
           double* row = rows + rowbase(sr) * 4;
           for (int k0 = j + 3; k0 <= i; k0 += 32 * kCB) {
             Quat av[kCB], bv[kCB];
@@ -727,7 +787,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPThreads, 1) k_ch
               const int k = k0 + lane + 32 * u;
               if (k <= i) {
                 av[u] = ldQ(row + (size_t)k * 4);
-                bv[u] = ldQ(cb + (size_t)k * 4);
+                bv[u] = ldQ(cb + (size_t)slot(k) * 4);
               }
             }
 #pragma unroll
@@ -749,7 +809,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPThreads, 1) k_ch
               const int i = i0 + lane + 32 * u;
               if (i < q) {
                 av[u] = ldQ(w + (size_t)i * 4);
-                bv[u] = ldQ(cb + (size_t)i * 4);
+                bv[u] = ldQ(cb + (size_t)slot(i) * 4);
               }
             }
 #pragma unroll
@@ -761,7 +821,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPThreads, 1) k_ch
           __syncwarp();
         }
       }
-      for (int i = j + 3 + bt; i < q; i += 32 * kPB) diag[i] = diag[i] - qnorm2(ldQ(cb + (size_t)i * 4));
+      for (int i = j + 3 + bt; i < q; i += 32 * kPB) diag[i] = diag[i] - qnorm2(ldQ(cb + (size_t)slot(i) * 4));
       named_sync(2, 32 * kPB);  // every bulk warp is done with step j
       if (bt == 0) mbar_arrive(bdone);
     }
@@ -786,7 +846,8 @@ static size_t chol_pipe_smem(int64_t q) {
     const int64_t nown = (q - c + kCl - 1) / kCl;
     const int64_t rows = nown * (c + 1) + 8 * nown * (nown - 1);
     const int64_t cols = nown * (q - c) - 8 * nown * (nown - 1);
-    const size_t b = (size_t)(kPBuf * q * 4 + 2 * q + 2 + 2 * kPBuf + 4 * (rows + cols)) * sizeof(double);
+    const int64_t cs = kCl * (int64_t)chol_bulk_ns(q) > q ? kCl * (int64_t)chol_bulk_ns(q) : q;  // either layout
+    const size_t b = (size_t)(kPBuf * cs * 4 + 2 * q + 2 + 2 * kPBuf + 4 * (rows + cols)) * sizeof(double);
     best = b > best ? b : best;
   }
   return best;
@@ -847,11 +908,22 @@ void launch_chol_inv_cluster(const CholJob* jobs, int njobs, int64_t q, unsigned
   if ((pipe_env == 1 || (pipe_env < 0 && q >= kPipeQMin)) && chol_pipe_smem(q) <= 226 * 1024) {
     static std::atomic<unsigned> setp{0};
     if (first_on_device(setp)) {
-      cudaFuncSetAttribute(k_chol_inv_pipe, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      cudaFuncSetAttribute(k_chol_inv_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
+      for (auto f : {k_chol_inv_pipe<true>, k_chol_inv_pipe<false>}) {
+        cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
+      }
     }
     ++::qcur::g_launches;
-    k_chol_inv_pipe<<<kCl * njobs, kPThreads, chol_pipe_smem(q), st>>>(P);
+    // QCUR_CHOL_BULK=1: the column exchange by one bulk copy per destination (bit-identical factors;
+    // measured slower: q = 200 pair 477 vs 279 us, the send 1978 vs 1007 cycles per step)
+    static const int bulk_env = [] {
+      const char* e = std::getenv("QCUR_CHOL_BULK");
+      return e ? std::atoi(e) : 0;
+    }();
+    if (bulk_env)
+      k_chol_inv_pipe<true><<<kCl * njobs, kPThreads, chol_pipe_smem(q), st>>>(P);
+    else
+      k_chol_inv_pipe<false><<<kCl * njobs, kPThreads, chol_pipe_smem(q), st>>>(P);
     return;
   }
   ++::qcur::g_launches;
