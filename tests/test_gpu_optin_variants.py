@@ -7,7 +7,7 @@ environment switch and compared with the default path on the same input.
   within the oracle bars (different rounding from the DMMA product, so not bitwise).
 * QCUR_CHOL_PIPE=0 / 1, QCUR_CHOL_BULK=1 and QCUR_SMALL_GEMM=0: the one-column / pipelined / bulk-copy
   cluster Cholesky give identical factors; the DMMA GEMM for the q x q products stays within the bars.
-* QCUR_RDIG_EARLY=0, QCUR_PREPB_BCOL=1, QCUR_NATIVE_GRAPH=1: scheduling / launch-shape variants with
+* QCUR_RDIG_EARLY=0, QCUR_PREPB_BCOL=0, QCUR_NATIVE_GRAPH=1: scheduling / launch-shape variants with
   the same bits (the last only affects DeviceApprox graph replays, not this public-API run)."""
 import os
 import subprocess
@@ -48,7 +48,7 @@ def default_run(tmp_path_factory):
 
 @pytest.mark.parametrize("env,bitwise", [({"QCUR_OZ_BMC": "1"}, True), ({"QCUR_CHOL_PIPE": "0"}, True),
                                          ({"QCUR_CHOL_BULK": "1"}, True), ({"QCUR_RDIG_EARLY": "0"}, True),
-                                         ({"QCUR_PREPB_BCOL": "1"}, True), ({"QCUR_NATIVE_GRAPH": "1"}, True),
+                                         ({"QCUR_PREPB_BCOL": "0"}, True), ({"QCUR_NATIVE_GRAPH": "1"}, True),
                                          ({"QCUR_CHOL_PIPE": "1"}, True), ({"QCUR_INT8_MIN_Q1": "1"}, False),
                                          ({"QCUR_SMALL_GEMM": "0"}, False)])
 def test_optin_variant_matches_default(tmp_path, default_run, env, bitwise):
