@@ -25,7 +25,8 @@ namespace {
 #ifndef QCUR_SMALL_KS  // build-time variant for A/B timing
 #define QCUR_SMALL_KS 4
 #endif
-constexpr int kKS = QCUR_SMALL_KS;  // CTAs per cluster (k ranges): 4-CTA clusters pack the GPCs in one wave
+constexpr int kKS = QCUR_SMALL_KS;
+static_assert(kKS == 1 || kKS == 2 || kKS == 4 || kKS == 8, "the cluster's ranks split the 32-row reduction evenly");  // CTAs per cluster (k ranges): 4-CTA clusters pack the GPCs in one wave
                                    // at q = 200 (8-CTA clusters: 784 CTAs in ~3 waves, 49 us for the pair)
 constexpr int kT = 32;        // output tile edge (quaternions)
 constexpr int kKC = 16;       // quaternions of K staged per step
