@@ -256,9 +256,18 @@ bool small_env_on() {
 }
 }  // namespace
 
+// q x q products, and tall products with small N and K while their total work is small (the
+// triangular Q_1 = Z L_1^-H and P = C U of cfg1 / cfg4: 1000-1024 rows, q = 40-80, where the persistent
+// DMMA GEMM spends ~24 us on ~1e6-7e6 quaternion MACs); QCUR_SMALL_MNK overrides the work bound
 bool qgemm_small_ok(const GemmArgs& g) {
-  return small_env_on() && !g.whole_tiles && g.Mq >= 1 && g.Nq >= 1 && g.Kq >= 1 && g.Mq <= kSmallMax &&
-         g.Nq <= kSmallMax && g.Kq <= kSmallMax && (g.opA == 0 || g.opA == 1) && (g.opB == 0 || g.opB == 1);
+  static const double mnk_max = [] {
+    const char* e = getenv("QCUR_SMALL_MNK");
+    return e ? atof(e) : 1.2e7;
+  }();
+  const bool shape = g.Nq <= kSmallMax && g.Kq <= kSmallMax &&
+                     (g.Mq <= kSmallMax || (double)g.Mq * (double)g.Nq * (double)g.Kq <= mnk_max);
+  return small_env_on() && !g.whole_tiles && g.Mq >= 1 && g.Nq >= 1 && g.Kq >= 1 && shape &&
+         (g.opA == 0 || g.opA == 1) && (g.opB == 0 || g.opB == 1);
 }
 
 void launch_qgemm_small(const GemmArgs* g, int np, cudaStream_t st) {
