@@ -1,5 +1,6 @@
-// Small quaternion products C = alpha op(A) op(B) + beta C with M, N, K <= kSmallMax (the q x q
-// products of a factorization step and of the core: S += E E, F = L1^{-H} S, U = F_C M F_R^H;
+// Small quaternion products C = alpha op(A) op(B) + beta C with N, K <= kSmallMax and M <= kSmallMax or
+// little total work (the q x q products of a factorization step and of the core: S += E E,
+// F = L1^{-H} S, U = F_C M F_R^H; at the small configurations also Q_1 = Z L_1^{-H} and P = C U;
 // linalg.py:346-362 / cur.py:268 on the device).
 //
 // The persistent DMMA GEMM (k_qgemm.cu) is built for tall products: at q = 200 a q x q x q product is
