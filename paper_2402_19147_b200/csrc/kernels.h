@@ -93,8 +93,8 @@ struct GemmArgs {
                         // depend on M (row blocks of a generated matrix concatenate bit for bit)
 };
 size_t qgemm_workspace_bytes(const GemmArgs& g);
-// small products (M, N, K <= 256, not whole_tiles): launch_qgemm / launch_qgemm_pair route them to
-// k_qgemm_small (no workspace or counters used)
+// small products (N, K <= 256 and M <= 256 or M N K <= 1.2e7 quaternion MACs, not whole_tiles):
+// launch_qgemm / launch_qgemm_pair route them to k_qgemm_small (no workspace or counters used)
 bool qgemm_small_ok(const GemmArgs& g);
 void launch_qgemm_small(const GemmArgs* g, int np, cudaStream_t st);
 // counters: >= 65536 zero-initialised uints owned by the caller (split-K tickets)
