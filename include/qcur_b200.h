@@ -282,6 +282,20 @@ int qcur_factor(qcur_ctx* ctx, const double* src_dev, int zh, int64_t p, int64_t
  * qcur_graph_begin starts capturing the context stream (not the legacy default stream), the
  * captured ABI calls follow, qcur_graph_end closes the capture and returns the executable graph,
  * qcur_graph_launch replays it on the context stream, qcur_graph_destroy frees it. */
+/* The drop-in path with the INT8 X Q_R's residues of X formed while X uploads (make_plan on a host
+ * matrix, then qmcur with the same r): qcur_xq_workspace_bytes gives the device workspace the residues
+ * live in (0: the shape does not take the INT8 X Q_R), qcur_upload_length_xq is qcur_upload_length that
+ * also fills it, and qcur_qmcur_host_xq is qcur_qmcur_host that consumes it instead of forming the
+ * residues itself.  Same results as the plain calls (identical residues). */
+size_t qcur_xq_workspace_bytes(qcur_ctx* ctx, int64_t m, int64_t n, int64_t r);
+int qcur_upload_length_xq(qcur_ctx* ctx, const double* a0, const double* a1, const double* a2, const double* a3,
+                          int64_t m, int64_t n, int64_t r, double* x_dev, double* col_dev, double* row_dev,
+                          void* xq_ws);
+int qcur_qmcur_host_xq(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, const double* col_probs_dev,
+                       const double* row_probs_dev, int64_t num_cols, int64_t num_rows, const uint64_t state[4],
+                       int core, int64_t* col_idx_dev, int64_t* row_idx_dev, double* c_dev, double* u_dev,
+                       double* r_dev, int64_t* col_idx_host, int64_t* row_idx_host, double* const c_host[4],
+                       double* const u_host[4], double* const r_host[4], void* xq_ws);
 int qcur_graph_begin(qcur_ctx* ctx);
 int qcur_graph_end(qcur_ctx* ctx, void** exec_out);
 int qcur_graph_launch(qcur_ctx* ctx, void* exec);

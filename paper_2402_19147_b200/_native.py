@@ -52,6 +52,7 @@ EXPORTS = (
     "qcur_project_observed", "qcur_complete_sweep", "qcur_cur_given", "qcur_qgemv",
     "qcur_upload_length", "qcur_status_async", "qcur_status_map",
     "qcur_graph_begin", "qcur_graph_end", "qcur_graph_launch", "qcur_graph_destroy",
+    "qcur_xq_workspace_bytes", "qcur_upload_length_xq", "qcur_qmcur_host_xq",
 )
 
 _c_dp = ctypes.c_void_p
@@ -109,6 +110,12 @@ def load_library() -> ctypes.CDLL:
             "qcur_status_async": (ctypes.c_int, [_c_dp, _c_dp]),
             "qcur_status_map": (ctypes.c_int, [_c_dp, ctypes.c_uint]),
             "qcur_upload_length": (ctypes.c_int, [_c_dp, _c_dp, _c_dp, _c_dp, _c_dp, _i64, _i64, _c_dp, _c_dp, _c_dp]),
+            "qcur_xq_workspace_bytes": (ctypes.c_size_t, [_c_dp, _i64, _i64, _i64]),
+            "qcur_upload_length_xq": (ctypes.c_int, [_c_dp, _c_dp, _c_dp, _c_dp, _c_dp, _i64, _i64, _i64, _c_dp, _c_dp,
+                                                     _c_dp, _c_dp]),
+            "qcur_qmcur_host_xq": (ctypes.c_int, [_c_dp, _c_dp, _i64, _i64, _c_dp, _c_dp, _i64, _i64, _u64p,
+                                                  ctypes.c_int, _c_dp, _c_dp, _c_dp, _c_dp, _c_dp, _c_dp, _c_dp,
+                                                  _c_dp4, _c_dp4, _c_dp4, _c_dp]),
             "qcur_qgemv": (ctypes.c_int, [_c_dp, ctypes.c_int, _i64, _i64, _c_dp, _i64, _c_dp, _c_dp]),
             "qcur_cur_given": (ctypes.c_int, [_c_dp, _c_dp, _i64, _i64, _c_dp, _i64, _c_dp, _i64, _c_dp, _c_dp, _c_dp]),
             "qcur_project_observed": (ctypes.c_int, [_c_dp, _c_dp, _c_dp, _c_dp, _i64, _i64, _c_dp]),

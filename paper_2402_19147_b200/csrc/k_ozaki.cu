@@ -1646,6 +1646,21 @@ int launch_ozaki_prepare(const double* X, int64_t m, int64_t n, int64_t ldx, int
   return 0;
 }
 
+// Phase 1 for rows [row0, row0 + rows) of an m-row X (the chunk at X_rows): the same residues and
+// exponents launch_ozaki_prepare writes for those rows (used while X is uploaded chunk by chunk)
+int launch_ozaki_prepare_rows(const double* X_rows, int64_t rows, int64_t row0, int64_t m, int64_t n, int64_t ldx,
+                              int64_t r, int L, void* workspace, cudaStream_t st) {
+  if (L != 15 || rows < 1) return 1;
+  const OzPlan pl = oz_plan(m, n, r, L);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(((uintptr_t)workspace + 255) / 256 * 256);
+  uint8_t* ares = ws + pl.off_ares + row0 * pl.Kpitch;
+  int* ex = reinterpret_cast<int*>(ws + pl.off_ex) + row0;
+  ++::qcur::g_launches;
+  k_oz_xres<15, 256, 8><<<(unsigned)rows, 256, 0, st>>>(X_rows, pl.K, ldx * 4, pl.bits, ares, pl.Kpitch,
+                                                         m * pl.Kpitch, ex, rows);
+  return 0;
+}
+
 // Phase 2a: column exponents and residues of E(B).
 int launch_ozaki_prep_b(int64_t m, int64_t n, const double* B, int64_t r, int64_t ldb, int L, void* workspace,
                         cudaStream_t st) {

@@ -241,6 +241,8 @@ int64_t ozaki_chunk_rows(int64_t m, int64_t n, int64_t r, double cap_bytes);
 int launch_ozaki_gemm(const double* X, int64_t m, int64_t n, int64_t ldx, const double* B, int64_t r, int64_t ldb,
                       double* Y, int64_t ldy, int L, void* workspace, cudaStream_t st);
 // the same in two phases: prepare (residues of X; depends on X only) and finish (B, GEMMs, CRT)
+int launch_ozaki_prepare_rows(const double* X_rows, int64_t rows, int64_t row0, int64_t m, int64_t n, int64_t ldx,
+                              int64_t r, int L, void* workspace, cudaStream_t st);
 int launch_ozaki_prepare(const double* X, int64_t m, int64_t n, int64_t ldx, int64_t r, int L, void* workspace,
                          cudaStream_t st);
 int launch_ozaki_finish(int64_t m, int64_t n, const double* B, int64_t r, int64_t ldb, double* Y, int64_t ldy, int L,

@@ -1514,9 +1514,35 @@ int qcur_upload_planar(qcur_ctx* ctx, const double* a0, const double* a1, const 
   return QCUR_OK;
 }
 
+namespace {
+int upload_length_impl(qcur_ctx* ctx, const double* a0, const double* a1, const double* a2, const double* a3,
+                       int64_t m, int64_t n, double* x_dev, double* col_dev, double* row_dev, int64_t xq_r,
+                       void* xq_ws);
+}  // namespace
+
 int qcur_upload_length(qcur_ctx* ctx, const double* a0, const double* a1, const double* a2, const double* a3,
                        int64_t m, int64_t n, double* x_dev, double* col_dev, double* row_dev) {
   DeviceGuard device_guard_(ctx);
+  return upload_length_impl(ctx, a0, a1, a2, a3, m, n, x_dev, col_dev, row_dev, 0, nullptr);
+}
+
+size_t qcur_xq_workspace_bytes(qcur_ctx* ctx, int64_t m, int64_t n, int64_t r) {
+  DeviceGuard device_guard_(ctx);
+  if (!ctx || m < 1 || n < 1 || r < 1 || r > m || ctx->xq_moduli != 15 || !use_int8(ctx, m, n, r)) return 0;
+  return ozaki_workspace_bytes(m, n, r, 15) + 256;
+}
+
+int qcur_upload_length_xq(qcur_ctx* ctx, const double* a0, const double* a1, const double* a2, const double* a3,
+                          int64_t m, int64_t n, int64_t r, double* x_dev, double* col_dev, double* row_dev,
+                          void* xq_ws) {
+  DeviceGuard device_guard_(ctx);
+  return upload_length_impl(ctx, a0, a1, a2, a3, m, n, x_dev, col_dev, row_dev, r, xq_ws);
+}
+
+namespace {
+int upload_length_impl(qcur_ctx* ctx, const double* a0, const double* a1, const double* a2, const double* a3,
+                       int64_t m, int64_t n, double* x_dev, double* col_dev, double* row_dev, int64_t xq_r,
+                       void* xq_ws) {
   if (m < 1 || n < 1) return ctx->fail(QCUR_E_SHAPE, "degenerate matrix shape (%lld, %lld)", (long long)m, (long long)n);
   // row chunks of ~32 MB per plane: the copy engine streams chunk k+1 while the SMs convert
   // chunk k and carry numpy's sequential column sums through it (colstrip with acc_in)
@@ -1557,6 +1583,10 @@ int qcur_upload_length(qcur_ctx* ctx, const double* a0, const double* a1, const 
     launch_planar_to_interleaved(buf[b][0], buf[b][1], buf[b][2], buf[b][3], nr, n, x_dev + r0 * n * 4, st);
     cudaEventRecord(ev_used[b], st);
     launch_colstrip(x_dev + r0 * n * 4, nr, n, n, sq + r0 * n, colsum2[b], st, c == 0 ? nullptr : colsum2[b ^ 1]);
+    // the residues of X for the INT8 X Q_R of a later qmcur on this matrix: the SMs and HBM are idle
+    // while the link streams the next chunk (rows are scaled independently: chunking changes nothing)
+    if (xq_ws && launch_ozaki_prepare_rows(x_dev + r0 * n * 4, nr, r0, m, n, n, xq_r, 15, xq_ws, st))
+      return ctx->fail(QCUR_E_PARAMETER, "upload residues: unsupported modulus count");
   }
   double* colsum = colsum2[(nchunks - 1) & 1];
   for (int b = 0; b < 2; ++b) {
@@ -1568,6 +1598,7 @@ int qcur_upload_length(qcur_ctx* ctx, const double* a0, const double* a1, const 
   if ((rc = length_tail(ctx, sq, colsum, m, n, col_dev, row_dev))) return rc;
   return sync_status(ctx);
 }
+}  // namespace
 
 int qcur_download_planar(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, int64_t ld, double* a0,
                          double* a1, double* a2, double* a3) {
@@ -1673,6 +1704,44 @@ int qcur_qmcur_host(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, co
   if (rc) return rc;
   if ((rc = reset_status(ctx))) return rc;
   if ((rc = qmcur_impl(ctx, x_dev, m, n, colp, rowp, c, r, state, J, I, C, U, R, core, &ho))) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    return rc;
+  }
+  return sync_status(ctx);
+}
+
+// qcur_qmcur_host whose X residues were formed at upload (qcur_upload_length_xq into xq_ws, for the same r)
+int qcur_qmcur_host_xq(qcur_ctx* ctx, const double* x_dev, int64_t m, int64_t n, const double* colp,
+                       const double* rowp, int64_t c, int64_t r, const uint64_t state[4], int core, int64_t* J,
+                       int64_t* I, double* C, double* U, double* R, int64_t* J_host, int64_t* I_host,
+                       double* const C_host[4], double* const U_host[4], double* const R_host[4], void* xq_ws) {
+  DeviceGuard device_guard_(ctx);
+  if (core != QCUR_CORE_PROJECTION && core != QCUR_CORE_INTERSECTION)
+    return ctx->fail(QCUR_E_PARAMETER, "unknown core mode %d", core);
+  if (m < 1 || n < 1 || c < 1 || r < 1 || c > n || r > m) return ctx->fail(QCUR_E_SHAPE, "qmcur: bad sizes");
+  if (!J_host || !I_host || !C_host || !U_host || !R_host) return ctx->fail(QCUR_E_PARAMETER, "null host output");
+  HostOut ho{J_host, I_host, {}, {}, {}};
+  for (int k = 0; k < 4; ++k) {
+    ho.C[k] = C_host[k];
+    ho.U[k] = U_host[k];
+    ho.R[k] = R_host[k];
+    if (!ho.C[k] || !ho.U[k] || !ho.R[k]) return ctx->fail(QCUR_E_PARAMETER, "null host plane");
+  }
+  // the residues are used only on the path whose policy formed them (INT8 X Q_R at this shape)
+  void* oz = (xq_ws && core == QCUR_CORE_PROJECTION && ctx->xq_moduli == 15 && use_int8(ctx, m, n, r) && m >= c &&
+              n >= r)
+                 ? xq_ws
+                 : nullptr;
+  int rc = ctx->reserve(qmcur_ws_bytes(m, n, c, r) + qbytes(r, c) + pinv_ws_bytes(r, c) + host_out_ws_bytes(m, n, c, r));
+  if (rc) return rc;
+  if ((rc = reset_status(ctx))) return rc;
+  // qmcur joins the side stream's residues through ev_sjoin: here they were formed on this stream at
+  // upload, so the join event is recorded here (its previous record may belong to a graph capture)
+  if (oz) {
+    cudaError_t e = cudaEventRecord(ctx->ev_sjoin, ctx->stream);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "residues join");
+  }
+  if ((rc = qmcur_impl(ctx, x_dev, m, n, colp, rowp, c, r, state, J, I, C, U, R, core, &ho, oz))) {
     cudaStreamSynchronize(ctx->copy_stream);
     return rc;
   }

@@ -134,11 +134,12 @@ def _to_dev_vec(dev, arr: np.ndarray):
     return dev.torch.from_numpy(np.array(arr, dtype=np.float64, copy=True)).to(f"cuda:{dev.index}")
 
 
-def length_distributions(x) -> tuple[np.ndarray, np.ndarray]:
+def length_distributions(x, _xq_rows: int | None = None) -> tuple[np.ndarray, np.ndarray]:
     """Squared-norm weights (col_probs, row_probs), bit-identical to the
     reference's numpy evaluation (cur.py:132-150).
 
-    Raises DegenerateDistributionError for the zero matrix."""
+    Raises DegenerateDistributionError for the zero matrix.  (_xq_rows: make_plan's row count; when
+    the later qmcur takes the INT8 X Q_R, the residues of X are formed while X uploads.)"""
     dev = _native.device()
     m, n = (int(v) for v in x.shape)
     col = dev.empty(n)
@@ -148,8 +149,20 @@ def length_distributions(x) -> tuple[np.ndarray, np.ndarray]:
         # the device copy stays cached on x for qmcur / the error that follow
         a0, a1, a2, a3 = (np.ascontiguousarray(p, dtype=np.float64) for p in x.planes)
         xd = dev.empty_q(m, n)
-        dev.call("qcur_upload_length", a0.ctypes.data, a1.ctypes.data, a2.ctypes.data, a3.ctypes.data, m, n,
-                 xd.data_ptr(), col.data_ptr(), row.data_ptr())
+        ws = None
+        if _xq_rows is not None and 0 < int(_xq_rows) <= m:
+            with dev.lock:
+                nb = int(dev.lib.qcur_xq_workspace_bytes(dev.handle, m, n, int(_xq_rows)))
+            if nb > 0:
+                ws = dev.empty(nb, dtype=dev.torch.uint8)
+        if ws is not None:
+            dev.call("qcur_upload_length_xq", a0.ctypes.data, a1.ctypes.data, a2.ctypes.data, a3.ctypes.data, m, n,
+                     int(_xq_rows), xd.data_ptr(), col.data_ptr(), row.data_ptr(), ws.data_ptr())
+            x._xq = (dev, int(_xq_rows), ws)
+        else:
+            dev.call("qcur_upload_length", a0.ctypes.data, a1.ctypes.data, a2.ctypes.data, a3.ctypes.data, m, n,
+                     xd.data_ptr(), col.data_ptr(), row.data_ptr())
+            x._xq = None
         x._dev = (dev, xd)
     else:
         xd = to_device(x, dev)
@@ -186,7 +199,7 @@ def make_plan(x, strategy: str, rank: int, seed: int, num_rows: int | None = Non
     m, n = (int(v) for v in x.shape)
     d_rows, d_cols = default_sample_counts(rank, m, n)
     if strategy == "length":
-        col_probs, row_probs = length_distributions(x)
+        col_probs, row_probs = length_distributions(x, _xq_rows=num_rows if num_rows is not None else d_rows)
     else:
         col_probs, row_probs = uniform_distributions(m, n)
     return SamplingPlan(
@@ -280,9 +293,16 @@ def qmcur(x, plan: SamplingPlan, core: str = "projection") -> CURFactors:
     hj, hi = dev.pinned_vec(c), dev.pinned_vec(r)
     hc, hu, hr = dev.pinned_planes(m, c), dev.pinned_planes(c, r), dev.pinned_planes(r, n)
     ptrs = [_native._c_dp4(*(p.ctypes.data for p in planes)) for planes in (hc, hu, hr)]
-    dev.call("qcur_qmcur_host", xd.data_ptr(), m, n, colp.data_ptr(), rowp.data_ptr(), c, r,
-             state.ctypes.data_as(_native._u64p), core_code, J.data_ptr(), I.data_ptr(), C.data_ptr(),
-             U.data_ptr(), R.data_ptr(), hj.ctypes.data, hi.ctypes.data, *ptrs)
+    xq = getattr(x, "_xq", None) if isinstance(x, QMatrix) else None
+    if xq is not None and xq[0] is dev and xq[1] == r:
+        # the residues of X for the INT8 X Q_R were formed while make_plan uploaded X
+        dev.call("qcur_qmcur_host_xq", xd.data_ptr(), m, n, colp.data_ptr(), rowp.data_ptr(), c, r,
+                 state.ctypes.data_as(_native._u64p), core_code, J.data_ptr(), I.data_ptr(), C.data_ptr(),
+                 U.data_ptr(), R.data_ptr(), hj.ctypes.data, hi.ctypes.data, *ptrs, xq[2].data_ptr())
+    else:
+        dev.call("qcur_qmcur_host", xd.data_ptr(), m, n, colp.data_ptr(), rowp.data_ptr(), c, r,
+                 state.ctypes.data_as(_native._u64p), core_code, J.data_ptr(), I.data_ptr(), C.data_ptr(),
+                 U.data_ptr(), R.data_ptr(), hj.ctypes.data, hi.ctypes.data, *ptrs)
     return CURFactors(
         row_indices=hi,
         col_indices=hj,
