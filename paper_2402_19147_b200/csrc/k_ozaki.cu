@@ -328,6 +328,91 @@ __global__ void k_oz_bres(const double* __restrict__ B, int64_t Kq, int64_t Nq, 
   }
 }
 
+// k_oz_bres with the moduli as compile-time constants and the FP32 limb reduction of k_oz_xres
+// (pair_residue) instead of FP64 quotients per modulus and value: the FP64 pipe bounded k_oz_bres
+// (cfg2 Q_R: 48 us for 74 MB).  Same layout and signs.  An odd modulus' byte may be the other centred
+// representative of the same residue (r vs r - p); every consumer reduces the int32 sums modulo p,
+// so the products are bit-identical (tests compare the factors).
+// residues of one quaternion b (already loaded; zero for padding) of column j, row k of E(B') with
+// column exponent e: the layout and signs of k_oz_bres, for the L compile-time moduli
+template <int L>
+__device__ __forceinline__ void bres_quat_fast(const double (&b)[4], int e, uint8_t* o0, int64_t pitch, int64_t plane) {
+  const double s1 = ldexp(1.0, e / 2), s2 = ldexp(1.0, e - e / 2);  // scale2's two steps
+  const long long magic_bits = __double_as_longlong(kMagic);
+  const f32x2 mag = dup(kMagicF), nmag = dup(-kMagicF), lmag = dup(-8388608.0f);
+  unsigned lb[4], lm[4][4];
+  float sg[4];
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    const long long iv = __double_as_longlong(b[h] * s1 * s2 + kMagic) - magic_bits;  // rint(b 2^e)
+    lb[h] = (unsigned)iv & 0xffu;
+    const unsigned long long u = (unsigned long long)(iv < 0 ? -iv : iv);
+    sg[h] = iv < 0 ? -1.0f : 1.0f;
+    lm[h][0] = 0x4B000000u | ((unsigned)u & 0x1fffu);
+    lm[h][1] = 0x4B000000u | ((unsigned)(u >> 13) & 0x1fffu);
+    lm[h][2] = 0x4B000000u | ((unsigned)(u >> 26) & 0x1fffu);
+    lm[h][3] = 0x4B000000u | (unsigned)(u >> 39);
+  }
+  f32x2 f[2][4];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const f32x2 sgn = pk(sg[2 * h], sg[2 * h + 1]);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      f[h][i] = fmul2(fadd2(((f32x2)lm[2 * h][i]) | ((f32x2)lm[2 * h + 1][i] << 32), lmag), sgn);
+  }
+  auto store = [&](uint8_t* o, const unsigned* r) {
+    unsigned n[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) n[u] = (0u - r[u]) & 0xffu;
+    *reinterpret_cast<unsigned*>(o) = r[0] | (n[1] << 8) | (n[2] << 16) | (n[3] << 24);
+    *reinterpret_cast<unsigned*>(o + pitch) = r[1] | (r[0] << 8) | (r[3] << 16) | (n[2] << 24);
+    *reinterpret_cast<unsigned*>(o + 2 * pitch) = r[2] | (n[3] << 8) | (r[0] << 16) | (r[1] << 24);
+    *reinterpret_cast<unsigned*>(o + 3 * pitch) = r[3] | (r[2] << 8) | (n[1] << 16) | (r[0] << 24);
+  };
+  store(o0, lb);
+#define OZ_BPLANE(l)                                                                        \
+  if constexpr (l < L) {                                                                    \
+    const f32x2 a = pair_residue<l>(f[0][0], f[0][1], f[0][2], f[0][3], mag, nmag);         \
+    const f32x2 c = pair_residue<l>(f[1][0], f[1][1], f[1][2], f[1][3], mag, nmag);         \
+    const unsigned r[4] = {(unsigned)a & 0xffu, (unsigned)(a >> 32) & 0xffu, (unsigned)c & 0xffu, \
+                           (unsigned)(c >> 32) & 0xffu};                                    \
+    store(o0 + (l) * plane, r);                                                             \
+  }
+  OZ_BPLANE(1) OZ_BPLANE(2) OZ_BPLANE(3) OZ_BPLANE(4) OZ_BPLANE(5) OZ_BPLANE(6) OZ_BPLANE(7) OZ_BPLANE(8)
+  OZ_BPLANE(9) OZ_BPLANE(10) OZ_BPLANE(11) OZ_BPLANE(12) OZ_BPLANE(13) OZ_BPLANE(14) OZ_BPLANE(15)
+  OZ_BPLANE(16) OZ_BPLANE(17) OZ_BPLANE(18) OZ_BPLANE(19)
+#undef OZ_BPLANE
+}
+
+// QCUR_BRES_FAST=0: the FP64-quotient residue kernels (A/B; default on)
+static int bres_fast_on() {
+  static const int v = [] {
+    const char* e = std::getenv("QCUR_BRES_FAST");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
+
+template <int L>
+__global__ void __launch_bounds__(256) k_oz_bres_fast(const double* __restrict__ B, int64_t Kq, int64_t Nq, int64_t ldb,
+                                                      const int* __restrict__ fx, uint8_t* __restrict__ res,
+                                                      int64_t pitch, int64_t plane) {
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t kq_pad = pitch / 4;
+  if (id >= Nq * kq_pad) return;
+  const int64_t j = id / kq_pad, k = id - j * kq_pad;
+  double b[4] = {0.0, 0.0, 0.0, 0.0};
+  if (k < Kq) {
+    const Quat q = ldq_nc(B + (k * ldb + j) * 4);
+    b[0] = q.w;
+    b[1] = q.x;
+    b[2] = q.y;
+    b[3] = q.z;
+  }
+  bres_quat_fast<L>(b, fx[j], res + (4 * j) * pitch + 4 * k, pitch, plane);
+}
+
 // The small right operand of a factorization product (Q_1 = Z L_1^{-H}: B = L_1^{-H}, q x q) for up to
 // two problems in one launch: one CTA per quaternion column j of B reduces the column maximum, stores
 // the exponent and writes the residues of E(B') for that column (k_oz_bmax + k_oz_bexp + k_oz_bres
@@ -343,7 +428,7 @@ struct OzBColJobs {
   OzBColJob j[2];
 };
 
-template <int NT>
+template <int NT, int L = 0>
 __global__ void __launch_bounds__(NT) k_oz_bcol(const __grid_constant__ OzBColJobs J, const __grid_constant__ OzMods md) {
   const OzBColJob& jb = J.j[blockIdx.y];
   const int64_t j = blockIdx.x;
@@ -378,6 +463,17 @@ __global__ void __launch_bounds__(NT) k_oz_bcol(const __grid_constant__ OzBColJo
   const int64_t kq_pad = jb.pitch / 4;
   for (int64_t k = threadIdx.x; k < kq_pad; k += NT) {
     double b[4] = {0.0, 0.0, 0.0, 0.0};
+    if constexpr (L > 0) {  // the FP32 limb reduction of k_oz_bres_fast
+      if (k < jb.Kq) {
+        const Quat q = ld(k);
+        b[0] = q.w;
+        b[1] = q.x;
+        b[2] = q.y;
+        b[3] = q.z;
+      }
+      bres_quat_fast<L>(b, e, jb.res + (4 * j) * jb.pitch + 4 * k, jb.pitch, jb.plane);
+      continue;
+    }
     if (k < jb.Kq) {
       const Quat q = ld(k);
       b[0] = (scale2(q.w, e) + kMagic) - kMagic;
@@ -1682,7 +1778,9 @@ int launch_ozaki_prep_b(int64_t m, int64_t n, const double* B, int64_t r, int64_
     OzBColJobs bj{};
     bj.j[0] = OzBColJob{B, n, r, ldb, pl.Kpitch, bplane, 0, pl.bits, fx, bres};
     ++::qcur::g_launches;
-    k_oz_bcol<1024><<<dim3((unsigned)r, 1), 1024, 0, st>>>(bj, md);
+    if (bres_fast_on() && md.L == 15) k_oz_bcol<1024, 15><<<dim3((unsigned)r, 1), 1024, 0, st>>>(bj, md);
+    else if (bres_fast_on() && md.L == 14) k_oz_bcol<1024, 14><<<dim3((unsigned)r, 1), 1024, 0, st>>>(bj, md);
+    else k_oz_bcol<1024><<<dim3((unsigned)r, 1), 1024, 0, st>>>(bj, md);
     return 0;
   }
   unsigned long long* cmax = reinterpret_cast<unsigned long long*>(ws + pl.off_cmax);
@@ -1694,7 +1792,14 @@ int launch_ozaki_prep_b(int64_t m, int64_t n, const double* B, int64_t r, int64_
   k_oz_bexp<<<(unsigned)((r + 255) / 256), 256, 0, st>>>(cmax, r, pl.bits, fx);
   const int64_t nb_threads = r * (pl.Kpitch / 4);
   ++::qcur::g_launches;
-  k_oz_bres<<<(unsigned)((nb_threads + 255) / 256), 256, 0, st>>>(B, n, r, ldb, md, fx, bres, pl.Kpitch, bplane);
+  const int bres_env = bres_fast_on();
+  const unsigned nblk = (unsigned)((nb_threads + 255) / 256);
+  if (bres_env && md.L == 15)
+    k_oz_bres_fast<15><<<nblk, 256, 0, st>>>(B, n, r, ldb, fx, bres, pl.Kpitch, bplane);
+  else if (bres_env && md.L == 14)
+    k_oz_bres_fast<14><<<nblk, 256, 0, st>>>(B, n, r, ldb, fx, bres, pl.Kpitch, bplane);
+  else
+    k_oz_bres<<<nblk, 256, 0, st>>>(B, n, r, ldb, md, fx, bres, pl.Kpitch, bplane);
   return 0;
 }
 
@@ -1901,7 +2006,9 @@ int launch_ozaki_pair(const double* const* X, const int64_t* m, const int64_t* n
     if (!oz_job(jobs[k], pl[k], m[k], ares, pl[k].Kpitch, ws[k] + pl[k].off_bres, L, ws[k] + pl[k].off_res)) return 2;
   }
   ++::qcur::g_launches;
-  k_oz_bcol<256><<<dim3((unsigned)rmax, (unsigned)np), 256, 0, st>>>(bj, oz_mods(L));
+  if (bres_fast_on() && L == 15) k_oz_bcol<256, 15><<<dim3((unsigned)rmax, (unsigned)np), 256, 0, st>>>(bj, oz_mods(L));
+  else if (bres_fast_on() && L == 14) k_oz_bcol<256, 14><<<dim3((unsigned)rmax, (unsigned)np), 256, 0, st>>>(bj, oz_mods(L));
+  else k_oz_bcol<256><<<dim3((unsigned)rmax, (unsigned)np), 256, 0, st>>>(bj, oz_mods(L));
   oz_launch_gemm(jobs, np, L, st);
   for (int k = 0; k < np; ++k) {
     const int rc = oz_launch_crt(ws[k] + pl[k].off_res, m[k], pl[k], reinterpret_cast<int*>(ws[k] + pl[k].off_ex),
