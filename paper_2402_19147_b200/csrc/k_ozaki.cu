@@ -385,7 +385,88 @@ __device__ __forceinline__ void bres_quat_fast(const double (&b)[4], int e, uint
 #undef OZ_BPLANE
 }
 
-// QCUR_BRES_FAST=0: the FP64-quotient residue kernels (A/B; default on)
+// k_oz_bres_fast with coalesced reads: a CTA takes 32 rows k x 8 columns j of B (each warp reads four
+// 256-byte row segments instead of 32 quaternions a row apart), forms the residues of one plane at a
+// time and stages its 4 x 8 output rows of 32 words in shared memory, so every warp store is 128
+// contiguous bytes of one output row.  Same bytes as k_oz_bres_fast.  Measured slower at cfg2 (61.9 vs
+// 39 us: 30 barriers per 256 quaternions), kept opt-in (QCUR_BRES_FAST=3).
+template <int L>
+__global__ void __launch_bounds__(256) k_oz_bres_tile(const double* __restrict__ B, int64_t Kq, int64_t Nq, int64_t ldb,
+                                                      const int* __restrict__ fx, uint8_t* __restrict__ res,
+                                                      int64_t pitch, int64_t plane) {
+  __shared__ unsigned st[32][33];  // [4 jj + t][k]
+  const int jj = threadIdx.x & 7, kk = threadIdx.x >> 3;
+  const int64_t kq_pad = pitch / 4;
+  const int64_t k = (int64_t)blockIdx.x * 32 + kk, j = (int64_t)blockIdx.y * 8 + jj;
+  double b[4] = {0.0, 0.0, 0.0, 0.0};
+  if (j < Nq && k < Kq) {
+    const Quat q = ldq_nc(B + (k * ldb + j) * 4);
+    b[0] = q.w;
+    b[1] = q.x;
+    b[2] = q.y;
+    b[3] = q.z;
+  }
+  const int e = j < Nq ? fx[j] : 0;
+  const double s1 = ldexp(1.0, e / 2), s2 = ldexp(1.0, e - e / 2);
+  const long long magic_bits = __double_as_longlong(kMagic);
+  const f32x2 mag = dup(kMagicF), nmag = dup(-kMagicF), lmag = dup(-8388608.0f);
+  unsigned lb[4], lm[4][4];
+  float sg[4];
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    const long long iv = __double_as_longlong(b[h] * s1 * s2 + kMagic) - magic_bits;
+    lb[h] = (unsigned)iv & 0xffu;
+    const unsigned long long u = (unsigned long long)(iv < 0 ? -iv : iv);
+    sg[h] = iv < 0 ? -1.0f : 1.0f;
+    lm[h][0] = 0x4B000000u | ((unsigned)u & 0x1fffu);
+    lm[h][1] = 0x4B000000u | ((unsigned)(u >> 13) & 0x1fffu);
+    lm[h][2] = 0x4B000000u | ((unsigned)(u >> 26) & 0x1fffu);
+    lm[h][3] = 0x4B000000u | (unsigned)(u >> 39);
+  }
+  f32x2 f[2][4];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const f32x2 sgn = pk(sg[2 * h], sg[2 * h + 1]);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      f[h][i] = fmul2(fadd2(((f32x2)lm[2 * h][i]) | ((f32x2)lm[2 * h + 1][i] << 32), lmag), sgn);
+  }
+  // writer: word w of the tile (4 per thread): output row 4 (j0 + w / 128) + (w / 32) % 4, column k0 + w % 32
+  const int64_t k0 = (int64_t)blockIdx.x * 32, j0 = (int64_t)blockIdx.y * 8;
+  auto stage_and_write = [&](int l, const unsigned* r) {
+    unsigned n[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) n[u] = (0u - r[u]) & 0xffu;
+    st[4 * jj + 0][kk] = r[0] | (n[1] << 8) | (n[2] << 16) | (n[3] << 24);
+    st[4 * jj + 1][kk] = r[1] | (r[0] << 8) | (r[3] << 16) | (n[2] << 24);
+    st[4 * jj + 2][kk] = r[2] | (n[3] << 8) | (r[0] << 16) | (r[1] << 24);
+    st[4 * jj + 3][kk] = r[3] | (r[2] << 8) | (n[1] << 16) | (r[0] << 24);
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int w = threadIdx.x + 256 * i, row = w >> 5, kc = w & 31;
+      const int64_t jo = j0 + (row >> 2), ko = k0 + kc;
+      if (jo < Nq && ko < kq_pad)
+        *reinterpret_cast<unsigned*>(res + l * plane + (4 * jo + (row & 3)) * pitch + 4 * ko) = st[row][kc];
+    }
+    __syncthreads();
+  };
+  stage_and_write(0, lb);
+#define OZ_TPLANE(l)                                                                        \
+  if constexpr (l < L) {                                                                    \
+    const f32x2 a = pair_residue<l>(f[0][0], f[0][1], f[0][2], f[0][3], mag, nmag);         \
+    const f32x2 c = pair_residue<l>(f[1][0], f[1][1], f[1][2], f[1][3], mag, nmag);         \
+    const unsigned r[4] = {(unsigned)a & 0xffu, (unsigned)(a >> 32) & 0xffu, (unsigned)c & 0xffu, \
+                           (unsigned)(c >> 32) & 0xffu};                                    \
+    stage_and_write(l, r);                                                                  \
+  }
+  OZ_TPLANE(1) OZ_TPLANE(2) OZ_TPLANE(3) OZ_TPLANE(4) OZ_TPLANE(5) OZ_TPLANE(6) OZ_TPLANE(7) OZ_TPLANE(8)
+  OZ_TPLANE(9) OZ_TPLANE(10) OZ_TPLANE(11) OZ_TPLANE(12) OZ_TPLANE(13) OZ_TPLANE(14) OZ_TPLANE(15)
+  OZ_TPLANE(16) OZ_TPLANE(17) OZ_TPLANE(18) OZ_TPLANE(19)
+#undef OZ_TPLANE
+}
+
+// QCUR_BRES_FAST=0: the FP64-quotient residue kernels; 3: k_oz_bres_tile (A/B: 61.9 vs 39 us at cfg2; default 1)
 static int bres_fast_on() {
   static const int v = [] {
     const char* e = std::getenv("QCUR_BRES_FAST");
@@ -1794,7 +1875,12 @@ int launch_ozaki_prep_b(int64_t m, int64_t n, const double* B, int64_t r, int64_
   ++::qcur::g_launches;
   const int bres_env = bres_fast_on();
   const unsigned nblk = (unsigned)((nb_threads + 255) / 256);
-  if (bres_env && md.L == 15)
+  const dim3 tgrid((unsigned)((pl.Kpitch / 4 + 31) / 32), (unsigned)((r + 7) / 8));
+  if (bres_env == 3 && md.L == 15)
+    k_oz_bres_tile<15><<<tgrid, 256, 0, st>>>(B, n, r, ldb, fx, bres, pl.Kpitch, bplane);
+  else if (bres_env == 3 && md.L == 14)
+    k_oz_bres_tile<14><<<tgrid, 256, 0, st>>>(B, n, r, ldb, fx, bres, pl.Kpitch, bplane);
+  else if (bres_env && md.L == 15)
     k_oz_bres_fast<15><<<nblk, 256, 0, st>>>(B, n, r, ldb, fx, bres, pl.Kpitch, bplane);
   else if (bres_env && md.L == 14)
     k_oz_bres_fast<14><<<nblk, 256, 0, st>>>(B, n, r, ldb, fx, bres, pl.Kpitch, bplane);

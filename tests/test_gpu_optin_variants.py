@@ -9,8 +9,8 @@ environment switch and compared with the default path on the same input.
   cluster Cholesky give identical factors; the DMMA GEMM for the q x q products stays within the bars.
 * QCUR_RDIG_EARLY=0, QCUR_PREPB_BCOL=0, QCUR_NATIVE_GRAPH=1: scheduling / launch-shape variants with
   the same bits (the last only affects DeviceApprox graph replays, not this public-API run).
-* QCUR_BRES_FAST=0 (with and without QCUR_PREPB_BCOL=0): the FP64-quotient residues of the right
-  operand; the default FP32-limb residues may store the other centred representative of a residue,
+* QCUR_BRES_FAST=0 (with and without QCUR_PREPB_BCOL=0) and =3: the FP64-quotient residues of the right
+  operand, and the FP32-limb kernel with a shared-memory transpose tile; the default FP32-limb residues may store the other centred representative of a residue,
   and the products reduce modulo p, so the factors are bitwise equal."""
 import os
 import subprocess
@@ -54,7 +54,8 @@ def default_run(tmp_path_factory):
                                          ({"QCUR_PREPB_BCOL": "0"}, True), ({"QCUR_NATIVE_GRAPH": "1"}, True),
                                          ({"QCUR_CHOL_PIPE": "1"}, True), ({"QCUR_INT8_MIN_Q1": "1"}, False),
                                          ({"QCUR_SMALL_GEMM": "0"}, False), ({"QCUR_BRES_FAST": "0"}, True),
-                                         ({"QCUR_BRES_FAST": "0", "QCUR_PREPB_BCOL": "0"}, True)])
+                                         ({"QCUR_BRES_FAST": "0", "QCUR_PREPB_BCOL": "0"}, True),
+                                         ({"QCUR_BRES_FAST": "3", "QCUR_PREPB_BCOL": "0"}, True)])
 def test_optin_variant_matches_default(tmp_path, default_run, env, bitwise):
     got = run(env, str(tmp_path / "v.npz"))
     assert np.array_equal(got["I"], default_run["I"]) and np.array_equal(got["J"], default_run["J"])
